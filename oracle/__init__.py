@@ -1,0 +1,22 @@
+"""CPU oracle for the symmetric-tensor contraction hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` /
+`--impl reference` legs may import anything from this package. The product
+path (`paper_2508_10076_b200`, the C-ABI library) never imports, links or calls
+it, and this package never imports the product path: the two share no code.
+Only `workloads/` (seeded input recipes, no arithmetic of the method) serves both.
+
+What it computes is the *plain definition* (SURVEY.md §8(c)): embed every
+symmetric tensor into a dense array over all legs and contract with a dense
+einsum in float64 (fermions: a dense Alg. 4 with Koszul signs). Modules:
+
+  sectors     sector algebra of the kinds the configs use
+  su2         exact Clebsch-Gordan / 6j (sign * sqrt(rational)) and the paper's F, R
+  layout      canonical block layout re-derived from readings C4/C5
+  dense       dense embedding / projection (P:972-983 abelian; P:1387-1433 Wigner-Eckart)
+  contract    dense einsum contraction; dense Alg. 4 with Koszul signs (reading C13)
+  blocksparse tier 2: charge-tuple einsum for full-size abelian configs (no matricisation)
+
+Parity status per function is listed in DESIGN.md §Oracle; the fermionic sign
+convention beyond the pins of reading C13 is "parity unpinned".
+"""

@@ -1,0 +1,62 @@
+"""Sector algebra for the kinds the configs use (oracle side; test infrastructure).
+
+Labels are tuples of ints:
+  Z2      (g,)      g in {0,1}; fusion = xor
+  fZ2     (g,)      fermion parity (SVect) g in {0,1}
+  U1      (q,)      fusion = addition, dual = negation
+  U1xU1   (N, 2Sz)  Deligne product of two U1, componentwise
+  fU1xU1  (N, 2Sz)  as U1xU1 with fermion parity N mod 2 (BASELINE cfg3, reading C14)
+  SU2     (2j,)     N^{j1 j2}_{j3} = 1 iff |j1-j2| <= j3 <= j1+j2 (and integrality), d = 2j+1
+                    P:2303-2312
+"""
+
+KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2")
+
+
+def width(kind):
+    return 2 if kind in ("U1xU1", "fU1xU1") else 1
+
+
+def unit(kind):
+    return (0, 0) if width(kind) == 2 else (0,)
+
+
+def dual(kind, a):
+    if kind in ("Z2", "fZ2", "SU2"):
+        return tuple(a)  # self-dual (SU2: "all irreps are self-dual")
+    return tuple(-x for x in a)
+
+
+def fuse(kind, a, b):
+    """All c with N^{ab}_c = 1, ascending (multiplicity-free for every kind here)."""
+    if kind in ("Z2", "fZ2"):
+        return [((a[0] + b[0]) % 2,)]
+    if kind == "U1":
+        return [(a[0] + b[0],)]
+    if kind in ("U1xU1", "fU1xU1"):
+        return [(a[0] + b[0], a[1] + b[1])]
+    if kind == "SU2":
+        lo, hi = abs(a[0] - b[0]), a[0] + b[0]
+        return [(j,) for j in range(lo, hi + 1, 2)]
+    raise ValueError(kind)
+
+
+def qdim(kind, a):
+    return a[0] + 1 if kind == "SU2" else 1
+
+
+def parity(kind, a):
+    """Fermion parity (0 for bosonic kinds). fU1xU1: N mod 2 (BASELINE cfg3)."""
+    if kind == "fZ2":
+        return a[0] % 2
+    if kind == "fU1xU1":
+        return a[0] % 2
+    return 0
+
+
+def is_fermionic(kind):
+    return kind in ("fZ2", "fU1xU1")
+
+
+def is_abelian(kind):
+    return kind != "SU2"

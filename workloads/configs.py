@@ -1,0 +1,138 @@
+"""The five BASELINE.json configs as plain data (spaces, tensors, contraction order).
+
+Spaces are dicts {"kind": str, "sectors": [(label, degeneracy), ...], "dual": bool}
+with labels as tuples of ints: Z2 (0|1,), U1 (q,), U1xU1/fU1xU1 (N, 2Sz), SU2 (2j,).
+`sectors` always lists the sectors of the underlying (non-dual) space V; a dual
+space V* is the same dict with "dual": True (reading C6).
+
+Readings: C3 leg spaces/arrows from the paper's benchmark
+spaces, C15 Gaussian rounding, C16 sigma units, C17 literal 13x13
+cfg3 grid, C18 cfg3 MPO charges, C19 cfg5 MPO multiplets, C20 cfg4 leg-dim knob.
+No arithmetic of the method lives here.
+"""
+import math
+
+
+def space(kind, sectors, dual=False):
+    return {"kind": kind, "sectors": sorted((tuple(l), int(d)) for l, d in sectors if d > 0), "dual": dual}
+
+
+def dual(sp):
+    return {"kind": sp["kind"], "sectors": list(sp["sectors"]), "dual": not sp["dual"]}
+
+
+def gaussian_degeneracies(labels, weights, total, tie_key):
+    """Reading C15: n = floor(T w / sum w), then largest remainder.
+
+    Ties in the remainder are broken by `tie_key(label)` (smaller first: |q| or
+    |N|+|2Sz|), then by ascending label. Zero degeneracies are dropped.
+    """
+    wsum = sum(weights)
+    exact = [total * w / wsum for w in weights]
+    base = [int(math.floor(x)) for x in exact]
+    rem = total - sum(base)
+    order = sorted(range(len(labels)), key=lambda i: (-(exact[i] - base[i]), tie_key(labels[i]), labels[i]))
+    for i in order[:rem]:
+        base[i] += 1
+    return [(labels[i], base[i]) for i in range(len(labels)) if base[i] > 0]
+
+
+# ---------------------------------------------------------------- config 1 (Z2)
+def cfg1():
+    V = space("Z2", [((0,), 8), ((1,), 8)])
+    A = {"cod": [V, V], "dom": [V, V]}            # legs (a, c; b, d)
+    B = {"cod": [V, dual(V)], "dom": [V, V]}      # legs (d, c; e, f)
+    a, b, c, d, e, f = 1, 2, 3, 4, 5, 6
+    return {
+        "cfg": 1, "kind": "Z2", "dtype": "f64",
+        "tensors": {"A": (A, 0), "B": (B, 1)},
+        "steps": [("A", [a, c, b, d], "B", [d, c, e, f], "C", [a, b, e, f], 2)],
+    }
+
+
+# -------------------------------------------------------- config 2 (U(1) DMRG)
+def _u1_bond(chi, qmax, sigma):
+    labels = [(q,) for q in range(-qmax, qmax + 1, 2)]
+    weights = [math.exp(-q * q / (2 * sigma * sigma)) for (q,) in labels]
+    return gaussian_degeneracies(labels, weights, chi, lambda l: abs(l[0]))
+
+
+def _dmrg_chain(cfg, kind, P, W, V):
+    # C3: L = FL: V <- V (x) W ; theta: V (x) P (x) P <- V ; W = O: W (x) P <- P (x) W ;
+    #     R = FR: W (x) V* <- V*
+    L = {"cod": [V], "dom": [V, W]}                        # (alpha', alpha, a)
+    TH = {"cod": [V, P, P], "dom": [V]}                    # (alpha, s1, s2, beta)
+    W1 = {"cod": [W, P], "dom": [P, W]}                    # (a, s1', s1, b)
+    W2 = {"cod": [W, P], "dom": [P, W]}                    # (b, s2', s2, c)
+    R = {"cod": [W, dual(V)], "dom": [dual(V)]}            # (c, beta', beta)
+    al_, al, a, s1, s2, be, s1p, b, s2p, c, bep = range(1, 12)
+    return {
+        "cfg": cfg, "kind": kind, "dtype": "f64",
+        "tensors": {"L": (L, 0), "theta": (TH, 1), "W1": (W1, 2), "W2": (W2, 3), "R": (R, 4)},
+        "steps": [
+            ("L", [al_, al, a], "theta", [al, s1, s2, be], "T1", [al_, a, s1, s2, be], 2),
+            ("T1", [al_, a, s1, s2, be], "W1", [a, s1p, s1, b], "T2", [al_, s2, be, s1p, b], 3),
+            ("T2", [al_, s2, be, s1p, b], "W2", [b, s2p, s2, c], "T3", [al_, be, s1p, s2p, c], 3),
+            ("T3", [al_, be, s1p, s2p, c], "R", [c, bep, be], "out", [al_, s1p, s2p, bep], 3),
+        ],
+    }
+
+
+def cfg2(chi=512):
+    P = space("U1", [((1,), 1), ((-1,), 1)])
+    W = space("U1", [((0,), 3), ((2,), 1), ((-2,), 1)])
+    V = space("U1", _u1_bond(chi, 16, 6.0))
+    return _dmrg_chain(2, "U1", P, W, V)
+
+
+# ------------------------------------------- config 3 (fermionic U(1)xU(1) Hubbard)
+def _u1u1_bond(chi, sigma_n=2.5, sigma_s=2.5):
+    labels = [(n, s) for n in range(-6, 7) for s in range(-6, 7)]  # reading C17: literal 13x13 grid
+    weights = [math.exp(-n * n / (2 * sigma_n ** 2) - s * s / (2 * sigma_s ** 2)) for n, s in labels]
+    return gaussian_degeneracies(labels, weights, chi, lambda l: abs(l[0]) + abs(l[1]))
+
+
+def cfg3(chi=2048):
+    P = space("fU1xU1", [((0, 0), 1), ((1, 1), 1), ((1, -1), 1), ((2, 0), 1)])
+    # C18: identity channels + four single-fermion operators, D = 10
+    W = space("fU1xU1", [((0, 0), 2), ((1, 1), 2), ((1, -1), 2), ((-1, 1), 2), ((-1, -1), 2)])
+    V = space("fU1xU1", _u1u1_bond(chi))
+    return _dmrg_chain(3, "fU1xU1", P, W, V)
+
+
+# ------------------------------------------------------- config 4 (U(1) PEPS)
+def cfg4_leg(d_leg):
+    labels = [(q,) for q in range(-10, 11)]
+    weights = [math.exp(-q * q / (2 * 4.0 ** 2)) for (q,) in labels]
+    return space("U1", gaussian_degeneracies(labels, weights, d_leg, lambda l: abs(l[0])))
+
+
+def cfg4(d_leg=384, complex_=False):
+    V = cfg4_leg(d_leg)
+    A = {"cod": [V, V], "dom": [V, V]}   # (x1, x2; x3, x4)
+    B = {"cod": [V, V], "dom": [V, V]}   # (y1, y2; y3, y4)
+    x1, x2, x3, x4, y2, y4 = 1, 2, 3, 4, 5, 6
+    # contract x2-y3 and x4-y1: B's legs (y1, y2; y3, y4) = (x4, y2; x2, y4)
+    return {
+        "cfg": 4, "kind": "U1", "dtype": "c64" if complex_ else "f64", "d_leg": d_leg,
+        "tensors": {"A": (A, 0), "B": (B, 1)},
+        "steps": [("A", [x1, x2, x3, x4], "B", [x4, y2, x2, y4], "C", [x1, y2, x3, y4], 2)],
+    }
+
+
+# --------------------------------------------------------------- config 5 (SU(2))
+def cfg5(mults=(24, 40, 40, 32, 24, 12, 6)):
+    P = space("SU2", [((2,), 1)])                                   # spin 1
+    V = space("SU2", [((2 * j,), m) for j, m in enumerate(mults)])  # j = 0..6
+    W = space("SU2", [((0,), 2), ((2,), 1)])                        # C19: 2 x (0) + 1 x (1)
+    L = {"cod": [V], "dom": [V, W]}      # FL: V <- V (x) W  (alpha'; alpha, a)
+    A = {"cod": [V, P], "dom": [V]}      # V (x) P <- V      (alpha, s; beta)
+    al_, al, a, s, be = 1, 2, 3, 4, 5
+    return {
+        "cfg": 5, "kind": "SU2", "dtype": "f64",
+        "tensors": {"L": (L, 0), "A": (A, 1)},
+        "steps": [("L", [al_, al, a], "A", [al, s, be], "C", [al_, s, a, be], 2)],
+    }
+
+
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
