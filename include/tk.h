@@ -1,0 +1,173 @@
+/*
+ * tk.h -- C ABI of the B200-native symmetric-tensor contraction library (libtk_b200.so).
+ *
+ * The operations are those of the paper (PAPER.md = arXiv 2508.10076, TensorKit.jl):
+ *   tk_space_*    graded vector space V = (+)_a C^{N_a} (x) V^(a) with a duality flag
+ *                 (P:880-915 eq. gradedrepresentation/gradedbasis)
+ *   tk_tensor_*   block layout of a tensor map W_1(x)..(x)W_N2 -> V_1(x)..(x)V_N1
+ *                 (P:204-224 definition; storage t = G_V^dag o t~ o G_W, P:296-316;
+ *                 abelian grouping eq. abeliangrouping; fusion-tree pairs and
+ *                 the block-diagonal embedding P:1475-1495)
+ *   tk_permute    generalized permute with fusion-tree recoupling (Alg. 2 P:471-488,
+ *                 Alg. 6, Alg. 10)
+ *   tk_contract   pairwise contraction = permute, permute, per-sector GEMM, permute
+ *                 (Alg. 4, Alg. 8; reading C1: B uses (p^B, q^B))
+ *
+ * Conventions:
+ *  - Sector labels are int32 tuples of the kind's width: "Z2"/"fZ2" {g}, "U1" {q},
+ *    "U1xU1"/"fU1xU1" {N, 2Sz} (fermion parity N mod 2), "SU2" {2j}.
+ *  - A space lists the sectors of the UNDERLYING space V; is_dual = 1 makes it V*. Fusion
+ *    trees label a dual leg by the dual sector (reading C6).
+ *  - Legs are numbered codomain first, then domain, 0-based in this ABI.
+ *  - Layout (readings C4/C5): blocks by coupled sector ascending, each block a column-major
+ *    rows x cols matrix, blocks concatenated; trees in a block ordered by (uncoupled labels,
+ *    first leg most significant; then inner labels); a tree pair's reduced array is the
+ *    strided region at (row_off, col_off), column-major over (cod legs..., dom legs...).
+ *  - Fermionic kinds: permute signs follow reading C13 (Koszul sign of the bent order),
+ *    fixed by the paper's SVect data under the unitary convention.
+ *  - SU(2): F from eq. SU2FSymbol, R^{j1j2}_{j3} = (-1)^{j1+j2-j3}
+ *    (reading C8: the printed sign at P:2329 violates the unit axiom), Z phase reading C7.
+ *
+ * Ownership: tk_space / tk_tensor are immutable, reference-counted host objects; a tensor
+ * retains its spaces. All tensor DATA lives in caller-owned device memory (e.g. PyTorch
+ * tensors passed as raw pointers); the caller also provides the workspace. The library's
+ * only device allocations are the small per-plan descriptor tables, owned by the plan cache
+ * (freed by tk_cache_clear). Float64 data is double[]; ComplexF64 is interleaved (re, im).
+ * Data pointers must be 8-byte aligned; workspace pointers 256-byte aligned.
+ *
+ * Errors: every call returns a tk_status; on error nothing is launched and no output is
+ * touched; tk_last_error() returns a thread-local message. Kernels run asynchronously on
+ * the given stream; launch failures map to TK_ERR_CUDA.
+ */
+#ifndef TK_H_
+#define TK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TK_OK = 0,
+  TK_ERR_INVALID_ARGUMENT = 1,
+  TK_ERR_UNKNOWN_LABEL = 2,        /* a label/sector not valid for the kind */
+  TK_ERR_SECTOR_MISMATCH = 3,      /* spaces of different sector kinds combined */
+  TK_ERR_SPACE_MISMATCH = 4,       /* contracted legs not dual, or output space != required */
+  TK_ERR_INVALID_PERMUTATION = 5,  /* (p, q) not a permutation of the legs */
+  TK_ERR_BRAIDING_UNAVAILABLE = 6,
+  TK_ERR_MALFORMED_NETWORK = 7,    /* label list inconsistent (repeats, missing open labels) */
+  TK_ERR_UNSUPPORTED = 8,
+  TK_ERR_WORKSPACE_TOO_SMALL = 9,
+  TK_ERR_CUDA = 10
+} tk_status;
+
+typedef enum { TK_F64 = 0, TK_C64 = 1 } tk_dtype;
+
+typedef struct tk_space tk_space;
+typedef struct tk_tensor tk_tensor;
+typedef struct CUstream_st* tk_stream; /* = cudaStream_t; NULL = legacy default stream */
+
+/* ------------------------------------------------------------------ spaces (host) */
+/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2". labels: n_sectors x width int32,
+ * degeneracies: n_sectors int64 > 0 (zero entries are dropped). Sectors may be given
+ * in any order; they are stored ascending. Duplicate labels -> TK_ERR_INVALID_ARGUMENT. */
+tk_status tk_space_create(const char* kind, int32_t n_sectors, const int32_t* labels,
+                          const int64_t* degeneracies, int32_t is_dual, tk_space** out);
+/* Grammar "U1[-2:3, 0:5]'" / "SU2[0:1, 1/2:2]" / "U1xU1[(1,-1):2]"; trailing ' = dual. */
+tk_status tk_space_parse(const char* text, tk_space** out);
+/* n_sectors, total dim = sum N_a d_a, is_dual, label width (any out pointer may be NULL). */
+tk_status tk_space_info(const tk_space* s, int32_t* n_sectors, int64_t* dim, int32_t* is_dual,
+                        int32_t* width);
+/* Copy the underlying sectors (ascending) and degeneracies; arrays sized by tk_space_info. */
+tk_status tk_space_sectors(const tk_space* s, int32_t* labels, int64_t* degeneracies);
+tk_status tk_space_dual(const tk_space* s, tk_space** out);
+void tk_space_retain(tk_space* s);
+void tk_space_release(tk_space* s);
+
+/* ----------------------------------------------------------------- tensors (host) */
+/* Block layout of W_1..W_{n_dom} -> V_1..V_{n_cod}. Host only. */
+tk_status tk_tensor_create(tk_dtype dtype, int32_t n_cod, tk_space* const* cod, int32_t n_dom,
+                           tk_space* const* dom, tk_tensor** out);
+/* Stored scalars (Float64 count; ComplexF64: complex count -- buffer holds 2x doubles). */
+tk_status tk_tensor_nelems(const tk_tensor* t, int64_t* n);
+/* n_cod, n_dom, dtype, sector width, number of blocks, number of subblocks, key length
+ * (int32 per subblock key = width * (n_cod + max(n_cod-2,0) + 1 + n_dom + max(n_dom-2,0))). */
+tk_status tk_tensor_info(const tk_tensor* t, int32_t* n_cod, int32_t* n_dom, int32_t* dtype,
+                         int32_t* width, int32_t* n_blocks, int32_t* n_subblocks, int32_t* key_len);
+/* Per block (ascending coupled label): coupled (width int32), rows, cols, element offset. */
+tk_status tk_tensor_blocks(const tk_tensor* t, int32_t* coupled, int64_t* rows, int64_t* cols,
+                           int64_t* offset);
+/* Per subblock (block by block, fusion tree major, splitting tree minor): the tree-pair key
+ * (cod uncoupled, cod inner, coupled, dom uncoupled, dom inner labels; key_len int32),
+ * block index, row_off, col_off, extents (n_cod + n_dom int64 each, padded to 8 per subblock),
+ * and the flat element offset of element (0,..,0). Any array may be NULL. */
+tk_status tk_tensor_subblocks(const tk_tensor* t, int32_t* keys, int32_t* block, int64_t* row_off,
+                              int64_t* col_off, int64_t* extents8, int64_t* offset);
+void tk_tensor_retain(tk_tensor* t);
+void tk_tensor_release(tk_tensor* t);
+
+/* Output HomSpace of a contraction from @tensor labels: C[labC] := A[labA] * B[labB], the
+ * first n_cod_C labels of labC forming C's codomain (spaces by the selection rule of Alg. 2,
+ * P:471-486). Errors: MALFORMED_NETWORK (repeats / labC != open labels), SPACE_MISMATCH
+ * (contracted legs not a ket/bra pair). */
+tk_status tk_contract_output(const tk_tensor* A, const int32_t* labA, const tk_tensor* B,
+                             const int32_t* labB, const int32_t* labC, int32_t n_cod_C,
+                             tk_tensor** C);
+
+/* ---------------------------------------------------------------- device operations */
+/* C = alpha * permute(A, (p, q)) + beta * C   (Alg. 2/6/10). p: np codomain legs of C taken
+ * from A's legs, q: nq domain legs; C must have exactly the spaces the selection rule gives
+ * (else TK_ERR_SPACE_MISMATCH). beta == 0 never reads C. a, c: device pointers, must not
+ * overlap. ws/ws_bytes: device workspace (tk_permute_workspace bytes; currently 0). */
+tk_status tk_permute_workspace(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q,
+                               int32_t nq, const tk_tensor* C, size_t* bytes);
+tk_status tk_permute(const tk_tensor* A, const void* a, const int32_t* p, int32_t np,
+                     const int32_t* q, int32_t nq, const tk_tensor* C, void* c, double alpha,
+                     double beta, void* ws, size_t ws_bytes, tk_stream stream);
+
+/* C[labC] = alpha * sum A[labA] B[labB] + beta * C (labels as in tk_contract_output; C must
+ * have the HomSpace tk_contract_output returns). conjA/conjB: complex-conjugate the operand
+ * (ComplexF64 only; must be 0 for Float64). Workspace holds the permuted operands A~, B~ and
+ * C~ (reading C2 tuples) -- query its size with tk_contract_workspace. */
+tk_status tk_contract_workspace(const tk_tensor* A, const int32_t* labA, const tk_tensor* B,
+                                const int32_t* labB, const tk_tensor* C, const int32_t* labC,
+                                size_t* bytes);
+tk_status tk_contract(const tk_tensor* A, const void* a, const int32_t* labA, int32_t conjA,
+                      const tk_tensor* B, const void* b, const int32_t* labB, int32_t conjB,
+                      const tk_tensor* C, void* c, const int32_t* labC, double alpha, double beta,
+                      void* ws, size_t ws_bytes, tk_stream stream);
+
+/* --------------------------------------------------------------- instrumentation */
+/* Per-phase CUDA-event timing of the NEXT tk_contract call(s) on the same thread: when
+ * enabled, tk_contract records events around each launch on its stream; tk_phase_times
+ * (after the stream is synchronized) returns milliseconds of [permute A, permute B, GEMM,
+ * permute C] for the most recent call, and per-phase algorithmic bytes / flops. */
+tk_status tk_profile_enable(int32_t on);
+tk_status tk_phase_times(float* ms4, double* bytes4, double* flops);
+/* Number of kernel launches issued by the most recent tk_contract / tk_permute call. */
+int32_t tk_last_launch_count(void);
+
+/* ------------------------------------------------------- topological data (host) */
+/* F^{abc}_d[e,f] (e = a(x)b inner, f = b(x)c inner) and R^{ab}_c of the planner's tables,
+ * exported so tests can pin them against the oracle. */
+tk_status tk_fsymbol(const char* kind, const int32_t* a, const int32_t* b, const int32_t* c,
+                     const int32_t* d, const int32_t* e, const int32_t* f, double* out);
+tk_status tk_rsymbol(const char* kind, const int32_t* a, const int32_t* b, const int32_t* c,
+                     double* out);
+
+/* Transfer matrix of a permute on tree pairs: for A -> permute(A,(p,q)) = C, writes the dense
+ * (nsub_A x nsub_C) coefficient matrix (row = A subblock, col = C subblock, subblock order of
+ * tk_tensor_subblocks) into out. Host only; for tests and the paper's §4.3 examples. */
+tk_status tk_permute_transfer(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q,
+                              int32_t nq, const tk_tensor* C, double* out);
+
+const char* tk_last_error(void);
+void tk_cache_clear(void);
+const char* tk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TK_H_ */

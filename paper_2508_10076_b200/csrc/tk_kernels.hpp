@@ -1,0 +1,63 @@
+// Device-side descriptor tables shared by the host planner and the sm_100a kernels.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tk {
+
+constexpr int kMaxLegs = 8;
+constexpr int kMaxGroupMembers = 8;  // k_src, k_dst of one recoupling group (SU(2) cfg5: <= 3)
+
+// One uncoupled-charge group of a permute (Alg. 10): y_j = alpha * sum_i M[i][j] perm(x_i) + beta * y_j.
+// Legs are listed in DESTINATION order after dropping extent-1 legs and merging legs that are
+// adjacent and contiguous on both sides. A leg's stride in member m is  a[l] + b[l] * ld(m):
+// codomain legs have b = 0, domain legs a = 0 (column-major blocks, reading C5).
+struct PermGroup {
+  int32_t ndim;
+  int32_t ksrc, kdst;
+  int32_t coef_off;     // into coefs: ksrc * kdst, row-major [i][j]
+  int32_t src_mem;      // into members: ksrc source members
+  int32_t dst_mem;      // into members: kdst destination members
+  int32_t mode;         // 0 = rows (dst leg 0 is also contiguous-ish in src), 1 = tiled transpose
+  int32_t tleg;         // mode 1: index (dst order) of the src-fastest leg
+  int32_t ext[kMaxLegs];
+  int64_t sa[kMaxLegs], sb[kMaxLegs];
+  int64_t da[kMaxLegs], db[kMaxLegs];
+  int64_t nelem;
+};
+
+struct PermMember {
+  int64_t off;  // element offset of the subblock's element (0,...,0)
+  int64_t ld;   // rows of its block
+};
+
+// A CTA work item: `count` work units of group `group` starting at unit `first`.
+// mode 0 unit = one row (dst leg 0); mode 1 unit = one 32x32 tile of (leg 0, leg tleg) x rest.
+struct PermJob {
+  int32_t group;
+  int32_t count;
+  int64_t first;
+};
+
+// Grouped GEMM: C^c = alpha * A^c B^c + beta * C^c, all column-major.
+struct GemmGroup {
+  int64_t a_off, b_off, c_off;  // element offsets into the A~, B~, C base pointers
+  int32_t M, N, K;
+  int32_t lda, ldb, ldc;
+};
+
+struct GemmTile {
+  int32_t group;
+  int32_t m0, n0;
+  int32_t pad;
+};
+
+// launchers (tk_kernels.cu)
+cudaError_t launch_permute(const double* src, double* dst, const PermGroup* groups, const PermMember* members,
+                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_tiled,
+                           double alpha, double beta, int complex_, cudaStream_t st);
+cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
+                        int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st);
+
+}  // namespace tk

@@ -1,0 +1,791 @@
+// Host planner: permute plans (Alg. 6 / Alg. 10) and contraction plans (Alg. 4 / Alg. 8),
+// memoised in a mutex-guarded cache, plus the device-side C ABI calls.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+
+#include <cuda_runtime.h>
+
+#include "tk_internal.hpp"
+#include "tk_kernels.hpp"
+
+namespace tk {
+
+// ------------------------------------------------------------------ device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  void upload(const std::vector<T>& v) {
+    n = v.size() * sizeof(T);
+    if (n == 0) return;
+    if (cudaMalloc(&p, n) != cudaSuccess) TK_THROW(TK_ERR_CUDA, "cudaMalloc of plan table failed");
+    if (cudaMemcpy(p, v.data(), n, cudaMemcpyHostToDevice) != cudaSuccess)
+      TK_THROW(TK_ERR_CUDA, "upload of plan table failed");
+  }
+};
+
+// ------------------------------------------------------------------ permute plan
+struct PermPlan {
+  bool identity = false;
+  std::vector<PermGroup> groups;
+  std::vector<PermMember> members;
+  std::vector<double> coefs;
+  std::vector<PermJob> jobs;
+  int njobs_rows = 0, njobs_tiled = 0;
+  DevBuf d_groups, d_members, d_coefs, d_jobs;
+  double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
+  int64_t n_src = 0, n_dst = 0;
+  bool uploaded = false;
+  void upload() {
+    if (uploaded) return;
+    d_groups.upload(groups);
+    d_members.upload(members);
+    d_coefs.upload(coefs);
+    d_jobs.upload(jobs);
+    uploaded = true;
+  }
+};
+
+static std::vector<int> dst_from_src_legs(const std::vector<int>& p, const std::vector<int>& q) {
+  std::vector<int> v(p.begin(), p.end());
+  v.insert(v.end(), q.begin(), q.end());
+  return v;
+}
+
+static void validate_perm(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
+  int N = A.nlegs();
+  if ((int)(p.size() + q.size()) != N) TK_THROW(TK_ERR_INVALID_PERMUTATION, "|p| + |q| != number of legs");
+  std::vector<int> seen(N, 0);
+  for (int x : p) {
+    if (x < 0 || x >= N || seen[x]++) TK_THROW(TK_ERR_INVALID_PERMUTATION, "(p, q) is not a permutation");
+  }
+  for (int x : q) {
+    if (x < 0 || x >= N || seen[x]++) TK_THROW(TK_ERR_INVALID_PERMUTATION, "(p, q) is not a permutation");
+  }
+}
+
+// Space selection rule of Alg. 2.
+static void permuted_spaces(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q,
+                            std::vector<Space*>& cod, std::vector<Space*>& dom) {
+  int n1 = A.n_cod();
+  auto leg = [&](int i) -> Space* { return i < n1 ? A.cod[i] : A.dom[i - n1]; };
+  cod.clear();
+  dom.clear();
+  for (int i : p) cod.push_back(i < n1 ? tk::make_space(leg(i)->kind, leg(i)->sectors, leg(i)->degs, leg(i)->dual)
+                                       : dual_space(leg(i)));
+  for (int j : q) dom.push_back(j < n1 ? dual_space(leg(j))
+                                       : tk::make_space(leg(j)->kind, leg(j)->sectors, leg(j)->degs, leg(j)->dual));
+}
+
+static void check_target(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C) {
+  if (C.n_cod() != (int)p.size() || C.n_dom() != (int)q.size())
+    TK_THROW(TK_ERR_SPACE_MISMATCH, "output tensor has the wrong number of codomain/domain legs");
+  if (C.kind != A.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+  std::vector<Space*> cod, dom;
+  permuted_spaces(A, p, q, cod, dom);
+  bool ok = true;
+  for (size_t i = 0; i < cod.size(); ++i) ok = ok && same_space(cod[i], C.cod[i]);
+  for (size_t j = 0; j < dom.size(); ++j) ok = ok && same_space(dom[j], C.dom[j]);
+  for (auto* s : cod) tk_space_release((tk_space*)s);
+  for (auto* s : dom) tk_space_release((tk_space*)s);
+  if (!ok) TK_THROW(TK_ERR_SPACE_MISMATCH, "output spaces differ from the permuted spaces (Alg. 2 selection rule)");
+}
+
+static Tree abelian_tree(Kind k, const std::vector<Sector>& unc) {
+  Tree t;
+  t.unc = unc;
+  std::vector<Sector> tmp;
+  Sector e = unc.empty() ? sector_unit(k) : unc[0];
+  std::vector<Sector> chain;
+  if (!unc.empty()) chain.push_back(e);
+  for (size_t i = 1; i < unc.size(); ++i) {
+    sector_fuse(k, e, unc[i], tmp);
+    e = tmp[0];
+    chain.push_back(e);
+  }
+  for (size_t i = 1; i + 1 < unc.size(); ++i) t.inner.push_back(chain[i]);
+  t.coupled = unc.empty() ? sector_unit(k) : e;
+  return t;
+}
+
+// per-leg strides (a, b) of a subblock: codomain legs (a = prod of previous cod extents, b = 0),
+// domain legs (a = 0, b = prod of previous dom extents); element stride = a + b * ld.
+static void leg_strides(const std::vector<int64_t>& ext, int n1, std::vector<int64_t>& a, std::vector<int64_t>& b) {
+  int N = (int)ext.size();
+  a.assign(N, 0);
+  b.assign(N, 0);
+  int64_t s = 1;
+  for (int i = 0; i < n1; ++i) {
+    a[i] = s;
+    s *= ext[i];
+  }
+  s = 1;
+  for (int i = n1; i < N; ++i) {
+    b[i] = s;
+    s *= ext[i];
+  }
+}
+
+static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_ext, int src_n1,
+                                  const std::vector<int>& src_leg, int dst_n1) {
+  int N = (int)src_leg.size();
+  std::vector<int64_t> sa, sb, da, db, dext(N);
+  leg_strides(src_ext, src_n1, sa, sb);
+  for (int k = 0; k < N; ++k) dext[k] = src_ext[src_leg[k]];
+  leg_strides(dext, dst_n1, da, db);
+  // dst order, drop extent-1 legs, merge contiguous neighbours
+  struct L {
+    int64_t e, sa, sb, da, db;
+  };
+  std::vector<L> legs;
+  for (int k = 0; k < N; ++k) {
+    if (dext[k] == 1) continue;
+    L l{dext[k], sa[src_leg[k]], sb[src_leg[k]], da[k], db[k]};
+    if (!legs.empty()) {
+      L& pv = legs.back();
+      if (l.sa == pv.sa * pv.e && l.sb == pv.sb * pv.e && l.da == pv.da * pv.e && l.db == pv.db * pv.e) {
+        pv.e *= l.e;
+        continue;
+      }
+    }
+    legs.push_back(l);
+  }
+  if (legs.empty()) legs.push_back(L{1, 0, 0, 0, 0});
+  if ((int)legs.size() > kMaxLegs) TK_THROW(TK_ERR_UNSUPPORTED, "too many legs after merging");
+  g.ndim = (int)legs.size();
+  g.nelem = 1;
+  for (int i = 0; i < kMaxLegs; ++i) {
+    if (i < g.ndim) {
+      g.ext[i] = (int32_t)legs[i].e;
+      g.sa[i] = legs[i].sa;
+      g.sb[i] = legs[i].sb;
+      g.da[i] = legs[i].da;
+      g.db[i] = legs[i].db;
+      g.nelem *= legs[i].e;
+    } else {
+      g.ext[i] = 1;
+      g.sa[i] = g.sb[i] = g.da[i] = g.db[i] = 0;
+    }
+  }
+  // mode: rows if dst leg 0 is also src-contiguous; otherwise tile (leg 0) x (src-fastest leg)
+  g.mode = 0;
+  g.tleg = 0;
+  bool lead_unit = (g.sa[0] == 1 && g.sb[0] == 0);
+  if (!lead_unit && g.ext[0] >= 4) {
+    for (int i = 1; i < g.ndim; ++i)
+      if (g.sa[i] == 1 && g.sb[i] == 0 && g.ext[i] >= 4) {
+        g.mode = 1;
+        g.tleg = i;
+        break;
+      }
+  }
+}
+
+static void make_jobs(PermPlan& P) {
+  std::vector<PermJob> rows, tiles;
+  for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
+    const PermGroup& g = P.groups[gi];
+    if (g.mode == 0) {
+      int64_t nrows = g.nelem / g.ext[0];
+      int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, 8192 / std::max(1, g.ext[0])));
+      for (int64_t r = 0; r < nrows; r += per) rows.push_back(PermJob{gi, (int32_t)std::min(per, nrows - r), r});
+    } else {
+      int64_t t0 = (g.ext[0] + 31) / 32, t1 = (g.ext[g.tleg] + 31) / 32;
+      int64_t rest = g.nelem / ((int64_t)g.ext[0] * g.ext[g.tleg]);
+      int64_t ntiles = t0 * t1 * rest;
+      int64_t per = 8;
+      for (int64_t r = 0; r < ntiles; r += per) tiles.push_back(PermJob{gi, (int32_t)std::min(per, ntiles - r), r});
+    }
+  }
+  P.njobs_rows = (int)rows.size();
+  P.njobs_tiled = (int)tiles.size();
+  P.jobs = rows;
+  P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
+}
+
+static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
+                            PermPlan& P, int elem_bytes) {
+  Kind k = A.kind;
+  int n1 = A.n_cod(), N = A.nlegs();
+  std::vector<int> src_leg = dst_from_src_legs(p, q);
+  bool ident = C.n_cod() == n1;
+  for (int i = 0; i < N && ident; ++i) ident = src_leg[i] == i;
+  P.identity = ident;
+  P.n_src = A.nelems;
+  P.n_dst = C.nelems;
+  P.bytes = (double)(A.nelems + C.nelems) * elem_bytes;
+  std::vector<bool> isdual;
+  for (auto* s : A.cod) isdual.push_back(s->dual);
+  for (auto* s : A.dom) isdual.push_back(s->dual);
+  std::vector<char> dst_done(C.subs.size(), 0);
+
+  if (kind_abelian(k)) {
+    // Alg. 6: one destination per source, coefficient = Koszul sign (reading C13)
+    for (int i = 0; i < (int)A.subs.size(); ++i) {
+      const Tree& s = A.s_tree(i);
+      const Tree& f = A.f_tree(i);
+      std::vector<Sector> lab(s.unc);
+      lab.insert(lab.end(), f.unc.begin(), f.unc.end());
+      std::vector<int64_t> ext(s.dims);
+      ext.insert(ext.end(), f.dims.begin(), f.dims.end());
+      std::vector<Sector> cu, du;
+      for (int kk = 0; kk < (int)src_leg.size(); ++kk) {
+        int l = src_leg[kk];
+        bool was_cod = l < n1, now_cod = kk < C.n_cod();
+        Sector x = (was_cod == now_cod) ? lab[l] : sector_dual(k, lab[l]);
+        (now_cod ? cu : du).push_back(x);
+      }
+      Tree ts = abelian_tree(k, cu), tf = abelian_tree(k, du);
+      auto it = C.sub_index.find(tree_pair_key(ts, tf));
+      if (it == C.sub_index.end()) TK_THROW(TK_ERR_SPACE_MISMATCH, "internal: permuted channel not in output layout");
+      int j = it->second;
+      dst_done[j] = 1;
+      PermGroup g{};
+      g.ksrc = 1;
+      g.kdst = 1;
+      g.coef_off = (int)P.coefs.size();
+      P.coefs.push_back((double)koszul_sign(k, lab, n1, p, q));
+      g.src_mem = (int)P.members.size();
+      P.members.push_back(PermMember{A.subs[i].off, A.ld(i)});
+      g.dst_mem = (int)P.members.size();
+      P.members.push_back(PermMember{C.subs[j].off, C.ld(j)});
+      finish_group_geometry(g, ext, n1, src_leg, C.n_cod());
+      P.groups.push_back(g);
+    }
+  } else {
+    // Alg. 10: group tree pairs by their uncoupled labels; per group a k_src x k_dst matrix
+    std::map<std::string, std::vector<int>> by_unc;
+    for (int i = 0; i < (int)A.subs.size(); ++i) {
+      const Tree& s = A.s_tree(i);
+      const Tree& f = A.f_tree(i);
+      std::ostringstream os;
+      for (auto& x : s.unc) os << x.v[0] << "," << x.v[1] << ";";
+      os << "|";
+      for (auto& x : f.unc) os << x.v[0] << "," << x.v[1] << ";";
+      by_unc[os.str()].push_back(i);
+    }
+    std::vector<TPTerm> terms;
+    for (auto& kv : by_unc) {
+      const std::vector<int>& srcs = kv.second;
+      std::vector<int> dsts;
+      std::map<int, int> dpos;
+      std::vector<std::vector<std::pair<int, double>>> rows(srcs.size());
+      for (size_t a = 0; a < srcs.size(); ++a) {
+        permute_tree_pair(k, A.s_tree(srcs[a]), A.f_tree(srcs[a]), p, q, isdual, terms);
+        for (auto& t : terms) {
+          auto it = C.sub_index.find(tree_pair_key(t.s, t.f));
+          if (it == C.sub_index.end()) TK_THROW(TK_ERR_SPACE_MISMATCH, "internal: transformed tree pair not in output");
+          int j = it->second;
+          if (!dpos.count(j)) {
+            dpos[j] = (int)dsts.size();
+            dsts.push_back(j);
+          }
+          rows[a].push_back({dpos[j], t.coef});
+        }
+      }
+      // also include every C tree pair with the permuted uncoupled labels (zero columns are written too)
+      {
+        const Tree& s0 = A.s_tree(srcs[0]);
+        const Tree& f0 = A.f_tree(srcs[0]);
+        std::vector<Sector> lab(s0.unc);
+        lab.insert(lab.end(), f0.unc.begin(), f0.unc.end());
+        std::vector<Sector> cu, du;
+        for (int kk = 0; kk < (int)src_leg.size(); ++kk) {
+          int l = src_leg[kk];
+          bool was_cod = l < n1, now_cod = kk < C.n_cod();
+          (now_cod ? cu : du).push_back((was_cod == now_cod) ? lab[l] : sector_dual(k, lab[l]));
+        }
+        for (int j = 0; j < (int)C.subs.size(); ++j) {
+          if (dpos.count(j)) continue;
+          if (C.s_tree(j).unc == cu && C.f_tree(j).unc == du) {
+            dpos[j] = (int)dsts.size();
+            dsts.push_back(j);
+          }
+        }
+      }
+      if ((int)srcs.size() > kMaxGroupMembers || (int)dsts.size() > kMaxGroupMembers)
+        TK_THROW(TK_ERR_UNSUPPORTED, "recoupling group larger than 8 tree pairs");
+      PermGroup g{};
+      g.ksrc = (int)srcs.size();
+      g.kdst = (int)dsts.size();
+      g.coef_off = (int)P.coefs.size();
+      std::vector<double> M(g.ksrc * g.kdst, 0.0);
+      for (size_t a = 0; a < srcs.size(); ++a)
+        for (auto& e : rows[a]) M[a * g.kdst + e.first] += e.second;
+      P.coefs.insert(P.coefs.end(), M.begin(), M.end());
+      g.src_mem = (int)P.members.size();
+      for (int i : srcs) P.members.push_back(PermMember{A.subs[i].off, A.ld(i)});
+      g.dst_mem = (int)P.members.size();
+      for (int j : dsts) {
+        P.members.push_back(PermMember{C.subs[j].off, C.ld(j)});
+        dst_done[j] = 1;
+      }
+      const Tree& s0 = A.s_tree(srcs[0]);
+      const Tree& f0 = A.f_tree(srcs[0]);
+      std::vector<int64_t> ext(s0.dims);
+      ext.insert(ext.end(), f0.dims.begin(), f0.dims.end());
+      finish_group_geometry(g, ext, n1, src_leg, C.n_cod());
+      P.groups.push_back(g);
+    }
+  }
+  for (size_t j = 0; j < dst_done.size(); ++j)
+    if (!dst_done[j]) TK_THROW(TK_ERR_SPACE_MISMATCH, "internal: output subblock not covered by the permute plan");
+  make_jobs(P);
+}
+
+// host-side transfer matrix (tests, §4.3 examples)
+void permute_transfer_matrix(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
+                             double* out) {
+  validate_perm(A, p, q);
+  check_target(A, p, q, C);
+  PermPlan P;
+  build_perm_plan(A, p, q, C, P, 8);
+  size_t nc = C.subs.size();
+  std::fill(out, out + A.subs.size() * nc, 0.0);
+  // map member offsets back to subblock indices
+  std::map<int64_t, int> aoff, coff;
+  for (int i = 0; i < (int)A.subs.size(); ++i) aoff[A.subs[i].off] = i;
+  for (int j = 0; j < (int)C.subs.size(); ++j) coff[C.subs[j].off] = j;
+  for (auto& g : P.groups)
+    for (int a = 0; a < g.ksrc; ++a)
+      for (int b = 0; b < g.kdst; ++b) {
+        int i = aoff.at(P.members[g.src_mem + a].off);
+        int j = coff.at(P.members[g.dst_mem + b].off);
+        out[i * nc + j] += P.coefs[g.coef_off + a * g.kdst + b];
+      }
+}
+
+// ------------------------------------------------------------------ contraction plan
+struct ContractPlan {
+  Tensor* At = nullptr;  // A~ (canonical layout, reading C2 tuples)
+  Tensor* Bt = nullptr;
+  Tensor* Ct = nullptr;
+  PermPlan pa, pb, pc;
+  std::vector<GemmGroup> ggroups;
+  std::vector<GemmTile> tiles;
+  int ntiles_big = 0, ntiles_small = 0;
+  DevBuf d_ggroups, d_tiles;
+  size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
+  double flops = 0;
+  bool uploaded = false;
+  ~ContractPlan() {
+    if (At) tk_tensor_release((tk_tensor*)At);
+    if (Bt) tk_tensor_release((tk_tensor*)Bt);
+    if (Ct) tk_tensor_release((tk_tensor*)Ct);
+  }
+  void upload() {
+    if (uploaded) return;
+    if (!pa.identity) pa.upload();
+    if (!pb.identity) pb.upload();
+    if (!pc.identity) pc.upload();
+    d_ggroups.upload(ggroups);
+    d_tiles.upload(tiles);
+    uploaded = true;
+  }
+};
+
+struct Tuples {
+  std::vector<int> pA, qA, pB, qB, pAB, qAB;
+};
+
+// Reading C2: A~ = (open A in A order ; contracted in A order), B~ = (contracted ; open B),
+// C~ = (open A ; open B), then permute C~ to labC. Validates labels.
+static Tuples tuples_from_labels(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
+                                 const int32_t* labC, int nC, int nC_cod) {
+  int NA = A.nlegs(), NB = B.nlegs();
+  auto has = [](const int32_t* v, int n, int32_t x) {
+    int c = 0;
+    for (int i = 0; i < n; ++i) c += v[i] == x;
+    return c;
+  };
+  for (int i = 0; i < NA; ++i)
+    if (has(labA, NA, labA[i]) != 1) TK_THROW(TK_ERR_MALFORMED_NETWORK, "repeated label in A (traces unsupported)");
+  for (int i = 0; i < NB; ++i)
+    if (has(labB, NB, labB[i]) != 1) TK_THROW(TK_ERR_MALFORMED_NETWORK, "repeated label in B (traces unsupported)");
+  Tuples t;
+  std::vector<int32_t> openA, openB;
+  for (int i = 0; i < NA; ++i) {
+    if (has(labB, NB, labA[i])) {
+      t.qA.push_back(i);
+      int j = 0;
+      while (labB[j] != labA[i]) ++j;
+      t.pB.push_back(j);
+    } else {
+      t.pA.push_back(i);
+      openA.push_back(labA[i]);
+    }
+  }
+  for (int j = 0; j < NB; ++j)
+    if (!has(labA, NA, labB[j])) {
+      t.qB.push_back(j);
+      openB.push_back(labB[j]);
+    }
+  std::vector<int32_t> ct(openA);
+  ct.insert(ct.end(), openB.begin(), openB.end());
+  if ((int)ct.size() != nC) TK_THROW(TK_ERR_MALFORMED_NETWORK, "labC must list exactly the open labels");
+  if (nC_cod < 0 || nC_cod > nC) TK_THROW(TK_ERR_INVALID_ARGUMENT, "bad codomain count for C");
+  for (int i = 0; i < nC; ++i) {
+    int pos = -1;
+    for (int j = 0; j < nC; ++j)
+      if (ct[j] == labC[i]) pos = j;
+    if (has(labC, nC, labC[i]) != 1) TK_THROW(TK_ERR_MALFORMED_NETWORK, "repeated label in labC");
+    if (pos < 0) TK_THROW(TK_ERR_UNKNOWN_LABEL, "labC has a label that is not open");
+    (i < nC_cod ? t.pAB : t.qAB).push_back(pos);
+  }
+  // contracted legs must be a ket/bra pair: normalised spaces (cod: X, dom: X*) dual to each other
+  for (size_t c = 0; c < t.qA.size(); ++c) {
+    int ia = t.qA[c], jb = t.pB[c];
+    const Space* sa = ia < A.n_cod() ? A.cod[ia] : A.dom[ia - A.n_cod()];
+    const Space* sb = jb < B.n_cod() ? B.cod[jb] : B.dom[jb - B.n_cod()];
+    bool da = sa->dual ^ (ia >= A.n_cod()), db = sb->dual ^ (jb >= B.n_cod());
+    if (sa->kind != sb->kind || sa->sectors != sb->sectors || sa->degs != sb->degs || da == db)
+      TK_THROW(TK_ERR_SPACE_MISMATCH, "contracted legs are not a ket/bra pair of the same space");
+  }
+  return t;
+}
+
+static Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, tk_dtype dt) {
+  std::vector<Space*> cod, dom;
+  permuted_spaces(A, p, q, cod, dom);
+  Tensor* t = make_tensor(dt, cod, dom);
+  for (auto* s : cod) tk_space_release((tk_space*)s);
+  for (auto* s : dom) tk_space_release((tk_space*)s);
+  return t;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
+                                const Tensor& C, const int32_t* labC, ContractPlan& P) {
+  if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+  if (A.dtype != TK_F64 || B.dtype != TK_F64 || C.dtype != TK_F64)
+    TK_THROW(TK_ERR_UNSUPPORTED, "tk_contract: only Float64 in this build");
+  Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
+  P.At = permuted_tensor(A, t.pA, t.qA, A.dtype);
+  P.Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
+  {
+    std::vector<Space*> cod(P.At->cod), dom(P.Bt->dom);
+    P.Ct = make_tensor(C.dtype, cod, dom);
+  }
+  check_target(*P.Ct, t.pAB, t.qAB, C);
+  build_perm_plan(A, t.pA, t.qA, *P.At, P.pa, 8);
+  build_perm_plan(B, t.pB, t.qB, *P.Bt, P.pb, 8);
+  build_perm_plan(*P.Ct, t.pAB, t.qAB, C, P.pc, 8);
+  // workspace: A~ | B~ | C~ (skipped when the permute is the identity)
+  size_t off = 0;
+  if (!P.pa.identity) {
+    P.off_a = off;
+    off = align256(off + (size_t)P.At->nelems * 8);
+  }
+  if (!P.pb.identity) {
+    P.off_b = off;
+    off = align256(off + (size_t)P.Bt->nelems * 8);
+  }
+  if (!P.pc.identity) {
+    P.off_c = off;
+    off = align256(off + (size_t)P.Ct->nelems * 8);
+  }
+  P.ws_bytes = off;
+  // Alg. 8: one GEMM per coupled sector of C~; K = 0 blocks are zero-filled
+  std::map<Sector, int> a_blk, b_blk;
+  for (int i = 0; i < (int)P.At->blocks.size(); ++i) a_blk[P.At->blocks[i].coupled] = i;
+  for (int i = 0; i < (int)P.Bt->blocks.size(); ++i) b_blk[P.Bt->blocks[i].coupled] = i;
+  std::vector<GemmTile> big, small;
+  for (int ci = 0; ci < (int)P.Ct->blocks.size(); ++ci) {
+    const Block& cb = P.Ct->blocks[ci];
+    GemmGroup g{};
+    g.M = (int32_t)cb.rows;
+    g.N = (int32_t)cb.cols;
+    g.c_off = cb.off;
+    g.ldc = (int32_t)cb.rows;
+    auto ia = a_blk.find(cb.coupled);
+    auto ib = b_blk.find(cb.coupled);
+    if (ia != a_blk.end() && ib != b_blk.end()) {
+      const Block& ab = P.At->blocks[ia->second];
+      const Block& bb = P.Bt->blocks[ib->second];
+      if (ab.rows != cb.rows || bb.cols != cb.cols || ab.cols != bb.rows)
+        TK_THROW(TK_ERR_SPACE_MISMATCH, "internal: block shapes of A~, B~, C~ disagree");
+      g.K = (int32_t)ab.cols;
+      g.a_off = ab.off;
+      g.b_off = bb.off;
+      g.lda = (int32_t)ab.rows;
+      g.ldb = (int32_t)bb.rows;
+    } else {
+      g.K = 0;
+      g.lda = g.ldb = 1;
+    }
+    P.flops += 2.0 * g.M * (double)g.N * g.K;
+    int gi = (int)P.ggroups.size();
+    P.ggroups.push_back(g);
+    bool isbig = g.M >= 96 && g.N >= 96;
+    int bm = isbig ? 128 : 64, bn = isbig ? 128 : 64;
+    for (int m0 = 0; m0 < g.M; m0 += bm)
+      for (int n0 = 0; n0 < g.N; n0 += bn) (isbig ? big : small).push_back(GemmTile{gi, m0, n0, g.K});
+  }
+  auto by_k = [](const GemmTile& x, const GemmTile& y) { return x.pad > y.pad; };  // LPT: long K first
+  std::stable_sort(big.begin(), big.end(), by_k);
+  std::stable_sort(small.begin(), small.end(), by_k);
+  P.ntiles_big = (int)big.size();
+  P.ntiles_small = (int)small.size();
+  P.tiles = big;
+  P.tiles.insert(P.tiles.end(), small.begin(), small.end());
+}
+
+// ------------------------------------------------------------------ plan cache
+static std::mutex g_cache_mu;
+static std::map<std::string, std::unique_ptr<ContractPlan>> g_contract_cache;
+static std::map<std::string, std::unique_ptr<PermPlan>> g_perm_cache;
+
+static std::string labels_key(const int32_t* v, int n) {
+  std::ostringstream os;
+  for (int i = 0; i < n; ++i) os << v[i] << ",";
+  return os.str();
+}
+
+static ContractPlan* get_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
+                                       const Tensor& C, const int32_t* labC) {
+  std::string key = A.sig + "#" + labels_key(labA, A.nlegs()) + "#" + B.sig + "#" + labels_key(labB, B.nlegs()) +
+                    "#" + C.sig + "#" + labels_key(labC, C.nlegs());
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  auto it = g_contract_cache.find(key);
+  if (it != g_contract_cache.end()) return it->second.get();
+  auto P = std::make_unique<ContractPlan>();
+  build_contract_plan(A, labA, B, labB, C, labC, *P);
+  ContractPlan* raw = P.get();
+  g_contract_cache[key] = std::move(P);
+  return raw;
+}
+
+static PermPlan* get_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C) {
+  std::ostringstream os;
+  os << A.sig << "#";
+  for (int x : p) os << x << ",";
+  os << "#";
+  for (int x : q) os << x << ",";
+  os << "#" << C.sig;
+  std::string key = os.str();
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  auto it = g_perm_cache.find(key);
+  if (it != g_perm_cache.end()) return it->second.get();
+  validate_perm(A, p, q);
+  check_target(A, p, q, C);
+  auto P = std::make_unique<PermPlan>();
+  build_perm_plan(A, p, q, C, *P, A.dtype == TK_C64 ? 16 : 8);
+  PermPlan* raw = P.get();
+  g_perm_cache[key] = std::move(P);
+  return raw;
+}
+
+void cache_clear() {
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  g_contract_cache.clear();
+  g_perm_cache.clear();
+}
+
+// ------------------------------------------------------------------ profiling state
+struct Prof {
+  bool on = false;
+  cudaEvent_t ev[5] = {};
+  bool have = false;
+  float ms[4] = {0, 0, 0, 0};
+  double bytes[4] = {0, 0, 0, 0};
+  double flops = 0;
+};
+static thread_local Prof g_prof;
+static thread_local int g_launches = 0;
+
+static void prof_record(int i, cudaStream_t st) {
+  if (!g_prof.on) return;
+  if (!g_prof.ev[0])
+    for (auto& e : g_prof.ev) cudaEventCreate(&e);
+  cudaEventRecord(g_prof.ev[i], st);
+}
+
+static void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) TK_THROW(TK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static void run_permute(PermPlan& P, const double* src, double* dst, double alpha, double beta, bool cplx,
+                        cudaStream_t st) {
+  P.upload();
+  if (P.jobs.empty()) return;
+  check_cuda(launch_permute(src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p,
+                            (const double*)P.d_coefs.p, (const PermJob*)P.d_jobs.p, P.njobs_rows, P.njobs_tiled,
+                            alpha, beta, cplx ? 1 : 0, st),
+             "permute launch");
+  ++g_launches;
+}
+
+}  // namespace tk
+
+using namespace tk;
+
+#define TK_API_BEGIN try {
+#define TK_API_END                                    \
+  return TK_OK;                                       \
+  }                                                   \
+  catch (const tk::Error& e) {                        \
+    tk::set_last_error(e.what());                     \
+    return e.code;                                    \
+  }                                                   \
+  catch (const std::exception& e) {                   \
+    tk::set_last_error(e.what());                     \
+    return TK_ERR_INVALID_ARGUMENT;                   \
+  }
+
+extern "C" {
+
+tk_status tk_permute_workspace(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                               const tk_tensor* C, size_t* bytes) {
+  TK_API_BEGIN
+  if (!A || !C || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<int> pv(p, p + np), qv(q, q + nq);
+  get_perm_plan(*(const Tensor*)A, pv, qv, *(const Tensor*)C);
+  *bytes = 0;
+  TK_API_END
+}
+
+tk_status tk_permute(const tk_tensor* A_, const void* a, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                     const tk_tensor* C_, void* c, double alpha, double beta, void*, size_t, tk_stream stream) {
+  TK_API_BEGIN
+  if (!A_ || !C_ || (!a && ((const Tensor*)A_)->nelems) || (!c && ((const Tensor*)C_)->nelems))
+    TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  if (np < 0 || nq < 0 || (np && !p) || (nq && !q)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "bad permutation arrays");
+  const Tensor& A = *(const Tensor*)A_;
+  const Tensor& C = *(const Tensor*)C_;
+  if (A.dtype != C.dtype) TK_THROW(TK_ERR_INVALID_ARGUMENT, "dtype mismatch");
+  std::vector<int> pv(p, p + np), qv(q, q + nq);
+  PermPlan* P = get_perm_plan(A, pv, qv, C);
+  g_launches = 0;
+  run_permute(*P, (const double*)a, (double*)c, alpha, beta, A.dtype == TK_C64, (cudaStream_t)stream);
+  TK_API_END
+}
+
+tk_status tk_permute_transfer(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                              const tk_tensor* C, double* out) {
+  TK_API_BEGIN
+  if (!A || !C || !out) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<int> pv(p, p + np), qv(q, q + nq);
+  permute_transfer_matrix(*(const Tensor*)A, pv, qv, *(const Tensor*)C, out);
+  TK_API_END
+}
+
+tk_status tk_contract_output(const tk_tensor* A_, const int32_t* labA, const tk_tensor* B_, const int32_t* labB,
+                             const int32_t* labC, int32_t n_cod_C, tk_tensor** out) {
+  TK_API_BEGIN
+  if (!A_ || !B_ || !labA || !labB || !out) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  const Tensor& A = *(const Tensor*)A_;
+  const Tensor& B = *(const Tensor*)B_;
+  if (A.kind != B.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+  // number of open labels
+  int nopen = 0;
+  for (int i = 0; i < A.nlegs(); ++i) {
+    bool in = false;
+    for (int j = 0; j < B.nlegs(); ++j) in |= labA[i] == labB[j];
+    nopen += !in;
+  }
+  for (int j = 0; j < B.nlegs(); ++j) {
+    bool in = false;
+    for (int i = 0; i < A.nlegs(); ++i) in |= labA[i] == labB[j];
+    nopen += !in;
+  }
+  if (nopen > 0 && !labC) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null labC");
+  Tuples t = tuples_from_labels(A, labA, B, labB, labC, nopen, n_cod_C);
+  Tensor* At = permuted_tensor(A, t.pA, t.qA, A.dtype);
+  Tensor* Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
+  std::vector<Space*> cod(At->cod), dom(Bt->dom);
+  Tensor* Ct = make_tensor(A.dtype, cod, dom);
+  Tensor* C = permuted_tensor(*Ct, t.pAB, t.qAB, A.dtype);
+  tk_tensor_release((tk_tensor*)At);
+  tk_tensor_release((tk_tensor*)Bt);
+  tk_tensor_release((tk_tensor*)Ct);
+  *out = (tk_tensor*)C;
+  TK_API_END
+}
+
+tk_status tk_contract_workspace(const tk_tensor* A, const int32_t* labA, const tk_tensor* B, const int32_t* labB,
+                                const tk_tensor* C, const int32_t* labC, size_t* bytes) {
+  TK_API_BEGIN
+  if (!A || !B || !C || !labA || !labB || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  ContractPlan* P = get_contract_plan(*(const Tensor*)A, labA, *(const Tensor*)B, labB, *(const Tensor*)C, labC);
+  *bytes = P->ws_bytes;
+  TK_API_END
+}
+
+tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, int32_t conjA, const tk_tensor* B_,
+                      const void* b, const int32_t* labB, int32_t conjB, const tk_tensor* C_, void* c,
+                      const int32_t* labC, double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
+  TK_API_BEGIN
+  if (!A_ || !B_ || !C_ || !labA || !labB) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  const Tensor& A = *(const Tensor*)A_;
+  const Tensor& B = *(const Tensor*)B_;
+  const Tensor& C = *(const Tensor*)C_;
+  if ((conjA || conjB) && A.dtype == TK_F64) TK_THROW(TK_ERR_INVALID_ARGUMENT, "conj flags need ComplexF64");
+  if ((!a && A.nelems) || (!b && B.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
+  ContractPlan* P = get_contract_plan(A, labA, B, labB, C, labC);
+  if (ws_bytes < P->ws_bytes || (P->ws_bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+  if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  P->upload();
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  const double* At = P->pa.identity ? (const double*)a : (const double*)(w + P->off_a);
+  const double* Bt = P->pb.identity ? (const double*)b : (const double*)(w + P->off_b);
+  double* Ct = P->pc.identity ? (double*)c : (double*)(w + P->off_c);
+  g_launches = 0;
+  prof_record(0, st);
+  if (!P->pa.identity) run_permute(P->pa, (const double*)a, (double*)At, 1.0, 0.0, false, st);
+  prof_record(1, st);
+  if (!P->pb.identity) run_permute(P->pb, (const double*)b, (double*)Bt, 1.0, 0.0, false, st);
+  prof_record(2, st);
+  double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
+  if (!P->tiles.empty()) {
+    check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, (const GemmTile*)P->d_tiles.p,
+                           P->ntiles_big, P->ntiles_small, ga, gb, st),
+               "gemm launch");
+    ++g_launches;
+  }
+  prof_record(3, st);
+  if (!P->pc.identity) run_permute(P->pc, Ct, (double*)c, alpha, beta, false, st);
+  prof_record(4, st);
+  if (g_prof.on) {
+    g_prof.have = true;
+    g_prof.bytes[0] = P->pa.identity ? 0 : P->pa.bytes;
+    g_prof.bytes[1] = P->pb.identity ? 0 : P->pb.bytes;
+    g_prof.bytes[2] = 0;
+    g_prof.bytes[3] = P->pc.identity ? 0 : P->pc.bytes;
+    g_prof.flops = P->flops;
+  }
+  TK_API_END
+}
+
+tk_status tk_profile_enable(int32_t on) {
+  g_prof.on = on != 0;
+  return TK_OK;
+}
+
+tk_status tk_phase_times(float* ms4, double* bytes4, double* flops) {
+  TK_API_BEGIN
+  if (!g_prof.have) TK_THROW(TK_ERR_INVALID_ARGUMENT, "no profiled tk_contract call");
+  for (int i = 0; i < 4; ++i) {
+    float m = 0;
+    check_cuda(cudaEventElapsedTime(&m, g_prof.ev[i], g_prof.ev[i + 1]), "event timing");
+    if (ms4) ms4[i] = m;
+    if (bytes4) bytes4[i] = g_prof.bytes[i];
+  }
+  if (flops) *flops = g_prof.flops;
+  TK_API_END
+}
+
+int32_t tk_last_launch_count(void) { return g_launches; }
+
+void tk_cache_clear(void) { tk::cache_clear(); }
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// Sector algebra and topological data for the planner (host).
+//
+// Kinds and their data:
+//   Z2       P:1011-1022 fusion table; bosonic (F = R = 1)
+//   fZ2      SVect: F trivial (eq. trivialF), R^{JJ}_I = -1, chi = d = 1
+//   U1       charge addition, dual = negation; bosonic
+//   U1xU1    Deligne product U1 x U1: componentwise
+//   fU1xU1   U1xU1 with fermion parity N mod 2 (BASELINE cfg3), i.e. fZ2 (x) U1 (x) U1 restricted;
+//            R = (-1)^{p_a p_b} (Deligne product of R-symbols)
+//   SU2      N^{j1j2}_{j3}, F via 6j (eq. SU2FSymbol, reading C9),
+//            R^{j1j2}_{j3} = (-1)^{j1+j2-j3} (reading C8), chi_j = (-1)^{2j}
+// B-symbol: B^{ab}_c = sqrt(d_a d_b / d_c) F^{a b bbar}_a[c, I].
+#include <cmath>
+#include <cstring>
+
+#include "tk_internal.hpp"
+
+namespace tk {
+
+Kind parse_kind(const std::string& s) {
+  if (s == "Z2") return Kind::Z2;
+  if (s == "fZ2") return Kind::FZ2;
+  if (s == "U1") return Kind::U1;
+  if (s == "U1xU1") return Kind::U1U1;
+  if (s == "fU1xU1") return Kind::FU1U1;
+  if (s == "SU2") return Kind::SU2;
+  TK_THROW(TK_ERR_UNKNOWN_LABEL, "unknown sector kind '" + s + "'");
+}
+
+const char* kind_name(Kind k) {
+  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2"};
+  return names[(int)k];
+}
+
+int kind_width(Kind k) { return (k == Kind::U1U1 || k == Kind::FU1U1) ? 2 : 1; }
+bool kind_abelian(Kind k) { return k != Kind::SU2; }
+bool kind_fermionic(Kind k) { return k == Kind::FZ2 || k == Kind::FU1U1; }
+Sector sector_unit(Kind) { return Sector{}; }
+
+Sector sector_dual(Kind k, const Sector& a) {
+  switch (k) {
+    case Kind::Z2:
+    case Kind::FZ2:
+    case Kind::SU2:
+      return a;  // self-dual (SU2: "all irreps are self-dual")
+    case Kind::U1:
+      return Sector{{-a.v[0], 0}};
+    default:
+      return Sector{{-a.v[0], -a.v[1]}};
+  }
+}
+
+void sector_validate(Kind k, const Sector& a) {
+  bool ok = true;
+  switch (k) {
+    case Kind::Z2:
+    case Kind::FZ2:
+      ok = (a.v[0] == 0 || a.v[0] == 1) && a.v[1] == 0;
+      break;
+    case Kind::U1:
+      ok = a.v[1] == 0;
+      break;
+    case Kind::SU2:
+      ok = a.v[0] >= 0 && a.v[1] == 0;
+      break;
+    default:
+      break;
+  }
+  if (!ok) TK_THROW(TK_ERR_UNKNOWN_LABEL, std::string("invalid ") + kind_name(k) + " label");
+}
+
+void sector_fuse(Kind k, const Sector& a, const Sector& b, std::vector<Sector>& out) {
+  out.clear();
+  switch (k) {
+    case Kind::Z2:
+    case Kind::FZ2:
+      out.push_back(Sector{{(a.v[0] + b.v[0]) & 1, 0}});
+      break;
+    case Kind::U1:
+      out.push_back(Sector{{a.v[0] + b.v[0], 0}});
+      break;
+    case Kind::U1U1:
+    case Kind::FU1U1:
+      out.push_back(Sector{{a.v[0] + b.v[0], a.v[1] + b.v[1]}});
+      break;
+    case Kind::SU2: {
+      int lo = std::abs(a.v[0] - b.v[0]), hi = a.v[0] + b.v[0];
+      for (int j = lo; j <= hi; j += 2) out.push_back(Sector{{j, 0}});
+      break;
+    }
+  }
+}
+
+static bool su2_tri(int a, int b, int c) { return std::abs(a - b) <= c && c <= a + b && ((a + b + c) & 1) == 0; }
+
+bool sector_admissible(Kind k, const Sector& a, const Sector& b, const Sector& c) {
+  if (k == Kind::SU2) return su2_tri(a.v[0], b.v[0], c.v[0]);
+  std::vector<Sector> tmp;
+  sector_fuse(k, a, b, tmp);
+  return tmp[0] == c;
+}
+
+double sector_dim(Kind k, const Sector& a) { return k == Kind::SU2 ? (double)(a.v[0] + 1) : 1.0; }
+
+int sector_parity(Kind k, const Sector& a) {
+  if (k == Kind::FZ2) return a.v[0] & 1;
+  if (k == Kind::FU1U1) return a.v[0] & 1;  // N mod 2 (works for negative N in two's complement)
+  return 0;
+}
+
+double sector_fs(Kind k, const Sector& a) {
+  if (k == Kind::SU2) return (a.v[0] & 1) ? -1.0 : 1.0;  // (-1)^{2j}
+  return 1.0;
+}
+
+// ---- SU(2) 6j symbol via the Racah sum, long double factorials (doubled spins).
+static long double lfact(int n) {
+  static long double tab[256];
+  static bool init = false;
+  if (!init) {
+    tab[0] = 1.0L;
+    for (int i = 1; i < 256; ++i) tab[i] = tab[i - 1] * (long double)i;
+    init = true;
+  }
+  if (n < 0 || n >= 256) TK_THROW(TK_ERR_UNSUPPORTED, "SU2 spin too large for the 6j table");
+  return tab[n];
+}
+
+static long double tri_delta(int a, int b, int c) {
+  return std::sqrt(lfact((a + b - c) / 2) * lfact((a - b + c) / 2) * lfact((-a + b + c) / 2) /
+                   lfact((a + b + c) / 2 + 1));
+}
+
+static double sixj(int j1, int j2, int j3, int j4, int j5, int j6) {
+  if (!su2_tri(j1, j2, j3) || !su2_tri(j1, j5, j6) || !su2_tri(j4, j2, j6) || !su2_tri(j4, j5, j3))
+    return 0.0;
+  long double pre = tri_delta(j1, j2, j3) * tri_delta(j1, j5, j6) * tri_delta(j4, j2, j6) * tri_delta(j4, j5, j3);
+  int a1 = (j1 + j2 + j3) / 2, a2 = (j1 + j5 + j6) / 2, a3 = (j4 + j2 + j6) / 2, a4 = (j4 + j5 + j3) / 2;
+  int b1 = (j1 + j2 + j4 + j5) / 2, b2 = (j2 + j3 + j5 + j6) / 2, b3 = (j3 + j1 + j6 + j4) / 2;
+  int lo = std::max(std::max(a1, a2), std::max(a3, a4));
+  int hi = std::min(b1, std::min(b2, b3));
+  long double s = 0;
+  for (int t = lo; t <= hi; ++t) {
+    long double term = lfact(t + 1) / (lfact(t - a1) * lfact(t - a2) * lfact(t - a3) * lfact(t - a4) *
+                                       lfact(b1 - t) * lfact(b2 - t) * lfact(b3 - t));
+    s += (t & 1) ? -term : term;
+  }
+  return (double)(pre * s);
+}
+
+double fsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c, const Sector& d,
+               const Sector& e, const Sector& f) {
+  if (!sector_admissible(k, a, b, e) || !sector_admissible(k, e, c, d) || !sector_admissible(k, b, c, f) ||
+      !sector_admissible(k, a, f, d))
+    return 0.0;
+  if (k != Kind::SU2) return 1.0;  // abelian / SVect: trivial F (eq. trivialF)
+  int j1 = a.v[0], j2 = b.v[0], j3 = c.v[0], j4 = d.v[0], je = e.v[0], jf = f.v[0];
+  double sg = (((j1 + j2 + j3 + j4) / 2) & 1) ? -1.0 : 1.0;
+  return std::sqrt((double)(je + 1) * (double)(jf + 1)) * sg * sixj(j1, j2, je, j3, j4, jf);
+}
+
+double rsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c) {
+  if (!sector_admissible(k, a, b, c)) return 0.0;
+  if (k == Kind::SU2) return (((a.v[0] + b.v[0] - c.v[0]) / 2) & 1) ? -1.0 : 1.0;  // reading C8
+  if (kind_fermionic(k)) return (sector_parity(k, a) & sector_parity(k, b)) ? -1.0 : 1.0;
+  return 1.0;
+}
+
+double bsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c) {
+  if (!sector_admissible(k, a, b, c)) return 0.0;
+  if (k != Kind::SU2) return 1.0;
+  Sector bb = sector_dual(k, b);
+  double da = sector_dim(k, a), db = sector_dim(k, b), dc = sector_dim(k, c);
+  return std::sqrt(da * db / dc) * fsymbol(k, a, b, bb, a, c, sector_unit(k));
+}
+
+}  // namespace tk

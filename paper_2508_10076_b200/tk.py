@@ -1,0 +1,319 @@
+"""Thin ctypes binding of libtk_b200.so (include/tk.h). Argument marshalling only.
+
+Every operation runs in the C++ planner / sm_100a kernels of the library; this
+module only converts Python values to the C ABI and raises on error. There is
+no fallback: if the in-tree library is missing, importing fails loudly.
+PyTorch is used by callers only for device memory and streams (raw pointers and
+`torch.cuda.current_stream().cuda_stream` are passed through).
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtk_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_10076_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = ["TK_OK", "TK_ERR_INVALID_ARGUMENT", "TK_ERR_UNKNOWN_LABEL", "TK_ERR_SECTOR_MISMATCH",
+          "TK_ERR_SPACE_MISMATCH", "TK_ERR_INVALID_PERMUTATION", "TK_ERR_BRAIDING_UNAVAILABLE",
+          "TK_ERR_MALFORMED_NETWORK", "TK_ERR_UNSUPPORTED", "TK_ERR_WORKSPACE_TOO_SMALL", "TK_ERR_CUDA"]
+TK_F64, TK_C64 = 0, 1
+
+_p = ctypes.c_void_p
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class TKError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS[code] if 0 <= code < len(STATUS) else code}: {msg}")
+        self.code = code
+        self.status = STATUS[code] if 0 <= code < len(STATUS) else str(code)
+
+
+def _sig(name, args, res=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_lib_tk_last_error = _sig("tk_last_error", [], ctypes.c_char_p)
+
+
+def _check(code):
+    if code != 0:
+        raise TKError(code, _lib_tk_last_error().decode())
+
+
+_space_create = _sig("tk_space_create", [ctypes.c_char_p, ctypes.c_int32, _i32p, _i64p, ctypes.c_int32,
+                                         ctypes.POINTER(_p)])
+_space_parse = _sig("tk_space_parse", [ctypes.c_char_p, ctypes.POINTER(_p)])
+_space_info = _sig("tk_space_info", [_p, _i32p, _i64p, _i32p, _i32p])
+_space_sectors = _sig("tk_space_sectors", [_p, _i32p, _i64p])
+_space_release = _sig("tk_space_release", [_p], None)
+_tensor_create = _sig("tk_tensor_create", [ctypes.c_int, ctypes.c_int32, ctypes.POINTER(_p), ctypes.c_int32,
+                                           ctypes.POINTER(_p), ctypes.POINTER(_p)])
+_tensor_nelems = _sig("tk_tensor_nelems", [_p, _i64p])
+_tensor_info = _sig("tk_tensor_info", [_p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p])
+_tensor_blocks = _sig("tk_tensor_blocks", [_p, _i32p, _i64p, _i64p, _i64p])
+_tensor_subblocks = _sig("tk_tensor_subblocks", [_p, _i32p, _i32p, _i64p, _i64p, _i64p, _i64p])
+_tensor_release = _sig("tk_tensor_release", [_p], None)
+_contract_output = _sig("tk_contract_output", [_p, _i32p, _p, _i32p, _i32p, ctypes.c_int32, ctypes.POINTER(_p)])
+_permute_workspace = _sig("tk_permute_workspace", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p,
+                                                   ctypes.POINTER(ctypes.c_size_t)])
+_permute = _sig("tk_permute", [_p, _p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _p, ctypes.c_double,
+                               ctypes.c_double, _p, ctypes.c_size_t, _p])
+_permute_transfer = _sig("tk_permute_transfer", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _dp])
+_contract_workspace = _sig("tk_contract_workspace", [_p, _i32p, _p, _i32p, _p, _i32p,
+                                                     ctypes.POINTER(ctypes.c_size_t)])
+_contract = _sig("tk_contract", [_p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p,
+                                 ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
+_profile_enable = _sig("tk_profile_enable", [ctypes.c_int32])
+_phase_times = _sig("tk_phase_times", [ctypes.POINTER(ctypes.c_float), _dp, _dp])
+_last_launch_count = _sig("tk_last_launch_count", [], ctypes.c_int32)
+_fsymbol = _sig("tk_fsymbol", [ctypes.c_char_p] + [_i32p] * 6 + [_dp])
+_rsymbol = _sig("tk_rsymbol", [ctypes.c_char_p] + [_i32p] * 3 + [_dp])
+_cache_clear = _sig("tk_cache_clear", [], None)
+_version = _sig("tk_version", [], ctypes.c_char_p)
+
+EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sectors", "tk_space_dual",
+            "tk_space_retain", "tk_space_release", "tk_tensor_create", "tk_tensor_nelems", "tk_tensor_info",
+            "tk_tensor_blocks", "tk_tensor_subblocks", "tk_tensor_retain", "tk_tensor_release",
+            "tk_contract_output", "tk_permute_workspace", "tk_permute", "tk_contract_workspace", "tk_contract",
+            "tk_profile_enable", "tk_phase_times", "tk_last_launch_count", "tk_fsymbol", "tk_rsymbol",
+            "tk_permute_transfer", "tk_last_error", "tk_cache_clear", "tk_version"]
+
+
+def _i32(seq):
+    a = np.ascontiguousarray(np.asarray(seq, dtype=np.int32).ravel())
+    return a, a.ctypes.data_as(_i32p)
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            return None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+# ---------------------------------------------------------------------- objects
+class Space:
+    """tk_space handle (reference counted on the C side)."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _space_release is not None:
+            _space_release(self.h)
+            self.h = None
+
+    def info(self):
+        n, dim, dual, w = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        _check(_space_info(self.h, ctypes.byref(n), ctypes.byref(dim), ctypes.byref(dual), ctypes.byref(w)))
+        return n.value, dim.value, bool(dual.value), w.value
+
+    def sectors(self):
+        n, _, _, w = self.info()
+        lab = np.zeros(n * w, np.int32)
+        deg = np.zeros(n, np.int64)
+        _check(_space_sectors(self.h, lab.ctypes.data_as(_i32p), deg.ctypes.data_as(_i64p)))
+        return [tuple(int(x) for x in lab[i * w:(i + 1) * w]) for i in range(n)], deg
+
+
+class Tensor:
+    """tk_tensor handle: host-side block layout of a tensor map."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _tensor_release is not None:
+            _tensor_release(self.h)
+            self.h = None
+
+    @property
+    def nelems(self):
+        n = ctypes.c_int64()
+        _check(_tensor_nelems(self.h, ctypes.byref(n)))
+        return n.value
+
+    def info(self):
+        v = [ctypes.c_int32() for _ in range(7)]
+        _check(_tensor_info(self.h, *[ctypes.byref(x) for x in v]))
+        keys = ("n_cod", "n_dom", "dtype", "width", "n_blocks", "n_subblocks", "key_len")
+        return dict(zip(keys, (x.value for x in v)))
+
+    def blocks(self):
+        inf = self.info()
+        nb, w = inf["n_blocks"], inf["width"]
+        cp = np.zeros(max(nb * w, 1), np.int32)
+        rows, cols, off = (np.zeros(max(nb, 1), np.int64) for _ in range(3))
+        _check(_tensor_blocks(self.h, cp.ctypes.data_as(_i32p), rows.ctypes.data_as(_i64p),
+                              cols.ctypes.data_as(_i64p), off.ctypes.data_as(_i64p)))
+        return cp[:nb * w].reshape(nb, w), rows[:nb], cols[:nb], off[:nb]
+
+    def subblocks(self):
+        inf = self.info()
+        ns, kl = inf["n_subblocks"], inf["key_len"]
+        keys = np.zeros(max(ns * kl, 1), np.int32)
+        blk = np.zeros(max(ns, 1), np.int32)
+        ro, co, off = (np.zeros(max(ns, 1), np.int64) for _ in range(3))
+        ext = np.zeros(max(ns, 1) * 8, np.int64)
+        _check(_tensor_subblocks(self.h, keys.ctypes.data_as(_i32p), blk.ctypes.data_as(_i32p),
+                                 ro.ctypes.data_as(_i64p), co.ctypes.data_as(_i64p), ext.ctypes.data_as(_i64p),
+                                 off.ctypes.data_as(_i64p)))
+        return {"keys": keys[:ns * kl].reshape(ns, kl), "block": blk[:ns], "row_off": ro[:ns], "col_off": co[:ns],
+                "extents": ext[:ns * 8].reshape(ns, 8), "offset": off[:ns]}
+
+
+# ---------------------------------------------------------------------- calls
+def tk_space_create(kind, labels, degeneracies, is_dual=False):
+    labels = np.asarray(labels, dtype=np.int32)
+    n = len(degeneracies)
+    lab, lp = _i32(labels)
+    deg = np.ascontiguousarray(np.asarray(degeneracies, dtype=np.int64))
+    h = _p()
+    _check(_space_create(kind.encode(), n, lp, deg.ctypes.data_as(_i64p), int(bool(is_dual)), ctypes.byref(h)))
+    return Space(h.value)
+
+
+def tk_space_parse(text):
+    h = _p()
+    _check(_space_parse(text.encode(), ctypes.byref(h)))
+    return Space(h.value)
+
+
+def tk_tensor_create(dtype, cod, dom):
+    cod_arr = (_p * max(len(cod), 1))(*[s.h for s in cod])
+    dom_arr = (_p * max(len(dom), 1))(*[s.h for s in dom])
+    h = _p()
+    _check(_tensor_create(dtype, len(cod), cod_arr, len(dom), dom_arr, ctypes.byref(h)))
+    return Tensor(h.value)
+
+
+def tk_contract_output(A, labA, B, labB, labC, n_cod_C):
+    a, ap = _i32(labA)
+    b, bp = _i32(labB)
+    c, cp = _i32(labC)
+    h = _p()
+    _check(_contract_output(A.h, ap, B.h, bp, cp, n_cod_C, ctypes.byref(h)))
+    return Tensor(h.value)
+
+
+def tk_permute_workspace(A, p, q, C):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    n = ctypes.c_size_t()
+    _check(_permute_workspace(A.h, pp, len(p), qp, len(q), C.h, ctypes.byref(n)))
+    return n.value
+
+
+def tk_permute(A, a, p, q, C, c, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, stream=None):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    _check(_permute(A.h, _ptr(a), pp, len(p), qp, len(q), C.h, _ptr(c), float(alpha), float(beta), _ptr(ws),
+                    ws_bytes, _stream(stream)))
+
+
+def tk_permute_transfer(A, p, q, C):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    na, nc = A.info()["n_subblocks"], C.info()["n_subblocks"]
+    out = np.zeros((na, nc))
+    _check(_permute_transfer(A.h, pp, len(p), qp, len(q), C.h, out.ctypes.data_as(_dp)))
+    return out
+
+
+def tk_contract_workspace(A, labA, B, labB, C, labC):
+    a, ap = _i32(labA)
+    b, bp = _i32(labB)
+    c, cp = _i32(labC)
+    n = ctypes.c_size_t()
+    _check(_contract_workspace(A.h, ap, B.h, bp, C.h, cp, ctypes.byref(n)))
+    return n.value
+
+
+def tk_contract(A, a, labA, B, b, labB, C, c, labC, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, conjA=False,
+                conjB=False, stream=None):
+    la, ap = _i32(labA)
+    lb, bp = _i32(labB)
+    lc, cp = _i32(labC)
+    _check(_contract(A.h, _ptr(a), ap, int(conjA), B.h, _ptr(b), bp, int(conjB), C.h, _ptr(c), cp, float(alpha),
+                     float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def tk_profile_enable(on=True):
+    _check(_profile_enable(int(bool(on))))
+
+
+def tk_phase_times():
+    ms = (ctypes.c_float * 4)()
+    by = (ctypes.c_double * 4)()
+    fl = ctypes.c_double()
+    _check(_phase_times(ms, by, ctypes.byref(fl)))
+    return list(ms), list(by), fl.value
+
+
+def tk_last_launch_count():
+    return int(_last_launch_count())
+
+
+def tk_fsymbol(kind, a, b, c, d, e, f):
+    args = [_i32(x) for x in (a, b, c, d, e, f)]
+    out = ctypes.c_double()
+    _check(_fsymbol(kind.encode(), *[x[1] for x in args], ctypes.byref(out)))
+    return out.value
+
+
+def tk_rsymbol(kind, a, b, c):
+    args = [_i32(x) for x in (a, b, c)]
+    out = ctypes.c_double()
+    _check(_rsymbol(kind.encode(), *[x[1] for x in args], ctypes.byref(out)))
+    return out.value
+
+
+def tk_cache_clear():
+    _cache_clear()
+
+
+def tk_version():
+    return _version().decode()
+
+
+def tk_last_error():
+    return _lib_tk_last_error().decode()
+
+
+# ------------------------------------------------------------ marshalling helpers
+def space_from_spec(spec):
+    """tk_space from a workloads/configs.py space dict (argument marshalling)."""
+    labels = [list(l) for l, _ in spec["sectors"]]
+    degs = [d for _, d in spec["sectors"]]
+    return tk_space_create(spec["kind"], labels, degs, spec["dual"])
+
+
+def tensor_from_spec(spec, dtype=TK_F64):
+    cod = [space_from_spec(s) for s in spec["cod"]]
+    dom = [space_from_spec(s) for s in spec["dom"]]
+    return tk_tensor_create(dtype, cod, dom)

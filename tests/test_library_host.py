@@ -1,0 +1,197 @@
+"""CPU tests of the C-ABI library's host side (no GPU needed).
+
+  * the library loads and exports every symbol include/tk.h declares
+  * block layouts and sector bookkeeping equal the oracle's, integer for integer (reading C25)
+  * the planner's F / R tables equal the oracle's exact 6j / CG values
+  * permute transfer matrices (fusion-tree moves in C++) equal the oracle's dense
+    Clebsch-Gordan projections -- including the paper's §4.3 matrices -- and, for
+    fermions, the dense Koszul permute
+  * error statuses for malformed input
+"""
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2508_10076_b200 import tk
+from oracle import layout as OL, dense as OD, contract as OC, su2 as OS
+from workloads import configs as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tk.h")).read()
+    names = sorted(set(re.findall(r"\b(tk_[a-z_0-9]+)\s*\(", hdr)))
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(tk._lib, n), n
+    assert set(names) == set(tk.EXPORTED)
+
+
+def oracle_layout(spec):
+    kind = spec["cod"][0]["kind"] if spec["cod"] else spec["dom"][0]["kind"]
+    return OL.homspace_layout(kind, spec["cod"], spec["dom"])
+
+
+def assert_same_layout(spec):
+    t = tk.tensor_from_spec(spec)
+    lo = oracle_layout(spec)
+    assert t.nelems == lo.nelems
+    cp, rows, cols, off = t.blocks()
+    assert [tuple(x) for x in cp] == [tuple(b[0]) for b in lo.blocks]
+    assert list(rows) == [b[1] for b in lo.blocks] and list(cols) == [b[2] for b in lo.blocks]
+    assert list(off) == [b[3] for b in lo.blocks]
+    from paper_2508_10076_b200 import layout_io
+    keys = layout_io.decode_keys(t)
+    sb = t.subblocks()
+    assert len(keys) == len(lo.subblocks)
+    n = len(spec["cod"]) + len(spec["dom"])
+    for i, s in enumerate(lo.subblocks):
+        assert keys[i] == s.key
+        assert sb["block"][i] == s.block and sb["row_off"][i] == s.row_off and sb["col_off"][i] == s.col_off
+        assert tuple(sb["extents"][i][:n]) == s.extents and sb["offset"][i] == s.offset
+
+
+@pytest.mark.parametrize("cfgfun", [W.cfg1, lambda: W.cfg2(), lambda: W.cfg3(chi=256), lambda: W.cfg4(d_leg=64),
+                                    lambda: W.cfg5()])
+def test_layout_equals_oracle(cfgfun):
+    cfg = cfgfun()
+    for name, (spec, _) in cfg["tensors"].items():
+        assert_same_layout(spec)
+
+
+def test_layout_duals_and_empty_codomain():
+    V = W.space("U1", [((-1,), 2), ((0,), 1), ((2,), 3)])
+    S = W.space("SU2", [((0,), 2), ((1,), 1), ((2,), 2)])
+    for spec in ({"cod": [V, W.dual(V)], "dom": [V]}, {"cod": [], "dom": [V, W.dual(V)]},
+                 {"cod": [W.dual(V), V, V], "dom": []}, {"cod": [S, W.dual(S), S], "dom": [S]},
+                 {"cod": [], "dom": [S, S]}):
+        assert_same_layout(spec)
+
+
+def test_topological_data_equals_oracle():
+    for j1, j2, j3, j4 in itertools.product(range(5), repeat=4):
+        for e in range(9):
+            for f in range(9):
+                ref = OS.fsymbol(j1, j2, j3, j4, e, f)
+                got = tk.tk_fsymbol("SU2", [j1], [j2], [j3], [j4], [e], [f])
+                assert abs(got - ref) < 1e-14
+    for a, b in itertools.product(range(7), repeat=2):
+        for c in range(14):
+            assert tk.tk_rsymbol("SU2", [a], [b], [c]) == OS.rsymbol(a, b, c)
+    assert tk.tk_rsymbol("fU1xU1", [1, 1], [-1, 1], [0, 2]) == -1.0
+    assert tk.tk_rsymbol("fU1xU1", [2, 0], [1, 1], [3, 1]) == 1.0
+
+
+# ------------------------------------------------------------ permute transfer
+def oracle_transfer(kind, cod, dom, p, q):
+    lt = OL.homspace_layout(kind, cod, dom)
+    c2, d2 = OC.permuted_spaces(cod, dom, p, q)
+    ls = OL.homspace_layout(kind, c2, d2)
+    par = [OD.parity_vector(s) for s in cod + dom]
+    M = np.zeros((len(lt.subblocks), len(ls.subblocks)))
+    for i, sb in enumerate(lt.subblocks):
+        x = np.zeros(lt.nelems)
+        x[sb.offset] = 1.0  # first element of the subblock: tree-pair coefficient (all-degeneracy-1 spaces)
+        y = OD.from_dense(ls, OC.permute_dense(OD.to_dense(lt, x), par, len(cod), p, q))
+        for j, sc in enumerate(ls.subblocks):
+            M[i, j] = y[sc.offset]
+    return M, c2, d2
+
+
+def lib_transfer(kind, cod, dom, p, q):
+    A = tk.tensor_from_spec({"cod": cod, "dom": dom})
+    c2, d2 = OC.permuted_spaces(cod, dom, p, q)
+    C = tk.tensor_from_spec({"cod": c2, "dom": d2})
+    return tk.tk_permute_transfer(A, p, q, C)
+
+
+def test_transfer_golden_P1805_P1850():
+    from tests.test_oracle_golden import load_matrix
+    V = W.space("SU2", [((0,), 1), ((1,), 1)])
+    M = lib_transfer("SU2", [V, V], [V, V], [1, 3], [0, 2])
+    assert np.abs(M - load_matrix("su2_transpose_P1805.txt")).max() < 1e-14
+    M = lib_transfer("SU2", [V, V], [V, V], [1, 0], [3, 2])
+    assert np.abs(M - load_matrix("su2_permute_P1850.txt")).max() < 1e-14
+
+
+def _random_perms(N, rng, n):
+    out = []
+    for _ in range(n):
+        perm = list(rng.permutation(N))
+        k = int(rng.integers(0, N + 1))
+        out.append((perm[:k], perm[k:]))
+    return out
+
+
+@pytest.mark.parametrize("kind,secs", [
+    ("SU2", [((0,), 1), ((1,), 1), ((2,), 1)]),
+    ("SU2", [((1,), 1), ((2,), 1), ((3,), 1)]),
+    ("fU1xU1", [((0, 0), 1), ((1, 1), 1), ((1, -1), 1), ((2, 0), 1)]),
+    ("fZ2", [((0,), 1), ((1,), 1)]),
+    ("U1", [((-1,), 1), ((0,), 1), ((1,), 1)]),
+])
+def test_transfer_random_vs_oracle(kind, secs):
+    rng = np.random.default_rng(42)
+    V = W.space(kind, secs)
+    Vd = W.dual(V)
+    shapes = [([V, Vd], [V]), ([V], [V, V]), ([V, V], [Vd, V]), ([Vd, V, V], [V]), ([V, V, Vd, V], [])]
+    for cod, dom in shapes:
+        N = len(cod) + len(dom)
+        for p, q in _random_perms(N, rng, 6):
+            ref, _, _ = oracle_transfer(kind, cod, dom, p, q)
+            got = lib_transfer(kind, cod, dom, p, q)
+            assert np.abs(got - ref).max() < 1e-13, (cod, dom, p, q)
+
+
+# ------------------------------------------------------------------ errors
+def test_error_statuses():
+    V = tk.tk_space_parse("U1[-1:2, 0:1, 1:2]")
+    assert V.info()[:3] == (3, 5, False)
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_space_create("Z3", [[0]], [1])
+    assert e.value.status == "TK_ERR_UNKNOWN_LABEL"
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_space_create("Z2", [[0], [0]], [1, 2])
+    assert e.value.status == "TK_ERR_INVALID_ARGUMENT"
+    A = tk.tk_tensor_create(tk.TK_F64, [V, V], [V])
+    B = tk.tk_tensor_create(tk.TK_F64, [V], [V])
+    with pytest.raises(tk.TKError) as e:   # contracted legs both kets
+        tk.tk_contract_output(A, [1, 2, 3], B, [2, 4], [1, 3, 4], 2)
+    assert e.value.status == "TK_ERR_SPACE_MISMATCH"
+    with pytest.raises(tk.TKError) as e:   # labC repeats an open label
+        tk.tk_contract_output(A, [1, 2, 3], B, [3, 4], [1, 1, 4], 1)
+    assert e.value.status == "TK_ERR_MALFORMED_NETWORK"
+    with pytest.raises(tk.TKError) as e:   # labC names a contracted label
+        tk.tk_contract_output(A, [1, 2, 3], B, [3, 4], [1, 2, 3], 1)
+    assert e.value.status == "TK_ERR_UNKNOWN_LABEL"
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_permute_transfer(A, [0, 0], [1], A)
+    assert e.value.status == "TK_ERR_INVALID_PERMUTATION"
+    with pytest.raises(tk.TKError) as e:   # wrong output spaces
+        tk.tk_permute_transfer(A, [1, 0], [2], B)
+    assert e.value.status == "TK_ERR_SPACE_MISMATCH"
+    S = tk.tk_space_parse("SU2[0:1, 1/2:2]'")
+    n, dim, dual, w = S.info()
+    assert (n, dim, dual) == (2, 5, True)
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_tensor_create(tk.TK_F64, [V], [S])
+    assert e.value.status == "TK_ERR_SECTOR_MISMATCH"
+
+
+@pytest.mark.parametrize("cfgfun", [W.cfg1, lambda: W.cfg2(chi=64), lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=32),
+                                    lambda: W.cfg5(mults=(2, 2, 1, 1, 1, 1, 1))])
+def test_contract_output_spaces(cfgfun):
+    cfg = cfgfun()
+    specs = {k: v[0] for k, v in cfg["tensors"].items()}
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+        A, B = tk.tensor_from_spec(specs[na]), tk.tensor_from_spec(specs[nb])
+        C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+        cod, dom = OC.output_spaces(specs[na]["cod"], specs[na]["dom"], specs[nb]["cod"], specs[nb]["dom"],
+                                    la, lb, lc, ncod)
+        specs[nc] = {"cod": cod, "dom": dom}
+        assert_same_layout(specs[nc])
+        assert C.nelems == OL.homspace_layout(cfg["kind"], cod, dom).nelems
