@@ -1,0 +1,123 @@
+"""Shared test harness: run a config through the CUDA path and through the oracle.
+
+CUDA side: library tensors, inputs placed by the library's layout (layout_io),
+tk_contract on the current stream, result copied back as a flat buffer.
+Oracle side: the oracle's own layout, the same keyed seeded values, dense
+embedding + einsum (tier 1) or charge-tuple einsum (tier 2).
+"""
+import math
+
+import numpy as np
+
+from oracle import layout as OL, dense as OD, contract as OC, blocksparse as BS
+from workloads import gen
+
+
+# ------------------------------------------------------------------ oracle side
+def oracle_flat(layout, cfg, tidx, complex_=False):
+    flat = np.zeros(layout.nelems, dtype=np.complex128 if complex_ else np.float64)
+    for sb in layout.subblocks:
+        n = math.prod(sb.extents)
+        v = gen.subblock_values(cfg, tidx, sb.key, n, complex_)
+        OD.subblock_array(layout, flat, sb)[...] = v.reshape(sb.extents, order="F")
+    return flat
+
+
+def oracle_chain_dense(cfg):
+    """Tier 1: dense results of every step of a config. Returns {name: (layout, dense)}."""
+    kind = cfg["kind"]
+    T = {}
+    for name, (spec, idx) in cfg["tensors"].items():
+        lt = OL.homspace_layout(kind, spec["cod"], spec["dom"])
+        T[name] = (spec["cod"], spec["dom"], lt, OD.to_dense(lt, oracle_flat(lt, cfg["cfg"], idx)))
+    out = {}
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+        Ac, Ad, _, A = T[na]
+        Bc, Bd, _, B = T[nb]
+        D = OC.contract(kind, A, Ac + Ad, len(Ac), la, B, Bc + Bd, len(Bc), lb, lc, ncod)
+        cod, dom = OC.output_spaces(Ac, Ad, Bc, Bd, la, lb, lc, ncod)
+        lt = OL.homspace_layout(kind, cod, dom)
+        T[nc] = (cod, dom, lt, D)
+        out[nc] = (lt, D)
+    return out
+
+
+class LazyBlocks(dict):
+    """Charge-tuple blocks of an input tensor, generated on first access (keyed values are
+    independent of placement, so block[key] = values reshaped column-major over the legs)."""
+
+    def __init__(self, layout, cfg, tidx):
+        super().__init__()
+        self._sub = {tuple(sb.key[0]) + tuple(sb.key[3]): sb for sb in layout.subblocks}
+        self._cfg, self._tidx = cfg, tidx
+
+    def __iter__(self):
+        return iter(self._sub)
+
+    def __contains__(self, k):
+        return k in self._sub
+
+    def __len__(self):
+        return len(self._sub)
+
+    def __getitem__(self, k):
+        if not dict.__contains__(self, k):
+            sb = self._sub[k]
+            v = gen.subblock_values(self._cfg, self._tidx, sb.key, math.prod(sb.extents))
+            dict.__setitem__(self, k, v.reshape(sb.extents, order="F"))
+        return dict.__getitem__(self, k)
+
+    def keys(self):
+        return self._sub.keys()
+
+
+def oracle_chain_blocks(cfg, out_keys_last=None):
+    """Tier 2 (abelian): charge-tuple einsum through the chain. Returns {name: (layout, blocks)}."""
+    kind = cfg["kind"]
+    T = {}
+    for name, (spec, idx) in cfg["tensors"].items():
+        lt = OL.homspace_layout(kind, spec["cod"], spec["dom"])
+        T[name] = (spec["cod"], spec["dom"], LazyBlocks(lt, cfg["cfg"], idx))
+    out = {}
+    steps = cfg["steps"]
+    for si, (na, la, nb, lb, nc, lc, ncod) in enumerate(steps):
+        Ac, Ad, Ab = T[na]
+        Bc, Bd, Bb = T[nb]
+        keys = out_keys_last if si == len(steps) - 1 else None
+        blocks, (cod, dom) = BS.contract_blocks(kind, Ab, Ac, Ad, la, Bb, Bc, Bd, lb, lc, ncod, out_keys=keys)
+        T[nc] = (cod, dom, blocks)
+        out[nc] = (OL.homspace_layout(kind, cod, dom), blocks)
+    return out
+
+
+def flat_blocks(layout, flat):
+    return BS.to_blocks(layout, flat)
+
+
+# ------------------------------------------------------------------ CUDA side
+def gpu_chain(cfg, alpha=1.0, beta=0.0, c_init=None, keep=True):
+    """Run every step of cfg through tk_contract. Returns {name: (tk.Tensor, host flat)}."""
+    import torch
+    from paper_2508_10076_b200 import tk, layout_io
+    dev = torch.device("cuda")
+    T = {}
+    for name, (spec, idx) in cfg["tensors"].items():
+        t = tk.tensor_from_spec(spec)
+        flat = layout_io.fill(t, cfg["cfg"], idx)
+        T[name] = (t, torch.from_numpy(flat).to(dev))
+    out = {}
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+        A, a = T[na]
+        B, b = T[nb]
+        C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+        if c_init is not None:
+            c = torch.from_numpy(c_init(C)).to(dev)
+        else:
+            c = torch.full((C.nelems,), float("nan"), dtype=torch.float64, device=dev)
+        ws_n = tk.tk_contract_workspace(A, la, B, lb, C, lc)
+        ws = torch.empty(max(ws_n // 8 + 32, 1), dtype=torch.float64, device=dev)
+        tk.tk_contract(A, a, la, B, b, lb, C, c, lc, alpha=alpha, beta=beta, ws=ws, ws_bytes=ws.numel() * 8)
+        torch.cuda.synchronize()
+        T[nc] = (C, c)
+        out[nc] = (C, c.cpu().numpy() if keep else None)
+    return out

@@ -1,0 +1,160 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle -- needs a B200.
+
+Tolerance: relative Frobenius error <= 1e-12 in Float64 (BASELINE north_star);
+layouts are compared exactly elsewhere (test_library_host.py). Every output buffer
+starts as NaN so that an element the kernels fail to write cannot pass.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from oracle import layout as OL, dense as OD, contract as OC, blocksparse as BS  # noqa: E402
+from workloads import configs as W  # noqa: E402
+from tests import harness as H  # noqa: E402
+
+TOL = 1e-12
+
+
+def rel_err_dense(layout, flat, D):
+    return OC.rel_frobenius(OD.to_dense(layout, flat), D)
+
+
+def rel_err_blocks(layout, flat, blocks, keys=None):
+    got = BS.to_blocks(layout, flat)
+    num = den = 0.0
+    for k, g in got.items():
+        if keys is not None and k not in keys:
+            continue
+        r = blocks.get(k)
+        if r is None:
+            r = np.zeros_like(g)
+        num += float(np.sum((g - r) ** 2))
+        den += float(np.sum(r ** 2))
+    return math.sqrt(num / den) if den > 0 else math.sqrt(num)
+
+
+@pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=96), lambda: W.cfg4(d_leg=32),
+                                    lambda: W.cfg5(), lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1))],
+                         ids=["cfg1", "cfg2", "cfg3_chi96", "cfg4_d32", "cfg5", "cfg5_small"])
+def test_chain_dense_oracle(cfgfun):
+    cfg = cfgfun()
+    ref = H.oracle_chain_dense(cfg)
+    got = H.gpu_chain(cfg)
+    for name, (lt, D) in ref.items():
+        C, flat = got[name]
+        assert C.nelems == lt.nelems
+        assert not np.isnan(flat).any(), f"{name}: unwritten output elements"
+        err = rel_err_dense(lt, flat, D)
+        assert err <= TOL, f"{name}: rel Frobenius {err:.3e}"
+
+
+@pytest.mark.parametrize("cfgfun", [lambda: W.cfg3(), lambda: W.cfg4(d_leg=128)], ids=["cfg3_full", "cfg4_d128"])
+def test_chain_tier2_oracle(cfgfun):
+    cfg = cfgfun()
+    ref = H.oracle_chain_blocks(cfg)
+    got = H.gpu_chain(cfg)
+    for name, (lt, blocks) in ref.items():
+        C, flat = got[name]
+        assert not np.isnan(flat).any()
+        err = rel_err_blocks(lt, flat, blocks)
+        assert err <= TOL, f"{name}: rel Frobenius {err:.3e}"
+
+
+def test_alpha_beta_accumulate():
+    cfg = W.cfg2(chi=128)
+    cfg["steps"] = cfg["steps"][:1]
+    ref = H.oracle_chain_dense(cfg)
+    rng = np.random.default_rng(3)
+    init = {}
+
+    def c_init(C):
+        x = rng.standard_normal(C.nelems)
+        init["x"] = x
+        return x
+
+    got = H.gpu_chain(cfg, alpha=-0.75, beta=0.5, c_init=c_init)
+    lt, D = ref["T1"]
+    C, flat = got["T1"]
+    want = -0.75 * D + 0.5 * OD.to_dense(lt, init["x"])
+    assert rel_err_dense(lt, flat, want) <= TOL
+
+
+def test_cfg4_full_size_sampled():
+    """BASELINE cfg4 at its full (bench) size: sampled output subblocks via the tier-2 oracle."""
+    cfg = W.cfg4()
+    got = H.gpu_chain(cfg)
+    C, flat = got["C"]
+    lt = OL.homspace_layout("U1", *_spaces(cfg))
+    rng = np.random.default_rng(0)
+    idx = rng.choice(len(lt.subblocks), size=24, replace=False)
+    keys = [tuple(lt.subblocks[i].key[0]) + tuple(lt.subblocks[i].key[3]) for i in idx]
+    # oracle inputs restricted to what the sampled outputs need is done inside contract_blocks
+    ref = H.oracle_chain_blocks(cfg, out_keys_last=keys)
+    _, blocks = ref["C"]
+    err = rel_err_blocks(lt, flat, blocks, keys=set(keys))
+    assert err <= TOL, f"rel Frobenius {err:.3e}"
+    assert not np.isnan(flat).any()
+
+
+def _spaces(cfg):
+    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
+    A, B = cfg["tensors"][na][0], cfg["tensors"][nb][0]
+    return OC.output_spaces(A["cod"], A["dom"], B["cod"], B["dom"], la, lb, lc, ncod)
+
+
+# ------------------------------------------------------------------ tk_permute
+def _perm_case(kind, secs, cod_d, dom_d, p, q, alpha=1.0, beta=0.0, seed=0):
+    from paper_2508_10076_b200 import tk
+    V = W.space(kind, secs)
+    cod = [W.dual(V) if d else V for d in cod_d]
+    dom = [W.dual(V) if d else V for d in dom_d]
+    lt = OL.homspace_layout(kind, cod, dom)
+    x = np.random.default_rng(seed).standard_normal(lt.nelems)
+    c2, d2 = OC.permuted_spaces(cod, dom, p, q)
+    ls = OL.homspace_layout(kind, c2, d2)
+    par = [OD.parity_vector(s) for s in cod + dom]
+    ref = OC.permute_dense(OD.to_dense(lt, x), par, len(cod), p, q)
+    A = tk.tensor_from_spec({"cod": cod, "dom": dom})
+    C = tk.tensor_from_spec({"cod": c2, "dom": d2})
+    a = torch.from_numpy(x).cuda()
+    y0 = np.random.default_rng(seed + 1).standard_normal(ls.nelems)
+    c = torch.from_numpy(y0 if beta != 0 else np.full(ls.nelems, np.nan)).cuda()
+    tk.tk_permute(A, a, p, q, C, c, alpha=alpha, beta=beta)
+    torch.cuda.synchronize()
+    got = c.cpu().numpy()
+    want = alpha * ref + (beta * OD.to_dense(ls, y0) if beta != 0 else 0)
+    return OC.rel_frobenius(OD.to_dense(ls, got), want)
+
+
+@pytest.mark.parametrize("kind,secs", [
+    ("U1", [((-2,), 3), ((-1,), 17), ((0,), 40), ((1,), 33), ((3,), 5)]),
+    ("fU1xU1", [((0, 0), 9), ((1, 1), 21), ((1, -1), 4), ((2, 0), 35), ((-1, 1), 2)]),
+    ("SU2", [((0,), 5), ((1,), 3), ((2,), 4), ((3,), 2)]),
+    ("Z2", [((0,), 37), ((1,), 29)]),
+])
+def test_permute_random(kind, secs):
+    rng = np.random.default_rng(11)
+    for trial in range(8):
+        N = int(rng.integers(2, 5))
+        n1 = int(rng.integers(0, N + 1))
+        duals = [bool(x) for x in rng.integers(0, 2, N)]
+        perm = list(rng.permutation(N))
+        k = int(rng.integers(0, N + 1))
+        if kind == "SU2" and N > 3:
+            continue
+        err = _perm_case(kind, secs, duals[:n1], duals[n1:], perm[:k], perm[k:],
+                         alpha=float(rng.choice([1.0, -2.0])), beta=float(rng.choice([0.0, 0.5])), seed=trial)
+        assert err <= TOL, (trial, N, n1, perm, k, err)
+
+
+def test_permute_large_tiled_paths():
+    # big extents exercise the 32x32 smem-tiled transpose (src-fastest != dst-fastest) and the rows path
+    secs = [((-1,), 70), ((0,), 90), ((1,), 65)]
+    assert _perm_case("U1", secs, [0, 0], [0, 0], [2, 0], [1, 3]) <= TOL   # B-operand pattern of cfg4
+    assert _perm_case("U1", secs, [0, 0], [0, 0], [0, 2], [1, 3]) <= TOL   # A-operand pattern of cfg4
+    assert _perm_case("U1", secs, [0, 1], [1], [2, 1, 0], []) <= TOL
