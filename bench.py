@@ -1,0 +1,356 @@
+"""Benchmark of the symmetric-tensor contraction hot path on B200 (BASELINE.json metric).
+
+metric: useful block GFLOP/s of tk_contract (Float64) -- SUM over coupled sectors of 2 M_c K_c N_c
+        (block-sparse flops only, never the dense equivalent) / time -- plus permute GB/s,
+        each as a fraction of roofline.
+workload (N=1): config 4, "U(1) PEPS/CTMRG-style large contraction, Float64", the largest
+        U(1) config, at leg dim 384 (reading C20: the literal 4096 needs 115 TB per operand).
+        A step = one tk_contract C(x1,y2;x3,y4) = sum A(x1,x2;x3,x4) B(x4,y2;x2,y4):
+        permute A, permute B, grouped DMMA GEMM, permute C (all launches inside the timed region).
+Inputs are resident in HBM and far larger than L2 (8.9 GB per operand), so no flush is needed.
+
+Multi-GPU: the path does not shard in this build ("replicas only"): every rank runs
+the same workload on its own GPU; value = all ranks' flops / max-over-ranks time.
+
+--impl reference: the CPU oracle (tier-2 charge-tuple einsum) timed on the host cores on a
+bounded sample of the same workload (a fixed set of output subblocks per step).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0      # measured DMMA microbenchmark, profiles/r01_fp64_peak.txt
+DGEMM_TFLOPS = 35.45         # measured cuBLAS DGEMM 8192^3, profiles/r01_dgemm_peak.json
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def workload(args):
+    from workloads import configs as W
+    cfg = W.cfg4(d_leg=args.d_leg)
+    return cfg
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def oracle_inputs(cfg):
+    """Input blocks for the oracle, generated on first use and then cached (so that timed
+    oracle steps measure the contraction, not the input generator)."""
+    from oracle import layout as OL, blocksparse as BS
+    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
+    A, B = cfg["tensors"][na][0], cfg["tensors"][nb][0]
+    kind = cfg["kind"]
+    return (BS.LazyBlocks(OL.homspace_layout(kind, A["cod"], A["dom"]), cfg["cfg"], cfg["tensors"][na][1]),
+            BS.LazyBlocks(OL.homspace_layout(kind, B["cod"], B["dom"]), cfg["cfg"], cfg["tensors"][nb][1]))
+
+
+def oracle_sample(cfg, budget_s, keys=None, seed=0, inputs=None):
+    """Tier-2 oracle on output subblocks of C. Returns (flops, seconds, keys used)."""
+    from oracle import layout as OL, contract as OC, blocksparse as BS
+    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
+    A, B = cfg["tensors"][na][0], cfg["tensors"][nb][0]
+    kind = cfg["kind"]
+    Ab, Bb = inputs if inputs is not None else oracle_inputs(cfg)
+    cod, dom = OC.output_spaces(A["cod"], A["dom"], B["cod"], B["dom"], la, lb, lc, ncod)
+    lt = OL.homspace_layout(kind, cod, dom)
+    all_keys = [tuple(s.key[0]) + tuple(s.key[3]) for s in lt.subblocks]
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(len(all_keys))
+    stats = {"flops": 0.0}
+    used = []
+    t0 = time.perf_counter()
+    if keys is not None:
+        BS.contract_blocks(kind, Ab, A["cod"], A["dom"], la, Bb, B["cod"], B["dom"], lb, lc, ncod,
+                           out_keys=keys, stats=stats)
+        used = keys
+    else:
+        # grow the batch of output subblocks until one batch alone takes about budget_s
+        n = 4
+        while True:
+            batch = [all_keys[i] for i in order[:n]]
+            stats = {"flops": 0.0}
+            t0 = time.perf_counter()
+            BS.contract_blocks(kind, Ab, A["cod"], A["dom"], la, Bb, B["cod"], B["dom"], lb, lc, ncod,
+                               out_keys=batch, stats=stats)
+            dt = time.perf_counter() - t0
+            used = batch
+            if dt >= budget_s or n >= len(all_keys):
+                break
+            n = min(len(all_keys), max(n + 1, int(n * min(8.0, 1.2 * budget_s / max(dt, 1e-3)))))
+    return stats["flops"], time.perf_counter() - t0, used
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = workload(args)
+    cores = len(os.sched_getaffinity(0))
+    # calibrate one step's sample (~8 s of oracle work), then time W + K identical steps
+    inputs = oracle_inputs(cfg)
+    _, _, keys = oracle_sample(cfg, budget_s=args.ref_step_s, inputs=inputs)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, 0, keys=keys, inputs=inputs)
+    fl, tot = 0.0, 0.0
+    for _ in range(args.steps):
+        f, t, _ = oracle_sample(cfg, 0, keys=keys, inputs=inputs)
+        fl += f
+        tot += t
+    value = fl / tot / 1e9
+    sample = (f"{len(keys)} of the C output subblocks of cfg4 (D_leg={args.d_leg}) per step, "
+              f"tier-2 charge-tuple einsum (oracle/blocksparse.py)")
+    line = {
+        "impl": "reference", "metric": "useful block GFLOP/s of tk_contract (Float64)", "value": round(value, 4),
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot / args.steps, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), workloads/gen.py)",
+        "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4, Float64, D_leg={args.d_leg}", "d_leg": args.d_leg},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    from paper_2508_10076_b200 import tk, layout_io
+
+    cfg = workload(args)
+    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
+    A = tk.tensor_from_spec(cfg["tensors"][na][0])
+    B = tk.tensor_from_spec(cfg["tensors"][nb][0])
+    C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+    t0 = time.time()
+    a_h = torch.from_numpy(layout_io.fill(A, cfg["cfg"], cfg["tensors"][na][1]))
+    b_h = torch.from_numpy(layout_io.fill(B, cfg["cfg"], cfg["tensors"][nb][1]))
+    t_fill = time.time() - t0
+    a = a_h.to(dev)
+    b = b_h.to(dev)
+    c = torch.empty(C.nelems, dtype=torch.float64, device=dev)
+    t0 = time.perf_counter()
+    ws_n = tk.tk_contract_workspace(A, la, B, lb, C, lc)   # builds + caches the plan (cold)
+    t_plan_cold = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tk.tk_contract_workspace(A, la, B, lb, C, lc)
+    t_plan_cached = time.perf_counter() - t0
+    ws = torch.empty(ws_n // 8 + 64, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        tk.tk_contract(A, a, la, B, b, lb, C, c, lc, ws=ws, ws_bytes=ws.numel() * 8, stream=stream)
+
+    tk.tk_profile_enable(True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.3)
+    phase = np.zeros(4)
+    launches = 0
+    flops = 0.0
+    pbytes = np.zeros(4)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+        launches += tk.tk_last_launch_count()
+        stream.synchronize()   # per-phase events are read back each step (one host sync per ~0.7 s step)
+        ms4, by4, fl = tk.tk_phase_times()
+        phase += np.array(ms4)
+        pbytes = np.array(by4)
+        flops = fl
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    total_ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * flops * args.steps / (total_ms * 1e-3) / 1e9
+
+    # ---- end to end through the public call with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        a_p = a_h.pin_memory()
+        b_p = b_h.pin_memory()
+        c_p = torch.empty(C.nelems, dtype=torch.float64).pin_memory()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        x0.record(stream)
+        for _ in range(args.e2e_steps):
+            a.copy_(a_p, non_blocking=True)
+            b.copy_(b_p, non_blocking=True)
+            step()
+            c_p.copy_(c, non_blocking=True)
+        x1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = x0.elapsed_time(x1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": round(world * flops * args.e2e_steps / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int((A.nelems + B.nelems) * 8), "d2h_bytes_per_step": int(C.nelems * 8),
+               "ms_per_step": round(e2e_ms / args.e2e_steps, 2)}
+
+    peaks = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    ph = phase / args.steps
+    gemm_tf = flops / (ph[2] * 1e-3) / 1e12
+    perm = {}
+    for i, nm in ((0, "permute_A"), (1, "permute_B"), (3, "permute_C")):
+        if pbytes[i] > 0:
+            gbs = pbytes[i] / (ph[i] * 1e-3) / 1e9
+            perm[nm] = {"ms": round(float(ph[i]), 3), "GB_s": round(gbs, 1), "frac_of_measured_hbm": round(gbs / hbm, 3),
+                        "frac_of_8TBs": round(gbs / 8000.0, 3), "bytes": int(pbytes[i])}
+    perm_bytes = float(pbytes[0] + pbytes[1] + pbytes[3])
+    perm_ms = float(ph[0] + ph[1] + ph[3])
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("gemm_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        inputs = oracle_inputs(cfg)
+        _, _, keys = oracle_sample(cfg, budget_s=args.cpu_budget_s / 2, inputs=inputs)   # calibrate + generate
+        fl_s, t_s, _ = oracle_sample(cfg, 0, keys=keys, inputs=inputs)
+        cpu = {"value": round(fl_s / t_s / 1e9, 4), "unit": "GFLOP/s", "cores": len(os.sched_getaffinity(0)),
+               "kind": "oracle",
+               "sample": f"{len(keys)} random C output subblocks of this workload via the tier-2 charge-tuple "
+                         f"einsum (oracle/blocksparse.py), {fl_s:.3e} useful flops in {t_s:.1f} s"}
+
+    line = {
+        "metric": "useful block GFLOP/s of tk_contract (Float64)",
+        "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded N(0,1) per subblock, workloads/gen.py)",
+        "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4 contraction, Float64, D_leg={args.d_leg} "
+                               f"(reading C20)", "d_leg": args.d_leg, "parallelism": "replicas only",
+                   "useful_flops_per_step": flops, "l2": "inputs (8.9 GB/operand) >> 126 MB L2, no flush needed"},
+        "roofline": {"bound": "tensor", "kernel": "gemm_big_kernel+gemm_small_kernel (grouped DMMA GEMM)",
+                     "achieved": round(gemm_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": round(gemm_tf / FP64_PEAK_TFLOPS, 4),
+                     "peak_source": "measured FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt;"
+                                    " MEASURED_PEAKS.json has no FP64 entry); cuBLAS DGEMM 8192^3 = 35.45",
+                     "traffic": traffic},
+        "permute": {"GB_s": round(perm_bytes / (perm_ms * 1e-3) / 1e9, 1) if perm_ms > 0 else None,
+                    "frac_of_measured_hbm": round(perm_bytes / (perm_ms * 1e-3) / 1e9 / hbm, 3) if perm_ms > 0 else None,
+                    "hbm_peak_gbs": hbm, "phases": perm},
+        "phase_ms": {"permute_A": round(float(ph[0]), 3), "permute_B": round(float(ph[1]), 3),
+                     "gemm": round(float(ph[2]), 3), "permute_C": round(float(ph[3]), 3)},
+        "planner_ms": {"cold": round(t_plan_cold * 1e3, 2), "cached": round(t_plan_cached * 1e3, 4)},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "input_fill_s": round(t_fill, 2),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--d-leg", type=int, default=384)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

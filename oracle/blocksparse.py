@@ -12,7 +12,11 @@ parities (the sign is constant over a charge tuple).
 
 Cross-checked against the dense tier 1 (contract.py) at reduced sizes.
 """
+import math
+
 import numpy as np
+
+from workloads import gen
 
 from . import sectors
 from .contract import tuples_from_labels, output_spaces, koszul_sign_pairs, _LETTERS
@@ -40,8 +44,11 @@ def _sign(kind, labels, n1, p, q):
     return -1.0 if s % 2 else 1.0
 
 
-def contract_blocks(kind, Ab, A_cod, A_dom, labA, Bb, B_cod, B_dom, labB, labC, n_cod_C, out_keys=None):
-    """Charge-tuple contraction. Returns dict C key -> ndarray (legs in labC order)."""
+def contract_blocks(kind, Ab, A_cod, A_dom, labA, Bb, B_cod, B_dom, labB, labC, n_cod_C, out_keys=None, stats=None):
+    """Charge-tuple contraction. Returns dict C key -> ndarray (legs in labC order).
+
+    `stats` (optional dict) accumulates 'flops' = sum over terms of 2 |a| |b| / |contracted|.
+    """
     labA, labB, labC = list(labA), list(labB), list(labC)
     A_sp, B_sp = list(A_cod) + list(A_dom), list(B_cod) + list(B_dom)
     C_cod, C_dom = output_spaces(A_cod, A_dom, B_cod, B_dom, labA, labB, labC, n_cod_C)
@@ -94,7 +101,13 @@ def contract_blocks(kind, Ab, A_cod, A_dom, labA, Bb, B_cod, B_dom, labB, labC, 
             u = dict(zip(openA, ao))
             u.update(zip(openB, bo))
             kc = ckey(u)
-            term = np.einsum(spec, Ab[ka], Bb[kb], optimize=True)
+            xa, xb = Ab[ka], Bb[kb]
+            term = np.einsum(spec, xa, xb, optimize=True)
+            if stats is not None:
+                ncon = 1
+                for l in con:
+                    ncon *= xa.shape[labA.index(l)]
+                stats["flops"] = stats.get("flops", 0.0) + 2.0 * xa.size * xb.size / max(ncon, 1)
             if ferm:
                 ct_labels = [ka[i] for i in pA] + [kb[j] for j in qB]
                 s = (_sign(kind, list(ka), len(A_cod), pA, qA) * _sign(kind, list(kb), len(B_cod), pB, qB)
@@ -105,3 +118,32 @@ def contract_blocks(kind, Ab, A_cod, A_dom, labA, Bb, B_cod, B_dom, labB, labC, 
             else:
                 out[kc] = term
     return out, (C_cod, C_dom)
+
+
+class LazyBlocks(dict):
+    """Charge-tuple blocks of an input tensor, generated on first access (keyed values are
+    independent of placement, so block[key] = values reshaped column-major over the legs)."""
+
+    def __init__(self, layout, cfg, tidx):
+        super().__init__()
+        self._sub = {tuple(sb.key[0]) + tuple(sb.key[3]): sb for sb in layout.subblocks}
+        self._cfg, self._tidx = cfg, tidx
+
+    def __iter__(self):
+        return iter(self._sub)
+
+    def __contains__(self, k):
+        return k in self._sub
+
+    def __len__(self):
+        return len(self._sub)
+
+    def __getitem__(self, k):
+        if not dict.__contains__(self, k):
+            sb = self._sub[k]
+            v = gen.subblock_values(self._cfg, self._tidx, sb.key, math.prod(sb.extents))
+            dict.__setitem__(self, k, v.reshape(sb.extents, order="F"))
+        return dict.__getitem__(self, k)
+
+    def keys(self):
+        return self._sub.keys()

@@ -96,14 +96,29 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
     const int64_t so = sh.moff[0], sl = sh.mld[0], dof = sh.moff[kMaxGroupMembers], dl = sh.mld[kMaxGroupMembers];
     const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
     const double c = alpha * sh.coef[0];
-    for (uint32_t e = tid; e < total; e += kPermThreads) {
-      uint32_t r = fd.div(e);
-      uint32_t i0 = e - r * n0;
-      T x = __ldg(src + so + sh.rsa[r] + sl * sh.rsb[r] + (int64_t)i0 * s0);
-      T* yp = dst + dof + sh.rda[r] + dl * sh.rdb[r] + (int64_t)i0 * d0;
-      T y = Num<T>::scale(c, x);
-      if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
-      *yp = y;
+    constexpr int U = 4;  // independent loads in flight per thread
+    for (uint32_t e0 = tid; e0 < total; e0 += U * kPermThreads) {
+      T x[U];
+      int64_t yo[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t e = e0 + u * kPermThreads;
+        if (e < total) {
+          uint32_t r = fd.div(e);
+          uint32_t i0 = e - r * n0;
+          x[u] = __ldg(src + so + sh.rsa[r] + sl * sh.rsb[r] + (int64_t)i0 * s0);
+          yo[u] = dof + sh.rda[r] + dl * sh.rdb[r] + (int64_t)i0 * d0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t e = e0 + u * kPermThreads;
+        if (e < total) {
+          T y = Num<T>::scale(c, x[u]);
+          if (beta != 0.0) y = Num<T>::axpy(beta, dst[yo[u]], y);
+          dst[yo[u]] = y;
+        }
+      }
     }
     return;
   }
@@ -133,51 +148,68 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
 
 template <typename T>
 __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
-                              PermShared& sh, T (*tile)[33], double alpha, double beta) {
-  // single source / destination member (abelian groups); leg 0 = dst-fastest, leg t = src-fastest
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+                              PermShared& sh, T* __restrict__ S, double alpha, double beta) {
+  // One source / destination member (abelian groups). Leg 0 = dst-fastest, leg t = src-fastest.
+  // A tile holds chunk c0 of leg 0 x chunk ct of leg t x R consecutive "rest" indices (all other
+  // legs). Loads walk the tile in source order (leg t fastest: coalesced reads), stores walk it in
+  // destination order (leg 0 fastest: coalesced writes); S[r][it][i0] with an odd row pitch
+  // keeps both phases free of shared-memory bank conflicts.
+  const int tid = threadIdx.x;
   const int t = g.tleg;
   const int n0 = g.ext[0], nt = g.ext[t];
-  const int T0 = (n0 + 31) >> 5, Tt = (nt + 31) >> 5;
+  const int c0 = g.c0, ct = g.ct, R = g.R, c0p = c0 | 1;
   const int64_t so = sh.moff[0], sl = sh.mld[0], dof = sh.moff[kMaxGroupMembers], dl = sh.mld[kMaxGroupMembers];
   const int64_t s0 = g.sa[0] + sl * g.sb[0], st = g.sa[t] + sl * g.sb[t];
   const int64_t d0 = g.da[0] + dl * g.db[0], dt = g.da[t] + dl * g.db[t];
   const double c = alpha * sh.coef[0];
+  FastDiv f_ct, f_c0;
+  f_ct.init((uint32_t)ct);
+  f_c0.init((uint32_t)c0);
+  const uint32_t tile_n = (uint32_t)(R * ct * c0);
   for (int u = 0; u < job.count; ++u) {
     int64_t U = job.first + u;
-    int u0 = (int)(U % T0);
-    U /= T0;
-    int ut = (int)(U % Tt);
-    int64_t R = U / Tt;
-    int64_t sbase = so, dbase = dof;
-    for (int l = 1; l < g.ndim; ++l) {
-      if (l == t) continue;
-      int64_t e = g.ext[l];
-      int64_t i = R % e;
-      R /= e;
-      sbase += i * (g.sa[l] + sl * g.sb[l]);
-      dbase += i * (g.da[l] + dl * g.db[l]);
-    }
-    const int i0base = u0 * 32, itbase = ut * 32;
-    __syncthreads();
-    // load: lanes run along the src-fastest leg (coalesced)
-    if (itbase + tx < nt) {
-      for (int b = ty; b < 32; b += kPermThreads / 32) {
-        int i0 = i0base + b;
-        if (i0 < n0) tile[b][tx] = __ldg(src + sbase + (int64_t)i0 * s0 + (int64_t)(itbase + tx) * st);
+    const int u0 = (int)(U % g.T0);
+    U /= g.T0;
+    const int ut = (int)(U % g.Tt);
+    const int64_t rb = (U / g.Tt) * R;
+    const int i0b = u0 * c0, itb = ut * ct;
+    const int nr = (int)min((int64_t)R, g.nrest - rb);
+    const int m0 = min(c0, n0 - i0b), mt = min(ct, nt - itb);
+    __syncthreads();  // previous tile fully stored before its smem tables are overwritten
+    for (int r = tid; r < nr; r += kPermThreads) {
+      int64_t Rr = rb + r;
+      int64_t sbase = so, dbase = dof;
+      for (int l = 1; l < g.ndim; ++l) {
+        if (l == t) continue;
+        int64_t e = g.ext[l];
+        int64_t i = Rr % e;
+        Rr /= e;
+        sbase += i * (g.sa[l] + sl * g.sb[l]);
+        dbase += i * (g.da[l] + dl * g.db[l]);
       }
+      sh.rsa[r] = sbase + (int64_t)i0b * s0 + (int64_t)itb * st;
+      sh.rda[r] = dbase + (int64_t)i0b * d0 + (int64_t)itb * dt;
     }
     __syncthreads();
-    // store: lanes run along the dst-fastest leg (coalesced)
-    if (i0base + tx < n0) {
-      for (int a = ty; a < 32; a += kPermThreads / 32) {
-        int it = itbase + a;
-        if (it < nt) {
-          T* yp = dst + dbase + (int64_t)(i0base + tx) * d0 + (int64_t)it * dt;
-          T y = Num<T>::scale(c, tile[tx][a]);
-          if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
-          *yp = y;
-        }
+    for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // source order: it fastest
+      uint32_t q = f_ct.div(e);
+      int it = (int)(e - q * ct);
+      uint32_t r = f_c0.div(q);
+      int i0 = (int)(q - r * c0);
+      if ((int)r < nr && i0 < m0 && it < mt)
+        S[(r * ct + it) * c0p + i0] = __ldg(src + sh.rsa[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // destination order: i0 fastest
+      uint32_t q = f_c0.div(e);
+      int i0 = (int)(e - q * c0);
+      uint32_t r = f_ct.div(q);
+      int it = (int)(q - r * ct);
+      if ((int)r < nr && i0 < m0 && it < mt) {
+        T* yp = dst + sh.rda[r] + (int64_t)i0 * d0 + (int64_t)it * dt;
+        T y = Num<T>::scale(c, S[(r * ct + it) * c0p + i0]);
+        if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
+        *yp = y;
       }
     }
   }
@@ -191,7 +223,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const T* __restri
                                                                const PermJob* __restrict__ jobs, double alpha,
                                                                double beta) {
   __shared__ PermShared sh;
-  __shared__ T tile[32][33];
+  extern __shared__ __align__(16) unsigned char perm_dyn[];
+  T* S = reinterpret_cast<T*>(perm_dyn);
   const PermJob job = jobs[blockIdx.x];
   const PermGroup& g = groups[job.group];
   const int tid = threadIdx.x;
@@ -206,7 +239,7 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const T* __restri
   }
   __syncthreads();
   if (g.mode == 1 && g.ksrc == 1 && g.kdst == 1)
-    permute_tiled<T>(src, dst, g, job, sh, tile, alpha, beta);
+    permute_tiled<T>(src, dst, g, job, sh, S, alpha, beta);
   else
     permute_rows<T>(src, dst, g, job, sh, alpha, beta);
 }
@@ -216,11 +249,29 @@ cudaError_t launch_permute(const double* src, double* dst, const PermGroup* grou
                            double beta, int complex_, cudaStream_t st) {
   int n = njobs_rows + njobs_tiled;
   if (n == 0) return cudaSuccess;
-  if (complex_)
-    permute_kernel<double2><<<n, kPermThreads, 0, st>>>((const double2*)src, (double2*)dst, groups, members, coefs,
-                                                         jobs, alpha, beta);
-  else
-    permute_kernel<double><<<n, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta);
+  // rows jobs need no tile; tiled jobs get kTileElems elements of dynamic smem
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(permute_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kTileElems * sizeof(double2)));
+    attr = true;
+  }
+  if (njobs_rows) {
+    if (complex_)
+      permute_kernel<double2><<<njobs_rows, kPermThreads, 0, st>>>((const double2*)src, (double2*)dst, groups,
+                                                                    members, coefs, jobs, alpha, beta);
+    else
+      permute_kernel<double><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta);
+  }
+  if (njobs_tiled) {
+    const PermJob* tj = jobs + njobs_rows;
+    if (complex_)
+      permute_kernel<double2><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double2), st>>>(
+          (const double2*)src, (double2*)dst, groups, members, coefs, tj, alpha, beta);
+    else
+      permute_kernel<double><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double), st>>>(
+          src, dst, groups, members, coefs, tj, alpha, beta);
+  }
   return cudaGetLastError();
 }
 
@@ -229,6 +280,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
   uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   int n = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -242,20 +297,23 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Shared-memory pitches: As[k][m] with pitch BM+4 and Bs[n][k] with pitch BK+4 (both = 4 mod 16
+// doubles) make the m8n8k4 fragment loads conflict-free in each 16-lane phase of a 64-bit LDS.
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
 struct GemmCfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int MF = WM / 8, NF = WN / 8;
-  static constexpr int LDA_S = BM + 8;  // As[k][m], padded: conflict-free fragment loads
-  static constexpr int LDB_S = BK + 4;  // Bs[n][k]
+  static constexpr int LDA_S = BM + 4;
+  static constexpr int LDB_S = BK + 4;
   static constexpr int A_STAGE = BK * LDA_S, B_STAGE = BN * LDB_S;
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
-__device__ void gemm_tile(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                          const GemmGroup& g, int m0, int n0, double alpha, double beta, double* smem) {
+__device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const double* __restrict__ B,
+                                          double* __restrict__ C, const GemmGroup& g, int m0, int n0, double alpha,
+                                          double beta, bool vec, double* smem) {
   using Cfg = GemmCfg<BM, BN, WM, WN, BK, STAGES>;
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
@@ -277,21 +335,42 @@ __device__ void gemm_tile(const double* __restrict__ A, const double* __restrict
     const int k0 = kt * BK;
     double* as = As + s * Cfg::A_STAGE;
     double* bs = Bs + s * Cfg::B_STAGE;
+    if (vec) {
 #pragma unroll
-    for (int i = 0; i < (BM * BK) / Cfg::THREADS; ++i) {
-      int idx = tid + i * Cfg::THREADS;
-      int m = idx % BM, k = idx / BM;
-      bool ok = (m0 + m < M) && (k0 + k < K);
-      const double* gp = ok ? Ag + (int64_t)(m0 + m) + (int64_t)(k0 + k) * g.lda : A;
-      cp_async8(as + k * Cfg::LDA_S + m, gp, ok);
-    }
+      for (int i = 0; i < (BM / 2 * BK) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int m = 2 * (idx % (BM / 2)), k = idx / (BM / 2);
+        int gm = m0 + m, gk = k0 + k;
+        int nb = (gm < M && gk < K) ? (gm + 1 < M ? 16 : 8) : 0;
+        const double* gp = nb ? Ag + (int64_t)gm + (int64_t)gk * g.lda : A;
+        cp_async16(as + k * Cfg::LDA_S + m, gp, nb);
+      }
 #pragma unroll
-    for (int i = 0; i < (BN * BK) / Cfg::THREADS; ++i) {
-      int idx = tid + i * Cfg::THREADS;
-      int k = idx % BK, n = idx / BK;
-      bool ok = (n0 + n < N) && (k0 + k < K);
-      const double* gp = ok ? Bg + (int64_t)(k0 + k) + (int64_t)(n0 + n) * g.ldb : B;
-      cp_async8(bs + n * Cfg::LDB_S + k, gp, ok);
+      for (int i = 0; i < (BK / 2 * BN) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int k = 2 * (idx % (BK / 2)), n = idx / (BK / 2);
+        int gk = k0 + k, gn = n0 + n;
+        int nb = (gn < N && gk < K) ? (gk + 1 < K ? 16 : 8) : 0;
+        const double* gp = nb ? Bg + (int64_t)gk + (int64_t)gn * g.ldb : B;
+        cp_async16(bs + n * Cfg::LDB_S + k, gp, nb);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (BM * BK) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int m = idx % BM, k = idx / BM;
+        bool ok = (m0 + m < M) && (k0 + k < K);
+        const double* gp = ok ? Ag + (int64_t)(m0 + m) + (int64_t)(k0 + k) * g.lda : A;
+        cp_async8(as + k * Cfg::LDA_S + m, gp, ok);
+      }
+#pragma unroll
+      for (int i = 0; i < (BN * BK) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int k = idx % BK, n = idx / BK;
+        bool ok = (n0 + n < N) && (k0 + k < K);
+        const double* gp = ok ? Bg + (int64_t)(k0 + k) + (int64_t)(n0 + n) * g.ldb : B;
+        cp_async8(bs + n * Cfg::LDB_S + k, gp, ok);
+      }
     }
   };
 
@@ -308,15 +387,15 @@ __device__ void gemm_tile(const double* __restrict__ A, const double* __restrict
       if (nxt < nk) load_stage(nxt, nxt % STAGES);
       cp_async_commit();
     }
-    const double* as = As + (kt % STAGES) * Cfg::A_STAGE;
-    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE;
+    const double* as = As + (kt % STAGES) * Cfg::A_STAGE + wm * WM + gq;
+    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE + (wn * WN + gq) * Cfg::LDB_S + tq;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[Cfg::MF], bf[Cfg::NF];
 #pragma unroll
-      for (int i = 0; i < Cfg::MF; ++i) af[i] = as[(kk + tq) * Cfg::LDA_S + wm * WM + i * 8 + gq];
+      for (int i = 0; i < Cfg::MF; ++i) af[i] = as[(kk + tq) * Cfg::LDA_S + i * 8];
 #pragma unroll
-      for (int j = 0; j < Cfg::NF; ++j) bf[j] = bs[(wn * WN + j * 8 + gq) * Cfg::LDB_S + kk + tq];
+      for (int j = 0; j < Cfg::NF; ++j) bf[j] = bs[j * 8 * Cfg::LDB_S + kk];
 #pragma unroll
       for (int i = 0; i < Cfg::MF; ++i)
 #pragma unroll
@@ -324,7 +403,6 @@ __device__ void gemm_tile(const double* __restrict__ A, const double* __restrict
     }
   }
   cp_async_wait<0>();
-  __syncthreads();
   // epilogue: C = alpha * acc + beta * C (column-major, ldc)
   double* Cg = C + g.c_off;
 #pragma unroll
@@ -347,27 +425,29 @@ __device__ void gemm_tile(const double* __restrict__ A, const double* __restrict
   }
 }
 
-using BigCfg = GemmCfg<128, 128, 64, 32, 16, 3>;
-using SmallCfg = GemmCfg<64, 64, 32, 32, 16, 3>;
+#define TK_BIG 128, 128, 64, 32, 32, 3
+#define TK_SMALL 64, 64, 32, 32, 16, 3
+using BigCfg = GemmCfg<TK_BIG>;
+using SmallCfg = GemmCfg<TK_SMALL>;
 
 __global__ void __launch_bounds__(BigCfg::THREADS, 1)
     gemm_big_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                     const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                    double beta) {
+                    double beta, int base_vec) {
   extern __shared__ __align__(16) double smem[];
   const GemmTile t = tiles[blockIdx.x];
   const GemmGroup g = groups[t.group];
-  gemm_tile<128, 128, 64, 32, 16, 3>(A, B, C, g, t.m0, t.n0, alpha, beta, smem);
+  gemm_tile<TK_BIG>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
 __global__ void __launch_bounds__(SmallCfg::THREADS)
     gemm_small_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                      double beta) {
+                      double beta, int base_vec) {
   extern __shared__ __align__(16) double smem[];
   const GemmTile t = tiles[blockIdx.x];
   const GemmGroup g = groups[t.group];
-  gemm_tile<64, 64, 32, 32, 16, 3>(A, B, C, g, t.m0, t.n0, alpha, beta, smem);
+  gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
@@ -378,11 +458,12 @@ cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmG
     cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
     attr = true;
   }
+  const int base_vec = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0;
   if (ntiles_big)
-    gemm_big_kernel<<<ntiles_big, BigCfg::THREADS, BigCfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta);
+    gemm_big_kernel<<<ntiles_big, BigCfg::THREADS, BigCfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
   if (ntiles_small)
     gemm_small_kernel<<<ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st>>>(A, B, C, groups, tiles + ntiles_big,
-                                                                               alpha, beta);
+                                                                               alpha, beta, base_vec);
   return cudaGetLastError();
 }
 

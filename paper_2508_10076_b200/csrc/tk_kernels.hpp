@@ -19,8 +19,12 @@ struct PermGroup {
   int32_t coef_off;     // into coefs: ksrc * kdst, row-major [i][j]
   int32_t src_mem;      // into members: ksrc source members
   int32_t dst_mem;      // into members: kdst destination members
-  int32_t mode;         // 0 = rows (dst leg 0 is also contiguous-ish in src), 1 = tiled transpose
+  int32_t mode;         // 0 = rows (dst leg 0 is also unit-stride in src), 1 = smem-tiled transpose
   int32_t tleg;         // mode 1: index (dst order) of the src-fastest leg
+  int32_t c0, ct;       // mode 1: chunk of leg 0 / leg tleg held in one smem tile
+  int32_t R;            // mode 1: rest indices (all other legs) packed into one tile
+  int32_t T0, Tt;       // mode 1: number of chunks of leg 0 / leg tleg
+  int64_t nrest;        // mode 1: product of the other legs' extents
   int32_t ext[kMaxLegs];
   int64_t sa[kMaxLegs], sb[kMaxLegs];
   int64_t da[kMaxLegs], db[kMaxLegs];
@@ -33,7 +37,8 @@ struct PermMember {
 };
 
 // A CTA work item: `count` work units of group `group` starting at unit `first`.
-// mode 0 unit = one row (dst leg 0); mode 1 unit = one 32x32 tile of (leg 0, leg tleg) x rest.
+// mode 0 unit = one row (dst leg 0); mode 1 unit = one smem tile of c0 x ct x R elements.
+constexpr int kTileElems = 3072;  // smem tile capacity (elements, incl. padding)
 struct PermJob {
   int32_t group;
   int32_t count;
@@ -45,6 +50,8 @@ struct GemmGroup {
   int64_t a_off, b_off, c_off;  // element offsets into the A~, B~, C base pointers
   int32_t M, N, K;
   int32_t lda, ldb, ldc;
+  int32_t vec;                  // 1: A/B offsets and leading dims even -> 16-byte cp.async
+  int32_t pad_;
 };
 
 struct GemmTile {

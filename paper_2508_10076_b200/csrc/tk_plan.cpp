@@ -175,17 +175,29 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
       g.sa[i] = g.sb[i] = g.da[i] = g.db[i] = 0;
     }
   }
-  // mode: rows if dst leg 0 is also src-contiguous; otherwise tile (leg 0) x (src-fastest leg)
+  // mode: rows if dst leg 0 is also src-contiguous; otherwise tile (leg 0) x (src-fastest leg) x rest
   g.mode = 0;
   g.tleg = 0;
+  g.c0 = g.ct = g.R = g.T0 = g.Tt = 1;
+  g.nrest = 1;
   bool lead_unit = (g.sa[0] == 1 && g.sb[0] == 0);
-  if (!lead_unit && g.ext[0] >= 4) {
+  if (!lead_unit && g.ext[0] >= 2 && g.ksrc == 1 && g.kdst == 1) {
     for (int i = 1; i < g.ndim; ++i)
-      if (g.sa[i] == 1 && g.sb[i] == 0 && g.ext[i] >= 4) {
+      if (g.sa[i] == 1 && g.sb[i] == 0 && g.ext[i] >= 2) {
         g.mode = 1;
         g.tleg = i;
         break;
       }
+  }
+  if (g.mode == 1) {
+    int64_t n0 = g.ext[0], nt = g.ext[g.tleg];
+    g.c0 = (int32_t)std::min<int64_t>(n0, 64);
+    int64_t c0p = g.c0 | 1;
+    g.ct = (int32_t)std::min<int64_t>(nt, std::max<int64_t>(1, 2048 / c0p));
+    g.nrest = g.nelem / (n0 * nt);
+    g.R = (int32_t)std::max<int64_t>(1, std::min<int64_t>({256, g.nrest, kTileElems / (g.ct * c0p)}));
+    g.T0 = (int32_t)((n0 + g.c0 - 1) / g.c0);
+    g.Tt = (int32_t)((nt + g.ct - 1) / g.ct);
   }
 }
 
@@ -198,10 +210,8 @@ static void make_jobs(PermPlan& P) {
       int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, 8192 / std::max(1, g.ext[0])));
       for (int64_t r = 0; r < nrows; r += per) rows.push_back(PermJob{gi, (int32_t)std::min(per, nrows - r), r});
     } else {
-      int64_t t0 = (g.ext[0] + 31) / 32, t1 = (g.ext[g.tleg] + 31) / 32;
-      int64_t rest = g.nelem / ((int64_t)g.ext[0] * g.ext[g.tleg]);
-      int64_t ntiles = t0 * t1 * rest;
-      int64_t per = 8;
+      int64_t ntiles = (int64_t)g.T0 * g.Tt * ((g.nrest + g.R - 1) / g.R);
+      int64_t per = std::max<int64_t>(1, 8192 / ((int64_t)g.R * g.ct * g.c0));
       for (int64_t r = 0; r < ntiles; r += per) tiles.push_back(PermJob{gi, (int32_t)std::min(per, ntiles - r), r});
     }
   }
@@ -211,8 +221,46 @@ static void make_jobs(PermPlan& P) {
   P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
 }
 
+// Internal (workspace) layout of A~, B~, C~: same blocks and subblock order as the canonical
+// layout, but every block's leading dimension is padded to a multiple of 4 doubles and every block
+// starts 32-byte aligned, so the GEMM can use 16-byte cp.async and columns start on sector bounds.
+struct PadLayout {
+  std::vector<int64_t> off, ld;
+  int64_t total = 0;
+};
+
+static PadLayout pad_layout(const Tensor& t) {
+  PadLayout pl;
+  int64_t o = 0;
+  for (const Block& b : t.blocks) {
+    int64_t ld = (b.rows + 3) & ~int64_t(3);
+    pl.off.push_back(o);
+    pl.ld.push_back(ld);
+    o += ld * b.cols;
+  }
+  pl.total = o;
+  return pl;
+}
+
+static int64_t sub_off(const Tensor& t, const PadLayout* pl, int i) {
+  if (!pl) return t.subs[i].off;
+  const Subblock& sb = t.subs[i];
+  return pl->off[sb.block] + sb.row_off + pl->ld[sb.block] * sb.col_off;
+}
+static int64_t sub_ld(const Tensor& t, const PadLayout* pl, int i) { return pl ? pl->ld[t.subs[i].block] : t.ld(i); }
+
+static bool is_identity_perm(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
+  if ((int)p.size() != A.n_cod()) return false;
+  for (int i = 0; i < (int)p.size(); ++i)
+    if (p[i] != i) return false;
+  for (int j = 0; j < (int)q.size(); ++j)
+    if (q[j] != A.n_cod() + j) return false;
+  return true;
+}
+
 static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
-                            PermPlan& P, int elem_bytes) {
+                            PermPlan& P, int elem_bytes, const PadLayout* spl = nullptr,
+                            const PadLayout* dpl = nullptr) {
   Kind k = A.kind;
   int n1 = A.n_cod(), N = A.nlegs();
   std::vector<int> src_leg = dst_from_src_legs(p, q);
@@ -254,9 +302,9 @@ static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const st
       g.coef_off = (int)P.coefs.size();
       P.coefs.push_back((double)koszul_sign(k, lab, n1, p, q));
       g.src_mem = (int)P.members.size();
-      P.members.push_back(PermMember{A.subs[i].off, A.ld(i)});
+      P.members.push_back(PermMember{sub_off(A, spl, i), sub_ld(A, spl, i)});
       g.dst_mem = (int)P.members.size();
-      P.members.push_back(PermMember{C.subs[j].off, C.ld(j)});
+      P.members.push_back(PermMember{sub_off(C, dpl, j), sub_ld(C, dpl, j)});
       finish_group_geometry(g, ext, n1, src_leg, C.n_cod());
       P.groups.push_back(g);
     }
@@ -322,10 +370,10 @@ static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const st
         for (auto& e : rows[a]) M[a * g.kdst + e.first] += e.second;
       P.coefs.insert(P.coefs.end(), M.begin(), M.end());
       g.src_mem = (int)P.members.size();
-      for (int i : srcs) P.members.push_back(PermMember{A.subs[i].off, A.ld(i)});
+      for (int i : srcs) P.members.push_back(PermMember{sub_off(A, spl, i), sub_ld(A, spl, i)});
       g.dst_mem = (int)P.members.size();
       for (int j : dsts) {
-        P.members.push_back(PermMember{C.subs[j].off, C.ld(j)});
+        P.members.push_back(PermMember{sub_off(C, dpl, j), sub_ld(C, dpl, j)});
         dst_done[j] = 1;
       }
       const Tree& s0 = A.s_tree(srcs[0]);
@@ -369,6 +417,7 @@ struct ContractPlan {
   Tensor* Bt = nullptr;
   Tensor* Ct = nullptr;
   PermPlan pa, pb, pc;
+  PadLayout la, lb, lc;  // workspace layouts of A~, B~, C~
   std::vector<GemmGroup> ggroups;
   std::vector<GemmTile> tiles;
   int ntiles_big = 0, ntiles_small = 0;
@@ -476,22 +525,30 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     P.Ct = make_tensor(C.dtype, cod, dom);
   }
   check_target(*P.Ct, t.pAB, t.qAB, C);
-  build_perm_plan(A, t.pA, t.qA, *P.At, P.pa, 8);
-  build_perm_plan(B, t.pB, t.qB, *P.Bt, P.pb, 8);
-  build_perm_plan(*P.Ct, t.pAB, t.qAB, C, P.pc, 8);
+  bool ia_id = is_identity_perm(A, t.pA, t.qA), ib_id = is_identity_perm(B, t.pB, t.qB);
+  bool ic_id = is_identity_perm(*P.Ct, t.pAB, t.qAB);
+  P.la = pad_layout(*P.At);
+  P.lb = pad_layout(*P.Bt);
+  P.lc = pad_layout(*P.Ct);
+  const PadLayout* pla = ia_id ? nullptr : &P.la;
+  const PadLayout* plb = ib_id ? nullptr : &P.lb;
+  const PadLayout* plc = ic_id ? nullptr : &P.lc;
+  build_perm_plan(A, t.pA, t.qA, *P.At, P.pa, 8, nullptr, pla);
+  build_perm_plan(B, t.pB, t.qB, *P.Bt, P.pb, 8, nullptr, plb);
+  build_perm_plan(*P.Ct, t.pAB, t.qAB, C, P.pc, 8, plc, nullptr);
   // workspace: A~ | B~ | C~ (skipped when the permute is the identity)
   size_t off = 0;
   if (!P.pa.identity) {
     P.off_a = off;
-    off = align256(off + (size_t)P.At->nelems * 8);
+    off = align256(off + (size_t)P.la.total * 8);
   }
   if (!P.pb.identity) {
     P.off_b = off;
-    off = align256(off + (size_t)P.Bt->nelems * 8);
+    off = align256(off + (size_t)P.lb.total * 8);
   }
   if (!P.pc.identity) {
     P.off_c = off;
-    off = align256(off + (size_t)P.Ct->nelems * 8);
+    off = align256(off + (size_t)P.lc.total * 8);
   }
   P.ws_bytes = off;
   // Alg. 8: one GEMM per coupled sector of C~; K = 0 blocks are zero-filled
@@ -504,8 +561,8 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     GemmGroup g{};
     g.M = (int32_t)cb.rows;
     g.N = (int32_t)cb.cols;
-    g.c_off = cb.off;
-    g.ldc = (int32_t)cb.rows;
+    g.c_off = plc ? plc->off[ci] : cb.off;
+    g.ldc = (int32_t)(plc ? plc->ld[ci] : cb.rows);
     auto ia = a_blk.find(cb.coupled);
     auto ib = b_blk.find(cb.coupled);
     if (ia != a_blk.end() && ib != b_blk.end()) {
@@ -514,10 +571,11 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
       if (ab.rows != cb.rows || bb.cols != cb.cols || ab.cols != bb.rows)
         TK_THROW(TK_ERR_SPACE_MISMATCH, "internal: block shapes of A~, B~, C~ disagree");
       g.K = (int32_t)ab.cols;
-      g.a_off = ab.off;
-      g.b_off = bb.off;
-      g.lda = (int32_t)ab.rows;
-      g.ldb = (int32_t)bb.rows;
+      g.a_off = pla ? pla->off[ia->second] : ab.off;
+      g.b_off = plb ? plb->off[ib->second] : bb.off;
+      g.lda = (int32_t)(pla ? pla->ld[ia->second] : ab.rows);
+      g.ldb = (int32_t)(plb ? plb->ld[ib->second] : bb.rows);
+      g.vec = (g.a_off % 2 == 0) && (g.lda % 2 == 0) && (g.b_off % 2 == 0) && (g.ldb % 2 == 0);
     } else {
       g.K = 0;
       g.lda = g.ldb = 1;

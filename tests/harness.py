@@ -42,33 +42,7 @@ def oracle_chain_dense(cfg):
     return out
 
 
-class LazyBlocks(dict):
-    """Charge-tuple blocks of an input tensor, generated on first access (keyed values are
-    independent of placement, so block[key] = values reshaped column-major over the legs)."""
-
-    def __init__(self, layout, cfg, tidx):
-        super().__init__()
-        self._sub = {tuple(sb.key[0]) + tuple(sb.key[3]): sb for sb in layout.subblocks}
-        self._cfg, self._tidx = cfg, tidx
-
-    def __iter__(self):
-        return iter(self._sub)
-
-    def __contains__(self, k):
-        return k in self._sub
-
-    def __len__(self):
-        return len(self._sub)
-
-    def __getitem__(self, k):
-        if not dict.__contains__(self, k):
-            sb = self._sub[k]
-            v = gen.subblock_values(self._cfg, self._tidx, sb.key, math.prod(sb.extents))
-            dict.__setitem__(self, k, v.reshape(sb.extents, order="F"))
-        return dict.__getitem__(self, k)
-
-    def keys(self):
-        return self._sub.keys()
+LazyBlocks = BS.LazyBlocks
 
 
 def oracle_chain_blocks(cfg, out_keys_last=None):
