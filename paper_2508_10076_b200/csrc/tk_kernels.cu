@@ -14,6 +14,7 @@
 //                  of all groups listed by the planner (long-K first); K = 0 groups write
 //                  beta*C (the zero fill of P:1271).
 #include <cstdint>
+#include <cstdlib>
 
 #include "tk_kernels.hpp"
 
@@ -96,10 +97,9 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
     const int64_t so = sh.moff[0], sl = sh.mld[0], dof = sh.moff[kMaxGroupMembers], dl = sh.mld[kMaxGroupMembers];
     const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
     const double c = alpha * sh.coef[0];
-    constexpr int U = 4;  // independent loads in flight per thread
+    constexpr int U = 8;  // independent loads in flight per thread (bytes in flight hide DRAM latency)
     for (uint32_t e0 = tid; e0 < total; e0 += U * kPermThreads) {
       T x[U];
-      int64_t yo[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         uint32_t e = e0 + u * kPermThreads;
@@ -107,16 +107,18 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
           uint32_t r = fd.div(e);
           uint32_t i0 = e - r * n0;
           x[u] = __ldg(src + so + sh.rsa[r] + sl * sh.rsb[r] + (int64_t)i0 * s0);
-          yo[u] = dof + sh.rda[r] + dl * sh.rdb[r] + (int64_t)i0 * d0;
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         uint32_t e = e0 + u * kPermThreads;
         if (e < total) {
+          uint32_t r = fd.div(e);
+          uint32_t i0 = e - r * n0;
+          T* yp = dst + dof + sh.rda[r] + dl * sh.rdb[r] + (int64_t)i0 * d0;
           T y = Num<T>::scale(c, x[u]);
-          if (beta != 0.0) y = Num<T>::axpy(beta, dst[yo[u]], y);
-          dst[yo[u]] = y;
+          if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
+          *yp = y;
         }
       }
     }
@@ -149,9 +151,9 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
 template <typename T>
 __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
                               PermShared& sh, T* __restrict__ S, double alpha, double beta) {
-  // One source / destination member (abelian groups). Leg 0 = dst-fastest, leg t = src-fastest.
+  // One source / destination member (abelian groups). Leg 0 = dst-fastest, leg t = dst leg 1.
   // A tile holds chunk c0 of leg 0 x chunk ct of leg t x R consecutive "rest" indices (all other
-  // legs). Loads walk the tile in source order (leg t fastest: coalesced reads), stores walk it in
+  // legs). Loads walk the tile in source-stride order (coalesced reads), stores walk it in
   // destination order (leg 0 fastest: coalesced writes); S[r][it][i0] with an odd row pitch
   // keeps both phases free of shared-memory bank conflicts.
   const int tid = threadIdx.x;
@@ -162,9 +164,14 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
   const int64_t s0 = g.sa[0] + sl * g.sb[0], st = g.sa[t] + sl * g.sb[t];
   const int64_t d0 = g.da[0] + dl * g.db[0], dt = g.da[t] + dl * g.db[t];
   const double c = alpha * sh.coef[0];
-  FastDiv f_ct, f_c0;
+  FastDiv f_ct, f_c0, fa, fb;
   f_ct.init((uint32_t)ct);
   f_c0.init((uint32_t)c0);
+  const int o0 = g.lorder % 3, o1 = (g.lorder / 3) % 3;
+  const uint32_t za = (uint32_t)(o0 == 0 ? c0 : (o0 == 1 ? ct : R));
+  const uint32_t zb = (uint32_t)(o1 == 0 ? c0 : (o1 == 1 ? ct : R));
+  fa.init(za);
+  fb.init(zb);
   const uint32_t tile_n = (uint32_t)(R * ct * c0);
   for (int u = 0; u < job.count; ++u) {
     int64_t U = job.first + u;
@@ -191,13 +198,31 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
       sh.rda[r] = dbase + (int64_t)i0b * d0 + (int64_t)itb * dt;
     }
     __syncthreads();
-    for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // source order: it fastest
-      uint32_t q = f_ct.div(e);
-      int it = (int)(e - q * ct);
-      uint32_t r = f_c0.div(q);
-      int i0 = (int)(q - r * c0);
-      if ((int)r < nr && i0 < m0 && it < mt)
-        S[(r * ct + it) * c0p + i0] = __ldg(src + sh.rsa[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+    constexpr int UL = 8;  // independent global loads in flight per thread
+    for (uint32_t e0 = tid; e0 < tile_n; e0 += UL * kPermThreads) {  // source order (planner's lorder)
+      T v[UL];
+      int so_[UL];
+#pragma unroll
+      for (int k = 0; k < UL; ++k) {
+        uint32_t e = e0 + k * kPermThreads;
+        so_[k] = -1;
+        if (e < tile_n) {
+          uint32_t q = fa.div(e);
+          int x0 = (int)(e - q * za);
+          uint32_t x2 = fb.div(q);
+          int x1 = (int)(q - x2 * zb);
+          int i0 = o0 == 0 ? x0 : (o1 == 0 ? x1 : (int)x2);
+          int it = o0 == 1 ? x0 : (o1 == 1 ? x1 : (int)x2);
+          int r = o0 == 2 ? x0 : (o1 == 2 ? x1 : (int)x2);
+          if (r < nr && i0 < m0 && it < mt) {
+            v[k] = __ldg(src + sh.rsa[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+            so_[k] = (r * ct + it) * c0p + i0;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UL; ++k)
+        if (so_[k] >= 0) S[so_[k]] = v[k];
     }
     __syncthreads();
     for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // destination order: i0 fastest
@@ -216,17 +241,8 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kPermThreads) permute_kernel(const T* __restrict__ src, T* __restrict__ dst,
-                                                               const PermGroup* __restrict__ groups,
-                                                               const PermMember* __restrict__ members,
-                                                               const double* __restrict__ coefs,
-                                                               const PermJob* __restrict__ jobs, double alpha,
-                                                               double beta) {
-  __shared__ PermShared sh;
-  extern __shared__ __align__(16) unsigned char perm_dyn[];
-  T* S = reinterpret_cast<T*>(perm_dyn);
-  const PermJob job = jobs[blockIdx.x];
-  const PermGroup& g = groups[job.group];
+__device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMember* __restrict__ members,
+                                                const double* __restrict__ coefs, PermShared& sh) {
   const int tid = threadIdx.x;
   if (tid < g.ksrc * g.kdst) sh.coef[tid] = coefs[g.coef_off + tid];
   if (tid < g.ksrc) {
@@ -238,10 +254,37 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const T* __restri
     sh.mld[kMaxGroupMembers + tid] = members[g.dst_mem + tid].ld;
   }
   __syncthreads();
-  if (g.mode == 1 && g.ksrc == 1 && g.kdst == 1)
-    permute_tiled<T>(src, dst, g, job, sh, S, alpha, beta);
-  else
-    permute_rows<T>(src, dst, g, job, sh, alpha, beta);
+}
+
+// rows jobs: <= 64 registers so that 4 CTAs (32 warps) share an SM -> enough loads in flight
+template <typename T>
+__global__ void __launch_bounds__(kPermThreads, 4) permute_rows_kernel(const T* __restrict__ src, T* __restrict__ dst,
+                                                                       const PermGroup* __restrict__ groups,
+                                                                       const PermMember* __restrict__ members,
+                                                                       const double* __restrict__ coefs,
+                                                                       const PermJob* __restrict__ jobs, double alpha,
+                                                                       double beta) {
+  __shared__ PermShared sh;
+  const PermJob job = jobs[blockIdx.x];
+  const PermGroup& g = groups[job.group];
+  load_job_header<T>(g, members, coefs, sh);
+  permute_rows<T>(src, dst, g, job, sh, alpha, beta);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kPermThreads, 3) permute_tiled_kernel(const T* __restrict__ src, T* __restrict__ dst,
+                                                                        const PermGroup* __restrict__ groups,
+                                                                        const PermMember* __restrict__ members,
+                                                                        const double* __restrict__ coefs,
+                                                                        const PermJob* __restrict__ jobs, double alpha,
+                                                                        double beta) {
+  __shared__ PermShared sh;
+  extern __shared__ __align__(16) unsigned char perm_dyn[];
+  T* S = reinterpret_cast<T*>(perm_dyn);
+  const PermJob job = jobs[blockIdx.x];
+  const PermGroup& g = groups[job.group];
+  load_job_header<T>(g, members, coefs, sh);
+  permute_tiled<T>(src, dst, g, job, sh, S, alpha, beta);
 }
 
 cudaError_t launch_permute(const double* src, double* dst, const PermGroup* groups, const PermMember* members,
@@ -252,24 +295,25 @@ cudaError_t launch_permute(const double* src, double* dst, const PermGroup* grou
   // rows jobs need no tile; tiled jobs get kTileElems elements of dynamic smem
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(permute_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(permute_tiled_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(kTileElems * sizeof(double2)));
     attr = true;
   }
   if (njobs_rows) {
     if (complex_)
-      permute_kernel<double2><<<njobs_rows, kPermThreads, 0, st>>>((const double2*)src, (double2*)dst, groups,
-                                                                    members, coefs, jobs, alpha, beta);
+      permute_rows_kernel<double2><<<njobs_rows, kPermThreads, 0, st>>>((const double2*)src, (double2*)dst, groups,
+                                                                         members, coefs, jobs, alpha, beta);
     else
-      permute_kernel<double><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta);
+      permute_rows_kernel<double><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha,
+                                                                        beta);
   }
   if (njobs_tiled) {
     const PermJob* tj = jobs + njobs_rows;
     if (complex_)
-      permute_kernel<double2><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double2), st>>>(
+      permute_tiled_kernel<double2><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double2), st>>>(
           (const double2*)src, (double2*)dst, groups, members, coefs, tj, alpha, beta);
     else
-      permute_kernel<double><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double), st>>>(
+      permute_tiled_kernel<double><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double), st>>>(
           src, dst, groups, members, coefs, tj, alpha, beta);
   }
   return cudaGetLastError();
@@ -426,8 +470,10 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
 }
 
 #define TK_BIG 128, 128, 64, 32, 32, 3
+#define TK_BIG16 128, 128, 32, 32, 32, 3
 #define TK_SMALL 64, 64, 32, 32, 16, 3
 using BigCfg = GemmCfg<TK_BIG>;
+using Big16Cfg = GemmCfg<TK_BIG16>;
 using SmallCfg = GemmCfg<TK_SMALL>;
 
 __global__ void __launch_bounds__(BigCfg::THREADS, 1)
@@ -438,6 +484,17 @@ __global__ void __launch_bounds__(BigCfg::THREADS, 1)
   const GemmTile t = tiles[blockIdx.x];
   const GemmGroup g = groups[t.group];
   gemm_tile<TK_BIG>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
+}
+
+// 16 warps of 32x32 on the same 128x128 tile: 4 warps per SMSP to hide LDS latency and barrier skew
+__global__ void __launch_bounds__(Big16Cfg::THREADS, 1)
+    gemm_big16_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
+                      double beta, int base_vec) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmTile t = tiles[blockIdx.x];
+  const GemmGroup g = groups[t.group];
+  gemm_tile<TK_BIG16>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
 __global__ void __launch_bounds__(SmallCfg::THREADS)
@@ -453,14 +510,21 @@ __global__ void __launch_bounds__(SmallCfg::THREADS)
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st) {
   static bool attr = false;
+  static int variant = 16;
   if (!attr) {
     cudaFuncSetAttribute(gemm_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BigCfg::SMEM);
+    cudaFuncSetAttribute(gemm_big16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Big16Cfg::SMEM);
     cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
+    const char* v = getenv("TK_GEMM_BIG_WARPS");
+    if (v) variant = atoi(v);
     attr = true;
   }
   const int base_vec = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0;
-  if (ntiles_big)
+  if (ntiles_big && variant == 8)
     gemm_big_kernel<<<ntiles_big, BigCfg::THREADS, BigCfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big)
+    gemm_big16_kernel<<<ntiles_big, Big16Cfg::THREADS, Big16Cfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta,
+                                                                            base_vec);
   if (ntiles_small)
     gemm_small_kernel<<<ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st>>>(A, B, C, groups, tiles + ntiles_big,
                                                                                alpha, beta, base_vec);

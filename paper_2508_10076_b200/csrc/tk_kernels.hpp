@@ -24,6 +24,9 @@ struct PermGroup {
   int32_t c0, ct;       // mode 1: chunk of leg 0 / leg tleg held in one smem tile
   int32_t R;            // mode 1: rest indices (all other legs) packed into one tile
   int32_t T0, Tt;       // mode 1: number of chunks of leg 0 / leg tleg
+  int32_t lorder;       // mode 1: load-phase walk order, 3 base-3 digits (fastest first) over
+                        //         {0: leg 0 chunk, 1: leg tleg chunk, 2: rest block}
+  int32_t pad0_;
   int64_t nrest;        // mode 1: product of the other legs' extents
   int32_t ext[kMaxLegs];
   int64_t sa[kMaxLegs], sb[kMaxLegs];
@@ -38,7 +41,7 @@ struct PermMember {
 
 // A CTA work item: `count` work units of group `group` starting at unit `first`.
 // mode 0 unit = one row (dst leg 0); mode 1 unit = one smem tile of c0 x ct x R elements.
-constexpr int kTileElems = 3072;  // smem tile capacity (elements, incl. padding)
+constexpr int kTileElems = 4608;  // smem tile capacity (elements, incl. padding)
 struct PermJob {
   int32_t group;
   int32_t count;

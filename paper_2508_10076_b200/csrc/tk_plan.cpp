@@ -2,6 +2,7 @@
 // memoised in a mutex-guarded cache, plus the device-side C ABI calls.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -175,22 +176,20 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
       g.sa[i] = g.sb[i] = g.da[i] = g.db[i] = 0;
     }
   }
-  // mode: rows if dst leg 0 is also src-contiguous; otherwise tile (leg 0) x (src-fastest leg) x rest
+  // mode 1 (smem tile): leg 0 (dst-fastest) x leg 1 (dst-next) x a block of the remaining legs, loaded
+  // in source-stride order and stored in destination order, so both sides stream long contiguous
+  // runs. Mode 0 (direct rows) for single-leg groups and for recoupling groups (k_src, k_dst > 1).
   g.mode = 0;
   g.tleg = 0;
   g.c0 = g.ct = g.R = g.T0 = g.Tt = 1;
+  g.lorder = 0 + 3 * 1 + 9 * 2;
   g.nrest = 1;
+  static const bool tile_all = getenv("TK_PERM_TILE_ALL") != nullptr;
   bool lead_unit = (g.sa[0] == 1 && g.sb[0] == 0);
-  if (!lead_unit && g.ext[0] >= 2 && g.ksrc == 1 && g.kdst == 1) {
-    for (int i = 1; i < g.ndim; ++i)
-      if (g.sa[i] == 1 && g.sb[i] == 0 && g.ext[i] >= 2) {
-        g.mode = 1;
-        g.tleg = i;
-        break;
-      }
-  }
-  if (g.mode == 1) {
-    int64_t n0 = g.ext[0], nt = g.ext[g.tleg];
+  if (g.ndim >= 2 && g.ksrc == 1 && g.kdst == 1 && (!lead_unit || tile_all)) {
+    g.mode = 1;
+    g.tleg = 1;
+    int64_t n0 = g.ext[0], nt = g.ext[1];
     g.c0 = (int32_t)std::min<int64_t>(n0, 64);
     int64_t c0p = g.c0 | 1;
     g.ct = (int32_t)std::min<int64_t>(nt, std::max<int64_t>(1, 2048 / c0p));
@@ -198,6 +197,15 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
     g.R = (int32_t)std::max<int64_t>(1, std::min<int64_t>({256, g.nrest, kTileElems / (g.ct * c0p)}));
     g.T0 = (int32_t)((n0 + g.c0 - 1) / g.c0);
     g.Tt = (int32_t)((nt + g.ct - 1) / g.ct);
+    // load order: the three tile dimensions sorted by source stride (column-major: b-part dominates)
+    auto key = [&](int leg) -> std::pair<int64_t, int64_t> {
+      if (leg < 0) return {INT64_MAX, INT64_MAX};
+      return {g.sb[leg], g.sa[leg]};
+    };
+    int rest0 = g.ndim >= 3 ? 2 : -1;
+    std::pair<std::pair<int64_t, int64_t>, int> d[3] = {{key(0), 0}, {key(1), 1}, {key(rest0), 2}};
+    std::sort(d, d + 3);
+    g.lorder = d[0].second + 3 * d[1].second + 9 * d[2].second;
   }
 }
 
