@@ -53,6 +53,12 @@ struct Num<double2> {
   static __device__ __forceinline__ double2 scale(double a, double2 x) { return make_double2(a * x.x, a * x.y); }
 };
 
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 constexpr int kPermThreads = 256;
 constexpr int kMaxRows = 256;
 
@@ -149,13 +155,23 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
 }
 
 template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+  uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+template <typename T>
 __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
                               PermShared& sh, T* __restrict__ S, double alpha, double beta) {
   // One source / destination member (abelian groups). Leg 0 = dst-fastest, leg t = dst leg 1.
   // A tile holds chunk c0 of leg 0 x chunk ct of leg t x R consecutive "rest" indices (all other
-  // legs). Loads walk the tile in source-stride order (coalesced reads), stores walk it in
-  // destination order (leg 0 fastest: coalesced writes); S[r][it][i0] with an odd row pitch
-  // keeps both phases free of shared-memory bank conflicts.
+  // legs). Loads walk the tile in source-stride order (coalesced reads) as cp.async straight into
+  // shared memory, double-buffered so that tile u+1 streams in while tile u is stored; stores walk
+  // the tile in destination order (leg 0 fastest: coalesced writes). S[r][it][i0] has an odd row
+  // pitch so both phases are free of shared-memory bank conflicts.
   const int tid = threadIdx.x;
   const int t = g.tleg;
   const int n0 = g.ext[0], nt = g.ext[t];
@@ -173,16 +189,26 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
   fa.init(za);
   fb.init(zb);
   const uint32_t tile_n = (uint32_t)(R * ct * c0);
-  for (int u = 0; u < job.count; ++u) {
+  const int half = kTileElems / 2;  // two tile buffers
+#define RS(b) (sh.rsa + (b) * (kMaxRows / 2))
+#define RD(b) (sh.rda + (b) * (kMaxRows / 2))
+
+  auto tile_geom = [&](int u, int& i0b, int& itb, int& nr, int& m0, int& mt, int64_t& rb) {
     int64_t U = job.first + u;
     const int u0 = (int)(U % g.T0);
     U /= g.T0;
     const int ut = (int)(U % g.Tt);
-    const int64_t rb = (U / g.Tt) * R;
-    const int i0b = u0 * c0, itb = ut * ct;
-    const int nr = (int)min((int64_t)R, g.nrest - rb);
-    const int m0 = min(c0, n0 - i0b), mt = min(ct, nt - itb);
-    __syncthreads();  // previous tile fully stored before its smem tables are overwritten
+    rb = (U / g.Tt) * R;
+    i0b = u0 * c0;
+    itb = ut * ct;
+    nr = (int)min((int64_t)R, g.nrest - rb);
+    m0 = min(c0, n0 - i0b);
+    mt = min(ct, nt - itb);
+  };
+  auto tables = [&](int u, int b) {  // per-rest-index base offsets of tile u into table buffer b
+    int i0b, itb, nr, m0, mt;
+    int64_t rb;
+    tile_geom(u, i0b, itb, nr, m0, mt, rb);
     for (int r = tid; r < nr; r += kPermThreads) {
       int64_t Rr = rb + r;
       int64_t sbase = so, dbase = dof;
@@ -194,50 +220,63 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
         sbase += i * (g.sa[l] + sl * g.sb[l]);
         dbase += i * (g.da[l] + dl * g.db[l]);
       }
-      sh.rsa[r] = sbase + (int64_t)i0b * s0 + (int64_t)itb * st;
-      sh.rda[r] = dbase + (int64_t)i0b * d0 + (int64_t)itb * dt;
+      RS(b)[r] = sbase + (int64_t)i0b * s0 + (int64_t)itb * st;
+      RD(b)[r] = dbase + (int64_t)i0b * d0 + (int64_t)itb * dt;
+    }
+  };
+  auto issue_loads = [&](int u, int b) {
+    int i0b, itb, nr, m0, mt;
+    int64_t rb;
+    tile_geom(u, i0b, itb, nr, m0, mt, rb);
+    T* Sb = S + b * half;
+    for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // source order (planner's lorder)
+      uint32_t q = fa.div(e);
+      int x0 = (int)(e - q * za);
+      uint32_t x2 = fb.div(q);
+      int x1 = (int)(q - x2 * zb);
+      int i0 = o0 == 0 ? x0 : (o1 == 0 ? x1 : (int)x2);
+      int it = o0 == 1 ? x0 : (o1 == 1 ? x1 : (int)x2);
+      int r = o0 == 2 ? x0 : (o1 == 2 ? x1 : (int)x2);
+      if (r < nr && i0 < m0 && it < mt)
+        cp_async_elem<T>(Sb + (r * ct + it) * c0p + i0, src + RS(b)[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+    }
+    cp_async_commit();
+  };
+
+  tables(0, 0);
+  __syncthreads();
+  issue_loads(0, 0);
+  for (int u = 0; u < job.count; ++u) {
+    const int b = u & 1;
+    if (u + 1 < job.count) {
+      tables(u + 1, b ^ 1);
+      __syncthreads();
+      issue_loads(u + 1, b ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    constexpr int UL = 8;  // independent global loads in flight per thread
-    for (uint32_t e0 = tid; e0 < tile_n; e0 += UL * kPermThreads) {  // source order (planner's lorder)
-      T v[UL];
-      int so_[UL];
-#pragma unroll
-      for (int k = 0; k < UL; ++k) {
-        uint32_t e = e0 + k * kPermThreads;
-        so_[k] = -1;
-        if (e < tile_n) {
-          uint32_t q = fa.div(e);
-          int x0 = (int)(e - q * za);
-          uint32_t x2 = fb.div(q);
-          int x1 = (int)(q - x2 * zb);
-          int i0 = o0 == 0 ? x0 : (o1 == 0 ? x1 : (int)x2);
-          int it = o0 == 1 ? x0 : (o1 == 1 ? x1 : (int)x2);
-          int r = o0 == 2 ? x0 : (o1 == 2 ? x1 : (int)x2);
-          if (r < nr && i0 < m0 && it < mt) {
-            v[k] = __ldg(src + sh.rsa[r] + (int64_t)i0 * s0 + (int64_t)it * st);
-            so_[k] = (r * ct + it) * c0p + i0;
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < UL; ++k)
-        if (so_[k] >= 0) S[so_[k]] = v[k];
-    }
-    __syncthreads();
+    int i0b, itb, nr, m0, mt;
+    int64_t rb;
+    tile_geom(u, i0b, itb, nr, m0, mt, rb);
+    const T* Sb = S + b * half;
     for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // destination order: i0 fastest
       uint32_t q = f_c0.div(e);
       int i0 = (int)(e - q * c0);
       uint32_t r = f_ct.div(q);
       int it = (int)(q - r * ct);
       if ((int)r < nr && i0 < m0 && it < mt) {
-        T* yp = dst + sh.rda[r] + (int64_t)i0 * d0 + (int64_t)it * dt;
-        T y = Num<T>::scale(c, S[(r * ct + it) * c0p + i0]);
+        T* yp = dst + RD(b)[r] + (int64_t)i0 * d0 + (int64_t)it * dt;
+        T y = Num<T>::scale(c, Sb[(r * ct + it) * c0p + i0]);
         if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
         *yp = y;
       }
     }
+    __syncthreads();  // buffer b and its tables are reused by tile u+2
   }
+#undef RS
+#undef RD
 }
 
 template <typename T>
@@ -272,7 +311,7 @@ __global__ void __launch_bounds__(kPermThreads, 4) permute_rows_kernel(const T* 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kPermThreads, 3) permute_tiled_kernel(const T* __restrict__ src, T* __restrict__ dst,
+__global__ void __launch_bounds__(kPermThreads, 4) permute_tiled_kernel(const T* __restrict__ src, T* __restrict__ dst,
                                                                         const PermGroup* __restrict__ groups,
                                                                         const PermMember* __restrict__ members,
                                                                         const double* __restrict__ coefs,
@@ -328,11 +367,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {

@@ -41,7 +41,7 @@ struct PermMember {
 
 // A CTA work item: `count` work units of group `group` starting at unit `first`.
 // mode 0 unit = one row (dst leg 0); mode 1 unit = one smem tile of c0 x ct x R elements.
-constexpr int kTileElems = 4608;  // smem tile capacity (elements, incl. padding)
+constexpr int kTileElems = 4608;  // smem capacity of the two tile buffers (elements, incl. padding)
 struct PermJob {
   int32_t group;
   int32_t count;

@@ -192,9 +192,9 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
     int64_t n0 = g.ext[0], nt = g.ext[1];
     g.c0 = (int32_t)std::min<int64_t>(n0, 64);
     int64_t c0p = g.c0 | 1;
-    g.ct = (int32_t)std::min<int64_t>(nt, std::max<int64_t>(1, 2048 / c0p));
+    g.ct = (int32_t)std::min<int64_t>(nt, std::max<int64_t>(1, 1024 / c0p));
     g.nrest = g.nelem / (n0 * nt);
-    g.R = (int32_t)std::max<int64_t>(1, std::min<int64_t>({256, g.nrest, kTileElems / (g.ct * c0p)}));
+    g.R = (int32_t)std::max<int64_t>(1, std::min<int64_t>({128, g.nrest, (kTileElems / 2) / (g.ct * c0p)}));
     g.T0 = (int32_t)((n0 + g.c0 - 1) / g.c0);
     g.Tt = (int32_t)((nt + g.ct - 1) / g.ct);
     // load order: the three tile dimensions sorted by source stride (column-major: b-part dominates)
@@ -219,7 +219,7 @@ static void make_jobs(PermPlan& P) {
       for (int64_t r = 0; r < nrows; r += per) rows.push_back(PermJob{gi, (int32_t)std::min(per, nrows - r), r});
     } else {
       int64_t ntiles = (int64_t)g.T0 * g.Tt * ((g.nrest + g.R - 1) / g.R);
-      int64_t per = std::max<int64_t>(1, 8192 / ((int64_t)g.R * g.ct * g.c0));
+      int64_t per = std::max<int64_t>(1, 16384 / ((int64_t)g.R * g.ct * g.c0));
       for (int64_t r = 0; r < ntiles; r += per) tiles.push_back(PermJob{gi, (int32_t)std::min(per, ntiles - r), r});
     }
   }
