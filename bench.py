@@ -310,7 +310,7 @@ def run_gpu(args):
         "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4 contraction, Float64, D_leg={args.d_leg} "
                                f"(reading C20)", "d_leg": args.d_leg, "parallelism": "replicas only",
                    "useful_flops_per_step": flops, "l2": "inputs (8.9 GB/operand) >> 126 MB L2, no flush needed"},
-        "roofline": {"bound": "tensor", "kernel": "gemm_big_kernel+gemm_small_kernel (grouped DMMA GEMM)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_mbar_kernel<2> + gemm_small_kernel (grouped DMMA GEMM, one launch per tile class)",
                      "achieved": round(gemm_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(gemm_tf / FP64_PEAK_TFLOPS, 4),
                      "peak_source": "measured FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt;"
@@ -343,7 +343,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--d-leg", type=int, default=384)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=24.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -503,6 +503,178 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
   }
 }
 
+// ---- mbarrier-pipelined variant: no CTA-wide barrier in the main loop. Every thread issues its
+// share of a stage's cp.async copies and signals them with cp.async.mbarrier.arrive.noinc on the
+// stage's "full" barrier; each warp waits only for the data it needs and releases the stage on an
+// "empty" barrier, so warps may drift up to STAGES-PD-1 stages apart without idling the DMMA pipe.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TK_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra TK_WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+template <int BM, int BN, int WM, int WN, int BK, int STAGES, int PD>
+__device__ __forceinline__ void gemm_tile_mbar(const double* __restrict__ A, const double* __restrict__ B,
+                                               double* __restrict__ C, const GemmGroup& g, int m0, int n0,
+                                               double alpha, double beta, bool vec, double* smem) {
+  using Cfg = GemmCfg<BM, BN, WM, WN, BK, STAGES>;
+  static_assert(PD >= 1 && PD <= STAGES - 1, "prefetch distance");
+  double* As = smem;
+  double* Bs = smem + STAGES * Cfg::A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::B_STAGE);
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
+  const int gq = lane >> 2, tq = lane & 3;
+  const double* Ag = A + g.a_off;
+  const double* Bg = B + g.b_off;
+  const int M = g.M, N = g.N, K = g.K;
+  const int nk = (K + BK - 1) / BK;
+  if (tid < STAGES) {
+    mbar_init(&full[tid], Cfg::THREADS);
+    mbar_init(&empty[tid], Cfg::THREADS / 32);
+  }
+  __syncthreads();
+
+  double acc[Cfg::MF][Cfg::NF][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MF; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load_stage = [&](int kt, int s) {
+    const int k0 = kt * BK;
+    double* as = As + s * Cfg::A_STAGE;
+    double* bs = Bs + s * Cfg::B_STAGE;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < (BM / 2 * BK) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int m = 2 * (idx % (BM / 2)), k = idx / (BM / 2);
+        int gm = m0 + m, gk = k0 + k;
+        int nb = (gm < M && gk < K) ? (gm + 1 < M ? 16 : 8) : 0;
+        const double* gp = nb ? Ag + (int64_t)gm + (int64_t)gk * g.lda : A;
+        cp_async16(as + k * Cfg::LDA_S + m, gp, nb);
+      }
+#pragma unroll
+      for (int i = 0; i < (BK / 2 * BN) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int k = 2 * (idx % (BK / 2)), n = idx / (BK / 2);
+        int gk = k0 + k, gn = n0 + n;
+        int nb = (gn < N && gk < K) ? (gk + 1 < K ? 16 : 8) : 0;
+        const double* gp = nb ? Bg + (int64_t)gk + (int64_t)gn * g.ldb : B;
+        cp_async16(bs + n * Cfg::LDB_S + k, gp, nb);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (BM * BK) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int m = idx % BM, k = idx / BM;
+        bool ok = (m0 + m < M) && (k0 + k < K);
+        const double* gp = ok ? Ag + (int64_t)(m0 + m) + (int64_t)(k0 + k) * g.lda : A;
+        cp_async8(as + k * Cfg::LDA_S + m, gp, ok);
+      }
+#pragma unroll
+      for (int i = 0; i < (BN * BK) / Cfg::THREADS; ++i) {
+        int idx = tid + i * Cfg::THREADS;
+        int k = idx % BK, n = idx / BK;
+        bool ok = (n0 + n < N) && (k0 + k < K);
+        const double* gp = ok ? Bg + (int64_t)(k0 + k) + (int64_t)(n0 + n) * g.ldb : B;
+        cp_async8(bs + n * Cfg::LDB_S + k, gp, ok);
+      }
+    }
+    cp_async_mbar_arrive(&full[s]);
+  };
+
+  for (int s = 0; s < PD && s < nk; ++s) load_stage(s, s);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int nxt = kt + PD;
+    if (nxt < nk) {
+      const int s2 = nxt % STAGES;
+      if (nxt >= STAGES) mbar_wait(&empty[s2], (uint32_t)(((nxt - STAGES) / STAGES) & 1));
+      load_stage(nxt, s2);
+    }
+    const int s = kt % STAGES;
+    mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
+    const double* as = As + s * Cfg::A_STAGE + wm * WM + gq;
+    const double* bs = Bs + s * Cfg::B_STAGE + (wn * WN + gq) * Cfg::LDB_S + tq;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::MF], bf[Cfg::NF];
+#pragma unroll
+      for (int i = 0; i < Cfg::MF; ++i) af[i] = as[(kk + tq) * Cfg::LDA_S + i * 8];
+#pragma unroll
+      for (int j = 0; j < Cfg::NF; ++j) bf[j] = bs[j * 8 * Cfg::LDB_S + kk];
+#pragma unroll
+      for (int i = 0; i < Cfg::MF; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NF; ++j) dmma884(acc[i][j], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  double* Cg = C + g.c_off;
+#pragma unroll
+  for (int i = 0; i < Cfg::MF; ++i) {
+    int m = m0 + wm * WM + i * 8 + gq;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < Cfg::NF; ++j) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        int n = n0 + wn * WN + j * 8 + 2 * tq + c;
+        if (n < N) {
+          double* p = Cg + (int64_t)m + (int64_t)n * g.ldc;
+          double v = alpha * acc[i][j][c];
+          if (beta != 0.0) v = fma(beta, *p, v);
+          *p = v;
+        }
+      }
+    }
+  }
+}
+
+#define TK_MBAR 128, 128, 32, 32, 16, 6
+#define TK_MBAR8 128, 128, 64, 32, 16, 6
+using MbarCfg = GemmCfg<TK_MBAR>;
+using Mbar8Cfg = GemmCfg<TK_MBAR8>;
+constexpr size_t kMbarSmem = MbarCfg::SMEM + 2 * 6 * sizeof(uint64_t);
+
+template <int PD>
+__global__ void __launch_bounds__(MbarCfg::THREADS, 1)
+    gemm_mbar_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                     const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
+                     double beta, int base_vec) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmTile t = tiles[blockIdx.x];
+  const GemmGroup g = groups[t.group];
+  gemm_tile_mbar<TK_MBAR, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
+}
+
+template <int PD>
+__global__ void __launch_bounds__(Mbar8Cfg::THREADS, 1)
+    gemm_mbar8_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
+                      double beta, int base_vec) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmTile t = tiles[blockIdx.x];
+  const GemmGroup g = groups[t.group];
+  gemm_tile_mbar<TK_MBAR8, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
+}
+
 #define TK_BIG 128, 128, 64, 32, 32, 3
 #define TK_BIG16 128, 128, 32, 32, 32, 3
 #define TK_SMALL 64, 64, 32, 32, 16, 3
@@ -544,17 +716,35 @@ __global__ void __launch_bounds__(SmallCfg::THREADS)
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st) {
   static bool attr = false;
-  static int variant = 16;
+  static int variant = 2;  // mbarrier pipeline, 16 warps of 32x32, BK 16, 6 stages, prefetch distance 2
   if (!attr) {
     cudaFuncSetAttribute(gemm_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BigCfg::SMEM);
     cudaFuncSetAttribute(gemm_big16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Big16Cfg::SMEM);
+    cudaFuncSetAttribute(gemm_mbar_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
+    cudaFuncSetAttribute(gemm_mbar_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
+    cudaFuncSetAttribute(gemm_mbar_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
+    cudaFuncSetAttribute(gemm_mbar8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
+    cudaFuncSetAttribute(gemm_mbar8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
+    cudaFuncSetAttribute(gemm_mbar_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
     cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
     const char* v = getenv("TK_GEMM_BIG_WARPS");
     if (v) variant = atoi(v);
     attr = true;
   }
   const int base_vec = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0;
-  if (ntiles_big && variant == 8)
+  if (ntiles_big && variant == 0)
+    gemm_mbar_kernel<3><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big && variant == 2)
+    gemm_mbar_kernel<2><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big && variant == 4)
+    gemm_mbar_kernel<4><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big && variant == 1)
+    gemm_mbar8_kernel<3><<<ntiles_big, Mbar8Cfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big && variant == 5)
+    gemm_mbar8_kernel<2><<<ntiles_big, Mbar8Cfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big && variant == 6)
+    gemm_mbar_kernel<1><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
+  else if (ntiles_big && variant == 8)
     gemm_big_kernel<<<ntiles_big, BigCfg::THREADS, BigCfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
   else if (ntiles_big)
     gemm_big16_kernel<<<ntiles_big, Big16Cfg::THREADS, Big16Cfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta,
