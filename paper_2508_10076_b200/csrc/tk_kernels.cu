@@ -68,15 +68,18 @@ struct PermShared {
   int64_t moff[2 * kMaxGroupMembers], mld[2 * kMaxGroupMembers];
 };
 
-template <typename T>
+template <typename T, bool SINGLE>
 __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
                              PermShared& sh, double alpha, double beta) {
   const int tid = threadIdx.x;
   const int cnt = job.count;
+  const int ks = g.ksrc, kd = g.kdst;
+  constexpr bool single = SINGLE;
+  const int64_t sl = sh.mld[0], dl = sh.mld[kMaxGroupMembers];
   for (int r = tid; r < cnt; r += kPermThreads) {
     int64_t R = job.first + r;
     int64_t sa = 0, sb = 0, da = 0, db = 0;
-#pragma unroll
+#pragma unroll 1
     for (int l = 1; l < kMaxLegs; ++l) {
       if (l < g.ndim) {
         int64_t e = g.ext[l];
@@ -88,22 +91,25 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
         db += i * g.db[l];
       }
     }
-    sh.rsa[r] = sa;
-    sh.rsb[r] = sb;
-    sh.rda[r] = da;
-    sh.rdb[r] = db;
+    if (single) {  // final element offsets of the row start
+      sh.rsa[r] = sh.moff[0] + sa + sl * sb;
+      sh.rda[r] = sh.moff[kMaxGroupMembers] + da + dl * db;
+    } else {
+      sh.rsa[r] = sa;
+      sh.rsb[r] = sb;
+      sh.rda[r] = da;
+      sh.rdb[r] = db;
+    }
   }
   __syncthreads();
-  const uint32_t n0 = (uint32_t)g.ext[0];
-  FastDiv fd;
-  fd.init(n0);
-  const uint32_t total = (uint32_t)cnt * n0;
-  const int ks = g.ksrc, kd = g.kdst;
-  if (ks == 1 && kd == 1) {
-    const int64_t so = sh.moff[0], sl = sh.mld[0], dof = sh.moff[kMaxGroupMembers], dl = sh.mld[kMaxGroupMembers];
+  const int n0 = g.ext[0];
+  if constexpr (SINGLE) {
     const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
     const double c = alpha * sh.coef[0];
     constexpr int U = 8;  // independent loads in flight per thread (bytes in flight hide DRAM latency)
+    FastDiv fd;
+    fd.init((uint32_t)n0);
+    const uint32_t total = (uint32_t)cnt * (uint32_t)n0;
     for (uint32_t e0 = tid; e0 < total; e0 += U * kPermThreads) {
       T x[U];
 #pragma unroll
@@ -111,8 +117,8 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
         uint32_t e = e0 + u * kPermThreads;
         if (e < total) {
           uint32_t r = fd.div(e);
-          uint32_t i0 = e - r * n0;
-          x[u] = __ldg(src + so + sh.rsa[r] + sl * sh.rsb[r] + (int64_t)i0 * s0);
+          uint32_t i0 = e - r * (uint32_t)n0;
+          x[u] = __ldg(src + sh.rsa[r] + (int64_t)i0 * s0);
         }
       }
 #pragma unroll
@@ -120,8 +126,8 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
         uint32_t e = e0 + u * kPermThreads;
         if (e < total) {
           uint32_t r = fd.div(e);
-          uint32_t i0 = e - r * n0;
-          T* yp = dst + dof + sh.rda[r] + dl * sh.rdb[r] + (int64_t)i0 * d0;
+          uint32_t i0 = e - r * (uint32_t)n0;
+          T* yp = dst + sh.rda[r] + (int64_t)i0 * d0;
           T y = Num<T>::scale(c, x[u]);
           if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
           *yp = y;
@@ -130,9 +136,13 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
     }
     return;
   }
+  // recoupling groups (k_src, k_dst > 1): y_j = alpha * sum_i M[i][j] x_i (+ beta y_j)
+  FastDiv fd;
+  fd.init((uint32_t)n0);
+  const uint32_t total = (uint32_t)cnt * (uint32_t)n0;
   for (uint32_t e = tid; e < total; e += kPermThreads) {
     uint32_t r = fd.div(e);
-    uint32_t i0 = e - r * n0;
+    uint32_t i0 = e - r * (uint32_t)n0;
     T x[kMaxGroupMembers];
 #pragma unroll
     for (int i = 0; i < kMaxGroupMembers; ++i)
@@ -163,6 +173,70 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 
+// Mixed-radix counter over a (za, zb, *) box, advanced by a fixed step: no divisions per element.
+struct Walk3 {
+  int x0, x1, x2, d0, d1, d2, za, zb;
+  __device__ __forceinline__ void init(int start, int step, int za_, int zb_) {
+    za = za_;
+    zb = zb_;
+    x0 = start % za;
+    int q = start / za;
+    x1 = q % zb;
+    x2 = q / zb;
+    d0 = step % za;
+    q = step / za;
+    d1 = q % zb;
+    d2 = q / zb;
+  }
+  __device__ __forceinline__ void next() {
+    x0 += d0;
+    int c = x0 >= za;
+    x0 -= c ? za : 0;
+    x1 += d1 + c;
+    c = x1 >= zb;
+    x1 -= c ? zb : 0;
+    x2 += d2 + c;
+  }
+};
+
+// Tile phases, specialised on the load walk order (O0 fastest, O1, O2) over {0: i0, 1: it, 2: r}.
+template <typename T, int O0, int O1, int O2>
+__device__ __forceinline__ void tile_load(const T* __restrict__ src, T* __restrict__ Sb, const int64_t* __restrict__ rs,
+                                          int c0, int ct, int R, int c0p, int nr, int m0, int mt, int64_t s0,
+                                          int64_t st) {
+  const int sz[3] = {c0, ct, R};
+  const int n = c0 * ct * R;
+  Walk3 w;
+  w.init(threadIdx.x, kPermThreads, sz[O0], sz[O1]);
+  for (int e = threadIdx.x; e < n; e += kPermThreads, w.next()) {
+    int v[3];
+    v[O0] = w.x0;
+    v[O1] = w.x1;
+    v[O2] = w.x2;
+    const int i0 = v[0], it = v[1], r = v[2];
+    if (r < nr && i0 < m0 && it < mt)
+      cp_async_elem<T>(Sb + (r * ct + it) * c0p + i0, src + rs[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_store(T* __restrict__ dst, const T* __restrict__ Sb, const int64_t* __restrict__ rd,
+                                           int c0, int ct, int R, int c0p, int nr, int m0, int mt, int64_t d0,
+                                           int64_t dt, double c, double beta) {
+  const int n = c0 * ct * R;
+  Walk3 w;
+  w.init(threadIdx.x, kPermThreads, c0, ct);
+  for (int e = threadIdx.x; e < n; e += kPermThreads, w.next()) {
+    const int i0 = w.x0, it = w.x1, r = w.x2;
+    if (r < nr && i0 < m0 && it < mt) {
+      T* yp = dst + rd[r] + (int64_t)i0 * d0 + (int64_t)it * dt;
+      T y = Num<T>::scale(c, Sb[(r * ct + it) * c0p + i0]);
+      if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
+      *yp = y;
+    }
+  }
+}
+
 template <typename T>
 __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
                               PermShared& sh, T* __restrict__ S, double alpha, double beta) {
@@ -180,18 +254,8 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
   const int64_t s0 = g.sa[0] + sl * g.sb[0], st = g.sa[t] + sl * g.sb[t];
   const int64_t d0 = g.da[0] + dl * g.db[0], dt = g.da[t] + dl * g.db[t];
   const double c = alpha * sh.coef[0];
-  FastDiv f_ct, f_c0, fa, fb;
-  f_ct.init((uint32_t)ct);
-  f_c0.init((uint32_t)c0);
-  const int o0 = g.lorder % 3, o1 = (g.lorder / 3) % 3;
-  const uint32_t za = (uint32_t)(o0 == 0 ? c0 : (o0 == 1 ? ct : R));
-  const uint32_t zb = (uint32_t)(o1 == 0 ? c0 : (o1 == 1 ? ct : R));
-  fa.init(za);
-  fb.init(zb);
-  const uint32_t tile_n = (uint32_t)(R * ct * c0);
+  const int lorder = g.lorder;
   const int half = kTileElems / 2;  // two tile buffers
-#define RS(b) (sh.rsa + (b) * (kMaxRows / 2))
-#define RD(b) (sh.rda + (b) * (kMaxRows / 2))
 
   auto tile_geom = [&](int u, int& i0b, int& itb, int& nr, int& m0, int& mt, int64_t& rb) {
     int64_t U = job.first + u;
@@ -209,6 +273,8 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
     int i0b, itb, nr, m0, mt;
     int64_t rb;
     tile_geom(u, i0b, itb, nr, m0, mt, rb);
+    int64_t* rs = sh.rsa + b * (kMaxRows / 2);
+    int64_t* rd = sh.rda + b * (kMaxRows / 2);
     for (int r = tid; r < nr; r += kPermThreads) {
       int64_t Rr = rb + r;
       int64_t sbase = so, dbase = dof;
@@ -220,8 +286,8 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
         sbase += i * (g.sa[l] + sl * g.sb[l]);
         dbase += i * (g.da[l] + dl * g.db[l]);
       }
-      RS(b)[r] = sbase + (int64_t)i0b * s0 + (int64_t)itb * st;
-      RD(b)[r] = dbase + (int64_t)i0b * d0 + (int64_t)itb * dt;
+      rs[r] = sbase + (int64_t)i0b * s0 + (int64_t)itb * st;
+      rd[r] = dbase + (int64_t)i0b * d0 + (int64_t)itb * dt;
     }
   };
   auto issue_loads = [&](int u, int b) {
@@ -229,16 +295,14 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
     int64_t rb;
     tile_geom(u, i0b, itb, nr, m0, mt, rb);
     T* Sb = S + b * half;
-    for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // source order (planner's lorder)
-      uint32_t q = fa.div(e);
-      int x0 = (int)(e - q * za);
-      uint32_t x2 = fb.div(q);
-      int x1 = (int)(q - x2 * zb);
-      int i0 = o0 == 0 ? x0 : (o1 == 0 ? x1 : (int)x2);
-      int it = o0 == 1 ? x0 : (o1 == 1 ? x1 : (int)x2);
-      int r = o0 == 2 ? x0 : (o1 == 2 ? x1 : (int)x2);
-      if (r < nr && i0 < m0 && it < mt)
-        cp_async_elem<T>(Sb + (r * ct + it) * c0p + i0, src + RS(b)[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+    const int64_t* rs = sh.rsa + b * (kMaxRows / 2);
+    switch (lorder) {
+      case 0 + 3 * 1 + 9 * 2: tile_load<T, 0, 1, 2>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
+      case 0 + 3 * 2 + 9 * 1: tile_load<T, 0, 2, 1>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
+      case 1 + 3 * 0 + 9 * 2: tile_load<T, 1, 0, 2>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
+      case 1 + 3 * 2 + 9 * 0: tile_load<T, 1, 2, 0>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
+      case 2 + 3 * 0 + 9 * 1: tile_load<T, 2, 0, 1>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
+      default: tile_load<T, 2, 1, 0>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
     }
     cp_async_commit();
   };
@@ -260,23 +324,9 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
     int i0b, itb, nr, m0, mt;
     int64_t rb;
     tile_geom(u, i0b, itb, nr, m0, mt, rb);
-    const T* Sb = S + b * half;
-    for (uint32_t e = tid; e < tile_n; e += kPermThreads) {  // destination order: i0 fastest
-      uint32_t q = f_c0.div(e);
-      int i0 = (int)(e - q * c0);
-      uint32_t r = f_ct.div(q);
-      int it = (int)(q - r * ct);
-      if ((int)r < nr && i0 < m0 && it < mt) {
-        T* yp = dst + RD(b)[r] + (int64_t)i0 * d0 + (int64_t)it * dt;
-        T y = Num<T>::scale(c, Sb[(r * ct + it) * c0p + i0]);
-        if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
-        *yp = y;
-      }
-    }
+    tile_store<T>(dst, S + b * half, sh.rda + b * (kMaxRows / 2), c0, ct, R, c0p, nr, m0, mt, d0, dt, c, beta);
     __syncthreads();  // buffer b and its tables are reused by tile u+2
   }
-#undef RS
-#undef RD
 }
 
 template <typename T>
@@ -295,7 +345,7 @@ __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMe
   __syncthreads();
 }
 
-// rows jobs: <= 64 registers so that 4 CTAs (32 warps) share an SM -> enough loads in flight
+// rows jobs of single-member groups: <= 64 registers so that 4 CTAs (32 warps) share an SM
 template <typename T>
 __global__ void __launch_bounds__(kPermThreads, 4) permute_rows_kernel(const T* __restrict__ src, T* __restrict__ dst,
                                                                        const PermGroup* __restrict__ groups,
@@ -307,7 +357,20 @@ __global__ void __launch_bounds__(kPermThreads, 4) permute_rows_kernel(const T* 
   const PermJob job = jobs[blockIdx.x];
   const PermGroup& g = groups[job.group];
   load_job_header<T>(g, members, coefs, sh);
-  permute_rows<T>(src, dst, g, job, sh, alpha, beta);
+  permute_rows<T, true>(src, dst, g, job, sh, alpha, beta);
+}
+
+// rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight)
+template <typename T>
+__global__ void __launch_bounds__(kPermThreads, 2) permute_recouple_kernel(
+    const T* __restrict__ src, T* __restrict__ dst, const PermGroup* __restrict__ groups,
+    const PermMember* __restrict__ members, const double* __restrict__ coefs, const PermJob* __restrict__ jobs,
+    double alpha, double beta) {
+  __shared__ PermShared sh;
+  const PermJob job = jobs[blockIdx.x];
+  const PermGroup& g = groups[job.group];
+  load_job_header<T>(g, members, coefs, sh);
+  permute_rows<T, false>(src, dst, g, job, sh, alpha, beta);
 }
 
 template <typename T>
@@ -327,31 +390,35 @@ __global__ void __launch_bounds__(kPermThreads, 4) permute_tiled_kernel(const T*
 }
 
 cudaError_t launch_permute(const double* src, double* dst, const PermGroup* groups, const PermMember* members,
-                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_tiled, double alpha,
-                           double beta, int complex_, cudaStream_t st) {
-  int n = njobs_rows + njobs_tiled;
-  if (n == 0) return cudaSuccess;
-  // rows jobs need no tile; tiled jobs get kTileElems elements of dynamic smem
+                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi, int njobs_tiled,
+                           double alpha, double beta, int complex_, cudaStream_t st) {
+  // job table layout: [rows (single member) | rows (recoupling groups) | tiled]
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(permute_tiled_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(kTileElems * sizeof(double2)));
     attr = true;
   }
-  if (njobs_rows) {
-    if (complex_)
-      permute_rows_kernel<double2><<<njobs_rows, kPermThreads, 0, st>>>((const double2*)src, (double2*)dst, groups,
-                                                                         members, coefs, jobs, alpha, beta);
-    else
-      permute_rows_kernel<double><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha,
-                                                                        beta);
-  }
-  if (njobs_tiled) {
-    const PermJob* tj = jobs + njobs_rows;
-    if (complex_)
+  const PermJob* mj = jobs + njobs_rows;
+  const PermJob* tj = jobs + njobs_rows + njobs_multi;
+  if (complex_) {
+    const double2* s2 = (const double2*)src;
+    double2* d2 = (double2*)dst;
+    if (njobs_rows)
+      permute_rows_kernel<double2><<<njobs_rows, kPermThreads, 0, st>>>(s2, d2, groups, members, coefs, jobs, alpha, beta);
+    if (njobs_multi)
+      permute_recouple_kernel<double2><<<njobs_multi, kPermThreads, 0, st>>>(s2, d2, groups, members, coefs, mj, alpha,
+                                                                             beta);
+    if (njobs_tiled)
       permute_tiled_kernel<double2><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double2), st>>>(
-          (const double2*)src, (double2*)dst, groups, members, coefs, tj, alpha, beta);
-    else
+          s2, d2, groups, members, coefs, tj, alpha, beta);
+  } else {
+    if (njobs_rows)
+      permute_rows_kernel<double><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta);
+    if (njobs_multi)
+      permute_recouple_kernel<double><<<njobs_multi, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, mj, alpha,
+                                                                            beta);
+    if (njobs_tiled)
       permute_tiled_kernel<double><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double), st>>>(
           src, dst, groups, members, coefs, tj, alpha, beta);
   }

@@ -65,8 +65,8 @@ struct GemmTile {
 
 // launchers (tk_kernels.cu)
 cudaError_t launch_permute(const double* src, double* dst, const PermGroup* groups, const PermMember* members,
-                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_tiled,
-                           double alpha, double beta, int complex_, cudaStream_t st);
+                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi,
+                           int njobs_tiled, double alpha, double beta, int complex_, cudaStream_t st);
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st);
 

@@ -40,7 +40,7 @@ struct PermPlan {
   std::vector<PermMember> members;
   std::vector<double> coefs;
   std::vector<PermJob> jobs;
-  int njobs_rows = 0, njobs_tiled = 0;
+  int njobs_rows = 0, njobs_multi = 0, njobs_tiled = 0;
   DevBuf d_groups, d_members, d_coefs, d_jobs;
   double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
   int64_t n_src = 0, n_dst = 0;
@@ -210,13 +210,14 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
 }
 
 static void make_jobs(PermPlan& P) {
-  std::vector<PermJob> rows, tiles;
+  std::vector<PermJob> rows, multi, tiles;
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
     if (g.mode == 0) {
       int64_t nrows = g.nelem / g.ext[0];
       int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, 8192 / std::max(1, g.ext[0])));
-      for (int64_t r = 0; r < nrows; r += per) rows.push_back(PermJob{gi, (int32_t)std::min(per, nrows - r), r});
+      auto& dst = (g.ksrc == 1 && g.kdst == 1) ? rows : multi;
+      for (int64_t r = 0; r < nrows; r += per) dst.push_back(PermJob{gi, (int32_t)std::min(per, nrows - r), r});
     } else {
       int64_t ntiles = (int64_t)g.T0 * g.Tt * ((g.nrest + g.R - 1) / g.R);
       int64_t per = std::max<int64_t>(1, 16384 / ((int64_t)g.R * g.ct * g.c0));
@@ -224,8 +225,10 @@ static void make_jobs(PermPlan& P) {
     }
   }
   P.njobs_rows = (int)rows.size();
+  P.njobs_multi = (int)multi.size();
   P.njobs_tiled = (int)tiles.size();
   P.jobs = rows;
+  P.jobs.insert(P.jobs.end(), multi.begin(), multi.end());
   P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
 }
 
@@ -509,6 +512,34 @@ static Tuples tuples_from_labels(const Tensor& A, const int32_t* labA, const Ten
   return t;
 }
 
+// Bosonic kinds: the order of the contracted legs inside A~ / B~ is free (the permutes are plain
+// basis changes, reading C2), so pick the order (A's or B's) that makes the operand permutes cheapest:
+// identity (no pass) < leading leg kept (coalesced rows path) < leading leg changes (smem transpose).
+// Fermionic kinds keep reading C2 literally, because there the tuples fix the signs (C13).
+static double perm_cost(const Tensor& X, const std::vector<int>& p, const std::vector<int>& q) {
+  if (is_identity_perm(X, p, q)) return 0.0;
+  int lead = p.empty() ? q[0] : p[0];
+  return (double)X.nelems * (lead == 0 ? 1.0 : 2.0);
+}
+
+static void choose_contracted_order(const Tensor& A, const Tensor& B, Tuples& t) {
+  if (kind_fermionic(A.kind) || t.qA.size() < 2) return;
+  std::vector<int> idx(t.qA.size());
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return t.pB[x] < t.pB[y]; });
+  std::vector<int> qA2, pB2;
+  for (int i : idx) {
+    qA2.push_back(t.qA[i]);
+    pB2.push_back(t.pB[i]);
+  }
+  double c1 = perm_cost(A, t.pA, t.qA) + perm_cost(B, t.pB, t.qB);
+  double c2 = perm_cost(A, t.pA, qA2) + perm_cost(B, pB2, t.qB);
+  if (c2 < c1) {
+    t.qA = qA2;
+    t.pB = pB2;
+  }
+}
+
 static Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, tk_dtype dt) {
   std::vector<Space*> cod, dom;
   permuted_spaces(A, p, q, cod, dom);
@@ -526,6 +557,7 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   if (A.dtype != TK_F64 || B.dtype != TK_F64 || C.dtype != TK_F64)
     TK_THROW(TK_ERR_UNSUPPORTED, "tk_contract: only Float64 in this build");
   Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
+  choose_contracted_order(A, B, t);
   P.At = permuted_tensor(A, t.pA, t.qA, A.dtype);
   P.Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
   {
@@ -684,7 +716,7 @@ static void run_permute(PermPlan& P, const double* src, double* dst, double alph
   P.upload();
   if (P.jobs.empty()) return;
   check_cuda(launch_permute(src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p,
-                            (const double*)P.d_coefs.p, (const PermJob*)P.d_jobs.p, P.njobs_rows, P.njobs_tiled,
+                            (const double*)P.d_coefs.p, (const PermJob*)P.d_jobs.p, P.njobs_rows, P.njobs_multi, P.njobs_tiled,
                             alpha, beta, cplx ? 1 : 0, st),
              "permute launch");
   ++g_launches;
