@@ -625,8 +625,14 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     P.ggroups.push_back(g);
     bool isbig = g.M >= 96 && g.N >= 96;
     int bm = isbig ? 128 : 64, bn = isbig ? 128 : 64;
-    for (int m0 = 0; m0 < g.M; m0 += bm)
-      for (int n0 = 0; n0 < g.N; n0 += bn) (isbig ? big : small).push_back(GemmTile{gi, m0, n0, g.K});
+    // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that one wave of
+    // ~148 co-resident tiles covers a ~G x 12 rectangle and shares the A and B k-slices in L2
+    // (row-major order re-read all of B from DRAM once per tile-row).
+    const int ntm = (g.M + bm - 1) / bm, ntn = (g.N + bn - 1) / bn, G = 12;
+    for (int mb = 0; mb < ntm; mb += G)
+      for (int nt = 0; nt < ntn; ++nt)
+        for (int mt = mb; mt < std::min(ntm, mb + G); ++mt)
+          (isbig ? big : small).push_back(GemmTile{gi, mt * bm, nt * bn, g.K});
   }
   auto by_k = [](const GemmTile& x, const GemmTile& y) { return x.pad > y.pad; };  // LPT: long K first
   std::stable_sort(big.begin(), big.end(), by_k);
