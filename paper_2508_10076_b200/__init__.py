@@ -6,4 +6,7 @@ sm_100a CUDA kernels (batched subblock permute, grouped FP64 DMMA GEMM).
 `paper_2508_10076_b200.tk` is its thin ctypes binding; `layout_io` places and
 reads seeded subblock values through the library's own layout queries.
 """
-from . import tk  # noqa: F401  (fails loudly when the in-tree library is missing)
+# `tk` is not imported here so that `paper_2508_10076_b200.build` can run on a fresh checkout;
+# importing `paper_2508_10076_b200.tk` raises ImportError when the in-tree library is missing
+# (there is no CPU fallback).
+__all__ = ["tk", "layout_io", "build"]
