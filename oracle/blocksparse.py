@@ -124,10 +124,10 @@ class LazyBlocks(dict):
     """Charge-tuple blocks of an input tensor, generated on first access (keyed values are
     independent of placement, so block[key] = values reshaped column-major over the legs)."""
 
-    def __init__(self, layout, cfg, tidx):
+    def __init__(self, layout, cfg, tidx, complex_=False):
         super().__init__()
         self._sub = {tuple(sb.key[0]) + tuple(sb.key[3]): sb for sb in layout.subblocks}
-        self._cfg, self._tidx = cfg, tidx
+        self._cfg, self._tidx, self._complex = cfg, tidx, complex_
 
     def __iter__(self):
         return iter(self._sub)
@@ -141,7 +141,7 @@ class LazyBlocks(dict):
     def __getitem__(self, k):
         if not dict.__contains__(self, k):
             sb = self._sub[k]
-            v = gen.subblock_values(self._cfg, self._tidx, sb.key, math.prod(sb.extents))
+            v = gen.subblock_values(self._cfg, self._tidx, sb.key, math.prod(sb.extents), self._complex)
             dict.__setitem__(self, k, v.reshape(sb.extents, order="F"))
         return dict.__getitem__(self, k)
 

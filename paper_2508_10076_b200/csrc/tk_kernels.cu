@@ -15,6 +15,7 @@
 //                  beta*C (the zero fill of P:1271).
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "tk_kernels.hpp"
 
@@ -62,19 +63,56 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr int kPermThreads = 256;
 constexpr int kMaxRows = 256;
 
+// Element I/O of the permute kernels per complex mode CM (see PermCM in tk_kernels.hpp). Offsets are in
+// units of the pointer type: complex elements for interleaved buffers, doubles for planar ones. A
+// planar member's imaginary part sits d1 doubles after its real part; the real representation of a
+// B~ block stores [[re, im], [-im, re]] at +0, +d1, +d2, +d1+d2 (d1 = N ld, d2 = K).
+template <int CM>
+struct CIO {
+  using V = typename std::conditional<CM == kPermReal, double, double2>::type;  // value in registers
+  using S = typename std::conditional<CM == kPermReal || CM == kPermPlanarToC, double, double2>::type;
+  using D = typename std::conditional<CM == kPermCToC || CM == kPermPlanarToC, double2, double>::type;
+  static __device__ __forceinline__ V load(const S* __restrict__ src, int64_t o, int64_t d1) {
+    if constexpr (CM == kPermPlanarToC)
+      return make_double2(__ldg(src + o), __ldg(src + o + d1));
+    else
+      return __ldg(src + o);
+  }
+  // y already carries alpha * coefficient; ims = -1 conjugates (operand permutes of tk_contract)
+  static __device__ __forceinline__ void store(D* __restrict__ dst, int64_t o, int64_t d1, int64_t d2, V y,
+                                               double beta, double ims) {
+    if constexpr (CM == kPermReal || CM == kPermCToC || CM == kPermPlanarToC) {
+      if (beta != 0.0) y = Num<V>::axpy(beta, dst[o], y);
+      dst[o] = y;
+    } else if constexpr (CM == kPermCToPlanar) {  // workspace target: beta == 0 (host-checked)
+      dst[o] = y.x;
+      dst[o + d1] = ims * y.y;
+    } else {  // kPermCToRealRep
+      const double im = ims * y.y;
+      dst[o] = y.x;
+      dst[o + d1] = im;
+      dst[o + d2] = -im;
+      dst[o + d1 + d2] = y.x;
+    }
+  }
+};
+
 struct PermShared {
   int64_t rsa[kMaxRows], rsb[kMaxRows], rda[kMaxRows], rdb[kMaxRows];
   double coef[kMaxGroupMembers * kMaxGroupMembers];
   int64_t moff[2 * kMaxGroupMembers], mld[2 * kMaxGroupMembers];
+  int64_t md1[2 * kMaxGroupMembers], md2[2 * kMaxGroupMembers];
 };
 
-template <typename T, bool SINGLE>
-__device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
-                             PermShared& sh, double alpha, double beta) {
+template <int CM, bool SINGLE>
+__device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                             const PermGroup& g, const PermJob& job, PermShared& sh, double alpha, double beta,
+                             double ims) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
   const int tid = threadIdx.x;
   const int cnt = job.count;
   const int ks = g.ksrc, kd = g.kdst;
-  constexpr bool single = SINGLE;
   const int64_t sl = sh.mld[0], dl = sh.mld[kMaxGroupMembers];
   for (int r = tid; r < cnt; r += kPermThreads) {
     int64_t R = job.first + r;
@@ -91,7 +129,7 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
         db += i * g.db[l];
       }
     }
-    if (single) {  // final element offsets of the row start
+    if (SINGLE) {  // final element offsets of the row start
       sh.rsa[r] = sh.moff[0] + sa + sl * sb;
       sh.rda[r] = sh.moff[kMaxGroupMembers] + da + dl * db;
     } else {
@@ -105,20 +143,22 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
   const int n0 = g.ext[0];
   if constexpr (SINGLE) {
     const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
+    const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
     const double c = alpha * sh.coef[0];
-    constexpr int U = 8;  // independent loads in flight per thread (bytes in flight hide DRAM latency)
+    // independent loads in flight per thread (64 bytes: bytes in flight hide DRAM latency)
+    constexpr int U = sizeof(V) == 16 ? 4 : 8;
     FastDiv fd;
     fd.init((uint32_t)n0);
     const uint32_t total = (uint32_t)cnt * (uint32_t)n0;
     for (uint32_t e0 = tid; e0 < total; e0 += U * kPermThreads) {
-      T x[U];
+      V x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         uint32_t e = e0 + u * kPermThreads;
         if (e < total) {
           uint32_t r = fd.div(e);
           uint32_t i0 = e - r * (uint32_t)n0;
-          x[u] = __ldg(src + sh.rsa[r] + (int64_t)i0 * s0);
+          x[u] = IO::load(src, sh.rsa[r] + (int64_t)i0 * s0, sd1);
         }
       }
 #pragma unroll
@@ -127,10 +167,7 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
         if (e < total) {
           uint32_t r = fd.div(e);
           uint32_t i0 = e - r * (uint32_t)n0;
-          T* yp = dst + sh.rda[r] + (int64_t)i0 * d0;
-          T y = Num<T>::scale(c, x[u]);
-          if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
-          *yp = y;
+          IO::store(dst, sh.rda[r] + (int64_t)i0 * d0, dd1, dd2, Num<V>::scale(c, x[u]), beta, ims);
         }
       }
     }
@@ -143,23 +180,22 @@ __device__ void permute_rows(const T* __restrict__ src, T* __restrict__ dst, con
   for (uint32_t e = tid; e < total; e += kPermThreads) {
     uint32_t r = fd.div(e);
     uint32_t i0 = e - r * (uint32_t)n0;
-    T x[kMaxGroupMembers];
+    V x[kMaxGroupMembers];
 #pragma unroll
     for (int i = 0; i < kMaxGroupMembers; ++i)
       if (i < ks) {
         int64_t ld = sh.mld[i];
-        x[i] = __ldg(src + sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]));
+        x[i] = IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]), sh.md1[i]);
       }
     for (int j = 0; j < kd; ++j) {
-      T acc = Num<T>::zero();
+      V acc = Num<V>::zero();
 #pragma unroll
       for (int i = 0; i < kMaxGroupMembers; ++i)
-        if (i < ks) acc = Num<T>::axpy(sh.coef[i * kd + j], x[i], acc);
-      int64_t ld = sh.mld[kMaxGroupMembers + j];
-      T* yp = dst + sh.moff[kMaxGroupMembers + j] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]);
-      T y = Num<T>::scale(alpha, acc);
-      if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
-      *yp = y;
+        if (i < ks) acc = Num<V>::axpy(sh.coef[i * kd + j], x[i], acc);
+      const int jm = kMaxGroupMembers + j;
+      int64_t ld = sh.mld[jm];
+      IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]), sh.md1[jm],
+                sh.md2[jm], Num<V>::scale(alpha, acc), beta, ims);
     }
   }
 }
@@ -171,6 +207,17 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
   else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// stage one source element into shared memory (planar sources: real and imaginary part separately)
+template <int CM>
+__device__ __forceinline__ void stage_elem(typename CIO<CM>::V* smem, const typename CIO<CM>::S* gmem, int64_t d1) {
+  if constexpr (CM == kPermPlanarToC) {
+    cp_async_elem<double>(&smem->x, gmem);
+    cp_async_elem<double>(&smem->y, gmem + d1);
+  } else {
+    cp_async_elem<typename CIO<CM>::S>(smem, gmem);
+  }
 }
 
 // Mixed-radix counter over a (za, zb, *) box, advanced by a fixed step: no divisions per element.
@@ -200,10 +247,10 @@ struct Walk3 {
 };
 
 // Tile phases, specialised on the load walk order (O0 fastest, O1, O2) over {0: i0, 1: it, 2: r}.
-template <typename T, int O0, int O1, int O2>
-__device__ __forceinline__ void tile_load(const T* __restrict__ src, T* __restrict__ Sb, const int64_t* __restrict__ rs,
-                                          int c0, int ct, int R, int c0p, int nr, int m0, int mt, int64_t s0,
-                                          int64_t st) {
+template <int CM, int O0, int O1, int O2>
+__device__ __forceinline__ void tile_load(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::V* __restrict__ Sb,
+                                          const int64_t* __restrict__ rs, int c0, int ct, int R, int c0p, int nr,
+                                          int m0, int mt, int64_t s0, int64_t st, int64_t sd1) {
   const int sz[3] = {c0, ct, R};
   const int n = c0 * ct * R;
   Walk3 w;
@@ -215,31 +262,31 @@ __device__ __forceinline__ void tile_load(const T* __restrict__ src, T* __restri
     v[O2] = w.x2;
     const int i0 = v[0], it = v[1], r = v[2];
     if (r < nr && i0 < m0 && it < mt)
-      cp_async_elem<T>(Sb + (r * ct + it) * c0p + i0, src + rs[r] + (int64_t)i0 * s0 + (int64_t)it * st);
+      stage_elem<CM>(Sb + (r * ct + it) * c0p + i0, src + rs[r] + (int64_t)i0 * s0 + (int64_t)it * st, sd1);
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void tile_store(T* __restrict__ dst, const T* __restrict__ Sb, const int64_t* __restrict__ rd,
-                                           int c0, int ct, int R, int c0p, int nr, int m0, int mt, int64_t d0,
-                                           int64_t dt, double c, double beta) {
+template <int CM>
+__device__ __forceinline__ void tile_store(typename CIO<CM>::D* __restrict__ dst, const typename CIO<CM>::V* __restrict__ Sb,
+                                           const int64_t* __restrict__ rd, int c0, int ct, int R, int c0p, int nr,
+                                           int m0, int mt, int64_t d0, int64_t dt, int64_t dd1, int64_t dd2, double c,
+                                           double beta, double ims) {
+  using V = typename CIO<CM>::V;
   const int n = c0 * ct * R;
   Walk3 w;
   w.init(threadIdx.x, kPermThreads, c0, ct);
   for (int e = threadIdx.x; e < n; e += kPermThreads, w.next()) {
     const int i0 = w.x0, it = w.x1, r = w.x2;
-    if (r < nr && i0 < m0 && it < mt) {
-      T* yp = dst + rd[r] + (int64_t)i0 * d0 + (int64_t)it * dt;
-      T y = Num<T>::scale(c, Sb[(r * ct + it) * c0p + i0]);
-      if (beta != 0.0) y = Num<T>::axpy(beta, *yp, y);
-      *yp = y;
-    }
+    if (r < nr && i0 < m0 && it < mt)
+      CIO<CM>::store(dst, rd[r] + (int64_t)i0 * d0 + (int64_t)it * dt, dd1, dd2,
+                     Num<V>::scale(c, Sb[(r * ct + it) * c0p + i0]), beta, ims);
   }
 }
 
-template <typename T>
-__device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, const PermGroup& g, const PermJob& job,
-                              PermShared& sh, T* __restrict__ S, double alpha, double beta) {
+template <int CM>
+__device__ void permute_tiled(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                              const PermGroup& g, const PermJob& job, PermShared& sh, typename CIO<CM>::V* __restrict__ S,
+                              double alpha, double beta, double ims) {
   // One source / destination member (abelian groups). Leg 0 = dst-fastest, leg t = dst leg 1.
   // A tile holds chunk c0 of leg 0 x chunk ct of leg t x R consecutive "rest" indices (all other
   // legs). Loads walk the tile in source-stride order (coalesced reads) as cp.async straight into
@@ -253,6 +300,7 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
   const int64_t so = sh.moff[0], sl = sh.mld[0], dof = sh.moff[kMaxGroupMembers], dl = sh.mld[kMaxGroupMembers];
   const int64_t s0 = g.sa[0] + sl * g.sb[0], st = g.sa[t] + sl * g.sb[t];
   const int64_t d0 = g.da[0] + dl * g.db[0], dt = g.da[t] + dl * g.db[t];
+  const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
   const double c = alpha * sh.coef[0];
   const int lorder = g.lorder;
   const int half = kTileElems / 2;  // two tile buffers
@@ -294,15 +342,15 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
     int i0b, itb, nr, m0, mt;
     int64_t rb;
     tile_geom(u, i0b, itb, nr, m0, mt, rb);
-    T* Sb = S + b * half;
+    typename CIO<CM>::V* Sb = S + b * half;
     const int64_t* rs = sh.rsa + b * (kMaxRows / 2);
     switch (lorder) {
-      case 0 + 3 * 1 + 9 * 2: tile_load<T, 0, 1, 2>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
-      case 0 + 3 * 2 + 9 * 1: tile_load<T, 0, 2, 1>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
-      case 1 + 3 * 0 + 9 * 2: tile_load<T, 1, 0, 2>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
-      case 1 + 3 * 2 + 9 * 0: tile_load<T, 1, 2, 0>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
-      case 2 + 3 * 0 + 9 * 1: tile_load<T, 2, 0, 1>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
-      default: tile_load<T, 2, 1, 0>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st); break;
+      case 0 + 3 * 1 + 9 * 2: tile_load<CM, 0, 1, 2>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st, sd1); break;
+      case 0 + 3 * 2 + 9 * 1: tile_load<CM, 0, 2, 1>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st, sd1); break;
+      case 1 + 3 * 0 + 9 * 2: tile_load<CM, 1, 0, 2>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st, sd1); break;
+      case 1 + 3 * 2 + 9 * 0: tile_load<CM, 1, 2, 0>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st, sd1); break;
+      case 2 + 3 * 0 + 9 * 1: tile_load<CM, 2, 0, 1>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st, sd1); break;
+      default: tile_load<CM, 2, 1, 0>(src, Sb, rs, c0, ct, R, c0p, nr, m0, mt, s0, st, sd1); break;
     }
     cp_async_commit();
   };
@@ -324,103 +372,122 @@ __device__ void permute_tiled(const T* __restrict__ src, T* __restrict__ dst, co
     int i0b, itb, nr, m0, mt;
     int64_t rb;
     tile_geom(u, i0b, itb, nr, m0, mt, rb);
-    tile_store<T>(dst, S + b * half, sh.rda + b * (kMaxRows / 2), c0, ct, R, c0p, nr, m0, mt, d0, dt, c, beta);
+    tile_store<CM>(dst, S + b * half, sh.rda + b * (kMaxRows / 2), c0, ct, R, c0p, nr, m0, mt, d0, dt, dd1, dd2, c,
+                   beta, ims);
     __syncthreads();  // buffer b and its tables are reused by tile u+2
   }
 }
 
-template <typename T>
 __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMember* __restrict__ members,
                                                 const double* __restrict__ coefs, PermShared& sh) {
   const int tid = threadIdx.x;
   if (tid < g.ksrc * g.kdst) sh.coef[tid] = coefs[g.coef_off + tid];
   if (tid < g.ksrc) {
-    sh.moff[tid] = members[g.src_mem + tid].off;
-    sh.mld[tid] = members[g.src_mem + tid].ld;
+    const PermMember m = members[g.src_mem + tid];
+    sh.moff[tid] = m.off;
+    sh.mld[tid] = m.ld;
+    sh.md1[tid] = m.d1;
+    sh.md2[tid] = m.d2;
   }
   if (tid < g.kdst) {
-    sh.moff[kMaxGroupMembers + tid] = members[g.dst_mem + tid].off;
-    sh.mld[kMaxGroupMembers + tid] = members[g.dst_mem + tid].ld;
+    const PermMember m = members[g.dst_mem + tid];
+    sh.moff[kMaxGroupMembers + tid] = m.off;
+    sh.mld[kMaxGroupMembers + tid] = m.ld;
+    sh.md1[kMaxGroupMembers + tid] = m.d1;
+    sh.md2[kMaxGroupMembers + tid] = m.d2;
   }
   __syncthreads();
 }
 
 // rows jobs of single-member groups: <= 64 registers so that 4 CTAs (32 warps) share an SM
-template <typename T>
-__global__ void __launch_bounds__(kPermThreads, 4) permute_rows_kernel(const T* __restrict__ src, T* __restrict__ dst,
-                                                                       const PermGroup* __restrict__ groups,
-                                                                       const PermMember* __restrict__ members,
-                                                                       const double* __restrict__ coefs,
-                                                                       const PermJob* __restrict__ jobs, double alpha,
-                                                                       double beta) {
+template <int CM>
+__global__ void __launch_bounds__(kPermThreads, 4)
+    permute_rows_kernel(const void* __restrict__ src, void* __restrict__ dst, const PermGroup* __restrict__ groups,
+                        const PermMember* __restrict__ members, const double* __restrict__ coefs,
+                        const PermJob* __restrict__ jobs, double alpha, double beta, double ims) {
   __shared__ PermShared sh;
   const PermJob job = jobs[blockIdx.x];
   const PermGroup& g = groups[job.group];
-  load_job_header<T>(g, members, coefs, sh);
-  permute_rows<T, true>(src, dst, g, job, sh, alpha, beta);
+  load_job_header(g, members, coefs, sh);
+  permute_rows<CM, true>((const typename CIO<CM>::S*)src, (typename CIO<CM>::D*)dst, g, job, sh, alpha, beta, ims);
 }
 
 // rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight)
-template <typename T>
-__global__ void __launch_bounds__(kPermThreads, 2) permute_recouple_kernel(
-    const T* __restrict__ src, T* __restrict__ dst, const PermGroup* __restrict__ groups,
-    const PermMember* __restrict__ members, const double* __restrict__ coefs, const PermJob* __restrict__ jobs,
-    double alpha, double beta) {
+template <int CM>
+__global__ void __launch_bounds__(kPermThreads, 2)
+    permute_recouple_kernel(const void* __restrict__ src, void* __restrict__ dst, const PermGroup* __restrict__ groups,
+                            const PermMember* __restrict__ members, const double* __restrict__ coefs,
+                            const PermJob* __restrict__ jobs, double alpha, double beta, double ims) {
   __shared__ PermShared sh;
   const PermJob job = jobs[blockIdx.x];
   const PermGroup& g = groups[job.group];
-  load_job_header<T>(g, members, coefs, sh);
-  permute_rows<T, false>(src, dst, g, job, sh, alpha, beta);
+  load_job_header(g, members, coefs, sh);
+  permute_rows<CM, false>((const typename CIO<CM>::S*)src, (typename CIO<CM>::D*)dst, g, job, sh, alpha, beta, ims);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kPermThreads, 4) permute_tiled_kernel(const T* __restrict__ src, T* __restrict__ dst,
-                                                                        const PermGroup* __restrict__ groups,
-                                                                        const PermMember* __restrict__ members,
-                                                                        const double* __restrict__ coefs,
-                                                                        const PermJob* __restrict__ jobs, double alpha,
-                                                                        double beta) {
+template <int CM>
+__global__ void __launch_bounds__(kPermThreads, 4)
+    permute_tiled_kernel(const void* __restrict__ src, void* __restrict__ dst, const PermGroup* __restrict__ groups,
+                         const PermMember* __restrict__ members, const double* __restrict__ coefs,
+                         const PermJob* __restrict__ jobs, double alpha, double beta, double ims) {
   __shared__ PermShared sh;
   extern __shared__ __align__(16) unsigned char perm_dyn[];
-  T* S = reinterpret_cast<T*>(perm_dyn);
   const PermJob job = jobs[blockIdx.x];
   const PermGroup& g = groups[job.group];
-  load_job_header<T>(g, members, coefs, sh);
-  permute_tiled<T>(src, dst, g, job, sh, S, alpha, beta);
+  load_job_header(g, members, coefs, sh);
+  permute_tiled<CM>((const typename CIO<CM>::S*)src, (typename CIO<CM>::D*)dst, g, job, sh,
+                    reinterpret_cast<typename CIO<CM>::V*>(perm_dyn), alpha, beta, ims);
 }
 
-cudaError_t launch_permute(const double* src, double* dst, const PermGroup* groups, const PermMember* members,
-                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi, int njobs_tiled,
-                           double alpha, double beta, int complex_, cudaStream_t st) {
-  // job table layout: [rows (single member) | rows (recoupling groups) | tiled]
+template <int CM>
+static void launch_permute_cm(const void* src, void* dst, const PermGroup* groups, const PermMember* members,
+                              const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi,
+                              int njobs_tiled, double alpha, double beta, double ims, cudaStream_t st) {
+  constexpr int smem = kTileElems * (int)sizeof(typename CIO<CM>::V);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(permute_tiled_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kTileElems * sizeof(double2)));
+    cudaFuncSetAttribute(permute_tiled_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
+  // job table layout: [rows (single member) | rows (recoupling groups) | tiled]
   const PermJob* mj = jobs + njobs_rows;
   const PermJob* tj = jobs + njobs_rows + njobs_multi;
-  if (complex_) {
-    const double2* s2 = (const double2*)src;
-    double2* d2 = (double2*)dst;
-    if (njobs_rows)
-      permute_rows_kernel<double2><<<njobs_rows, kPermThreads, 0, st>>>(s2, d2, groups, members, coefs, jobs, alpha, beta);
-    if (njobs_multi)
-      permute_recouple_kernel<double2><<<njobs_multi, kPermThreads, 0, st>>>(s2, d2, groups, members, coefs, mj, alpha,
-                                                                             beta);
-    if (njobs_tiled)
-      permute_tiled_kernel<double2><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double2), st>>>(
-          s2, d2, groups, members, coefs, tj, alpha, beta);
-  } else {
-    if (njobs_rows)
-      permute_rows_kernel<double><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta);
-    if (njobs_multi)
-      permute_recouple_kernel<double><<<njobs_multi, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, mj, alpha,
-                                                                            beta);
-    if (njobs_tiled)
-      permute_tiled_kernel<double><<<njobs_tiled, kPermThreads, kTileElems * sizeof(double), st>>>(
-          src, dst, groups, members, coefs, tj, alpha, beta);
+  if (njobs_rows)
+    permute_rows_kernel<CM><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta, ims);
+  if (njobs_multi)
+    permute_recouple_kernel<CM><<<njobs_multi, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, mj, alpha, beta,
+                                                                      ims);
+  if (njobs_tiled)
+    permute_tiled_kernel<CM><<<njobs_tiled, kPermThreads, smem, st>>>(src, dst, groups, members, coefs, tj, alpha, beta,
+                                                                      ims);
+}
+
+cudaError_t launch_permute(const void* src, void* dst, const PermGroup* groups, const PermMember* members,
+                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi, int njobs_tiled,
+                           double alpha, double beta, int cm, double ims, cudaStream_t st) {
+  switch (cm) {
+    case kPermReal:
+      launch_permute_cm<kPermReal>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled, alpha,
+                                   beta, ims, st);
+      break;
+    case kPermCToC:
+      launch_permute_cm<kPermCToC>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled, alpha,
+                                   beta, ims, st);
+      break;
+    case kPermCToPlanar:
+      launch_permute_cm<kPermCToPlanar>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled,
+                                        alpha, beta, ims, st);
+      break;
+    case kPermCToRealRep:
+      launch_permute_cm<kPermCToRealRep>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled,
+                                         alpha, beta, ims, st);
+      break;
+    case kPermPlanarToC:
+      launch_permute_cm<kPermPlanarToC>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled,
+                                        alpha, beta, ims, st);
+      break;
+    default:
+      return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

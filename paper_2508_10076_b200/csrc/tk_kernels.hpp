@@ -37,6 +37,21 @@ struct PermGroup {
 struct PermMember {
   int64_t off;  // element offset of the subblock's element (0,...,0)
   int64_t ld;   // rows of its block
+  int64_t d1;   // planar complex: offset of the imaginary part relative to the real part (doubles)
+  int64_t d2;   // real representation of B~: offset of the [-im, re] row half (doubles)
+};
+
+// Complex modes of a permute launch. ComplexF64 contractions run as ONE real GEMM over the real
+// representation of the complex blocks (north_star: "ComplexF64 via real GEMMs"; reading C21: 4 real
+// products, no 3M): A~ is planar [Ar | Ai] (M x 2K), B~ is [[Br, Bi], [-Bi, Br]] (2K x 2N), so that
+// A~ B~ = [Ar Br - Ai Bi | Ar Bi + Ai Br] = [Cr | Ci] = C~ (M x 2N). The permute kernels do the
+// (de)interleaving in flight while they permute.
+enum PermCM : int {
+  kPermReal = 0,         // Float64 -> Float64
+  kPermCToC = 1,         // interleaved ComplexF64 -> interleaved (tk_permute)
+  kPermCToPlanar = 2,    // interleaved -> planar re | im (+d1)          (A~)
+  kPermCToRealRep = 3,   // interleaved -> [[re, im], [-im, re]]          (B~)
+  kPermPlanarToC = 4     // planar (+d1) -> interleaved                   (C~ -> C)
 };
 
 // A CTA work item: `count` work units of group `group` starting at unit `first`.
@@ -64,9 +79,11 @@ struct GemmTile {
 };
 
 // launchers (tk_kernels.cu)
-cudaError_t launch_permute(const double* src, double* dst, const PermGroup* groups, const PermMember* members,
+// ims = -1 conjugates the source (tk_contract conjA / conjB; modes 2 and 3 only). Modes 2 and 3
+// write workspace only and require beta == 0.
+cudaError_t launch_permute(const void* src, void* dst, const PermGroup* groups, const PermMember* members,
                            const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi,
-                           int njobs_tiled, double alpha, double beta, int complex_, cudaStream_t st);
+                           int njobs_tiled, double alpha, double beta, int cm, double ims, cudaStream_t st);
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st);
 

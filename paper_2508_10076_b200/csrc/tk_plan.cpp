@@ -235,30 +235,42 @@ static void make_jobs(PermPlan& P) {
 // Internal (workspace) layout of A~, B~, C~: same blocks and subblock order as the canonical
 // layout, but every block's leading dimension is padded to a multiple of 4 doubles and every block
 // starts 32-byte aligned, so the GEMM can use 16-byte cp.async and columns start on sector bounds.
+// ComplexF64 blocks are stored as their real representation (PermCM in tk_kernels.hpp):
+// planar   (A~, C~): rows x 2cols, [re | im], imaginary part d1 = cols * ld doubles after the real part;
+// real rep (B~):     2rows x 2cols, [[re, im], [-im, re]], d1 = cols * ld, d2 = rows.
+enum class PadKind { Real, Planar, RealRep };
 struct PadLayout {
-  std::vector<int64_t> off, ld;
-  int64_t total = 0;
+  PadKind kind = PadKind::Real;
+  std::vector<int64_t> off, ld, d1, d2;  // in doubles
+  int64_t total = 0;                     // doubles
 };
 
-static PadLayout pad_layout(const Tensor& t) {
+static PadLayout pad_layout(const Tensor& t, PadKind kind = PadKind::Real) {
   PadLayout pl;
+  pl.kind = kind;
   int64_t o = 0;
   for (const Block& b : t.blocks) {
-    int64_t ld = (b.rows + 3) & ~int64_t(3);
+    int64_t r = kind == PadKind::RealRep ? 2 * b.rows : b.rows;
+    int64_t c = kind == PadKind::Real ? b.cols : 2 * b.cols;
+    int64_t ld = (r + 3) & ~int64_t(3);
     pl.off.push_back(o);
     pl.ld.push_back(ld);
-    o += ld * b.cols;
+    pl.d1.push_back(kind == PadKind::Real ? 0 : b.cols * ld);
+    pl.d2.push_back(kind == PadKind::RealRep ? b.rows : 0);
+    o += ld * c;
   }
   pl.total = o;
   return pl;
 }
 
-static int64_t sub_off(const Tensor& t, const PadLayout* pl, int i) {
-  if (!pl) return t.subs[i].off;
+// permute-table member of subblock i: canonical layout (pl == nullptr; offsets in elements of the
+// tensor's dtype) or a workspace layout (offsets in doubles)
+static PermMember sub_member(const Tensor& t, const PadLayout* pl, int i) {
   const Subblock& sb = t.subs[i];
-  return pl->off[sb.block] + sb.row_off + pl->ld[sb.block] * sb.col_off;
+  if (!pl) return PermMember{sb.off, t.ld(i), 0, 0};
+  int b = sb.block;
+  return PermMember{pl->off[b] + sb.row_off + pl->ld[b] * sb.col_off, pl->ld[b], pl->d1[b], pl->d2[b]};
 }
-static int64_t sub_ld(const Tensor& t, const PadLayout* pl, int i) { return pl ? pl->ld[t.subs[i].block] : t.ld(i); }
 
 static bool is_identity_perm(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
   if ((int)p.size() != A.n_cod()) return false;
@@ -313,9 +325,9 @@ static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const st
       g.coef_off = (int)P.coefs.size();
       P.coefs.push_back((double)koszul_sign(k, lab, n1, p, q));
       g.src_mem = (int)P.members.size();
-      P.members.push_back(PermMember{sub_off(A, spl, i), sub_ld(A, spl, i)});
+      P.members.push_back(sub_member(A, spl, i));
       g.dst_mem = (int)P.members.size();
-      P.members.push_back(PermMember{sub_off(C, dpl, j), sub_ld(C, dpl, j)});
+      P.members.push_back(sub_member(C, dpl, j));
       finish_group_geometry(g, ext, n1, src_leg, C.n_cod());
       P.groups.push_back(g);
     }
@@ -381,10 +393,10 @@ static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const st
         for (auto& e : rows[a]) M[a * g.kdst + e.first] += e.second;
       P.coefs.insert(P.coefs.end(), M.begin(), M.end());
       g.src_mem = (int)P.members.size();
-      for (int i : srcs) P.members.push_back(PermMember{sub_off(A, spl, i), sub_ld(A, spl, i)});
+      for (int i : srcs) P.members.push_back(sub_member(A, spl, i));
       g.dst_mem = (int)P.members.size();
       for (int j : dsts) {
-        P.members.push_back(PermMember{sub_off(C, dpl, j), sub_ld(C, dpl, j)});
+        P.members.push_back(sub_member(C, dpl, j));
         dst_done[j] = 1;
       }
       const Tree& s0 = A.s_tree(srcs[0]);
@@ -432,6 +444,7 @@ struct ContractPlan {
   std::vector<GemmGroup> ggroups;
   std::vector<GemmTile> tiles;
   int ntiles_big = 0, ntiles_small = 0;
+  bool cplx = false;  // ComplexF64: workspace in the real representation (PermCM), one real GEMM
   DevBuf d_ggroups, d_tiles;
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
@@ -554,8 +567,8 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
                                 const Tensor& C, const int32_t* labC, ContractPlan& P) {
   if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
-  if (A.dtype != TK_F64 || B.dtype != TK_F64 || C.dtype != TK_F64)
-    TK_THROW(TK_ERR_UNSUPPORTED, "tk_contract: only Float64 in this build");
+  if (A.dtype != B.dtype || A.dtype != C.dtype) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_contract: dtypes differ");
+  P.cplx = A.dtype == TK_C64;
   Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
   choose_contracted_order(A, B, t);
   P.At = permuted_tensor(A, t.pA, t.qA, A.dtype);
@@ -565,17 +578,22 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     P.Ct = make_tensor(C.dtype, cod, dom);
   }
   check_target(*P.Ct, t.pAB, t.qAB, C);
-  bool ia_id = is_identity_perm(A, t.pA, t.qA), ib_id = is_identity_perm(B, t.pB, t.qB);
-  bool ic_id = is_identity_perm(*P.Ct, t.pAB, t.qAB);
-  P.la = pad_layout(*P.At);
-  P.lb = pad_layout(*P.Bt);
-  P.lc = pad_layout(*P.Ct);
+  // ComplexF64 always passes through the workspace (the permutes also change the representation)
+  bool ia_id = !P.cplx && is_identity_perm(A, t.pA, t.qA), ib_id = !P.cplx && is_identity_perm(B, t.pB, t.qB);
+  bool ic_id = !P.cplx && is_identity_perm(*P.Ct, t.pAB, t.qAB);
+  P.la = pad_layout(*P.At, P.cplx ? PadKind::Planar : PadKind::Real);
+  P.lb = pad_layout(*P.Bt, P.cplx ? PadKind::RealRep : PadKind::Real);
+  P.lc = pad_layout(*P.Ct, P.cplx ? PadKind::Planar : PadKind::Real);
   const PadLayout* pla = ia_id ? nullptr : &P.la;
   const PadLayout* plb = ib_id ? nullptr : &P.lb;
   const PadLayout* plc = ic_id ? nullptr : &P.lc;
-  build_perm_plan(A, t.pA, t.qA, *P.At, P.pa, 8, nullptr, pla);
-  build_perm_plan(B, t.pB, t.qB, *P.Bt, P.pb, 8, nullptr, plb);
-  build_perm_plan(*P.Ct, t.pAB, t.qAB, C, P.pc, 8, plc, nullptr);
+  const int eb = P.cplx ? 16 : 8;
+  build_perm_plan(A, t.pA, t.qA, *P.At, P.pa, eb, nullptr, pla);
+  build_perm_plan(B, t.pB, t.qB, *P.Bt, P.pb, eb, nullptr, plb);
+  build_perm_plan(*P.Ct, t.pAB, t.qAB, C, P.pc, eb, plc, nullptr);
+  P.pa.identity = ia_id;
+  P.pb.identity = ib_id;
+  P.pc.identity = ic_id;
   // workspace: A~ | B~ | C~ (skipped when the permute is the identity)
   size_t off = 0;
   if (!P.pa.identity) {
@@ -591,7 +609,10 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     off = align256(off + (size_t)P.lc.total * 8);
   }
   P.ws_bytes = off;
-  // Alg. 8: one GEMM per coupled sector of C~; K = 0 blocks are zero-filled
+  // Alg. 8: one GEMM per coupled sector of C~; K = 0 blocks are zero-filled.
+  // ComplexF64: the real GEMM of the real representation, M x 2K times 2K x 2N (= 8MKN real flops,
+  // the useful complex flop count of reading C21).
+  const int cm = P.cplx ? 2 : 1;
   std::map<Sector, int> a_blk, b_blk;
   for (int i = 0; i < (int)P.At->blocks.size(); ++i) a_blk[P.At->blocks[i].coupled] = i;
   for (int i = 0; i < (int)P.Bt->blocks.size(); ++i) b_blk[P.Bt->blocks[i].coupled] = i;
@@ -600,7 +621,7 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     const Block& cb = P.Ct->blocks[ci];
     GemmGroup g{};
     g.M = (int32_t)cb.rows;
-    g.N = (int32_t)cb.cols;
+    g.N = (int32_t)(cm * cb.cols);
     g.c_off = plc ? plc->off[ci] : cb.off;
     g.ldc = (int32_t)(plc ? plc->ld[ci] : cb.rows);
     auto ia = a_blk.find(cb.coupled);
@@ -610,7 +631,7 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
       const Block& bb = P.Bt->blocks[ib->second];
       if (ab.rows != cb.rows || bb.cols != cb.cols || ab.cols != bb.rows)
         TK_THROW(TK_ERR_SPACE_MISMATCH, "internal: block shapes of A~, B~, C~ disagree");
-      g.K = (int32_t)ab.cols;
+      g.K = (int32_t)(cm * ab.cols);
       g.a_off = pla ? pla->off[ia->second] : ab.off;
       g.b_off = plb ? plb->off[ib->second] : bb.off;
       g.lda = (int32_t)(pla ? pla->ld[ia->second] : ab.rows);
@@ -717,13 +738,13 @@ static void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) TK_THROW(TK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-static void run_permute(PermPlan& P, const double* src, double* dst, double alpha, double beta, bool cplx,
+static void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double beta, int cm, double ims,
                         cudaStream_t st) {
   P.upload();
   if (P.jobs.empty()) return;
   check_cuda(launch_permute(src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p,
                             (const double*)P.d_coefs.p, (const PermJob*)P.d_jobs.p, P.njobs_rows, P.njobs_multi, P.njobs_tiled,
-                            alpha, beta, cplx ? 1 : 0, st),
+                            alpha, beta, cm, ims, st),
              "permute launch");
   ++g_launches;
 }
@@ -769,7 +790,7 @@ tk_status tk_permute(const tk_tensor* A_, const void* a, const int32_t* p, int32
   std::vector<int> pv(p, p + np), qv(q, q + nq);
   PermPlan* P = get_perm_plan(A, pv, qv, C);
   g_launches = 0;
-  run_permute(*P, (const double*)a, (double*)c, alpha, beta, A.dtype == TK_C64, (cudaStream_t)stream);
+  run_permute(*P, a, c, alpha, beta, A.dtype == TK_C64 ? kPermCToC : kPermReal, 1.0, (cudaStream_t)stream);
   TK_API_END
 }
 
@@ -845,9 +866,12 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
   double* Ct = P->pc.identity ? (double*)c : (double*)(w + P->off_c);
   g_launches = 0;
   prof_record(0, st);
-  if (!P->pa.identity) run_permute(P->pa, (const double*)a, (double*)At, 1.0, 0.0, false, st);
+  const bool cx = P->cplx;
+  if (!P->pa.identity)
+    run_permute(P->pa, a, (double*)At, 1.0, 0.0, cx ? kPermCToPlanar : kPermReal, conjA ? -1.0 : 1.0, st);
   prof_record(1, st);
-  if (!P->pb.identity) run_permute(P->pb, (const double*)b, (double*)Bt, 1.0, 0.0, false, st);
+  if (!P->pb.identity)
+    run_permute(P->pb, b, (double*)Bt, 1.0, 0.0, cx ? kPermCToRealRep : kPermReal, conjB ? -1.0 : 1.0, st);
   prof_record(2, st);
   double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
   if (!P->tiles.empty()) {
@@ -857,7 +881,7 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
     ++g_launches;
   }
   prof_record(3, st);
-  if (!P->pc.identity) run_permute(P->pc, Ct, (double*)c, alpha, beta, false, st);
+  if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
   prof_record(4, st);
   if (g_prof.on) {
     g_prof.have = true;

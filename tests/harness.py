@@ -23,17 +23,23 @@ def oracle_flat(layout, cfg, tidx, complex_=False):
     return flat
 
 
-def oracle_chain_dense(cfg):
-    """Tier 1: dense results of every step of a config. Returns {name: (layout, dense)}."""
+def oracle_chain_dense(cfg, complex_=False, conj=None):
+    """Tier 1: dense results of every step of a config. Returns {name: (layout, dense)}.
+
+    complex_: ComplexF64 inputs; conj: {step index: (conjA, conjB)} -- elementwise complex
+    conjugation of that step's operands (tk_contract's conjA / conjB)."""
     kind = cfg["kind"]
     T = {}
     for name, (spec, idx) in cfg["tensors"].items():
         lt = OL.homspace_layout(kind, spec["cod"], spec["dom"])
-        T[name] = (spec["cod"], spec["dom"], lt, OD.to_dense(lt, oracle_flat(lt, cfg["cfg"], idx)))
+        T[name] = (spec["cod"], spec["dom"], lt, OD.to_dense(lt, oracle_flat(lt, cfg["cfg"], idx, complex_)))
     out = {}
-    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+    for si, (na, la, nb, lb, nc, lc, ncod) in enumerate(cfg["steps"]):
         Ac, Ad, _, A = T[na]
         Bc, Bd, _, B = T[nb]
+        ca, cb = (conj or {}).get(si, (False, False))
+        A = np.conj(A) if ca else A
+        B = np.conj(B) if cb else B
         D = OC.contract(kind, A, Ac + Ad, len(Ac), la, B, Bc + Bd, len(Bc), lb, lc, ncod)
         cod, dom = OC.output_spaces(Ac, Ad, Bc, Bd, la, lb, lc, ncod)
         lt = OL.homspace_layout(kind, cod, dom)
@@ -45,13 +51,13 @@ def oracle_chain_dense(cfg):
 LazyBlocks = BS.LazyBlocks
 
 
-def oracle_chain_blocks(cfg, out_keys_last=None):
+def oracle_chain_blocks(cfg, out_keys_last=None, complex_=False):
     """Tier 2 (abelian): charge-tuple einsum through the chain. Returns {name: (layout, blocks)}."""
     kind = cfg["kind"]
     T = {}
     for name, (spec, idx) in cfg["tensors"].items():
         lt = OL.homspace_layout(kind, spec["cod"], spec["dom"])
-        T[name] = (spec["cod"], spec["dom"], LazyBlocks(lt, cfg["cfg"], idx))
+        T[name] = (spec["cod"], spec["dom"], LazyBlocks(lt, cfg["cfg"], idx, complex_))
     out = {}
     steps = cfg["steps"]
     for si, (na, la, nb, lb, nc, lc, ncod) in enumerate(steps):
@@ -69,28 +75,31 @@ def flat_blocks(layout, flat):
 
 
 # ------------------------------------------------------------------ CUDA side
-def gpu_chain(cfg, alpha=1.0, beta=0.0, c_init=None, keep=True):
+def gpu_chain(cfg, alpha=1.0, beta=0.0, c_init=None, keep=True, complex_=False, conj=None):
     """Run every step of cfg through tk_contract. Returns {name: (tk.Tensor, host flat)}."""
     import torch
     from paper_2508_10076_b200 import tk, layout_io
     dev = torch.device("cuda")
+    dt = torch.complex128 if complex_ else torch.float64
     T = {}
     for name, (spec, idx) in cfg["tensors"].items():
-        t = tk.tensor_from_spec(spec)
-        flat = layout_io.fill(t, cfg["cfg"], idx)
+        t = tk.tensor_from_spec(spec, tk.TK_C64 if complex_ else tk.TK_F64)
+        flat = layout_io.fill(t, cfg["cfg"], idx, complex_)
         T[name] = (t, torch.from_numpy(flat).to(dev))
     out = {}
-    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+    for si, (na, la, nb, lb, nc, lc, ncod) in enumerate(cfg["steps"]):
+        ca, cb = (conj or {}).get(si, (False, False))
         A, a = T[na]
         B, b = T[nb]
         C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
         if c_init is not None:
             c = torch.from_numpy(c_init(C)).to(dev)
         else:
-            c = torch.full((C.nelems,), float("nan"), dtype=torch.float64, device=dev)
+            c = torch.full((C.nelems,), float("nan"), dtype=dt, device=dev)
         ws_n = tk.tk_contract_workspace(A, la, B, lb, C, lc)
         ws = torch.empty(max(ws_n // 8 + 32, 1), dtype=torch.float64, device=dev)
-        tk.tk_contract(A, a, la, B, b, lb, C, c, lc, alpha=alpha, beta=beta, ws=ws, ws_bytes=ws.numel() * 8)
+        tk.tk_contract(A, a, la, B, b, lb, C, c, lc, alpha=alpha, beta=beta, ws=ws, ws_bytes=ws.numel() * 8,
+                       conjA=ca, conjB=cb)
         torch.cuda.synchronize()
         T[nc] = (C, c)
         out[nc] = (C, c.cpu().numpy() if keep else None)

@@ -33,8 +33,8 @@ def rel_err_blocks(layout, flat, blocks, keys=None):
         r = blocks.get(k)
         if r is None:
             r = np.zeros_like(g)
-        num += float(np.sum((g - r) ** 2))
-        den += float(np.sum(r ** 2))
+        num += float(np.sum(np.abs(g - r) ** 2))
+        den += float(np.sum(np.abs(r) ** 2))
     return math.sqrt(num / den) if den > 0 else math.sqrt(num)
 
 
@@ -95,6 +95,67 @@ def test_cfg4_full_size_sampled():
     keys = [tuple(lt.subblocks[i].key[0]) + tuple(lt.subblocks[i].key[3]) for i in idx]
     # oracle inputs restricted to what the sampled outputs need is done inside contract_blocks
     ref = H.oracle_chain_blocks(cfg, out_keys_last=keys)
+    _, blocks = ref["C"]
+    err = rel_err_blocks(lt, flat, blocks, keys=set(keys))
+    assert err <= TOL, f"rel Frobenius {err:.3e}"
+    assert not np.isnan(flat).any()
+
+
+# ------------------------------------------------------------------ ComplexF64 (cfg4 names it)
+@pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=24),
+                                    lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1))],
+                         ids=["cfg1", "cfg2", "cfg3_chi64", "cfg4_d24", "cfg5_small"])
+def test_chain_complex_dense_oracle(cfgfun):
+    """ComplexF64 through the real-representation GEMM (reading C21) against the dense oracle."""
+    cfg = cfgfun()
+    ref = H.oracle_chain_dense(cfg, complex_=True)
+    got = H.gpu_chain(cfg, complex_=True)
+    for name, (lt, D) in ref.items():
+        C, flat = got[name]
+        assert flat.dtype == np.complex128 and not np.isnan(flat).any(), name
+        err = rel_err_dense(lt, flat, D)
+        assert err <= TOL, f"{name}: rel Frobenius {err:.3e}"
+
+
+@pytest.mark.parametrize("ca,cb", [(True, False), (False, True), (True, True)])
+def test_complex_conj_flags(ca, cb):
+    cfg = W.cfg3(chi=48)
+    cfg["steps"] = cfg["steps"][:2]
+    conj = {0: (ca, cb), 1: (cb, ca)}
+    ref = H.oracle_chain_dense(cfg, complex_=True, conj=conj)
+    got = H.gpu_chain(cfg, complex_=True, conj=conj)
+    for name, (lt, D) in ref.items():
+        err = rel_err_dense(lt, got[name][1], D)
+        assert err <= TOL, f"{name}: rel Frobenius {err:.3e}"
+
+
+def test_complex_alpha_beta():
+    cfg = W.cfg4(d_leg=16)
+    ref = H.oracle_chain_dense(cfg, complex_=True)
+    rng = np.random.default_rng(5)
+    init = {}
+
+    def c_init(C):
+        x = rng.standard_normal(C.nelems) + 1j * rng.standard_normal(C.nelems)
+        init["x"] = x
+        return x
+
+    got = H.gpu_chain(cfg, alpha=0.5, beta=-1.25, c_init=c_init, complex_=True)
+    lt, D = ref["C"]
+    want = 0.5 * D - 1.25 * OD.to_dense(lt, init["x"])
+    assert rel_err_dense(lt, got["C"][1], want) <= TOL
+
+
+def test_cfg4_complex_bench_size_sampled():
+    """cfg4 ComplexF64 at its bench size (D_leg 320, reading C20): sampled output subblocks, tier 2."""
+    cfg = W.cfg4(d_leg=320)
+    got = H.gpu_chain(cfg, complex_=True)
+    C, flat = got["C"]
+    lt = OL.homspace_layout("U1", *_spaces(cfg))
+    rng = np.random.default_rng(1)
+    idx = rng.choice(len(lt.subblocks), size=16, replace=False)
+    keys = [tuple(lt.subblocks[i].key[0]) + tuple(lt.subblocks[i].key[3]) for i in idx]
+    ref = H.oracle_chain_blocks(cfg, out_keys_last=keys, complex_=True)
     _, blocks = ref["C"]
     err = rel_err_blocks(lt, flat, blocks, keys=set(keys))
     assert err <= TOL, f"rel Frobenius {err:.3e}"
