@@ -42,8 +42,12 @@ def load_peaks():
 
 def workload(args):
     from workloads import configs as W
-    cfg = W.cfg4(d_leg=args.d_leg)
+    cfg = W.cfg4(d_leg=args.d_leg, complex_=args.dtype == "c64")
     return cfg
+
+
+def dtype_name(args):
+    return "ComplexF64" if args.dtype == "c64" else "Float64"
 
 
 class ClockSampler:
@@ -97,8 +101,9 @@ def oracle_inputs(cfg):
     (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
     A, B = cfg["tensors"][na][0], cfg["tensors"][nb][0]
     kind = cfg["kind"]
-    return (BS.LazyBlocks(OL.homspace_layout(kind, A["cod"], A["dom"]), cfg["cfg"], cfg["tensors"][na][1]),
-            BS.LazyBlocks(OL.homspace_layout(kind, B["cod"], B["dom"]), cfg["cfg"], cfg["tensors"][nb][1]))
+    cx = cfg.get("dtype") == "c64"
+    return (BS.LazyBlocks(OL.homspace_layout(kind, A["cod"], A["dom"]), cfg["cfg"], cfg["tensors"][na][1], cx),
+            BS.LazyBlocks(OL.homspace_layout(kind, B["cod"], B["dom"]), cfg["cfg"], cfg["tensors"][nb][1], cx))
 
 
 def oracle_sample(cfg, budget_s, keys=None, seed=0, inputs=None):
@@ -134,7 +139,8 @@ def oracle_sample(cfg, budget_s, keys=None, seed=0, inputs=None):
             if dt >= budget_s or n >= len(all_keys):
                 break
             n = min(len(all_keys), max(n + 1, int(n * min(8.0, 1.2 * budget_s / max(dt, 1e-3)))))
-    return stats["flops"], time.perf_counter() - t0, used
+    # useful flops: 2MKN per real block product, 8MKN per complex one (reading C21)
+    return stats["flops"] * (4.0 if cfg.get("dtype") == "c64" else 1.0), time.perf_counter() - t0, used
 
 
 def run_reference(args):
@@ -154,14 +160,16 @@ def run_reference(args):
         fl += f
         tot += t
     value = fl / tot / 1e9
-    sample = (f"{len(keys)} of the C output subblocks of cfg4 (D_leg={args.d_leg}) per step, "
+    sample = (f"{len(keys)} of the C output subblocks of cfg4 ({dtype_name(args)}, D_leg={args.d_leg}) per step, "
               f"tier-2 charge-tuple einsum (oracle/blocksparse.py)")
     line = {
-        "impl": "reference", "metric": "useful block GFLOP/s of tk_contract (Float64)", "value": round(value, 4),
+        "impl": "reference", "metric": f"useful block GFLOP/s of tk_contract ({dtype_name(args)})",
+        "value": round(value, 4),
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * tot / args.steps, 2), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), workloads/gen.py)",
-        "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4, Float64, D_leg={args.d_leg}", "d_leg": args.d_leg},
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded N(0,1), workloads/gen.py)",
+        "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4 contraction, {dtype_name(args)}, D_leg={args.d_leg} "
+                               f"(reading C20)", "d_leg": args.d_leg},
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -186,16 +194,18 @@ def run_gpu(args):
 
     cfg = workload(args)
     (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
-    A = tk.tensor_from_spec(cfg["tensors"][na][0])
-    B = tk.tensor_from_spec(cfg["tensors"][nb][0])
+    cplx = args.dtype == "c64"
+    tdt, esz = (torch.complex128, 16) if cplx else (torch.float64, 8)
+    A = tk.tensor_from_spec(cfg["tensors"][na][0], tk.TK_C64 if cplx else tk.TK_F64)
+    B = tk.tensor_from_spec(cfg["tensors"][nb][0], tk.TK_C64 if cplx else tk.TK_F64)
     C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
     t0 = time.time()
-    a_h = torch.from_numpy(layout_io.fill(A, cfg["cfg"], cfg["tensors"][na][1]))
-    b_h = torch.from_numpy(layout_io.fill(B, cfg["cfg"], cfg["tensors"][nb][1]))
+    a_h = torch.from_numpy(layout_io.fill(A, cfg["cfg"], cfg["tensors"][na][1], cplx))
+    b_h = torch.from_numpy(layout_io.fill(B, cfg["cfg"], cfg["tensors"][nb][1], cplx))
     t_fill = time.time() - t0
     a = a_h.to(dev)
     b = b_h.to(dev)
-    c = torch.empty(C.nelems, dtype=torch.float64, device=dev)
+    c = torch.empty(C.nelems, dtype=tdt, device=dev)
     t0 = time.perf_counter()
     ws_n = tk.tk_contract_workspace(A, la, B, lb, C, lc)   # builds + caches the plan (cold)
     t_plan_cold = time.perf_counter() - t0
@@ -252,7 +262,7 @@ def run_gpu(args):
     if args.e2e_steps > 0:
         a_p = a_h.pin_memory()
         b_p = b_h.pin_memory()
-        c_p = torch.empty(C.nelems, dtype=torch.float64).pin_memory()
+        c_p = torch.empty(C.nelems, dtype=tdt).pin_memory()
         x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         x0.record(stream)
@@ -269,7 +279,7 @@ def run_gpu(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": round(world * flops * args.e2e_steps / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int((A.nelems + B.nelems) * 8), "d2h_bytes_per_step": int(C.nelems * 8),
+               "h2d_bytes_per_step": int((A.nelems + B.nelems) * esz), "d2h_bytes_per_step": int(C.nelems * esz),
                "ms_per_step": round(e2e_ms / args.e2e_steps, 2)}
 
     peaks = load_peaks()
@@ -293,7 +303,7 @@ def run_gpu(args):
             traffic = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not cplx:
         inputs = oracle_inputs(cfg)
         _, _, keys = oracle_sample(cfg, budget_s=args.cpu_budget_s / 2, inputs=inputs)   # calibrate + generate
         fl_s, t_s, _ = oracle_sample(cfg, 0, keys=keys, inputs=inputs)
@@ -303,13 +313,14 @@ def run_gpu(args):
                          f"einsum (oracle/blocksparse.py), {fl_s:.3e} useful flops in {t_s:.1f} s"}
 
     line = {
-        "metric": "useful block GFLOP/s of tk_contract (Float64)",
+        "metric": f"useful block GFLOP/s of tk_contract ({dtype_name(args)})",
         "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded N(0,1) per subblock, workloads/gen.py)",
-        "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4 contraction, Float64, D_leg={args.d_leg} "
+        "dtype": args.dtype, "data": "synthetic (seeded N(0,1) per subblock, workloads/gen.py)",
+        "config": {"workload": f"cfg4 U(1) PEPS rank-4 x rank-4 contraction, {dtype_name(args)}, D_leg={args.d_leg} "
                                f"(reading C20)", "d_leg": args.d_leg, "parallelism": "replicas only",
-                   "useful_flops_per_step": flops, "l2": "inputs (8.9 GB/operand) >> 126 MB L2, no flush needed"},
+                   "useful_flops_per_step": flops,
+                   "l2": f"inputs ({A.nelems * esz / 1e9:.1f} GB/operand) >> 126 MB L2, no flush needed"},
         "roofline": {"bound": "tensor", "kernel": "gemm_mbar_kernel<2> + gemm_small_kernel (grouped DMMA GEMM, one launch per tile class)",
                      "achieved": round(gemm_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(gemm_tf / FP64_PEAK_TFLOPS, 4),
@@ -341,12 +352,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--d-leg", type=int, default=384)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "c64"],
+                    help="f64: the BASELINE metric (D_leg 384); c64: cfg4's ComplexF64 variant (D_leg 320)")
+    ap.add_argument("--d-leg", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-budget-s", type=float, default=24.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.d_leg is None:
+        args.d_leg = 320 if args.dtype == "c64" else 384
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

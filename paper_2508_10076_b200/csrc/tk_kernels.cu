@@ -60,6 +60,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Programmatic dependent launch (sm_90+): every kernel lets the next kernel in the stream start its
+// launch early (launch_dependents) and reads/writes tensor data only after griddepcontrol.wait, which
+// returns once the preceding grid has completed and its writes are visible. Descriptor tables (plan
+// constants) are read before the wait, so job/group decoding overlaps the previous kernel's tail.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 constexpr int kPermThreads = 256;
 constexpr int kMaxRows = 256;
 
@@ -115,14 +122,15 @@ __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typena
   const int ks = g.ksrc, kd = g.kdst;
   const int64_t sl = sh.mld[0], dl = sh.mld[kMaxGroupMembers];
   for (int r = tid; r < cnt; r += kPermThreads) {
-    int64_t R = job.first + r;
+    uint32_t R = (uint32_t)(job.first + r);  // group element counts are < 2^31 (host-checked)
     int64_t sa = 0, sb = 0, da = 0, db = 0;
 #pragma unroll 1
     for (int l = 1; l < kMaxLegs; ++l) {
       if (l < g.ndim) {
-        int64_t e = g.ext[l];
-        int64_t i = R % e;
-        R /= e;
+        const uint32_t e = (uint32_t)g.ext[l];
+        const uint32_t q = R / e;
+        const int64_t i = R - q * e;
+        R = q;
         sa += i * g.sa[l];
         sb += i * g.sb[l];
         da += i * g.da[l];
@@ -140,6 +148,7 @@ __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typena
     }
   }
   __syncthreads();
+  pdl_wait();
   const int n0 = g.ext[0];
   if constexpr (SINGLE) {
     const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
@@ -324,13 +333,14 @@ __device__ void permute_tiled(const typename CIO<CM>::S* __restrict__ src, typen
     int64_t* rs = sh.rsa + b * (kMaxRows / 2);
     int64_t* rd = sh.rda + b * (kMaxRows / 2);
     for (int r = tid; r < nr; r += kPermThreads) {
-      int64_t Rr = rb + r;
+      uint32_t Rr = (uint32_t)(rb + r);
       int64_t sbase = so, dbase = dof;
       for (int l = 1; l < g.ndim; ++l) {
         if (l == t) continue;
-        int64_t e = g.ext[l];
-        int64_t i = Rr % e;
-        Rr /= e;
+        const uint32_t e = (uint32_t)g.ext[l];
+        const uint32_t q = Rr / e;
+        const int64_t i = Rr - q * e;
+        Rr = q;
         sbase += i * (g.sa[l] + sl * g.sb[l]);
         dbase += i * (g.da[l] + dl * g.db[l]);
       }
@@ -357,6 +367,7 @@ __device__ void permute_tiled(const typename CIO<CM>::S* __restrict__ src, typen
 
   tables(0, 0);
   __syncthreads();
+  pdl_wait();
   issue_loads(0, 0);
   for (int u = 0; u < job.count; ++u) {
     const int b = u & 1;
@@ -399,95 +410,227 @@ __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMe
   __syncthreads();
 }
 
-// rows jobs of single-member groups: <= 64 registers so that 4 CTAs (32 warps) share an SM
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute (PDL); TK_NO_PDL=1 disables it
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool pdl = getenv("TK_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// packed jobs of small single-member rows groups (see kPackGroups): per CTA, the groups' row tables
+// are built once into shared memory, then all elements of the job are walked as one flat range with
+// 64 bytes of loads in flight per thread; each thread advances its group index monotonically.
+struct PackShared {
+  int64_t rs[kPackRows], rd[kPackRows];
+  int64_t s0[kPackGroups], d0[kPackGroups], sd1[kPackGroups], dd1[kPackGroups], dd2[kPackGroups];
+  double c[kPackGroups];
+  uint32_t fm[kPackGroups], fs[kPackGroups], n0[kPackGroups];
+  int32_t rstart[kPackGroups + 1], estart[kPackGroups + 1];
+};
+
 template <int CM>
-__global__ void __launch_bounds__(kPermThreads, 4)
-    permute_rows_kernel(const void* __restrict__ src, void* __restrict__ dst, const PermGroup* __restrict__ groups,
-                        const PermMember* __restrict__ members, const double* __restrict__ coefs,
-                        const PermJob* __restrict__ jobs, double alpha, double beta, double ims) {
-  __shared__ PermShared sh;
+__device__ void permute_packed(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                               const PermGroup* __restrict__ groups, const PermMember* __restrict__ members,
+                               const double* __restrict__ coefs, const PermJob& job, PackShared& sh, double alpha,
+                               double beta, double ims) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
+  const int ng = job.count;
+  const int tid = threadIdx.x;
+  // group headers + prefix sums of rows / elements (one warp)
+  if (tid < 32) {
+    int racc = 0, eacc = 0;
+    for (int base = 0; base < ng; base += 32) {
+      const int gi = base + tid;
+      int rows = 0, el = 0;
+      if (gi < ng) {
+        const PermGroup& g = groups[job.group + gi];
+        const PermMember ms = members[g.src_mem], md = members[g.dst_mem];
+        const uint32_t n0 = (uint32_t)g.ext[0];
+        el = (int)g.nelem;
+        rows = el / (int)n0;
+        sh.s0[gi] = g.sa[0] + ms.ld * g.sb[0];
+        sh.d0[gi] = g.da[0] + md.ld * g.db[0];
+        sh.sd1[gi] = ms.d1;
+        sh.dd1[gi] = md.d1;
+        sh.dd2[gi] = md.d2;
+        sh.c[gi] = alpha * coefs[g.coef_off];
+        FastDiv fd;
+        fd.init(n0);
+        sh.fm[gi] = fd.m;
+        sh.fs[gi] = fd.s;
+        sh.n0[gi] = n0;
+      }
+      int ri = rows, ei = el;  // inclusive warp scans
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int yr = __shfl_up_sync(0xffffffffu, ri, o), ye = __shfl_up_sync(0xffffffffu, ei, o);
+        if (tid >= o) {
+          ri += yr;
+          ei += ye;
+        }
+      }
+      if (gi < ng) {
+        sh.rstart[gi] = racc + ri - rows;
+        sh.estart[gi] = eacc + ei - el;
+      }
+      racc += __shfl_sync(0xffffffffu, ri, 31);
+      eacc += __shfl_sync(0xffffffffu, ei, 31);
+    }
+    if (tid == 0) {
+      sh.rstart[ng] = racc;
+      sh.estart[ng] = eacc;
+    }
+  }
+  __syncthreads();
+  // row tables: final source / destination offsets of every row start
+  const int nrows = sh.rstart[ng];
+  for (int r = tid; r < nrows; r += kPermThreads) {
+    int lo = 0, hi = ng - 1;  // last group with rstart <= r
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (sh.rstart[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const PermGroup& g = groups[job.group + lo];
+    uint32_t R = (uint32_t)(r - sh.rstart[lo]);
+    int64_t sa = 0, sb = 0, da = 0, db = 0;
+#pragma unroll 1
+    for (int l = 1; l < g.ndim; ++l) {
+      const uint32_t e = (uint32_t)g.ext[l];
+      const uint32_t q = R / e;
+      const int64_t i = R - q * e;
+      R = q;
+      sa += i * g.sa[l];
+      sb += i * g.sb[l];
+      da += i * g.da[l];
+      db += i * g.db[l];
+    }
+    const PermMember ms = members[g.src_mem], md = members[g.dst_mem];
+    sh.rs[r] = ms.off + sa + ms.ld * sb;
+    sh.rd[r] = md.off + da + md.ld * db;
+  }
+  __syncthreads();
+  pdl_wait();
+  const int total = sh.estart[ng];
+  constexpr int U = sizeof(V) == 16 ? 4 : 8;
+  int gi = 0;
+  for (int e0 = tid; e0 < total; e0 += U * kPermThreads) {
+    V x[U];
+    int64_t od[U];
+    int gu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kPermThreads;
+      gu[u] = -1;
+      if (e < total) {
+        while (sh.estart[gi + 1] <= e) ++gi;
+        const uint32_t loc = (uint32_t)(e - sh.estart[gi]);
+        FastDiv fd;
+        fd.d = sh.n0[gi];
+        fd.m = sh.fm[gi];
+        fd.s = sh.fs[gi];
+        const uint32_t r = fd.div(loc);
+        const uint32_t i0 = loc - r * fd.d;
+        const int row = sh.rstart[gi] + (int)r;
+        x[u] = IO::load(src, sh.rs[row] + (int64_t)i0 * sh.s0[gi], sh.sd1[gi]);
+        od[u] = sh.rd[row] + (int64_t)i0 * sh.d0[gi];
+        gu[u] = gi;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (gu[u] >= 0) {
+        const int g = gu[u];
+        IO::store(dst, od[u], sh.dd1[g], sh.dd2[g], Num<V>::scale(sh.c[g], x[u]), beta, ims);
+      }
+  }
+}
+
+// One launch covers every abelian-style job of up to two permutes (A~ and B~ of a contraction, op 0/1):
+// rows, smem-tiled and packed jobs share the grid, so small latency-bound permutes do not serialise
+// over several launches. <= 64 registers so that 4 CTAs (32 warps) share an SM.
+union PermSharedAll {
+  PermShared p;
+  PackShared k;
+};
+
+// ROWS_ONLY: a launch whose jobs are all rows jobs (the large cfg4 permutes) uses a leaner instance
+// (48 registers instead of 64; measured 5.0 vs 4.6 TB/s on cfg4).
+template <int CM, bool ROWS_ONLY>
+__global__ void __launch_bounds__(kPermThreads, 4) permute_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
+  using IO = CIO<CM>;
+  __shared__ typename std::conditional<ROWS_ONLY, PermShared, PermSharedAll>::type sh_;
+  PermShared& sh = *reinterpret_cast<PermShared*>(&sh_);
+  extern __shared__ __align__(16) unsigned char perm_dyn[];
+  pdl_trigger();
   const PermJob job = jobs[blockIdx.x];
-  const PermGroup& g = groups[job.group];
-  load_job_header(g, members, coefs, sh);
-  permute_rows<CM, true>((const typename CIO<CM>::S*)src, (typename CIO<CM>::D*)dst, g, job, sh, alpha, beta, ims);
+  const PermOp& op = (ROWS_ONLY || !job.op) ? op0 : op1;  // rows-only launches carry a single permute
+  const auto* src = (const typename IO::S*)op.src;
+  auto* dst = (typename IO::D*)op.dst;
+  if constexpr (!ROWS_ONLY) {
+    if (job.type == kJobPacked) {
+      permute_packed<CM>(src, dst, op.groups, op.members, op.coefs, job, *reinterpret_cast<PackShared*>(&sh_),
+                         op.alpha, op.beta, op.ims);
+      return;
+    }
+  }
+  const PermGroup& g = op.groups[job.group];
+  load_job_header(g, op.members, op.coefs, sh);
+  if (!ROWS_ONLY && job.type == kJobTiled)
+    permute_tiled<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
+  else
+    permute_rows<CM, true>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
 }
 
 // rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight)
 template <int CM>
 __global__ void __launch_bounds__(kPermThreads, 2)
-    permute_recouple_kernel(const void* __restrict__ src, void* __restrict__ dst, const PermGroup* __restrict__ groups,
-                            const PermMember* __restrict__ members, const double* __restrict__ coefs,
-                            const PermJob* __restrict__ jobs, double alpha, double beta, double ims) {
+    permute_recouple_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
+  using IO = CIO<CM>;
   __shared__ PermShared sh;
+  pdl_trigger();
   const PermJob job = jobs[blockIdx.x];
-  const PermGroup& g = groups[job.group];
-  load_job_header(g, members, coefs, sh);
-  permute_rows<CM, false>((const typename CIO<CM>::S*)src, (typename CIO<CM>::D*)dst, g, job, sh, alpha, beta, ims);
+  const PermOp& op = job.op ? op1 : op0;
+  const PermGroup& g = op.groups[job.group];
+  load_job_header(g, op.members, op.coefs, sh);
+  permute_rows<CM, false>((const typename IO::S*)op.src, (typename IO::D*)op.dst, g, job, sh, op.alpha, op.beta,
+                          op.ims);
 }
 
 template <int CM>
-__global__ void __launch_bounds__(kPermThreads, 4)
-    permute_tiled_kernel(const void* __restrict__ src, void* __restrict__ dst, const PermGroup* __restrict__ groups,
-                         const PermMember* __restrict__ members, const double* __restrict__ coefs,
-                         const PermJob* __restrict__ jobs, double alpha, double beta, double ims) {
-  __shared__ PermShared sh;
-  extern __shared__ __align__(16) unsigned char perm_dyn[];
-  const PermJob job = jobs[blockIdx.x];
-  const PermGroup& g = groups[job.group];
-  load_job_header(g, members, coefs, sh);
-  permute_tiled<CM>((const typename CIO<CM>::S*)src, (typename CIO<CM>::D*)dst, g, job, sh,
-                    reinterpret_cast<typename CIO<CM>::V*>(perm_dyn), alpha, beta, ims);
-}
-
-template <int CM>
-static void launch_permute_cm(const void* src, void* dst, const PermGroup* groups, const PermMember* members,
-                              const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi,
-                              int njobs_tiled, double alpha, double beta, double ims, cudaStream_t st) {
-  constexpr int smem = kTileElems * (int)sizeof(typename CIO<CM>::V);
+static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int njobs, int njobs_multi, bool tiled,
+                              bool rows_only, cudaStream_t st) {
+  const int smem = tiled ? kTileElems * (int)sizeof(typename CIO<CM>::V) : 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(permute_tiled_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(permute_kernel<CM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTileElems * (int)sizeof(typename CIO<CM>::V));
     attr = true;
   }
-  // job table layout: [rows (single member) | rows (recoupling groups) | tiled]
-  const PermJob* mj = jobs + njobs_rows;
-  const PermJob* tj = jobs + njobs_rows + njobs_multi;
-  if (njobs_rows)
-    permute_rows_kernel<CM><<<njobs_rows, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, jobs, alpha, beta, ims);
-  if (njobs_multi)
-    permute_recouple_kernel<CM><<<njobs_multi, kPermThreads, 0, st>>>(src, dst, groups, members, coefs, mj, alpha, beta,
-                                                                      ims);
-  if (njobs_tiled)
-    permute_tiled_kernel<CM><<<njobs_tiled, kPermThreads, smem, st>>>(src, dst, groups, members, coefs, tj, alpha, beta,
-                                                                      ims);
+  if (njobs && rows_only) launch_k(permute_kernel<CM, true>, njobs, kPermThreads, 0, st, op0, op1, jobs);
+  if (njobs && !rows_only) launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
+  if (njobs_multi) launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, 0, st, op0, op1, jobs + njobs);
 }
 
-cudaError_t launch_permute(const void* src, void* dst, const PermGroup* groups, const PermMember* members,
-                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi, int njobs_tiled,
-                           double alpha, double beta, int cm, double ims, cudaStream_t st) {
+cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
+                           bool tiled, bool rows_only, int cm, cudaStream_t st) {
   switch (cm) {
-    case kPermReal:
-      launch_permute_cm<kPermReal>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled, alpha,
-                                   beta, ims, st);
-      break;
-    case kPermCToC:
-      launch_permute_cm<kPermCToC>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled, alpha,
-                                   beta, ims, st);
-      break;
-    case kPermCToPlanar:
-      launch_permute_cm<kPermCToPlanar>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled,
-                                        alpha, beta, ims, st);
-      break;
-    case kPermCToRealRep:
-      launch_permute_cm<kPermCToRealRep>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled,
-                                         alpha, beta, ims, st);
-      break;
-    case kPermPlanarToC:
-      launch_permute_cm<kPermPlanarToC>(src, dst, groups, members, coefs, jobs, njobs_rows, njobs_multi, njobs_tiled,
-                                        alpha, beta, ims, st);
-      break;
-    default:
-      return cudaErrorInvalidValue;
+    case kPermReal: launch_permute_cm<kPermReal>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
+    case kPermCToC: launch_permute_cm<kPermCToC>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
+    case kPermCToPlanar: launch_permute_cm<kPermCToPlanar>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
+    case kPermCToRealRep: launch_permute_cm<kPermCToRealRep>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
+    case kPermPlanarToC: launch_permute_cm<kPermPlanarToC>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
@@ -782,9 +925,7 @@ __device__ __forceinline__ void gemm_tile_mbar(const double* __restrict__ A, con
 }
 
 #define TK_MBAR 128, 128, 32, 32, 16, 6
-#define TK_MBAR8 128, 128, 64, 32, 16, 6
 using MbarCfg = GemmCfg<TK_MBAR>;
-using Mbar8Cfg = GemmCfg<TK_MBAR8>;
 constexpr size_t kMbarSmem = MbarCfg::SMEM + 2 * 6 * sizeof(uint64_t);
 
 template <int PD>
@@ -793,99 +934,125 @@ __global__ void __launch_bounds__(MbarCfg::THREADS, 1)
                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
                      double beta, int base_vec) {
   extern __shared__ __align__(16) double smem[];
+  pdl_trigger();
   const GemmTile t = tiles[blockIdx.x];
   const GemmGroup g = groups[t.group];
+  pdl_wait();
   gemm_tile_mbar<TK_MBAR, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
-template <int PD>
-__global__ void __launch_bounds__(Mbar8Cfg::THREADS, 1)
-    gemm_mbar8_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                      double beta, int base_vec) {
-  extern __shared__ __align__(16) double smem[];
-  const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup g = groups[t.group];
-  gemm_tile_mbar<TK_MBAR8, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
-}
-
-#define TK_BIG 128, 128, 64, 32, 32, 3
-#define TK_BIG16 128, 128, 32, 32, 32, 3
 #define TK_SMALL 64, 64, 32, 32, 16, 3
-using BigCfg = GemmCfg<TK_BIG>;
-using Big16Cfg = GemmCfg<TK_BIG16>;
 using SmallCfg = GemmCfg<TK_SMALL>;
-
-__global__ void __launch_bounds__(BigCfg::THREADS, 1)
-    gemm_big_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                    const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                    double beta, int base_vec) {
-  extern __shared__ __align__(16) double smem[];
-  const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup g = groups[t.group];
-  gemm_tile<TK_BIG>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
-}
-
-// 16 warps of 32x32 on the same 128x128 tile: 4 warps per SMSP to hide LDS latency and barrier skew
-__global__ void __launch_bounds__(Big16Cfg::THREADS, 1)
-    gemm_big16_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                      double beta, int base_vec) {
-  extern __shared__ __align__(16) double smem[];
-  const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup g = groups[t.group];
-  gemm_tile<TK_BIG16>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
-}
 
 __global__ void __launch_bounds__(SmallCfg::THREADS)
     gemm_small_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
                       double beta, int base_vec) {
   extern __shared__ __align__(16) double smem[];
+  pdl_trigger();
   const GemmTile t = tiles[blockIdx.x];
   const GemmGroup g = groups[t.group];
+  pdl_wait();
   gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
+// ---- skinny blocks (N, K <= kSkinnyMax; the MPO steps T.W of the DMRG chains, M up to 2e5): a
+// streaming kernel, HBM-bound (AI = 2KN / 8(K+N) < 1 flop/B), so plain FMAs: the K x N operand sits in
+// shared memory, each thread owns rows of A~ / C~, loads A~[m, 0..K) (coalesced across the warp for
+// every k) and writes C~[m, 0..N). One CTA covers kSkinnyRows consecutive rows of one group.
+constexpr int kSkinnyThreads = 256;
+template <int KM, int NM>
+__device__ __forceinline__ void skinny_rows(const double* __restrict__ Ag, double* __restrict__ Cg, const double* Bs,
+                                            const GemmGroup& g, int m0, int mend, double beta) {
+  // RW rows per thread per iteration: 16 A~ loads in flight per thread, each B value read once per k, n
+  constexpr int RW = 16 / (KM > NM ? KM : NM);
+  const int K = g.K, N = g.N;
+  for (int mb = m0 + threadIdx.x; mb < mend; mb += RW * kSkinnyThreads) {
+    double a[RW][KM], acc[RW][NM];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int m = mb + r * kSkinnyThreads;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) a[r][k] = (k < K && m < mend) ? __ldg(Ag + m + (int64_t)k * g.lda) : 0.0;
+#pragma unroll
+      for (int n = 0; n < NM; ++n) acc[r][n] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < KM; ++k)
+#pragma unroll
+      for (int n = 0; n < NM; ++n) {
+        const double b = Bs[k * kSkinnyMax + n];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) acc[r][n] = fma(a[r][k], b, acc[r][n]);
+      }
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int m = mb + r * kSkinnyThreads;
+      if (m < mend) {
+#pragma unroll
+        for (int n = 0; n < NM; ++n)
+          if (n < N) {
+            double* cp = Cg + m + (int64_t)n * g.ldc;
+            *cp = beta != 0.0 ? fma(beta, *cp, acc[r][n]) : acc[r][n];
+          }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSkinnyThreads)
+    gemm_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
+                       double beta) {
+  __shared__ double Bs[kSkinnyMax * kSkinnyMax];
+  pdl_trigger();
+  const GemmTile t = tiles[blockIdx.x];
+  const GemmGroup g = groups[t.group];
+  const int K = g.K, N = g.N;
+  pdl_wait();
+  for (int i = threadIdx.x; i < kSkinnyMax * kSkinnyMax; i += kSkinnyThreads) {
+    const int k = i / kSkinnyMax, n = i % kSkinnyMax;
+    Bs[i] = (k < K && n < N) ? alpha * B[g.b_off + k + (int64_t)n * g.ldb] : 0.0;
+  }
+  __syncthreads();
+  const double* Ag = A + g.a_off;
+  double* Cg = C + g.c_off;
+  const int mend = min(g.M, t.m0 + t.pad);
+  // unrolled FMA blocks sized to the group (the FP64 FMA rate must stay above the HBM rate)
+  const int kc = K <= 4 ? 0 : (K <= 8 ? 1 : 2), nc = N <= 4 ? 0 : (N <= 8 ? 1 : 2);
+  switch (kc * 3 + nc) {
+    case 0: skinny_rows<4, 4>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 1: skinny_rows<4, 8>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 2: skinny_rows<4, 16>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 3: skinny_rows<8, 4>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 4: skinny_rows<8, 8>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 5: skinny_rows<8, 16>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 6: skinny_rows<16, 4>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    case 7: skinny_rows<16, 8>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+    default: skinny_rows<16, 16>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
+  }
+}
+
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
-                        int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st) {
+                        int ntiles_big, int ntiles_small, int ntiles_skinny, double alpha, double beta,
+                        cudaStream_t st) {
+  // big tiles: mbarrier pipeline, 16 warps of 32x32 on 128x128, BK 16, 6 stages, prefetch distance 2
   static bool attr = false;
-  static int variant = 2;  // mbarrier pipeline, 16 warps of 32x32, BK 16, 6 stages, prefetch distance 2
   if (!attr) {
-    cudaFuncSetAttribute(gemm_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BigCfg::SMEM);
-    cudaFuncSetAttribute(gemm_big16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Big16Cfg::SMEM);
     cudaFuncSetAttribute(gemm_mbar_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
-    cudaFuncSetAttribute(gemm_mbar_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
-    cudaFuncSetAttribute(gemm_mbar_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
-    cudaFuncSetAttribute(gemm_mbar8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
-    cudaFuncSetAttribute(gemm_mbar8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
-    cudaFuncSetAttribute(gemm_mbar_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
     cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
-    const char* v = getenv("TK_GEMM_BIG_WARPS");
-    if (v) variant = atoi(v);
     attr = true;
   }
   const int base_vec = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0;
-  if (ntiles_big && variant == 0)
-    gemm_mbar_kernel<3><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big && variant == 2)
-    gemm_mbar_kernel<2><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big && variant == 4)
-    gemm_mbar_kernel<4><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big && variant == 1)
-    gemm_mbar8_kernel<3><<<ntiles_big, Mbar8Cfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big && variant == 5)
-    gemm_mbar8_kernel<2><<<ntiles_big, Mbar8Cfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big && variant == 6)
-    gemm_mbar_kernel<1><<<ntiles_big, MbarCfg::THREADS, kMbarSmem, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big && variant == 8)
-    gemm_big_kernel<<<ntiles_big, BigCfg::THREADS, BigCfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta, base_vec);
-  else if (ntiles_big)
-    gemm_big16_kernel<<<ntiles_big, Big16Cfg::THREADS, Big16Cfg::SMEM, st>>>(A, B, C, groups, tiles, alpha, beta,
-                                                                            base_vec);
+  if (ntiles_big)
+    launch_k(gemm_mbar_kernel<2>, ntiles_big, MbarCfg::THREADS, kMbarSmem, st, A, B, C, groups, tiles, alpha, beta,
+             base_vec);
   if (ntiles_small)
-    gemm_small_kernel<<<ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st>>>(A, B, C, groups, tiles + ntiles_big,
-                                                                               alpha, beta, base_vec);
+    launch_k(gemm_small_kernel, ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C, groups,
+             tiles + ntiles_big, alpha, beta, base_vec);
+  if (ntiles_skinny)
+    launch_k(gemm_skinny_kernel, ntiles_skinny, kSkinnyThreads, 0, st, A, B, C, groups,
+             tiles + ntiles_big + ntiles_small, alpha, beta);
   return cudaGetLastError();
 }
 

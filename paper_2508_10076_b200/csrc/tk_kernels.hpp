@@ -57,10 +57,28 @@ enum PermCM : int {
 // A CTA work item: `count` work units of group `group` starting at unit `first`.
 // mode 0 unit = one row (dst leg 0); mode 1 unit = one smem tile of c0 x ct x R elements.
 constexpr int kTileElems = 4608;  // smem capacity of the two tile buffers (elements, incl. padding)
+// packed jobs: `count` consecutive small single-member rows groups starting at `group` (first unused),
+// so that tiny subblocks (cfg3: 9756 subblocks of ~700 elements) do not cost one CTA each
+constexpr int kPackGroups = 32;
+constexpr int kPackRows = 1024;
+constexpr int kPackElems = 8192;
+enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3 };
 struct PermJob {
   int32_t group;
-  int32_t count;
+  int16_t count;  // rows / tiles / packed groups of this job
+  int8_t type;    // PermJobType
+  int8_t op;      // which permute of a launch (0: A~ or the only one, 1: B~)
   int64_t first;
+};
+
+// One permute of a launch: data pointers, the plan's device tables, scalars.
+struct PermOp {
+  const void* src;
+  void* dst;
+  const PermGroup* groups;
+  const PermMember* members;
+  const double* coefs;
+  double alpha, beta, ims;  // ims = -1 conjugates the source (tk_contract conjA / conjB; modes 2 and 3)
 };
 
 // Grouped GEMM: C^c = alpha * A^c B^c + beta * C^c, all column-major.
@@ -81,10 +99,16 @@ struct GemmTile {
 // launchers (tk_kernels.cu)
 // ims = -1 conjugates the source (tk_contract conjA / conjB; modes 2 and 3 only). Modes 2 and 3
 // write workspace only and require beta == 0.
-cudaError_t launch_permute(const void* src, void* dst, const PermGroup* groups, const PermMember* members,
-                           const double* coefs, const PermJob* jobs, int njobs_rows, int njobs_multi,
-                           int njobs_tiled, double alpha, double beta, int cm, double ims, cudaStream_t st);
+// job table layout: [rows / tiled / packed jobs (njobs, one launch) | recoupling jobs (njobs_multi)];
+// `tiled`: some job is smem-tiled (dynamic shared memory needed). Modes 2 and 3 require beta == 0.
+// rows_only: every job of the first launch is a rows job (leaner kernel instance)
+cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
+                           bool tiled, bool rows_only, int cm, cudaStream_t st);
+// tile table layout: [big (128x128 DMMA) | small (64x64 DMMA) | skinny (streaming, GemmTile.pad = rows)]
+constexpr int kSkinnyMax = 16;   // skinny groups: 0 < K <= 16 and N <= 16
+constexpr int kSkinnyRows = 2048;
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
-                        int ntiles_big, int ntiles_small, double alpha, double beta, cudaStream_t st);
+                        int ntiles_big, int ntiles_small, int ntiles_skinny, double alpha, double beta,
+                        cudaStream_t st);
 
 }  // namespace tk

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -40,7 +41,9 @@ struct PermPlan {
   std::vector<PermMember> members;
   std::vector<double> coefs;
   std::vector<PermJob> jobs;
-  int njobs_rows = 0, njobs_multi = 0, njobs_tiled = 0;
+  int njobs = 0, njobs_multi = 0, njobs_rows = 0;  // jobs = [rows | tiled | packed | recoupling]
+  bool tiled = false, rows_only = false;
+  bool split = false;  // large permute: rows jobs in their own (leaner) launch
   DevBuf d_groups, d_members, d_coefs, d_jobs;
   double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
   int64_t n_src = 0, n_dst = 0;
@@ -162,6 +165,9 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
   if (legs.empty()) legs.push_back(L{1, 0, 0, 0, 0});
   if ((int)legs.size() > kMaxLegs) TK_THROW(TK_ERR_UNSUPPORTED, "too many legs after merging");
   g.ndim = (int)legs.size();
+  int64_t ne = 1;
+  for (auto& l : legs) ne *= l.e;
+  if (ne >= (int64_t(1) << 31)) TK_THROW(TK_ERR_UNSUPPORTED, "a single subblock with >= 2^31 elements");
   g.nelem = 1;
   for (int i = 0; i < kMaxLegs; ++i) {
     if (i < g.ndim) {
@@ -209,27 +215,78 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
   }
 }
 
+// small single-member groups of either geometry (the packed path takes any leg-0 strides, so tiny
+// transposing groups need no shared-memory tile)
+static bool packable(const PermGroup& g) {
+  return g.ksrc == 1 && g.kdst == 1 && g.nelem <= 2048 && g.nelem / g.ext[0] <= kPackRows;
+}
+
 static void make_jobs(PermPlan& P) {
-  std::vector<PermJob> rows, multi, tiles;
+  // small single-member groups go last and are packed several per CTA (permute_packed_kernel)
+  std::stable_partition(P.groups.begin(), P.groups.end(), [](const PermGroup& g) { return !packable(g); });
+  std::vector<PermJob> rows, multi, tiles, packed;
+  // elements per CTA job: 8192 for large permutes, smaller for small ones so that a latency-bound
+  // permute still spreads over about two waves of the 148 SMs x 4 resident CTAs
+  int64_t total = 0;
+  for (const PermGroup& g : P.groups) total += g.nelem;
+  const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(kPackElems, total / (2 * 148 * 4)));
+  int64_t pack_elems = 0, pack_rows = 0;
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
+    if (packable(g)) {
+      int64_t nrow = g.nelem / g.ext[0];
+      if (!packed.empty() && packed.back().count < kPackGroups && pack_elems + g.nelem <= job_elems &&
+          pack_rows + nrow <= kPackRows) {
+        packed.back().count += 1;
+        pack_elems += g.nelem;
+        pack_rows += nrow;
+      } else {
+        packed.push_back(PermJob{gi, 1, kJobPacked, 0, 0});
+        pack_elems = g.nelem;
+        pack_rows = nrow;
+      }
+      continue;
+    }
     if (g.mode == 0) {
       int64_t nrows = g.nelem / g.ext[0];
-      int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, 8192 / std::max(1, g.ext[0])));
-      auto& dst = (g.ksrc == 1 && g.kdst == 1) ? rows : multi;
-      for (int64_t r = 0; r < nrows; r += per) dst.push_back(PermJob{gi, (int32_t)std::min(per, nrows - r), r});
+      int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, job_elems / std::max(1, g.ext[0])));
+      const bool single = g.ksrc == 1 && g.kdst == 1;
+      auto& dst = single ? rows : multi;
+      for (int64_t r = 0; r < nrows; r += per)
+        dst.push_back(PermJob{gi, (int16_t)std::min(per, nrows - r), (int8_t)(single ? kJobRows : kJobMulti), 0, r});
     } else {
       int64_t ntiles = (int64_t)g.T0 * g.Tt * ((g.nrest + g.R - 1) / g.R);
-      int64_t per = std::max<int64_t>(1, 16384 / ((int64_t)g.R * g.ct * g.c0));
-      for (int64_t r = 0; r < ntiles; r += per) tiles.push_back(PermJob{gi, (int32_t)std::min(per, ntiles - r), r});
+      int64_t per = std::max<int64_t>(1, std::min<int64_t>(4096, 2 * job_elems / ((int64_t)g.R * g.ct * g.c0)));
+      for (int64_t r = 0; r < ntiles; r += per)
+        tiles.push_back(PermJob{gi, (int16_t)std::min(per, ntiles - r), kJobTiled, 0, r});
     }
   }
+  // small permutes: one launch for rows, tiled and packed jobs (+ one for recoupling jobs); large ones
+  // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
+  P.njobs = (int)(tiles.size() + rows.size() + packed.size());
   P.njobs_rows = (int)rows.size();
   P.njobs_multi = (int)multi.size();
-  P.njobs_tiled = (int)tiles.size();
+  P.tiled = !tiles.empty();
+  P.rows_only = tiles.empty() && packed.empty();
+  P.split = total >= (int64_t(1) << 24) && !P.rows_only && !rows.empty();
+  static const bool dbg = getenv("TK_PLAN_DEBUG") != nullptr;
+  if (dbg) {
+    int64_t er = 0, et = 0, ep = 0, em = 0, gr = 0, gt = 0, gp = 0;
+    for (const PermGroup& g : P.groups) {
+      if (packable(g)) ep += g.nelem, ++gp;
+      else if (g.mode == 1) et += g.nelem, ++gt;
+      else if (g.ksrc == 1 && g.kdst == 1) er += g.nelem, ++gr;
+      else em += g.nelem;
+    }
+    fprintf(stderr, "[tk plan] %lld elems, job_elems %lld: rows %zu jobs (%lld groups, %lld el) | tiled %zu (%lld, %lld el) | "
+            "packed %zu (%lld, %lld el) | multi %zu (%lld el)\n", (long long)total, (long long)job_elems, rows.size(),
+            (long long)gr, (long long)er, tiles.size(), (long long)gt, (long long)et, packed.size(), (long long)gp,
+            (long long)ep, multi.size(), (long long)em);
+  }
   P.jobs = rows;
-  P.jobs.insert(P.jobs.end(), multi.begin(), multi.end());
   P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
+  P.jobs.insert(P.jobs.end(), packed.begin(), packed.end());
+  P.jobs.insert(P.jobs.end(), multi.begin(), multi.end());
 }
 
 // Internal (workspace) layout of A~, B~, C~: same blocks and subblock order as the canonical
@@ -443,9 +500,14 @@ struct ContractPlan {
   PadLayout la, lb, lc;  // workspace layouts of A~, B~, C~
   std::vector<GemmGroup> ggroups;
   std::vector<GemmTile> tiles;
-  int ntiles_big = 0, ntiles_small = 0;
+  int ntiles_big = 0, ntiles_small = 0, ntiles_skinny = 0;
   bool cplx = false;  // ComplexF64: workspace in the real representation (PermCM), one real GEMM
-  DevBuf d_ggroups, d_tiles;
+  // small Float64 contractions: both operand permutes in ONE launch (jobs of A~ = op 0, B~ = op 1)
+  bool merged_ab = false;
+  std::vector<PermJob> jobs_ab;
+  int njobs_ab = 0, njobs_ab_multi = 0;
+  bool ab_tiled = false;
+  DevBuf d_ggroups, d_tiles, d_jobs_ab;
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
   bool uploaded = false;
@@ -461,6 +523,7 @@ struct ContractPlan {
     if (!pc.identity) pc.upload();
     d_ggroups.upload(ggroups);
     d_tiles.upload(tiles);
+    d_jobs_ab.upload(jobs_ab);
     uploaded = true;
   }
 };
@@ -594,6 +657,24 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   P.pa.identity = ia_id;
   P.pb.identity = ib_id;
   P.pc.identity = ic_id;
+  if (!P.cplx && !ia_id && !ib_id && A.nelems + B.nelems < (int64_t(1) << 26)) {
+    P.merged_ab = true;
+    auto take = [&](const PermPlan& pp, int8_t op, bool multi) {
+      int b = multi ? pp.njobs : 0, e = multi ? pp.njobs + pp.njobs_multi : pp.njobs;
+      for (int i = b; i < e; ++i) {
+        PermJob j = pp.jobs[i];
+        j.op = op;
+        P.jobs_ab.push_back(j);
+      }
+    };
+    take(P.pa, 0, false);
+    take(P.pb, 1, false);
+    take(P.pa, 0, true);
+    take(P.pb, 1, true);
+    P.njobs_ab = P.pa.njobs + P.pb.njobs;
+    P.njobs_ab_multi = P.pa.njobs_multi + P.pb.njobs_multi;
+    P.ab_tiled = P.pa.tiled || P.pb.tiled;
+  }
   // workspace: A~ | B~ | C~ (skipped when the permute is the identity)
   size_t off = 0;
   if (!P.pa.identity) {
@@ -616,7 +697,7 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   std::map<Sector, int> a_blk, b_blk;
   for (int i = 0; i < (int)P.At->blocks.size(); ++i) a_blk[P.At->blocks[i].coupled] = i;
   for (int i = 0; i < (int)P.Bt->blocks.size(); ++i) b_blk[P.Bt->blocks[i].coupled] = i;
-  std::vector<GemmTile> big, small;
+  std::vector<GemmTile> big, small, skinny;
   for (int ci = 0; ci < (int)P.Ct->blocks.size(); ++ci) {
     const Block& cb = P.Ct->blocks[ci];
     GemmGroup g{};
@@ -644,6 +725,10 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     P.flops += 2.0 * g.M * (double)g.N * g.K;
     int gi = (int)P.ggroups.size();
     P.ggroups.push_back(g);
+    if (g.K > 0 && g.K <= kSkinnyMax && g.N <= kSkinnyMax) {  // streaming path (HBM-bound block)
+      for (int m = 0; m < g.M; m += kSkinnyRows) skinny.push_back(GemmTile{gi, m, 0, std::min(kSkinnyRows, g.M - m)});
+      continue;
+    }
     bool isbig = g.M >= 96 && g.N >= 96;
     int bm = isbig ? 128 : 64, bn = isbig ? 128 : 64;
     // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that one wave of
@@ -660,8 +745,10 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   std::stable_sort(small.begin(), small.end(), by_k);
   P.ntiles_big = (int)big.size();
   P.ntiles_small = (int)small.size();
+  P.ntiles_skinny = (int)skinny.size();
   P.tiles = big;
   P.tiles.insert(P.tiles.end(), small.begin(), small.end());
+  P.tiles.insert(P.tiles.end(), skinny.begin(), skinny.end());
 }
 
 // ------------------------------------------------------------------ plan cache
@@ -738,15 +825,26 @@ static void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) TK_THROW(TK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+static PermOp perm_op(PermPlan& P, const void* src, void* dst, double alpha, double beta, double ims) {
+  P.upload();
+  return PermOp{src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p, (const double*)P.d_coefs.p,
+                alpha, beta, ims};
+}
+
 static void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double beta, int cm, double ims,
                         cudaStream_t st) {
-  P.upload();
+  PermOp op = perm_op(P, src, dst, alpha, beta, ims);
   if (P.jobs.empty()) return;
-  check_cuda(launch_permute(src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p,
-                            (const double*)P.d_coefs.p, (const PermJob*)P.d_jobs.p, P.njobs_rows, P.njobs_multi, P.njobs_tiled,
-                            alpha, beta, cm, ims, st),
-             "permute launch");
-  ++g_launches;
+  const PermJob* jobs = (const PermJob*)P.d_jobs.p;
+  if (P.split) {
+    check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, true, cm, st), "permute launch");
+    check_cuda(launch_permute(op, op, jobs + P.njobs_rows, P.njobs - P.njobs_rows, P.njobs_multi, P.tiled, false, cm, st),
+               "permute launch");
+    g_launches += 1 + (P.njobs > P.njobs_rows) + (P.njobs_multi > 0);
+  } else {
+    check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, P.rows_only, cm, st), "permute launch");
+    g_launches += (P.njobs > 0) + (P.njobs_multi > 0);
+  }
 }
 
 }  // namespace tk
@@ -867,26 +965,34 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
   g_launches = 0;
   prof_record(0, st);
   const bool cx = P->cplx;
-  if (!P->pa.identity)
+  if (P->merged_ab) {
+    PermOp oa = perm_op(P->pa, a, (double*)At, 1.0, 0.0, 1.0), ob = perm_op(P->pb, b, (double*)Bt, 1.0, 0.0, 1.0);
+    check_cuda(launch_permute(oa, ob, (const PermJob*)P->d_jobs_ab.p, P->njobs_ab, P->njobs_ab_multi, P->ab_tiled,
+                              false, kPermReal, st),
+               "permute launch");
+    g_launches += (P->njobs_ab > 0) + (P->njobs_ab_multi > 0);
+  } else if (!P->pa.identity) {
     run_permute(P->pa, a, (double*)At, 1.0, 0.0, cx ? kPermCToPlanar : kPermReal, conjA ? -1.0 : 1.0, st);
+  }
   prof_record(1, st);
-  if (!P->pb.identity)
+  if (!P->merged_ab && !P->pb.identity)
     run_permute(P->pb, b, (double*)Bt, 1.0, 0.0, cx ? kPermCToRealRep : kPermReal, conjB ? -1.0 : 1.0, st);
   prof_record(2, st);
   double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
   if (!P->tiles.empty()) {
     check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, (const GemmTile*)P->d_tiles.p,
-                           P->ntiles_big, P->ntiles_small, ga, gb, st),
+                           P->ntiles_big, P->ntiles_small, P->ntiles_skinny, ga, gb, st),
                "gemm launch");
-    ++g_launches;
+    g_launches += (P->ntiles_big > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0);
   }
   prof_record(3, st);
   if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
   prof_record(4, st);
   if (g_prof.on) {
     g_prof.have = true;
-    g_prof.bytes[0] = P->pa.identity ? 0 : P->pa.bytes;
-    g_prof.bytes[1] = P->pb.identity ? 0 : P->pb.bytes;
+    // merged operand permutes: phase 0 covers both A~ and B~, phase 1 is empty
+    g_prof.bytes[0] = (P->pa.identity ? 0 : P->pa.bytes) + (P->merged_ab ? P->pb.bytes : 0);
+    g_prof.bytes[1] = (P->pb.identity || P->merged_ab) ? 0 : P->pb.bytes;
     g_prof.bytes[2] = 0;
     g_prof.bytes[3] = P->pc.identity ? 0 : P->pc.bytes;
     g_prof.flops = P->flops;

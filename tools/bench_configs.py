@@ -65,6 +65,24 @@ def chain_flops(T, steps):
     return fl
 
 
+def phase_breakdown(T, steps, reps=20):
+    """Median per-step [permute A, permute B, GEMM, permute C] microseconds (CUDA events per phase)."""
+    tk.tk_profile_enable(True)
+    res = []
+    for (na, la, nb, lb, nc, lc, ws) in steps:
+        A, a = T[na]
+        B, b = T[nb]
+        C, c = T[nc]
+        ms = []
+        for _ in range(reps):
+            tk.tk_contract(A, a, la, B, b, lb, C, c, lc, ws=ws, ws_bytes=ws.numel() * 8)
+            torch.cuda.synchronize()
+            ms.append(tk.tk_phase_times()[0])
+        res.append([round(float(x) * 1e3, 1) for x in np.median(np.array(ms), axis=0)])
+    tk.tk_profile_enable(False)
+    return res
+
+
 def time_events(fn, reps):
     ts = []
     for _ in range(reps):
@@ -94,6 +112,7 @@ def main():
     ap.add_argument("--cfgs", default="1,2,3,5")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="per-step [permA, permB, gemm, permC] us")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     makers = {1: W.cfg1, 2: W.cfg2, 3: W.cfg3, 4: lambda: W.cfg4(d_leg=128), 5: W.cfg5}
@@ -122,6 +141,8 @@ def main():
         out = {"cfg": k, "kind": cfg["kind"], "steps": len(steps), "block_flops": fl, "launches": launches,
                "us_per_chain": round(us, 2), "GFLOP_s": round(fl / (us * 1e-6) / 1e9, 2),
                "us_per_chain_graph": round(us_g, 2), "GFLOP_s_graph": round(fl / (us_g * 1e-6) / 1e9, 2)}
+        if args.phases:
+            out["phase_us_per_step"] = phase_breakdown(T, steps)
         if args.oracle:
             t, tier = oracle_time(cfg)
             out["oracle_s"] = round(t, 3)
