@@ -39,8 +39,9 @@ def rel_err_blocks(layout, flat, blocks, keys=None):
 
 
 @pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=96), lambda: W.cfg4(d_leg=32),
-                                    lambda: W.cfg5(), lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1))],
-                         ids=["cfg1", "cfg2", "cfg3_chi96", "cfg4_d32", "cfg5", "cfg5_small"])
+                                    lambda: W.cfg5(), lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1)),
+                                    lambda: W.cfg6(), lambda: W.cfg6(mults=(3, 4, 3, 2, 2, 1, 1))],
+                         ids=["cfg1", "cfg2", "cfg3_chi96", "cfg4_d32", "cfg5", "cfg5_small", "cfg6", "cfg6_small"])
 def test_chain_dense_oracle(cfgfun):
     cfg = cfgfun()
     ref = H.oracle_chain_dense(cfg)
@@ -103,8 +104,9 @@ def test_cfg4_full_size_sampled():
 
 # ------------------------------------------------------------------ ComplexF64 (cfg4 names it)
 @pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=24),
-                                    lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1))],
-                         ids=["cfg1", "cfg2", "cfg3_chi64", "cfg4_d24", "cfg5_small"])
+                                    lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1)),
+                                    lambda: W.cfg6(mults=(3, 4, 3, 2, 2, 1, 1))],
+                         ids=["cfg1", "cfg2", "cfg3_chi64", "cfg4_d24", "cfg5_small", "cfg6_small"])
 def test_chain_complex_dense_oracle(cfgfun):
     """ComplexF64 through the real-representation GEMM (reading C21) against the dense oracle."""
     cfg = cfgfun()

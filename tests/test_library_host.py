@@ -56,7 +56,7 @@ def assert_same_layout(spec):
 
 
 @pytest.mark.parametrize("cfgfun", [W.cfg1, lambda: W.cfg2(), lambda: W.cfg3(chi=256), lambda: W.cfg4(d_leg=64),
-                                    lambda: W.cfg5()])
+                                    lambda: W.cfg5(), lambda: W.cfg6()])
 def test_layout_equals_oracle(cfgfun):
     cfg = cfgfun()
     for name, (spec, _) in cfg["tensors"].items():
@@ -183,7 +183,8 @@ def test_error_statuses():
 
 
 @pytest.mark.parametrize("cfgfun", [W.cfg1, lambda: W.cfg2(chi=64), lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=32),
-                                    lambda: W.cfg5(mults=(2, 2, 1, 1, 1, 1, 1))])
+                                    lambda: W.cfg5(mults=(2, 2, 1, 1, 1, 1, 1)),
+                                    lambda: W.cfg6(mults=(2, 2, 1, 1, 1, 1, 1))])
 def test_contract_output_spaces(cfgfun):
     cfg = cfgfun()
     specs = {k: v[0] for k, v in cfg["tensors"].items()}

@@ -264,14 +264,23 @@ def test_su2_equivariance_roundtrip():
         assert np.abs(Mc @ T - T @ Md).max() < 1e-12
 
 
-def test_su2_contraction_supported_on_output_layout():
-    cfg = W.cfg5(mults=(2, 2, 1, 1, 1, 1, 1))
-    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
-    Lt, At = cfg["tensors"]["L"][0], cfg["tensors"]["A"][0]
-    l1, x1 = rand_tensor("SU2", Lt["cod"], Lt["dom"], 11)
-    l2, x2 = rand_tensor("SU2", At["cod"], At["dom"], 12)
-    out = C.contract_einsum(Dn.to_dense(l1, x1), la, Dn.to_dense(l2, x2), lb, lc)
-    Ccod, Cdom = C.output_spaces(Lt["cod"], Lt["dom"], At["cod"], At["dom"], la, lb, lc, ncod)
-    lc_ = L.homspace_layout("SU2", Ccod, Cdom)
-    back = Dn.to_dense(lc_, Dn.from_dense(lc_, out))
-    assert C.rel_frobenius(back, out) < 1e-13
+@pytest.mark.parametrize("cfgfun", [lambda: W.cfg5(mults=(2, 2, 1, 1, 1, 1, 1)),
+                                    lambda: W.cfg6(mults=(2, 2, 1, 1, 1, 1, 1))], ids=["cfg5", "cfg6"])
+def test_su2_contraction_supported_on_output_layout(cfgfun):
+    """Every step's dense einsum result lies in the span of the output layout's CG basis (it is an
+    SU(2) intertwiner): projecting onto the reduced blocks and back loses nothing."""
+    cfg = cfgfun()
+    specs = {k: v[0] for k, v in cfg["tensors"].items()}
+    dense = {}
+    for i, (k, (spec, _)) in enumerate(cfg["tensors"].items()):
+        lt, x = rand_tensor("SU2", spec["cod"], spec["dom"], 11 + i)
+        dense[k] = Dn.to_dense(lt, x)
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+        out = C.contract_einsum(dense[na], la, dense[nb], lb, lc)
+        Ccod, Cdom = C.output_spaces(specs[na]["cod"], specs[na]["dom"], specs[nb]["cod"], specs[nb]["dom"],
+                                     la, lb, lc, ncod)
+        specs[nc] = {"cod": Ccod, "dom": Cdom}
+        lc_ = L.homspace_layout("SU2", Ccod, Cdom)
+        back = Dn.to_dense(lc_, Dn.from_dense(lc_, out))
+        assert C.rel_frobenius(back, out) < 1e-13
+        dense[nc] = out

@@ -135,4 +135,29 @@ def cfg5(mults=(24, 40, 40, 32, 24, 12, 6)):
     }
 
 
-CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
+# ------------------------------- config 6 (single-site SU(2) chain)
+def cfg6(mults=(24, 40, 40, 32, 24, 12, 6)):
+    """Single-site effective Hamiltonian A' = FL . A . O . FR (Alg. 11) with the paper's
+    spin-1 Heisenberg spaces P = (1), W = 2 (0) + (1), V = sum_i d_i (i + 1/2).
+    The d_i live in an external benchmark repo (absent here): the cfg5 multiplicities are reused,
+    shifted to half-integer spins 1/2 .. 13/2 (dim V = sum d_i (2i + 2) = 1172)."""
+    P = space("SU2", [((2,), 1)])
+    V = space("SU2", [((2 * j + 1,), m) for j, m in enumerate(mults)])
+    W = space("SU2", [((0,), 2), ((2,), 1)])
+    FL = {"cod": [V], "dom": [V, W]}                 # (alpha'; alpha, a)
+    A = {"cod": [V, P], "dom": [V]}                  # (alpha, s; beta)
+    O = {"cod": [W, P], "dom": [P, W]}               # (a, s'; s, b)
+    FR = {"cod": [W, dual(V)], "dom": [dual(V)]}     # (b, beta'; beta)
+    al_, al, a, s, be, sp, b, bep = range(1, 9)
+    return {
+        "cfg": 6, "kind": "SU2", "dtype": "f64",
+        "tensors": {"FL": (FL, 0), "A": (A, 1), "O": (O, 2), "FR": (FR, 3)},
+        "steps": [
+            ("FL", [al_, al, a], "A", [al, s, be], "T1", [al_, a, s, be], 2),
+            ("T1", [al_, a, s, be], "O", [a, sp, s, b], "T2", [al_, sp, be, b], 2),
+            ("T2", [al_, sp, be, b], "FR", [b, bep, be], "out", [al_, sp, bep], 2),
+        ],
+    }
+
+
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6}
