@@ -139,6 +139,36 @@ tk_status tk_contract(const tk_tensor* A, const void* a, const int32_t* labA, in
                       const tk_tensor* C, void* c, const int32_t* labC, double alpha, double beta,
                       void* ws, size_t ws_bytes, tk_stream stream);
 
+/* -------------------------------------------------- blockwise truncated SVD */
+/* A~ = permute(A, (p, q)) = U S Vh, block by block (eq. svd, "directly acting on the matrix
+ * representation" P:799-809; Alg. 9). U: (A~ codomain) <- W, S: W <- W diagonal, Vh: W <- (A~
+ * domain), with W the new bond space: one sector per coupled sector c of A~, degeneracy k_c = kept values.
+ * Float64 only. Three steps, all on the caller's workspace (tk_svd_workspace bytes, 256-byte aligned):
+ *   tk_svd          permute + one-sided Jacobi SVD of every block (async on `stream`);
+ *   tk_svd_truncate synchronises `stream`, reads the spectrum, applies the global truncation rule
+ *                   (values sorted descending over all blocks, ties by block then index; a value of block c
+ *                   weighs d_c; max_dim > 0 keeps greedily while sum_kept d_c <= max_dim; rel_tol > 0 drops
+ *                   the smallest values while sqrt(sum_dropped d_c s^2) <= rel_tol ||A||; both may be set;
+ *                   neither: keep all min(rows, cols) values) and returns new host objects W, U, S, Vh, the
+ *                   truncation error sqrt(sum_dropped d_c s^2) and ||A|| = sqrt(sum_c d_c sum s^2);
+ *   tk_svd_extract  writes U, S, Vh (canonical layouts, caller-owned device buffers) from the workspace.
+ * The workspace must not change between the three calls. Blocks with min(rows, cols) > 2048 ->
+ * TK_ERR_UNSUPPORTED. Zero singular values give zero U (or Vh) columns. */
+tk_status tk_svd_workspace(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                           size_t* bytes);
+tk_status tk_svd(const tk_tensor* A, const void* a, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                 void* ws, size_t ws_bytes, tk_stream stream);
+/* Host copy of all block spectra (sorted descending per block, blocks in A~'s order): n_blocks, per
+ * block count min(rows, cols), sigma = concatenation. Synchronises `stream`. Any output may be NULL. */
+tk_status tk_svd_spectrum(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                          const void* ws, tk_stream stream, int32_t* n_blocks, int64_t* counts, double* sigma);
+tk_status tk_svd_truncate(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                          const void* ws, int64_t max_dim, double rel_tol, tk_stream stream, tk_space** W,
+                          tk_tensor** U, tk_tensor** S, tk_tensor** Vh, double* trunc_err, double* norm);
+tk_status tk_svd_extract(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
+                         const void* ws, const tk_tensor* U, void* u, const tk_tensor* S, void* s,
+                         const tk_tensor* Vh, void* vh, tk_stream stream);
+
 /* --------------------------------------------------------------- instrumentation */
 /* Per-phase CUDA-event timing of the NEXT tk_contract call(s) on the same thread: when
  * enabled, tk_contract records events around each launch on its stream; tk_phase_times

@@ -14,49 +14,9 @@
 
 #include "tk_internal.hpp"
 #include "tk_kernels.hpp"
+#include "tk_plan.hpp"
 
 namespace tk {
-
-// ------------------------------------------------------------------ device buffers
-struct DevBuf {
-  void* p = nullptr;
-  size_t n = 0;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-  template <typename T>
-  void upload(const std::vector<T>& v) {
-    n = v.size() * sizeof(T);
-    if (n == 0) return;
-    if (cudaMalloc(&p, n) != cudaSuccess) TK_THROW(TK_ERR_CUDA, "cudaMalloc of plan table failed");
-    if (cudaMemcpy(p, v.data(), n, cudaMemcpyHostToDevice) != cudaSuccess)
-      TK_THROW(TK_ERR_CUDA, "upload of plan table failed");
-  }
-};
-
-// ------------------------------------------------------------------ permute plan
-struct PermPlan {
-  bool identity = false;
-  std::vector<PermGroup> groups;
-  std::vector<PermMember> members;
-  std::vector<double> coefs;
-  std::vector<PermJob> jobs;
-  int njobs = 0, njobs_multi = 0, njobs_rows = 0;  // jobs = [rows | tiled | packed | recoupling]
-  bool tiled = false, rows_only = false;
-  bool split = false;  // large permute: rows jobs in their own (leaner) launch
-  DevBuf d_groups, d_members, d_coefs, d_jobs;
-  double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
-  int64_t n_src = 0, n_dst = 0;
-  bool uploaded = false;
-  void upload() {
-    if (uploaded) return;
-    d_groups.upload(groups);
-    d_members.upload(members);
-    d_coefs.upload(coefs);
-    d_jobs.upload(jobs);
-    uploaded = true;
-  }
-};
 
 static std::vector<int> dst_from_src_legs(const std::vector<int>& p, const std::vector<int>& q) {
   std::vector<int> v(p.begin(), p.end());
@@ -64,7 +24,7 @@ static std::vector<int> dst_from_src_legs(const std::vector<int>& p, const std::
   return v;
 }
 
-static void validate_perm(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
+void validate_perm(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
   int N = A.nlegs();
   if ((int)(p.size() + q.size()) != N) TK_THROW(TK_ERR_INVALID_PERMUTATION, "|p| + |q| != number of legs");
   std::vector<int> seen(N, 0);
@@ -89,7 +49,7 @@ static void permuted_spaces(const Tensor& A, const std::vector<int>& p, const st
                                        : tk::make_space(leg(j)->kind, leg(j)->sectors, leg(j)->degs, leg(j)->dual));
 }
 
-static void check_target(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C) {
+void check_target(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C) {
   if (C.n_cod() != (int)p.size() || C.n_dom() != (int)q.size())
     TK_THROW(TK_ERR_SPACE_MISMATCH, "output tensor has the wrong number of codomain/domain legs");
   if (C.kind != A.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
@@ -289,20 +249,7 @@ static void make_jobs(PermPlan& P) {
   P.jobs.insert(P.jobs.end(), multi.begin(), multi.end());
 }
 
-// Internal (workspace) layout of A~, B~, C~: same blocks and subblock order as the canonical
-// layout, but every block's leading dimension is padded to a multiple of 4 doubles and every block
-// starts 32-byte aligned, so the GEMM can use 16-byte cp.async and columns start on sector bounds.
-// ComplexF64 blocks are stored as their real representation (PermCM in tk_kernels.hpp):
-// planar   (A~, C~): rows x 2cols, [re | im], imaginary part d1 = cols * ld doubles after the real part;
-// real rep (B~):     2rows x 2cols, [[re, im], [-im, re]], d1 = cols * ld, d2 = rows.
-enum class PadKind { Real, Planar, RealRep };
-struct PadLayout {
-  PadKind kind = PadKind::Real;
-  std::vector<int64_t> off, ld, d1, d2;  // in doubles
-  int64_t total = 0;                     // doubles
-};
-
-static PadLayout pad_layout(const Tensor& t, PadKind kind = PadKind::Real) {
+PadLayout pad_layout(const Tensor& t, PadKind kind) {
   PadLayout pl;
   pl.kind = kind;
   int64_t o = 0;
@@ -338,9 +285,8 @@ static bool is_identity_perm(const Tensor& A, const std::vector<int>& p, const s
   return true;
 }
 
-static void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
-                            PermPlan& P, int elem_bytes, const PadLayout* spl = nullptr,
-                            const PadLayout* dpl = nullptr) {
+void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
+                     PermPlan& P, int elem_bytes, const PadLayout* spl, const PadLayout* dpl) {
   Kind k = A.kind;
   int n1 = A.n_cod(), N = A.nlegs();
   std::vector<int> src_leg = dst_from_src_legs(p, q);
@@ -616,7 +562,7 @@ static void choose_contracted_order(const Tensor& A, const Tensor& B, Tuples& t)
   }
 }
 
-static Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, tk_dtype dt) {
+Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, tk_dtype dt) {
   std::vector<Space*> cod, dom;
   permuted_spaces(A, p, q, cod, dom);
   Tensor* t = make_tensor(dt, cod, dom);
@@ -625,7 +571,7 @@ static Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const
   return t;
 }
 
-static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
                                 const Tensor& C, const int32_t* labC, ContractPlan& P) {
@@ -797,9 +743,12 @@ static PermPlan* get_perm_plan(const Tensor& A, const std::vector<int>& p, const
 }
 
 void cache_clear() {
-  std::lock_guard<std::mutex> g(g_cache_mu);
-  g_contract_cache.clear();
-  g_perm_cache.clear();
+  {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    g_contract_cache.clear();
+    g_perm_cache.clear();
+  }
+  svd_cache_clear();
 }
 
 // ------------------------------------------------------------------ profiling state
@@ -813,6 +762,8 @@ struct Prof {
 };
 static thread_local Prof g_prof;
 static thread_local int g_launches = 0;
+void add_launches(int n) { g_launches += n; }
+void reset_launches() { g_launches = 0; }
 
 static void prof_record(int i, cudaStream_t st) {
   if (!g_prof.on) return;
@@ -821,7 +772,7 @@ static void prof_record(int i, cudaStream_t st) {
   cudaEventRecord(g_prof.ev[i], st);
 }
 
-static void check_cuda(cudaError_t e, const char* what) {
+void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) TK_THROW(TK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
@@ -831,7 +782,7 @@ static PermOp perm_op(PermPlan& P, const void* src, void* dst, double alpha, dou
                 alpha, beta, ims};
 }
 
-static void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double beta, int cm, double ims,
+void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double beta, int cm, double ims,
                         cudaStream_t st) {
   PermOp op = perm_op(P, src, dst, alpha, beta, ims);
   if (P.jobs.empty()) return;

@@ -81,6 +81,16 @@ _phase_times = _sig("tk_phase_times", [ctypes.POINTER(ctypes.c_float), _dp, _dp]
 _last_launch_count = _sig("tk_last_launch_count", [], ctypes.c_int32)
 _fsymbol = _sig("tk_fsymbol", [ctypes.c_char_p] + [_i32p] * 6 + [_dp])
 _rsymbol = _sig("tk_rsymbol", [ctypes.c_char_p] + [_i32p] * 3 + [_dp])
+_svd_workspace = _sig("tk_svd_workspace", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32,
+                                           ctypes.POINTER(ctypes.c_size_t)])
+_svd = _sig("tk_svd", [_p, _p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, ctypes.c_size_t, _p])
+_svd_spectrum = _sig("tk_svd_spectrum", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _p, _i32p, _i64p,
+                                         _dp])
+_svd_truncate = _sig("tk_svd_truncate", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, ctypes.c_int64,
+                                         ctypes.c_double, _p, ctypes.POINTER(_p), ctypes.POINTER(_p),
+                                         ctypes.POINTER(_p), ctypes.POINTER(_p), _dp, _dp])
+_svd_extract = _sig("tk_svd_extract", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _p, _p, _p, _p, _p,
+                                       _p, _p])
 _cache_clear = _sig("tk_cache_clear", [], None)
 _version = _sig("tk_version", [], ctypes.c_char_p)
 
@@ -89,7 +99,8 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_tensor_blocks", "tk_tensor_subblocks", "tk_tensor_retain", "tk_tensor_release",
             "tk_contract_output", "tk_permute_workspace", "tk_permute", "tk_contract_workspace", "tk_contract",
             "tk_profile_enable", "tk_phase_times", "tk_last_launch_count", "tk_fsymbol", "tk_rsymbol",
-            "tk_permute_transfer", "tk_last_error", "tk_cache_clear", "tk_version"]
+            "tk_permute_transfer", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
+            "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract"]
 
 
 def _i32(seq):
@@ -291,6 +302,57 @@ def tk_rsymbol(kind, a, b, c):
     out = ctypes.c_double()
     _check(_rsymbol(kind.encode(), *[x[1] for x in args], ctypes.byref(out)))
     return out.value
+
+
+def tk_svd_workspace(A, p, q):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    n = ctypes.c_size_t()
+    _check(_svd_workspace(A.h, pp, len(p), qp, len(q), ctypes.byref(n)))
+    return n.value
+
+
+def tk_svd(A, a, p, q, ws, ws_bytes, stream=None):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    _check(_svd(A.h, _ptr(a), pp, len(p), qp, len(q), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def tk_svd_spectrum(A, p, q, ws, stream=None):
+    """Per-block singular values (host), blocks in the order of permute(A, (p, q))."""
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    nb = ctypes.c_int32()
+    _check(_svd_spectrum(A.h, pp, len(p), qp, len(q), _ptr(ws), _stream(stream), ctypes.byref(nb), None, None))
+    counts = np.zeros(max(nb.value, 1), np.int64)
+    _check(_svd_spectrum(A.h, pp, len(p), qp, len(q), _ptr(ws), _stream(stream), None,
+                         counts.ctypes.data_as(_i64p), None))
+    sig = np.zeros(max(int(counts[:nb.value].sum()), 1))
+    _check(_svd_spectrum(A.h, pp, len(p), qp, len(q), _ptr(ws), _stream(stream), None, None,
+                         sig.ctypes.data_as(_dp)))
+    out, o = [], 0
+    for k in counts[:nb.value]:
+        out.append(sig[o:o + k].copy())
+        o += k
+    return out
+
+
+def tk_svd_truncate(A, p, q, ws, max_dim=0, rel_tol=0.0, stream=None):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    w, u, s, vh = _p(), _p(), _p(), _p()
+    err, nrm = ctypes.c_double(), ctypes.c_double()
+    _check(_svd_truncate(A.h, pp, len(p), qp, len(q), _ptr(ws), int(max_dim), float(rel_tol), _stream(stream),
+                         ctypes.byref(w), ctypes.byref(u), ctypes.byref(s), ctypes.byref(vh), ctypes.byref(err),
+                         ctypes.byref(nrm)))
+    return Space(w.value), Tensor(u.value), Tensor(s.value), Tensor(vh.value), err.value, nrm.value
+
+
+def tk_svd_extract(A, p, q, ws, U, u, S, s, Vh, vh, stream=None):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    _check(_svd_extract(A.h, pp, len(p), qp, len(q), _ptr(ws), U.h, _ptr(u), S.h, _ptr(s), Vh.h, _ptr(vh),
+                        _stream(stream)))
 
 
 def tk_cache_clear():
