@@ -18,6 +18,8 @@
 // columns/rows into U, S, Vh in their canonical block layouts.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -48,100 +50,126 @@ struct SvdOut {     // extraction target of one block (canonical layouts of U, S
   int32_t blk;      // SvdBlock index
 };
 
-constexpr int kSvdThreads = 512;
+constexpr int kSvdThreads = 1024;
 constexpr int kSvdWarps = kSvdThreads / 32;
+constexpr int kSvdLanes = 8;                                  // lanes per column pair
+constexpr int kSvdGroups = kSvdThreads / kSvdLanes;           // pairs rotated concurrently
 constexpr int kSvdMaxK = 2048;         // per-block limit on min(M, N) (shared scratch below)
-constexpr int kSvdSmemBytes = 200 * 1024;
+constexpr int kSvdSmemBytes = 206 * 1024;
 constexpr int kSvdMaxSweeps = 60;
 
+// SvdBlock.smem: 2 = G and V in shared memory, 1 = G only (V recovered as X^T G S^-2 afterwards),
+// 0 = both in the (L2-resident) workspace.
+
+__device__ __forceinline__ double group_sum(double x) {  // sum over the 8 lanes of a pair group
+#pragma unroll
+  for (int o = kSvdLanes / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
 
-__global__ void __launch_bounds__(kSvdThreads, 1)
-    svd_jacobi_kernel(double* __restrict__ ws, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int rotated;
-  __shared__ double sig[kSvdMaxK];
-  const SvdBlock b = blocks[blockIdx.x];
+// MODE is a template parameter so that shared-memory operands compile to LDS/STS (a runtime choice
+// of pointer would leave generic LD/ST on the critical path of every rotation)
+template <int MODE>
+__device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict__ ws, int32_t* __restrict__ idx,
+                                          double* sm, double* sig, int& rotated, int debug) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / kSvdLanes, gl = tid % kSvdLanes;
   const int R = b.R, K = b.K;
-  if (K == 0) return;
-  // working copies: G (R x K, ld ldG) and V (K x K, ld ldV), in smem when they fit
-  const int ldG = b.smem ? R : b.ldg, ldV = b.smem ? K : b.ldv;
-  double* G = b.smem ? sm : ws + b.g_off;
-  double* V = b.smem ? sm + (size_t)R * K : ws + b.v_off;
+  // working copies: G (R x K, ld ldG) and V (K x K, ld ldV)
+  constexpr bool gs = MODE >= 1, vs = MODE == 2, accv = MODE != 1;
+  const int ldG = gs ? R : b.ldg, ldV = vs ? K : b.ldv;
+  double* G = gs ? sm : ws + b.g_off;
+  double* V = vs ? sm + (size_t)R * K : ws + b.v_off;
   const double* A = ws + b.a_off;
   for (int64_t e = tid; e < (int64_t)R * K; e += kSvdThreads) {
     const int i = (int)(e % R), j = (int)(e / R);
     const double x = b.trans ? A[j + (int64_t)i * b.lda] : A[i + (int64_t)j * b.lda];
-    if (b.smem || b.trans) G[i + (int64_t)j * ldG] = x;
+    if (gs || b.trans) G[i + (int64_t)j * ldG] = x;
   }
-  for (int64_t e = tid; e < (int64_t)K * K; e += kSvdThreads) {
-    const int i = (int)(e % K), j = (int)(e / K);
-    V[i + (int64_t)j * ldV] = (i == j) ? 1.0 : 0.0;
-  }
+  if (accv)
+    for (int64_t e = tid; e < (int64_t)K * K; e += kSvdThreads) {
+      const int i = (int)(e % K), j = (int)(e / K);
+      V[i + (int64_t)j * ldV] = (i == j) ? 1.0 : 0.0;
+    }
   __syncthreads();
   const int n = K + (K & 1);  // circle method over n players; player K (if K odd) is a bye
   // stop rotating a pair once its cosine is at the rounding level of a length-R dot product
   const double tol = 2.3e-16 * sqrt((double)R);
-  for (int sweep = 0; sweep < kSvdMaxSweeps; ++sweep) {
+  int sweep = 0;
+  for (; sweep < kSvdMaxSweeps; ++sweep) {
     if (tid == 0) rotated = 0;
     __syncthreads();
+    int any = 0;
     for (int r = 0; r < n - 1; ++r) {
-      for (int pr = warp; pr < n / 2; pr += kSvdWarps) {
-        int p, q;
-        if (pr == 0) {
-          p = n - 1;
-          q = r;
-        } else {
-          p = (r + pr) % (n - 1);
-          q = (r - pr + n - 1) % (n - 1);
+      // groups of 8 lanes each own one disjoint column pair of round r (all lanes of a warp stay
+      // converged for the group shuffles; idle groups run empty loops)
+      for (int base = 0; base < n / 2; base += kSvdGroups) {
+        const int pr = base + grp;
+        int p = 0, q = 0;
+        bool act = pr < n / 2;
+        if (act) {
+          if (pr == 0) {
+            p = n - 1;
+            q = r;
+          } else {
+            p = (r + pr) % (n - 1);
+            q = (r - pr + n - 1) % (n - 1);
+          }
+          if (p > q) {
+            const int t = p;
+            p = q;
+            q = t;
+          }
+          act = q < K;
         }
-        if (p >= K || q >= K) continue;
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
-        }
+        const int len = act ? R : 0;
         double* gp = G + (int64_t)p * ldG;
         double* gq = G + (int64_t)q * ldG;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < R; i += 32) {
+        for (int i = gl; i < len; i += kSvdLanes) {
           const double x = gp[i], y = gq[i];
           al = fma(x, x, al);
           be = fma(y, y, be);
           ga = fma(x, y, ga);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
-        // 2x2 symmetric Schur rotation of [[al, ga], [ga, be]] (Hestenes one-sided Jacobi)
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        for (int i = lane; i < R; i += 32) {
-          const double x = gp[i], y = gq[i];
-          gp[i] = c * x - s * y;
-          gq[i] = s * x + c * y;
+        al = group_sum(al);
+        be = group_sum(be);
+        ga = group_sum(ga);
+        if (act && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          // 2x2 symmetric Schur rotation of [[al, ga], [ga, be]] (Hestenes one-sided Jacobi)
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int i = gl; i < R; i += kSvdLanes) {
+            const double x = gp[i], y = gq[i];
+            gp[i] = c * x - s * y;
+            gq[i] = s * x + c * y;
+          }
+          if (accv) {
+            double* vp = V + (int64_t)p * ldV;
+            double* vq = V + (int64_t)q * ldV;
+            for (int i = gl; i < K; i += kSvdLanes) {
+              const double x = vp[i], y = vq[i];
+              vp[i] = c * x - s * y;
+              vq[i] = s * x + c * y;
+            }
+          }
+          any = 1;
         }
-        double* vp = V + (int64_t)p * ldV;
-        double* vq = V + (int64_t)q * ldV;
-        for (int i = lane; i < K; i += 32) {
-          const double x = vp[i], y = vq[i];
-          vp[i] = c * x - s * y;
-          vq[i] = s * x + c * y;
-        }
-        if (lane == 0) rotated = 1;
       }
       __syncthreads();
     }
+    if (any) rotated = 1;
+    __syncthreads();
     if (!rotated) break;
     __syncthreads();
   }
+  if (debug && tid == 0) printf("[tk svd] block %d: %d x %d, mode %d, %d sweeps\n", blockIdx.x, R, K, MODE, sweep + 1);
   // singular values = column norms; rank by value (descending, ties by column index)
   for (int j = warp; j < K; j += kSvdWarps) {
     const double* g = G + (int64_t)j * ldG;
@@ -160,19 +188,69 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
     sv[rank] = sj;
     pv[rank] = j;
   }
-  // write the converged G and V back to the workspace (the extraction kernel reads them there)
-  if (b.smem) {
-    double* Gw = ws + b.g_off;
+  if (!accv) {
+    // G = X V with X the tall input (A~ or A~^T, untouched in the workspace): V = X^T G S^-2. A warp
+    // takes one row i of V: column i of X is staged in the warp's smem slot (coalesced load), then its
+    // lanes sweep 32 consecutive columns j of G with 4 independent accumulators each.
     double* Vw = ws + b.v_off;
+    double* xs = sm + (size_t)R * K + (size_t)warp * R;
+    for (int i = warp; i < K; i += kSvdWarps) {
+      for (int r = lane; r < R; r += 32) xs[r] = b.trans ? A[i + (int64_t)r * b.lda] : A[r + (int64_t)i * b.lda];
+      __syncwarp();
+      for (int j0 = 0; j0 < K; j0 += 32) {
+        const int j = j0 + lane;
+        const int jj = j < K ? j : K - 1;
+        const double* g = G + (int64_t)jj * ldG;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int r = 0;
+        for (; r + 3 < R; r += 4) {
+          a0 = fma(xs[r], g[r], a0);
+          a1 = fma(xs[r + 1], g[r + 1], a1);
+          a2 = fma(xs[r + 2], g[r + 2], a2);
+          a3 = fma(xs[r + 3], g[r + 3], a3);
+        }
+        for (; r < R; ++r) a0 = fma(xs[r], g[r], a0);
+        if (j < K) {
+          const double s2 = sig[j] * sig[j];
+          Vw[i + (int64_t)j * b.ldv] = s2 > 0.0 ? ((a0 + a1) + (a2 + a3)) / s2 : 0.0;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // write the converged G (and V) back to the workspace (the extraction kernel reads them there); for
+  // a non-transposed block G's home is A~ itself, which the V recovery above still reads
+  __syncthreads();
+  if (gs) {
+    double* Gw = ws + b.g_off;
     for (int64_t e = tid; e < (int64_t)R * K; e += kSvdThreads) {
       const int i = (int)(e % R), j = (int)(e / R);
       Gw[i + (int64_t)j * b.ldg] = G[i + (int64_t)j * ldG];
     }
+  }
+  if (vs) {
+    double* Vw = ws + b.v_off;
     for (int64_t e = tid; e < (int64_t)K * K; e += kSvdThreads) {
       const int i = (int)(e % K), j = (int)(e / K);
       Vw[i + (int64_t)j * b.ldv] = V[i + (int64_t)j * ldV];
     }
   }
+}
+
+__global__ void __launch_bounds__(kSvdThreads, 1)
+    svd_jacobi_kernel(double* __restrict__ ws, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
+                      int debug) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int rotated;
+  __shared__ double sig[kSvdMaxK];
+  const SvdBlock b = blocks[blockIdx.x];
+  if (b.K == 0) return;
+  if (b.smem == 2)
+    svd_block<2>(b, ws, idx, sm, sig, rotated, debug);
+  else if (b.smem == 1)
+    svd_block<1>(b, ws, idx, sm, sig, rotated, debug);
+  else
+    svd_block<0>(b, ws, idx, sm, sig, rotated, debug);
 }
 
 // U[:, r] = G[:, perm r] / s_r (or V[:, perm r] when transposed); Vh[r, :] = V[:, perm r]^T (or G / s);
@@ -294,9 +372,10 @@ static SvdPlan* get_svd_plan(const Tensor& A, const std::vector<int>& p, const s
     nsig += b.K;
     b.p_off = nidx;
     nidx += b.K;
-    const int64_t need = ((int64_t)b.R * b.K + (int64_t)b.K * b.K) * 8;
-    b.smem = need <= kSvdSmemBytes;
-    if (b.smem) P->smem_bytes = std::max<int>(P->smem_bytes, (int)need);
+    const int64_t need2 = ((int64_t)b.R * b.K + (int64_t)b.K * b.K) * 8;
+    const int64_t need1 = ((int64_t)b.R * b.K + (int64_t)kSvdWarps * b.R) * 8;  // + per-warp X column slots
+    b.smem = need2 <= kSvdSmemBytes ? 2 : (need1 <= kSvdSmemBytes ? 1 : 0);
+    if (b.smem) P->smem_bytes = std::max<int>(P->smem_bytes, (int)(b.smem == 2 ? need2 : need1));
     P->blocks.push_back(b);
   }
   const int64_t sig_base = off;
@@ -421,6 +500,7 @@ tk_status tk_svd(const tk_tensor* A_, const void* a, const int32_t* p, int32_t n
   reset_launches();
   run_permute(P->pa, a, ws, 1.0, 0.0, kPermReal, 1.0, st);
   if (!P->blocks.empty()) {
+    static const bool dbg = getenv("TK_SVD_DEBUG") != nullptr;
     static bool attr = false;
     if (!attr) {
       check_cuda(cudaFuncSetAttribute(svd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
@@ -428,7 +508,7 @@ tk_status tk_svd(const tk_tensor* A_, const void* a, const int32_t* p, int32_t n
       attr = true;
     }
     svd_jacobi_kernel<<<(unsigned)P->blocks.size(), kSvdThreads, P->smem_bytes, st>>>(
-        (double*)ws, (int32_t*)((char*)ws + P->idx_off), (const SvdBlock*)P->d_blocks.p);
+        (double*)ws, (int32_t*)((char*)ws + P->idx_off), (const SvdBlock*)P->d_blocks.p, dbg ? 1 : 0);
     check_cuda(cudaGetLastError(), "svd launch");
     add_launches(1);
   }
