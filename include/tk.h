@@ -15,7 +15,8 @@
  *
  * Conventions:
  *  - Sector labels are int32 tuples of the kind's width: "Z2"/"fZ2" {g}, "U1" {q},
- *    "U1xU1"/"fU1xU1" {N, 2Sz} (fermion parity N mod 2), "SU2" {2j}.
+ *    "U1xU1"/"fU1xU1" {N, 2Sz} (fermion parity N mod 2), "SU2" {2j}, "fU1xSU2" {N, 2j} (the Hubbard
+ *    fZ2 x U1 x SU2 Deligne product, P:2380-2412 / P:2582-2591; fermion parity N mod 2).
  *  - A space lists the sectors of the UNDERLYING space V; is_dual = 1 makes it V*. Fusion
  *    trees label a dual leg by the dual sector (reading C6).
  *  - Legs are numbered codomain first, then domain, 0-based in this ABI.
@@ -70,12 +71,13 @@ typedef struct tk_tensor tk_tensor;
 typedef struct CUstream_st* tk_stream; /* = cudaStream_t; NULL = legacy default stream */
 
 /* ------------------------------------------------------------------ spaces (host) */
-/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2". labels: n_sectors x width int32,
+/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2" | "fU1xSU2". labels: n_sectors x width int32,
  * degeneracies: n_sectors int64 > 0 (zero entries are dropped). Sectors may be given
  * in any order; they are stored ascending. Duplicate labels -> TK_ERR_INVALID_ARGUMENT. */
 tk_status tk_space_create(const char* kind, int32_t n_sectors, const int32_t* labels,
                           const int64_t* degeneracies, int32_t is_dual, tk_space** out);
-/* Grammar "U1[-2:3, 0:5]'" / "SU2[0:1, 1/2:2]" / "U1xU1[(1,-1):2]"; trailing ' = dual. */
+/* Grammar "U1[-2:3, 0:5]'" / "SU2[0:1, 1/2:2]" / "U1xU1[(1,-1):2]" / "fU1xSU2[(1,1/2):3]";
+ * trailing ' = dual. */
 tk_status tk_space_parse(const char* text, tk_space** out);
 /* n_sectors, total dim = sum N_a d_a, is_dual, label width (any out pointer may be NULL). */
 tk_status tk_space_info(const tk_space* s, int32_t* n_sectors, int64_t* dim, int32_t* is_dual,

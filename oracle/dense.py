@@ -36,32 +36,34 @@ def leg_basis(sp):
     return out, off
 
 
-def _splitting_tensor(uncoupled, inner, coupled):
-    """X[mu_1..mu_N, mu_c] for the canonical left-to-right SU(2) tree (doubled spins)."""
+def _splitting_tensor(kind, uncoupled, inner, coupled):
+    """X[mu_1..mu_N, mu_c] for the canonical left-to-right SU(2) tree (doubled spins of the SU(2)
+    factor; a U(1) factor is one-dimensional and only selects the sector)."""
+    j = lambda lab: sectors.spin2(kind, lab)  # noqa: E731
     n = len(uncoupled)
     if n == 0:
         return np.ones((1,))
     if n == 1:
-        return np.eye(uncoupled[0][0] + 1)
+        return np.eye(j(uncoupled[0]) + 1)
     chain = list(inner) + [coupled]
-    X = su2.cg_tensor(uncoupled[0][0], uncoupled[1][0], chain[0][0])
+    X = su2.cg_tensor(j(uncoupled[0]), j(uncoupled[1]), j(chain[0]))
     for k in range(2, n):
-        C = su2.cg_tensor(chain[k - 2][0], uncoupled[k][0], chain[k - 1][0])
+        C = su2.cg_tensor(j(chain[k - 2]), j(uncoupled[k]), j(chain[k - 1]))
         X = np.tensordot(X, C, axes=([X.ndim - 1], [0]))
     return X
 
 
-def basis_tensor(cod, dom, key):
+def basis_tensor(kind, cod, dom, key):
     """Dense basis element X_s o X_f^dagger of tree pair `key`, shape (d_cod..., d_dom...)."""
     s_unc, s_inn, c, f_unc, f_inn = key
-    Xs = _splitting_tensor(s_unc, s_inn, c)
-    Xf = _splitting_tensor(f_unc, f_inn, c)
+    Xs = _splitting_tensor(kind, s_unc, s_inn, c)
+    Xf = _splitting_tensor(kind, f_unc, f_inn, c)
     for k, sp in enumerate(cod):
         if sp["dual"]:
-            Xs = su2.z_flip(Xs, k, s_unc[k][0])
+            Xs = su2.z_flip(Xs, k, sectors.spin2(kind, s_unc[k]))
     for k, sp in enumerate(dom):
         if sp["dual"]:
-            Xf = su2.z_flip(Xf, k, f_unc[k][0])
+            Xf = su2.z_flip(Xf, k, sectors.spin2(kind, f_unc[k]))
     return np.tensordot(Xs, Xf, axes=([Xs.ndim - 1], [Xf.ndim - 1]))
 
 
@@ -101,7 +103,7 @@ def to_dense(layout, flat):
             idx = tuple(slice(o, o + n) for o, n, _ in sl)
             D[idx] = R
         else:
-            B = basis_tensor(layout.cod, layout.dom, sb.key)
+            B = basis_tensor(kind, layout.cod, layout.dom, sb.key)
             T = np.multiply.outer(R, B)  # (n_1..n_N, d_1..d_N)
             perm = [x for k in range(nl) for x in (k, nl + k)]
             T = T.transpose(perm).reshape([n * d for _, n, d in sl])
@@ -124,7 +126,7 @@ def from_dense(layout, D):
         else:
             idx = tuple(slice(o, o + n * d) for o, n, d in sl)
             sub = D[idx].reshape([x for _, n, d in sl for x in (n, d)])
-            B = basis_tensor(layout.cod, layout.dom, sb.key)
+            B = basis_tensor(kind, layout.cod, layout.dom, sb.key)
             # contract the inner (d) axes with B
             sub = np.tensordot(sub, B, axes=([2 * k + 1 for k in range(nl)], list(range(nl))))
             dc = sectors.qdim(kind, sb.key[2])

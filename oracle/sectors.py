@@ -8,13 +8,24 @@ Labels are tuples of ints:
   fU1xU1  (N, 2Sz)  as U1xU1 with fermion parity N mod 2 (BASELINE cfg3, reading C14)
   SU2     (2j,)     N^{j1 j2}_{j3} = 1 iff |j1-j2| <= j3 <= j1+j2 (and integrality), d = 2j+1
                     P:2303-2312
+  fU1xSU2 (N, 2j)   Hubbard fZ2 x U1 x SU2 as a Deligne product:
+                    charges add, spins by the SU2 rule, d = 2j+1, fermion parity N mod 2 (reading C14)
 """
 
-KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2")
+KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2")
 
 
 def width(kind):
-    return 2 if kind in ("U1xU1", "fU1xU1") else 1
+    return 2 if kind in ("U1xU1", "fU1xU1", "fU1xSU2") else 1
+
+
+def spin2(kind, a):
+    """Doubled spin of the SU(2) factor of a label (0 for kinds without one)."""
+    if kind == "SU2":
+        return a[0]
+    if kind == "fU1xSU2":
+        return a[1]
+    return 0
 
 
 def unit(kind):
@@ -24,6 +35,8 @@ def unit(kind):
 def dual(kind, a):
     if kind in ("Z2", "fZ2", "SU2"):
         return tuple(a)  # self-dual (SU2: "all irreps are self-dual")
+    if kind == "fU1xSU2":
+        return (-a[0], a[1])  # Deligne product: componentwise duals
     return tuple(-x for x in a)
 
 
@@ -38,25 +51,28 @@ def fuse(kind, a, b):
     if kind == "SU2":
         lo, hi = abs(a[0] - b[0]), a[0] + b[0]
         return [(j,) for j in range(lo, hi + 1, 2)]
+    if kind == "fU1xSU2":
+        lo, hi = abs(a[1] - b[1]), a[1] + b[1]
+        return [(a[0] + b[0], j) for j in range(lo, hi + 1, 2)]
     raise ValueError(kind)
 
 
 def qdim(kind, a):
-    return a[0] + 1 if kind == "SU2" else 1
+    return spin2(kind, a) + 1
 
 
 def parity(kind, a):
     """Fermion parity (0 for bosonic kinds). fU1xU1: N mod 2 (BASELINE cfg3)."""
     if kind == "fZ2":
         return a[0] % 2
-    if kind == "fU1xU1":
+    if kind in ("fU1xU1", "fU1xSU2"):
         return a[0] % 2
     return 0
 
 
 def is_fermionic(kind):
-    return kind in ("fZ2", "fU1xU1")
+    return kind in ("fZ2", "fU1xU1", "fU1xSU2")
 
 
 def is_abelian(kind):
-    return kind != "SU2"
+    return kind not in ("SU2", "fU1xSU2")

@@ -70,12 +70,13 @@ tk_status tk_space_parse(const char* text, tk_space** out) {
   std::vector<Sector> secs;
   std::vector<int64_t> degs;
   size_t i = 0;
-  auto parse_num = [&](size_t& j) -> int32_t {  // integer or p/2 (SU2: returns doubled)
+  // integer, or j / p/2 for a spin component (SU2 labels, the second entry of fU1xSU2): returns doubled
+  auto parse_num = [&](size_t& j, bool spin) -> int32_t {
     size_t st = j;
     if (j < body.size() && (body[j] == '-' || body[j] == '+')) ++j;
     while (j < body.size() && std::isdigit((unsigned char)body[j])) ++j;
     long v = std::strtol(body.substr(st, j - st).c_str(), nullptr, 10);
-    if (k == Kind::SU2) {
+    if (spin) {
       if (j < body.size() && body[j] == '/') {
         ++j;
         size_t st2 = j;
@@ -92,14 +93,14 @@ tk_status tk_space_parse(const char* text, tk_space** out) {
     Sector sc;
     if (body[i] == '(') {
       ++i;
-      sc.v[0] = parse_num(i);
+      sc.v[0] = parse_num(i, false);
       if (i >= body.size() || body[i] != ',') TK_THROW(TK_ERR_INVALID_ARGUMENT, "bad tuple label");
       ++i;
-      sc.v[1] = parse_num(i);
+      sc.v[1] = parse_num(i, k == Kind::FU1SU2);
       if (i >= body.size() || body[i] != ')') TK_THROW(TK_ERR_INVALID_ARGUMENT, "bad tuple label");
       ++i;
     } else {
-      sc.v[0] = parse_num(i);
+      sc.v[0] = parse_num(i, k == Kind::SU2);
     }
     if (i >= body.size() || body[i] != ':') TK_THROW(TK_ERR_INVALID_ARGUMENT, "expected ':'");
     ++i;

@@ -9,6 +9,10 @@
 //            R = (-1)^{p_a p_b} (Deligne product of R-symbols)
 //   SU2      N^{j1j2}_{j3}, F via 6j (eq. SU2FSymbol, reading C9),
 //            R^{j1j2}_{j3} = (-1)^{j1+j2-j3} (reading C8), chi_j = (-1)^{2j}
+//   fU1xSU2  Hubbard fZ2 (x) U1 (x) SU2, labels (N, 2j), fermion parity N mod 2 (reading C14
+//            as for fU1xU1): Deligne product data -- fusion componentwise, d = 2j+1,
+//            F = F_SU2 on the spins (U1 and SVect F are trivial), R = R_SU2 * (-1)^{p_a p_b},
+//            chi = (-1)^{2j} (SVect chi = 1)
 // B-symbol: B^{ab}_c = sqrt(d_a d_b / d_c) F^{a b bbar}_a[c, I].
 #include <cmath>
 #include <cstring>
@@ -24,17 +28,20 @@ Kind parse_kind(const std::string& s) {
   if (s == "U1xU1") return Kind::U1U1;
   if (s == "fU1xU1") return Kind::FU1U1;
   if (s == "SU2") return Kind::SU2;
+  if (s == "fU1xSU2") return Kind::FU1SU2;
   TK_THROW(TK_ERR_UNKNOWN_LABEL, "unknown sector kind '" + s + "'");
 }
 
 const char* kind_name(Kind k) {
-  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2"};
+  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2"};
   return names[(int)k];
 }
 
-int kind_width(Kind k) { return (k == Kind::U1U1 || k == Kind::FU1U1) ? 2 : 1; }
-bool kind_abelian(Kind k) { return k != Kind::SU2; }
-bool kind_fermionic(Kind k) { return k == Kind::FZ2 || k == Kind::FU1U1; }
+int kind_width(Kind k) { return (k == Kind::U1U1 || k == Kind::FU1U1 || k == Kind::FU1SU2) ? 2 : 1; }
+bool kind_abelian(Kind k) { return k != Kind::SU2 && k != Kind::FU1SU2; }
+bool kind_fermionic(Kind k) { return k == Kind::FZ2 || k == Kind::FU1U1 || k == Kind::FU1SU2; }
+// doubled spin of the SU(2) factor (0 for kinds without one)
+static int spin2(Kind k, const Sector& a) { return k == Kind::SU2 ? a.v[0] : (k == Kind::FU1SU2 ? a.v[1] : 0); }
 Sector sector_unit(Kind) { return Sector{}; }
 
 Sector sector_dual(Kind k, const Sector& a) {
@@ -45,6 +52,8 @@ Sector sector_dual(Kind k, const Sector& a) {
       return a;  // self-dual (SU2: "all irreps are self-dual")
     case Kind::U1:
       return Sector{{-a.v[0], 0}};
+    case Kind::FU1SU2:
+      return Sector{{-a.v[0], a.v[1]}};
     default:
       return Sector{{-a.v[0], -a.v[1]}};
   }
@@ -62,6 +71,9 @@ void sector_validate(Kind k, const Sector& a) {
       break;
     case Kind::SU2:
       ok = a.v[0] >= 0 && a.v[1] == 0;
+      break;
+    case Kind::FU1SU2:
+      ok = a.v[1] >= 0;
       break;
     default:
       break;
@@ -88,6 +100,11 @@ void sector_fuse(Kind k, const Sector& a, const Sector& b, std::vector<Sector>& 
       for (int j = lo; j <= hi; j += 2) out.push_back(Sector{{j, 0}});
       break;
     }
+    case Kind::FU1SU2: {
+      int lo = std::abs(a.v[1] - b.v[1]), hi = a.v[1] + b.v[1];
+      for (int j = lo; j <= hi; j += 2) out.push_back(Sector{{a.v[0] + b.v[0], j}});
+      break;
+    }
   }
 }
 
@@ -95,22 +112,22 @@ static bool su2_tri(int a, int b, int c) { return std::abs(a - b) <= c && c <= a
 
 bool sector_admissible(Kind k, const Sector& a, const Sector& b, const Sector& c) {
   if (k == Kind::SU2) return su2_tri(a.v[0], b.v[0], c.v[0]);
+  if (k == Kind::FU1SU2) return c.v[0] == a.v[0] + b.v[0] && su2_tri(a.v[1], b.v[1], c.v[1]);
   std::vector<Sector> tmp;
   sector_fuse(k, a, b, tmp);
   return tmp[0] == c;
 }
 
-double sector_dim(Kind k, const Sector& a) { return k == Kind::SU2 ? (double)(a.v[0] + 1) : 1.0; }
+double sector_dim(Kind k, const Sector& a) { return (double)(spin2(k, a) + 1); }
 
 int sector_parity(Kind k, const Sector& a) {
   if (k == Kind::FZ2) return a.v[0] & 1;
-  if (k == Kind::FU1U1) return a.v[0] & 1;  // N mod 2 (works for negative N in two's complement)
+  if (k == Kind::FU1U1 || k == Kind::FU1SU2) return a.v[0] & 1;  // N mod 2 (two's complement: also N < 0)
   return 0;
 }
 
 double sector_fs(Kind k, const Sector& a) {
-  if (k == Kind::SU2) return (a.v[0] & 1) ? -1.0 : 1.0;  // (-1)^{2j}
-  return 1.0;
+  return (spin2(k, a) & 1) ? -1.0 : 1.0;  // (-1)^{2j}; 1 for the abelian kinds and SVect
 }
 
 // ---- SU(2) 6j symbol via the Racah sum, long double factorials (doubled spins).
@@ -153,22 +170,25 @@ double fsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c, const 
   if (!sector_admissible(k, a, b, e) || !sector_admissible(k, e, c, d) || !sector_admissible(k, b, c, f) ||
       !sector_admissible(k, a, f, d))
     return 0.0;
-  if (k != Kind::SU2) return 1.0;  // abelian / SVect: trivial F (eq. trivialF)
-  int j1 = a.v[0], j2 = b.v[0], j3 = c.v[0], j4 = d.v[0], je = e.v[0], jf = f.v[0];
+  if (kind_abelian(k)) return 1.0;  // abelian / SVect: trivial F (eq. trivialF)
+  // SU(2) factor (Deligne product: F is the product of the factors' F)
+  int j1 = spin2(k, a), j2 = spin2(k, b), j3 = spin2(k, c), j4 = spin2(k, d), je = spin2(k, e), jf = spin2(k, f);
   double sg = (((j1 + j2 + j3 + j4) / 2) & 1) ? -1.0 : 1.0;
   return std::sqrt((double)(je + 1) * (double)(jf + 1)) * sg * sixj(j1, j2, je, j3, j4, jf);
 }
 
 double rsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c) {
   if (!sector_admissible(k, a, b, c)) return 0.0;
-  if (k == Kind::SU2) return (((a.v[0] + b.v[0] - c.v[0]) / 2) & 1) ? -1.0 : 1.0;  // reading C8
-  if (kind_fermionic(k)) return (sector_parity(k, a) & sector_parity(k, b)) ? -1.0 : 1.0;
-  return 1.0;
+  double r = 1.0;
+  if (!kind_abelian(k))  // SU(2) factor, reading C8
+    r = (((spin2(k, a) + spin2(k, b) - spin2(k, c)) / 2) & 1) ? -1.0 : 1.0;
+  if (kind_fermionic(k) && (sector_parity(k, a) & sector_parity(k, b))) r = -r;  // SVect factor
+  return r;  // Deligne product of R-symbols
 }
 
 double bsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c) {
   if (!sector_admissible(k, a, b, c)) return 0.0;
-  if (k != Kind::SU2) return 1.0;
+  if (kind_abelian(k)) return 1.0;
   Sector bb = sector_dual(k, b);
   double da = sector_dim(k, a), db = sector_dim(k, b), dc = sector_dim(k, c);
   return std::sqrt(da * db / dc) * fsymbol(k, a, b, bb, a, c, sector_unit(k));

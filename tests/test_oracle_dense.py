@@ -36,6 +36,7 @@ def rand_tensor(kind, cod, dom, seed):
     ("U1", [((-1,), 2), ((0,), 1), ((2,), 3)]),
     ("fU1xU1", [((0, 0), 1), ((1, 1), 2), ((1, -1), 1), ((-1, 1), 2)]),
     ("SU2", [((0,), 2), ((1,), 1), ((2,), 2)]),
+    ("fU1xSU2", [((0, 0), 2), ((1, 1), 1), ((-1, 1), 2), ((2, 0), 1), ((0, 2), 1)]),
 ])
 def test_fuse_dimension(kind, secs):
     # sum_c rows(c) * d_c over ALL coupled sectors == prod of leg dims
@@ -284,3 +285,82 @@ def test_su2_contraction_supported_on_output_layout(cfgfun):
         back = Dn.to_dense(lc_, Dn.from_dense(lc_, out))
         assert C.rel_frobenius(back, out) < 1e-13
         dense[nc] = out
+
+
+# ------------------------------------------------------ fZ2 x U1 x SU2
+def _leg_rep_u1su2(spc, th, phi):
+    """U(1) x SU(2) action on one fU1xSU2 leg: exp(i N phi) (x) D^j(th) per multiplet."""
+    from scipy.linalg import block_diag
+    blocks = []
+    for lab, n in sorted(spc["sectors"]):
+        Dj = np.exp(1j * lab[0] * phi) * _wigner_D(lab[1], th)
+        blocks.extend([Dj] * n)
+    M = block_diag(*blocks)
+    return M.conj() if spc["dual"] else M
+
+
+HUB = [((0, 0), 2), ((1, 1), 1), ((-1, 1), 2), ((2, 0), 1), ((1, 3), 1)]
+
+
+def test_u1su2_equivariance_roundtrip():
+    """Deligne product embedding: the dense tensor is invariant under U(1) x SU(2)
+    (charge phase times Wigner-D on every leg), and from_dense o to_dense = id."""
+    V = sp("fU1xSU2", HUB)
+    P = sp("fU1xSU2", [((0, 0), 1), ((1, 1), 1), ((2, 0), 1)])
+    th, phi = np.array([0.4, -0.9, 1.3]), 0.77
+    for cod, dom in (([V, P], [V]), ([V, W.dual(V)], [P]), ([W.dual(P), V], [V, W.dual(P)])):
+        lt, x = rand_tensor("fU1xSU2", cod, dom, 21)
+        D = Dn.to_dense(lt, x)
+        assert np.abs(Dn.from_dense(lt, D) - x).max() < 1e-13
+        Mc = np.ones((1, 1))
+        for s_ in cod:
+            Mc = np.kron(Mc, _leg_rep_u1su2(s_, th, phi))
+        Md = np.ones((1, 1))
+        for s_ in dom:
+            Md = np.kron(Md, _leg_rep_u1su2(s_, th, phi))
+        T = D.reshape(Mc.shape[0], Md.shape[0])
+        assert np.abs(Mc @ T - T @ Md).max() < 1e-12
+
+
+def test_u1su2_even_charges_reduce_to_su2():
+    """Bosonic limit of the product: with every charge even the fermionic Alg. 4 contraction equals the
+    plain einsum, and the dense embedding equals the SU(2) one (same reduced values, same CG)."""
+    # sectors listed so that the (N, 2j) order equals the 2j order: both legs index the same basis
+    Vh = sp("fU1xSU2", [((0, 0), 2), ((2, 2), 1), ((4, 4), 1)])
+    Vs = sp("SU2", [((0,), 2), ((2,), 1), ((4,), 1)])  # the same spins, charges dropped
+    la, xa = rand_tensor("fU1xSU2", [Vh, Vh], [Vh], 31)
+    ls, xs = rand_tensor("SU2", [Vs, Vs], [Vs], 31)
+    Dh, Ds = Dn.to_dense(la, xa), Dn.to_dense(ls, xs)
+    assert Dh.shape == Ds.shape
+    lb, xb = rand_tensor("fU1xSU2", [Vh], [Vh, W.dual(Vh)], 32)
+    B = Dn.to_dense(lb, xb)
+    r1 = C.contract_alg4(Dh, [Vh, Vh, Vh], 2, [1, 2, 3], B, [Vh, Vh, W.dual(Vh)], 1, [3, 4, 5], [2, 5, 1, 4], 2)
+    r2 = C.contract_einsum(Dh, [1, 2, 3], B, [3, 4, 5], [2, 5, 1, 4])
+    assert C.rel_frobenius(r1, r2) < 1e-14
+    # where the U(1) charges allow a block, the fU1xSU2 tensor IS an SU(2) intertwiner: its dense array
+    # is supported on the SU(2) layout of the same legs (projection onto the SU(2) basis loses nothing)
+    back = Dn.to_dense(ls, Dn.from_dense(ls, Dh))
+    assert C.rel_frobenius(back, Dh) < 1e-13
+
+
+def test_u1su2_fermion_permute_inverse():
+    rng = np.random.default_rng(8)
+    V = sp("fU1xSU2", HUB)
+    cod, dom = [V, W.dual(V)], [V, V]
+    lt, x = rand_tensor("fU1xSU2", cod, dom, 33)
+    D = Dn.to_dense(lt, x)
+    par = [Dn.parity_vector(s_) for s_ in cod + dom]
+    N, n1 = 4, 2
+    for _ in range(10):
+        perm = list(rng.permutation(N))
+        k = int(rng.integers(0, N + 1))
+        p, q = perm[:k], perm[k:]
+        Pd = C.permute_dense(D, par, n1, p, q)
+        order = p + q
+        inv = [order.index(i) for i in range(N)]
+        back = C.permute_dense(Pd, [par[i] for i in order], k, inv[:n1], inv[n1:])
+        assert np.array_equal(back, D)
+        # the permuted dense tensor is again an intertwiner of the permuted HomSpace
+        c2, d2 = C.permuted_spaces(cod, dom, p, q)
+        l2 = L.homspace_layout("fU1xSU2", c2, d2)
+        assert C.rel_frobenius(Dn.to_dense(l2, Dn.from_dense(l2, Pd)), Pd) < 1e-13

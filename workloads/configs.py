@@ -160,4 +160,23 @@ def cfg6(mults=(24, 40, 40, 32, 24, 12, 6)):
     }
 
 
-CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6}
+# ------------------------- config 7 (non-abelian fermionic Hubbard, fZ2 x U1 x SU2)
+def _u1su2_bond(n_mult, sigma_n=2.5, sigma_j=1.5):
+    """Multiplets (N, 2j) with N = -6..6, 2j = 0..6 and N = 2j (mod 2) (the sectors a Hubbard chain
+    reaches from the physical space), multiplicities ~ exp(-N^2/2s_N^2 - j^2/2s_j^2) by reading C15."""
+    labels = [(n, tj) for n in range(-6, 7) for tj in range(0, 7) if (n - tj) % 2 == 0]
+    weights = [math.exp(-n * n / (2 * sigma_n ** 2) - (tj / 2) ** 2 / (2 * sigma_j ** 2)) for n, tj in labels]
+    return gaussian_degeneracies(labels, weights, n_mult, lambda l: abs(l[0]) + l[1])
+
+
+def cfg7(n_mult=700):
+    """Hubbard two-site update with fZ2 x U1 x SU2, the cfg3 chain with the spin promoted
+    to SU(2): P = (0,0) + (1,1/2) + (2,0) (dim 4); W = 2 (0,0) + 2 (1,1/2) + 2 (-1,1/2) (dim 10: the
+    cfg3 channels of reading C18 grouped into doublets); V: 700 multiplets, dim 2058 (~ cfg3's 2048)."""
+    P = space("fU1xSU2", [((0, 0), 1), ((1, 1), 1), ((2, 0), 1)])
+    W = space("fU1xSU2", [((0, 0), 2), ((1, 1), 2), ((-1, 1), 2)])
+    V = space("fU1xSU2", _u1su2_bond(n_mult))
+    return _dmrg_chain(7, "fU1xSU2", P, W, V)
+
+
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6, 7: cfg7}
