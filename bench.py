@@ -178,6 +178,24 @@ def run_reference(args):
     return 0
 
 
+# --------------------------------------------------------------------------- multi-rank plumbing
+def max_over_ranks(x, world, device=None):
+    """Max of a per-rank device time over all ranks (the contract's max-over-ranks timing)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_gflops(flops_per_step, steps, world, total_ms):
+    """Replicas only: every rank runs the same workload; value = all ranks' flops /
+    the slowest rank's time (weak scaling)."""
+    return world * flops_per_step * steps / (total_ms * 1e-3) / 1e9
+
+
 # --------------------------------------------------------------------------- GPU
 def run_gpu(args):
     import torch
@@ -250,12 +268,9 @@ def run_gpu(args):
         dist.barrier()
     total_ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, world, dev)
     ms_step = total_ms / args.steps
-    value = world * flops * args.steps / (total_ms * 1e-3) / 1e9
+    value = whole_job_gflops(flops, args.steps, world, total_ms)
 
     # ---- end to end through the public call with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -274,11 +289,8 @@ def run_gpu(args):
         x1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = x0.elapsed_time(x1)
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": round(world * flops * args.e2e_steps / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+        e2e_ms = max_over_ranks(e2e_ms, world, dev)
+        e2e = {"value": round(whole_job_gflops(flops, args.e2e_steps, world, e2e_ms), 2), "unit": "GFLOP/s",
                "h2d_bytes_per_step": int((A.nelems + B.nelems) * esz), "d2h_bytes_per_step": int(C.nelems * esz),
                "ms_per_step": round(e2e_ms / args.e2e_steps, 2)}
 
