@@ -36,21 +36,57 @@ def leg_basis(sp):
     return out, off
 
 
-def _splitting_tensor(kind, uncoupled, inner, coupled):
-    """X[mu_1..mu_N, mu_c] for the canonical left-to-right SU(2) tree (doubled spins of the SU(2)
-    factor; a U(1) factor is one-dimensional and only selects the sector)."""
-    j = lambda lab: sectors.spin2(kind, lab)  # noqa: E731
-    n = len(uncoupled)
+def _splitting_tensor_su2(js_unc, js_chain):
+    """X[mu_1..mu_N, mu_c] of ONE SU(2) factor along the canonical left-to-right tree (doubled spins;
+    js_chain = inner labels then the coupled label)."""
+    n = len(js_unc)
     if n == 0:
         return np.ones((1,))
     if n == 1:
-        return np.eye(j(uncoupled[0]) + 1)
-    chain = list(inner) + [coupled]
-    X = su2.cg_tensor(j(uncoupled[0]), j(uncoupled[1]), j(chain[0]))
+        return np.eye(js_unc[0] + 1)
+    X = su2.cg_tensor(js_unc[0], js_unc[1], js_chain[0])
     for k in range(2, n):
-        C = su2.cg_tensor(j(chain[k - 2]), j(uncoupled[k]), j(chain[k - 1]))
+        C = su2.cg_tensor(js_chain[k - 2], js_unc[k], js_chain[k - 1])
         X = np.tensordot(X, C, axes=([X.ndim - 1], [0]))
     return X
+
+
+def _kron_axes(Xs):
+    """Per-axis Kronecker product of equal-rank tensors: index mu = (mu_1 * d_2 + mu_2) per axis."""
+    X = Xs[0]
+    for Y in Xs[1:]:
+        nd = X.ndim
+        Z = np.multiply.outer(X, Y)
+        Z = Z.transpose([a for k in range(nd) for a in (k, nd + k)])
+        X = Z.reshape([X.shape[k] * Y.shape[k] for k in range(nd)])
+    return X
+
+
+def _splitting_tensor(kind, uncoupled, inner, coupled):
+    """X[mu_1..mu_N, mu_c] for the canonical left-to-right tree: the Kronecker product over the
+    SU(2) factors of the kind (Deligne product); a U(1) factor is one-dimensional and
+    only selects the sector."""
+    chain = list(inner) + [coupled]
+    nf = len(sectors.spins2(kind, coupled))
+    parts = []
+    for f in range(nf):
+        js_unc = [sectors.spins2(kind, a)[f] for a in uncoupled]
+        js_chain = [sectors.spins2(kind, a)[f] for a in chain]
+        parts.append(_splitting_tensor_su2(js_unc, js_chain))
+    return _kron_axes(parts)
+
+
+def _z_flip(kind, X, axis, lab):
+    """Z (reading C7) on one leg: the Kronecker product of the factors' Z."""
+    js = sectors.spins2(kind, lab)
+    if len(js) == 1:
+        return su2.z_flip(X, axis, js[0])
+    dims = [j + 1 for j in js]
+    sh = list(X.shape)
+    Y = X.reshape(sh[:axis] + dims + sh[axis + 1:])
+    for f, j in enumerate(js):
+        Y = su2.z_flip(Y, axis + f, j)
+    return Y.reshape(sh)
 
 
 def basis_tensor(kind, cod, dom, key):
@@ -60,10 +96,10 @@ def basis_tensor(kind, cod, dom, key):
     Xf = _splitting_tensor(kind, f_unc, f_inn, c)
     for k, sp in enumerate(cod):
         if sp["dual"]:
-            Xs = su2.z_flip(Xs, k, sectors.spin2(kind, s_unc[k]))
+            Xs = _z_flip(kind, Xs, k, s_unc[k])
     for k, sp in enumerate(dom):
         if sp["dual"]:
-            Xf = su2.z_flip(Xf, k, sectors.spin2(kind, f_unc[k]))
+            Xf = _z_flip(kind, Xf, k, f_unc[k])
     return np.tensordot(Xs, Xf, axes=([Xs.ndim - 1], [Xf.ndim - 1]))
 
 

@@ -10,22 +10,32 @@ Labels are tuples of ints:
                     P:2303-2312
   fU1xSU2 (N, 2j)   Hubbard fZ2 x U1 x SU2 as a Deligne product:
                     charges add, spins by the SU2 rule, d = 2j+1, fermion parity N mod 2 (reading C14)
+  fSU2xSU2 (2jc, 2js) Hubbard at half filling, fZ2 x SU2(charge) x SU2(spin): both
+                    factors by the SU2 rule, d = (2jc+1)(2js+1), fermion parity 2js mod 2
 """
 
-KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2")
+KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2", "fSU2xSU2")
 
 
 def width(kind):
-    return 2 if kind in ("U1xU1", "fU1xU1", "fU1xSU2") else 1
+    return 2 if kind in ("U1xU1", "fU1xU1", "fU1xSU2", "fSU2xSU2") else 1
+
+
+def spins2(kind, a):
+    """Doubled spins of the SU(2) factors of a label, in factor order ([] for abelian kinds)."""
+    if kind == "SU2":
+        return [a[0]]
+    if kind == "fU1xSU2":
+        return [a[1]]
+    if kind == "fSU2xSU2":
+        return [a[0], a[1]]
+    return []
 
 
 def spin2(kind, a):
-    """Doubled spin of the SU(2) factor of a label (0 for kinds without one)."""
-    if kind == "SU2":
-        return a[0]
-    if kind == "fU1xSU2":
-        return a[1]
-    return 0
+    """Doubled spin of the single SU(2) factor (0 for kinds without one)."""
+    js = spins2(kind, a)
+    return js[0] if js else 0
 
 
 def unit(kind):
@@ -33,7 +43,7 @@ def unit(kind):
 
 
 def dual(kind, a):
-    if kind in ("Z2", "fZ2", "SU2"):
+    if kind in ("Z2", "fZ2", "SU2", "fSU2xSU2"):
         return tuple(a)  # self-dual (SU2: "all irreps are self-dual")
     if kind == "fU1xSU2":
         return (-a[0], a[1])  # Deligne product: componentwise duals
@@ -54,11 +64,17 @@ def fuse(kind, a, b):
     if kind == "fU1xSU2":
         lo, hi = abs(a[1] - b[1]), a[1] + b[1]
         return [(a[0] + b[0], j) for j in range(lo, hi + 1, 2)]
+    if kind == "fSU2xSU2":
+        return [(jc, js) for jc in range(abs(a[0] - b[0]), a[0] + b[0] + 1, 2)
+                for js in range(abs(a[1] - b[1]), a[1] + b[1] + 1, 2)]
     raise ValueError(kind)
 
 
 def qdim(kind, a):
-    return spin2(kind, a) + 1
+    d = 1
+    for j in spins2(kind, a):
+        d *= j + 1
+    return d
 
 
 def parity(kind, a):
@@ -67,12 +83,14 @@ def parity(kind, a):
         return a[0] % 2
     if kind in ("fU1xU1", "fU1xSU2"):
         return a[0] % 2
+    if kind == "fSU2xSU2":
+        return a[1] % 2
     return 0
 
 
 def is_fermionic(kind):
-    return kind in ("fZ2", "fU1xU1", "fU1xSU2")
+    return kind in ("fZ2", "fU1xU1", "fU1xSU2", "fSU2xSU2")
 
 
 def is_abelian(kind):
-    return kind not in ("SU2", "fU1xSU2")
+    return kind not in ("SU2", "fU1xSU2", "fSU2xSU2")

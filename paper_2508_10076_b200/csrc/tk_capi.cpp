@@ -93,10 +93,10 @@ tk_status tk_space_parse(const char* text, tk_space** out) {
     Sector sc;
     if (body[i] == '(') {
       ++i;
-      sc.v[0] = parse_num(i, false);
+      sc.v[0] = parse_num(i, k == Kind::FSU2SU2);
       if (i >= body.size() || body[i] != ',') TK_THROW(TK_ERR_INVALID_ARGUMENT, "bad tuple label");
       ++i;
-      sc.v[1] = parse_num(i, k == Kind::FU1SU2);
+      sc.v[1] = parse_num(i, k == Kind::FU1SU2 || k == Kind::FSU2SU2);
       if (i >= body.size() || body[i] != ')') TK_THROW(TK_ERR_INVALID_ARGUMENT, "bad tuple label");
       ++i;
     } else {

@@ -25,8 +25,8 @@ void set_last_error(const std::string& m);
 // ------------------------------------------------------------------ sectors
 // Sector kinds (P:1011-1022 Z2; P:2347-2362 SVect; U1 S:138; Deligne products P:2380-2412;
 // SU(2) P:2303-2332). Labels are up to two int32: Z2/fZ2 {g}, U1 {q}, U1xU1 {N, 2Sz}, SU2 {2j},
-// fU1xSU2 {N, 2j}.
-enum class Kind : int { Z2 = 0, FZ2 = 1, U1 = 2, U1U1 = 3, FU1U1 = 4, SU2 = 5, FU1SU2 = 6 };
+// fU1xSU2 {N, 2j}, fSU2xSU2 {2j_charge, 2j_spin}.
+enum class Kind : int { Z2 = 0, FZ2 = 1, U1 = 2, U1U1 = 3, FU1U1 = 4, SU2 = 5, FU1SU2 = 6, FSU2SU2 = 7 };
 
 struct Sector {
   int32_t v[2] = {0, 0};

@@ -186,25 +186,33 @@ __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typena
   FastDiv fd;
   fd.init((uint32_t)n0);
   const uint32_t total = (uint32_t)cnt * (uint32_t)n0;
+  // destinations in chunks of kRegMembers accumulators; every source element is read once per chunk
+  // (once in total for groups of <= 8 destinations, e.g. all of cfg5; re-reads hit L1 otherwise)
   for (uint32_t e = tid; e < total; e += kPermThreads) {
     uint32_t r = fd.div(e);
     uint32_t i0 = e - r * (uint32_t)n0;
-    V x[kMaxGroupMembers];
+    for (int j0 = 0; j0 < kd; j0 += kRegMembers) {
+      V acc[kRegMembers];
 #pragma unroll
-    for (int i = 0; i < kMaxGroupMembers; ++i)
-      if (i < ks) {
-        int64_t ld = sh.mld[i];
-        x[i] = IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]), sh.md1[i]);
+      for (int jj = 0; jj < kRegMembers; ++jj) acc[jj] = Num<V>::zero();
+#pragma unroll 4
+      for (int i = 0; i < ks; ++i) {
+        const int64_t ld = sh.mld[i];
+        const V x =
+            IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]), sh.md1[i]);
+        const double* cr = sh.coef + i * kd + j0;
+#pragma unroll
+        for (int jj = 0; jj < kRegMembers; ++jj)
+          if (j0 + jj < kd) acc[jj] = Num<V>::axpy(cr[jj], x, acc[jj]);
       }
-    for (int j = 0; j < kd; ++j) {
-      V acc = Num<V>::zero();
 #pragma unroll
-      for (int i = 0; i < kMaxGroupMembers; ++i)
-        if (i < ks) acc = Num<V>::axpy(sh.coef[i * kd + j], x[i], acc);
-      const int jm = kMaxGroupMembers + j;
-      int64_t ld = sh.mld[jm];
-      IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]), sh.md1[jm],
-                sh.md2[jm], Num<V>::scale(alpha, acc), beta, ims);
+      for (int jj = 0; jj < kRegMembers; ++jj)
+        if (j0 + jj < kd) {
+          const int jm = kMaxGroupMembers + j0 + jj;
+          const int64_t ld = sh.mld[jm];
+          IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]),
+                    sh.md1[jm], sh.md2[jm], Num<V>::scale(alpha, acc[jj]), beta, ims);
+        }
     }
   }
 }
@@ -392,7 +400,7 @@ __device__ void permute_tiled(const typename CIO<CM>::S* __restrict__ src, typen
 __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMember* __restrict__ members,
                                                 const double* __restrict__ coefs, PermShared& sh) {
   const int tid = threadIdx.x;
-  if (tid < g.ksrc * g.kdst) sh.coef[tid] = coefs[g.coef_off + tid];
+  for (int i = tid; i < g.ksrc * g.kdst; i += kPermThreads) sh.coef[i] = coefs[g.coef_off + i];
   if (tid < g.ksrc) {
     const PermMember m = members[g.src_mem + tid];
     sh.moff[tid] = m.off;

@@ -7,7 +7,8 @@
 namespace tk {
 
 constexpr int kMaxLegs = 8;
-constexpr int kMaxGroupMembers = 8;  // k_src, k_dst of one recoupling group (SU(2) cfg5: <= 3)
+constexpr int kMaxGroupMembers = 32;  // k_src, k_dst of one recoupling group (cfg5: <= 3; fSU2xSU2 rank 4: > 8)
+constexpr int kRegMembers = 8;        // destinations accumulated in registers per pass
 
 // One uncoupled-charge group of a permute (Alg. 10): y_j = alpha * sum_i M[i][j] perm(x_i) + beta * y_j.
 // Legs are listed in DESTINATION order after dropping extent-1 legs and merging legs that are

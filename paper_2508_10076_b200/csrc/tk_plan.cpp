@@ -386,7 +386,7 @@ void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vect
         }
       }
       if ((int)srcs.size() > kMaxGroupMembers || (int)dsts.size() > kMaxGroupMembers)
-        TK_THROW(TK_ERR_UNSUPPORTED, "recoupling group larger than 8 tree pairs");
+        TK_THROW(TK_ERR_UNSUPPORTED, "recoupling group larger than 32 tree pairs");
       PermGroup g{};
       g.ksrc = (int)srcs.size();
       g.kdst = (int)dsts.size();

@@ -13,6 +13,10 @@
 //            as for fU1xU1): Deligne product data -- fusion componentwise, d = 2j+1,
 //            F = F_SU2 on the spins (U1 and SVect F are trivial), R = R_SU2 * (-1)^{p_a p_b},
 //            chi = (-1)^{2j} (SVect chi = 1)
+//   fSU2xSU2 Hubbard at half filling, fZ2 (x) SU2 (x) SU2 (charge and spin SU(2)): labels
+//            (2j_charge, 2j_spin), fermion parity 2j_spin mod 2 (the singly occupied spin-1/2 site is odd,
+//            the empty/doubly occupied charge doublet even); Deligne product data: F = F(charge) F(spin),
+//            R = R(charge) R(spin) (-1)^{p_a p_b}, d = (2jc+1)(2js+1), chi = (-1)^{2jc+2js}
 // B-symbol: B^{ab}_c = sqrt(d_a d_b / d_c) F^{a b bbar}_a[c, I].
 #include <cmath>
 #include <cstring>
@@ -29,19 +33,31 @@ Kind parse_kind(const std::string& s) {
   if (s == "fU1xU1") return Kind::FU1U1;
   if (s == "SU2") return Kind::SU2;
   if (s == "fU1xSU2") return Kind::FU1SU2;
+  if (s == "fSU2xSU2") return Kind::FSU2SU2;
   TK_THROW(TK_ERR_UNKNOWN_LABEL, "unknown sector kind '" + s + "'");
 }
 
 const char* kind_name(Kind k) {
-  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2"};
+  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2", "fSU2xSU2"};
   return names[(int)k];
 }
 
-int kind_width(Kind k) { return (k == Kind::U1U1 || k == Kind::FU1U1 || k == Kind::FU1SU2) ? 2 : 1; }
-bool kind_abelian(Kind k) { return k != Kind::SU2 && k != Kind::FU1SU2; }
-bool kind_fermionic(Kind k) { return k == Kind::FZ2 || k == Kind::FU1U1 || k == Kind::FU1SU2; }
-// doubled spin of the SU(2) factor (0 for kinds without one)
-static int spin2(Kind k, const Sector& a) { return k == Kind::SU2 ? a.v[0] : (k == Kind::FU1SU2 ? a.v[1] : 0); }
+int kind_width(Kind k) {
+  return (k == Kind::U1U1 || k == Kind::FU1U1 || k == Kind::FU1SU2 || k == Kind::FSU2SU2) ? 2 : 1;
+}
+bool kind_abelian(Kind k) { return k != Kind::SU2 && k != Kind::FU1SU2 && k != Kind::FSU2SU2; }
+bool kind_fermionic(Kind k) {
+  return k == Kind::FZ2 || k == Kind::FU1U1 || k == Kind::FU1SU2 || k == Kind::FSU2SU2;
+}
+// doubled spins of the SU(2) factors of a label (n = number of factors: 0, 1 or 2)
+static int spins2(Kind k, const Sector& a, int* j) {
+  switch (k) {
+    case Kind::SU2: j[0] = a.v[0]; return 1;
+    case Kind::FU1SU2: j[0] = a.v[1]; return 1;
+    case Kind::FSU2SU2: j[0] = a.v[0]; j[1] = a.v[1]; return 2;
+    default: return 0;
+  }
+}
 Sector sector_unit(Kind) { return Sector{}; }
 
 Sector sector_dual(Kind k, const Sector& a) {
@@ -49,6 +65,7 @@ Sector sector_dual(Kind k, const Sector& a) {
     case Kind::Z2:
     case Kind::FZ2:
     case Kind::SU2:
+    case Kind::FSU2SU2:
       return a;  // self-dual (SU2: "all irreps are self-dual")
     case Kind::U1:
       return Sector{{-a.v[0], 0}};
@@ -74,6 +91,9 @@ void sector_validate(Kind k, const Sector& a) {
       break;
     case Kind::FU1SU2:
       ok = a.v[1] >= 0;
+      break;
+    case Kind::FSU2SU2:
+      ok = a.v[0] >= 0 && a.v[1] >= 0;
       break;
     default:
       break;
@@ -105,6 +125,11 @@ void sector_fuse(Kind k, const Sector& a, const Sector& b, std::vector<Sector>& 
       for (int j = lo; j <= hi; j += 2) out.push_back(Sector{{a.v[0] + b.v[0], j}});
       break;
     }
+    case Kind::FSU2SU2: {
+      for (int jc = std::abs(a.v[0] - b.v[0]); jc <= a.v[0] + b.v[0]; jc += 2)
+        for (int js = std::abs(a.v[1] - b.v[1]); js <= a.v[1] + b.v[1]; js += 2) out.push_back(Sector{{jc, js}});
+      break;
+    }
   }
 }
 
@@ -113,21 +138,32 @@ static bool su2_tri(int a, int b, int c) { return std::abs(a - b) <= c && c <= a
 bool sector_admissible(Kind k, const Sector& a, const Sector& b, const Sector& c) {
   if (k == Kind::SU2) return su2_tri(a.v[0], b.v[0], c.v[0]);
   if (k == Kind::FU1SU2) return c.v[0] == a.v[0] + b.v[0] && su2_tri(a.v[1], b.v[1], c.v[1]);
+  if (k == Kind::FSU2SU2) return su2_tri(a.v[0], b.v[0], c.v[0]) && su2_tri(a.v[1], b.v[1], c.v[1]);
   std::vector<Sector> tmp;
   sector_fuse(k, a, b, tmp);
   return tmp[0] == c;
 }
 
-double sector_dim(Kind k, const Sector& a) { return (double)(spin2(k, a) + 1); }
+double sector_dim(Kind k, const Sector& a) {
+  int j[2] = {0, 0};
+  int n = spins2(k, a, j);
+  double d = 1.0;
+  for (int i = 0; i < n; ++i) d *= (double)(j[i] + 1);
+  return d;
+}
 
 int sector_parity(Kind k, const Sector& a) {
   if (k == Kind::FZ2) return a.v[0] & 1;
   if (k == Kind::FU1U1 || k == Kind::FU1SU2) return a.v[0] & 1;  // N mod 2 (two's complement: also N < 0)
+  if (k == Kind::FSU2SU2) return a.v[1] & 1;                       // 2 j_spin mod 2
   return 0;
 }
 
 double sector_fs(Kind k, const Sector& a) {
-  return (spin2(k, a) & 1) ? -1.0 : 1.0;  // (-1)^{2j}; 1 for the abelian kinds and SVect
+  int j[2] = {0, 0};
+  int n = spins2(k, a, j), t = 0;
+  for (int i = 0; i < n; ++i) t += j[i];
+  return (t & 1) ? -1.0 : 1.0;  // prod (-1)^{2j}; 1 for the abelian kinds and SVect
 }
 
 // ---- SU(2) 6j symbol via the Racah sum, long double factorials (doubled spins).
@@ -171,17 +207,31 @@ double fsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c, const 
       !sector_admissible(k, a, f, d))
     return 0.0;
   if (kind_abelian(k)) return 1.0;  // abelian / SVect: trivial F (eq. trivialF)
-  // SU(2) factor (Deligne product: F is the product of the factors' F)
-  int j1 = spin2(k, a), j2 = spin2(k, b), j3 = spin2(k, c), j4 = spin2(k, d), je = spin2(k, e), jf = spin2(k, f);
-  double sg = (((j1 + j2 + j3 + j4) / 2) & 1) ? -1.0 : 1.0;
-  return std::sqrt((double)(je + 1) * (double)(jf + 1)) * sg * sixj(j1, j2, je, j3, j4, jf);
+  // SU(2) factors (Deligne product: F is the product of the factors' F)
+  int ja[2], jb[2], jc[2], jd[2], je[2], jf[2];
+  int n = spins2(k, a, ja);
+  spins2(k, b, jb);
+  spins2(k, c, jc);
+  spins2(k, d, jd);
+  spins2(k, e, je);
+  spins2(k, f, jf);
+  double r = 1.0;
+  for (int i = 0; i < n; ++i) {
+    double sg = (((ja[i] + jb[i] + jc[i] + jd[i]) / 2) & 1) ? -1.0 : 1.0;
+    r *= std::sqrt((double)(je[i] + 1) * (double)(jf[i] + 1)) * sg * sixj(ja[i], jb[i], je[i], jc[i], jd[i], jf[i]);
+  }
+  return r;
 }
 
 double rsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c) {
   if (!sector_admissible(k, a, b, c)) return 0.0;
   double r = 1.0;
-  if (!kind_abelian(k))  // SU(2) factor, reading C8
-    r = (((spin2(k, a) + spin2(k, b) - spin2(k, c)) / 2) & 1) ? -1.0 : 1.0;
+  int ja[2], jb[2], jc[2];
+  int n = spins2(k, a, ja);
+  spins2(k, b, jb);
+  spins2(k, c, jc);
+  for (int i = 0; i < n; ++i)  // SU(2) factors, reading C8
+    if (((ja[i] + jb[i] - jc[i]) / 2) & 1) r = -r;
   if (kind_fermionic(k) && (sector_parity(k, a) & sector_parity(k, b))) r = -r;  // SVect factor
   return r;  // Deligne product of R-symbols
 }

@@ -41,9 +41,10 @@ def rel_err_blocks(layout, flat, blocks, keys=None):
 @pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=96), lambda: W.cfg4(d_leg=32),
                                     lambda: W.cfg5(), lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1)),
                                     lambda: W.cfg6(), lambda: W.cfg6(mults=(3, 4, 3, 2, 2, 1, 1)),
-                                    lambda: W.cfg7(n_mult=50), lambda: W.cfg7(n_mult=24)],
+                                    lambda: W.cfg7(n_mult=50), lambda: W.cfg7(n_mult=24),
+                                    lambda: W.cfg8(n_mult=30), lambda: W.cfg8(n_mult=12)],
                          ids=["cfg1", "cfg2", "cfg3_chi96", "cfg4_d32", "cfg5", "cfg5_small", "cfg6", "cfg6_small",
-                              "cfg7_m50", "cfg7_m24"])
+                              "cfg7_m50", "cfg7_m24", "cfg8_m30", "cfg8_m12"])
 def test_chain_dense_oracle(cfgfun):
     cfg = cfgfun()
     ref = H.oracle_chain_dense(cfg)
@@ -107,8 +108,10 @@ def test_cfg4_full_size_sampled():
 # ------------------------------------------------------------------ ComplexF64 (cfg4 names it)
 @pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=24),
                                     lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1)),
-                                    lambda: W.cfg6(mults=(3, 4, 3, 2, 2, 1, 1)), lambda: W.cfg7(n_mult=24)],
-                         ids=["cfg1", "cfg2", "cfg3_chi64", "cfg4_d24", "cfg5_small", "cfg6_small", "cfg7_m24"])
+                                    lambda: W.cfg6(mults=(3, 4, 3, 2, 2, 1, 1)), lambda: W.cfg7(n_mult=24),
+                                    lambda: W.cfg8(n_mult=12)],
+                         ids=["cfg1", "cfg2", "cfg3_chi64", "cfg4_d24", "cfg5_small", "cfg6_small", "cfg7_m24",
+                              "cfg8_m12"])
 def test_chain_complex_dense_oracle(cfgfun):
     """ComplexF64 through the real-representation GEMM (reading C21) against the dense oracle."""
     cfg = cfgfun()
@@ -202,6 +205,7 @@ def _perm_case(kind, secs, cod_d, dom_d, p, q, alpha=1.0, beta=0.0, seed=0):
     ("SU2", [((0,), 5), ((1,), 3), ((2,), 4), ((3,), 2)]),
     ("Z2", [((0,), 37), ((1,), 29)]),
     ("fU1xSU2", [((0, 0), 5), ((1, 1), 3), ((-1, 1), 4), ((2, 0), 2), ((1, 3), 2)]),
+    ("fSU2xSU2", [((0, 0), 4), ((1, 1), 3), ((0, 2), 2), ((2, 0), 2), ((1, 0), 2), ((0, 1), 3)]),
 ])
 def test_permute_random(kind, secs):
     rng = np.random.default_rng(11)
@@ -211,7 +215,7 @@ def test_permute_random(kind, secs):
         duals = [bool(x) for x in rng.integers(0, 2, N)]
         perm = list(rng.permutation(N))
         k = int(rng.integers(0, N + 1))
-        if kind in ("SU2", "fU1xSU2") and N > 3:
+        if kind in ("SU2", "fU1xSU2", "fSU2xSU2") and N > 3:
             continue
         err = _perm_case(kind, secs, duals[:n1], duals[n1:], perm[:k], perm[k:],
                          alpha=float(rng.choice([1.0, -2.0])), beta=float(rng.choice([0.0, 0.5])), seed=trial)

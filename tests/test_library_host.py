@@ -56,7 +56,8 @@ def assert_same_layout(spec):
 
 
 @pytest.mark.parametrize("cfgfun", [W.cfg1, lambda: W.cfg2(), lambda: W.cfg3(chi=256), lambda: W.cfg4(d_leg=64),
-                                    lambda: W.cfg5(), lambda: W.cfg6(), lambda: W.cfg7(n_mult=200)])
+                                    lambda: W.cfg5(), lambda: W.cfg6(), lambda: W.cfg7(n_mult=200),
+                                    lambda: W.cfg8(n_mult=60)])
 def test_layout_equals_oracle(cfgfun):
     cfg = cfgfun()
     for name, (spec, _) in cfg["tensors"].items():
@@ -135,6 +136,8 @@ def _random_perms(N, rng, n):
     ("U1", [((-1,), 1), ((0,), 1), ((1,), 1)]),
     ("fU1xSU2", [((0, 0), 1), ((1, 1), 1), ((-1, 1), 1), ((2, 0), 1)]),
     ("fU1xSU2", [((0, 2), 1), ((1, 1), 1), ((-1, 3), 1)]),
+    ("fSU2xSU2", [((0, 0), 1), ((1, 1), 1), ((0, 2), 1)]),
+    ("fSU2xSU2", [((0, 1), 1), ((1, 0), 1), ((2, 2), 1)]),
 ])
 def test_transfer_random_vs_oracle(kind, secs):
     rng = np.random.default_rng(42)
@@ -186,7 +189,8 @@ def test_error_statuses():
 
 @pytest.mark.parametrize("cfgfun", [W.cfg1, lambda: W.cfg2(chi=64), lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=32),
                                     lambda: W.cfg5(mults=(2, 2, 1, 1, 1, 1, 1)),
-                                    lambda: W.cfg6(mults=(2, 2, 1, 1, 1, 1, 1)), lambda: W.cfg7(n_mult=60)])
+                                    lambda: W.cfg6(mults=(2, 2, 1, 1, 1, 1, 1)), lambda: W.cfg7(n_mult=60),
+                                    lambda: W.cfg8(n_mult=20)])
 def test_contract_output_spaces(cfgfun):
     cfg = cfgfun()
     specs = {k: v[0] for k, v in cfg["tensors"].items()}

@@ -37,6 +37,7 @@ def rand_tensor(kind, cod, dom, seed):
     ("fU1xU1", [((0, 0), 1), ((1, 1), 2), ((1, -1), 1), ((-1, 1), 2)]),
     ("SU2", [((0,), 2), ((1,), 1), ((2,), 2)]),
     ("fU1xSU2", [((0, 0), 2), ((1, 1), 1), ((-1, 1), 2), ((2, 0), 1), ((0, 2), 1)]),
+    ("fSU2xSU2", [((0, 0), 2), ((1, 1), 1), ((0, 2), 1), ((2, 0), 1), ((1, 3), 1)]),
 ])
 def test_fuse_dimension(kind, secs):
     # sum_c rows(c) * d_c over ALL coupled sectors == prod of leg dims
@@ -363,4 +364,75 @@ def test_u1su2_fermion_permute_inverse():
         # the permuted dense tensor is again an intertwiner of the permuted HomSpace
         c2, d2 = C.permuted_spaces(cod, dom, p, q)
         l2 = L.homspace_layout("fU1xSU2", c2, d2)
+        assert C.rel_frobenius(Dn.to_dense(l2, Dn.from_dense(l2, Pd)), Pd) < 1e-13
+
+
+# --------------------------------------------- fZ2 x SU2 x SU2 (half filling)
+SO4 = [((0, 0), 2), ((1, 1), 1), ((0, 2), 1), ((2, 0), 2), ((1, 3), 1)]
+
+
+def _leg_rep_su2su2(spc, thc, ths):
+    from scipy.linalg import block_diag
+    blocks = []
+    for lab, n in sorted(spc["sectors"]):
+        blocks.extend([np.kron(_wigner_D(lab[0], thc), _wigner_D(lab[1], ths))] * n)
+    M = block_diag(*blocks)
+    return M.conj() if spc["dual"] else M
+
+
+def test_su2su2_equivariance_roundtrip():
+    """Deligne product embedding: invariant under SU(2) x SU(2) (charge and spin rotations)."""
+    V = sp("fSU2xSU2", SO4)
+    P = sp("fSU2xSU2", [((0, 1), 1), ((1, 0), 1)])
+    thc, ths = np.array([0.2, 1.1, -0.5]), np.array([-0.7, 0.3, 0.9])
+    # V's sectors have j_c + j_s integer, P's half-integer (one site): pair the P legs
+    for cod, dom in (([V, P], [V, P]), ([V, W.dual(V)], [P, P]), ([W.dual(P), V], [V, W.dual(P)])):
+        lt, x = rand_tensor("fSU2xSU2", cod, dom, 41)
+        assert lt.nelems > 0
+        D = Dn.to_dense(lt, x)
+        assert np.abs(Dn.from_dense(lt, D) - x).max() < 1e-13
+        Mc = np.ones((1, 1))
+        for s_ in cod:
+            Mc = np.kron(Mc, _leg_rep_su2su2(s_, thc, ths))
+        Md = np.ones((1, 1))
+        for s_ in dom:
+            Md = np.kron(Md, _leg_rep_su2su2(s_, thc, ths))
+        T = D.reshape(Mc.shape[0], Md.shape[0])
+        assert np.abs(Mc @ T - T @ Md).max() < 1e-12
+
+
+@pytest.mark.parametrize("factor", [0, 1])
+def test_su2su2_single_factor_reduces_to_su2(factor):
+    """With one factor trivial (j = 0 on every leg) the product embedding IS the SU(2) one."""
+    js = [0, 2, 4]
+    lab = (lambda j: (0, j)) if factor == 1 else (lambda j: (j, 0))
+    Vh = sp("fSU2xSU2", [(lab(j), n) for j, n in zip(js, (2, 1, 1))])
+    Vs = sp("SU2", [((j,), n) for j, n in zip(js, (2, 1, 1))])
+    for cod_d, dom_d in (([0, 0], [0]), ([0, 1], [0, 0])):
+        ch = [W.dual(Vh) if d else Vh for d in cod_d], [W.dual(Vh) if d else Vh for d in dom_d]
+        cs = [W.dual(Vs) if d else Vs for d in cod_d], [W.dual(Vs) if d else Vs for d in dom_d]
+        lh, xh = rand_tensor("fSU2xSU2", *ch, 51)
+        ls, xs = rand_tensor("SU2", *cs, 51)
+        assert lh.nelems == ls.nelems
+        assert np.array_equal(Dn.to_dense(lh, xh), Dn.to_dense(ls, xs))
+
+
+def test_su2su2_fermion_permute_inverse():
+    rng = np.random.default_rng(9)
+    V = sp("fSU2xSU2", SO4)
+    cod, dom = [V, W.dual(V)], [V, V]
+    lt, x = rand_tensor("fSU2xSU2", cod, dom, 43)
+    D = Dn.to_dense(lt, x)
+    par = [Dn.parity_vector(s_) for s_ in cod + dom]
+    N, n1 = 4, 2
+    for _ in range(8):
+        perm = list(rng.permutation(N))
+        k = int(rng.integers(0, N + 1))
+        p, q = perm[:k], perm[k:]
+        Pd = C.permute_dense(D, par, n1, p, q)
+        order = p + q
+        inv = [order.index(i) for i in range(N)]
+        assert np.array_equal(C.permute_dense(Pd, [par[i] for i in order], k, inv[:n1], inv[n1:]), D)
+        c2, d2 = C.permuted_spaces(cod, dom, p, q)
+        l2 = L.homspace_layout("fSU2xSU2", c2, d2)
         assert C.rel_frobenius(Dn.to_dense(l2, Dn.from_dense(l2, Pd)), Pd) < 1e-13

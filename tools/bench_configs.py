@@ -98,7 +98,7 @@ def time_events(fn, reps):
 def oracle_time(cfg):
     from tests import harness as H
     t0 = time.perf_counter()
-    if cfg["cfg"] == 7:
+    if cfg["cfg"] in (7, 8):
         return None, "none at full size (dense oracle needs 5.4 GB intermediates)"
     if cfg["cfg"] == 3:
         H.oracle_chain_blocks(cfg)
@@ -111,13 +111,13 @@ def oracle_time(cfg):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cfgs", default="1,2,3,5,6,7")
+    ap.add_argument("--cfgs", default="1,2,3,5,6,7,8")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--phases", action="store_true", help="per-step [permA, permB, gemm, permC] us")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    makers = {1: W.cfg1, 2: W.cfg2, 3: W.cfg3, 4: lambda: W.cfg4(d_leg=128), 5: W.cfg5, 6: W.cfg6, 7: W.cfg7}
+    makers = {1: W.cfg1, 2: W.cfg2, 3: W.cfg3, 4: lambda: W.cfg4(d_leg=128), 5: W.cfg5, 6: W.cfg6, 7: W.cfg7, 8: W.cfg8}
     for k in [int(x) for x in args.cfgs.split(",")]:
         cfg = makers[k]()
         T, steps = build(cfg, dev)

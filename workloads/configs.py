@@ -179,4 +179,24 @@ def cfg7(n_mult=700):
     return _dmrg_chain(7, "fU1xSU2", P, W, V)
 
 
-CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6, 7: cfg7}
+# ----------------------- config 8 (Hubbard at half filling, fZ2 x SU2 x SU2)
+def _su2su2_bond(n_mult, sigma_c=1.2, sigma_s=1.5):
+    """Multiplets (2jc, 2js), 0..6 each, with jc + js integer (bonds cut after an even number of sites),
+    multiplicities ~ exp(-jc^2/2s_c^2 - js^2/2s_s^2) by reading C15."""
+    labels = [(c, t) for c in range(0, 7) for t in range(0, 7) if (c + t) % 2 == 0]
+    weights = [math.exp(-(c / 2) ** 2 / (2 * sigma_c ** 2) - (t / 2) ** 2 / (2 * sigma_s ** 2)) for c, t in labels]
+    return gaussian_degeneracies(labels, weights, n_mult, lambda l: l[0] + l[1])
+
+
+def cfg8(n_mult=270):
+    """Hubbard two-site update at half filling with fZ2 x SU2(charge) x SU2(spin): the cfg3
+    chain with P = (1/2, 0) + (0, 1/2) (charge doublet: empty/double; spin doublet: single, odd),
+    W = 2 (0,0) + 2 (1/2,1/2) (the D = 10 channels: identity and the four single-fermion operators as
+    one SO(4) vector, odd), V: 270 multiplets (dim ~ 2000, as cfg3)."""
+    P = space("fSU2xSU2", [((1, 0), 1), ((0, 1), 1)])
+    W = space("fSU2xSU2", [((0, 0), 2), ((1, 1), 2)])
+    V = space("fSU2xSU2", _su2su2_bond(n_mult))
+    return _dmrg_chain(8, "fSU2xSU2", P, W, V)
+
+
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6, 7: cfg7, 8: cfg8}
