@@ -435,6 +435,22 @@ static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, c
   cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+template <typename... KArgs, typename... Args>
+static void launch_k2(void (*kern)(KArgs...), dim3 grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool pdl = getenv("TK_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // packed jobs of small single-member rows groups (see kPackGroups): per CTA, the groups' row tables
 // are built once into shared memory, then all elements of the job are walked as one flat range with
 // 64 bytes of loads in flight per thread; each thread advances its group index monotonically.
@@ -673,10 +689,13 @@ struct GemmCfg {
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 
+// k range [kb, ke) (split-K: ke - kb < K); part != nullptr: write the raw partial tile (BM x BN,
+// column-major) for the split-K reduction instead of alpha * acc + beta * C.
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
 __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const double* __restrict__ B,
                                           double* __restrict__ C, const GemmGroup& g, int m0, int n0, double alpha,
-                                          double beta, bool vec, double* smem) {
+                                          double beta, bool vec, double* smem, int kb, int ke,
+                                          double* __restrict__ part) {
   using Cfg = GemmCfg<BM, BN, WM, WN, BK, STAGES>;
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
@@ -685,8 +704,8 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
   const int gq = lane >> 2, tq = lane & 3;
   const double* Ag = A + g.a_off;
   const double* Bg = B + g.b_off;
-  const int M = g.M, N = g.N, K = g.K;
-  const int nk = (K + BK - 1) / BK;
+  const int M = g.M, N = g.N, K = ke;
+  const int nk = (ke - kb + BK - 1) / BK;
 
   double acc[Cfg::MF][Cfg::NF][2];
 #pragma unroll
@@ -695,7 +714,7 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
     for (int j = 0; j < Cfg::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto load_stage = [&](int kt, int s) {
-    const int k0 = kt * BK;
+    const int k0 = kb + kt * BK;
     double* as = As + s * Cfg::A_STAGE;
     double* bs = Bs + s * Cfg::B_STAGE;
     if (vec) {
@@ -766,6 +785,18 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
     }
   }
   cp_async_wait<0>();
+  if (part) {  // split-K partial: raw accumulators, the reduction applies alpha / beta
+#pragma unroll
+    for (int i = 0; i < Cfg::MF; ++i)
+#pragma unroll
+      for (int j = 0; j < Cfg::NF; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int ml = wm * WM + i * 8 + gq, nl = wn * WN + j * 8 + 2 * tq + c;
+          part[ml + nl * BM] = acc[i][j][c];
+        }
+    return;
+  }
   // epilogue: C = alpha * acc + beta * C (column-major, ldc)
   double* Cg = C + g.c_off;
 #pragma unroll
@@ -955,13 +986,45 @@ using SmallCfg = GemmCfg<TK_SMALL>;
 __global__ void __launch_bounds__(SmallCfg::THREADS)
     gemm_small_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                      double beta, int base_vec) {
+                      double beta, int base_vec, double* __restrict__ parts) {
   extern __shared__ __align__(16) double smem[];
   pdl_trigger();
   const GemmTile t = tiles[blockIdx.x];
   const GemmGroup g = groups[t.group];
   pdl_wait();
-  gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
+  double* part = t.slot >= 0 ? parts + (int64_t)t.slot * (64 * 64) : nullptr;
+  gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem, t.k0, t.k1, part);
+}
+
+// split-K reduction of 64 x 64 tiles: C = alpha * sum_s partial_s + beta * C, summed in slot order
+// (deterministic). gridDim.y = 4 quarters of a tile, one element per thread; all partial loads of an
+// element are issued before the (ordered) sum, so the kernel costs about one L2 round trip.
+constexpr int kSplitMax = 16;
+__global__ void __launch_bounds__(256)
+    gemm_splitk_reduce_kernel(double* __restrict__ C, const GemmGroup* __restrict__ groups,
+                              const GemmTile* __restrict__ heads, const double* __restrict__ parts, double alpha,
+                              double beta) {
+  pdl_trigger();
+  const GemmTile t = heads[blockIdx.x];
+  const GemmGroup g = groups[t.group];
+  pdl_wait();
+  double* Cg = C + g.c_off;
+  for (int e = blockIdx.y * 1024 + threadIdx.x; e < (blockIdx.y + 1) * 1024; e += 256) {
+    const int ml = e % 64, nl = e / 64;
+    const int m = t.m0 + ml, n = t.n0 + nl;
+    if (m >= g.M || n >= g.N) continue;
+    double x[kSplitMax];
+#pragma unroll
+    for (int sidx = 0; sidx < kSplitMax; ++sidx)
+      x[sidx] = sidx < t.nsplit ? parts[(int64_t)(t.slot + sidx) * (64 * 64) + e] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int sidx = 0; sidx < kSplitMax; ++sidx) acc += x[sidx];
+    double* p = Cg + (int64_t)m + (int64_t)n * g.ldc;
+    double v = alpha * acc;
+    if (beta != 0.0) v = fma(beta, *p, v);
+    *p = v;
+  }
 }
 
 // ---- skinny blocks (N, K <= kSkinnyMax; the MPO steps T.W of the DMRG chains, M up to 2e5): a
@@ -1042,8 +1105,8 @@ __global__ void __launch_bounds__(kSkinnyThreads)
 }
 
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
-                        int ntiles_big, int ntiles_small, int ntiles_skinny, double alpha, double beta,
-                        cudaStream_t st) {
+                        int ntiles_big, int ntiles_small, int ntiles_skinny, const GemmTile* split_heads,
+                        int nsplit_heads, double* parts, double alpha, double beta, cudaStream_t st) {
   // big tiles: mbarrier pipeline, 16 warps of 32x32 on 128x128, BK 16, 6 stages, prefetch distance 2
   static bool attr = false;
   if (!attr) {
@@ -1057,7 +1120,10 @@ cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmG
              base_vec);
   if (ntiles_small)
     launch_k(gemm_small_kernel, ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C, groups,
-             tiles + ntiles_big, alpha, beta, base_vec);
+             tiles + ntiles_big, alpha, beta, base_vec, parts);
+  if (nsplit_heads)
+    launch_k2(gemm_splitk_reduce_kernel, dim3(nsplit_heads, 4), 256, 0, st, C, groups, split_heads,
+              (const double*)parts, alpha, beta);
   if (ntiles_skinny)
     launch_k(gemm_skinny_kernel, ntiles_skinny, kSkinnyThreads, 0, st, A, B, C, groups,
              tiles + ntiles_big + ntiles_small, alpha, beta);

@@ -94,7 +94,10 @@ struct GemmGroup {
 struct GemmTile {
   int32_t group;
   int32_t m0, n0;
-  int32_t pad;
+  int32_t pad;         // sort key (K) / skinny: rows of the tile
+  int32_t k0, k1;      // k range of this tile (split-K: a slice of [0, K))
+  int32_t slot;        // split-K: partial-tile slot (-1: write C directly); reduction heads: first slot
+  int32_t nsplit;      // reduction heads: number of partial slots
 };
 
 // launchers (tk_kernels.cu)
@@ -108,8 +111,10 @@ cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* 
 // tile table layout: [big (128x128 DMMA) | small (64x64 DMMA) | skinny (streaming, GemmTile.pad = rows)]
 constexpr int kSkinnyMax = 16;   // skinny groups: 0 < K <= 16 and N <= 16
 constexpr int kSkinnyRows = 2048;
+// split-K (small tiles of under-filled launches): partial 64x64 tiles in `parts`, then one reduction
+// CTA per head tile (deterministic order)
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
-                        int ntiles_big, int ntiles_small, int ntiles_skinny, double alpha, double beta,
-                        cudaStream_t st);
+                        int ntiles_big, int ntiles_small, int ntiles_skinny, const GemmTile* split_heads,
+                        int nsplit_heads, double* parts, double alpha, double beta, cudaStream_t st);
 
 }  // namespace tk

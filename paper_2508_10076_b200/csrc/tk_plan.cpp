@@ -447,6 +447,10 @@ struct ContractPlan {
   std::vector<GemmGroup> ggroups;
   std::vector<GemmTile> tiles;
   int ntiles_big = 0, ntiles_small = 0, ntiles_skinny = 0;
+  std::vector<GemmTile> split_heads;  // split-K reduction targets
+  int nslots = 0;
+  size_t off_parts = 0;
+  DevBuf d_heads;
   bool cplx = false;  // ComplexF64: workspace in the real representation (PermCM), one real GEMM
   // small Float64 contractions: both operand permutes in ONE launch (jobs of A~ = op 0, B~ = op 1)
   bool merged_ab = false;
@@ -469,6 +473,7 @@ struct ContractPlan {
     if (!pc.identity) pc.upload();
     d_ggroups.upload(ggroups);
     d_tiles.upload(tiles);
+    d_heads.upload(split_heads);
     d_jobs_ab.upload(jobs_ab);
     uploaded = true;
   }
@@ -672,10 +677,14 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     int gi = (int)P.ggroups.size();
     P.ggroups.push_back(g);
     if (g.K > 0 && g.K <= kSkinnyMax && g.N <= kSkinnyMax) {  // streaming path (HBM-bound block)
-      for (int m = 0; m < g.M; m += kSkinnyRows) skinny.push_back(GemmTile{gi, m, 0, std::min(kSkinnyRows, g.M - m)});
+      for (int m = 0; m < g.M; m += kSkinnyRows)
+        skinny.push_back(GemmTile{gi, m, 0, std::min(kSkinnyRows, g.M - m), 0, g.K, -1, 0});
       continue;
     }
-    bool isbig = g.M >= 96 && g.N >= 96;
+    // short-K blocks (K <= 128: the L.theta steps of the DMRG chains) take 64 x 64 tiles: 4x the CTAs,
+    // 3 CTAs per SM, so tile epilogues overlap other tiles' main loops (measured cfg2 step 1: 30 -> 15 us)
+    static const int small_k = getenv("TK_GEMM_SMALL_K") ? atoi(getenv("TK_GEMM_SMALL_K")) : 128;
+    bool isbig = g.M >= 96 && g.N >= 96 && g.K > small_k;
     int bm = isbig ? 128 : 64, bn = isbig ? 128 : 64;
     // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that one wave of
     // ~148 co-resident tiles covers a ~G x 12 rectangle and shares the A and B k-slices in L2
@@ -684,11 +693,41 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     for (int mb = 0; mb < ntm; mb += G)
       for (int nt = 0; nt < ntn; ++nt)
         for (int mt = mb; mt < std::min(ntm, mb + G); ++mt)
-          (isbig ? big : small).push_back(GemmTile{gi, mt * bm, nt * bn, g.K});
+          (isbig ? big : small).push_back(GemmTile{gi, mt * bm, nt * bn, g.K, 0, g.K, -1, 0});
+  }
+  // split-K for under-filled launches (fewer than two tiles per SM): long-K small tiles are cut into
+  // S slices of 64-multiples, each writing a partial tile; one reduction CTA per tile sums them in a
+  // fixed order (deterministic) and applies alpha / beta.
+  const int ntot = (int)(big.size() + small.size());
+  static const bool no_split = getenv("TK_NO_SPLITK") != nullptr;
+  if (!no_split && ntot > 0 && ntot < 2 * 148) {
+    const int want = (2 * 148 + ntot - 1) / ntot;
+    std::vector<GemmTile> out;
+    int slot = 0;
+    for (const GemmTile& t : small) {
+      const int K = t.k1;
+      const int S = std::min(std::min(want, K / 64), 16);  // kSplitMax in the reduction kernel
+      if (S < 2) {
+        out.push_back(t);
+        continue;
+      }
+      const int chunk = ((K + S - 1) / S + 15) & ~15;
+      int ns = 0;
+      for (int k = 0; k < K; k += chunk, ++ns)
+        out.push_back(GemmTile{t.group, t.m0, t.n0, std::min(chunk, K - k), k, std::min(K, k + chunk), slot + ns, 0});
+      P.split_heads.push_back(GemmTile{t.group, t.m0, t.n0, K, 0, K, slot, ns});
+      slot += ns;
+    }
+    small = out;
+    P.nslots = slot;
   }
   auto by_k = [](const GemmTile& x, const GemmTile& y) { return x.pad > y.pad; };  // LPT: long K first
   std::stable_sort(big.begin(), big.end(), by_k);
   std::stable_sort(small.begin(), small.end(), by_k);
+  if (P.nslots) {
+    P.off_parts = P.ws_bytes;
+    P.ws_bytes = align256(P.ws_bytes + (size_t)P.nslots * 64 * 64 * 8);
+  }
   P.ntiles_big = (int)big.size();
   P.ntiles_small = (int)small.size();
   P.ntiles_skinny = (int)skinny.size();
@@ -932,9 +971,10 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
   double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
   if (!P->tiles.empty()) {
     check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, (const GemmTile*)P->d_tiles.p,
-                           P->ntiles_big, P->ntiles_small, P->ntiles_skinny, ga, gb, st),
+                           P->ntiles_big, P->ntiles_small, P->ntiles_skinny, (const GemmTile*)P->d_heads.p,
+                           (int)P->split_heads.size(), (double*)(w + P->off_parts), ga, gb, st),
                "gemm launch");
-    g_launches += (P->ntiles_big > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0);
+    g_launches += (P->ntiles_big > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0) + !P->split_heads.empty();
   }
   prof_record(3, st);
   if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
