@@ -397,6 +397,83 @@ __device__ void permute_tiled(const typename CIO<CM>::S* __restrict__ src, typen
   }
 }
 
+// Box jobs (mode 2): dst leg 0 is unit-stride on both sides; the source's next-fastest leg (leg 2,
+// source stride n0) and the destination's (leg 1, destination stride n0) differ, so rows of n0 elements
+// alone give short scattered runs (cfg4: median 144 bytes). A box n0 x c1 x c2 is loaded as c1 source
+// runs of n0*c2 contiguous elements into shared memory S[i1][i2*n0 + i0] (odd plane pitch P1), and
+// stored as c2 destination runs of n0*c1 contiguous elements. 8 loads per thread in flight.
+template <int CM>
+__device__ void permute_box(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                            const PermGroup& g, const PermJob& job, PermShared& sh, typename CIO<CM>::V* __restrict__ S,
+                            double alpha, double beta, double ims) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
+  const int tid = threadIdx.x;
+  const int n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
+  const int c1 = g.ct, c2 = g.R;
+  const int64_t sl = sh.mld[0], dl = sh.mld[kMaxGroupMembers];
+  const int64_t so = sh.moff[0], dof = sh.moff[kMaxGroupMembers];
+  const int64_t s1 = g.sa[1] + sl * g.sb[1], d2 = g.da[2] + dl * g.db[2];
+  const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
+  const double c = alpha * sh.coef[0];
+  FastDiv fn0;
+  fn0.init((uint32_t)n0);
+  pdl_wait();  // tensor data only after the preceding grid has completed (PDL)
+  for (int u = 0; u < job.count; ++u) {
+    int64_t b = job.first + u;
+    const int b1 = (int)(b % g.T0);
+    b /= g.T0;
+    const int b2 = (int)(b % g.Tt);
+    uint32_t rest = (uint32_t)(b / g.Tt);
+    int64_t sbase = so, dbase = dof;
+    for (int l = 3; l < g.ndim; ++l) {
+      const uint32_t e = (uint32_t)g.ext[l], q = rest / e, i = rest - q * e;
+      rest = q;
+      sbase += (int64_t)i * (g.sa[l] + sl * g.sb[l]);
+      dbase += (int64_t)i * (g.da[l] + dl * g.db[l]);
+    }
+    const int i1b = b1 * c1, i2b = b2 * c2;
+    const int m1 = min(c1, n1 - i1b), m2 = min(c2, n2 - i2b);
+    sbase += (int64_t)i1b * s1 + (int64_t)i2b * n0;   // leg 2: source stride n0
+    dbase += (int64_t)i1b * n0 + (int64_t)i2b * d2;   // leg 1: destination stride n0
+    const uint32_t Ls = (uint32_t)n0 * m2, Ld = (uint32_t)n0 * m1, tot = Ls * m1;
+    const uint32_t P1 = Ls | 1;  // plane pitch of S[i1][.]
+    FastDiv fs, fd;
+    fs.init(Ls);
+    fd.init(Ld);
+    // load phase: source runs (i1 major), contiguous over r = i2 * n0 + i0
+    constexpr int U = sizeof(V) == 16 ? 4 : 8;
+    for (uint32_t e0 = tid; e0 < tot; e0 += U * kPermThreads) {
+      V x[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t e = e0 + k * kPermThreads;
+        if (e < tot) {
+          const uint32_t i1 = fs.div(e), r = e - i1 * Ls;
+          x[k] = IO::load(src, sbase + (int64_t)i1 * s1 + r, sd1);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t e = e0 + k * kPermThreads;
+        if (e < tot) {
+          const uint32_t i1 = fs.div(e), r = e - i1 * Ls;
+          S[i1 * P1 + r] = x[k];
+        }
+      }
+    }
+    __syncthreads();
+    // store phase: destination runs (i2 major), contiguous over r' = i1 * n0 + i0
+    for (uint32_t e = tid; e < tot; e += kPermThreads) {
+      const uint32_t i2 = fd.div(e), rr = e - i2 * Ld;
+      const uint32_t i1 = fn0.div(rr), i0 = rr - i1 * (uint32_t)n0;
+      IO::store(dst, dbase + (int64_t)i2 * d2 + rr, dd1, dd2, Num<V>::scale(c, S[i1 * P1 + i2 * (uint32_t)n0 + i0]),
+                beta, ims);
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMember* __restrict__ members,
                                                 const double* __restrict__ coefs, PermShared& sh) {
   const int tid = threadIdx.x;
@@ -612,6 +689,8 @@ __global__ void __launch_bounds__(kPermThreads, 4) permute_kernel(PermOp op0, Pe
   load_job_header(g, op.members, op.coefs, sh);
   if (!ROWS_ONLY && job.type == kJobTiled)
     permute_tiled<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
+  else if (!ROWS_ONLY && job.type == kJobBox)
+    permute_box<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
   else
     permute_rows<CM, true>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
 }

@@ -20,7 +20,10 @@ struct PermGroup {
   int32_t coef_off;     // into coefs: ksrc * kdst, row-major [i][j]
   int32_t src_mem;      // into members: ksrc source members
   int32_t dst_mem;      // into members: kdst destination members
-  int32_t mode;         // 0 = rows (dst leg 0 is also unit-stride in src), 1 = smem-tiled transpose
+  int32_t mode;         // 0 = rows (dst leg 0 is also unit-stride in src), 1 = smem-tiled transpose,
+                        // 2 = box: leg 0 unit-stride on both sides, legs 1 (dst-next) and 2 (src-next)
+                        //     swapped through a shared-memory box n0 x c1 x c2 (c0 = n0, ct = c1 chunk
+                        //     of leg 1, R = c2 chunk of leg 2, T0 / Tt chunk counts, nrest = legs 3..)
   int32_t tleg;         // mode 1: index (dst order) of the src-fastest leg
   int32_t c0, ct;       // mode 1: chunk of leg 0 / leg tleg held in one smem tile
   int32_t R;            // mode 1: rest indices (all other legs) packed into one tile
@@ -63,7 +66,8 @@ constexpr int kTileElems = 4608;  // smem capacity of the two tile buffers (elem
 constexpr int kPackGroups = 32;
 constexpr int kPackRows = 1024;
 constexpr int kPackElems = 8192;
-enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3 };
+enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3, kJobBox = 4 };
+constexpr int kBoxElems = 4096;  // doubles per box (ComplexF64: half as many elements)
 struct PermJob {
   int32_t group;
   int16_t count;  // rows / tiles / packed groups of this job

@@ -151,7 +151,47 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
   g.lorder = 0 + 3 * 1 + 9 * 2;
   g.nrest = 1;
   static const bool tile_all = getenv("TK_PERM_TILE_ALL") != nullptr;
+  // box mode is an opt-in experiment (TK_BOX=1): measured 2.7 TB/s on cfg4 against 5.0 TB/s for the
+  // rows path (profiles/r01_ncu_summary.md), so the rows path stays the default
+  static const bool no_box = getenv("TK_BOX") == nullptr;
   bool lead_unit = (g.sa[0] == 1 && g.sb[0] == 0);
+  // mode 2 (box): leg 0 unit-stride on both sides but short (n0 < 128), and the source's next-fastest
+  // leg is not the destination's: swap those two legs through a shared-memory box
+  if (!no_box && lead_unit && g.ndim >= 3 && g.ksrc == 1 && g.kdst == 1 && g.ext[0] < 128) {
+    int sleg = 1;
+    for (int l = 2; l < g.ndim; ++l)
+      if (std::make_pair(g.sb[l], g.sa[l]) < std::make_pair(g.sb[sleg], g.sa[sleg])) sleg = l;
+    // the box kernel walks contiguous runs: source leg sleg right after leg 0 (stride n0, codomain),
+    // destination leg 1 right after leg 0 (stride n0, codomain)
+    const bool runs = g.sb[sleg] == 0 && g.sa[sleg] == g.ext[0] && g.db[1] == 0 && g.da[1] == g.ext[0];
+    if (sleg != 1 && runs) {
+      std::vector<int> order{0, 1, sleg};
+      for (int l = 2; l < g.ndim; ++l)
+        if (l != sleg) order.push_back(l);
+      PermGroup h = g;
+      for (int k = 0; k < g.ndim; ++k) {
+        h.ext[k] = g.ext[order[k]];
+        h.sa[k] = g.sa[order[k]];
+        h.sb[k] = g.sb[order[k]];
+        h.da[k] = g.da[order[k]];
+        h.db[k] = g.db[order[k]];
+      }
+      g = h;
+      g.mode = 2;
+      const int64_t n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
+      const int64_t budget = std::max<int64_t>(1, (kBoxElems - 64) / n0);  // + odd plane padding
+      int64_t c2 = std::min<int64_t>(n2, std::max<int64_t>(1, (int64_t)std::sqrt((double)budget)));
+      int64_t c1 = std::min<int64_t>(n1, std::max<int64_t>(1, budget / c2));
+      c2 = std::min<int64_t>(n2, std::max<int64_t>(1, budget / c1));
+      g.c0 = (int32_t)n0;
+      g.ct = (int32_t)c1;
+      g.R = (int32_t)c2;
+      g.T0 = (int32_t)((n1 + c1 - 1) / c1);
+      g.Tt = (int32_t)((n2 + c2 - 1) / c2);
+      g.nrest = g.nelem / (n0 * n1 * n2);
+      return;
+    }
+  }
   if (g.ndim >= 2 && g.ksrc == 1 && g.kdst == 1 && (!lead_unit || tile_all)) {
     g.mode = 1;
     g.tleg = 1;
@@ -184,7 +224,7 @@ static bool packable(const PermGroup& g) {
 static void make_jobs(PermPlan& P) {
   // small single-member groups go last and are packed several per CTA (permute_packed_kernel)
   std::stable_partition(P.groups.begin(), P.groups.end(), [](const PermGroup& g) { return !packable(g); });
-  std::vector<PermJob> rows, multi, tiles, packed;
+  std::vector<PermJob> rows, multi, tiles, packed, boxes;
   // elements per CTA job: 8192 for large permutes, smaller for small ones so that a latency-bound
   // permute still spreads over about two waves of the 148 SMs x 4 resident CTAs
   int64_t total = 0;
@@ -207,6 +247,13 @@ static void make_jobs(PermPlan& P) {
       }
       continue;
     }
+    if (g.mode == 2) {
+      const int64_t nbox = (int64_t)g.T0 * g.Tt * g.nrest;
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4096, job_elems / ((int64_t)g.c0 * g.ct * g.R)));
+      for (int64_t r = 0; r < nbox; r += per)
+        boxes.push_back(PermJob{gi, (int16_t)std::min(per, nbox - r), kJobBox, 0, r});
+      continue;
+    }
     if (g.mode == 0) {
       int64_t nrows = g.nelem / g.ext[0];
       int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, job_elems / std::max(1, g.ext[0])));
@@ -223,10 +270,11 @@ static void make_jobs(PermPlan& P) {
   }
   // small permutes: one launch for rows, tiled and packed jobs (+ one for recoupling jobs); large ones
   // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
+  tiles.insert(tiles.end(), boxes.begin(), boxes.end());  // box jobs run beside the tiled ones
   P.njobs = (int)(tiles.size() + rows.size() + packed.size());
   P.njobs_rows = (int)rows.size();
   P.njobs_multi = (int)multi.size();
-  P.tiled = !tiles.empty();
+  P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
   P.rows_only = tiles.empty() && packed.empty();
   P.split = total >= (int64_t(1) << 24) && !P.rows_only && !rows.empty();
   static const bool dbg = getenv("TK_PLAN_DEBUG") != nullptr;
@@ -608,7 +656,8 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   P.pa.identity = ia_id;
   P.pb.identity = ib_id;
   P.pc.identity = ic_id;
-  if (!P.cplx && !ia_id && !ib_id && A.nelems + B.nelems < (int64_t(1) << 26)) {
+  static const bool no_merge = getenv("TK_NO_MERGE") != nullptr;
+  if (!no_merge && !P.cplx && !ia_id && !ib_id && A.nelems + B.nelems < (int64_t(1) << 26)) {
     P.merged_ab = true;
     auto take = [&](const PermPlan& pp, int8_t op, bool multi) {
       int b = multi ? pp.njobs : 0, e = multi ? pp.njobs + pp.njobs_multi : pp.njobs;
