@@ -68,6 +68,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 constexpr int kPermThreads = 256;
+#ifndef TK_ROWS_U
+#define TK_ROWS_U 8  // loads in flight per thread in the rows path (Float64)
+#endif
 constexpr int kMaxRows = 256;
 
 // Element I/O of the permute kernels per complex mode CM (see PermCM in tk_kernels.hpp). Offsets are in
@@ -155,7 +158,7 @@ __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typena
     const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
     const double c = alpha * sh.coef[0];
     // independent loads in flight per thread (64 bytes: bytes in flight hide DRAM latency)
-    constexpr int U = sizeof(V) == 16 ? 4 : 8;
+    constexpr int U = sizeof(V) == 16 ? TK_ROWS_U / 2 : TK_ROWS_U;
     FastDiv fd;
     fd.init((uint32_t)n0);
     const uint32_t total = (uint32_t)cnt * (uint32_t)n0;

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtk_b200.so")
+LIB_PATH = os.environ.get("TK_LIB_PATH") or os.path.join(_HERE, "libtk_b200.so")  # override: experiments
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_10076_b200.build` "
