@@ -91,7 +91,9 @@ void tk_space_retain(tk_space* s);
 void tk_space_release(tk_space* s);
 
 /* ----------------------------------------------------------------- tensors (host) */
-/* Block layout of W_1..W_{n_dom} -> V_1..V_{n_cod}. Host only. */
+/* Block layout of W_1..W_{n_dom} -> V_1..V_{n_cod}. Host only. At least one leg
+ * (the kind comes from the spaces); rank-0 (scalar) tensors arise from tk_contract_output of full
+ * contractions: one 1 x 1 block at the unit sector. */
 tk_status tk_tensor_create(tk_dtype dtype, int32_t n_cod, tk_space* const* cod, int32_t n_dom,
                            tk_space* const* dom, tk_tensor** out);
 /* Stored scalars (Float64 count; ComplexF64: complex count -- buffer holds 2x doubles). */

@@ -114,7 +114,9 @@ struct Tensor {
 
 std::string tree_pair_key(const Tree& s, const Tree& f);
 void enumerate_trees(Kind k, const std::vector<Space*>& legs, std::map<Sector, std::vector<Tree>>& out);
-Tensor* make_tensor(tk_dtype dtype, const std::vector<Space*>& cod, const std::vector<Space*>& dom);
+// rank 0 (no legs, a scalar: one 1 x 1 block at the unit sector) needs the kind from the caller
+Tensor* make_tensor(tk_dtype dtype, const std::vector<Space*>& cod, const std::vector<Space*>& dom,
+                    int kind_if_rank0 = -1);
 Space* make_space(Kind k, std::vector<Sector> sectors, std::vector<int64_t> degs, bool dual);
 Space* dual_space(const Space* s);
 bool same_space(const Space* a, const Space* b);

@@ -67,7 +67,13 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-constexpr int kPermThreads = 256;
+#ifndef TK_PERM_THREADS
+#define TK_PERM_THREADS 256  // threads per permute CTA
+#endif
+#ifndef TK_PERM_MINB
+#define TK_PERM_MINB 4       // resident permute CTAs per SM (register budget: 64 / thread at 256 x 4)
+#endif
+constexpr int kPermThreads = TK_PERM_THREADS;
 #ifndef TK_ROWS_U
 #define TK_ROWS_U 8  // loads in flight per thread in the rows path (Float64)
 #endif
@@ -671,7 +677,7 @@ union PermSharedAll {
 // ROWS_ONLY: a launch whose jobs are all rows jobs (the large cfg4 permutes) uses a leaner instance
 // (48 registers instead of 64; measured 5.0 vs 4.6 TB/s on cfg4).
 template <int CM, bool ROWS_ONLY>
-__global__ void __launch_bounds__(kPermThreads, 4) permute_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB) permute_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
   using IO = CIO<CM>;
   __shared__ typename std::conditional<ROWS_ONLY, PermShared, PermSharedAll>::type sh_;
   PermShared& sh = *reinterpret_cast<PermShared*>(&sh_);

@@ -184,9 +184,11 @@ void Tensor::write_key(int sub, int32_t* out) const {
   for (auto& x : f.inner) put(x);
 }
 
-Tensor* make_tensor(tk_dtype dtype, const std::vector<Space*>& cod, const std::vector<Space*>& dom) {
-  if (cod.empty() && dom.empty()) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tensor with no legs");
-  Kind k = cod.empty() ? dom[0]->kind : cod[0]->kind;
+Tensor* make_tensor(tk_dtype dtype, const std::vector<Space*>& cod, const std::vector<Space*>& dom,
+                    int kind_if_rank0) {
+  if (cod.empty() && dom.empty() && kind_if_rank0 < 0)
+    TK_THROW(TK_ERR_INVALID_ARGUMENT, "tensor with no legs (its sector kind is unknown)");
+  Kind k = !cod.empty() ? cod[0]->kind : (!dom.empty() ? dom[0]->kind : (Kind)kind_if_rank0);
   for (auto* s : cod)
     if (s->kind != k) TK_THROW(TK_ERR_SECTOR_MISMATCH, "legs of different sector kinds");
   for (auto* s : dom)
@@ -239,7 +241,7 @@ Tensor* make_tensor(tk_dtype dtype, const std::vector<Space*>& cod, const std::v
       }
   }
   std::ostringstream os;
-  os << (int)dtype << "|" << cod.size() << "|";
+  os << (int)dtype << "|" << kind_name(k) << "|" << cod.size() << "|";
   for (auto* s : cod) os << s->signature();
   os << "|";
   for (auto* s : dom) os << s->signature();

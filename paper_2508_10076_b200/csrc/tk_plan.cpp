@@ -229,7 +229,8 @@ static void make_jobs(PermPlan& P) {
   // permute still spreads over about two waves of the 148 SMs x 4 resident CTAs
   int64_t total = 0;
   for (const PermGroup& g : P.groups) total += g.nelem;
-  const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(kPackElems, total / (2 * 148 * 4)));
+  static const int64_t job_div = getenv("TK_JOB_DIV") ? atoll(getenv("TK_JOB_DIV")) : 2 * 148 * 4;
+  const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(kPackElems, total / job_div));
   int64_t pack_elems = 0, pack_rows = 0;
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
@@ -618,7 +619,7 @@ static void choose_contracted_order(const Tensor& A, const Tensor& B, Tuples& t)
 Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, tk_dtype dt) {
   std::vector<Space*> cod, dom;
   permuted_spaces(A, p, q, cod, dom);
-  Tensor* t = make_tensor(dt, cod, dom);
+  Tensor* t = make_tensor(dt, cod, dom, (int)A.kind);
   for (auto* s : cod) tk_space_release((tk_space*)s);
   for (auto* s : dom) tk_space_release((tk_space*)s);
   return t;
@@ -637,7 +638,7 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   P.Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
   {
     std::vector<Space*> cod(P.At->cod), dom(P.Bt->dom);
-    P.Ct = make_tensor(C.dtype, cod, dom);
+    P.Ct = make_tensor(C.dtype, cod, dom, (int)A.kind);
   }
   check_target(*P.Ct, t.pAB, t.qAB, C);
   // ComplexF64 always passes through the workspace (the permutes also change the representation)
@@ -964,7 +965,7 @@ tk_status tk_contract_output(const tk_tensor* A_, const int32_t* labA, const tk_
   Tensor* At = permuted_tensor(A, t.pA, t.qA, A.dtype);
   Tensor* Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
   std::vector<Space*> cod(At->cod), dom(Bt->dom);
-  Tensor* Ct = make_tensor(A.dtype, cod, dom);
+  Tensor* Ct = make_tensor(A.dtype, cod, dom, (int)A.kind);
   Tensor* C = permuted_tensor(*Ct, t.pAB, t.qAB, A.dtype);
   tk_tensor_release((tk_tensor*)At);
   tk_tensor_release((tk_tensor*)Bt);

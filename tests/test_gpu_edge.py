@@ -1,0 +1,121 @@
+"""Degenerate and edge cases of the CUDA path against the oracle -- needs a B200.
+
+  * empty tensors (no allowed sector) and outputs with no coupled sector shared by A~ and B~
+    (every block K = 0: C = beta * C);
+  * full contractions to a scalar (rank-0 output) and outer products (no contracted leg);
+  * alpha = 0 (C = beta * C, inputs may hold NaN-free garbage), beta = 1 accumulation, negative alpha;
+  * ragged subblocks (single-element sectors next to large ones), every kind;
+  * the workspace contract: too small -> TK_ERR_WORKSPACE_TOO_SMALL with C untouched.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from oracle import layout as OL, dense as OD, contract as OC  # noqa: E402
+from workloads import configs as W  # noqa: E402
+
+TOL = 1e-12
+
+
+def _run(kind, A_sp, labA, B_sp, labB, labC, ncod, alpha=1.0, beta=0.0, seed=0, c0=None):
+    from paper_2508_10076_b200 import tk
+    la = OL.homspace_layout(kind, A_sp["cod"], A_sp["dom"])
+    lb = OL.homspace_layout(kind, B_sp["cod"], B_sp["dom"])
+    rng = np.random.default_rng(seed)
+    xa, xb = rng.standard_normal(la.nelems), rng.standard_normal(lb.nelems)
+    A, B = tk.tensor_from_spec(A_sp), tk.tensor_from_spec(B_sp)
+    C = tk.tk_contract_output(A, labA, B, labB, labC, ncod)
+    cod, dom = OC.output_spaces(A_sp["cod"], A_sp["dom"], B_sp["cod"], B_sp["dom"], labA, labB, labC, ncod)
+    lc = OL.homspace_layout(kind, cod, dom)
+    assert C.nelems == lc.nelems
+    y0 = rng.standard_normal(lc.nelems) if c0 is None else c0
+    a, b = torch.from_numpy(xa).cuda(), torch.from_numpy(xb).cuda()
+    c = torch.from_numpy(y0.copy()).cuda()
+    nws = tk.tk_contract_workspace(A, labA, B, labB, C, labC)
+    ws = torch.empty(max(nws // 8 + 32, 1), dtype=torch.float64, device="cuda")
+    tk.tk_contract(A, a, labA, B, b, labB, C, c, labC, alpha=alpha, beta=beta, ws=ws, ws_bytes=ws.numel() * 8)
+    torch.cuda.synchronize()
+    D = OC.contract(kind, OD.to_dense(la, xa), A_sp["cod"] + A_sp["dom"], len(A_sp["cod"]), labA,
+                    OD.to_dense(lb, xb), B_sp["cod"] + B_sp["dom"], len(B_sp["cod"]), labB, labC, ncod)
+    want = alpha * D + (beta * OD.to_dense(lc, y0) if beta != 0 else 0.0)
+    got = OD.to_dense(lc, c.cpu().numpy())
+    return got, want, lc
+
+
+def _check(got, want):
+    if np.linalg.norm(want.ravel()) == 0:
+        assert np.abs(got).max(initial=0.0) == 0.0
+    else:
+        assert OC.rel_frobenius(got, want) <= TOL
+
+
+def test_all_blocks_zero_k():
+    """A~ and B~ share no coupled sector: every GEMM group has K = 0 and C = beta * C."""
+    V = W.space("U1", [((0,), 3), ((1,), 2)])
+    X = W.space("U1", [((5,), 2)])        # contracted leg: charges 5 cannot balance V's
+    A = {"cod": [V], "dom": [X]}
+    B = {"cod": [X], "dom": [V]}
+    for beta in (0.0, 0.5):
+        got, want, lc = _run("U1", A, [1, 2], B, [2, 3], [1, 3], 1, beta=beta)
+        _check(got, want)
+
+
+def test_empty_operand():
+    """An operand with no allowed sector (nelems 0): the output is beta * C."""
+    V = W.space("U1", [((1,), 3)])
+    A = {"cod": [V, V], "dom": [V]}       # charge 2 <- 1: nothing allowed
+    B = {"cod": [V], "dom": [V]}
+    from paper_2508_10076_b200 import tk
+    assert tk.tensor_from_spec(A).nelems == 0
+    got, want, lc = _run("U1", A, [1, 2, 3], B, [3, 4], [1, 2, 4], 2, beta=-1.0)
+    _check(got, want)
+
+
+@pytest.mark.parametrize("kind,secs", [
+    ("U1", [((-1,), 1), ((0,), 17), ((1,), 2)]),
+    ("fU1xU1", [((0, 0), 1), ((1, 1), 9), ((1, -1), 1), ((2, 0), 5)]),
+    ("SU2", [((0,), 1), ((1,), 7), ((2,), 1)]),
+    ("fU1xSU2", [((0, 0), 1), ((1, 1), 6), ((-1, 1), 1)]),
+])
+def test_scalar_and_outer_product(kind, secs):
+    """Full contraction to a rank-0 tensor (trace of A^T B) and the outer product (no shared leg)."""
+    V = W.space(kind, secs)
+    A = {"cod": [V, V], "dom": [V]}
+    B = {"cod": [V], "dom": [V, V]}
+    got, want, lc = _run(kind, A, [1, 2, 3], B, [3, 1, 2], [], 0)
+    assert lc.nelems <= 1
+    _check(got, want)
+    S = {"cod": [V], "dom": [V]}
+    got, want, lc = _run(kind, S, [1, 2], S, [3, 4], [1, 3, 2, 4], 2, seed=2)
+    _check(got, want)
+
+
+@pytest.mark.parametrize("alpha,beta", [(0.0, 1.0), (0.0, 0.0), (-1.5, 1.0), (2.0, -0.25)])
+def test_alpha_beta_degenerate(alpha, beta):
+    cfg = W.cfg2(chi=96)
+    (na, la_, nb, lb_, nc, lc_, ncod) = cfg["steps"][0]
+    A, B = cfg["tensors"][na][0], cfg["tensors"][nb][0]
+    got, want, lc = _run("U1", A, la_, B, lb_, lc_, ncod, alpha=alpha, beta=beta, seed=5)
+    _check(got, want)
+
+
+def test_workspace_too_small_leaves_output():
+    from paper_2508_10076_b200 import tk
+    cfg = W.cfg4(d_leg=16)
+    (na, la_, nb, lb_, nc, lc_, ncod) = cfg["steps"][0]
+    A, B = tk.tensor_from_spec(cfg["tensors"][na][0]), tk.tensor_from_spec(cfg["tensors"][nb][0])
+    C = tk.tk_contract_output(A, la_, B, lb_, lc_, ncod)
+    a = torch.zeros(A.nelems, dtype=torch.float64, device="cuda")
+    b = torch.zeros(B.nelems, dtype=torch.float64, device="cuda")
+    c = torch.full((C.nelems,), 7.0, dtype=torch.float64, device="cuda")
+    nws = tk.tk_contract_workspace(A, la_, B, lb_, C, lc_)
+    assert nws > 0
+    ws = torch.empty(nws // 8 + 32, dtype=torch.float64, device="cuda")
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_contract(A, a, la_, B, b, lb_, C, c, lc_, ws=ws, ws_bytes=nws - 8)
+    assert e.value.status == "TK_ERR_WORKSPACE_TOO_SMALL"
+    torch.cuda.synchronize()
+    assert bool((c == 7.0).all())
