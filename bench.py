@@ -390,7 +390,7 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "c64"],
                     help="f64: the BASELINE metric (D_leg 384); c64: cfg4's ComplexF64 variant (D_leg 320)")
     ap.add_argument("--d-leg", type=int, default=None)
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-budget-s", type=float, default=24.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
