@@ -18,7 +18,9 @@
  *    "U1xU1"/"fU1xU1" {N, 2Sz} (fermion parity N mod 2), "SU2" {2j}, "fU1xSU2" {N, 2j} (the Hubbard
  *    fZ2 x U1 x SU2 Deligne product, P:2380-2412 / P:2582-2591; fermion parity N mod 2), "fSU2xSU2"
  *    {2j_charge, 2j_spin} (fZ2 x SU2 x SU2 at half filling; j_charge + j_spin integer,
- *    fermion parity 2j_spin mod 2).
+ *    fermion parity 2j_spin mod 2), "Fib" {0: I, 1: tau}, "Ising" {0: I, 1: sigma, 2: psi} (
+ *    their R-symbols are complex, so only planar -- cyclic -- permutes are available: anything that
+ *    would braid returns TK_ERR_BRAIDING_UNAVAILABLE).
  *  - A space lists the sectors of the UNDERLYING space V; is_dual = 1 makes it V*. Fusion
  *    trees label a dual leg by the dual sector (reading C6).
  *  - Legs are numbered codomain first, then domain, 0-based in this ABI.
@@ -73,7 +75,8 @@ typedef struct tk_tensor tk_tensor;
 typedef struct CUstream_st* tk_stream; /* = cudaStream_t; NULL = legacy default stream */
 
 /* ------------------------------------------------------------------ spaces (host) */
-/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2" | "fU1xSU2" | "fSU2xSU2". labels: n_sectors x width int32,
+/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2" | "fU1xSU2" | "fSU2xSU2" | "Fib" | "Ising".
+ * labels: n_sectors x width int32,
  * degeneracies: n_sectors int64 > 0 (zero entries are dropped). Sectors may be given
  * in any order; they are stored ascending. Duplicate labels -> TK_ERR_INVALID_ARGUMENT. */
 tk_status tk_space_create(const char* kind, int32_t n_sectors, const int32_t* labels,
@@ -198,6 +201,12 @@ tk_status tk_rsymbol(const char* kind, const int32_t* a, const int32_t* b, const
  * tk_tensor_subblocks) into out. Host only; for tests and the paper's §4.3 examples. */
 tk_status tk_permute_transfer(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q,
                               int32_t nq, const tk_tensor* C, double* out);
+
+/* As tk_permute_transfer, but through the planar route (cyclic rotations and bends only, Alg. 1/5
+ * P:398-415) that kinds without braiding use; (p, q) must be a cyclic transpose, else
+ * TK_ERR_BRAIDING_UNAVAILABLE. kappa_mode < 0 keeps the library's convention (test hook). */
+tk_status tk_permute_transfer_planar(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q,
+                                     int32_t nq, const tk_tensor* C, int32_t kappa_mode, double* out);
 
 const char* tk_last_error(void);
 void tk_cache_clear(void);

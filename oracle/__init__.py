@@ -16,6 +16,9 @@ einsum in float64 (fermions: a dense Alg. 4 with Koszul signs). Modules:
   dense       dense embedding / projection (P:972-983 abelian; P:1387-1433 Wigner-Eckart)
   contract    dense einsum contraction; dense Alg. 4 with Koszul signs (reading C13)
   blocksparse tier 2: charge-tuple einsum for full-size abelian configs (no matricisation)
+  svd         blockwise truncated SVD: own permute + LAPACK per block + the global truncation rule
+  planar      planar (cyclic) transposes on tree pairs for anyons (Fib, Ising) with no dense
+              embedding; pinned against the dense SU(2) oracle and by pentagon / unitarity / rotation
 
 Parity status per function is listed in DESIGN.md §Oracle; the fermionic sign
 convention beyond the pins of reading C13 is "parity unpinned".

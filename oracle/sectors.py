@@ -12,9 +12,14 @@ Labels are tuples of ints:
                     charges add, spins by the SU2 rule, d = 2j+1, fermion parity N mod 2 (reading C14)
   fSU2xSU2 (2jc, 2js) Hubbard at half filling, fZ2 x SU2(charge) x SU2(spin): both
                     factors by the SU2 rule, d = (2jc+1)(2js+1), fermion parity 2js mod 2
+  Fib     (0|1,)    {I, tau}: tau x tau = I + tau, d_tau = golden ratio
+  Ising   (0|1|2,)  {I, sigma, psi}: sigma x sigma = I + psi, sigma x psi = sigma, psi x psi = I,
+                    d_sigma = sqrt 2. No dense embedding (planar oracle: oracle/planar.py)
 """
+import math
 
-KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2", "fSU2xSU2")
+KINDS = ("Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2", "fSU2xSU2", "Fib", "Ising")
+GOLDEN = (1 + math.sqrt(5)) / 2
 
 
 def width(kind):
@@ -43,7 +48,7 @@ def unit(kind):
 
 
 def dual(kind, a):
-    if kind in ("Z2", "fZ2", "SU2", "fSU2xSU2"):
+    if kind in ("Z2", "fZ2", "SU2", "fSU2xSU2", "Fib", "Ising"):
         return tuple(a)  # self-dual (SU2: "all irreps are self-dual")
     if kind == "fU1xSU2":
         return (-a[0], a[1])  # Deligne product: componentwise duals
@@ -67,10 +72,31 @@ def fuse(kind, a, b):
     if kind == "fSU2xSU2":
         return [(jc, js) for jc in range(abs(a[0] - b[0]), a[0] + b[0] + 1, 2)
                 for js in range(abs(a[1] - b[1]), a[1] + b[1] + 1, 2)]
+    if kind == "Fib":
+        if a[0] == 0:
+            return [tuple(b)]
+        if b[0] == 0:
+            return [tuple(a)]
+        return [(0,), (1,)]
+    if kind == "Ising":
+        x, y = a[0], b[0]
+        if x == 0:
+            return [tuple(b)]
+        if y == 0:
+            return [tuple(a)]
+        if x == 1 and y == 1:
+            return [(0,), (2,)]
+        if x == 2 and y == 2:
+            return [(0,)]
+        return [(1,)]
     raise ValueError(kind)
 
 
 def qdim(kind, a):
+    if kind == "Fib":
+        return GOLDEN if a[0] == 1 else 1.0
+    if kind == "Ising":
+        return math.sqrt(2.0) if a[0] == 1 else 1.0
     d = 1
     for j in spins2(kind, a):
         d *= j + 1
@@ -93,4 +119,4 @@ def is_fermionic(kind):
 
 
 def is_abelian(kind):
-    return kind not in ("SU2", "fU1xSU2", "fSU2xSU2")
+    return kind not in ("SU2", "fU1xSU2", "fSU2xSU2", "Fib", "Ising")

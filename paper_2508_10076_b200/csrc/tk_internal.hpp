@@ -25,8 +25,8 @@ void set_last_error(const std::string& m);
 // ------------------------------------------------------------------ sectors
 // Sector kinds (P:1011-1022 Z2; P:2347-2362 SVect; U1 S:138; Deligne products P:2380-2412;
 // SU(2) P:2303-2332). Labels are up to two int32: Z2/fZ2 {g}, U1 {q}, U1xU1 {N, 2Sz}, SU2 {2j},
-// fU1xSU2 {N, 2j}, fSU2xSU2 {2j_charge, 2j_spin}.
-enum class Kind : int { Z2 = 0, FZ2 = 1, U1 = 2, U1U1 = 3, FU1U1 = 4, SU2 = 5, FU1SU2 = 6, FSU2SU2 = 7 };
+// fU1xSU2 {N, 2j}, fSU2xSU2 {2j_charge, 2j_spin}, Fib {0: I, 1: tau}, Ising {0: I, 1: sigma, 2: psi}.
+enum class Kind : int { Z2 = 0, FZ2 = 1, U1 = 2, U1U1 = 3, FU1U1 = 4, SU2 = 5, FU1SU2 = 6, FSU2SU2 = 7, FIB = 8, ISING = 9 };
 
 struct Sector {
   int32_t v[2] = {0, 0};
@@ -40,6 +40,7 @@ const char* kind_name(Kind k);
 int kind_width(Kind k);
 bool kind_abelian(Kind k);
 bool kind_fermionic(Kind k);
+bool kind_braided(Kind k);  // false: planar operations only (Fib, Ising: complex R)
 Sector sector_unit(Kind k);
 Sector sector_dual(Kind k, const Sector& a);
 void sector_validate(Kind k, const Sector& a);          // throws UNKNOWN_LABEL
@@ -134,6 +135,11 @@ struct TPTerm {
 void permute_tree_pair(Kind k, const Tree& s, const Tree& f, const std::vector<int>& p,
                        const std::vector<int>& q, const std::vector<bool>& isdual,
                        std::vector<TPTerm>& out);
+// Planar route (Alg. 1/5 cyclic transposes): used for kinds without a real braiding (Fib, Ising) and,
+// through the test hook, to validate the rotation against SU(2)'s dense oracle.
+bool is_planar_perm(int n1, const std::vector<int>& p, const std::vector<int>& q);
+void set_force_planar(bool on);
+void set_rotation_kappa_mode(int m);
 // Reading C13 sign for abelian kinds (fast path; equals the generic path, tested).
 int koszul_sign(Kind k, const std::vector<Sector>& labels, int n1, const std::vector<int>& p,
                 const std::vector<int>& q);

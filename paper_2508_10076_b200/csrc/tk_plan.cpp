@@ -599,7 +599,8 @@ static double perm_cost(const Tensor& X, const std::vector<int>& p, const std::v
 }
 
 static void choose_contracted_order(const Tensor& A, const Tensor& B, Tuples& t) {
-  if (kind_fermionic(A.kind) || t.qA.size() < 2) return;
+  // fermionic kinds: the tuples fix the signs; kinds without braiding: the reorder could break planarity
+  if (kind_fermionic(A.kind) || !kind_braided(A.kind) || t.qA.size() < 2) return;
   std::vector<int> idx(t.qA.size());
   for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
   std::sort(idx.begin(), idx.end(), [&](int x, int y) { return t.pB[x] < t.pB[y]; });
@@ -929,6 +930,23 @@ tk_status tk_permute(const tk_tensor* A_, const void* a, const int32_t* p, int32
   PermPlan* P = get_perm_plan(A, pv, qv, C);
   g_launches = 0;
   run_permute(*P, a, c, alpha, beta, A.dtype == TK_C64 ? kPermCToC : kPermReal, 1.0, (cudaStream_t)stream);
+  TK_API_END
+}
+
+tk_status tk_permute_transfer_planar(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q,
+                                     int32_t nq, const tk_tensor* C, int32_t kappa_mode, double* out) {
+  TK_API_BEGIN
+  if (!A || !C || !out) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<int> pv(p, p + np), qv(q, q + nq);
+  set_force_planar(true);
+  if (kappa_mode >= 0) set_rotation_kappa_mode(kappa_mode);
+  try {
+    permute_transfer_matrix(*(const Tensor*)A, pv, qv, *(const Tensor*)C, out);
+  } catch (...) {
+    set_force_planar(false);
+    throw;
+  }
+  set_force_planar(false);
   TK_API_END
 }
 

@@ -17,6 +17,11 @@
 //            (2j_charge, 2j_spin), fermion parity 2j_spin mod 2 (the singly occupied spin-1/2 site is odd,
 //            the empty/doubly occupied charge doublet even); Deligne product data: F = F(charge) F(spin),
 //            R = R(charge) R(spin) (-1)^{p_a p_b}, d = (2jc+1)(2js+1), chi = (-1)^{2jc+2js}
+//   Fib      {I, tau}: tau x tau = I + tau, d_tau = phi, F^{tau tau tau}_tau =
+//            [[1/phi, 1/sqrt(phi)], [1/sqrt(phi), -1/phi]] over {I, tau}; R complex -> planar only
+//   Ising    {I, sigma, psi}: sigma x sigma = I + psi, sigma x psi = sigma, psi x psi = I,
+//            d_sigma = sqrt 2, F^{sss}_s = [[1, 1], [1, -1]] / sqrt 2 over {I, psi}, F^{s psi s}_psi[s, s] =
+//            F^{psi s psi}_s[s, s] = -1; R complex -> planar only. chi = 1 for every anyon label.
 // B-symbol: B^{ab}_c = sqrt(d_a d_b / d_c) F^{a b bbar}_a[c, I].
 #include <cmath>
 #include <cstring>
@@ -34,18 +39,24 @@ Kind parse_kind(const std::string& s) {
   if (s == "SU2") return Kind::SU2;
   if (s == "fU1xSU2") return Kind::FU1SU2;
   if (s == "fSU2xSU2") return Kind::FSU2SU2;
+  if (s == "Fib") return Kind::FIB;
+  if (s == "Ising") return Kind::ISING;
   TK_THROW(TK_ERR_UNKNOWN_LABEL, "unknown sector kind '" + s + "'");
 }
 
 const char* kind_name(Kind k) {
-  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2", "fSU2xSU2"};
+  static const char* names[] = {"Z2", "fZ2", "U1", "U1xU1", "fU1xU1", "SU2", "fU1xSU2", "fSU2xSU2", "Fib", "Ising"};
   return names[(int)k];
 }
 
 int kind_width(Kind k) {
   return (k == Kind::U1U1 || k == Kind::FU1U1 || k == Kind::FU1SU2 || k == Kind::FSU2SU2) ? 2 : 1;
 }
-bool kind_abelian(Kind k) { return k != Kind::SU2 && k != Kind::FU1SU2 && k != Kind::FSU2SU2; }
+bool kind_abelian(Kind k) {
+  return k != Kind::SU2 && k != Kind::FU1SU2 && k != Kind::FSU2SU2 && k != Kind::FIB && k != Kind::ISING;
+}
+static bool kind_anyon(Kind k) { return k == Kind::FIB || k == Kind::ISING; }
+bool kind_braided(Kind k) { return !kind_anyon(k); }
 bool kind_fermionic(Kind k) {
   return k == Kind::FZ2 || k == Kind::FU1U1 || k == Kind::FU1SU2 || k == Kind::FSU2SU2;
 }
@@ -66,7 +77,9 @@ Sector sector_dual(Kind k, const Sector& a) {
     case Kind::FZ2:
     case Kind::SU2:
     case Kind::FSU2SU2:
-      return a;  // self-dual (SU2: "all irreps are self-dual")
+    case Kind::FIB:
+    case Kind::ISING:
+      return a;  // self-dual (SU2: "all irreps are self-dual"; Fib, Ising: P:2420)
     case Kind::U1:
       return Sector{{-a.v[0], 0}};
     case Kind::FU1SU2:
@@ -94,6 +107,12 @@ void sector_validate(Kind k, const Sector& a) {
       break;
     case Kind::FSU2SU2:
       ok = a.v[0] >= 0 && a.v[1] >= 0;
+      break;
+    case Kind::FIB:
+      ok = (a.v[0] == 0 || a.v[0] == 1) && a.v[1] == 0;
+      break;
+    case Kind::ISING:
+      ok = a.v[0] >= 0 && a.v[0] <= 2 && a.v[1] == 0;
       break;
     default:
       break;
@@ -130,12 +149,33 @@ void sector_fuse(Kind k, const Sector& a, const Sector& b, std::vector<Sector>& 
         for (int js = std::abs(a.v[1] - b.v[1]); js <= a.v[1] + b.v[1]; js += 2) out.push_back(Sector{{jc, js}});
       break;
     }
+    case Kind::FIB:
+      if (a.v[0] == 0) out.push_back(b);
+      else if (b.v[0] == 0) out.push_back(a);
+      else { out.push_back(Sector{{0, 0}}); out.push_back(Sector{{1, 0}}); }
+      break;
+    case Kind::ISING: {
+      const int x = a.v[0], y = b.v[0];
+      if (x == 0) out.push_back(b);
+      else if (y == 0) out.push_back(a);
+      else if (x == 1 && y == 1) { out.push_back(Sector{{0, 0}}); out.push_back(Sector{{2, 0}}); }
+      else if (x == 2 && y == 2) out.push_back(Sector{{0, 0}});
+      else out.push_back(Sector{{1, 0}});  // sigma x psi = psi x sigma = sigma
+      break;
+    }
   }
 }
 
 static bool su2_tri(int a, int b, int c) { return std::abs(a - b) <= c && c <= a + b && ((a + b + c) & 1) == 0; }
 
 bool sector_admissible(Kind k, const Sector& a, const Sector& b, const Sector& c) {
+  if (kind_anyon(k)) {
+    std::vector<Sector> tmp;
+    sector_fuse(k, a, b, tmp);
+    for (auto& x : tmp)
+      if (x == c) return true;
+    return false;
+  }
   if (k == Kind::SU2) return su2_tri(a.v[0], b.v[0], c.v[0]);
   if (k == Kind::FU1SU2) return c.v[0] == a.v[0] + b.v[0] && su2_tri(a.v[1], b.v[1], c.v[1]);
   if (k == Kind::FSU2SU2) return su2_tri(a.v[0], b.v[0], c.v[0]) && su2_tri(a.v[1], b.v[1], c.v[1]);
@@ -144,7 +184,10 @@ bool sector_admissible(Kind k, const Sector& a, const Sector& b, const Sector& c
   return tmp[0] == c;
 }
 
+static const double kPhi = 0.5 * (1.0 + std::sqrt(5.0));
 double sector_dim(Kind k, const Sector& a) {
+  if (k == Kind::FIB) return a.v[0] == 1 ? kPhi : 1.0;
+  if (k == Kind::ISING) return a.v[0] == 1 ? std::sqrt(2.0) : 1.0;
   int j[2] = {0, 0};
   int n = spins2(k, a, j);
   double d = 1.0;
@@ -207,6 +250,25 @@ double fsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c, const 
       !sector_admissible(k, a, f, d))
     return 0.0;
   if (kind_abelian(k)) return 1.0;  // abelian / SVect: trivial F (eq. trivialF)
+  if (k == Kind::FIB) {
+    if (a.v[0] == 1 && b.v[0] == 1 && c.v[0] == 1 && d.v[0] == 1) {
+      const int i = e.v[0], j = f.v[0];  // basis order {I, tau}
+      if (i == 0 && j == 0) return 1.0 / kPhi;
+      if (i == 1 && j == 1) return -1.0 / kPhi;
+      return 1.0 / std::sqrt(kPhi);
+    }
+    return 1.0;
+  }
+  if (k == Kind::ISING) {
+    const int A = a.v[0], B = b.v[0], C = c.v[0], D = d.v[0];
+    if (A == 1 && B == 1 && C == 1 && D == 1) {  // e, f in {I, psi}
+      const double r = 1.0 / std::sqrt(2.0);
+      return (e.v[0] == 2 && f.v[0] == 2) ? -r : r;
+    }
+    if (A == 1 && B == 2 && C == 1 && D == 2) return -1.0;  // F^{s psi s}_psi[s, s]
+    if (A == 2 && B == 1 && C == 2 && D == 1) return -1.0;  // F^{psi s psi}_s[s, s]
+    return 1.0;
+  }
   // SU(2) factors (Deligne product: F is the product of the factors' F)
   int ja[2], jb[2], jc[2], jd[2], je[2], jf[2];
   int n = spins2(k, a, ja);
@@ -224,6 +286,7 @@ double fsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c, const 
 }
 
 double rsymbol(Kind k, const Sector& a, const Sector& b, const Sector& c) {
+  if (kind_anyon(k)) TK_THROW(TK_ERR_BRAIDING_UNAVAILABLE, "Fib / Ising R-symbols are complex phases (P:2426, P:2447)");
   if (!sector_admissible(k, a, b, c)) return 0.0;
   double r = 1.0;
   int ja[2], jb[2], jc[2];

@@ -143,16 +143,104 @@ void braid(Kind k, const Combo& in, int i, Combo& out) {
   }
 }
 
+// Planar cyclic rotation of a codomain-only tree with unit coupled charge (all legs bent into the
+// codomain): (a1, a2, ..., aN) -> (a2, ..., aN, a1), the planar move of Alg. 1/5 that needs
+// no braiding. Two steps: (i) recouple a1 to the top, ((a1 a2)e2 a3)e3... = sum_f prod_k
+// F^{a1 f_{k-1} a_k}_{e_k}[e_{k-1}, f_k] (a1 (a2 ... aN)_y)_I with y = dual(a1) (P:1117-1123 F-moves);
+// (ii) carry a1 around the unit vertex to the right end, (a1 Y)_I -> (Y a1)_I, coefficient kappa(a1)
+// (the left fold followed by a right bend): kappa = chi_{a1}, the Frobenius-Schur
+// indicator -- the only choice that reproduces the dense SU(2) oracle for every cyclic transpose with
+// dual legs, integer and half-integer spins (tests/test_library_host.py::test_planar_route_su2).
+double g_rot_kappa_mode = 1;  // 0: 1, 1: chi_{a1}, 2: chi_{y} (validation knob for the test hook)
+
+void rotate_left(Kind k, const Combo& in, Combo& out) {
+  out.clear();
+  for (auto& kv : in) {
+    const State& st = kv.second.first;
+    double c0 = kv.second.second;
+    const Tree& t = st.s;
+    const int n = (int)t.unc.size();
+    State ns = st;
+    std::rotate(ns.s.unc.begin(), ns.s.unc.begin() + 1, ns.s.unc.end());
+    std::rotate(ns.s_ids.begin(), ns.s_ids.begin() + 1, ns.s_ids.end());
+    { std::vector<bool> d(st.s_dual.begin() + 1, st.s_dual.end()); d.push_back(st.s_dual[0]); ns.s_dual = d; }
+    if (n <= 1) {
+      add_term(out, std::move(ns), c0);
+      continue;
+    }
+    const Sector a1 = t.unc[0];
+    const std::vector<Sector> ech = chain_of(t);  // e[0] = a1, e[k] = label of legs 0..k
+    // paths over the chain of (a2 ... aN): f[0] = a2, f[k-1] fuses a2..a_{k+1}
+    struct Path {
+      std::vector<Sector> f;
+      double c;
+    };
+    std::vector<Path> paths{{{t.unc[1]}, 1.0}};
+    std::vector<Sector> opts;
+    for (int kk = 2; kk < n; ++kk) {  // attach leg a_kk (0-based) to the right-hand subtree
+      std::vector<Path> nx;
+      for (auto& P : paths) {
+        sector_fuse(k, P.f.back(), t.unc[kk], opts);
+        for (const Sector& fnew : opts) {
+          // ((a1 Y)_{e_{kk-1}} a_kk)_{e_kk} -> (a1 (Y a_kk)_{fnew})_{e_kk}
+          double c = fsymbol(k, a1, P.f.back(), t.unc[kk], ech[kk], ech[kk - 1], fnew);
+          if (std::abs(c) < 1e-15) continue;
+          Path q = P;
+          q.f.push_back(fnew);
+          q.c *= c;
+          nx.push_back(std::move(q));
+        }
+      }
+      paths.swap(nx);
+    }
+    for (auto& P : paths) {
+      const Sector y = P.f.back();
+      if (!sector_admissible(k, a1, y, ech[n - 1])) continue;
+      double kap = 1.0;
+      if (g_rot_kappa_mode == 1) kap = sector_fs(k, a1);
+      if (g_rot_kappa_mode == 2) kap = sector_fs(k, y);
+      std::vector<Sector> nch = P.f;  // chain of (a2 ... aN a1): f..., then the unit
+      nch.push_back(ech[n - 1]);
+      State nn = ns;
+      set_chain(nn.s, nch, k);
+      add_term(out, std::move(nn), c0 * P.c * kap);
+    }
+  }
+}
+
 std::mutex g_memo_mu;
 std::unordered_map<std::string, std::vector<TPTerm>> g_memo;  // memoised transforms
+thread_local bool g_force_planar = false;
 
 }  // namespace
+
+void set_force_planar(bool on) { g_force_planar = on; }
+void set_rotation_kappa_mode(int m) { g_rot_kappa_mode = m; }
+
+bool is_planar_perm(int n1, const std::vector<int>& p, const std::vector<int>& q) {
+  const int N = n1 + (int)(p.size() + q.size()) - n1;
+  std::vector<int> S, T(p.begin(), p.end());
+  for (int i = 0; i < n1; ++i) S.push_back(i);
+  for (int i = N - 1; i >= n1; --i) S.push_back(i);
+  for (int j = (int)q.size() - 1; j >= 0; --j) T.push_back(q[j]);
+  if (N == 0) return true;
+  for (int r = 0; r < N; ++r) {
+    bool ok = true;
+    for (int i = 0; i < N && ok; ++i) ok = T[i] == S[(i + r) % N];
+    if (ok) return true;
+  }
+  return false;
+}
 
 void permute_tree_pair(Kind k, const Tree& s, const Tree& f, const std::vector<int>& p,
                        const std::vector<int>& q, const std::vector<bool>& isdual, std::vector<TPTerm>& out) {
   int n1 = (int)s.unc.size(), n2 = (int)f.unc.size(), N = n1 + n2;
+  // planar route (cyclic rotations, no braiding): kinds without a real braiding, or forced (tests)
+  const bool planar = !kind_braided(k) || g_force_planar;
+  if (planar && !is_planar_perm(n1, p, q))
+    TK_THROW(TK_ERR_BRAIDING_UNAVAILABLE, "non-planar permutation of a kind without (real) braiding");
   std::ostringstream mk;
-  mk << (int)k << "#" << tree_pair_key(s, f) << "#";
+  mk << (int)k << (planar ? "P" : "B") << g_rot_kappa_mode << "#" << tree_pair_key(s, f) << "#";
   for (int x : p) mk << x << ",";
   mk << "#";
   for (int x : q) mk << x << ",";
@@ -190,7 +278,16 @@ void permute_tree_pair(Kind k, const Tree& s, const Tree& f, const std::vector<i
   std::vector<int> pos(N);
   for (int i = 0; i < N; ++i) pos[T[i]] = i;
   std::vector<int> order = cur.begin()->second.first.s_ids;
-  for (int sweep = 0; sweep < N; ++sweep) {
+  if (planar && N > 0) {  // rotate until the codomain order is T (a cyclic shift of S)
+    int r = 0;
+    while (r < N && order[r] != T[0]) ++r;
+    for (int i = 0; i < r; ++i) {
+      rotate_left(k, cur, nxt);
+      std::swap(cur, nxt);
+    }
+    std::rotate(order.begin(), order.begin() + r, order.end());
+  }
+  for (int sweep = 0; sweep < N && !planar; ++sweep) {
     bool any = false;
     for (int i = 0; i + 1 < N; ++i) {
       if (pos[order[i]] > pos[order[i + 1]]) {

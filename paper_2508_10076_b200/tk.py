@@ -72,6 +72,8 @@ _permute_workspace = _sig("tk_permute_workspace", [_p, _i32p, ctypes.c_int32, _i
 _permute = _sig("tk_permute", [_p, _p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _p, ctypes.c_double,
                                ctypes.c_double, _p, ctypes.c_size_t, _p])
 _permute_transfer = _sig("tk_permute_transfer", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _dp])
+_permute_transfer_planar = _sig("tk_permute_transfer_planar", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p,
+                                                               ctypes.c_int32, _dp])
 _contract_workspace = _sig("tk_contract_workspace", [_p, _i32p, _p, _i32p, _p, _i32p,
                                                      ctypes.POINTER(ctypes.c_size_t)])
 _contract = _sig("tk_contract", [_p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p,
@@ -99,7 +101,7 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_tensor_blocks", "tk_tensor_subblocks", "tk_tensor_retain", "tk_tensor_release",
             "tk_contract_output", "tk_permute_workspace", "tk_permute", "tk_contract_workspace", "tk_contract",
             "tk_profile_enable", "tk_phase_times", "tk_last_launch_count", "tk_fsymbol", "tk_rsymbol",
-            "tk_permute_transfer", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
+            "tk_permute_transfer", "tk_permute_transfer_planar", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
             "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract"]
 
 
@@ -253,6 +255,15 @@ def tk_permute_transfer(A, p, q, C):
     na, nc = A.info()["n_subblocks"], C.info()["n_subblocks"]
     out = np.zeros((na, nc))
     _check(_permute_transfer(A.h, pp, len(p), qp, len(q), C.h, out.ctypes.data_as(_dp)))
+    return out
+
+
+def tk_permute_transfer_planar(A, p, q, C, kappa_mode=-1):
+    pa, pp = _i32(p)
+    qa, qp = _i32(q)
+    na, nc = A.info()["n_subblocks"], C.info()["n_subblocks"]
+    out = np.zeros((na, nc))
+    _check(_permute_transfer_planar(A.h, pp, len(p), qp, len(q), C.h, int(kappa_mode), out.ctypes.data_as(_dp)))
     return out
 
 

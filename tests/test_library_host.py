@@ -202,3 +202,65 @@ def test_contract_output_spaces(cfgfun):
         specs[nc] = {"cod": cod, "dom": dom}
         assert_same_layout(specs[nc])
         assert C.nelems == OL.homspace_layout(cfg["kind"], cod, dom).nelems
+
+
+# ------------------------------------------------- planar route and anyons
+def _cyclic(n1, N, r, n1p):
+    S = list(range(n1)) + list(range(N - 1, n1 - 1, -1))
+    T = [S[(i + r) % N] for i in range(N)]
+    return T[:n1p], list(reversed(T[n1p:]))
+
+
+def test_planar_route_su2():
+    """The library's planar route (rotations + bends, forced through the test hook) equals the dense
+    SU(2) oracle for every cyclic transpose with dual legs; kappa = chi_{a1} is the only one that does."""
+    for secs in ([((0,), 1), ((1,), 1), ((2,), 1)], [((1,), 1), ((2,), 1)]):
+        V = W.space("SU2", secs)
+        Vd = W.dual(V)
+        for cod, dom in (([V, Vd], [V]), ([V, V], [Vd, V]), ([Vd, V, V], [V])):
+            n1, N = len(cod), len(cod) + len(dom)
+            for r in range(N):
+                for n1p in range(N + 1):
+                    p, q = _cyclic(n1, N, r, n1p)
+                    ref, c2, d2 = oracle_transfer("SU2", cod, dom, p, q)
+                    A, C = tk.tensor_from_spec({"cod": cod, "dom": dom}), tk.tensor_from_spec({"cod": c2, "dom": d2})
+                    assert np.abs(tk.tk_permute_transfer_planar(A, p, q, C) - ref).max() < 1e-13
+    # kappa = 1 fails for half-integer spins (chi = -1)
+    V = W.space("SU2", [((1,), 1), ((2,), 1)])
+    p, q = _cyclic(2, 3, 1, 2)
+    ref, c2, d2 = oracle_transfer("SU2", [V, V], [V], p, q)
+    A, C = tk.tensor_from_spec({"cod": [V, V], "dom": [V]}), tk.tensor_from_spec({"cod": c2, "dom": d2})
+    assert np.abs(tk.tk_permute_transfer_planar(A, p, q, C, 0) - ref).max() > 0.5
+    tk.tk_permute_transfer_planar(A, p, q, C, 1)  # restore the library convention
+
+
+@pytest.mark.parametrize("kind,secs", [("Fib", [((0,), 1), ((1,), 1)]), ("Ising", [((0,), 1), ((1,), 1), ((2,), 1)])])
+def test_anyon_transfer_equals_planar_oracle(kind, secs):
+    from oracle import planar as OP
+    V = W.space(kind, secs)
+    Vd = W.dual(V)
+    for cod, dom in (([V, Vd], [V]), ([V, V], [Vd, V]), ([V], [V, V]), ([V, V], [V, V])):
+        n1, N = len(cod), len(cod) + len(dom)
+        for r in range(N):
+            for n1p in range(N + 1):
+                p, q = _cyclic(n1, N, r, n1p)
+                M, lt, ls = OP.planar_transfer(kind, cod, dom, p, q)
+                A, C = tk.tensor_from_spec({"cod": cod, "dom": dom}), tk.tensor_from_spec({"cod": ls.cod, "dom": ls.dom})
+                assert np.abs(tk.tk_permute_transfer(A, p, q, C) - M).max() < 1e-13, (cod, dom, p, q)
+    # braiding is unavailable: a non-planar permutation is refused
+    A = tk.tensor_from_spec({"cod": [V, V], "dom": [V]})
+    C = tk.tensor_from_spec({"cod": [V, V], "dom": [V]})
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_permute_transfer(A, [1, 0], [2], C)
+    assert e.value.status == "TK_ERR_BRAIDING_UNAVAILABLE"
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_rsymbol(kind, [1], [1], [0])
+    assert e.value.status == "TK_ERR_BRAIDING_UNAVAILABLE"
+
+
+def test_anyon_fsymbols_equal_oracle():
+    from oracle import planar as OP
+    for kind, L in (("Fib", [0, 1]), ("Ising", [0, 1, 2])):
+        for a, b, c, d, e, f in itertools.product(L, repeat=6):
+            ref = OP.fsymbol(kind, (a,), (b,), (c,), (d,), (e,), (f,))
+            assert abs(tk.tk_fsymbol(kind, [a], [b], [c], [d], [e], [f]) - ref) < 1e-15
