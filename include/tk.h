@@ -178,6 +178,25 @@ tk_status tk_svd_extract(const tk_tensor* A, const int32_t* p, int32_t np, const
                          const void* ws, const tk_tensor* U, void* u, const tk_tensor* S, void* s,
                          const tk_tensor* Vh, void* vh, tk_stream stream);
 
+/* ---------------------------------------------------------- partial trace */
+/* C = alpha * permute(trace(A, (pt, qt)), (p, q)) + beta * C (Alg. 3, Alg. 7 P:1225-1257,
+ * fusion-tree traces P:1880-1904). nt pairs (1..4): leg pt[i] of A, read as a codomain leg (Alg. 3's
+ * "(a_1 ...; b_1^* ...)"), is contracted with leg qt[i], read as a domain leg; they must be a ket/bra pair
+ * of one space (else TK_ERR_SPACE_MISMATCH). (p, q) arrange the remaining legs (indices of A's legs);
+ * C's spaces follow the Alg. 2 selection rule (tk_trace_output). Planar kinds (Fib, Ising) need the pairs
+ * nested in the cyclic leg order; fermionic kinds -> TK_ERR_UNSUPPORTED; Float64 only. Workspace:
+ * tk_trace_workspace bytes (A permuted so the pairs close at the tree ends), 256-byte aligned. */
+tk_status tk_trace_output(const tk_tensor* A, const int32_t* pt, const int32_t* qt, int32_t nt, const int32_t* p,
+                          int32_t np, const int32_t* q, int32_t nq, tk_tensor** C);
+tk_status tk_trace_workspace(const tk_tensor* A, const int32_t* pt, const int32_t* qt, int32_t nt, const int32_t* p,
+                             int32_t np, const int32_t* q, int32_t nq, const tk_tensor* C, size_t* bytes);
+tk_status tk_trace(const tk_tensor* A, const void* a, const int32_t* pt, const int32_t* qt, int32_t nt,
+                   const int32_t* p, int32_t np, const int32_t* q, int32_t nq, const tk_tensor* C, void* c,
+                   double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream);
+/* Host transfer matrix of the trace on tree pairs (A subblocks x C subblocks); tests / §4.3 example. */
+tk_status tk_trace_transfer(const tk_tensor* A, const int32_t* pt, const int32_t* qt, int32_t nt, const int32_t* p,
+                            int32_t np, const int32_t* q, int32_t nq, const tk_tensor* C, double* out);
+
 /* --------------------------------------------------------------- instrumentation */
 /* Per-phase CUDA-event timing of the NEXT tk_contract call(s) on the same thread: when
  * enabled, tk_contract records events around each launch on its stream; tk_phase_times

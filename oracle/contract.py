@@ -139,3 +139,17 @@ def rel_frobenius(X, Y):
     """||X - Y||_F / ||Y||_F."""
     ny = np.linalg.norm(Y.ravel())
     return float(np.linalg.norm((X - Y).ravel()) / (ny if ny > 0 else 1.0))
+
+
+def partial_trace_dense(D, cod, dom, pt, qt, p, q):
+    """Plain partial trace (Alg. 3) of a dense bosonic tensor: legs pt[i] and qt[i] carry the
+    same dense index set (ket/bra pair) and are summed with a delta (the evaluation map),
+    then the remaining legs are arranged as (p..., q...). Returns (dense result, C cod, C dom)."""
+    N = D.ndim
+    letters = [_LETTERS[i] for i in range(N)]
+    for a, b in zip(pt, qt):
+        letters[b] = letters[a]
+    out = "".join(letters[i] for i in list(p) + list(q))
+    R = np.einsum("".join(letters) + "->" + out, D)
+    c2, d2 = permuted_spaces(cod, dom, p, q)
+    return R, c2, d2

@@ -226,3 +226,62 @@ def contract_planar(kind, A_spec, xa, labA, B_spec, xb, labB, labC, n_cod_C):
         Mb = Bt[bo:bo + br * bc].reshape(br, bc, order="F")
         Ct[off:off + rows * cols] = (Ma @ Mb).reshape(-1, order="F")
     return apply_planar(kind, lc.cod, lc.dom, Ct, pAB, qAB)
+
+
+def _peel_key(kind, unc, inner, coupled):
+    """Tree without its last leg: (unc, inner, coupled)."""
+    n = len(unc)
+    if n == 1:
+        return (), (), sectors.unit(kind)
+    if n == 2:
+        return (tuple(unc[0]),), (), tuple(unc[0])
+    return tuple(map(tuple, unc[:-1])), tuple(map(tuple, inner[:-1])), tuple(inner[-1])
+
+
+def trace_planar(kind, cod, dom, flat, pt, qt, p, q):
+    """Partial trace by tree manipulations: permute so that the traced pairs close at the
+    ends of the trees, (p..., pt... ; q..., qt...), then close the last splitting leg with the last
+    fusion leg: both trees lose that leg, their new coupled labels must agree (e), and the loop leaves
+    the factor d_c / d_e (the tadpole). Returns (reduced data of C, C's layout)."""
+    from .dense import subblock_array
+    nt = len(pt)
+    At, la = apply_planar(kind, cod, dom, flat, list(p) + list(pt), list(q) + list(qt))
+    from .contract import permuted_spaces
+    c2, d2 = permuted_spaces(cod, dom, p, q)
+    lc = homspace_layout(kind, c2, d2)
+    index = {(tuple(map(tuple, sb.key[0])), tuple(map(tuple, sb.key[1])), tuple(sb.key[2]),
+              tuple(map(tuple, sb.key[3])), tuple(map(tuple, sb.key[4]))): j for j, sb in enumerate(lc.subblocks)}
+    out = np.zeros(lc.nelems)
+    n1, n2 = len(p), len(q)
+    for sb in la.subblocks:
+        s_unc, s_inn, c, f_unc, f_inn = sb.key
+        s = (list(s_unc), list(s_inn), tuple(c))
+        f = (list(f_unc), list(f_inn), tuple(c))
+        coef, ok = 1.0, True
+        for _ in range(nt):
+            if tuple(s[0][-1]) != tuple(f[0][-1]):
+                ok = False
+                break
+            cc = s[2]
+            s = _peel_key(kind, *s)
+            f = _peel_key(kind, *f)
+            if tuple(s[2]) != tuple(f[2]):
+                ok = False
+                break
+            coef *= sectors.qdim(kind, cc) / sectors.qdim(kind, s[2])
+            s = (list(s[0]), list(s[1]), s[2])
+            f = (list(f[0]), list(f[1]), f[2])
+        if not ok:
+            continue
+        key = (tuple(map(tuple, s[0])), tuple(map(tuple, s[1])), tuple(s[2]), tuple(map(tuple, f[0])),
+               tuple(map(tuple, f[1])))
+        j = index[key]
+        x = np.asarray(subblock_array(la, At, sb))  # legs (p..., pt..., q..., qt...)
+        letters = "abcdefghijklmnop"
+        L = [letters[i] for i in range(x.ndim)]
+        for r in range(nt):
+            L[n1 + nt + n2 + r] = L[n1 + r]
+        outl = "".join(L[:n1] + L[n1 + nt:n1 + nt + n2])
+        y = np.einsum("".join(L) + "->" + outl, x)
+        subblock_array(lc, out, lc.subblocks[j])[...] += coef * y
+    return out, lc

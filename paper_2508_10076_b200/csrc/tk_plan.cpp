@@ -37,7 +37,7 @@ void validate_perm(const Tensor& A, const std::vector<int>& p, const std::vector
 }
 
 // Space selection rule of Alg. 2.
-static void permuted_spaces(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q,
+void permuted_spaces(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q,
                             std::vector<Space*>& cod, std::vector<Space*>& dom) {
   int n1 = A.n_cod();
   auto leg = [&](int i) -> Space* { return i < n1 ? A.cod[i] : A.dom[i - n1]; };
@@ -839,6 +839,7 @@ void cache_clear() {
     g_perm_cache.clear();
   }
   svd_cache_clear();
+  trace_cache_clear();
 }
 
 // ------------------------------------------------------------------ profiling state

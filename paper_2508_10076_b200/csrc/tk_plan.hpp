@@ -65,6 +65,12 @@ struct PadLayout {
 
 PadLayout pad_layout(const Tensor& t, PadKind kind = PadKind::Real);
 void validate_perm(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q);
+// Alg. 2 selection rule: spaces of permute(A, (p, q)) (new references, release after use)
+void permuted_spaces(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q,
+                     std::vector<Space*>& cod, std::vector<Space*>& dom);
+void trace_cache_clear();
+void permute_transfer_matrix(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
+                             double* out);
 void check_target(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C);
 void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C,
                      PermPlan& P, int elem_bytes, const PadLayout* spl = nullptr, const PadLayout* dpl = nullptr);

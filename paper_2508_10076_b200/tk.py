@@ -93,6 +93,14 @@ _svd_truncate = _sig("tk_svd_truncate", [_p, _i32p, ctypes.c_int32, _i32p, ctype
                                          ctypes.POINTER(_p), ctypes.POINTER(_p), _dp, _dp])
 _svd_extract = _sig("tk_svd_extract", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _p, _p, _p, _p, _p,
                                        _p, _p])
+_trace_output = _sig("tk_trace_output", [_p, _i32p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32,
+                                         ctypes.POINTER(_p)])
+_trace_workspace = _sig("tk_trace_workspace", [_p, _i32p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _i32p,
+                                               ctypes.c_int32, _p, ctypes.POINTER(ctypes.c_size_t)])
+_trace = _sig("tk_trace", [_p, _p, _i32p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _p, _p,
+                           ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
+_trace_transfer = _sig("tk_trace_transfer", [_p, _i32p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _i32p,
+                                             ctypes.c_int32, _p, _dp])
 _cache_clear = _sig("tk_cache_clear", [], None)
 _version = _sig("tk_version", [], ctypes.c_char_p)
 
@@ -102,7 +110,8 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_contract_output", "tk_permute_workspace", "tk_permute", "tk_contract_workspace", "tk_contract",
             "tk_profile_enable", "tk_phase_times", "tk_last_launch_count", "tk_fsymbol", "tk_rsymbol",
             "tk_permute_transfer", "tk_permute_transfer_planar", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
-            "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract"]
+            "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract", "tk_trace_output", "tk_trace_workspace",
+            "tk_trace", "tk_trace_transfer"]
 
 
 def _i32(seq):
@@ -364,6 +373,37 @@ def tk_svd_extract(A, p, q, ws, U, u, S, s, Vh, vh, stream=None):
     qa, qp = _i32(q)
     _check(_svd_extract(A.h, pp, len(p), qp, len(q), _ptr(ws), U.h, _ptr(u), S.h, _ptr(s), Vh.h, _ptr(vh),
                         _stream(stream)))
+
+
+def _trace_args(pt, qt, p, q):
+    a = [_i32(x) for x in (pt, qt, p, q)]
+    return a, (a[0][1], a[1][1], len(pt), a[2][1], len(p), a[3][1], len(q))
+
+
+def tk_trace_output(A, pt, qt, p, q):
+    keep, args = _trace_args(pt, qt, p, q)
+    h = _p()
+    _check(_trace_output(A.h, *args, ctypes.byref(h)))
+    return Tensor(h.value)
+
+
+def tk_trace_workspace(A, pt, qt, p, q, C):
+    keep, args = _trace_args(pt, qt, p, q)
+    n = ctypes.c_size_t()
+    _check(_trace_workspace(A.h, *args, C.h, ctypes.byref(n)))
+    return n.value
+
+
+def tk_trace(A, a, pt, qt, p, q, C, c, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, stream=None):
+    keep, args = _trace_args(pt, qt, p, q)
+    _check(_trace(A.h, _ptr(a), *args, C.h, _ptr(c), float(alpha), float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def tk_trace_transfer(A, pt, qt, p, q, C):
+    keep, args = _trace_args(pt, qt, p, q)
+    out = np.zeros((A.info()["n_subblocks"], C.info()["n_subblocks"]))
+    _check(_trace_transfer(A.h, *args, C.h, out.ctypes.data_as(_dp)))
+    return out
 
 
 def tk_cache_clear():

@@ -264,3 +264,77 @@ def test_anyon_fsymbols_equal_oracle():
         for a, b, c, d, e, f in itertools.product(L, repeat=6):
             ref = OP.fsymbol(kind, (a,), (b,), (c,), (d,), (e,), (f,))
             assert abs(tk.tk_fsymbol(kind, [a], [b], [c], [d], [e], [f]) - ref) < 1e-15
+
+
+# --------------------------------------------------------------- partial trace (NEXT-4)
+def test_trace_golden_P1892():
+    """§4.3's printed partial-trace matrix (reading C11: codomain leg 2 with domain leg 2)."""
+    from tests.test_oracle_golden import load_matrix
+    V = W.space("SU2", [((0,), 1), ((1,), 1)])
+    A = tk.tensor_from_spec({"cod": [V, V], "dom": [V, V]})
+    C = tk.tk_trace_output(A, [1], [3], [0], [2])
+    M = tk.tk_trace_transfer(A, [1], [3], [0], [2], C)
+    assert np.abs(M - load_matrix("su2_trace_P1892.txt")).max() < 1e-14
+
+
+def _dense_trace_transfer(kind, cod, dom, pt, qt, p, q):
+    lt = OL.homspace_layout(kind, cod, dom)
+    c2, d2 = OC.permuted_spaces(cod, dom, p, q)
+    lc = OL.homspace_layout(kind, c2, d2)
+    M = np.zeros((len(lt.subblocks), len(lc.subblocks)))
+    for i, sb in enumerate(lt.subblocks):
+        x = np.zeros(lt.nelems)
+        x[sb.offset] = 1.0
+        R, _, _ = OC.partial_trace_dense(OD.to_dense(lt, x), cod, dom, pt, qt, p, q)
+        y = OD.from_dense(lc, R)
+        for j, sc in enumerate(lc.subblocks):
+            M[i, j] = y[sc.offset]
+    return M, c2, d2
+
+
+@pytest.mark.parametrize("kind,secs", [("U1", [((-1,), 1), ((0,), 1), ((1,), 1)]),
+                                       ("SU2", [((0,), 1), ((1,), 1), ((2,), 1)]),
+                                       ("SU2", [((1,), 1), ((2,), 1)])])
+def test_trace_transfer_vs_dense(kind, secs):
+    V = W.space(kind, secs)
+    Vd = W.dual(V)
+    cases = [([V, V], [V, V], [1], [3], [0], [2]), ([V, V], [V, V], [0], [2], [3], [1]),
+             ([V, V], [V, V], [0], [3], [1], [2]), ([V, Vd, V], [V, V], [2], [4], [1, 0], [3]),
+             ([V, V], [V, V], [0, 1], [2, 3], [], []), ([Vd, V], [Vd, V], [0], [2], [1], [3]),
+             ([V, Vd, V], [V], [0], [1], [2], [3])]   # a codomain V with a codomain V*: ket/bra
+    for cod, dom, pt, qt, p, q in cases:
+        ref, c2, d2 = _dense_trace_transfer(kind, cod, dom, pt, qt, p, q)
+        A = tk.tensor_from_spec({"cod": cod, "dom": dom})
+        C = tk.tk_trace_output(A, pt, qt, p, q)   # rank 0 for full traces
+        assert np.abs(tk.tk_trace_transfer(A, pt, qt, p, q, C) - ref).max() < 1e-13, (pt, qt, p, q)
+
+
+def test_trace_errors():
+    V = W.space("U1", [((-1,), 1), ((1,), 2)])
+    A = tk.tensor_from_spec({"cod": [V, V], "dom": [V, V]})
+    with pytest.raises(tk.TKError) as e:   # two kets of V
+        tk.tk_trace_output(A, [0], [1], [2], [3])
+    assert e.value.status == "TK_ERR_SPACE_MISMATCH"
+    F = W.space("fU1xU1", [((0, 0), 1), ((1, 1), 1)])
+    B = tk.tensor_from_spec({"cod": [F, F], "dom": [F, F]})
+    with pytest.raises(tk.TKError) as e:
+        tk.tk_trace_output(B, [1], [3], [0], [2])
+    assert e.value.status == "TK_ERR_UNSUPPORTED"
+
+
+@pytest.mark.parametrize("kind,secs", [("Fib", [((0,), 1), ((1,), 1)]), ("Ising", [((0,), 1), ((1,), 1), ((2,), 1)])])
+def test_anyon_trace_vs_planar_oracle(kind, secs):
+    from oracle import planar as OP
+    V = W.space(kind, secs)
+    for cod, dom, pt, qt, p, q in (([V, V], [V, V], [1], [3], [0], [2]), ([V, V], [V, V], [2], [0], [1, 3], []),
+                                   ([V, V], [V, V], [0, 1], [2, 3], [], [])):
+        lt = OL.homspace_layout(kind, cod, dom)
+        A = tk.tensor_from_spec({"cod": cod, "dom": dom})
+        C = tk.tk_trace_output(A, pt, qt, p, q)
+        got = tk.tk_trace_transfer(A, pt, qt, p, q, C)
+        for i, sb in enumerate(lt.subblocks):
+            x = np.zeros(lt.nelems)
+            x[sb.offset] = 1.0
+            y, lc = OP.trace_planar(kind, cod, dom, x, pt, qt, p, q)
+            ref = np.array([y[sc.offset] for sc in lc.subblocks])
+            assert np.abs(got[i] - ref).max() < 1e-13

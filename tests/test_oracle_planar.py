@@ -91,3 +91,22 @@ def test_full_rotation_identity_and_unitarity(kind, secs):
             total = M if total is None else total @ M
             c, d = ls.cod, ls.dom
         assert np.abs(total - np.eye(total.shape[0])).max() < 1e-12
+
+
+@pytest.mark.parametrize("secs", [[((0,), 2), ((1,), 1), ((2,), 1)], [((1,), 2), ((2,), 1)]])
+def test_tree_trace_equals_dense_su2(secs):
+    """The tree-level partial trace (close the end legs, d_c/d_e) equals the plain dense trace for SU(2)."""
+    from oracle import dense as OD, contract as OC, layout as OL
+    V = W.space("SU2", secs)
+    Vd = W.dual(V)
+    rng = np.random.default_rng(1)
+    # planar traces (pairs nested in the cyclic leg order), closed at the tree ends
+    cases = [([V, V], [V, V], [1], [3], [0], [2]), ([V, V], [V, V], [2], [0], [1, 3], []),
+             ([V, V, V], [V, V], [2], [4], [0, 1], [3]), ([V, V], [V, V], [0, 1], [2, 3], [], []),
+             ([Vd, V], [Vd, V], [1], [3], [0], [2])]
+    for cod, dom, pt, qt, p, q in cases:
+        lt = OL.homspace_layout("SU2", cod, dom)
+        x = rng.standard_normal(lt.nelems)
+        got, lc = OP.trace_planar("SU2", cod, dom, x, pt, qt, p, q)
+        R, c2, d2 = OC.partial_trace_dense(OD.to_dense(lt, x), cod, dom, pt, qt, p, q)
+        assert OC.rel_frobenius(OD.to_dense(lc, got), R) < 1e-13, (pt, qt, p, q)
