@@ -32,7 +32,7 @@ def _spaces(kind, secs, cd, dd):
 
 
 @pytest.mark.parametrize("secs,nshapes", [([((0,), 1), ((1,), 1), ((2,), 1)], 4),
-                                         ([((1,), 1), ((2,), 1), ((3,), 1)], 2)])
+                                         ([((1,), 1), ((2,), 1)], 3)])
 def test_planar_moves_equal_dense_su2(secs, nshapes):
     from tests.test_library_host import oracle_transfer
     for cd, dd in SHAPES[:nshapes]:
