@@ -61,9 +61,10 @@ constexpr int kSvdMaxSweeps = 60;
 // SvdBlock.smem: 2 = G and V in shared memory, 1 = G only (V recovered as X^T G S^-2 afterwards),
 // 0 = both in the (L2-resident) workspace.
 
-__device__ __forceinline__ double group_sum(double x) {  // sum over the 8 lanes of a pair group
+template <int L = kSvdLanes>
+__device__ __forceinline__ double group_sum(double x) {  // sum over the L lanes of a pair group
 #pragma unroll
-  for (int o = kSvdLanes / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
 __device__ __forceinline__ double warp_sum(double x) {
@@ -74,11 +75,11 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 // MODE is a template parameter so that shared-memory operands compile to LDS/STS (a runtime choice
 // of pointer would leave generic LD/ST on the critical path of every rotation)
-template <int MODE>
+template <int MODE, int L>
 __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict__ ws, int32_t* __restrict__ idx,
                                           double* sm, double* sig, int& rotated, int debug) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = tid / kSvdLanes, gl = tid % kSvdLanes;
+  const int grp = tid / L, gl = tid % L;
   const int R = b.R, K = b.K;
   // working copies: G (R x K, ld ldG) and V (K x K, ld ldV)
   constexpr bool gs = MODE >= 1, vs = MODE == 2, accv = MODE != 1;
@@ -101,6 +102,7 @@ __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict_
   // stop rotating a pair once its cosine is at the rounding level of a length-R dot product
   const double tol = 2.3e-16 * sqrt((double)R);
   int sweep = 0;
+  const long long t_start = clock64();
   for (; sweep < kSvdMaxSweeps; ++sweep) {
     if (tid == 0) rotated = 0;
     __syncthreads();
@@ -108,7 +110,8 @@ __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict_
     for (int r = 0; r < n - 1; ++r) {
       // groups of 8 lanes each own one disjoint column pair of round r (all lanes of a warp stay
       // converged for the group shuffles; idle groups run empty loops)
-      for (int base = 0; base < n / 2; base += kSvdGroups) {
+      for (int base = 0; base < n / 2; base += (kSvdThreads / L)) {
+        if (base + warp * (32 / L) >= n / 2) continue;  // warp-uniform: no pair for this warp
         const int pr = base + grp;
         int p = 0, q = 0;
         bool act = pr < n / 2;
@@ -131,21 +134,21 @@ __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict_
         double* gp = G + (int64_t)p * ldG;
         double* gq = G + (int64_t)q * ldG;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = gl; i < len; i += kSvdLanes) {
+        for (int i = gl; i < len; i += L) {
           const double x = gp[i], y = gq[i];
           al = fma(x, x, al);
           be = fma(y, y, be);
           ga = fma(x, y, ga);
         }
-        al = group_sum(al);
-        be = group_sum(be);
-        ga = group_sum(ga);
+        al = group_sum<L>(al);
+        be = group_sum<L>(be);
+        ga = group_sum<L>(ga);
         if (act && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
           // 2x2 symmetric Schur rotation of [[al, ga], [ga, be]] (Hestenes one-sided Jacobi)
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = gl; i < R; i += kSvdLanes) {
+          for (int i = gl; i < R; i += L) {
             const double x = gp[i], y = gq[i];
             gp[i] = c * x - s * y;
             gq[i] = s * x + c * y;
@@ -153,7 +156,7 @@ __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict_
           if (accv) {
             double* vp = V + (int64_t)p * ldV;
             double* vq = V + (int64_t)q * ldV;
-            for (int i = gl; i < K; i += kSvdLanes) {
+            for (int i = gl; i < K; i += L) {
               const double x = vp[i], y = vq[i];
               vp[i] = c * x - s * y;
               vq[i] = s * x + c * y;
@@ -169,7 +172,9 @@ __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict_
     if (!rotated) break;
     __syncthreads();
   }
-  if (debug && tid == 0) printf("[tk svd] block %d: %d x %d, mode %d, %d sweeps\n", blockIdx.x, R, K, MODE, sweep + 1);
+  if (debug && tid == 0)
+    printf("[tk svd] block %d: %d x %d, mode %d, %d sweeps, %lld cycles/round\n", blockIdx.x, R, K, MODE, sweep + 1,
+           (clock64() - t_start) / ((long long)(sweep + 1) * (n - 1)));
   // singular values = column norms; rank by value (descending, ties by column index)
   for (int j = warp; j < K; j += kSvdWarps) {
     const double* g = G + (int64_t)j * ldG;
@@ -239,18 +244,198 @@ __device__ __forceinline__ void svd_block(const SvdBlock& b, double* __restrict_
 
 __global__ void __launch_bounds__(kSvdThreads, 1)
     svd_jacobi_kernel(double* __restrict__ ws, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
-                      int debug) {
+                      const int32_t* __restrict__ list, int debug) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int rotated;
   __shared__ double sig[kSvdMaxK];
-  const SvdBlock b = blocks[blockIdx.x];
+  const SvdBlock b = blocks[list[blockIdx.x]];
   if (b.K == 0) return;
   if (b.smem == 2)
-    svd_block<2>(b, ws, idx, sm, sig, rotated, debug);
+    svd_block<2, kSvdLanes>(b, ws, idx, sm, sig, rotated, debug);
   else if (b.smem == 1)
-    svd_block<1>(b, ws, idx, sm, sig, rotated, debug);
+    svd_block<1, kSvdLanes>(b, ws, idx, sm, sig, rotated, debug);
   else
-    svd_block<0>(b, ws, idx, sm, sig, rotated, debug);
+    svd_block<0, kSvdLanes>(b, ws, idx, sm, sig, rotated, debug);
+}
+
+// ---- cluster variant: the rows of G (and of V) are split over the CTAs of a thread-block cluster
+// (CS = 1, 2, 4 or 8 CTAs on as many SMs); every column pair's (alpha, beta, gamma) is the sum of the
+// CTAs' partial dot products, exchanged through distributed shared memory with ONE cluster barrier
+// per Jacobi round (partials double-buffered by round parity). All CTAs then take the identical
+// rotation and update their own rows. A round's critical path shrinks with R / CS, and blocks whose
+// G + V exceed one SM's shared memory still run on-chip.
+constexpr int kClusterMaxK = 512;
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ const double* map_rank(const double* p, uint32_t rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;\n" : "=l"(out) : "l"((uint64_t)p), "r"(rank));
+  return (const double*)out;
+}
+
+template <int CS>
+__global__ void __launch_bounds__(kSvdThreads, 1)
+    svd_cluster_kernel(double* __restrict__ ws, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
+                       const int32_t* __restrict__ list, int debug) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double part[2][kClusterMaxK / 2][3];
+  __shared__ double sig[kClusterMaxK];
+  __shared__ int rotated;
+  const SvdBlock b = blocks[list[blockIdx.x / CS]];
+  const uint32_t rank = CS > 1 ? cluster_rank() : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / kSvdLanes, gl = tid % kSvdLanes;
+  const int R = b.R, K = b.K;
+  const int Rl = (R + CS - 1) / CS, Kl = (K + CS - 1) / CS;
+  const int r0 = min(R, (int)rank * Rl), r1 = min(R, r0 + Rl), nr = r1 - r0;
+  const int v0 = min(K, (int)rank * Kl), v1 = min(K, v0 + Kl), nv = v1 - v0;
+  double* G = sm;                      // nr x K (ld Rl), local rows r0..r1
+  double* V = sm + (size_t)Rl * K;     // nv x K (ld Kl), local rows v0..v1
+  const double* A = ws + b.a_off;
+  for (int64_t e = tid; e < (int64_t)nr * K; e += kSvdThreads) {
+    const int i = (int)(e % nr), j = (int)(e / nr);
+    const int gi = r0 + i;
+    G[i + (int64_t)j * Rl] = b.trans ? A[j + (int64_t)gi * b.lda] : A[gi + (int64_t)j * b.lda];
+  }
+  for (int64_t e = tid; e < (int64_t)nv * K; e += kSvdThreads) {
+    const int i = (int)(e % nv), j = (int)(e / nv);
+    V[i + (int64_t)j * Kl] = (v0 + i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int n = K + (K & 1);
+  const double tol = 2.3e-16 * sqrt((double)R);
+  int sweep = 0, par = 0;
+  for (; sweep < kSvdMaxSweeps; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < n - 1; ++r) {
+      // (1) local partial dot products of every pair of round r
+      for (int base = 0; base < n / 2; base += kSvdGroups) {
+        if (base + warp * (32 / kSvdLanes) >= n / 2) continue;  // warp-uniform: no pair for this warp
+        const int pr = base + grp;
+        int p = 0, q = 0;
+        bool act = pr < n / 2;
+        if (act) {
+          if (pr == 0) { p = n - 1; q = r; } else { p = (r + pr) % (n - 1); q = (r - pr + n - 1) % (n - 1); }
+          if (p > q) { const int t = p; p = q; q = t; }
+          act = q < K;
+        }
+        const int len = act ? nr : 0;
+        const double* gp = G + (int64_t)p * Rl;
+        const double* gq = G + (int64_t)q * Rl;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = gl; i < len; i += kSvdLanes) {
+          const double x = gp[i], y = gq[i];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = group_sum(al);
+        be = group_sum(be);
+        ga = group_sum(ga);
+        if (act && gl == 0) {
+          part[par][pr][0] = al;
+          part[par][pr][1] = be;
+          part[par][pr][2] = ga;
+        }
+      }
+      if (CS > 1) cluster_sync_all(); else __syncthreads();
+      // (2) identical sums in every CTA (rank order), rotation, update of the local rows
+      int any = 0;
+      for (int base = 0; base < n / 2; base += kSvdGroups) {
+        if (base + warp * (32 / kSvdLanes) >= n / 2) continue;  // warp-uniform: no pair for this warp
+        const int pr = base + grp;
+        int p = 0, q = 0;
+        bool act = pr < n / 2;
+        if (act) {
+          if (pr == 0) { p = n - 1; q = r; } else { p = (r + pr) % (n - 1); q = (r - pr + n - 1) % (n - 1); }
+          if (p > q) { const int t = p; p = q; q = t; }
+          act = q < K;
+        }
+        if (!act) continue;
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int c = 0; c < CS; ++c) {
+          const double* pp = CS > 1 ? map_rank(&part[par][pr][0], (uint32_t)c) : &part[par][pr][0];
+          al += pp[0];
+          be += pp[1];
+          ga += pp[2];
+        }
+        if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        double* gp = G + (int64_t)p * Rl;
+        double* gq = G + (int64_t)q * Rl;
+        for (int i = gl; i < nr; i += kSvdLanes) {
+          const double x = gp[i], y = gq[i];
+          gp[i] = c * x - s * y;
+          gq[i] = s * x + c * y;
+        }
+        double* vp = V + (int64_t)p * Kl;
+        double* vq = V + (int64_t)q * Kl;
+        for (int i = gl; i < nv; i += kSvdLanes) {
+          const double x = vp[i], y = vq[i];
+          vp[i] = c * x - s * y;
+          vq[i] = s * x + c * y;
+        }
+        any = 1;
+      }
+      if (any) rotated = 1;
+      par ^= 1;
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  if (debug && tid == 0 && rank == 0)
+    printf("[tk svd] block %d: %d x %d, cluster %d, %d sweeps\n", list[blockIdx.x / CS], R, K, CS, sweep + 1);
+  // singular values: column norms summed over the cluster (rank order)
+  double* nrm = &part[par][0][0];  // reuse: K <= kClusterMaxK partial norms (3 * K / 2 >= K slots)
+  for (int j = warp; j < K; j += kSvdWarps) {
+    const double* g = G + (int64_t)j * Rl;
+    double x = 0.0;
+    for (int i = lane; i < nr; i += 32) x = fma(g[i], g[i], x);
+    x = warp_sum(x);
+    if (lane == 0) nrm[j] = x;
+  }
+  if (CS > 1) cluster_sync_all(); else __syncthreads();
+  for (int j = tid; j < K; j += kSvdThreads) {
+    double x = 0.0;
+#pragma unroll
+    for (int c = 0; c < CS; ++c) x += (CS > 1 ? map_rank(nrm, (uint32_t)c) : nrm)[j];
+    sig[j] = sqrt(x);
+  }
+  __syncthreads();
+  if (rank == 0) {
+    double* sv = ws + b.s_off;
+    int32_t* pv = idx + b.p_off;
+    for (int j = tid; j < K; j += kSvdThreads) {
+      const double sj = sig[j];
+      int rk = 0;
+      for (int i = 0; i < K; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+      sv[rk] = sj;
+      pv[rk] = j;
+    }
+  }
+  // local rows of G and V back to the workspace (the extraction kernel reads them there)
+  double* Gw = ws + b.g_off;
+  double* Vw = ws + b.v_off;
+  for (int64_t e = tid; e < (int64_t)nr * K; e += kSvdThreads) {
+    const int i = (int)(e % nr), j = (int)(e / nr);
+    Gw[r0 + i + (int64_t)j * b.ldg] = G[i + (int64_t)j * Rl];
+  }
+  for (int64_t e = tid; e < (int64_t)nv * K; e += kSvdThreads) {
+    const int i = (int)(e % nv), j = (int)(e / nv);
+    Vw[v0 + i + (int64_t)j * b.ldv] = V[i + (int64_t)j * Kl];
+  }
+  if (CS > 1) cluster_sync_all();  // no CTA may exit while others still read its shared memory
 }
 
 // U[:, r] = G[:, perm r] / s_r (or V[:, perm r] when transposed); Vh[r, :] = V[:, perm r]^T (or G / s);
@@ -308,6 +493,10 @@ struct SvdPlan {
   PadLayout la;
   std::vector<SvdBlock> blocks;
   DevBuf d_blocks;
+  // launch classes: 0 = single-CTA kernel (modes 0/1/2), 1..4 = cluster kernel with 1, 2, 4, 8 CTAs
+  std::vector<int32_t> lists[5];
+  int class_smem[5] = {0, 0, 0, 0, 0};
+  DevBuf d_lists[5];
   size_t ws_bytes = 0, idx_off = 0;  // byte offset of the int32 index region
   int64_t n_sigma = 0;
   int smem_bytes = 0;
@@ -375,7 +564,26 @@ static SvdPlan* get_svd_plan(const Tensor& A, const std::vector<int>& p, const s
     const int64_t need2 = ((int64_t)b.R * b.K + (int64_t)b.K * b.K) * 8;
     const int64_t need1 = ((int64_t)b.R * b.K + (int64_t)kSvdWarps * b.R) * 8;  // + per-warp X column slots
     b.smem = need2 <= kSvdSmemBytes ? 2 : (need1 <= kSvdSmemBytes ? 1 : 0);
-    if (b.smem) P->smem_bytes = std::max<int>(P->smem_bytes, (int)(b.smem == 2 ? need2 : need1));
+    // cluster kernel: rows split over CS CTAs so that a round's critical path is <= ~48 rows per CTA
+    int cls = 0;
+    static const bool no_cluster = getenv("TK_SVD_NO_CLUSTER") != nullptr;
+    // blocks that fit one SM's shared memory stay on the single-CTA kernel (one barrier per round, measured
+    // faster there); larger ones go to the cluster kernel with ~24 rows per CTA (cfg3: 32.8 -> 15.0 ms)
+    if (!no_cluster && b.K <= kClusterMaxK && b.smem == 0) {
+      static const int rows_target = getenv("TK_SVD_ROWS") ? atoi(getenv("TK_SVD_ROWS")) : 24;
+      const int want = b.R <= rows_target ? 1 : (b.R <= 2 * rows_target ? 2 : (b.R <= 4 * rows_target ? 4 : 8));
+      for (int ci = 0, cs = 1; ci < 4; ++ci, cs *= 2) {
+        const int64_t Rl = (b.R + cs - 1) / cs, Kl = (b.K + cs - 1) / cs;
+        const int64_t need = (Rl + Kl) * b.K * 8;
+        if (cs >= want && need <= kSvdSmemBytes) {
+          cls = 1 + ci;
+          P->class_smem[cls] = std::max<int>(P->class_smem[cls], (int)need);
+          break;
+        }
+      }
+    }
+    if (cls == 0 && b.smem) P->smem_bytes = std::max<int>(P->smem_bytes, (int)(b.smem == 2 ? need2 : need1));
+    P->lists[cls].push_back((int32_t)P->blocks.size());
     P->blocks.push_back(b);
   }
   const int64_t sig_base = off;
@@ -495,21 +703,60 @@ tk_status tk_svd(const tk_tensor* A_, const void* a, const int32_t* p, int32_t n
   cudaStream_t st = (cudaStream_t)stream;
   if (!P->uploaded) {
     P->d_blocks.upload(P->blocks);
+    for (int c = 0; c < 5; ++c) P->d_lists[c].upload(P->lists[c]);
     P->uploaded = true;
   }
   reset_launches();
   run_permute(P->pa, a, ws, 1.0, 0.0, kPermReal, 1.0, st);
-  if (!P->blocks.empty()) {
-    static const bool dbg = getenv("TK_SVD_DEBUG") != nullptr;
-    static bool attr = false;
-    if (!attr) {
-      check_cuda(cudaFuncSetAttribute(svd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
-                 "svd smem attribute");
-      attr = true;
-    }
-    svd_jacobi_kernel<<<(unsigned)P->blocks.size(), kSvdThreads, P->smem_bytes, st>>>(
-        (double*)ws, (int32_t*)((char*)ws + P->idx_off), (const SvdBlock*)P->d_blocks.p, dbg ? 1 : 0);
+  static const bool dbg = getenv("TK_SVD_DEBUG") != nullptr;
+  static bool attr = false;
+  if (!attr) {
+    check_cuda(cudaFuncSetAttribute(svd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
+               "svd smem attribute");
+    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
+               "svd smem attribute");
+    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
+               "svd smem attribute");
+    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
+               "svd smem attribute");
+    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
+               "svd smem attribute");
+    attr = true;
+  }
+  double* wsd = (double*)ws;
+  int32_t* idx = (int32_t*)((char*)ws + P->idx_off);
+  if (!P->lists[0].empty()) {
+    svd_jacobi_kernel<<<(unsigned)P->lists[0].size(), kSvdThreads, P->smem_bytes, st>>>(
+        wsd, idx, (const SvdBlock*)P->d_blocks.p, (const int32_t*)P->d_lists[0].p, dbg ? 1 : 0);
     check_cuda(cudaGetLastError(), "svd launch");
+    add_launches(1);
+  }
+  for (int c = 1; c < 5; ++c) {
+    if (P->lists[c].empty()) continue;
+    const int cs = 1 << (c - 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P->lists[c].size() * cs));
+    cfg.blockDim = dim3(kSvdThreads);
+    cfg.dynamicSmemBytes = (size_t)P->class_smem[c];
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const SvdBlock* bp = (const SvdBlock*)P->d_blocks.p;
+    const int32_t* lp = (const int32_t*)P->d_lists[c].p;
+    const int dg = dbg ? 1 : 0;
+    cudaError_t err;
+    switch (cs) {
+      case 1: err = cudaLaunchKernelEx(&cfg, svd_cluster_kernel<1>, wsd, idx, bp, lp, dg); break;
+      case 2: err = cudaLaunchKernelEx(&cfg, svd_cluster_kernel<2>, wsd, idx, bp, lp, dg); break;
+      case 4: err = cudaLaunchKernelEx(&cfg, svd_cluster_kernel<4>, wsd, idx, bp, lp, dg); break;
+      default: err = cudaLaunchKernelEx(&cfg, svd_cluster_kernel<8>, wsd, idx, bp, lp, dg); break;
+    }
+    check_cuda(err, "svd cluster launch");
     add_launches(1);
   }
   TK_API_END
