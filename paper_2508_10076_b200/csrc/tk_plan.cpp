@@ -751,8 +751,9 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   // fixed order (deterministic) and applies alpha / beta.
   const int ntot = (int)(big.size() + small.size());
   static const bool no_split = getenv("TK_NO_SPLITK") != nullptr;
-  if (!no_split && ntot > 0 && ntot < 2 * 148) {
-    const int want = (2 * 148 + ntot - 1) / ntot;
+  static const int split_target = getenv("TK_SPLIT_TARGET") ? atoi(getenv("TK_SPLIT_TARGET")) : 4;  // tiles/SM (measured: 2 -> 4 cfg3 291 -> 280 us)
+  if (!no_split && ntot > 0 && ntot < split_target * 148) {
+    const int want = (split_target * 148 + ntot - 1) / ntot;
     std::vector<GemmTile> out;
     int slot = 0;
     for (const GemmTile& t : small) {
