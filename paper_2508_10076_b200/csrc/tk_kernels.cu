@@ -859,17 +859,26 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
     }
     const double* as = As + (kt % STAGES) * Cfg::A_STAGE + wm * WM + gq;
     const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE + (wn * WN + gq) * Cfg::LDB_S + tq;
+    // padding is never multiplied: k-steps past K, and 8-row / 8-column fragments outside the block
+    // (warp-uniform guards; small sectors are mostly padding in 64 x 64 tiles)
+    const int kend = min(BK, K - (kb + kt * BK));
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
+      if (kk >= kend) break;
       double af[Cfg::MF], bf[Cfg::NF];
 #pragma unroll
       for (int i = 0; i < Cfg::MF; ++i) af[i] = as[(kk + tq) * Cfg::LDA_S + i * 8];
 #pragma unroll
       for (int j = 0; j < Cfg::NF; ++j) bf[j] = bs[j * 8 * Cfg::LDB_S + kk];
 #pragma unroll
-      for (int i = 0; i < Cfg::MF; ++i)
+      for (int i = 0; i < Cfg::MF; ++i) {
+        if (m0 + wm * WM + i * 8 >= M) break;
 #pragma unroll
-        for (int j = 0; j < Cfg::NF; ++j) dmma884(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < Cfg::NF; ++j) {
+          if (n0 + wn * WN + j * 8 >= N) break;
+          dmma884(acc[i][j], af[i], bf[j]);
+        }
+      }
     }
   }
   cp_async_wait<0>();
@@ -1068,10 +1077,16 @@ __global__ void __launch_bounds__(MbarCfg::THREADS, 1)
   gemm_tile_mbar<TK_MBAR, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
-#define TK_SMALL 64, 64, 32, 32, 16, 3
+#ifndef TK_SMALL_STAGES
+#define TK_SMALL_STAGES 3
+#endif
+#define TK_SMALL 64, 64, 32, 16, 16, TK_SMALL_STAGES
+#ifndef TK_SMALL_MINB
+#define TK_SMALL_MINB 2
+#endif
 using SmallCfg = GemmCfg<TK_SMALL>;
 
-__global__ void __launch_bounds__(SmallCfg::THREADS)
+__global__ void __launch_bounds__(SmallCfg::THREADS, TK_SMALL_MINB)
     gemm_small_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
                       double beta, int base_vec, double* __restrict__ parts) {
