@@ -666,12 +666,70 @@ __device__ void permute_packed(const typename CIO<CM>::S* __restrict__ src, type
   }
 }
 
+// kJobSeg (see SegGroup): copy the job's precomputed blob into shared memory, then walk its elements
+// as one flat range (as permute_packed) with 64 bytes of loads in flight per thread.
+template <int CM>
+__device__ void permute_seg(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                            const int64_t* __restrict__ blob, const PermJob& job, int64_t* sm, double alpha,
+                            double beta, double ims) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
+  const int tid = threadIdx.x;
+  {
+    const longlong2* g2 = reinterpret_cast<const longlong2*>(blob + job.first);
+    longlong2* s2 = reinterpret_cast<longlong2*>(sm);
+    const int n2 = job.group >> 1;
+    for (int i = tid; i < n2; i += kPermThreads) s2[i] = __ldg(g2 + i);
+  }
+  __syncthreads();
+  pdl_wait();
+  const SegHeader h = *reinterpret_cast<const SegHeader*>(sm);
+  const SegGroup* G = reinterpret_cast<const SegGroup*>(sm + 2);
+  const int64_t* rs = sm + 2 + 10 * h.ng;
+  const int64_t* rd = rs + h.nrows;
+  const int total = h.total, last = h.ng - 1;
+  constexpr int U = sizeof(V) == 16 ? 4 : 8;
+  int gi = 0;
+  for (int e0 = tid; e0 < total; e0 += U * kPermThreads) {
+    V x[U];
+    int64_t od[U];
+    int gu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kPermThreads;
+      gu[u] = -1;
+      if (e < total) {
+        while (gi < last && G[gi + 1].estart <= e) ++gi;
+        const SegGroup& g = G[gi];
+        const uint32_t loc = (uint32_t)(e - g.estart);
+        FastDiv fd;
+        fd.d = g.n0;
+        fd.m = g.fm;
+        fd.s = g.fs;
+        const uint32_t r = fd.div(loc);
+        const uint32_t i0 = loc - r * fd.d;
+        const int row = g.rstart + (int)r;
+        x[u] = IO::load(src, rs[row] + (int64_t)i0 * g.s0, g.sd1);
+        od[u] = rd[row] + (int64_t)i0 * g.d0;
+        gu[u] = gi;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (gu[u] >= 0) {
+        const SegGroup& g = G[gu[u]];
+        IO::store(dst, od[u], g.dd1, g.dd2, Num<V>::scale(alpha * g.c, x[u]), beta, ims);
+      }
+  }
+}
+
 // One launch covers every abelian-style job of up to two permutes (A~ and B~ of a contraction, op 0/1):
 // rows, smem-tiled and packed jobs share the grid, so small latency-bound permutes do not serialise
 // over several launches. <= 64 registers so that 4 CTAs (32 warps) share an SM.
 union PermSharedAll {
   PermShared p;
   PackShared k;
+  int64_t seg[kSegWords];
 };
 
 // ROWS_ONLY: a launch whose jobs are all rows jobs (the large cfg4 permutes) uses a leaner instance
@@ -679,7 +737,7 @@ union PermSharedAll {
 template <int CM, bool ROWS_ONLY>
 __global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB) permute_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
   using IO = CIO<CM>;
-  __shared__ typename std::conditional<ROWS_ONLY, PermShared, PermSharedAll>::type sh_;
+  __shared__ __align__(16) typename std::conditional<ROWS_ONLY, PermShared, PermSharedAll>::type sh_;
   PermShared& sh = *reinterpret_cast<PermShared*>(&sh_);
   extern __shared__ __align__(16) unsigned char perm_dyn[];
   pdl_trigger();
@@ -688,6 +746,10 @@ __global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB) permute_kernel(Per
   const auto* src = (const typename IO::S*)op.src;
   auto* dst = (typename IO::D*)op.dst;
   if constexpr (!ROWS_ONLY) {
+    if (job.type == kJobSeg) {
+      permute_seg<CM>(src, dst, op.blob, job, reinterpret_cast<int64_t*>(&sh_), op.alpha, op.beta, op.ims);
+      return;
+    }
     if (job.type == kJobPacked) {
       permute_packed<CM>(src, dst, op.groups, op.members, op.coefs, job, *reinterpret_cast<PackShared*>(&sh_),
                          op.alpha, op.beta, op.ims);

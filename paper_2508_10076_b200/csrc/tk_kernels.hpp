@@ -66,7 +66,27 @@ constexpr int kTileElems = 4608;  // smem capacity of the two tile buffers (elem
 constexpr int kPackGroups = 32;
 constexpr int kPackRows = 1024;
 constexpr int kPackElems = 8192;
-enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3, kJobBox = 4 };
+enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3, kJobBox = 4, kJobSeg = 5 };
+// Latency-regime jobs (kJobSeg, permutes below 2^24 elements): the planner precomputes everything a
+// CTA needs into one contiguous blob of 8-byte words -- SegHeader, `ng` SegGroup chunks (a row range
+// of one single-member group each), then the final source / destination offsets of every row start
+// (rs[nrows], rd[nrows]) -- so a CTA's prologue is one coalesced copy of plan data into shared memory
+// (issued before griddepcontrol.wait, overlapping the previous kernel) instead of a dependent chain of
+// job -> group -> member loads and per-row index divisions. Job: first = word offset of the blob,
+// group = its length in words (even), count = ng.
+struct SegHeader {
+  int32_t ng, nrows, total, pad;
+};
+struct SegGroup {
+  int32_t estart, rstart;  // first element / first row of this chunk within the job
+  uint32_t n0, fm, fs, pad;  // row length and its division magic (FastDiv)
+  int64_t s0, d0;          // element strides along the row (source, destination)
+  double c;                // coefficient (+-1 fermionic sign)
+  int64_t sd1, dd1, dd2;   // complex-mode offsets of the source / destination member (PermCM)
+  int64_t pad2;
+};
+static_assert(sizeof(SegHeader) == 16 && sizeof(SegGroup) == 80, "seg blob layout");
+constexpr int kSegWords = 2 + 10 * kPackGroups + 2 * kPackRows;
 constexpr int kBoxElems = 4096;  // doubles per box (ComplexF64: half as many elements)
 struct PermJob {
   int32_t group;
@@ -83,6 +103,7 @@ struct PermOp {
   const PermGroup* groups;
   const PermMember* members;
   const double* coefs;
+  const int64_t* blob;      // kJobSeg job blobs
   double alpha, beta, ims;  // ims = -1 conjugates the source (tk_contract conjA / conjB; modes 2 and 3)
 };
 

@@ -221,6 +221,88 @@ static bool packable(const PermGroup& g) {
   return g.ksrc == 1 && g.kdst == 1 && g.nelem <= 2048 && g.nelem / g.ext[0] <= kPackRows;
 }
 
+// Builds kJobSeg blobs (SegHeader in tk_kernels.hpp): row ranges of single-member groups are packed
+// greedily into jobs of <= job_elems elements, <= kPackGroups chunks and <= kPackRows rows; the row
+// start offsets are the same index arithmetic the rows kernel does per job (legs 1.. of the group).
+struct SegBuilder {
+  PermPlan& P;
+  std::vector<PermJob>& jobs;
+  int64_t job_elems;
+  std::vector<SegGroup> cg;
+  std::vector<int64_t> rs, rd;
+  int64_t elems = 0;
+  SegBuilder(PermPlan& P_, std::vector<PermJob>& j, int64_t je) : P(P_), jobs(j), job_elems(je) {}
+  static void fastdiv(uint32_t d, uint32_t& m, uint32_t& s) {  // = FastDiv::init (tk_kernels.cu)
+    s = 0;
+    while ((1u << s) < d) ++s;
+    m = (d <= 1) ? 0u : (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - d)) / d + 1);
+  }
+  void flush() {
+    if (cg.empty()) return;
+    const int64_t first = (int64_t)P.blob.size();
+    SegHeader h{(int32_t)cg.size(), (int32_t)rs.size(), (int32_t)elems, 0};
+    const int64_t* hw = reinterpret_cast<const int64_t*>(&h);
+    P.blob.insert(P.blob.end(), hw, hw + 2);
+    for (const SegGroup& g : cg) {
+      const int64_t* w = reinterpret_cast<const int64_t*>(&g);
+      P.blob.insert(P.blob.end(), w, w + 10);
+    }
+    P.blob.insert(P.blob.end(), rs.begin(), rs.end());
+    P.blob.insert(P.blob.end(), rd.begin(), rd.end());
+    if (P.blob.size() & 1) P.blob.push_back(0);
+    jobs.push_back(PermJob{(int32_t)(P.blob.size() - first), (int16_t)cg.size(), kJobSeg, 0, first});
+    cg.clear();
+    rs.clear();
+    rd.clear();
+    elems = 0;
+  }
+  void add(int gi) {
+    const PermGroup& g = P.groups[gi];
+    const PermMember ms = P.members[g.src_mem], md = P.members[g.dst_mem];
+    const int64_t n0 = g.ext[0], nrows = g.nelem / n0;
+    if (n0 > INT32_MAX / 2) TK_THROW(TK_ERR_UNSUPPORTED, "row too long for a seg job");
+    for (int64_t r0 = 0; r0 < nrows;) {
+      int64_t room = std::min<int64_t>((job_elems - elems) / n0, kPackRows - (int64_t)rs.size());
+      if ((int)cg.size() == kPackGroups || room <= 0) {
+        if (!cg.empty()) {
+          flush();
+          continue;
+        }
+        room = 1;  // one row longer than job_elems: a job of its own
+      }
+      const int64_t nr = std::min(room, nrows - r0);
+      SegGroup sg{};
+      sg.estart = (int32_t)elems;
+      sg.rstart = (int32_t)rs.size();
+      sg.n0 = (uint32_t)n0;
+      fastdiv(sg.n0, sg.fm, sg.fs);
+      sg.s0 = g.sa[0] + ms.ld * g.sb[0];
+      sg.d0 = g.da[0] + md.ld * g.db[0];
+      sg.c = P.coefs[g.coef_off];
+      sg.sd1 = ms.d1;
+      sg.dd1 = md.d1;
+      sg.dd2 = md.d2;
+      cg.push_back(sg);
+      for (int64_t r = r0; r < r0 + nr; ++r) {
+        int64_t R = r, sa = 0, sbb = 0, da = 0, db = 0;
+        for (int l = 1; l < g.ndim; ++l) {
+          const int64_t i = R % g.ext[l];
+          R /= g.ext[l];
+          sa += i * g.sa[l];
+          sbb += i * g.sb[l];
+          da += i * g.da[l];
+          db += i * g.db[l];
+        }
+        rs.push_back(ms.off + sa + ms.ld * sbb);
+        rd.push_back(md.off + da + md.ld * db);
+      }
+      elems += nr * n0;
+      r0 += nr;
+    }
+  }
+  void finish() { flush(); }
+};
+
 static void make_jobs(PermPlan& P) {
   // small single-member groups go last and are packed several per CTA (permute_packed_kernel)
   std::stable_partition(P.groups.begin(), P.groups.end(), [](const PermGroup& g) { return !packable(g); });
@@ -232,8 +314,17 @@ static void make_jobs(PermPlan& P) {
   static const int64_t job_div = getenv("TK_JOB_DIV") ? atoll(getenv("TK_JOB_DIV")) : 2 * 148 * 4;
   const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(kPackElems, total / job_div));
   int64_t pack_elems = 0, pack_rows = 0;
+  // latency regime: single-member rows / packable groups become kJobSeg blobs (TK_NO_SEG=1 disables)
+  static const bool no_seg = getenv("TK_NO_SEG") != nullptr;
+  const bool seg = !no_seg && total < (int64_t(1) << 24);
+  std::vector<PermJob> segs;
+  SegBuilder sb(P, segs, job_elems);
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
+    if (seg && g.ksrc == 1 && g.kdst == 1 && (packable(g) || g.mode == 0)) {
+      sb.add(gi);
+      continue;
+    }
     if (packable(g)) {
       int64_t nrow = g.nelem / g.ext[0];
       if (!packed.empty() && packed.back().count < kPackGroups && pack_elems + g.nelem <= job_elems &&
@@ -271,12 +362,14 @@ static void make_jobs(PermPlan& P) {
   }
   // small permutes: one launch for rows, tiled and packed jobs (+ one for recoupling jobs); large ones
   // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
+  sb.finish();
   tiles.insert(tiles.end(), boxes.begin(), boxes.end());  // box jobs run beside the tiled ones
+  rows.insert(rows.begin(), segs.begin(), segs.end());    // seg jobs lead the non-rows-only launch
   P.njobs = (int)(tiles.size() + rows.size() + packed.size());
-  P.njobs_rows = (int)rows.size();
+  P.njobs_rows = (int)(rows.size() - segs.size());
   P.njobs_multi = (int)multi.size();
   P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
-  P.rows_only = tiles.empty() && packed.empty();
+  P.rows_only = tiles.empty() && packed.empty() && segs.empty();
   P.split = total >= (int64_t(1) << 24) && !P.rows_only && !rows.empty();
   static const bool dbg = getenv("TK_PLAN_DEBUG") != nullptr;
   if (dbg) {
@@ -871,7 +964,7 @@ void check_cuda(cudaError_t e, const char* what) {
 static PermOp perm_op(PermPlan& P, const void* src, void* dst, double alpha, double beta, double ims) {
   P.upload();
   return PermOp{src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p, (const double*)P.d_coefs.p,
-                alpha, beta, ims};
+                (const int64_t*)P.d_blob.p, alpha, beta, ims};
 }
 
 void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double beta, int cm, double ims,

@@ -33,10 +33,11 @@ struct PermPlan {
   std::vector<PermMember> members;
   std::vector<double> coefs;
   std::vector<PermJob> jobs;
+  std::vector<int64_t> blob;  // kJobSeg job blobs (SegHeader | SegGroup[ng] | rs | rd per job)
   int njobs = 0, njobs_multi = 0, njobs_rows = 0;  // jobs = [rows | tiled | packed | recoupling]
   bool tiled = false, rows_only = false;
   bool split = false;  // large permute: rows jobs in their own (leaner) launch
-  DevBuf d_groups, d_members, d_coefs, d_jobs;
+  DevBuf d_groups, d_members, d_coefs, d_jobs, d_blob;
   double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
   int64_t n_src = 0, n_dst = 0;
   bool uploaded = false;
@@ -46,6 +47,7 @@ struct PermPlan {
     d_members.upload(members);
     d_coefs.upload(coefs);
     d_jobs.upload(jobs);
+    d_blob.upload(blob);
     uploaded = true;
   }
 };
