@@ -13,6 +13,7 @@
 //                  tensor-core path -- tcgen05 has no f64 kind), 3-stage cp.async pipeline, tiles
 //                  of all groups listed by the planner (long-K first); K = 0 groups write
 //                  beta*C (the zero fill of P:1271).
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -67,13 +68,9 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-#ifndef TK_PERM_THREADS
-#define TK_PERM_THREADS 256  // threads per permute CTA
-#endif
 #ifndef TK_PERM_MINB
 #define TK_PERM_MINB 4       // resident permute CTAs per SM (register budget: 64 / thread at 256 x 4)
 #endif
-constexpr int kPermThreads = TK_PERM_THREADS;
 #ifndef TK_ROWS_U
 #define TK_ROWS_U 8  // loads in flight per thread in the rows path (Float64)
 #endif
@@ -666,60 +663,130 @@ __device__ void permute_packed(const typename CIO<CM>::S* __restrict__ src, type
   }
 }
 
-// kJobSeg (see SegGroup): copy the job's precomputed blob into shared memory, then walk its elements
-// as one flat range (as permute_packed) with 64 bytes of loads in flight per thread.
+// kJobSeg (see SegGroup): with the job's blob in shared memory (sm), walk its elements as one flat
+// range with 64 bytes of loads in flight per thread. Each thread's elements are kPermThreads apart, so
+// (row, index in row) advance incrementally by (q, rem) of the current chunk; the division runs only
+// when a thread enters a new chunk.
 template <int CM>
-__device__ void permute_seg(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
-                            const int64_t* __restrict__ blob, const PermJob& job, int64_t* sm, double alpha,
-                            double beta, double ims) {
+__device__ __forceinline__ void seg_body(const typename CIO<CM>::S* __restrict__ src,
+                                         typename CIO<CM>::D* __restrict__ dst, const int64_t* sm, double alpha,
+                                         double beta, double ims) {
   using IO = CIO<CM>;
   using V = typename IO::V;
-  const int tid = threadIdx.x;
-  {
-    const longlong2* g2 = reinterpret_cast<const longlong2*>(blob + job.first);
-    longlong2* s2 = reinterpret_cast<longlong2*>(sm);
-    const int n2 = job.group >> 1;
-    for (int i = tid; i < n2; i += kPermThreads) s2[i] = __ldg(g2 + i);
-  }
-  __syncthreads();
-  pdl_wait();
   const SegHeader h = *reinterpret_cast<const SegHeader*>(sm);
   const SegGroup* G = reinterpret_cast<const SegGroup*>(sm + 2);
-  const int64_t* rs = sm + 2 + 10 * h.ng;
-  const int64_t* rd = rs + h.nrows;
+  const int32_t* rs = reinterpret_cast<const int32_t*>(sm + 2 + 10 * h.ng);
+  const int32_t* rd = rs + h.nrows;
   const int total = h.total, last = h.ng - 1;
   constexpr int U = sizeof(V) == 16 ? 4 : 8;
-  int gi = 0;
-  for (int e0 = tid; e0 < total; e0 += U * kPermThreads) {
+  int e = threadIdx.x;
+  if (e >= total) return;
+  int gi = 0, end = -1;  // end = -1: locate the chunk of the first element
+  uint32_t n0 = 1, q = 0, rem = 0, r = 0, i0 = 0;
+  int rst = 0, s0 = 0, d0 = 0;
+  while (e < total) {
     V x[U];
-    int64_t od[U];
+    int od[U];
     int gu[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * kPermThreads;
       gu[u] = -1;
       if (e < total) {
-        while (gi < last && G[gi + 1].estart <= e) ++gi;
-        const SegGroup& g = G[gi];
-        const uint32_t loc = (uint32_t)(e - g.estart);
-        FastDiv fd;
-        fd.d = g.n0;
-        fd.m = g.fm;
-        fd.s = g.fs;
-        const uint32_t r = fd.div(loc);
-        const uint32_t i0 = loc - r * fd.d;
-        const int row = g.rstart + (int)r;
-        x[u] = IO::load(src, rs[row] + (int64_t)i0 * g.s0, g.sd1);
-        od[u] = rd[row] + (int64_t)i0 * g.d0;
+        if (e >= end) {  // entering a later chunk
+          while (gi < last && G[gi + 1].estart <= e) ++gi;
+          end = gi < last ? G[gi + 1].estart : total;
+          n0 = G[gi].n0;
+          q = G[gi].q;
+          rem = G[gi].rem;
+          rst = G[gi].rstart;
+          s0 = (int)G[gi].s0;
+          d0 = (int)G[gi].d0;
+          FastDiv fd;
+          fd.d = n0;
+          fd.m = G[gi].fm;
+          fd.s = G[gi].fs;
+          const uint32_t loc = (uint32_t)(e - G[gi].estart);
+          r = fd.div(loc);
+          i0 = loc - r * n0;
+        }
+        const int row = rst + (int)r;
+        x[u] = IO::load(src, (int64_t)(rs[row] + (int)i0 * s0), G[gi].sd1);
+        od[u] = rd[row] + (int)i0 * d0;
         gu[u] = gi;
+        e += kPermThreads;
+        i0 += rem;
+        r += q;
+        if (i0 >= n0) {
+          i0 -= n0;
+          ++r;
+        }
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (gu[u] >= 0) {
         const SegGroup& g = G[gu[u]];
-        IO::store(dst, od[u], g.dd1, g.dd2, Num<V>::scale(alpha * g.c, x[u]), beta, ims);
+        IO::store(dst, (int64_t)od[u], g.dd1, g.dd2, Num<V>::scale(alpha * g.c, x[u]), beta, ims);
       }
+  }
+}
+
+// a seg job inside the general permute kernel (launches that mix seg with tiled / box jobs)
+template <int CM>
+__device__ void permute_seg(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                            const int64_t* __restrict__ blob, const PermJob& job, int64_t* sm, double alpha,
+                            double beta, double ims) {
+  const longlong2* g2 = reinterpret_cast<const longlong2*>(blob + job.first);
+  longlong2* s2 = reinterpret_cast<longlong2*>(sm);
+  const int n2 = job.group >> 1;
+  for (int i = threadIdx.x; i < n2; i += kPermThreads) s2[i] = __ldg(g2 + i);
+  __syncthreads();
+  pdl_wait();
+  seg_body<CM>(src, dst, sm, alpha, beta, ims);
+}
+
+__device__ __forceinline__ void seg_fetch(int64_t* buf, const int64_t* __restrict__ blob, const PermJob& job) {
+  const int n2 = job.group >> 1;
+  const int64_t* g = blob + job.first;
+  for (int i = threadIdx.x; i < n2; i += kPermThreads) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + 2 * i);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g + 2 * i));
+  }
+}
+
+// Launches made only of seg jobs: persistent CTAs (grid = resident capacity) walk the jobs with a
+// static stride; the next job's blob is fetched with cp.async into the second buffer while the current
+// job moves data, so the only exposed plan-data latency is the first job's.
+template <int CM>
+__global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB)
+    permute_seg_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs, int njobs) {
+  using IO = CIO<CM>;
+  __shared__ __align__(16) int64_t buf[2][kSegWords];
+  pdl_trigger();
+  const int G = gridDim.x;
+  int j = blockIdx.x;
+  PermJob cur = jobs[j], nxt{};
+  bool has_nxt = j + G < njobs;
+  if (has_nxt) nxt = jobs[j + G];
+  seg_fetch(buf[0], (cur.op ? op1 : op0).blob, cur);
+  cp_async_commit();
+  for (int it = 0;; ++it) {
+    const bool has_nn = j + 2 * G < njobs;
+    PermJob nn{};
+    if (has_nn) nn = jobs[j + 2 * G];
+    if (has_nxt) seg_fetch(buf[(it + 1) & 1], (nxt.op ? op1 : op0).blob, nxt);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (it == 0) pdl_wait();
+    const PermOp& op = cur.op ? op1 : op0;
+    seg_body<CM>((const typename IO::S*)op.src, (typename IO::D*)op.dst, buf[it & 1], op.alpha, op.beta, op.ims);
+    if (!has_nxt) break;
+    __syncthreads();  // buf[it & 1] is refilled by the next iteration's prefetch
+    j += G;
+    cur = nxt;
+    nxt = nn;
+    has_nxt = has_nn;
   }
 }
 
@@ -782,8 +849,21 @@ __global__ void __launch_bounds__(kPermThreads, 2)
 }
 
 template <int CM>
+static int seg_grid(int njobs) {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, permute_seg_kernel<CM>, kPermThreads, 0);
+    cap = std::max(1, sms * std::max(1, per));
+  }
+  return std::min(njobs, cap);
+}
+
+template <int CM>
 static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int njobs, int njobs_multi, bool tiled,
-                              bool rows_only, cudaStream_t st) {
+                              int variant, cudaStream_t st) {
   const int smem = tiled ? kTileElems * (int)sizeof(typename CIO<CM>::V) : 0;
   static bool attr = false;
   if (!attr) {
@@ -791,19 +871,23 @@ static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int n
                          kTileElems * (int)sizeof(typename CIO<CM>::V));
     attr = true;
   }
-  if (njobs && rows_only) launch_k(permute_kernel<CM, true>, njobs, kPermThreads, 0, st, op0, op1, jobs);
-  if (njobs && !rows_only) launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
+  if (njobs && variant == kLaunchRowsOnly) launch_k(permute_kernel<CM, true>, njobs, kPermThreads, 0, st, op0, op1, jobs);
+  static const bool persist = getenv("TK_SEG_PERSIST") != nullptr;
+  if (variant == kLaunchSegOnly && !persist) variant = kLaunchGeneral;
+  if (njobs && variant == kLaunchSegOnly)
+    launch_k(permute_seg_kernel<CM>, seg_grid<CM>(njobs), kPermThreads, 0, st, op0, op1, jobs, njobs);
+  if (njobs && variant == kLaunchGeneral) launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
   if (njobs_multi) launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, 0, st, op0, op1, jobs + njobs);
 }
 
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
-                           bool tiled, bool rows_only, int cm, cudaStream_t st) {
+                           bool tiled, int variant, int cm, cudaStream_t st) {
   switch (cm) {
-    case kPermReal: launch_permute_cm<kPermReal>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
-    case kPermCToC: launch_permute_cm<kPermCToC>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
-    case kPermCToPlanar: launch_permute_cm<kPermCToPlanar>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
-    case kPermCToRealRep: launch_permute_cm<kPermCToRealRep>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
-    case kPermPlanarToC: launch_permute_cm<kPermPlanarToC>(op0, op1, jobs, njobs, njobs_multi, tiled, rows_only, st); break;
+    case kPermReal: launch_permute_cm<kPermReal>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
+    case kPermCToC: launch_permute_cm<kPermCToC>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
+    case kPermCToPlanar: launch_permute_cm<kPermCToPlanar>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
+    case kPermCToRealRep: launch_permute_cm<kPermCToRealRep>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
+    case kPermPlanarToC: launch_permute_cm<kPermPlanarToC>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -60,6 +60,10 @@ enum PermCM : int {
 
 // A CTA work item: `count` work units of group `group` starting at unit `first`.
 // mode 0 unit = one row (dst leg 0); mode 1 unit = one smem tile of c0 x ct x R elements.
+#ifndef TK_PERM_THREADS
+#define TK_PERM_THREADS 256  // threads per permute CTA
+#endif
+constexpr int kPermThreads = TK_PERM_THREADS;
 constexpr int kTileElems = 4608;  // smem capacity of the two tile buffers (elements, incl. padding)
 // packed jobs: `count` consecutive small single-member rows groups starting at `group` (first unused),
 // so that tiny subblocks (cfg3: 9756 subblocks of ~700 elements) do not cost one CTA each
@@ -68,25 +72,25 @@ constexpr int kPackRows = 1024;
 constexpr int kPackElems = 8192;
 enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3, kJobBox = 4, kJobSeg = 5 };
 // Latency-regime jobs (kJobSeg, permutes below 2^24 elements): the planner precomputes everything a
-// CTA needs into one contiguous blob of 8-byte words -- SegHeader, `ng` SegGroup chunks (a row range
-// of one single-member group each), then the final source / destination offsets of every row start
-// (rs[nrows], rd[nrows]) -- so a CTA's prologue is one coalesced copy of plan data into shared memory
-// (issued before griddepcontrol.wait, overlapping the previous kernel) instead of a dependent chain of
-// job -> group -> member loads and per-row index divisions. Job: first = word offset of the blob,
-// group = its length in words (even), count = ng.
+// CTA needs into one contiguous blob -- SegHeader, `ng` SegGroup chunks (a row range of one
+// single-member group each), then the source / destination offsets of every row start as int32
+// (rs[nrows], rd[nrows]; offsets of permutes this small fit) -- so a CTA's prologue is one coalesced
+// copy of plan data into shared memory (issued before griddepcontrol.wait, overlapping the previous
+// kernel) instead of a dependent chain of job -> group -> member loads and per-row index divisions.
+// Job: first = 8-byte word offset of the blob, group = its length in words (even), count = ng.
 struct SegHeader {
   int32_t ng, nrows, total, pad;
 };
 struct SegGroup {
-  int32_t estart, rstart;  // first element / first row of this chunk within the job
-  uint32_t n0, fm, fs, pad;  // row length and its division magic (FastDiv)
-  int64_t s0, d0;          // element strides along the row (source, destination)
-  double c;                // coefficient (+-1 fermionic sign)
-  int64_t sd1, dd1, dd2;   // complex-mode offsets of the source / destination member (PermCM)
-  int64_t pad2;
+  int32_t estart, rstart;    // first element / first row of this chunk within the job
+  uint32_t n0, fm, fs;       // row length and its division magic (FastDiv)
+  uint32_t q, rem, pad;      // kPermThreads = q * n0 + rem (per-thread walk: stride kPermThreads)
+  int64_t s0, d0;            // element strides along the row (source, destination)
+  double c;                  // coefficient (+-1 fermionic sign)
+  int64_t sd1, dd1, dd2;     // complex-mode offsets of the source / destination member (PermCM)
 };
 static_assert(sizeof(SegHeader) == 16 && sizeof(SegGroup) == 80, "seg blob layout");
-constexpr int kSegWords = 2 + 10 * kPackGroups + 2 * kPackRows;
+constexpr int kSegWords = 2 + 10 * kPackGroups + kPackRows;  // rs + rd: 2 x kPackRows int32
 constexpr int kBoxElems = 4096;  // doubles per box (ComplexF64: half as many elements)
 struct PermJob {
   int32_t group;
@@ -130,9 +134,11 @@ struct GemmTile {
 // write workspace only and require beta == 0.
 // job table layout: [rows / tiled / packed jobs (njobs, one launch) | recoupling jobs (njobs_multi)];
 // `tiled`: some job is smem-tiled (dynamic shared memory needed). Modes 2 and 3 require beta == 0.
-// rows_only: every job of the first launch is a rows job (leaner kernel instance)
+// variant: kLaunchRowsOnly -- every job of the first launch is a rows job (leaner kernel instance);
+// kLaunchSegOnly -- every job is a kJobSeg job (persistent kernel with blob prefetch)
+enum PermLaunch : int { kLaunchGeneral = 0, kLaunchRowsOnly = 1, kLaunchSegOnly = 2 };
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
-                           bool tiled, bool rows_only, int cm, cudaStream_t st);
+                           bool tiled, int variant, int cm, cudaStream_t st);
 // tile table layout: [big (128x128 DMMA) | small (64x64 DMMA) | skinny (streaming, GemmTile.pad = rows)]
 constexpr int kSkinnyMax = 16;   // skinny groups: 0 < K <= 16 and N <= 16
 constexpr int kSkinnyRows = 2048;

@@ -229,7 +229,7 @@ struct SegBuilder {
   std::vector<PermJob>& jobs;
   int64_t job_elems;
   std::vector<SegGroup> cg;
-  std::vector<int64_t> rs, rd;
+  std::vector<int32_t> rs, rd;
   int64_t elems = 0;
   SegBuilder(PermPlan& P_, std::vector<PermJob>& j, int64_t je) : P(P_), jobs(j), job_elems(je) {}
   static void fastdiv(uint32_t d, uint32_t& m, uint32_t& s) {  // = FastDiv::init (tk_kernels.cu)
@@ -247,8 +247,11 @@ struct SegBuilder {
       const int64_t* w = reinterpret_cast<const int64_t*>(&g);
       P.blob.insert(P.blob.end(), w, w + 10);
     }
-    P.blob.insert(P.blob.end(), rs.begin(), rs.end());
-    P.blob.insert(P.blob.end(), rd.begin(), rd.end());
+    std::vector<int32_t> rr(rs);
+    rr.insert(rr.end(), rd.begin(), rd.end());
+    if (rr.size() & 1) rr.push_back(0);
+    const int64_t* rw = reinterpret_cast<const int64_t*>(rr.data());
+    P.blob.insert(P.blob.end(), rw, rw + rr.size() / 2);
     if (P.blob.size() & 1) P.blob.push_back(0);
     jobs.push_back(PermJob{(int32_t)(P.blob.size() - first), (int16_t)cg.size(), kJobSeg, 0, first});
     cg.clear();
@@ -259,7 +262,15 @@ struct SegBuilder {
   void add(int gi) {
     const PermGroup& g = P.groups[gi];
     const PermMember ms = P.members[g.src_mem], md = P.members[g.dst_mem];
-    const int64_t n0 = g.ext[0], nrows = g.nelem / n0;
+    // the row leg: destination leg 0 for rows groups (unit stride on both sides); for transposing
+    // groups the source-fastest leg, so loads stay coalesced and the stores scatter (TK_SEG_DSTLEG=1:
+    // always destination leg 0)
+    static const bool dst_leg = getenv("TK_SEG_DSTLEG") != nullptr;
+    int L = 0;
+    if (g.mode != 0 && !dst_leg)
+      for (int l = 1; l < g.ndim; ++l)
+        if (std::make_pair(g.sb[l], g.sa[l]) < std::make_pair(g.sb[L], g.sa[L])) L = l;
+    const int64_t n0 = g.ext[L], nrows = g.nelem / n0;
     if (n0 > INT32_MAX / 2) TK_THROW(TK_ERR_UNSUPPORTED, "row too long for a seg job");
     for (int64_t r0 = 0; r0 < nrows;) {
       int64_t room = std::min<int64_t>((job_elems - elems) / n0, kPackRows - (int64_t)rs.size());
@@ -276,8 +287,10 @@ struct SegBuilder {
       sg.rstart = (int32_t)rs.size();
       sg.n0 = (uint32_t)n0;
       fastdiv(sg.n0, sg.fm, sg.fs);
-      sg.s0 = g.sa[0] + ms.ld * g.sb[0];
-      sg.d0 = g.da[0] + md.ld * g.db[0];
+      sg.q = (uint32_t)(kPermThreads / n0);
+      sg.rem = (uint32_t)(kPermThreads % n0);
+      sg.s0 = g.sa[L] + ms.ld * g.sb[L];
+      sg.d0 = g.da[L] + md.ld * g.db[L];
       sg.c = P.coefs[g.coef_off];
       sg.sd1 = ms.d1;
       sg.dd1 = md.d1;
@@ -285,7 +298,8 @@ struct SegBuilder {
       cg.push_back(sg);
       for (int64_t r = r0; r < r0 + nr; ++r) {
         int64_t R = r, sa = 0, sbb = 0, da = 0, db = 0;
-        for (int l = 1; l < g.ndim; ++l) {
+        for (int l = 0; l < g.ndim; ++l) {
+          if (l == L) continue;
           const int64_t i = R % g.ext[l];
           R /= g.ext[l];
           sa += i * g.sa[l];
@@ -293,8 +307,13 @@ struct SegBuilder {
           da += i * g.da[l];
           db += i * g.db[l];
         }
-        rs.push_back(ms.off + sa + ms.ld * sbb);
-        rd.push_back(md.off + da + md.ld * db);
+        const int64_t os = ms.off + sa + ms.ld * sbb, od = md.off + da + md.ld * db;
+        // int32 offsets: the last element of the row (and its complex-mode partners) must fit
+        const int64_t reach = 2 * ((n0 - 1) * std::max<int64_t>(std::abs(sg.s0), std::abs(sg.d0)) + std::max(os, od)) +
+                              2 * (ms.d1 + md.d1 + md.d2);
+        if (reach >= INT32_MAX) TK_THROW(TK_ERR_UNSUPPORTED, "seg job offsets exceed int32");
+        rs.push_back((int32_t)os);
+        rd.push_back((int32_t)od);
       }
       elems += nr * n0;
       r0 += nr;
@@ -318,10 +337,12 @@ static void make_jobs(PermPlan& P) {
   static const bool no_seg = getenv("TK_NO_SEG") != nullptr;
   const bool seg = !no_seg && total < (int64_t(1) << 24);
   std::vector<PermJob> segs;
-  SegBuilder sb(P, segs, job_elems);
+  // seg jobs are walked by persistent CTAs (about 3 jobs each at full occupancy), so they are smaller
+  static const int64_t seg_div = getenv("TK_SEG_DIV") ? atoll(getenv("TK_SEG_DIV")) : 2 * 148 * 4;
+  SegBuilder sb(P, segs, std::max<int64_t>(256, std::min<int64_t>(kPackElems, total / seg_div)));
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
-    if (seg && g.ksrc == 1 && g.kdst == 1 && (packable(g) || g.mode == 0)) {
+    if (seg && g.ksrc == 1 && g.kdst == 1 && g.mode != 2) {
       sb.add(gi);
       continue;
     }
@@ -370,6 +391,7 @@ static void make_jobs(PermPlan& P) {
   P.njobs_multi = (int)multi.size();
   P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
   P.rows_only = tiles.empty() && packed.empty() && segs.empty();
+  P.seg_only = rows.size() == segs.size() && tiles.empty() && packed.empty();
   P.split = total >= (int64_t(1) << 24) && !P.rows_only && !rows.empty();
   static const bool dbg = getenv("TK_PLAN_DEBUG") != nullptr;
   if (dbg) {
@@ -598,7 +620,7 @@ struct ContractPlan {
   bool merged_ab = false;
   std::vector<PermJob> jobs_ab;
   int njobs_ab = 0, njobs_ab_multi = 0;
-  bool ab_tiled = false;
+  bool ab_tiled = false, ab_seg_only = false;
   DevBuf d_ggroups, d_tiles, d_jobs_ab;
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
@@ -769,6 +791,7 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
     P.njobs_ab = P.pa.njobs + P.pb.njobs;
     P.njobs_ab_multi = P.pa.njobs_multi + P.pb.njobs_multi;
     P.ab_tiled = P.pa.tiled || P.pb.tiled;
+    P.ab_seg_only = P.pa.seg_only && P.pb.seg_only;
   }
   // workspace: A~ | B~ | C~ (skipped when the permute is the identity)
   size_t off = 0;
@@ -973,12 +996,14 @@ void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double b
   if (P.jobs.empty()) return;
   const PermJob* jobs = (const PermJob*)P.d_jobs.p;
   if (P.split) {
-    check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, true, cm, st), "permute launch");
-    check_cuda(launch_permute(op, op, jobs + P.njobs_rows, P.njobs - P.njobs_rows, P.njobs_multi, P.tiled, false, cm, st),
+    check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, kLaunchRowsOnly, cm, st), "permute launch");
+    check_cuda(launch_permute(op, op, jobs + P.njobs_rows, P.njobs - P.njobs_rows, P.njobs_multi, P.tiled,
+                              kLaunchGeneral, cm, st),
                "permute launch");
     g_launches += 1 + (P.njobs > P.njobs_rows) + (P.njobs_multi > 0);
   } else {
-    check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, P.rows_only, cm, st), "permute launch");
+    const int variant = P.seg_only ? kLaunchSegOnly : P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
+    check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, variant, cm, st), "permute launch");
     g_launches += (P.njobs > 0) + (P.njobs_multi > 0);
   }
 }
@@ -1121,7 +1146,7 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
   if (P->merged_ab) {
     PermOp oa = perm_op(P->pa, a, (double*)At, 1.0, 0.0, 1.0), ob = perm_op(P->pb, b, (double*)Bt, 1.0, 0.0, 1.0);
     check_cuda(launch_permute(oa, ob, (const PermJob*)P->d_jobs_ab.p, P->njobs_ab, P->njobs_ab_multi, P->ab_tiled,
-                              false, kPermReal, st),
+                              P->ab_seg_only ? kLaunchSegOnly : kLaunchGeneral, kPermReal, st),
                "permute launch");
     g_launches += (P->njobs_ab > 0) + (P->njobs_ab_multi > 0);
   } else if (!P->pa.identity) {
