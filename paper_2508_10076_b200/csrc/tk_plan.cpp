@@ -899,6 +899,18 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   P.ntiles_big = (int)big.size();
   P.ntiles_small = (int)small.size();
   P.ntiles_skinny = (int)skinny.size();
+  if (getenv("TK_PLAN_DEBUG")) {
+    int mM = 0, mN = 0, mK = 0, nz = 0;
+    double fpad = 0;
+    for (const GemmGroup& g : P.ggroups) {
+      mM = std::max(mM, g.M), mN = std::max(mN, g.N), mK = std::max(mK, g.K), nz += g.K > 0;
+    }
+    for (const GemmTile& t : big) fpad += 2.0 * 128 * 128 * (t.k1 - t.k0);
+    for (const GemmTile& t : small) fpad += 2.0 * 64 * 64 * (t.k1 - t.k0);
+    fprintf(stderr, "[tk gemm] %zu groups (%d with K>0), %.3g flops, max M %d N %d K %d | big %zu small %zu skinny %zu "
+            "tiles, split slots %d | tile flops %.3g\n", P.ggroups.size(), nz, P.flops, mM, mN, mK, big.size(),
+            small.size(), skinny.size(), P.nslots, fpad);
+  }
   P.tiles = big;
   P.tiles.insert(P.tiles.end(), small.begin(), small.end());
   P.tiles.insert(P.tiles.end(), skinny.begin(), skinny.end());
