@@ -402,6 +402,14 @@ static void make_jobs(PermPlan& P) {
       else if (g.ksrc == 1 && g.kdst == 1) er += g.nelem, ++gr;
       else em += g.nelem;
     }
+    int sg_ng = 0, sg_rows = 0, sg_el = 0;
+    for (const PermJob& j : segs) {
+      const SegHeader* h = reinterpret_cast<const SegHeader*>(P.blob.data() + j.first);
+      sg_ng = std::max(sg_ng, h->ng), sg_rows = std::max(sg_rows, h->nrows), sg_el = std::max(sg_el, h->total);
+    }
+    if (!segs.empty())
+      fprintf(stderr, "[tk plan] seg: %zu jobs, max %d chunks / %d rows / %d elements per job\n", segs.size(), sg_ng,
+              sg_rows, sg_el);
     fprintf(stderr, "[tk plan] %lld elems, job_elems %lld: rows %zu jobs (%lld groups, %lld el) | tiled %zu (%lld, %lld el) | "
             "packed %zu (%lld, %lld el) | multi %zu (%lld el)\n", (long long)total, (long long)job_elems, rows.size(),
             (long long)gr, (long long)er, tiles.size(), (long long)gt, (long long)et, packed.size(), (long long)gp,

@@ -119,3 +119,50 @@ def test_workspace_too_small_leaves_output():
     assert e.value.status == "TK_ERR_WORKSPACE_TOO_SMALL"
     torch.cuda.synchronize()
     assert bool((c == 7.0).all())
+
+
+# ------------------------------------------------------------------ seg jobs (latency-regime permutes)
+# Permutes below 2^24 elements run as kJobSeg jobs (tk_kernels.hpp): chunks of <= 32 groups and
+# <= 1024 rows per job, one row longer than a job taking a job of its own, transposing groups walked
+# along the source-fastest leg. Each case below drives one of those limits.
+def test_seg_long_row():
+    V = [((0,), 10000)]
+    S = [((0,), 1), ((1,), 1)]
+    # V (x) S <- S, permuted to (S, V ; S): one 10000-element row per block (> job_elems = 512)
+    err = _perm_case_spaces("U1", [W.space("U1", V), W.space("U1", S)], [W.space("U1", S)], [1, 0], [2])
+    assert err <= TOL
+
+
+def test_seg_many_tiny_groups():
+    from tests.test_gpu_parity import _perm_case
+    secs = [((q,), 1) for q in range(-3, 4)]  # 1-element subblocks: > 32 groups per job
+    assert _perm_case("U1", secs, [0, 0], [0, 0], [2, 0], [3, 1], alpha=-1.5) <= TOL
+    assert _perm_case("fU1xU1", [((0, 0), 1), ((1, 1), 1), ((1, -1), 1), ((2, 0), 1), ((-1, 1), 1)],
+                      [0, 1], [0], [2, 1], [0]) <= TOL
+
+
+def test_seg_transposes():
+    from tests.test_gpu_parity import _perm_case
+    secs = [((0,), 40), ((1,), 30), ((-1,), 20)]
+    assert _perm_case("U1", secs, [0, 1], [], [1, 0], [], beta=0.5) <= TOL
+    assert _perm_case("U1", secs, [0], [0, 1], [2, 1], [0]) <= TOL
+    # 3.2 M elements in rows of 2: job_elems ~ 2700 > 1024 rows x 2, so the row limit of a job binds
+    V1 = W.space("U1", [((0,), 2), ((1,), 2), ((-1,), 2)])
+    V = W.space("U1", [((0,), 40), ((1,), 40), ((-1,), 40), ((2,), 20)])
+    assert _perm_case_spaces("U1", [V1, V], [V, V], [0, 2], [1, 3]) <= TOL
+
+
+def _perm_case_spaces(kind, cod, dom, p, q, seed=0):
+    from paper_2508_10076_b200 import tk
+    lt = OL.homspace_layout(kind, cod, dom)
+    x = np.random.default_rng(seed).standard_normal(lt.nelems)
+    c2, d2 = OC.permuted_spaces(cod, dom, p, q)
+    ls = OL.homspace_layout(kind, c2, d2)
+    par = [OD.parity_vector(s) for s in cod + dom]
+    ref = OC.permute_dense(OD.to_dense(lt, x), par, len(cod), p, q)
+    A = tk.tensor_from_spec({"cod": cod, "dom": dom})
+    C = tk.tensor_from_spec({"cod": c2, "dom": d2})
+    c = torch.full((ls.nelems,), float("nan"), dtype=torch.float64, device="cuda")
+    tk.tk_permute(A, torch.from_numpy(x).cuda(), p, q, C, c)
+    torch.cuda.synchronize()
+    return OC.rel_frobenius(OD.to_dense(ls, c.cpu().numpy()), ref)
