@@ -1218,7 +1218,7 @@ __global__ void __launch_bounds__(MbarCfg::THREADS, 1)
   extern __shared__ __align__(16) double smem[];
   pdl_trigger();
   const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup g = groups[t.group];
+  const GemmGroup& g = t.g;
   pdl_wait();
   gemm_tile_mbar<TK_MBAR, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(SmallCfg::THREADS, TK_SMALL_MINB)
   extern __shared__ __align__(16) double smem[];
   pdl_trigger();
   const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup g = groups[t.group];
+  const GemmGroup& g = t.g;
   pdl_wait();
   double* part = t.slot >= 0 ? parts + (int64_t)t.slot * (64 * 64) : nullptr;
   gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem, t.k0, t.k1, part);
@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__(256)
                               double beta) {
   pdl_trigger();
   const GemmTile t = heads[blockIdx.x];
-  const GemmGroup g = groups[t.group];
+  const GemmGroup& g = t.g;
   pdl_wait();
   double* Cg = C + g.c_off;
   for (int e = blockIdx.y * 1024 + threadIdx.x; e < (blockIdx.y + 1) * 1024; e += 256) {
@@ -1327,7 +1327,7 @@ __global__ void __launch_bounds__(kSkinnyThreads)
   __shared__ double Bs[kSkinnyMax * kSkinnyMax];
   pdl_trigger();
   const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup g = groups[t.group];
+  const GemmGroup& g = t.g;
   const int K = g.K, N = g.N;
   pdl_wait();
   for (int i = threadIdx.x; i < kSkinnyMax * kSkinnyMax; i += kSkinnyThreads) {

@@ -127,6 +127,7 @@ struct GemmTile {
   int32_t k0, k1;      // k range of this tile (split-K: a slice of [0, K))
   int32_t slot;        // split-K: partial-tile slot (-1: write C directly); reduction heads: first slot
   int32_t nsplit;      // reduction heads: number of partial slots
+  GemmGroup g;         // copy of groups[group]: a CTA's descriptors arrive in one round trip
 };
 
 // launchers (tk_kernels.cu)

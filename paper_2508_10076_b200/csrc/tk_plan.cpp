@@ -914,7 +914,14 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
       mM = std::max(mM, g.M), mN = std::max(mN, g.N), mK = std::max(mK, g.K), nz += g.K > 0;
     }
     for (const GemmTile& t : big) fpad += 2.0 * 128 * 128 * (t.k1 - t.k0);
-    for (const GemmTile& t : small) fpad += 2.0 * 64 * 64 * (t.k1 - t.k0);
+    double fdmma = 0;  // what the small kernel's fragment guards actually issue (8-row / 8-col / 4-k units)
+    for (const GemmTile& t : small) {
+      fpad += 2.0 * 64 * 64 * (t.k1 - t.k0);
+      const GemmGroup& g = P.ggroups[t.group];
+      auto up = [](int x, int q) { return (x + q - 1) / q * q; };
+      fdmma += 2.0 * up(std::min(64, g.M - t.m0), 8) * up(std::min(64, g.N - t.n0), 8) * up(t.k1 - t.k0, 4);
+    }
+    fprintf(stderr, "[tk gemm] small-tile DMMA flops issued %.3g\n", fdmma);
     fprintf(stderr, "[tk gemm] %zu groups (%d with K>0), %.3g flops, max M %d N %d K %d | big %zu small %zu skinny %zu "
             "tiles, split slots %d | tile flops %.3g\n", P.ggroups.size(), nz, P.flops, mM, mN, mK, big.size(),
             small.size(), skinny.size(), P.nslots, fpad);
@@ -922,6 +929,8 @@ static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tens
   P.tiles = big;
   P.tiles.insert(P.tiles.end(), small.begin(), small.end());
   P.tiles.insert(P.tiles.end(), skinny.begin(), skinny.end());
+  for (GemmTile& t : P.tiles) t.g = P.ggroups[t.group];
+  for (GemmTile& t : P.split_heads) t.g = P.ggroups[t.group];
 }
 
 // ------------------------------------------------------------------ plan cache
