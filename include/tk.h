@@ -148,6 +148,26 @@ tk_status tk_contract(const tk_tensor* A, const void* a, const int32_t* labA, in
                       const tk_tensor* C, void* c, const int32_t* labC, double alpha, double beta,
                       void* ws, size_t ws_bytes, tk_stream stream);
 
+/* Low-level Alg. 4 entry (Alg. 8; reading C1: B~ = permute(B, (pB, qB))):
+ *   A~ = permute(A, (pA, qA)),  B~ = permute(B, (pB, qB)),  C~ = A~ o B~,
+ *   C  = alpha * permute(C~, (pAB, qAB)) + beta * C.
+ * The tuples are given explicitly instead of being derived from labels by reading C2, so a caller can
+ * fix the operand orders -- for fermionic kinds they are part of the definition (reading C13).
+ * tup: the six 0-based tuples concatenated, pA | qA | pB | qB | pAB | qAB; ntup[6]: their lengths.
+ * (pA, qA) must permute A's legs and (pB, qB) B's (else TK_ERR_INVALID_PERMUTATION), |qA| == |pB|,
+ * leg qA[c] of A and pB[c] of B a ket/bra pair (else TK_ERR_SPACE_MISMATCH), (pAB, qAB) a permutation of
+ * the |pA| + |qB| legs of C~ (codomain: pA legs in pA order, domain: qB legs in qB order).
+ * tk_contract_tuples_output returns C's HomSpace; data, conj flags, alpha / beta, workspace and stream
+ * behave as in tk_contract. */
+tk_status tk_contract_tuples_output(const tk_tensor* A, const tk_tensor* B, const int32_t* tup,
+                                   const int32_t* ntup, tk_tensor** C);
+tk_status tk_contract_tuples_workspace(const tk_tensor* A, const tk_tensor* B, const tk_tensor* C,
+                                       const int32_t* tup, const int32_t* ntup, size_t* bytes);
+tk_status tk_contract_tuples(const tk_tensor* A, const void* a, int32_t conjA, const tk_tensor* B,
+                             const void* b, int32_t conjB, const tk_tensor* C, void* c,
+                             const int32_t* tup, const int32_t* ntup, double alpha, double beta,
+                             void* ws, size_t ws_bytes, tk_stream stream);
+
 /* -------------------------------------------------- blockwise truncated SVD */
 /* A~ = permute(A, (p, q)) = U S Vh, block by block (eq. svd, "directly acting on the matrix
  * representation" P:799-809; Alg. 9). U: (A~ codomain) <- W, S: W <- W diagonal, Vh: W <- (A~

@@ -116,6 +116,13 @@ def contract_alg4(A, A_spaces, nA, labA, B, B_spaces, nB, labB, labC, n_cod_C):
     A_spaces / B_spaces: the leg spaces in (cod..., dom...) order; nA, nB the codomain counts.
     """
     pA, qA, pB, qB, pAB, qAB = tuples_from_labels(labA, labB, labC, n_cod_C)
+    return contract_alg4_tuples(A, A_spaces, nA, B, B_spaces, nB, pA, qA, pB, qB, pAB, qAB)
+
+
+def contract_alg4_tuples(A, A_spaces, nA, B, B_spaces, nB, pA, qA, pB, qB, pAB, qAB):
+    """Dense Alg. 4 with explicit tuples: A~ = permute(A, (pA, qA)), B~ = permute(B, (pB, qB))
+    (reading C1), C~ = A~ o B~ (a matmul over the qA / pB legs), C = permute(C~, (pAB, qAB)).
+    Permutes carry the Koszul sign of reading C13 (+1 for bosonic kinds)."""
     parA = [parity_vector(sp) for sp in A_spaces]
     parB = [parity_vector(sp) for sp in B_spaces]
     At = permute_dense(A, parA, nA, pA, qA)

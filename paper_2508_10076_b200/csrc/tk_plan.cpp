@@ -655,6 +655,53 @@ struct Tuples {
   std::vector<int> pA, qA, pB, qB, pAB, qAB;
 };
 
+// contracted legs qA[c] <-> pB[c] must be a ket/bra pair: normalised spaces (cod: X, dom: X*) dual
+// to each other
+static void check_contracted_pairs(const Tensor& A, const Tensor& B, const Tuples& t) {
+  for (size_t c = 0; c < t.qA.size(); ++c) {
+    int ia = t.qA[c], jb = t.pB[c];
+    const Space* sa = ia < A.n_cod() ? A.cod[ia] : A.dom[ia - A.n_cod()];
+    const Space* sb = jb < B.n_cod() ? B.cod[jb] : B.dom[jb - B.n_cod()];
+    bool da = sa->dual ^ (ia >= A.n_cod()), db = sb->dual ^ (jb >= B.n_cod());
+    if (sa->kind != sb->kind || sa->sectors != sb->sectors || sa->degs != sb->degs || da == db)
+      TK_THROW(TK_ERR_SPACE_MISMATCH, "contracted legs are not a ket/bra pair of the same space");
+  }
+}
+
+// Explicit Alg. 4 tuples (reading C1: B~ = permute(B, (pB, qB))): (pA, qA) and (pB, qB)
+// permutations of A's and B's legs, |qA| == |pB|, (pAB, qAB) a permutation of C~'s |pA| + |qB| legs.
+static Tuples tuples_from_arrays(const Tensor& A, const Tensor& B, const int32_t* tup, const int32_t* ntup) {
+  if (!ntup) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null tuple counts");
+  int64_t tot = 0;
+  for (int i = 0; i < 6; ++i) {
+    if (ntup[i] < 0) TK_THROW(TK_ERR_INVALID_PERMUTATION, "negative tuple length");
+    tot += ntup[i];
+  }
+  if (tot && !tup) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null tuples");
+  Tuples t;
+  std::vector<int>* dst[6] = {&t.pA, &t.qA, &t.pB, &t.qB, &t.pAB, &t.qAB};
+  int64_t o = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int k = 0; k < ntup[i]; ++k) dst[i]->push_back(tup[o++]);
+  auto is_perm = [](const std::vector<int>& p, const std::vector<int>& q, int n) {
+    if ((int)(p.size() + q.size()) != n) return false;
+    std::vector<int> seen(n, 0);
+    for (const auto* v : {&p, &q})
+      for (int x : *v) {
+        if (x < 0 || x >= n || seen[x]) return false;
+        seen[x] = 1;
+      }
+    return true;
+  };
+  if (!is_perm(t.pA, t.qA, A.nlegs()) || !is_perm(t.pB, t.qB, B.nlegs()))
+    TK_THROW(TK_ERR_INVALID_PERMUTATION, "(pA, qA) / (pB, qB) must permute the operand's legs");
+  if (t.qA.size() != t.pB.size()) TK_THROW(TK_ERR_INVALID_PERMUTATION, "|qA| != |pB|");
+  if (!is_perm(t.pAB, t.qAB, (int)(t.pA.size() + t.qB.size())))
+    TK_THROW(TK_ERR_INVALID_PERMUTATION, "(pAB, qAB) must permute the |pA| + |qB| legs of A~ B~");
+  check_contracted_pairs(A, B, t);
+  return t;
+}
+
 // Reading C2: A~ = (open A in A order ; contracted in A order), B~ = (contracted ; open B),
 // C~ = (open A ; open B), then permute C~ to labC. Validates labels.
 static Tuples tuples_from_labels(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
@@ -699,15 +746,7 @@ static Tuples tuples_from_labels(const Tensor& A, const int32_t* labA, const Ten
     if (pos < 0) TK_THROW(TK_ERR_UNKNOWN_LABEL, "labC has a label that is not open");
     (i < nC_cod ? t.pAB : t.qAB).push_back(pos);
   }
-  // contracted legs must be a ket/bra pair: normalised spaces (cod: X, dom: X*) dual to each other
-  for (size_t c = 0; c < t.qA.size(); ++c) {
-    int ia = t.qA[c], jb = t.pB[c];
-    const Space* sa = ia < A.n_cod() ? A.cod[ia] : A.dom[ia - A.n_cod()];
-    const Space* sb = jb < B.n_cod() ? B.cod[jb] : B.dom[jb - B.n_cod()];
-    bool da = sa->dual ^ (ia >= A.n_cod()), db = sb->dual ^ (jb >= B.n_cod());
-    if (sa->kind != sb->kind || sa->sectors != sb->sectors || sa->degs != sb->degs || da == db)
-      TK_THROW(TK_ERR_SPACE_MISMATCH, "contracted legs are not a ket/bra pair of the same space");
-  }
+  check_contracted_pairs(A, B, t);
   return t;
 }
 
@@ -751,13 +790,10 @@ Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::v
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static void build_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
-                                const Tensor& C, const int32_t* labC, ContractPlan& P) {
+static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& C, const Tuples& t, ContractPlan& P) {
   if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
   if (A.dtype != B.dtype || A.dtype != C.dtype) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_contract: dtypes differ");
   P.cplx = A.dtype == TK_C64;
-  Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
-  choose_contracted_order(A, B, t);
   P.At = permuted_tensor(A, t.pA, t.qA, A.dtype);
   P.Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
   {
@@ -951,8 +987,32 @@ static ContractPlan* get_contract_plan(const Tensor& A, const int32_t* labA, con
   std::lock_guard<std::mutex> g(g_cache_mu);
   auto it = g_contract_cache.find(key);
   if (it != g_contract_cache.end()) return it->second.get();
+  if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+  Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
+  choose_contracted_order(A, B, t);
   auto P = std::make_unique<ContractPlan>();
-  build_contract_plan(A, labA, B, labB, C, labC, *P);
+  build_contract_plan(A, B, C, t, *P);
+  ContractPlan* raw = P.get();
+  g_contract_cache[key] = std::move(P);
+  return raw;
+}
+
+static ContractPlan* get_contract_plan_tuples(const Tensor& A, const Tensor& B, const Tensor& C, const int32_t* tup,
+                                              const int32_t* ntup) {
+  if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+  Tuples t = tuples_from_arrays(A, B, tup, ntup);
+  std::ostringstream os;
+  os << "T#" << A.sig << "#" << B.sig << "#" << C.sig;
+  for (const auto* v : {&t.pA, &t.qA, &t.pB, &t.qB, &t.pAB, &t.qAB}) {
+    os << "#";
+    for (int x : *v) os << x << ",";
+  }
+  std::string key = os.str();
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  auto it = g_contract_cache.find(key);
+  if (it != g_contract_cache.end()) return it->second.get();
+  auto P = std::make_unique<ContractPlan>();
+  build_contract_plan(A, B, C, t, *P);
   ContractPlan* raw = P.get();
   g_contract_cache[key] = std::move(P);
   return raw;
@@ -1141,26 +1201,9 @@ tk_status tk_contract_output(const tk_tensor* A_, const int32_t* labA, const tk_
   TK_API_END
 }
 
-tk_status tk_contract_workspace(const tk_tensor* A, const int32_t* labA, const tk_tensor* B, const int32_t* labB,
-                                const tk_tensor* C, const int32_t* labC, size_t* bytes) {
-  TK_API_BEGIN
-  if (!A || !B || !C || !labA || !labB || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  ContractPlan* P = get_contract_plan(*(const Tensor*)A, labA, *(const Tensor*)B, labB, *(const Tensor*)C, labC);
-  *bytes = P->ws_bytes;
-  TK_API_END
-}
-
-tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, int32_t conjA, const tk_tensor* B_,
-                      const void* b, const int32_t* labB, int32_t conjB, const tk_tensor* C_, void* c,
-                      const int32_t* labC, double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
-  TK_API_BEGIN
-  if (!A_ || !B_ || !C_ || !labA || !labB) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  const Tensor& A = *(const Tensor*)A_;
-  const Tensor& B = *(const Tensor*)B_;
-  const Tensor& C = *(const Tensor*)C_;
-  if ((conjA || conjB) && A.dtype == TK_F64) TK_THROW(TK_ERR_INVALID_ARGUMENT, "conj flags need ComplexF64");
-  if ((!a && A.nelems) || (!b && B.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
-  ContractPlan* P = get_contract_plan(A, labA, B, labB, C, labC);
+// one contraction through a plan: operand permutes, grouped GEMM, output permute (Alg. 4)
+static void run_contract(ContractPlan* P, const void* a, const void* b, void* c, int32_t conjA, int32_t conjB,
+                         double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
   if (ws_bytes < P->ws_bytes || (P->ws_bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
   if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
   P->upload();
@@ -1205,6 +1248,74 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
     g_prof.bytes[3] = P->pc.identity ? 0 : P->pc.bytes;
     g_prof.flops = P->flops;
   }
+}
+
+tk_status tk_contract_workspace(const tk_tensor* A, const int32_t* labA, const tk_tensor* B, const int32_t* labB,
+                                const tk_tensor* C, const int32_t* labC, size_t* bytes) {
+  TK_API_BEGIN
+  if (!A || !B || !C || !labA || !labB || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  ContractPlan* P = get_contract_plan(*(const Tensor*)A, labA, *(const Tensor*)B, labB, *(const Tensor*)C, labC);
+  *bytes = P->ws_bytes;
+  TK_API_END
+}
+
+tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, int32_t conjA, const tk_tensor* B_,
+                      const void* b, const int32_t* labB, int32_t conjB, const tk_tensor* C_, void* c,
+                      const int32_t* labC, double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
+  TK_API_BEGIN
+  if (!A_ || !B_ || !C_ || !labA || !labB) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  const Tensor& A = *(const Tensor*)A_;
+  const Tensor& B = *(const Tensor*)B_;
+  const Tensor& C = *(const Tensor*)C_;
+  if ((conjA || conjB) && A.dtype == TK_F64) TK_THROW(TK_ERR_INVALID_ARGUMENT, "conj flags need ComplexF64");
+  if ((!a && A.nelems) || (!b && B.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
+  ContractPlan* P = get_contract_plan(A, labA, B, labB, C, labC);
+  run_contract(P, a, b, c, conjA, conjB, alpha, beta, ws, ws_bytes, stream);
+  TK_API_END
+}
+
+tk_status tk_contract_tuples_output(const tk_tensor* A_, const tk_tensor* B_, const int32_t* tup,
+                                   const int32_t* ntup, tk_tensor** out) {
+  TK_API_BEGIN
+  if (!A_ || !B_ || !out) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  const Tensor& A = *(const Tensor*)A_;
+  const Tensor& B = *(const Tensor*)B_;
+  if (A.kind != B.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+  if (A.dtype != B.dtype) TK_THROW(TK_ERR_INVALID_ARGUMENT, "dtypes differ");
+  Tuples t = tuples_from_arrays(A, B, tup, ntup);
+  Tensor* At = permuted_tensor(A, t.pA, t.qA, A.dtype);
+  Tensor* Bt = permuted_tensor(B, t.pB, t.qB, B.dtype);
+  std::vector<Space*> cod(At->cod), dom(Bt->dom);
+  Tensor* Ct = make_tensor(A.dtype, cod, dom, (int)A.kind);
+  Tensor* C = permuted_tensor(*Ct, t.pAB, t.qAB, A.dtype);
+  tk_tensor_release((tk_tensor*)At);
+  tk_tensor_release((tk_tensor*)Bt);
+  tk_tensor_release((tk_tensor*)Ct);
+  *out = (tk_tensor*)C;
+  TK_API_END
+}
+
+tk_status tk_contract_tuples_workspace(const tk_tensor* A, const tk_tensor* B, const tk_tensor* C, const int32_t* tup,
+                                       const int32_t* ntup, size_t* bytes) {
+  TK_API_BEGIN
+  if (!A || !B || !C || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  ContractPlan* P = get_contract_plan_tuples(*(const Tensor*)A, *(const Tensor*)B, *(const Tensor*)C, tup, ntup);
+  *bytes = P->ws_bytes;
+  TK_API_END
+}
+
+tk_status tk_contract_tuples(const tk_tensor* A_, const void* a, int32_t conjA, const tk_tensor* B_, const void* b,
+                             int32_t conjB, const tk_tensor* C_, void* c, const int32_t* tup, const int32_t* ntup,
+                             double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
+  TK_API_BEGIN
+  if (!A_ || !B_ || !C_) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  const Tensor& A = *(const Tensor*)A_;
+  const Tensor& B = *(const Tensor*)B_;
+  const Tensor& C = *(const Tensor*)C_;
+  if ((conjA || conjB) && A.dtype == TK_F64) TK_THROW(TK_ERR_INVALID_ARGUMENT, "conj flags need ComplexF64");
+  if ((!a && A.nelems) || (!b && B.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
+  ContractPlan* P = get_contract_plan_tuples(A, B, C, tup, ntup);
+  run_contract(P, a, b, c, conjA, conjB, alpha, beta, ws, ws_bytes, stream);
   TK_API_END
 }
 

@@ -78,6 +78,11 @@ _contract_workspace = _sig("tk_contract_workspace", [_p, _i32p, _p, _i32p, _p, _
                                                      ctypes.POINTER(ctypes.c_size_t)])
 _contract = _sig("tk_contract", [_p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p,
                                  ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
+_contract_tuples_output = _sig("tk_contract_tuples_output", [_p, _p, _i32p, _i32p, ctypes.POINTER(_p)])
+_contract_tuples_workspace = _sig("tk_contract_tuples_workspace", [_p, _p, _p, _i32p, _i32p,
+                                                                   ctypes.POINTER(ctypes.c_size_t)])
+_contract_tuples = _sig("tk_contract_tuples", [_p, _p, ctypes.c_int32, _p, _p, ctypes.c_int32, _p, _p, _i32p, _i32p,
+                                               ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
 _profile_enable = _sig("tk_profile_enable", [ctypes.c_int32])
 _phase_times = _sig("tk_phase_times", [ctypes.POINTER(ctypes.c_float), _dp, _dp])
 _last_launch_count = _sig("tk_last_launch_count", [], ctypes.c_int32)
@@ -111,7 +116,8 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_profile_enable", "tk_phase_times", "tk_last_launch_count", "tk_fsymbol", "tk_rsymbol",
             "tk_permute_transfer", "tk_permute_transfer_planar", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
             "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract", "tk_trace_output", "tk_trace_workspace",
-            "tk_trace", "tk_trace_transfer"]
+            "tk_trace", "tk_trace_transfer", "tk_contract_tuples_output", "tk_contract_tuples_workspace",
+            "tk_contract_tuples"]
 
 
 def _i32(seq):
@@ -292,6 +298,37 @@ def tk_contract(A, a, labA, B, b, labB, C, c, labC, alpha=1.0, beta=0.0, ws=None
     lc, cp = _i32(labC)
     _check(_contract(A.h, _ptr(a), ap, int(conjA), B.h, _ptr(b), bp, int(conjB), C.h, _ptr(c), cp, float(alpha),
                      float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def _tuples(pA, qA, pB, qB, pAB, qAB):
+    parts = [list(map(int, x)) for x in (pA, qA, pB, qB, pAB, qAB)]
+    flat = [x for part in parts for x in part]
+    t, tp = _i32(flat if flat else [0])
+    n, np_ = _i32([len(x) for x in parts])
+    return (t, n), tp, np_
+
+
+def tk_contract_tuples_output(A, pA, qA, B, pB, qB, pAB, qAB):
+    keep, tp, np_ = _tuples(pA, qA, pB, qB, pAB, qAB)
+    h = _p()
+    _check(_contract_tuples_output(A.h, B.h, tp, np_, ctypes.byref(h)))
+    return Tensor(h.value)
+
+
+def tk_contract_tuples_workspace(A, pA, qA, B, pB, qB, C, pAB, qAB):
+    keep, tp, np_ = _tuples(pA, qA, pB, qB, pAB, qAB)
+    n = ctypes.c_size_t()
+    _check(_contract_tuples_workspace(A.h, B.h, C.h, tp, np_, ctypes.byref(n)))
+    return n.value
+
+
+def tk_contract_tuples(A, a, pA, qA, B, b, pB, qB, C, c, pAB, qAB, alpha=1.0, beta=0.0, ws=None, ws_bytes=0,
+                       conjA=False, conjB=False, stream=None):
+    """Alg. 4 with explicit tuples (include/tk.h): C = alpha permute(permute(A,(pA,qA)) o permute(B,(pB,qB)),
+    (pAB,qAB)) + beta C."""
+    keep, tp, np_ = _tuples(pA, qA, pB, qB, pAB, qAB)
+    _check(_contract_tuples(A.h, _ptr(a), int(conjA), B.h, _ptr(b), int(conjB), C.h, _ptr(c), tp, np_, float(alpha),
+                            float(beta), _ptr(ws), ws_bytes, _stream(stream)))
 
 
 def tk_profile_enable(on=True):

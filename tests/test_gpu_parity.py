@@ -228,3 +228,101 @@ def test_permute_large_tiled_paths():
     assert _perm_case("U1", secs, [0, 0], [0, 0], [2, 0], [1, 3]) <= TOL   # B-operand pattern of cfg4
     assert _perm_case("U1", secs, [0, 0], [0, 0], [0, 2], [1, 3]) <= TOL   # A-operand pattern of cfg4
     assert _perm_case("U1", secs, [0, 1], [1], [2, 1, 0], []) <= TOL
+
+
+# ------------------------------------------------------------------ tk_contract_tuples (explicit Alg. 4)
+def _tuples_case(kind, A_sp, B_sp, tup, alpha=1.0, beta=0.0, seed=0, cplx=False, conjA=False):
+    from paper_2508_10076_b200 import tk
+    pA, qA, pB, qB, pAB, qAB = tup
+    la = OL.homspace_layout(kind, A_sp["cod"], A_sp["dom"])
+    lb = OL.homspace_layout(kind, B_sp["cod"], B_sp["dom"])
+    rng = np.random.default_rng(seed)
+    def draw(n):
+        x = rng.standard_normal(n)
+        return x + 1j * rng.standard_normal(n) if cplx else x
+    xa, xb = draw(la.nelems), draw(lb.nelems)
+    dt = tk.TK_C64 if cplx else tk.TK_F64
+    A, B = tk.tensor_from_spec(A_sp, dt), tk.tensor_from_spec(B_sp, dt)
+    C = tk.tk_contract_tuples_output(A, pA, qA, B, pB, qB, pAB, qAB)
+    Asp, Bsp = A_sp["cod"] + A_sp["dom"], B_sp["cod"] + B_sp["dom"]
+    cod, dom = OC.permuted_spaces([Asp[i] for i in pA], [Bsp[j] for j in qB], pAB, qAB)
+    lc = OL.homspace_layout(kind, cod, dom)
+    assert C.nelems == lc.nelems
+    y0 = draw(lc.nelems)
+    tdt = torch.complex128 if cplx else torch.float64
+    a, b = torch.from_numpy(xa).to(tdt).cuda(), torch.from_numpy(xb).to(tdt).cuda()
+    c = torch.from_numpy(y0.copy()).to(tdt).cuda() if beta != 0 else torch.full((lc.nelems,), float("nan"), dtype=tdt,
+                                                                                 device="cuda")
+    nws = tk.tk_contract_tuples_workspace(A, pA, qA, B, pB, qB, C, pAB, qAB)
+    ws = torch.empty(max(nws // 8 + 32, 1), dtype=torch.float64, device="cuda")
+    tk.tk_contract_tuples(A, a, pA, qA, B, b, pB, qB, C, c, pAB, qAB, alpha=alpha, beta=beta, ws=ws,
+                          ws_bytes=ws.numel() * 8, conjA=conjA)
+    torch.cuda.synchronize()
+    DA = OD.to_dense(la, xa)
+    if conjA:
+        DA = np.conj(DA)
+    D = OC.contract_alg4_tuples(DA, Asp, len(A_sp["cod"]), OD.to_dense(lb, xb), Bsp, len(B_sp["cod"]),
+                                pA, qA, pB, qB, pAB, qAB)
+    want = alpha * D + (beta * OD.to_dense(lc, y0) if beta != 0 else 0.0)
+    return OC.rel_frobenius(OD.to_dense(lc, c.cpu().numpy()), want), (A, a, B, b, C, c, ws)
+
+
+_FV = [((0, 0), 3), ((1, 1), 4), ((1, -1), 2), ((2, 0), 3), ((-1, 1), 2)]
+# A: V V V <- V (legs 0..3), B: V <- V V* (legs 0..2); ket/bra pairs A2-B1 and A3-B0, open A0, A1, B2
+_TUPLES = [([0, 1], [2, 3], [1, 0], [2], [2, 0], [1]),      # base (= reading C2 for A[1,2,3,4] B[4,3,5] -> C[5,1;2])
+           ([1, 0], [2, 3], [1, 0], [2], [2, 1], [0]),      # pA reversed (pAB compensates)
+           ([0, 1], [3, 2], [0, 1], [2], [2, 0], [1]),      # contracted legs in the other order
+           ([0, 1], [2, 3], [1, 0], [2], [0, 2], [1]),      # output permute crossing A1 and B2 (odd-odd signs)
+           ([1, 0], [3, 2], [0, 1], [2], [1, 2], [0]),      # the same output, both reorders
+           ]
+
+
+@pytest.mark.parametrize("kind", ["fU1xU1", "U1xU1"])
+def test_contract_tuples_vs_oracle(kind):
+    V = W.space(kind, _FV)
+    A_sp = {"cod": [V, V, V], "dom": [V]}
+    B_sp = {"cod": [V], "dom": [V, W.dual(V)]}
+    outs = []
+    for i, tup in enumerate(_TUPLES):
+        err, (_, _, _, _, C, c, _) = _tuples_case(kind, A_sp, B_sp, tup, seed=3)
+        assert err <= TOL, (i, err)
+        outs.append(c.cpu().numpy())
+    # reading C13: reordering pA (with pAB) or the contracted pairs leaves C unchanged (same layout here)
+    for o in outs[1:3]:
+        assert np.allclose(o, outs[0], rtol=1e-13, atol=1e-13)
+    assert np.allclose(outs[4], outs[3], rtol=1e-13, atol=1e-13)
+
+
+def test_contract_tuples_matches_labels_path():
+    """Tuples equal to reading C2's (labels A[1,2,3,4], B[4,3,5] -> C[5,1;2]) give tk_contract's result."""
+    from paper_2508_10076_b200 import tk
+    V = W.space("fU1xU1", _FV)
+    A_sp = {"cod": [V, V, V], "dom": [V]}
+    B_sp = {"cod": [V], "dom": [V, W.dual(V)]}
+    err, (A, a, B, b, C, c, ws) = _tuples_case("fU1xU1", A_sp, B_sp, _TUPLES[0], seed=4)
+    assert err <= TOL
+    c2 = torch.full_like(c, float("nan"))
+    labA, labB, labC = [1, 2, 3, 4], [4, 3, 5], [5, 1, 2]
+    C2 = tk.tk_contract_output(A, labA, B, labB, labC, 2)
+    assert C2.nelems == C.nelems
+    nws = tk.tk_contract_workspace(A, labA, B, labB, C2, labC)
+    ws2 = torch.empty(nws // 8 + 32, dtype=torch.float64, device="cuda")
+    tk.tk_contract(A, a, labA, B, b, labB, C2, c2, labC, ws=ws2, ws_bytes=ws2.numel() * 8)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+
+
+def test_contract_tuples_su2_complex():
+    V = W.space("SU2", [((0,), 3), ((1,), 2), ((2,), 2)])
+    A_sp = {"cod": [V, V], "dom": [V]}
+    B_sp = {"cod": [V], "dom": [V, V]}
+    # contract A1-B1 (V cod / V dom) and A2-B0 (V dom / V cod), contracted legs in B's order
+    tup = ([0], [2, 1], [0, 1], [2], [1], [0])
+    err, _ = _tuples_case("SU2", A_sp, B_sp, tup, seed=5, alpha=-0.5)
+    assert err <= TOL
+    err, _ = _tuples_case("SU2", A_sp, B_sp, tup, seed=6, cplx=True, conjA=True, beta=0.25)
+    assert err <= TOL
+    Vf = W.space("fU1xU1", _FV)
+    err, _ = _tuples_case("fU1xU1", {"cod": [Vf, Vf, Vf], "dom": [Vf]}, {"cod": [Vf], "dom": [Vf, W.dual(Vf)]},
+                          _TUPLES[1], seed=7, cplx=True, conjA=True)
+    assert err <= TOL

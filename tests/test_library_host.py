@@ -338,3 +338,30 @@ def test_anyon_trace_vs_planar_oracle(kind, secs):
             y, lc = OP.trace_planar(kind, cod, dom, x, pt, qt, p, q)
             ref = np.array([y[sc.offset] for sc in lc.subblocks])
             assert np.abs(got[i] - ref).max() < 1e-13
+
+
+def test_contract_tuples_output_and_errors():
+    """tk_contract_tuples_output (Alg. 4 with explicit tuples): C~ = (pA legs ; qB legs) permuted
+    by (pAB, qAB) -- the same HomSpace the oracle's selection rule gives; the reading-C2 tuples reproduce
+    tk_contract_output; malformed tuples fail before any work."""
+    V = W.space("fU1xU1", [((0, 0), 2), ((1, 1), 3), ((1, -1), 1)])
+    A_sp, B_sp = {"cod": [V, V, V], "dom": [V]}, {"cod": [V], "dom": [V, W.dual(V)]}
+    A, B = tk.tensor_from_spec(A_sp), tk.tensor_from_spec(B_sp)
+    Asp, Bsp = A_sp["cod"] + A_sp["dom"], B_sp["cod"] + B_sp["dom"]
+    for tup in (([0, 1], [2, 3], [1, 0], [2], [2, 0], [1]), ([1, 0], [3, 2], [0, 1], [2], [0], [2, 1])):
+        C = tk.tk_contract_tuples_output(A, *tup[:2], B, *tup[2:])
+        cod, dom = OC.permuted_spaces([Asp[i] for i in tup[0]], [Bsp[j] for j in tup[3]], tup[4], tup[5])
+        assert C.nelems == OL.homspace_layout("fU1xU1", cod, dom).nelems
+        assert C.info()["n_cod"] == len(tup[4])
+    # reading C2 tuples of A[1,2,3,4] B[4,3,5] -> C[5,1;2]
+    C1 = tk.tk_contract_tuples_output(A, [0, 1], [2, 3], B, [1, 0], [2], [2, 0], [1])
+    C2 = tk.tk_contract_output(A, [1, 2, 3, 4], B, [4, 3, 5], [5, 1, 2], 2)
+    assert np.array_equal(C1.blocks()[1], C2.blocks()[1]) and np.array_equal(C1.blocks()[2], C2.blocks()[2])
+    bad = [(([0, 0], [2, 3], [1, 0], [2], [2, 0], [1]), "TK_ERR_INVALID_PERMUTATION"),   # repeated leg
+           (([0, 1], [2, 3], [0], [1, 2], [0, 1], [2]), "TK_ERR_INVALID_PERMUTATION"),   # |qA| != |pB|
+           (([0, 1], [2, 3], [1, 0], [2], [2, 2], [1]), "TK_ERR_INVALID_PERMUTATION"),   # pAB not a permutation
+           (([0, 1], [2, 3], [2, 0], [1], [2, 0], [1]), "TK_ERR_SPACE_MISMATCH")]        # A2 (V) with B2 (V* dom)
+    for tup, status in bad:
+        with pytest.raises(tk.TKError) as e:
+            tk.tk_contract_tuples_output(A, *tup[:2], B, *tup[2:])
+        assert e.value.status == status, tup

@@ -436,3 +436,48 @@ def test_su2su2_fermion_permute_inverse():
         c2, d2 = C.permuted_spaces(cod, dom, p, q)
         l2 = L.homspace_layout("fSU2xSU2", c2, d2)
         assert C.rel_frobenius(Dn.to_dense(l2, Dn.from_dense(l2, Pd)), Pd) < 1e-13
+
+
+# ------------------------------------------------------------ Alg. 4 with explicit tuples
+def test_alg4_tuples_bosonic_equals_einsum():
+    """Dense Alg. 4 with arbitrary tuple orders reproduces the plain einsum (bosonic: the
+    permutes are basis relabelings, so every (pA, qA, pB, qB, pAB, qAB) gives the same C)."""
+    rng = np.random.default_rng(21)
+    V = sp("U1", [((-1,), 2), ((0,), 3), ((1,), 2)])
+    la, xa = rand_tensor("U1", [V, V], [V], 1)
+    lb, xb = rand_tensor("U1", [V], [V, V], 2)
+    A, B = Dn.to_dense(la, xa), Dn.to_dense(lb, xb)
+    want = C.contract_einsum(A, [1, 2, 3], B, [3, 2, 5], [5, 1])
+    for _ in range(6):
+        ka = [int(x) for x in rng.permutation([1, 2])]   # contracted A legs (labels 2, 3 at A legs 1, 2)
+        qA = ka
+        pB = [{1: 1, 2: 0}[i] for i in qA]                # label 2 is B leg 1, label 3 is B leg 0
+        got = C.contract_alg4_tuples(A, [V, V, V], 2, B, [V, V, V], 1, [0], qA, pB, [2], [1], [0])
+        assert C.rel_frobenius(got, want) < 1e-14
+
+
+def test_alg4_tuples_fermionic_reorder_invariance():
+    """Reading C13 makes the Koszul sign a group action (permute o inverse = id), so under Alg. 4:
+    (i) reordering A~'s codomain legs pA (with pAB compensating) leaves C unchanged, and (ii) reordering
+    the contracted legs jointly in qA and pB leaves C unchanged (paired legs carry equal parities, so
+    the two domain/codomain signs cancel)."""
+    V = sp("fU1xU1", [((0, 0), 1), ((1, 1), 2), ((1, -1), 1), ((-1, 1), 1), ((-1, -1), 1), ((2, 0), 1)])
+    la, xa = rand_tensor("fU1xU1", [V, V, V], [V], 7)      # A: V V V <- V, legs 0..3
+    lb, xb = rand_tensor("fU1xU1", [V], [V, W.dual(V)], 8)  # B: V <- V V*, legs 0..2
+    A, B = Dn.to_dense(la, xa), Dn.to_dense(lb, xb)
+    Asp, Bsp = [V, V, V, V], [V, V, W.dual(V)]
+    # ket/bra pairs: A leg 2 (codomain V) with B leg 1 (domain V), A leg 3 (domain V) with B leg 0 (codomain V)
+    base = C.contract_alg4_tuples(A, Asp, 3, B, Bsp, 1, [0, 1], [2, 3], [1, 0], [2], [2, 0], [1])
+    # (i) pA reversed; C~ legs are now (1, 0, B2), so pAB/qAB must name them accordingly
+    r1 = C.contract_alg4_tuples(A, Asp, 3, B, Bsp, 1, [1, 0], [2, 3], [1, 0], [2], [2, 1], [0])
+    assert np.allclose(r1, base, rtol=0, atol=1e-14)
+    # (ii) contracted legs in the other order on both sides
+    r2 = C.contract_alg4_tuples(A, Asp, 3, B, Bsp, 1, [0, 1], [3, 2], [0, 1], [2], [2, 0], [1])
+    assert np.allclose(r2, base, rtol=0, atol=1e-14)
+    # the same checks on an output permute that crosses A1 and B2 (C[1,5;2]): there the signs are not
+    # trivial -- dropping them (bosonic einsum) differs -- and the invariances still hold
+    cross = C.contract_alg4_tuples(A, Asp, 3, B, Bsp, 1, [0, 1], [2, 3], [1, 0], [2], [0, 2], [1])
+    bos = C.contract_einsum(A, [1, 2, 3, 4], B, [4, 3, 5], [1, 5, 2])
+    assert C.rel_frobenius(bos, cross) > 1e-3
+    r3 = C.contract_alg4_tuples(A, Asp, 3, B, Bsp, 1, [1, 0], [3, 2], [0, 1], [2], [1, 2], [0])
+    assert np.allclose(r3, cross, rtol=0, atol=1e-14)
