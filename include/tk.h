@@ -75,7 +75,9 @@ typedef struct tk_tensor tk_tensor;
 typedef struct CUstream_st* tk_stream; /* = cudaStream_t; NULL = legacy default stream */
 
 /* ------------------------------------------------------------------ spaces (host) */
-/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2" | "fU1xSU2" | "fSU2xSU2" | "Fib" | "Ising".
+/* kind: "Z2" | "fZ2" | "U1" | "U1xU1" | "fU1xU1" | "SU2" | "fU1xSU2" | "fSU2xSU2" | "Fib" | "Ising"
+ * (also the Deligne spellings "fZ2xU1xU1", "fZ2xU1xSU2", "fZ2xSU2xSU2" of the three fermionic products;
+ * blanks around 'x' are ignored by tk_space_parse, so "fZ2 x U1 x SU2[...]" parses).
  * labels: n_sectors x width int32,
  * degeneracies: n_sectors int64 > 0 (zero entries are dropped). Sectors may be given
  * in any order; they are stored ascending. Duplicate labels -> TK_ERR_INVALID_ARGUMENT. */

@@ -41,6 +41,11 @@ Kind parse_kind(const std::string& s) {
   if (s == "fSU2xSU2") return Kind::FSU2SU2;
   if (s == "Fib") return Kind::FIB;
   if (s == "Ising") return Kind::ISING;
+  // the Deligne-product spellings of the fermionic kinds (reading C14: parity = N mod 2,
+  // resp. 2 j_spin mod 2 -- the restricted products these kinds are)
+  if (s == "fZ2xU1xU1") return Kind::FU1U1;
+  if (s == "fZ2xU1xSU2") return Kind::FU1SU2;
+  if (s == "fZ2xSU2xSU2") return Kind::FSU2SU2;
   TK_THROW(TK_ERR_UNKNOWN_LABEL, "unknown sector kind '" + s + "'");
 }
 

@@ -365,3 +365,16 @@ def test_contract_tuples_output_and_errors():
         with pytest.raises(tk.TKError) as e:
             tk.tk_contract_tuples_output(A, *tup[:2], B, *tup[2:])
         assert e.value.status == status, tup
+
+
+def test_parse_deligne_spellings():
+    """The fermionic product kinds parse under their Deligne spellings (reading C14)."""
+    pairs = [("fZ2 x U1 x SU2[(0,0):1, (1,1/2):2]", "fU1xSU2[(0,0):1, (1,1/2):2]"),
+             ("fZ2xSU2xSU2[(0,0):1, (1/2,1/2):3]'", "fSU2xSU2[(0,0):1, (1/2,1/2):3]'"),
+             ("fZ2 x U1 x U1[(1,1):2, (0,0):1]", "fU1xU1[(1,1):2, (0,0):1]")]
+    for a, b in pairs:
+        sa, sb = tk.tk_space_parse(a), tk.tk_space_parse(b)
+        assert sa.info() == sb.info()
+        la, da = sa.sectors()
+        lb, db = sb.sectors()
+        assert np.array_equal(la, lb) and np.array_equal(da, db)
