@@ -27,8 +27,7 @@ struct FastDiv {  // unsigned 32-bit division by a runtime constant (round-up ma
   uint32_t d, m, s;
   __device__ __forceinline__ void init(uint32_t dd) {
     d = dd;
-    s = 0;
-    while ((1u << s) < d) ++s;
+    s = dd <= 1 ? 0u : 32u - (uint32_t)__clz(dd - 1);  // ceil(log2 d)
     m = (d <= 1) ? 0u : (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - d)) / d + 1);
   }
   __device__ __forceinline__ uint32_t div(uint32_t n) const {
@@ -403,83 +402,6 @@ __device__ void permute_tiled(const typename CIO<CM>::S* __restrict__ src, typen
   }
 }
 
-// Box jobs (mode 2): dst leg 0 is unit-stride on both sides; the source's next-fastest leg (leg 2,
-// source stride n0) and the destination's (leg 1, destination stride n0) differ, so rows of n0 elements
-// alone give short scattered runs (cfg4: median 144 bytes). A box n0 x c1 x c2 is loaded as c1 source
-// runs of n0*c2 contiguous elements into shared memory S[i1][i2*n0 + i0] (odd plane pitch P1), and
-// stored as c2 destination runs of n0*c1 contiguous elements. 8 loads per thread in flight.
-template <int CM>
-__device__ void permute_box(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
-                            const PermGroup& g, const PermJob& job, PermShared& sh, typename CIO<CM>::V* __restrict__ S,
-                            double alpha, double beta, double ims) {
-  using IO = CIO<CM>;
-  using V = typename IO::V;
-  const int tid = threadIdx.x;
-  const int n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
-  const int c1 = g.ct, c2 = g.R;
-  const int64_t sl = sh.mld[0], dl = sh.mld[kMaxGroupMembers];
-  const int64_t so = sh.moff[0], dof = sh.moff[kMaxGroupMembers];
-  const int64_t s1 = g.sa[1] + sl * g.sb[1], d2 = g.da[2] + dl * g.db[2];
-  const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
-  const double c = alpha * sh.coef[0];
-  FastDiv fn0;
-  fn0.init((uint32_t)n0);
-  pdl_wait();  // tensor data only after the preceding grid has completed (PDL)
-  for (int u = 0; u < job.count; ++u) {
-    int64_t b = job.first + u;
-    const int b1 = (int)(b % g.T0);
-    b /= g.T0;
-    const int b2 = (int)(b % g.Tt);
-    uint32_t rest = (uint32_t)(b / g.Tt);
-    int64_t sbase = so, dbase = dof;
-    for (int l = 3; l < g.ndim; ++l) {
-      const uint32_t e = (uint32_t)g.ext[l], q = rest / e, i = rest - q * e;
-      rest = q;
-      sbase += (int64_t)i * (g.sa[l] + sl * g.sb[l]);
-      dbase += (int64_t)i * (g.da[l] + dl * g.db[l]);
-    }
-    const int i1b = b1 * c1, i2b = b2 * c2;
-    const int m1 = min(c1, n1 - i1b), m2 = min(c2, n2 - i2b);
-    sbase += (int64_t)i1b * s1 + (int64_t)i2b * n0;   // leg 2: source stride n0
-    dbase += (int64_t)i1b * n0 + (int64_t)i2b * d2;   // leg 1: destination stride n0
-    const uint32_t Ls = (uint32_t)n0 * m2, Ld = (uint32_t)n0 * m1, tot = Ls * m1;
-    const uint32_t P1 = Ls | 1;  // plane pitch of S[i1][.]
-    FastDiv fs, fd;
-    fs.init(Ls);
-    fd.init(Ld);
-    // load phase: source runs (i1 major), contiguous over r = i2 * n0 + i0
-    constexpr int U = sizeof(V) == 16 ? 4 : 8;
-    for (uint32_t e0 = tid; e0 < tot; e0 += U * kPermThreads) {
-      V x[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint32_t e = e0 + k * kPermThreads;
-        if (e < tot) {
-          const uint32_t i1 = fs.div(e), r = e - i1 * Ls;
-          x[k] = IO::load(src, sbase + (int64_t)i1 * s1 + r, sd1);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint32_t e = e0 + k * kPermThreads;
-        if (e < tot) {
-          const uint32_t i1 = fs.div(e), r = e - i1 * Ls;
-          S[i1 * P1 + r] = x[k];
-        }
-      }
-    }
-    __syncthreads();
-    // store phase: destination runs (i2 major), contiguous over r' = i1 * n0 + i0
-    for (uint32_t e = tid; e < tot; e += kPermThreads) {
-      const uint32_t i2 = fd.div(e), rr = e - i2 * Ld;
-      const uint32_t i1 = fn0.div(rr), i0 = rr - i1 * (uint32_t)n0;
-      IO::store(dst, dbase + (int64_t)i2 * d2 + rr, dd1, dd2, Num<V>::scale(c, S[i1 * P1 + i2 * (uint32_t)n0 + i0]),
-                beta, ims);
-    }
-    __syncthreads();
-  }
-}
-
 __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMember* __restrict__ members,
                                                 const double* __restrict__ coefs, PermShared& sh) {
   const int tid = threadIdx.x;
@@ -827,10 +749,119 @@ __global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB) permute_kernel(Per
   load_job_header(g, op.members, op.coefs, sh);
   if (!ROWS_ONLY && job.type == kJobTiled)
     permute_tiled<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
-  else if (!ROWS_ONLY && job.type == kJobBox)
-    permute_box<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
   else
     permute_rows<CM, true>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
+}
+
+// Box jobs (mode 2, large permutes whose leg 0 stays unit-stride on both sides but whose next legs
+// differ: the cfg4 operand and output permutes). A box n0 x m1 x m2 is contiguous along (leg 0, leg 2)
+// in the source -- m1 runs of n0*m2 elements -- and along (leg 0, leg 1) in the destination -- m2 runs
+// of n0*m1 -- so staging it in shared memory turns ~144-byte rows into runs of several KB on both
+// sides. A job is `count` consecutive boxes of one group; box u+1 streams in with cp.async (no
+// registers held) while box u is written out from the other buffer, so loads stay in flight through
+// the store phase. S[i1 * P1 + i2 * n0 + i0], plane pitch P1 = n0*m2 | 1.
+constexpr int kBoxBuf = kBoxElems + 64;  // doubles per buffer (a box plus its odd-pitch padding)
+template <int CM>
+__global__ void __launch_bounds__(kPermThreads, 3) permute_box_kernel(PermOp op, const PermJob* __restrict__ jobs) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
+  extern __shared__ __align__(16) unsigned char box_dyn[];
+  constexpr int kBuf = kBoxBuf * 8 / (int)sizeof(V);
+  V* S0 = reinterpret_cast<V*>(box_dyn);
+  pdl_trigger();
+  const PermJob job = jobs[blockIdx.x];
+  const PermGroup& g = op.groups[job.group];
+  const PermMember ms = op.members[g.src_mem], md = op.members[g.dst_mem];
+  const auto* src = (const typename IO::S*)op.src;
+  auto* dst = (typename IO::D*)op.dst;
+  const double c = op.alpha * op.coefs[g.coef_off];
+  const int tid = threadIdx.x;
+  const int n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
+  const int c1 = g.ct, c2 = g.R, T0 = g.T0, Tt = g.Tt;
+  const int64_t s1 = g.sa[1] + ms.ld * g.sb[1], d2 = g.da[2] + md.ld * g.db[2];
+  struct Box {
+    int64_t sbase, dbase;
+    int m1, m2;
+  };
+  auto box = [&](int64_t bb) {  // box index of a group < 2^31 (host-checked): 32-bit decode
+    uint32_t b = (uint32_t)bb;
+    const int b1 = (int)(b % (uint32_t)T0);
+    b /= (uint32_t)T0;
+    const int b2 = (int)(b % (uint32_t)Tt);
+    uint32_t rest = b / (uint32_t)Tt;
+    Box x{ms.off, md.off, 0, 0};
+    for (int l = 3; l < g.ndim; ++l) {
+      const uint32_t e = (uint32_t)g.ext[l], q = rest / e, i = rest - q * e;
+      rest = q;
+      x.sbase += (int64_t)i * (g.sa[l] + ms.ld * g.sb[l]);
+      x.dbase += (int64_t)i * (g.da[l] + md.ld * g.db[l]);
+    }
+    const int i1b = b1 * c1, i2b = b2 * c2;
+    x.m1 = min(c1, n1 - i1b);
+    x.m2 = min(c2, n2 - i2b);
+    x.sbase += (int64_t)i1b * s1 + (int64_t)i2b * n0;  // leg 2: source stride n0
+    x.dbase += (int64_t)i1b * n0 + (int64_t)i2b * d2;  // leg 1: destination stride n0
+    return x;
+  };
+  auto fetch = [&](const Box& x, V* S) {  // source runs: i1 major, contiguous over r = i2 * n0 + i0
+    const uint32_t Ls = (uint32_t)n0 * x.m2, tot = Ls * x.m1, P1 = Ls | 1;
+    FastDiv fs;
+    fs.init(Ls);
+    uint32_t i1 = fs.div((uint32_t)tid), r = tid - i1 * Ls;
+    const uint32_t qs = kPermThreads / Ls, rs_ = kPermThreads - qs * Ls;
+    for (uint32_t e = tid; e < tot; e += kPermThreads) {
+      stage_elem<CM>(S + i1 * P1 + r, src + x.sbase + (int64_t)i1 * s1 + r, ms.d1);
+      r += rs_;
+      i1 += qs;
+      if (r >= Ls) {
+        r -= Ls;
+        ++i1;
+      }
+    }
+  };
+  pdl_wait();  // tensor data only after the preceding grid has completed (PDL)
+  Box cur = box(job.first);
+  fetch(cur, S0);
+  cp_async_commit();
+  for (int u = 0; u < job.count; ++u) {
+    Box nxt{};
+    if (u + 1 < job.count) {
+      nxt = box(job.first + u + 1);
+      fetch(nxt, S0 + ((u + 1) & 1) * kBuf);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();  // box u landed for all threads
+    const V* S = S0 + (u & 1) * kBuf;
+    // destination runs: i2 major, contiguous over rr = i1 * n0 + i0; per-thread (i2, i1, i0) walked
+    // incrementally (stride kPermThreads), no division per element
+    const uint32_t Ls = (uint32_t)n0 * cur.m2, Ld = (uint32_t)n0 * cur.m1, tot = Ld * cur.m2, P1 = Ls | 1;
+    FastDiv fd, f0;
+    fd.init(Ld);
+    f0.init((uint32_t)n0);
+    uint32_t i2 = fd.div((uint32_t)tid), rr = tid - i2 * Ld;
+    uint32_t i1 = f0.div(rr), i0 = rr - i1 * (uint32_t)n0;
+    const uint32_t q2 = kPermThreads / Ld, r2 = kPermThreads - q2 * Ld;
+    const uint32_t q0 = r2 / (uint32_t)n0, r0 = r2 - q0 * (uint32_t)n0;
+    for (uint32_t e = tid; e < tot; e += kPermThreads) {
+      IO::store(dst, cur.dbase + (int64_t)i2 * d2 + i1 * (uint32_t)n0 + i0, md.d1, md.d2,
+                Num<V>::scale(c, S[i1 * P1 + i2 * (uint32_t)n0 + i0]), op.beta, op.ims);
+      // advance rr by r2 (carrying into i2), i.e. (i1, i0) by (q0, r0) within the run
+      i2 += q2;
+      i0 += r0;
+      i1 += q0;
+      if (i0 >= (uint32_t)n0) {
+        i0 -= n0;
+        ++i1;
+      }
+      if (i1 >= (uint32_t)cur.m1) {
+        i1 -= cur.m1;
+        ++i2;
+      }
+    }
+    __syncthreads();  // buffer u & 1 is refilled by iteration u + 1's prefetch
+    cur = nxt;
+  }
 }
 
 // rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight)
@@ -876,6 +907,15 @@ static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int n
   if (variant == kLaunchSegOnly && !persist) variant = kLaunchGeneral;
   if (njobs && variant == kLaunchSegOnly)
     launch_k(permute_seg_kernel<CM>, seg_grid<CM>(njobs), kPermThreads, 0, st, op0, op1, jobs, njobs);
+  if (njobs && variant == kLaunchBox) {
+    constexpr int smem = 2 * kBoxBuf * 8;
+    static bool battr = false;
+    if (!battr) {
+      cudaFuncSetAttribute(permute_box_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      battr = true;
+    }
+    launch_k(permute_box_kernel<CM>, njobs, kPermThreads, smem, st, op0, jobs);
+  }
   if (njobs && variant == kLaunchGeneral) launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
   if (njobs_multi) launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, 0, st, op0, op1, jobs + njobs);
 }

@@ -99,7 +99,7 @@ static void leg_strides(const std::vector<int64_t>& ext, int n1, std::vector<int
 }
 
 static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_ext, int src_n1,
-                                  const std::vector<int>& src_leg, int dst_n1) {
+                                  const std::vector<int>& src_leg, int dst_n1, int elem_bytes) {
   int N = (int)src_leg.size();
   std::vector<int64_t> sa, sb, da, db, dext(N);
   leg_strides(src_ext, src_n1, sa, sb);
@@ -179,7 +179,8 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
       g = h;
       g.mode = 2;
       const int64_t n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
-      const int64_t budget = std::max<int64_t>(1, (kBoxElems - 64) / n0);  // + odd plane padding
+      // a box fills one shared-memory buffer of kBoxElems doubles (+ odd plane padding)
+      const int64_t budget = std::max<int64_t>(1, (kBoxElems * 8 / elem_bytes - 64) / n0);
       int64_t c2 = std::min<int64_t>(n2, std::max<int64_t>(1, (int64_t)std::sqrt((double)budget)));
       int64_t c1 = std::min<int64_t>(n1, std::max<int64_t>(1, budget / c2));
       c2 = std::min<int64_t>(n2, std::max<int64_t>(1, budget / c1));
@@ -267,7 +268,7 @@ struct SegBuilder {
     // always destination leg 0)
     static const bool dst_leg = getenv("TK_SEG_DSTLEG") != nullptr;
     int L = 0;
-    if (g.mode != 0 && !dst_leg)
+    if (g.mode == 1 && !dst_leg)
       for (int l = 1; l < g.ndim; ++l)
         if (std::make_pair(g.sb[l], g.sa[l]) < std::make_pair(g.sb[L], g.sa[L])) L = l;
     const int64_t n0 = g.ext[L], nrows = g.nelem / n0;
@@ -342,7 +343,7 @@ static void make_jobs(PermPlan& P) {
   SegBuilder sb(P, segs, std::max<int64_t>(256, std::min<int64_t>(kPackElems, total / seg_div)));
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
-    if (seg && g.ksrc == 1 && g.kdst == 1 && g.mode != 2) {
+    if (seg && g.ksrc == 1 && g.kdst == 1) {
       sb.add(gi);
       continue;
     }
@@ -361,8 +362,10 @@ static void make_jobs(PermPlan& P) {
       continue;
     }
     if (g.mode == 2) {
+      // several boxes per job: the box kernel streams box u+1 in while box u is written out
       const int64_t nbox = (int64_t)g.T0 * g.Tt * g.nrest;
-      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4096, job_elems / ((int64_t)g.c0 * g.ct * g.R)));
+      if (nbox >= INT32_MAX) TK_THROW(TK_ERR_UNSUPPORTED, "a group with >= 2^31 boxes");
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4096, 4 * job_elems / ((int64_t)g.c0 * g.ct * g.R)));
       for (int64_t r = 0; r < nbox; r += per)
         boxes.push_back(PermJob{gi, (int16_t)std::min(per, nbox - r), kJobBox, 0, r});
       continue;
@@ -384,15 +387,17 @@ static void make_jobs(PermPlan& P) {
   // small permutes: one launch for rows, tiled and packed jobs (+ one for recoupling jobs); large ones
   // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
   sb.finish();
-  tiles.insert(tiles.end(), boxes.begin(), boxes.end());  // box jobs run beside the tiled ones
   rows.insert(rows.begin(), segs.begin(), segs.end());    // seg jobs lead the non-rows-only launch
-  P.njobs = (int)(tiles.size() + rows.size() + packed.size());
+  P.njobs = (int)(tiles.size() + rows.size() + packed.size() + boxes.size());
   P.njobs_rows = (int)(rows.size() - segs.size());
+  P.njobs_box = (int)boxes.size();
   P.njobs_multi = (int)multi.size();
   P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
   P.rows_only = tiles.empty() && packed.empty() && segs.empty();
   P.seg_only = rows.size() == segs.size() && tiles.empty() && packed.empty();
-  P.split = total >= (int64_t(1) << 24) && !P.rows_only && !rows.empty();
+  // large permutes (>= 2^24 elements) launch one kernel per job class: rows-only, box, the rest
+  P.split = total >= (int64_t(1) << 24);
+  if (!P.split && !boxes.empty()) TK_THROW(TK_ERR_CUDA, "internal: box jobs in a small permute");
   static const bool dbg = getenv("TK_PLAN_DEBUG") != nullptr;
   if (dbg) {
     int64_t er = 0, et = 0, ep = 0, em = 0, gr = 0, gt = 0, gp = 0;
@@ -416,6 +421,7 @@ static void make_jobs(PermPlan& P) {
             (long long)ep, multi.size(), (long long)em);
   }
   P.jobs = rows;
+  P.jobs.insert(P.jobs.end(), boxes.begin(), boxes.end());
   P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
   P.jobs.insert(P.jobs.end(), packed.begin(), packed.end());
   P.jobs.insert(P.jobs.end(), multi.begin(), multi.end());
@@ -503,7 +509,7 @@ void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vect
       P.members.push_back(sub_member(A, spl, i));
       g.dst_mem = (int)P.members.size();
       P.members.push_back(sub_member(C, dpl, j));
-      finish_group_geometry(g, ext, n1, src_leg, C.n_cod());
+      finish_group_geometry(g, ext, n1, src_leg, C.n_cod(), elem_bytes);
       P.groups.push_back(g);
     }
   } else {
@@ -578,7 +584,7 @@ void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vect
       const Tree& f0 = A.f_tree(srcs[0]);
       std::vector<int64_t> ext(s0.dims);
       ext.insert(ext.end(), f0.dims.begin(), f0.dims.end());
-      finish_group_geometry(g, ext, n1, src_leg, C.n_cod());
+      finish_group_geometry(g, ext, n1, src_leg, C.n_cod(), elem_bytes);
       P.groups.push_back(g);
     }
   }
@@ -818,7 +824,7 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   P.pb.identity = ib_id;
   P.pc.identity = ic_id;
   static const bool no_merge = getenv("TK_NO_MERGE") != nullptr;
-  if (!no_merge && !P.cplx && !ia_id && !ib_id && A.nelems + B.nelems < (int64_t(1) << 26)) {
+  if (!no_merge && !P.cplx && !ia_id && !ib_id && !P.pa.split && !P.pb.split) {
     P.merged_ab = true;
     auto take = [&](const PermPlan& pp, int8_t op, bool multi) {
       int b = multi ? pp.njobs : 0, e = multi ? pp.njobs + pp.njobs_multi : pp.njobs;
@@ -1085,11 +1091,16 @@ void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double b
   if (P.jobs.empty()) return;
   const PermJob* jobs = (const PermJob*)P.d_jobs.p;
   if (P.split) {
-    check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, kLaunchRowsOnly, cm, st), "permute launch");
-    check_cuda(launch_permute(op, op, jobs + P.njobs_rows, P.njobs - P.njobs_rows, P.njobs_multi, P.tiled,
+    const int nrest = P.njobs - P.njobs_rows - P.njobs_box;
+    if (P.njobs_rows)
+      check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, kLaunchRowsOnly, cm, st), "permute launch");
+    if (P.njobs_box)
+      check_cuda(launch_permute(op, op, jobs + P.njobs_rows, P.njobs_box, 0, false, kLaunchBox, cm, st),
+                 "permute launch");
+    check_cuda(launch_permute(op, op, jobs + P.njobs_rows + P.njobs_box, nrest, P.njobs_multi, P.tiled,
                               kLaunchGeneral, cm, st),
                "permute launch");
-    g_launches += 1 + (P.njobs > P.njobs_rows) + (P.njobs_multi > 0);
+    g_launches += (P.njobs_rows > 0) + (P.njobs_box > 0) + (nrest > 0) + (P.njobs_multi > 0);
   } else {
     const int variant = P.seg_only ? kLaunchSegOnly : P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
     check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, variant, cm, st), "permute launch");
