@@ -1393,6 +1393,121 @@ __global__ void __launch_bounds__(kSkinnyThreads)
   }
 }
 
+// ---- gathered skinny GEMM (GatherSeg in tk_kernels.hpp): one thread per row of A~^c. The tile's
+// subblock descriptors are staged in shared memory before griddepcontrol.wait (plan data); each thread
+// then issues its row's K element loads from A with cp.async into As[k][thread] (all in flight at
+// once, no registers held), waits for its own copies only, and computes its C~ row against the
+// K x N block of B~ in shared memory.
+template <int KM, int NM>
+__global__ void __launch_bounds__(kGatherRows, 3)
+    gather_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                         const GatherTile* __restrict__ tiles, const GatherSeg* __restrict__ segs,
+                         const int32_t* __restrict__ btab, double alpha, double beta) {
+  constexpr int RPT = gather_rows(KM) / kGatherRows;  // rows per thread
+  __shared__ double Bs[kSkinnyMax * kSkinnyMax];
+  __shared__ double As[KM][gather_rows(KM)];
+  __shared__ __align__(16) GatherSeg ss[gather_seg_cap(KM)];
+  pdl_trigger();
+  const GatherTile t = tiles[blockIdx.x];
+  const GemmGroup& g = t.g;
+  const int tid = threadIdx.x;
+  {
+    const int4* src4 = reinterpret_cast<const int4*>(segs + t.seg0);
+    int4* dst4 = reinterpret_cast<int4*>(ss);
+    for (int i = tid; i < t.nseg * (int)(sizeof(GatherSeg) / 16); i += kGatherRows) dst4[i] = __ldg(src4 + i);
+  }
+  const int K = g.K, N = g.N;
+  const int be = tid < K * N ? __ldg(btab + t.bt + tid) : -1;  // plan data: before the wait
+  for (int i = tid; i < kSkinnyMax * kSkinnyMax; i += kGatherRows) Bs[i] = 0.0;
+  __syncthreads();
+  pdl_wait();
+  // A~ rows first (cp.async, nothing held in registers), then the B~ block, then one wait for both
+  uint32_t neg[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    neg[j] = 0;
+    const int lr = tid + j * kGatherRows;
+    if (lr >= t.nrows) continue;
+    const int m = t.m0 + lr;
+    // this row's row tree: the last segment with r0 <= m (segments sorted by (r0, k0)); its column
+    // subblocks are the run of segments sharing that r0
+    int lo = 0, hi = t.nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ss[mid].r0 <= m) lo = mid; else hi = mid - 1;
+    }
+    const int r0 = ss[lo].r0;
+    while (lo > 0 && ss[lo - 1].r0 == r0) --lo;
+    for (int s = lo; s < t.nseg && ss[s].r0 == r0; ++s) {
+      const GatherSeg& q = ss[s];
+      uint32_t r = (uint32_t)(m - q.r0);
+      int rs = 0;
+      for (int l = 0; l < q.nrl; ++l) {
+        const uint32_t e = (uint32_t)q.ext[l], qq = r / e;
+        rs += (int)(r - qq * e) * q.str[l];
+        r = qq;
+      }
+      const double* a = A + q.src + rs;
+      for (int kk = 0; kk < q.nk; ++kk) cp_async8(&As[q.k0 + kk][lr], a + q.colsrc[kk], true);
+      if (q.neg) neg[j] |= ((1u << q.nk) - 1u) << q.k0;
+    }
+  }
+  cp_async_commit();
+  if (be >= 0) {
+    const double x = alpha * __ldg(B + (be >> 1));
+    Bs[(tid / N) * kSkinnyMax + tid % N] = (be & 1) ? -x : x;
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // Bs (and, formally, every thread's own As columns) visible
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = tid + j * kGatherRows;
+    if (lr >= t.nrows) break;
+    double acc[NM];
+#pragma unroll
+    for (int n = 0; n < NM; ++n) acc[n] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      if (k < K) {
+        const double x = As[k][lr];
+        const double a = (neg[j] >> k) & 1u ? -x : x;
+#pragma unroll
+        for (int n = 0; n < NM; ++n) acc[n] = fma(a, Bs[k * kSkinnyMax + n], acc[n]);
+      }
+    }
+    double* Cg = C + g.c_off + t.m0 + lr;
+#pragma unroll
+    for (int n = 0; n < NM; ++n)
+      if (n < N) {
+        double* cp = Cg + (int64_t)n * g.ldc;
+        *cp = beta != 0.0 ? fma(beta, *cp, acc[n]) : acc[n];
+      }
+  }
+}
+
+cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const GatherTile* tiles, int ntiles,
+                               const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
+                               double beta, cudaStream_t st) {
+  if (!ntiles) return cudaSuccess;
+  const int kc = kmax <= 4 ? 0 : (kmax <= 8 ? 1 : 2), nc = nmax <= 4 ? 0 : (nmax <= 8 ? 1 : 2);
+#define TK_GATHER(KM, NM)                                                                                   \
+  launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, 0, st, A, B, C, tiles, segs, btab, alpha, beta); \
+  break;
+  switch (kc * 3 + nc) {
+    case 0: TK_GATHER(4, 4)
+    case 1: TK_GATHER(4, 8)
+    case 2: TK_GATHER(4, 16)
+    case 3: TK_GATHER(8, 4)
+    case 4: TK_GATHER(8, 8)
+    case 5: TK_GATHER(8, 16)
+    case 6: TK_GATHER(16, 4)
+    case 7: TK_GATHER(16, 8)
+    default: TK_GATHER(16, 16)
+  }
+#undef TK_GATHER
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, int ntiles_skinny, const GemmTile* split_heads,
                         int nsplit_heads, double* parts, double alpha, double beta, cudaStream_t st) {

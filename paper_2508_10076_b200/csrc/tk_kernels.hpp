@@ -144,6 +144,37 @@ cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* 
 // tile table layout: [big (128x128 DMMA) | small (64x64 DMMA) | skinny (streaming, GemmTile.pad = rows)]
 constexpr int kSkinnyMax = 16;   // skinny groups: 0 < K <= 16 and N <= 16
 constexpr int kSkinnyRows = 2048;
+
+// Gathered skinny GEMM (abelian kinds, every GEMM block with K, N <= kSkinnyMax): C~^c = A~^c B~^c
+// with the rows of A~^c read straight from A -- the operand permute A -> A~ is not a separate pass.
+// A GatherSeg is one A~ subblock: rows [r0, r0 + nrows) x columns [k0, k0 + nk) of its block; element
+// (r0 + i, k0 + kk) is A[src + sum_l digit_l(i) * str[l] + colsrc[kk]] (digits of i over the row legs,
+// fastest first) times the coefficient (neg: -1, the fermionic sign of reading C13).
+constexpr int kGatherRows = 256;   // rows per tile (one per thread)
+constexpr int kGatherSegs = 128;   // subblocks per tile (64 when K > 8: shared memory)
+__host__ __device__ constexpr int gather_seg_cap(int kmax) { return kmax > 8 ? 64 : kmax > 4 ? 96 : kGatherSegs; }
+// rows per tile by K class: 2 rows per thread while the A~ staging (K x rows doubles) stays <= 16 KB... 32 KB
+__host__ __device__ constexpr int gather_rows(int kmax) { return kmax > 8 ? kGatherRows : 2 * kGatherRows; }
+struct GatherSeg {
+  int32_t r0, nrows, k0, nk;
+  int64_t src;
+  int32_t nrl, neg;
+  int32_t ext[4];
+  int32_t str[4];
+  int32_t colsrc[kSkinnyMax];
+};
+static_assert(sizeof(GatherSeg) == 128, "GatherSeg layout");
+struct GatherTile {
+  int32_t m0, nrows;   // rows [m0, m0 + nrows) of the group's block
+  int32_t seg0, nseg;  // its subblocks (row trees of those rows, every column tree), sorted by (r0, k0)
+  int32_t bt, pad;     // the group's K x N gather table for B~ (btab[bt + k * N + n]: 2 * offset into B
+                       // + (coefficient < 0), or -1 for a structural zero): B needs no permute pass either
+  GemmGroup g;
+};
+cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const GatherTile* tiles, int ntiles,
+                               const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
+                               double beta, cudaStream_t st);
+
 // split-K (small tiles of under-filled launches): partial 64x64 tiles in `parts`, then one reduction
 // CTA per head tile (deterministic order)
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,

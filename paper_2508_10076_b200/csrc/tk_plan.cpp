@@ -636,6 +636,13 @@ struct ContractPlan {
   int njobs_ab = 0, njobs_ab_multi = 0;
   bool ab_tiled = false, ab_seg_only = false;
   DevBuf d_ggroups, d_tiles, d_jobs_ab;
+  // gathered skinny GEMM (build_gather): the A~ permute folded into the GEMM's loads
+  bool gather = false;
+  std::vector<GatherSeg> gsegs;
+  std::vector<GatherTile> gtiles;
+  std::vector<int32_t> btab;
+  int g_kmax = 0, g_nmax = 0;
+  DevBuf d_gsegs, d_gtiles, d_btab;
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
   bool uploaded = false;
@@ -653,6 +660,9 @@ struct ContractPlan {
     d_tiles.upload(tiles);
     d_heads.upload(split_heads);
     d_jobs_ab.upload(jobs_ab);
+    d_gsegs.upload(gsegs);
+    d_gtiles.upload(gtiles);
+    d_btab.upload(btab);
     uploaded = true;
   }
 };
@@ -795,6 +805,194 @@ Tensor* permuted_tensor(const Tensor& A, const std::vector<int>& p, const std::v
 }
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Gathered skinny GEMM (GatherSeg, tk_kernels.hpp). Applies when every GEMM block with K > 0 is skinny
+// (K, N <= kSkinnyMax: the MPO steps T.W of the DMRG chains), the kind is abelian (single-member permute
+// groups, coefficient +-1), Float64, and A~ is a genuine permute of A: then the A -> A~ pass (read A,
+// write A~, read A~ again in the GEMM) becomes the GEMM's own gather from A. TK_NO_GATHER=1 disables.
+static void build_gather(const Tensor& A, ContractPlan& P) {
+  static const bool off = getenv("TK_NO_GATHER") != nullptr;
+  if (off || P.cplx || P.pa.identity || P.ntiles_skinny == 0 || A.nelems >= INT32_MAX) return;
+  for (const GemmGroup& g : P.ggroups)
+    if (g.K > 0 && (g.K > kSkinnyMax || g.N > kSkinnyMax)) return;
+  for (const PermGroup& g : P.pa.groups)
+    if (g.ksrc != 1 || g.kdst != 1) return;
+  // A~ subblocks per block of the padded layout, from the permute plan's destination members
+  const PadLayout& la = P.la;
+  const int nblk = (int)la.off.size();
+  std::vector<std::vector<GatherSeg>> per(nblk);
+  for (const PermGroup& g : P.pa.groups) {
+    const PermMember ms = P.pa.members[g.src_mem], md = P.pa.members[g.dst_mem];
+    const int b = (int)(std::upper_bound(la.off.begin(), la.off.end(), md.off) - la.off.begin()) - 1;
+    const int64_t rel = md.off - la.off[b];
+    GatherSeg q{};
+    q.r0 = (int32_t)(rel % la.ld[b]);
+    q.k0 = (int32_t)(rel / la.ld[b]);
+    q.src = ms.off;
+    const double c = P.pa.coefs[g.coef_off];
+    if (c != 1.0 && c != -1.0) return;  // only signs in flight
+    q.neg = c < 0;
+    int64_t nr = 1, nc = 1;
+    std::vector<std::pair<int64_t, int64_t>> cl;  // column legs (ext, source stride), fastest first
+    for (int l = 0; l < g.ndim; ++l) {
+      const int64_t str = g.sa[l] + ms.ld * g.sb[l];
+      if (g.db[l] == 0) {  // a row leg of A~ (destination rows)
+        if (q.nrl == 4) return;
+        q.ext[q.nrl] = g.ext[l];
+        q.str[q.nrl] = (int32_t)str;
+        ++q.nrl;
+        nr *= g.ext[l];
+      } else {
+        cl.push_back({g.ext[l], str});
+        nc *= g.ext[l];
+      }
+    }
+    if (nc > kSkinnyMax) return;
+    q.nrows = (int32_t)nr;
+    q.nk = (int32_t)nc;
+    for (int64_t kk = 0; kk < nc; ++kk) {
+      int64_t r = kk, o = 0;
+      for (auto& e : cl) {
+        o += (r % e.first) * e.second;
+        r /= e.first;
+      }
+      q.colsrc[kk] = (int32_t)o;
+    }
+    per[b].push_back(q);
+  }
+  // GEMM group of each A~ block (same coupled sector), coverage check, tiles of whole row trees
+  std::map<Sector, int> a_blk;
+  for (int i = 0; i < (int)P.At->blocks.size(); ++i) a_blk[P.At->blocks[i].coupled] = i;
+  std::vector<GatherSeg> segs;
+  std::vector<GatherTile> tiles;
+  int kmax = 0, nmax = 0;
+  for (const GemmGroup& g : P.ggroups)
+    if (g.K > 0) kmax = std::max(kmax, (int)g.K), nmax = std::max(nmax, (int)g.N);
+  // the kernel instance is chosen by the launch's K class (4 / 8 / 16), which fixes its segment capacity
+  const int kcls = kmax <= 4 ? 4 : kmax <= 8 ? 8 : 16;
+  // 2 rows per thread only when that still leaves >= 2 tiles per resident CTA slot (148 SMs x 4):
+  // measured cfg3 (1.95 M rows) 63 -> 47 us per T.W step, while cfg2 (0.2 M rows) prefers 256
+  int64_t rows_total = 0;
+  for (const GemmGroup& g : P.ggroups)
+    if (g.K > 0) rows_total += g.M;
+  const int cap = gather_seg_cap(kcls);
+  const int tile_rows = rows_total >= (int64_t)gather_rows(kcls) * 2 * 148 * 4 ? gather_rows(kcls) : kGatherRows;
+  for (int ci = 0; ci < (int)P.Ct->blocks.size(); ++ci) {
+    const GemmGroup& gg = P.ggroups[ci];
+    if (gg.K == 0) continue;
+    auto ia = a_blk.find(P.Ct->blocks[ci].coupled);
+    if (ia == a_blk.end()) return;
+    std::vector<GatherSeg>& v = per[ia->second];
+    std::sort(v.begin(), v.end(), [](const GatherSeg& x, const GatherSeg& y) {
+      return x.r0 != y.r0 ? x.r0 < y.r0 : x.k0 < y.k0;
+    });
+    int64_t cover = 0;
+    for (const GatherSeg& q : v) cover += (int64_t)q.nrows * q.nk;
+    if (cover != (int64_t)gg.M * gg.K) return;  // every A~ element from exactly one subblock
+    // row trees = runs of segments with equal r0 (they partition the block's rows); tiles are dense
+    // kGatherRows-row ranges, each carrying the segments of every row tree it overlaps (a row tree cut
+    // by a tile boundary has its segments copied into both tiles); fewer rows if that exceeds kGatherSegs
+    std::vector<size_t> run;  // start index of each row tree in v
+    for (size_t i = 0; i < v.size(); ++i)
+      if (i == 0 || v[i].r0 != v[i - 1].r0) run.push_back(i);
+    run.push_back(v.size());
+    size_t rt = 0;  // first row tree overlapping the current tile
+    for (int m0 = 0; m0 < gg.M;) {
+      while (v[run[rt]].r0 + v[run[rt]].nrows <= m0) ++rt;
+      int end = std::min(gg.M, m0 + tile_rows);
+      size_t last = rt, nseg = 0;
+      while (last < run.size() - 1 && v[run[last]].r0 < end) {
+        const size_t cnt = run[last + 1] - run[last];
+        if (nseg + cnt > (size_t)cap) {
+          if (last == rt) return;  // one row tree with too many column subblocks
+          end = v[run[last]].r0;   // stop before this row tree
+          break;
+        }
+        nseg += cnt;
+        ++last;
+      }
+      GatherTile t{};
+      t.g = gg;
+      t.m0 = m0;
+      t.nrows = end - m0;
+      t.seg0 = (int32_t)segs.size();
+      for (size_t x = run[rt]; x < run[last]; ++x) segs.push_back(v[x]);
+      t.nseg = (int32_t)(segs.size() - t.seg0);
+      tiles.push_back(t);
+      m0 = end;
+    }
+  }
+  // B~ gather tables (GatherTile::bt): entry (k, n) of each group's K x N block of B~
+  std::vector<int32_t> btab;
+  std::vector<int> bt_of(P.ggroups.size(), -1);
+  for (size_t ci = 0; ci < P.ggroups.size(); ++ci) {
+    const GemmGroup& gg = P.ggroups[ci];
+    if (gg.K == 0) continue;
+    bt_of[ci] = (int)btab.size();
+    btab.resize(btab.size() + (size_t)gg.K * gg.N, -1);
+    if (P.pb.identity)  // B~ is B itself (canonical layout)
+      for (int k = 0; k < gg.K; ++k)
+        for (int n = 0; n < gg.N; ++n) {
+          const int64_t o = gg.b_off + k + (int64_t)n * gg.ldb;
+          if (o >= (int64_t(1) << 30)) return;
+          btab[bt_of[ci] + k * gg.N + n] = (int32_t)(2 * o);
+        }
+  }
+  if (!P.pb.identity) {
+    std::map<Sector, int> c_of;  // coupled sector -> GEMM group
+    for (int ci = 0; ci < (int)P.Ct->blocks.size(); ++ci) c_of[P.Ct->blocks[ci].coupled] = ci;
+    const PadLayout& lb = P.lb;
+    for (const PermGroup& g : P.pb.groups) {
+      if (g.ksrc != 1 || g.kdst != 1) return;
+      const double c = P.pb.coefs[g.coef_off];
+      if (c != 1.0 && c != -1.0) return;
+      const PermMember ms = P.pb.members[g.src_mem], md = P.pb.members[g.dst_mem];
+      for (int64_t e = 0; e < g.nelem; ++e) {
+        int64_t r = e, so = ms.off, dof = md.off;
+        for (int l = 0; l < g.ndim; ++l) {
+          const int64_t i = r % g.ext[l];
+          r /= g.ext[l];
+          so += i * (g.sa[l] + ms.ld * g.sb[l]);
+          dof += i * (g.da[l] + md.ld * g.db[l]);
+        }
+        const int b = (int)(std::upper_bound(lb.off.begin(), lb.off.end(), dof) - lb.off.begin()) - 1;
+        const int64_t rel = dof - lb.off[b];
+        const int k = (int)(rel % lb.ld[b]), n = (int)(rel / lb.ld[b]);
+        auto it = c_of.find(P.Bt->blocks[b].coupled);
+        if (it == c_of.end() || bt_of[it->second] < 0 || so >= (int64_t(1) << 30)) return;
+        const GemmGroup& gg = P.ggroups[it->second];
+        if (k >= gg.K || n >= gg.N) return;
+        btab[bt_of[it->second] + k * gg.N + n] = (int32_t)(2 * so + (c < 0));
+      }
+    }
+  }
+  // tiles -> their group's table (tiles were built group by group in GEMM-group order)
+  {
+    size_t ti = 0;
+    for (size_t ci = 0; ci < P.ggroups.size(); ++ci) {
+      const GemmGroup& gg = P.ggroups[ci];
+      if (gg.K == 0) continue;
+      for (int m0 = 0; ti < tiles.size() && m0 < gg.M; ++ti) {
+        tiles[ti].bt = bt_of[ci];
+        m0 = tiles[ti].m0 + tiles[ti].nrows;
+      }
+    }
+    if (ti != tiles.size()) return;
+  }
+  P.gather = true;
+  P.btab = std::move(btab);
+  P.gsegs = std::move(segs);
+  P.gtiles = std::move(tiles);
+  P.g_kmax = kmax;
+  P.g_nmax = nmax;
+  // the skinny tiles are replaced; the A~ permute and its workspace are not used
+  P.tiles.resize(P.ntiles_big + P.ntiles_small);
+  P.ntiles_skinny = 0;
+  P.merged_ab = false;
+  if (getenv("TK_PLAN_DEBUG"))
+    fprintf(stderr, "[tk gather] %zu tiles, %zu subblocks, K <= %d, N <= %d\n", P.gtiles.size(), P.gsegs.size(), kmax,
+            nmax);
+}
 
 static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& C, const Tuples& t, ContractPlan& P) {
   if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
@@ -973,6 +1171,7 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   P.tiles.insert(P.tiles.end(), skinny.begin(), skinny.end());
   for (GemmTile& t : P.tiles) t.g = P.ggroups[t.group];
   for (GemmTile& t : P.split_heads) t.g = P.ggroups[t.group];
+  build_gather(A, P);
 }
 
 // ------------------------------------------------------------------ plan cache
@@ -1226,7 +1425,9 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
   g_launches = 0;
   prof_record(0, st);
   const bool cx = P->cplx;
-  if (P->merged_ab) {
+  if (P->gather) {  // A~ and B~ are gathered inside the GEMM: no permute pass
+    prof_record(1, st);
+  } else if (P->merged_ab) {
     PermOp oa = perm_op(P->pa, a, (double*)At, 1.0, 0.0, 1.0), ob = perm_op(P->pb, b, (double*)Bt, 1.0, 0.0, 1.0);
     check_cuda(launch_permute(oa, ob, (const PermJob*)P->d_jobs_ab.p, P->njobs_ab, P->njobs_ab_multi, P->ab_tiled,
                               P->ab_seg_only ? kLaunchSegOnly : kLaunchGeneral, kPermReal, st),
@@ -1235,8 +1436,8 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
   } else if (!P->pa.identity) {
     run_permute(P->pa, a, (double*)At, 1.0, 0.0, cx ? kPermCToPlanar : kPermReal, conjA ? -1.0 : 1.0, st);
   }
-  prof_record(1, st);
-  if (!P->merged_ab && !P->pb.identity)
+  if (!P->gather) prof_record(1, st);
+  if (!P->gather && !P->merged_ab && !P->pb.identity)
     run_permute(P->pb, b, (double*)Bt, 1.0, 0.0, cx ? kPermCToRealRep : kPermReal, conjB ? -1.0 : 1.0, st);
   prof_record(2, st);
   double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
@@ -1246,6 +1447,13 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
                            (int)P->split_heads.size(), (double*)(w + P->off_parts), ga, gb, st),
                "gemm launch");
     g_launches += (P->ntiles_big > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0) + !P->split_heads.empty();
+  }
+  if (P->gather) {
+    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const GatherTile*)P->d_gtiles.p,
+                                  (int)P->gtiles.size(), (const GatherSeg*)P->d_gsegs.p, (const int32_t*)P->d_btab.p,
+                                  P->g_kmax, P->g_nmax, ga, gb, st),
+               "gather gemm launch");
+    g_launches += !P->gtiles.empty();
   }
   prof_record(3, st);
   if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);

@@ -166,3 +166,25 @@ def _perm_case_spaces(kind, cod, dom, p, q, seed=0):
     tk.tk_permute(A, torch.from_numpy(x).cuda(), p, q, C, c)
     torch.cuda.synchronize()
     return OC.rel_frobenius(OD.to_dense(ls, c.cpu().numpy()), ref)
+
+
+# ------------------------------------------------------------------ gathered skinny GEMM
+# The T.W steps of the DMRG chains (every GEMM block K, N <= 16, abelian) run as one gathered GEMM:
+# A~ and B~ are read straight from A and B with the permutes' offsets and signs (tk_kernels.hpp,
+# GatherSeg). Cases: fermionic signs, alpha / beta accumulation, and an output permute after it.
+@pytest.mark.parametrize("cfgfun,kind", [(lambda: W.cfg3(chi=96), "fU1xU1"), (lambda: W.cfg2(chi=128), "U1")])
+def test_gather_gemm_alpha_beta_and_output_permute(cfgfun, kind):
+    cfg = cfgfun()
+    specs = {k: v[0] for k, v in cfg["tensors"].items()}
+    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][0]
+    cod, dom = OC.output_spaces(specs[na]["cod"], specs[na]["dom"], specs[nb]["cod"], specs[nb]["dom"],
+                                la, lb, lc, ncod)
+    T1 = {"cod": cod, "dom": dom}
+    (_, la2, nb2, lb2, _, lc2, ncod2) = cfg["steps"][1]
+    for alpha, beta in ((1.0, 0.0), (-0.5, 0.75)):
+        got, want, lc_ = _run(kind, T1, la2, specs[nb2], lb2, lc2, ncod2, alpha=alpha, beta=beta, seed=11)
+        _check(got, want)
+    # a non-identity output permute after the gathered GEMM (C~ -> C with alpha / beta)
+    lc3 = [lc2[2], lc2[0], lc2[4], lc2[1], lc2[3]]
+    got, want, _ = _run(kind, T1, la2, specs[nb2], lb2, lc3, 2, alpha=2.0, beta=-1.0, seed=12)
+    _check(got, want)
