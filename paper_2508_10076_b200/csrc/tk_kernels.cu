@@ -864,19 +864,119 @@ __global__ void __launch_bounds__(kPermThreads, 3) permute_box_kernel(PermOp op,
   }
 }
 
-// rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight)
+// rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight). The job's source
+// elements of all k_src members are staged in shared memory with cp.async -- one round trip for the
+// whole job instead of a chain of dependent loads per element (the sum over sources used to wait on
+// each load in turn) -- then y_j = alpha sum_i M[i][j] x_i is formed from shared memory and stored.
+// Jobs larger than the stage are walked in chunks.
 template <int CM>
-__global__ void __launch_bounds__(kPermThreads, 2)
+__global__ void __launch_bounds__(kPermThreads, 3)
     permute_recouple_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
   using IO = CIO<CM>;
+  using V = typename IO::V;
   __shared__ PermShared sh;
+  extern __shared__ __align__(16) unsigned char rc_dyn[];
+  V* Xs = reinterpret_cast<V*>(rc_dyn);
+  constexpr int kStage = kRecoupleStage * 8 / (int)sizeof(V);
   pdl_trigger();
   const PermJob job = jobs[blockIdx.x];
   const PermOp& op = job.op ? op1 : op0;
   const PermGroup& g = op.groups[job.group];
   load_job_header(g, op.members, op.coefs, sh);
-  permute_rows<CM, false>((const typename IO::S*)op.src, (typename IO::D*)op.dst, g, job, sh, op.alpha, op.beta,
-                          op.ims);
+  const auto* src = (const typename IO::S*)op.src;
+  auto* dst = (typename IO::D*)op.dst;
+  const int tid = threadIdx.x;
+  const int cnt = job.count, ks = g.ksrc, kd = g.kdst;
+  // row tables (offsets of every row start relative to the member bases, legs 1..)
+  for (int r = tid; r < cnt; r += kPermThreads) {
+    uint32_t R = (uint32_t)(job.first + r);
+    int64_t sa = 0, sb = 0, da = 0, db = 0;
+#pragma unroll 1
+    for (int l = 1; l < g.ndim; ++l) {
+      const uint32_t e = (uint32_t)g.ext[l], q = R / e;
+      const int64_t i = R - q * e;
+      R = q;
+      sa += i * g.sa[l];
+      sb += i * g.sb[l];
+      da += i * g.da[l];
+      db += i * g.db[l];
+    }
+    sh.rsa[r] = sa;
+    sh.rsb[r] = sb;
+    sh.rda[r] = da;
+    sh.rdb[r] = db;
+  }
+  __syncthreads();
+  pdl_wait();
+  const int n0 = g.ext[0];
+  const uint32_t E = (uint32_t)cnt * (uint32_t)n0;
+  const uint32_t chunk = (uint32_t)(kStage / ks);
+  FastDiv fn0;
+  fn0.init((uint32_t)n0);
+  if (ks <= 4) {  // few sources: their loads are all in flight at once from registers, no stage needed
+    for (uint32_t e = tid; e < E; e += kPermThreads) {
+      const uint32_t r = fn0.div(e), i0 = e - r * (uint32_t)n0;
+      V x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < ks) {
+          const int64_t ld = sh.mld[i];
+          x[i] = IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]),
+                          sh.md1[i]);
+        }
+      for (int j = 0; j < kd; ++j) {
+        V acc = Num<V>::zero();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < ks) acc = Num<V>::axpy(sh.coef[i * kd + j], x[i], acc);
+        const int jm = kMaxGroupMembers + j;
+        const int64_t ld = sh.mld[jm];
+        IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]), sh.md1[jm],
+                  sh.md2[jm], Num<V>::scale(op.alpha, acc), op.beta, op.ims);
+      }
+    }
+    return;
+  }
+  for (uint32_t e0 = 0; e0 < E; e0 += chunk) {
+    const uint32_t ec = min(chunk, E - e0);
+    FastDiv fc;
+    fc.init(ec);
+    // stage: Xs[i * ec + e] = source member i, element e0 + e
+    for (uint32_t idx = tid; idx < (uint32_t)ks * ec; idx += kPermThreads) {
+      const uint32_t i = fc.div(idx), e = e0 + (idx - i * ec);
+      const uint32_t r = fn0.div(e), i0 = e - r * (uint32_t)n0;
+      const int64_t ld = sh.mld[i];
+      stage_elem<CM>(Xs + idx, src + sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]),
+                     sh.md1[i]);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    for (uint32_t e = tid; e < ec; e += kPermThreads) {
+      const uint32_t ee = e0 + e, r = fn0.div(ee), i0 = ee - r * (uint32_t)n0;
+      for (int j0 = 0; j0 < kd; j0 += kRegMembers) {
+        V acc[kRegMembers];
+#pragma unroll
+        for (int jj = 0; jj < kRegMembers; ++jj) acc[jj] = Num<V>::zero();
+        for (int i = 0; i < ks; ++i) {
+          const V x = Xs[i * ec + e];
+          const double* cr = sh.coef + i * kd + j0;
+#pragma unroll
+          for (int jj = 0; jj < kRegMembers; ++jj)
+            if (j0 + jj < kd) acc[jj] = Num<V>::axpy(cr[jj], x, acc[jj]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < kRegMembers; ++jj)
+          if (j0 + jj < kd) {
+            const int jm = kMaxGroupMembers + j0 + jj;
+            const int64_t ld = sh.mld[jm];
+            IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]),
+                      sh.md1[jm], sh.md2[jm], Num<V>::scale(op.alpha, acc[jj]), op.beta, op.ims);
+          }
+      }
+    }
+    __syncthreads();  // the stage is refilled by the next chunk
+  }
 }
 
 template <int CM>
@@ -917,7 +1017,15 @@ static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int n
     launch_k(permute_box_kernel<CM>, njobs, kPermThreads, smem, st, op0, jobs);
   }
   if (njobs && variant == kLaunchGeneral) launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
-  if (njobs_multi) launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, 0, st, op0, op1, jobs + njobs);
+  if (njobs_multi) {
+    constexpr int rsmem = kRecoupleStage * 8;
+    static bool rattr = false;
+    if (!rattr) {
+      cudaFuncSetAttribute(permute_recouple_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
+      rattr = true;
+    }
+    launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, rsmem, st, op0, op1, jobs + njobs);
+  }
 }
 
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,

@@ -372,8 +372,10 @@ static void make_jobs(PermPlan& P) {
     }
     if (g.mode == 0) {
       int64_t nrows = g.nelem / g.ext[0];
-      int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, job_elems / std::max(1, g.ext[0])));
       const bool single = g.ksrc == 1 && g.kdst == 1;
+      // recoupling jobs: the job's k_src source rows must fit the kernel's shared-memory stage
+      const int64_t budget = single ? job_elems : std::min<int64_t>(job_elems, kRecoupleStage * 8 / P.elem_bytes / g.ksrc);
+      int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, budget / std::max(1, g.ext[0])));
       auto& dst = single ? rows : multi;
       for (int64_t r = 0; r < nrows; r += per)
         dst.push_back(PermJob{gi, (int16_t)std::min(per, nrows - r), (int8_t)(single ? kJobRows : kJobMulti), 0, r});
@@ -474,6 +476,7 @@ void build_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vect
   P.n_src = A.nelems;
   P.n_dst = C.nelems;
   P.bytes = (double)(A.nelems + C.nelems) * elem_bytes;
+  P.elem_bytes = elem_bytes;
   std::vector<bool> isdual;
   for (auto* s : A.cod) isdual.push_back(s->dual);
   for (auto* s : A.dom) isdual.push_back(s->dual);

@@ -38,6 +38,7 @@ struct PermPlan {
   bool tiled = false, rows_only = false, seg_only = false;
   bool split = false;  // large permute: rows jobs in their own (leaner) launch
   DevBuf d_groups, d_members, d_coefs, d_jobs, d_blob;
+  int elem_bytes = 8;  // 8 Float64, 16 ComplexF64
   double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
   int64_t n_src = 0, n_dst = 0;
   bool uploaded = false;
