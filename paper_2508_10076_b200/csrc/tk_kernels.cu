@@ -27,7 +27,8 @@ struct FastDiv {  // unsigned 32-bit division by a runtime constant (round-up ma
   uint32_t d, m, s;
   __device__ __forceinline__ void init(uint32_t dd) {
     d = dd;
-    s = dd <= 1 ? 0u : 32u - (uint32_t)__clz(dd - 1);  // ceil(log2 d)
+    s = 0;
+    while ((1u << s) < d) ++s;
     m = (d <= 1) ? 0u : (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - d)) / d + 1);
   }
   __device__ __forceinline__ uint32_t div(uint32_t n) const {
