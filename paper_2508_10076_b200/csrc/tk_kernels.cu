@@ -117,7 +117,10 @@ struct PermShared {
   int64_t md1[2 * kMaxGroupMembers], md2[2 * kMaxGroupMembers];
 };
 
-template <int CM, bool SINGLE>
+// single-member rows job: destination leg 0 is also unit-stride in the source; the row starts of the
+// job are decoded once into shared memory, then the job's elements are walked as one flat range with
+// TK_ROWS_U loads in flight per thread
+template <int CM>
 __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
                              const PermGroup& g, const PermJob& job, PermShared& sh, double alpha, double beta,
                              double ims) {
@@ -125,7 +128,6 @@ __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typena
   using V = typename IO::V;
   const int tid = threadIdx.x;
   const int cnt = job.count;
-  const int ks = g.ksrc, kd = g.kdst;
   const int64_t sl = sh.mld[0], dl = sh.mld[kMaxGroupMembers];
   for (int r = tid; r < cnt; r += kPermThreads) {
     uint32_t R = (uint32_t)(job.first + r);  // group element counts are < 2^31 (host-checked)
@@ -143,82 +145,39 @@ __device__ void permute_rows(const typename CIO<CM>::S* __restrict__ src, typena
         db += i * g.db[l];
       }
     }
-    if (SINGLE) {  // final element offsets of the row start
-      sh.rsa[r] = sh.moff[0] + sa + sl * sb;
-      sh.rda[r] = sh.moff[kMaxGroupMembers] + da + dl * db;
-    } else {
-      sh.rsa[r] = sa;
-      sh.rsb[r] = sb;
-      sh.rda[r] = da;
-      sh.rdb[r] = db;
-    }
+    sh.rsa[r] = sh.moff[0] + sa + sl * sb;  // final element offsets of the row start
+    sh.rda[r] = sh.moff[kMaxGroupMembers] + da + dl * db;
   }
   __syncthreads();
   pdl_wait();
   const int n0 = g.ext[0];
-  if constexpr (SINGLE) {
-    const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
-    const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
-    const double c = alpha * sh.coef[0];
-    // independent loads in flight per thread (64 bytes: bytes in flight hide DRAM latency)
-    constexpr int U = sizeof(V) == 16 ? TK_ROWS_U / 2 : TK_ROWS_U;
-    FastDiv fd;
-    fd.init((uint32_t)n0);
-    const uint32_t total = (uint32_t)cnt * (uint32_t)n0;
-    for (uint32_t e0 = tid; e0 < total; e0 += U * kPermThreads) {
-      V x[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        uint32_t e = e0 + u * kPermThreads;
-        if (e < total) {
-          uint32_t r = fd.div(e);
-          uint32_t i0 = e - r * (uint32_t)n0;
-          x[u] = IO::load(src, sh.rsa[r] + (int64_t)i0 * s0, sd1);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        uint32_t e = e0 + u * kPermThreads;
-        if (e < total) {
-          uint32_t r = fd.div(e);
-          uint32_t i0 = e - r * (uint32_t)n0;
-          IO::store(dst, sh.rda[r] + (int64_t)i0 * d0, dd1, dd2, Num<V>::scale(c, x[u]), beta, ims);
-        }
-      }
-    }
-    return;
-  }
-  // recoupling groups (k_src, k_dst > 1): y_j = alpha * sum_i M[i][j] x_i (+ beta y_j)
+  const int64_t s0 = g.sa[0] + sl * g.sb[0], d0 = g.da[0] + dl * g.db[0];
+  const int64_t sd1 = sh.md1[0], dd1 = sh.md1[kMaxGroupMembers], dd2 = sh.md2[kMaxGroupMembers];
+  const double c = alpha * sh.coef[0];
+  // independent loads in flight per thread (64 bytes: bytes in flight hide DRAM latency)
+  constexpr int U = sizeof(V) == 16 ? TK_ROWS_U / 2 : TK_ROWS_U;
   FastDiv fd;
   fd.init((uint32_t)n0);
   const uint32_t total = (uint32_t)cnt * (uint32_t)n0;
-  // destinations in chunks of kRegMembers accumulators; every source element is read once per chunk
-  // (once in total for groups of <= 8 destinations, e.g. all of cfg5; re-reads hit L1 otherwise)
-  for (uint32_t e = tid; e < total; e += kPermThreads) {
-    uint32_t r = fd.div(e);
-    uint32_t i0 = e - r * (uint32_t)n0;
-    for (int j0 = 0; j0 < kd; j0 += kRegMembers) {
-      V acc[kRegMembers];
+  for (uint32_t e0 = tid; e0 < total; e0 += U * kPermThreads) {
+    V x[U];
 #pragma unroll
-      for (int jj = 0; jj < kRegMembers; ++jj) acc[jj] = Num<V>::zero();
-#pragma unroll 4
-      for (int i = 0; i < ks; ++i) {
-        const int64_t ld = sh.mld[i];
-        const V x =
-            IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]), sh.md1[i]);
-        const double* cr = sh.coef + i * kd + j0;
-#pragma unroll
-        for (int jj = 0; jj < kRegMembers; ++jj)
-          if (j0 + jj < kd) acc[jj] = Num<V>::axpy(cr[jj], x, acc[jj]);
+    for (int u = 0; u < U; ++u) {
+      uint32_t e = e0 + u * kPermThreads;
+      if (e < total) {
+        uint32_t r = fd.div(e);
+        uint32_t i0 = e - r * (uint32_t)n0;
+        x[u] = IO::load(src, sh.rsa[r] + (int64_t)i0 * s0, sd1);
       }
+    }
 #pragma unroll
-      for (int jj = 0; jj < kRegMembers; ++jj)
-        if (j0 + jj < kd) {
-          const int jm = kMaxGroupMembers + j0 + jj;
-          const int64_t ld = sh.mld[jm];
-          IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]),
-                    sh.md1[jm], sh.md2[jm], Num<V>::scale(alpha, acc[jj]), beta, ims);
-        }
+    for (int u = 0; u < U; ++u) {
+      uint32_t e = e0 + u * kPermThreads;
+      if (e < total) {
+        uint32_t r = fd.div(e);
+        uint32_t i0 = e - r * (uint32_t)n0;
+        IO::store(dst, sh.rda[r] + (int64_t)i0 * d0, dd1, dd2, Num<V>::scale(c, x[u]), beta, ims);
+      }
     }
   }
 }
@@ -668,51 +627,6 @@ __device__ void permute_seg(const typename CIO<CM>::S* __restrict__ src, typenam
   seg_body<CM>(src, dst, sm, alpha, beta, ims);
 }
 
-__device__ __forceinline__ void seg_fetch(int64_t* buf, const int64_t* __restrict__ blob, const PermJob& job) {
-  const int n2 = job.group >> 1;
-  const int64_t* g = blob + job.first;
-  for (int i = threadIdx.x; i < n2; i += kPermThreads) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + 2 * i);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g + 2 * i));
-  }
-}
-
-// Launches made only of seg jobs: persistent CTAs (grid = resident capacity) walk the jobs with a
-// static stride; the next job's blob is fetched with cp.async into the second buffer while the current
-// job moves data, so the only exposed plan-data latency is the first job's.
-template <int CM>
-__global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB)
-    permute_seg_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs, int njobs) {
-  using IO = CIO<CM>;
-  __shared__ __align__(16) int64_t buf[2][kSegWords];
-  pdl_trigger();
-  const int G = gridDim.x;
-  int j = blockIdx.x;
-  PermJob cur = jobs[j], nxt{};
-  bool has_nxt = j + G < njobs;
-  if (has_nxt) nxt = jobs[j + G];
-  seg_fetch(buf[0], (cur.op ? op1 : op0).blob, cur);
-  cp_async_commit();
-  for (int it = 0;; ++it) {
-    const bool has_nn = j + 2 * G < njobs;
-    PermJob nn{};
-    if (has_nn) nn = jobs[j + 2 * G];
-    if (has_nxt) seg_fetch(buf[(it + 1) & 1], (nxt.op ? op1 : op0).blob, nxt);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (it == 0) pdl_wait();
-    const PermOp& op = cur.op ? op1 : op0;
-    seg_body<CM>((const typename IO::S*)op.src, (typename IO::D*)op.dst, buf[it & 1], op.alpha, op.beta, op.ims);
-    if (!has_nxt) break;
-    __syncthreads();  // buf[it & 1] is refilled by the next iteration's prefetch
-    j += G;
-    cur = nxt;
-    nxt = nn;
-    has_nxt = has_nn;
-  }
-}
-
 // One launch covers every abelian-style job of up to two permutes (A~ and B~ of a contraction, op 0/1):
 // rows, smem-tiled and packed jobs share the grid, so small latency-bound permutes do not serialise
 // over several launches. <= 64 registers so that 4 CTAs (32 warps) share an SM.
@@ -751,7 +665,7 @@ __global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB) permute_kernel(Per
   if (!ROWS_ONLY && job.type == kJobTiled)
     permute_tiled<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
   else
-    permute_rows<CM, true>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
+    permute_rows<CM>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
 }
 
 // Box jobs (mode 2, large permutes whose leg 0 stays unit-stride on both sides but whose next legs
@@ -981,19 +895,6 @@ __global__ void __launch_bounds__(kPermThreads, 3)
 }
 
 template <int CM>
-static int seg_grid(int njobs) {
-  static int cap = 0;
-  if (!cap) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, permute_seg_kernel<CM>, kPermThreads, 0);
-    cap = std::max(1, sms * std::max(1, per));
-  }
-  return std::min(njobs, cap);
-}
-
-template <int CM>
 static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int njobs, int njobs_multi, bool tiled,
                               int variant, cudaStream_t st) {
   const int smem = tiled ? kTileElems * (int)sizeof(typename CIO<CM>::V) : 0;
@@ -1004,10 +905,6 @@ static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int n
     attr = true;
   }
   if (njobs && variant == kLaunchRowsOnly) launch_k(permute_kernel<CM, true>, njobs, kPermThreads, 0, st, op0, op1, jobs);
-  static const bool persist = getenv("TK_SEG_PERSIST") != nullptr;
-  if (variant == kLaunchSegOnly && !persist) variant = kLaunchGeneral;
-  if (njobs && variant == kLaunchSegOnly)
-    launch_k(permute_seg_kernel<CM>, seg_grid<CM>(njobs), kPermThreads, 0, st, op0, op1, jobs, njobs);
   if (njobs && variant == kLaunchBox) {
     constexpr int smem = 2 * kBoxBuf * 8;
     static bool battr = false;

@@ -137,9 +137,8 @@ struct GemmTile {
 // job table layout: [rows / tiled / packed jobs (njobs, one launch) | recoupling jobs (njobs_multi)];
 // `tiled`: some job is smem-tiled (dynamic shared memory needed). Modes 2 and 3 require beta == 0.
 // variant: kLaunchRowsOnly -- every job of the first launch is a rows job (leaner kernel instance);
-// kLaunchSegOnly -- every job is a kJobSeg job (persistent kernel with blob prefetch);
 // kLaunchBox -- every job is a box job (mode 2, double-buffered shared-memory box kernel)
-enum PermLaunch : int { kLaunchGeneral = 0, kLaunchRowsOnly = 1, kLaunchSegOnly = 2, kLaunchBox = 3 };
+enum PermLaunch : int { kLaunchGeneral = 0, kLaunchRowsOnly = 1, kLaunchBox = 3 };
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
                            bool tiled, int variant, int cm, cudaStream_t st);
 // tile table layout: [big (128x128 DMMA) | small (64x64 DMMA) | skinny (streaming, GemmTile.pad = rows)]

@@ -396,7 +396,6 @@ static void make_jobs(PermPlan& P) {
   P.njobs_multi = (int)multi.size();
   P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
   P.rows_only = tiles.empty() && packed.empty() && segs.empty();
-  P.seg_only = rows.size() == segs.size() && tiles.empty() && packed.empty();
   // large permutes (>= 2^24 elements) launch one kernel per job class: rows-only, box, the rest
   P.split = total >= (int64_t(1) << 24);
   if (!P.split && !boxes.empty()) TK_THROW(TK_ERR_CUDA, "internal: box jobs in a small permute");
@@ -637,7 +636,7 @@ struct ContractPlan {
   bool merged_ab = false;
   std::vector<PermJob> jobs_ab;
   int njobs_ab = 0, njobs_ab_multi = 0;
-  bool ab_tiled = false, ab_seg_only = false;
+  bool ab_tiled = false;
   DevBuf d_ggroups, d_tiles, d_jobs_ab;
   // gathered skinny GEMM (build_gather): the A~ permute folded into the GEMM's loads
   bool gather = false;
@@ -1042,7 +1041,6 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
     P.njobs_ab = P.pa.njobs + P.pb.njobs;
     P.njobs_ab_multi = P.pa.njobs_multi + P.pb.njobs_multi;
     P.ab_tiled = P.pa.tiled || P.pb.tiled;
-    P.ab_seg_only = P.pa.seg_only && P.pb.seg_only;
   }
   // workspace: A~ | B~ | C~ (skipped when the permute is the identity)
   size_t off = 0;
@@ -1304,7 +1302,7 @@ void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double b
                "permute launch");
     g_launches += (P.njobs_rows > 0) + (P.njobs_box > 0) + (nrest > 0) + (P.njobs_multi > 0);
   } else {
-    const int variant = P.seg_only ? kLaunchSegOnly : P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
+    const int variant = P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
     check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, variant, cm, st), "permute launch");
     g_launches += (P.njobs > 0) + (P.njobs_multi > 0);
   }
@@ -1433,7 +1431,7 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
   } else if (P->merged_ab) {
     PermOp oa = perm_op(P->pa, a, (double*)At, 1.0, 0.0, 1.0), ob = perm_op(P->pb, b, (double*)Bt, 1.0, 0.0, 1.0);
     check_cuda(launch_permute(oa, ob, (const PermJob*)P->d_jobs_ab.p, P->njobs_ab, P->njobs_ab_multi, P->ab_tiled,
-                              P->ab_seg_only ? kLaunchSegOnly : kLaunchGeneral, kPermReal, st),
+                              kLaunchGeneral, kPermReal, st),
                "permute launch");
     g_launches += (P->njobs_ab > 0) + (P->njobs_ab_multi > 0);
   } else if (!P->pa.identity) {

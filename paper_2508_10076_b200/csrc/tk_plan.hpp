@@ -35,7 +35,7 @@ struct PermPlan {
   std::vector<PermJob> jobs;
   std::vector<int64_t> blob;  // kJobSeg job blobs (SegHeader | SegGroup[ng] | rs | rd per job)
   int njobs = 0, njobs_multi = 0, njobs_rows = 0, njobs_box = 0;  // jobs = [rows | box | seg/tiled/packed | recoupling]
-  bool tiled = false, rows_only = false, seg_only = false;
+  bool tiled = false, rows_only = false;
   bool split = false;  // large permute: rows jobs in their own (leaner) launch
   DevBuf d_groups, d_members, d_coefs, d_jobs, d_blob;
   int elem_bytes = 8;  // 8 Float64, 16 ComplexF64
