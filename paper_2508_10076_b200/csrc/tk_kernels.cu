@@ -627,6 +627,64 @@ __device__ void permute_seg(const typename CIO<CM>::S* __restrict__ src, typenam
   seg_body<CM>(src, dst, sm, alpha, beta, ims);
 }
 
+// recoupling jobs: offsets of every row start relative to the member bases (legs 1..), in smem
+__device__ __forceinline__ void recouple_row_tables(const PermGroup& g, const PermJob& job, PermShared& sh) {
+  for (int r = threadIdx.x; r < job.count; r += kPermThreads) {
+    uint32_t R = (uint32_t)(job.first + r);
+    int64_t sa = 0, sb = 0, da = 0, db = 0;
+#pragma unroll 1
+    for (int l = 1; l < g.ndim; ++l) {
+      const uint32_t e = (uint32_t)g.ext[l], q = R / e;
+      const int64_t i = R - q * e;
+      R = q;
+      sa += i * g.sa[l];
+      sb += i * g.sb[l];
+      da += i * g.da[l];
+      db += i * g.db[l];
+    }
+    sh.rsa[r] = sa;
+    sh.rsb[r] = sb;
+    sh.rda[r] = da;
+    sh.rdb[r] = db;
+  }
+  __syncthreads();
+}
+
+// recoupling groups of <= kRecoupleDirect sources: all of an element's source loads are in flight at
+// once from registers, then y_j = alpha sum_i M[i][j] x_i for every destination j
+template <int CM>
+__device__ void recouple_direct(const typename CIO<CM>::S* __restrict__ src, typename CIO<CM>::D* __restrict__ dst,
+                                const PermGroup& g, const PermJob& job, const PermShared& sh, double alpha,
+                                double beta, double ims) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
+  const int ks = g.ksrc, kd = g.kdst, n0 = g.ext[0];
+  const uint32_t E = (uint32_t)job.count * (uint32_t)n0;
+  FastDiv fn0;
+  fn0.init((uint32_t)n0);
+  for (uint32_t e = threadIdx.x; e < E; e += kPermThreads) {
+    const uint32_t r = fn0.div(e), i0 = e - r * (uint32_t)n0;
+    V x[kRecoupleDirect];
+#pragma unroll
+    for (int i = 0; i < kRecoupleDirect; ++i)
+      if (i < ks) {
+        const int64_t ld = sh.mld[i];
+        x[i] = IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]),
+                        sh.md1[i]);
+      }
+    for (int j = 0; j < kd; ++j) {
+      V acc = Num<V>::zero();
+#pragma unroll
+      for (int i = 0; i < kRecoupleDirect; ++i)
+        if (i < ks) acc = Num<V>::axpy(sh.coef[i * kd + j], x[i], acc);
+      const int jm = kMaxGroupMembers + j;
+      const int64_t ld = sh.mld[jm];
+      IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]), sh.md1[jm],
+                sh.md2[jm], Num<V>::scale(alpha, acc), beta, ims);
+    }
+  }
+}
+
 // One launch covers every abelian-style job of up to two permutes (A~ and B~ of a contraction, op 0/1):
 // rows, smem-tiled and packed jobs share the grid, so small latency-bound permutes do not serialise
 // over several launches. <= 64 registers so that 4 CTAs (32 warps) share an SM.
@@ -662,6 +720,14 @@ __global__ void __launch_bounds__(kPermThreads, TK_PERM_MINB) permute_kernel(Per
   }
   const PermGroup& g = op.groups[job.group];
   load_job_header(g, op.members, op.coefs, sh);
+  if constexpr (!ROWS_ONLY) {
+    if (job.type == kJobMulti) {  // a recoupling group of <= kRecoupleDirect sources (host-routed)
+      recouple_row_tables(g, job, sh);
+      pdl_wait();
+      recouple_direct<CM>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
+      return;
+    }
+  }
   if (!ROWS_ONLY && job.type == kJobTiled)
     permute_tiled<CM>(src, dst, g, job, sh, reinterpret_cast<typename IO::V*>(perm_dyn), op.alpha, op.beta, op.ims);
   else
@@ -802,56 +868,17 @@ __global__ void __launch_bounds__(kPermThreads, 3)
   auto* dst = (typename IO::D*)op.dst;
   const int tid = threadIdx.x;
   const int cnt = job.count, ks = g.ksrc, kd = g.kdst;
-  // row tables (offsets of every row start relative to the member bases, legs 1..)
-  for (int r = tid; r < cnt; r += kPermThreads) {
-    uint32_t R = (uint32_t)(job.first + r);
-    int64_t sa = 0, sb = 0, da = 0, db = 0;
-#pragma unroll 1
-    for (int l = 1; l < g.ndim; ++l) {
-      const uint32_t e = (uint32_t)g.ext[l], q = R / e;
-      const int64_t i = R - q * e;
-      R = q;
-      sa += i * g.sa[l];
-      sb += i * g.sb[l];
-      da += i * g.da[l];
-      db += i * g.db[l];
-    }
-    sh.rsa[r] = sa;
-    sh.rsb[r] = sb;
-    sh.rda[r] = da;
-    sh.rdb[r] = db;
-  }
-  __syncthreads();
+  recouple_row_tables(g, job, sh);
   pdl_wait();
+  if (ks <= kRecoupleDirect) {
+    recouple_direct<CM>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
+    return;
+  }
   const int n0 = g.ext[0];
   const uint32_t E = (uint32_t)cnt * (uint32_t)n0;
   const uint32_t chunk = (uint32_t)(kStage / ks);
   FastDiv fn0;
   fn0.init((uint32_t)n0);
-  if (ks <= 4) {  // few sources: their loads are all in flight at once from registers, no stage needed
-    for (uint32_t e = tid; e < E; e += kPermThreads) {
-      const uint32_t r = fn0.div(e), i0 = e - r * (uint32_t)n0;
-      V x[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < ks) {
-          const int64_t ld = sh.mld[i];
-          x[i] = IO::load(src, sh.moff[i] + sh.rsa[r] + ld * sh.rsb[r] + (int64_t)i0 * (g.sa[0] + ld * g.sb[0]),
-                          sh.md1[i]);
-        }
-      for (int j = 0; j < kd; ++j) {
-        V acc = Num<V>::zero();
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i < ks) acc = Num<V>::axpy(sh.coef[i * kd + j], x[i], acc);
-        const int jm = kMaxGroupMembers + j;
-        const int64_t ld = sh.mld[jm];
-        IO::store(dst, sh.moff[jm] + sh.rda[r] + ld * sh.rdb[r] + (int64_t)i0 * (g.da[0] + ld * g.db[0]), sh.md1[jm],
-                  sh.md2[jm], Num<V>::scale(op.alpha, acc), op.beta, op.ims);
-      }
-    }
-    return;
-  }
   for (uint32_t e0 = 0; e0 < E; e0 += chunk) {
     const uint32_t ec = min(chunk, E - e0);
     FastDiv fc;

@@ -92,6 +92,7 @@ struct SegGroup {
 static_assert(sizeof(SegHeader) == 16 && sizeof(SegGroup) == 80, "seg blob layout");
 constexpr int kSegWords = 2 + 10 * kPackGroups + kPackRows;  // rs + rd: 2 x kPackRows int32
 constexpr int kRecoupleStage = 4096;  // doubles of staged recoupling sources per CTA (32 KB)
+constexpr int kRecoupleDirect = 4;    // recoupling groups with <= 4 sources run beside the other jobs
 constexpr int kBoxElems = 4096;  // doubles per box (ComplexF64: half as many elements)
 struct PermJob {
   int32_t group;

@@ -326,7 +326,7 @@ struct SegBuilder {
 static void make_jobs(PermPlan& P) {
   // small single-member groups go last and are packed several per CTA (permute_packed_kernel)
   std::stable_partition(P.groups.begin(), P.groups.end(), [](const PermGroup& g) { return !packable(g); });
-  std::vector<PermJob> rows, multi, tiles, packed, boxes;
+  std::vector<PermJob> rows, multi, dmulti, tiles, packed, boxes;
   // elements per CTA job: 8192 for large permutes, smaller for small ones so that a latency-bound
   // permute still spreads over about two waves of the 148 SMs x 4 resident CTAs
   int64_t total = 0;
@@ -376,7 +376,9 @@ static void make_jobs(PermPlan& P) {
       // recoupling jobs: the job's k_src source rows must fit the kernel's shared-memory stage
       const int64_t budget = single ? job_elems : std::min<int64_t>(job_elems, kRecoupleStage * 8 / P.elem_bytes / g.ksrc);
       int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, budget / std::max(1, g.ext[0])));
-      auto& dst = single ? rows : multi;
+      // recoupling groups of few sources run inside the general launch (no second, serialised launch)
+      static const bool direct_ok = getenv("TK_NO_DIRECT_MULTI") == nullptr;
+      auto& dst = single ? rows : (direct_ok && g.ksrc <= kRecoupleDirect ? dmulti : multi);
       for (int64_t r = 0; r < nrows; r += per)
         dst.push_back(PermJob{gi, (int16_t)std::min(per, nrows - r), (int8_t)(single ? kJobRows : kJobMulti), 0, r});
     } else {
@@ -390,12 +392,12 @@ static void make_jobs(PermPlan& P) {
   // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
   sb.finish();
   rows.insert(rows.begin(), segs.begin(), segs.end());    // seg jobs lead the non-rows-only launch
-  P.njobs = (int)(tiles.size() + rows.size() + packed.size() + boxes.size());
+  P.njobs = (int)(tiles.size() + rows.size() + packed.size() + boxes.size() + dmulti.size());
   P.njobs_rows = (int)(rows.size() - segs.size());
   P.njobs_box = (int)boxes.size();
   P.njobs_multi = (int)multi.size();
   P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
-  P.rows_only = tiles.empty() && packed.empty() && segs.empty();
+  P.rows_only = tiles.empty() && packed.empty() && segs.empty() && dmulti.empty();
   // large permutes (>= 2^24 elements) launch one kernel per job class: rows-only, box, the rest
   P.split = total >= (int64_t(1) << 24);
   if (!P.split && !boxes.empty()) TK_THROW(TK_ERR_CUDA, "internal: box jobs in a small permute");
@@ -425,6 +427,7 @@ static void make_jobs(PermPlan& P) {
   P.jobs.insert(P.jobs.end(), boxes.begin(), boxes.end());
   P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
   P.jobs.insert(P.jobs.end(), packed.begin(), packed.end());
+  P.jobs.insert(P.jobs.end(), dmulti.begin(), dmulti.end());
   P.jobs.insert(P.jobs.end(), multi.begin(), multi.end());
 }
 
