@@ -410,6 +410,14 @@ static void make_jobs(PermPlan& P) {
       else if (g.ksrc == 1 && g.kdst == 1) er += g.nelem, ++gr;
       else em += g.nelem;
     }
+    std::map<int, std::pair<int, int64_t>> kh;  // k_src -> (groups, elements) of recoupling groups
+    for (const PermGroup& g : P.groups)
+      if (g.ksrc > 1 || g.kdst > 1) kh[g.ksrc].first++, kh[g.ksrc].second += g.nelem * g.ksrc;
+    if (!kh.empty()) {
+      fprintf(stderr, "[tk plan] recoupling k_src histogram (groups, source elements):");
+      for (auto& e : kh) fprintf(stderr, " %d:(%d, %lld)", e.first, e.second.first, (long long)e.second.second);
+      fprintf(stderr, "\n");
+    }
     int sg_ng = 0, sg_rows = 0, sg_el = 0;
     for (const PermJob& j : segs) {
       const SegHeader* h = reinterpret_cast<const SegHeader*>(P.blob.data() + j.first);
