@@ -1127,7 +1127,9 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   // fixed order (deterministic) and applies alpha / beta.
   const int ntot = (int)(big.size() + small.size());
   static const bool no_split = getenv("TK_NO_SPLITK") != nullptr;
-  static const int split_target = getenv("TK_SPLIT_TARGET") ? atoi(getenv("TK_SPLIT_TARGET")) : 4;  // tiles/SM (measured: 2 -> 4 cfg3 291 -> 280 us)
+  // tiles/SM below which long-K tiles are split (re-measured after the seg / gather changes: target 2
+  // gives cfg3 T3.R 47.5 us vs 52.7 at 4, cfg2 / cfg7 unchanged; tools/gpu_ab14.sh)
+  static const int split_target = getenv("TK_SPLIT_TARGET") ? atoi(getenv("TK_SPLIT_TARGET")) : 2;
   if (!no_split && ntot > 0 && ntot < split_target * 148) {
     const int want = (split_target * 148 + ntot - 1) / ntot;
     std::vector<GemmTile> out;
