@@ -1431,14 +1431,18 @@ __global__ void __launch_bounds__(kSkinnyThreads)
 // then issues its row's K element loads from A with cp.async into As[k][thread] (all in flight at
 // once, no registers held), waits for its own copies only, and computes its C~ row against the
 // K x N block of B~ in shared memory.
+#ifndef TK_GATHER_MINB
+#define TK_GATHER_MINB 3
+#endif
 template <int KM, int NM>
-__global__ void __launch_bounds__(kGatherRows, 3)
+__global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
     gather_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                          const GatherTile* __restrict__ tiles, const GatherSeg* __restrict__ segs,
                          const int32_t* __restrict__ btab, double alpha, double beta) {
   constexpr int RPT = gather_rows(KM) / kGatherRows;  // rows per thread
   __shared__ double Bs[kSkinnyMax * kSkinnyMax];
-  __shared__ double As[KM][gather_rows(KM)];
+  extern __shared__ __align__(16) double gather_dyn[];
+  double (*As)[gather_rows(KM)] = reinterpret_cast<double (*)[gather_rows(KM)]>(gather_dyn);  // [KM][rows]
   __shared__ __align__(16) GatherSeg ss[gather_seg_cap(KM)];
   pdl_trigger();
   const GatherTile t = tiles[blockIdx.x];
@@ -1523,8 +1527,16 @@ cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, cons
                                double beta, cudaStream_t st) {
   if (!ntiles) return cudaSuccess;
   const int kc = kmax <= 4 ? 0 : (kmax <= 8 ? 1 : 2), nc = nmax <= 4 ? 0 : (nmax <= 8 ? 1 : 2);
-#define TK_GATHER(KM, NM)                                                                                   \
-  launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, 0, st, A, B, C, tiles, segs, btab, alpha, beta); \
+#define TK_GATHER(KM, NM)                                                                                       \
+  {                                                                                                               \
+    constexpr int smem = KM * gather_rows(KM) * 8;                                                                \
+    static bool set = false;                                                                                      \
+    if (!set) {                                                                                                   \
+      cudaFuncSetAttribute(gather_skinny_kernel<KM, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+      set = true;                                                                                                 \
+    }                                                                                                             \
+    launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, smem, st, A, B, C, tiles, segs, btab, alpha, beta); \
+  }                                                                                                               \
   break;
   switch (kc * 3 + nc) {
     case 0: TK_GATHER(4, 4)

@@ -155,7 +155,10 @@ constexpr int kGatherRows = 256;   // rows per tile (one per thread)
 constexpr int kGatherSegs = 128;   // subblocks per tile (64 when K > 8: shared memory)
 __host__ __device__ constexpr int gather_seg_cap(int kmax) { return kmax > 8 ? 64 : kmax > 4 ? 96 : kGatherSegs; }
 // rows per tile by K class: 2 rows per thread while the A~ staging (K x rows doubles) stays <= 16 KB... 32 KB
-__host__ __device__ constexpr int gather_rows(int kmax) { return kmax > 8 ? kGatherRows : 2 * kGatherRows; }
+#ifndef TK_GATHER_RPT
+#define TK_GATHER_RPT 2  // rows per thread for K <= 8 (the A~ stage is dynamic shared memory)
+#endif
+__host__ __device__ constexpr int gather_rows(int kmax) { return kmax > 8 ? kGatherRows : TK_GATHER_RPT * kGatherRows; }
 struct GatherSeg {
   int32_t r0, nrows, k0, nk;
   int64_t src;

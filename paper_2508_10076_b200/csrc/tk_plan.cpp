@@ -889,7 +889,9 @@ static void build_gather(const Tensor& A, ContractPlan& P) {
   for (const GemmGroup& g : P.ggroups)
     if (g.K > 0) rows_total += g.M;
   const int cap = gather_seg_cap(kcls);
-  const int tile_rows = rows_total >= (int64_t)gather_rows(kcls) * 2 * 148 * 4 ? gather_rows(kcls) : kGatherRows;
+  static const int force_rows = getenv("TK_GATHER_ROWS") ? atoi(getenv("TK_GATHER_ROWS")) : 0;
+  int tile_rows = rows_total >= (int64_t)gather_rows(kcls) * 2 * 148 * 4 ? gather_rows(kcls) : kGatherRows;
+  if (force_rows > 0) tile_rows = std::min(force_rows, gather_rows(kcls));
   for (int ci = 0; ci < (int)P.Ct->blocks.size(); ++ci) {
     const GemmGroup& gg = P.ggroups[ci];
     if (gg.K == 0) continue;
