@@ -338,9 +338,12 @@ static void make_jobs(PermPlan& P) {
   static const bool no_seg = getenv("TK_NO_SEG") != nullptr;
   const bool seg = !no_seg && total < (int64_t(1) << 24);
   std::vector<PermJob> segs;
-  // seg jobs are walked by persistent CTAs (about 3 jobs each at full occupancy), so they are smaller
-  static const int64_t seg_div = getenv("TK_SEG_DIV") ? atoll(getenv("TK_SEG_DIV")) : 2 * 148 * 4;
-  SegBuilder sb(P, segs, std::max<int64_t>(256, std::min<int64_t>(kPackElems, total / seg_div)));
+  // seg job size: about total / 296 elements (measured against 1184 / 592 / 148 jobs per permute: fewer,
+  // larger jobs amortise each CTA's blob copy and tail -- cfg7 124 -> 112 us, cfg3 219 -> 213 us;
+  // tools/gpu_ab17.sh), within [256, TK_SEG_MAX = 8192] elements (the row table holds 1024 rows)
+  static const int64_t seg_div = getenv("TK_SEG_DIV") ? atoll(getenv("TK_SEG_DIV")) : 2 * 148;
+  static const int64_t seg_max = getenv("TK_SEG_MAX") ? atoll(getenv("TK_SEG_MAX")) : kPackElems;
+  SegBuilder sb(P, segs, std::max<int64_t>(256, std::min<int64_t>(seg_max, total / seg_div)));
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
     if (seg && g.ksrc == 1 && g.kdst == 1) {
