@@ -74,7 +74,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 #ifndef TK_ROWS_U
 #define TK_ROWS_U 8  // loads in flight per thread in the rows path (Float64)
 #endif
-constexpr int kMaxRows = 256;
 
 // Element I/O of the permute kernels per complex mode CM (see PermCM in tk_kernels.hpp). Offsets are in
 // units of the pointer type: complex elements for interleaved buffers, doubles for planar ones. A

@@ -8,6 +8,10 @@ namespace tk {
 
 constexpr int kMaxLegs = 8;
 constexpr int kMaxGroupMembers = 32;  // k_src, k_dst of one recoupling group (cfg5: <= 3; fSU2xSU2 rank 4: > 8)
+#ifndef TK_MAX_ROWS
+#define TK_MAX_ROWS 512  // cfg4 permutes: 512 -> 5.24 TB/s, 256 -> 4.98, 1024 -> 4.0 (tools/gpu_ab21.sh)
+#endif
+constexpr int kMaxRows = TK_MAX_ROWS;    // rows per rows / recoupling job (row tables in shared memory)
 constexpr int kRegMembers = 8;        // destinations accumulated in registers per pass
 
 // One uncoupled-charge group of a permute (Alg. 10): y_j = alpha * sum_i M[i][j] perm(x_i) + beta * y_j.

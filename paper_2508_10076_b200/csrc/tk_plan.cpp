@@ -332,7 +332,8 @@ static void make_jobs(PermPlan& P) {
   int64_t total = 0;
   for (const PermGroup& g : P.groups) total += g.nelem;
   static const int64_t job_div = getenv("TK_JOB_DIV") ? atoll(getenv("TK_JOB_DIV")) : 2 * 148 * 4;
-  const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(kPackElems, total / job_div));
+  static const int64_t job_max = getenv("TK_JOB_MAX") ? atoll(getenv("TK_JOB_MAX")) : kPackElems;
+  const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(job_max, total / job_div));
   int64_t pack_elems = 0, pack_rows = 0;
   // latency regime: single-member rows / packable groups become kJobSeg blobs (TK_NO_SEG=1 disables)
   static const bool no_seg = getenv("TK_NO_SEG") != nullptr;
@@ -378,7 +379,7 @@ static void make_jobs(PermPlan& P) {
       const bool single = g.ksrc == 1 && g.kdst == 1;
       // recoupling jobs: the job's k_src source rows must fit the kernel's shared-memory stage
       const int64_t budget = single ? job_elems : std::min<int64_t>(job_elems, kRecoupleStage * 8 / P.elem_bytes / g.ksrc);
-      int64_t per = std::max<int64_t>(1, std::min<int64_t>(256, budget / std::max(1, g.ext[0])));
+      int64_t per = std::max<int64_t>(1, std::min<int64_t>(kMaxRows, budget / std::max(1, g.ext[0])));
       // recoupling groups of few sources run inside the general launch (no second, serialised launch)
       static const bool direct_ok = getenv("TK_NO_DIRECT_MULTI") == nullptr;
       auto& dst = single ? rows : (direct_ok && g.ksrc <= kRecoupleDirect ? dmulti : multi);
