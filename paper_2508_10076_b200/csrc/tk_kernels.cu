@@ -1279,6 +1279,9 @@ __device__ __forceinline__ void gemm_tile_mbar(const double* __restrict__ A, con
 }
 
 #define TK_MBAR 128, 128, 32, 32, 16, 6
+#ifndef TK_MBAR_PD
+#define TK_MBAR_PD 2  // prefetch distance (k-steps) of the big-tile GEMM's stage ring
+#endif
 using MbarCfg = GemmCfg<TK_MBAR>;
 constexpr size_t kMbarSmem = MbarCfg::SMEM + 2 * 6 * sizeof(uint64_t);
 
@@ -1558,13 +1561,13 @@ cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmG
   // big tiles: mbarrier pipeline, 16 warps of 32x32 on 128x128, BK 16, 6 stages, prefetch distance 2
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_mbar_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
+    cudaFuncSetAttribute(gemm_mbar_kernel<TK_MBAR_PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
     cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
     attr = true;
   }
   const int base_vec = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0;
   if (ntiles_big)
-    launch_k(gemm_mbar_kernel<2>, ntiles_big, MbarCfg::THREADS, kMbarSmem, st, A, B, C, groups, tiles, alpha, beta,
+    launch_k(gemm_mbar_kernel<TK_MBAR_PD>, ntiles_big, MbarCfg::THREADS, kMbarSmem, st, A, B, C, groups, tiles, alpha, beta,
              base_vec);
   if (ntiles_small)
     launch_k(gemm_small_kernel, ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C, groups,
