@@ -1278,7 +1278,13 @@ __device__ __forceinline__ void gemm_tile_mbar(const double* __restrict__ A, con
   }
 }
 
-#define TK_MBAR 128, 128, 32, 32, 16, 6
+#ifndef TK_MBAR_BK
+#define TK_MBAR_BK 16
+#endif
+#ifndef TK_MBAR_STAGES
+#define TK_MBAR_STAGES 6
+#endif
+#define TK_MBAR 128, 128, 32, 32, TK_MBAR_BK, TK_MBAR_STAGES
 #ifndef TK_MBAR_PD
 #define TK_MBAR_PD 2  // prefetch distance (k-steps) of the big-tile GEMM's stage ring
 #endif
