@@ -245,7 +245,9 @@ def _tuples_case(kind, A_sp, B_sp, tup, alpha=1.0, beta=0.0, seed=0, cplx=False,
     A, B = tk.tensor_from_spec(A_sp, dt), tk.tensor_from_spec(B_sp, dt)
     C = tk.tk_contract_tuples_output(A, pA, qA, B, pB, qB, pAB, qAB)
     Asp, Bsp = A_sp["cod"] + A_sp["dom"], B_sp["cod"] + B_sp["dom"]
-    cod, dom = OC.permuted_spaces([Asp[i] for i in pA], [Bsp[j] for j in qB], pAB, qAB)
+    at_cod, _ = OC.permuted_spaces(A_sp["cod"], A_sp["dom"], pA, qA)   # selection rule
+    _, bt_dom = OC.permuted_spaces(B_sp["cod"], B_sp["dom"], pB, qB)
+    cod, dom = OC.permuted_spaces(at_cod, bt_dom, pAB, qAB)
     lc = OL.homspace_layout(kind, cod, dom)
     assert C.nelems == lc.nelems
     y0 = draw(lc.nelems)

@@ -350,7 +350,9 @@ def test_contract_tuples_output_and_errors():
     Asp, Bsp = A_sp["cod"] + A_sp["dom"], B_sp["cod"] + B_sp["dom"]
     for tup in (([0, 1], [2, 3], [1, 0], [2], [2, 0], [1]), ([1, 0], [3, 2], [0, 1], [2], [0], [2, 1])):
         C = tk.tk_contract_tuples_output(A, *tup[:2], B, *tup[2:])
-        cod, dom = OC.permuted_spaces([Asp[i] for i in tup[0]], [Bsp[j] for j in tup[3]], tup[4], tup[5])
+        at_cod, _ = OC.permuted_spaces(A_sp["cod"], A_sp["dom"], tup[0], tup[1])
+        _, bt_dom = OC.permuted_spaces(B_sp["cod"], B_sp["dom"], tup[2], tup[3])
+        cod, dom = OC.permuted_spaces(at_cod, bt_dom, tup[4], tup[5])
         assert C.nelems == OL.homspace_layout("fU1xU1", cod, dom).nelems
         assert C.info()["n_cod"] == len(tup[4])
     # reading C2 tuples of A[1,2,3,4] B[4,3,5] -> C[5,1;2]
