@@ -1110,8 +1110,9 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
     int gi = (int)P.ggroups.size();
     P.ggroups.push_back(g);
     if (g.K > 0 && g.K <= kSkinnyMax && g.N <= kSkinnyMax) {  // streaming path (HBM-bound block)
-      for (int m = 0; m < g.M; m += kSkinnyRows)
-        skinny.push_back(GemmTile{gi, m, 0, std::min(kSkinnyRows, g.M - m), 0, g.K, -1, 0});
+      static const int srows = getenv("TK_SKINNY_ROWS") ? atoi(getenv("TK_SKINNY_ROWS")) : kSkinnyRows;
+      for (int m = 0; m < g.M; m += srows)
+        skinny.push_back(GemmTile{gi, m, 0, std::min(srows, g.M - m), 0, g.K, -1, 0});
       continue;
     }
     // short-K blocks (K <= 128: the L.theta steps of the DMRG chains) take 64 x 64 tiles: 4x the CTAs,
@@ -1122,7 +1123,8 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
     // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that one wave of
     // ~148 co-resident tiles covers a ~G x 12 rectangle and shares the A and B k-slices in L2
     // (row-major order re-read all of B from DRAM once per tile-row).
-    const int ntm = (g.M + bm - 1) / bm, ntn = (g.N + bn - 1) / bn, G = 12;
+    static const int band = getenv("TK_GEMM_BAND") ? atoi(getenv("TK_GEMM_BAND")) : 12;
+    const int ntm = (g.M + bm - 1) / bm, ntn = (g.N + bn - 1) / bn, G = band;
     for (int mb = 0; mb < ntm; mb += G)
       for (int nt = 0; nt < ntn; ++nt)
         for (int mt = mb; mt < std::min(ntm, mb + G); ++mt)
