@@ -170,6 +170,26 @@ tk_status tk_contract_tuples(const tk_tensor* A, const void* a, int32_t conjA, c
                              const int32_t* tup, const int32_t* ntup, double alpha, double beta,
                              void* ws, size_t ws_bytes, tk_stream stream);
 
+/* ncon-style network contraction (the @tensor network convention):
+ * n tensors T[i] with label lists labels[i] (one label per leg, codomain legs first): positive labels
+ * are contracted and appear exactly twice, on two different tensors (a label twice on one tensor is a
+ * trace: TK_ERR_MALFORMED_NETWORK); negative labels -1, -2, ..., -m are the open legs, which become the
+ * output's legs in that order, the first n_cod_out of them its codomain. `order` lists every positive
+ * label; the network is contracted pairwise in that order -- each step takes the two tensors holding the
+ * next label and contracts all labels they share (tk_contract, reading C2; for fermionic kinds the order
+ * is part of the definition, reading C13). Disconnected pieces are joined by outer products at the end.
+ * Intermediates keep the (open A ; open B) order and live in the workspace (tk_ncon_workspace bytes,
+ * 256-byte aligned, caller-owned) together with the pairwise scratch. alpha / beta apply to the output
+ * only. Errors: MALFORMED_NETWORK, UNKNOWN_LABEL (order), SPACE_MISMATCH (legs or C's HomSpace),
+ * WORKSPACE_TOO_SMALL; a single tensor is TK_ERR_UNSUPPORTED (use tk_permute). */
+tk_status tk_ncon_output(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
+                         int32_t norder, int32_t n_cod_out, tk_tensor** C);
+tk_status tk_ncon_workspace(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
+                            int32_t norder, int32_t n_cod_out, size_t* bytes);
+tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data, const int32_t* const* labels,
+                  const int32_t* order, int32_t norder, int32_t n_cod_out, const tk_tensor* C, void* c,
+                  double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream);
+
 /* -------------------------------------------------- blockwise truncated SVD */
 /* A~ = permute(A, (p, q)) = U S Vh, block by block (eq. svd, "directly acting on the matrix
  * representation" P:799-809; Alg. 9). U: (A~ codomain) <- W, S: W <- W diagonal, Vh: W <- (A~

@@ -1,0 +1,224 @@
+// ncon-style network contraction (@tensor networks) on top of the pairwise
+// entry points: the network is contracted pair by pair in the caller's order, every step one
+// tk_contract (Alg. 4) whose intermediate lands in the caller's workspace. See include/tk.h.
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "tk_internal.hpp"
+
+using namespace tk;
+
+namespace {
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Item {
+  const tk_tensor* t;       // the tensor (borrowed input or owned intermediate)
+  bool owned;
+  std::vector<int32_t> lab;
+  const void* data;         // input pointer, or nullptr for an intermediate (at ws + off)
+  size_t off;
+};
+
+struct Step {
+  int a, b;                 // items contracted
+  std::vector<int32_t> labA, labB, labC;
+  int32_t ncod;
+  bool last;                // writes the network's output (alpha / beta, caller's buffer)
+};
+
+// Walks the network: validates the labels, decides the pairwise steps, creates the intermediate
+// HomSpaces and their workspace offsets. The final tensor's HomSpace is returned in *out (new
+// reference) when `out` is non-null; the workspace size in *bytes.
+void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order, int32_t norder,
+               int32_t n_cod_out, std::vector<Item>& items, std::vector<Step>& steps, size_t* bytes,
+               tk_tensor** out) {
+  if (n < 1 || !T || !labels) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: no tensors");
+  std::map<int32_t, int> count;
+  int nneg = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!T[i]) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: null tensor");
+    const Tensor& t = *(const Tensor*)T[i];
+    if (t.nlegs() > 0 && !labels[i]) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: null label list");
+    Item it{T[i], false, {}, nullptr, 0};
+    for (int l = 0; l < t.nlegs(); ++l) {
+      const int32_t x = labels[i][l];
+      if (x == 0) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: label 0");
+      if (x < 0) ++nneg;
+      if (++count[x] > (x > 0 ? 2 : 1)) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: label used too often");
+      it.lab.push_back(x);
+    }
+    items.push_back(it);
+  }
+  for (auto& e : count) {
+    if (e.first > 0 && e.second != 2) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: a positive label must appear twice");
+    if (e.first < -nneg) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: open labels must be -1 .. -m");
+  }
+  for (const Item& it : items)
+    for (size_t a = 0; a < it.lab.size(); ++a)
+      for (size_t b = a + 1; b < it.lab.size(); ++b)
+        if (it.lab[a] == it.lab[b]) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: traces within one tensor unsupported");
+  if (n_cod_out < 0 || n_cod_out > nneg) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: bad output codomain count");
+  std::vector<int32_t> seq(order, order + std::max(norder, 0));
+  for (int32_t x : seq)
+    if (x <= 0 || !count.count(x)) TK_THROW(TK_ERR_UNKNOWN_LABEL, "tk_ncon: order names an unknown label");
+  for (auto& e : count)
+    if (e.first > 0 && std::find(seq.begin(), seq.end(), e.first) == seq.end())
+      TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: order must list every contracted label");
+  std::vector<int32_t> outlab;
+  for (int k = 1; k <= nneg; ++k) outlab.push_back(-k);
+
+  std::vector<bool> alive(items.size(), true);
+  size_t off = 0, wsmax = 0;
+  auto contract_pair = [&](int a, int b) {
+    Step s{a, b, items[a].lab, items[b].lab, {}, 0, false};
+    std::vector<int32_t> oa, ob;
+    for (int32_t x : s.labA)
+      if (std::find(s.labB.begin(), s.labB.end(), x) == s.labB.end()) oa.push_back(x);
+    for (int32_t x : s.labB)
+      if (std::find(s.labA.begin(), s.labA.end(), x) == s.labA.end()) ob.push_back(x);
+    int nalive = 0;
+    for (bool al : alive) nalive += al;
+    s.last = nalive == 2;
+    if (s.last) {  // the network's output: legs -1, -2, ... with n_cod_out codomain legs
+      s.labC = outlab;
+      s.ncod = n_cod_out;
+    } else {  // intermediates keep C~'s own order (open A ; open B): no output permute
+      s.labC = oa;
+      s.labC.insert(s.labC.end(), ob.begin(), ob.end());
+      s.ncod = (int32_t)oa.size();
+    }
+    tk_tensor* C = nullptr;
+    tk_status st = tk_contract_output(items[a].t, s.labA.data(), items[b].t, s.labB.data(), s.labC.data(), s.ncod, &C);
+    if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    size_t w = 0;
+    st = tk_contract_workspace(items[a].t, s.labA.data(), items[b].t, s.labB.data(), C, s.labC.data(), &w);
+    if (st != TK_OK) {
+      tk_tensor_release(C);
+      TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    }
+    wsmax = std::max(wsmax, w);
+    const Tensor& c = *(const Tensor*)C;
+    Item it{C, true, s.labC, nullptr, off};
+    if (!s.last) off = align256(off + (size_t)c.nelems * (c.dtype == TK_C64 ? 16 : 8));
+    alive[a] = alive[b] = false;
+    items.push_back(it);
+    alive.push_back(true);
+    steps.push_back(s);
+  };
+  for (int32_t x : seq) {
+    int a = -1, b = -1;
+    for (int i = 0; i < (int)items.size(); ++i)
+      if (alive[i] && std::find(items[i].lab.begin(), items[i].lab.end(), x) != items[i].lab.end())
+        (a < 0 ? a : b) = i;
+    if (a < 0) continue;  // contracted already (shared with an earlier label of the same pair)
+    if (b < 0) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: internal label bookkeeping");
+    contract_pair(a, b);
+  }
+  // disconnected pieces: outer products, left to right
+  for (;;) {
+    std::vector<int> al;
+    for (int i = 0; i < (int)items.size(); ++i)
+      if (alive[i]) al.push_back(i);
+    if (al.size() < 2) break;
+    contract_pair(al[0], al[1]);
+  }
+  if (steps.empty()) TK_THROW(TK_ERR_UNSUPPORTED, "tk_ncon: a single tensor (use tk_permute)");
+  *bytes = off + wsmax;
+  if (out) {
+    *out = const_cast<tk_tensor*>(items.back().t);
+    items.back().owned = false;  // ownership moves to the caller
+  }
+}
+
+struct Release {  // intermediate HomSpaces are freed on every exit path
+  std::vector<Item>& items;
+  ~Release() {
+    for (Item& it : items)
+      if (it.owned) tk_tensor_release(const_cast<tk_tensor*>(it.t));
+  }
+};
+
+}  // namespace
+
+#define TK_API_BEGIN try {
+#define TK_API_END                  \
+  return TK_OK;                     \
+  }                                 \
+  catch (const tk::Error& e) {      \
+    set_last_error(e.what());       \
+    return e.code;                  \
+  }                                 \
+  catch (const std::exception& e) { \
+    set_last_error(e.what());       \
+    return TK_ERR_INVALID_ARGUMENT; \
+  }
+
+extern "C" {
+
+tk_status tk_ncon_output(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
+                         int32_t norder, int32_t n_cod_out, tk_tensor** out) {
+  std::vector<Item> items;
+  Release guard{items};
+  TK_API_BEGIN
+  if (!out) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<Step> steps;
+  size_t bytes = 0;
+  ncon_plan(n, T, labels, order, norder, n_cod_out, items, steps, &bytes, out);
+  TK_API_END
+}
+
+tk_status tk_ncon_workspace(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
+                            int32_t norder, int32_t n_cod_out, size_t* bytes) {
+  std::vector<Item> items;
+  Release guard{items};
+  TK_API_BEGIN
+  if (!bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<Step> steps;
+  ncon_plan(n, T, labels, order, norder, n_cod_out, items, steps, bytes, nullptr);
+  TK_API_END
+}
+
+tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data, const int32_t* const* labels,
+                  const int32_t* order, int32_t norder, int32_t n_cod_out, const tk_tensor* C, void* c, double alpha,
+                  double beta, void* ws, size_t ws_bytes, tk_stream stream) {
+  std::vector<Item> items;
+  Release guard{items};
+  TK_API_BEGIN
+  if (!data || !C) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<Step> steps;
+  size_t bytes = 0;
+  tk_tensor* out = nullptr;
+  ncon_plan(n, T, labels, order, norder, n_cod_out, items, steps, &bytes, &out);
+  const bool same = ((const Tensor*)out)->sig == ((const Tensor*)C)->sig;
+  tk_tensor_release(out);
+  if (!same) TK_THROW(TK_ERR_SPACE_MISMATCH, "tk_ncon: C does not have the network's output HomSpace");
+  if (ws_bytes < bytes || (bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "tk_ncon: workspace too small");
+  if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  for (int i = 0; i < n; ++i) items[i].data = data[i];
+  size_t inter = 0;  // intermediates occupy [0, inter) of the workspace, the pairwise scratch the rest
+  for (const Item& it : items)
+    if (it.owned && it.data == nullptr) {
+      const Tensor& t = *(const Tensor*)it.t;
+      inter = std::max(inter, align256(it.off + (size_t)t.nelems * (t.dtype == TK_C64 ? 16 : 8)));
+    }
+  char* w = (char*)ws;
+  for (size_t k = 0; k < steps.size(); ++k) {
+    const Step& s = steps[k];
+    Item& ia = items[s.a];
+    Item& ib = items[s.b];
+    const void* a = ia.data ? ia.data : (const void*)(w + ia.off);
+    const void* b = ib.data ? ib.data : (const void*)(w + ib.off);
+    Item& ic = items[n + k];
+    void* cc = s.last ? c : (void*)(w + ic.off);
+    const tk_tensor* Ct = s.last ? C : ic.t;
+    tk_status st = tk_contract(ia.t, a, s.labA.data(), 0, ib.t, b, s.labB.data(), 0, Ct, cc, s.labC.data(),
+                               s.last ? alpha : 1.0, s.last ? beta : 0.0, w + inter, ws_bytes - inter, stream);
+    if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+  }
+  TK_API_END
+}
+
+}  // extern "C"

@@ -83,6 +83,12 @@ _contract_tuples_workspace = _sig("tk_contract_tuples_workspace", [_p, _p, _p, _
                                                                    ctypes.POINTER(ctypes.c_size_t)])
 _contract_tuples = _sig("tk_contract_tuples", [_p, _p, ctypes.c_int32, _p, _p, ctypes.c_int32, _p, _p, _i32p, _i32p,
                                                ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
+_ncon_output = _sig("tk_ncon_output", [ctypes.c_int32, _p, _p, _i32p, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.POINTER(_p)])
+_ncon_workspace = _sig("tk_ncon_workspace", [ctypes.c_int32, _p, _p, _i32p, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.POINTER(ctypes.c_size_t)])
+_ncon = _sig("tk_ncon", [ctypes.c_int32, _p, _p, _p, _i32p, ctypes.c_int32, ctypes.c_int32, _p, _p, ctypes.c_double,
+                         ctypes.c_double, _p, ctypes.c_size_t, _p])
 _profile_enable = _sig("tk_profile_enable", [ctypes.c_int32])
 _phase_times = _sig("tk_phase_times", [ctypes.POINTER(ctypes.c_float), _dp, _dp])
 _last_launch_count = _sig("tk_last_launch_count", [], ctypes.c_int32)
@@ -117,7 +123,7 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_permute_transfer", "tk_permute_transfer_planar", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
             "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract", "tk_trace_output", "tk_trace_workspace",
             "tk_trace", "tk_trace_transfer", "tk_contract_tuples_output", "tk_contract_tuples_workspace",
-            "tk_contract_tuples"]
+            "tk_contract_tuples", "tk_ncon_output", "tk_ncon_workspace", "tk_ncon"]
 
 
 def _i32(seq):
@@ -329,6 +335,37 @@ def tk_contract_tuples(A, a, pA, qA, B, b, pB, qB, C, c, pAB, qAB, alpha=1.0, be
     keep, tp, np_ = _tuples(pA, qA, pB, qB, pAB, qAB)
     _check(_contract_tuples(A.h, _ptr(a), int(conjA), B.h, _ptr(b), int(conjB), C.h, _ptr(c), tp, np_, float(alpha),
                             float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def _ncon_args(tensors, labels, order):
+    n = len(tensors)
+    th = (_p * n)(*[t.h for t in tensors])
+    labs = [_i32(l if len(l) else [0]) for l in labels]
+    lp = (_i32p * n)(*[x[1] for x in labs])
+    o, op = _i32(order if len(order) else [0])
+    return n, th, lp, (labs, o), op, len(order)
+
+
+def tk_ncon_output(tensors, labels, order, n_cod_out):
+    """ncon network output HomSpace (include/tk.h): labels per tensor, > 0 contracted, -1..-m open."""
+    n, th, lp, keep, op, no = _ncon_args(tensors, labels, order)
+    h = _p()
+    _check(_ncon_output(n, ctypes.cast(th, _p), ctypes.cast(lp, _p), op, no, n_cod_out, ctypes.byref(h)))
+    return Tensor(h.value)
+
+
+def tk_ncon_workspace(tensors, labels, order, n_cod_out):
+    n, th, lp, keep, op, no = _ncon_args(tensors, labels, order)
+    b = ctypes.c_size_t()
+    _check(_ncon_workspace(n, ctypes.cast(th, _p), ctypes.cast(lp, _p), op, no, n_cod_out, ctypes.byref(b)))
+    return b.value
+
+
+def tk_ncon(tensors, datas, labels, order, n_cod_out, C, c, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, stream=None):
+    n, th, lp, keep, op, no = _ncon_args(tensors, labels, order)
+    dp = (_p * n)(*[_ptr(x) for x in datas])
+    _check(_ncon(n, ctypes.cast(th, _p), ctypes.cast(dp, _p), ctypes.cast(lp, _p), op, no, n_cod_out, C.h, _ptr(c),
+                 float(alpha), float(beta), _ptr(ws), ws_bytes, _stream(stream)))
 
 
 def tk_profile_enable(on=True):

@@ -1,0 +1,105 @@
+"""tk_ncon (network contraction) against the oracle -- needs a B200.
+
+The oracle side replays the network pair by pair exactly as include/tk.h specifies (each step
+contracts the two tensors holding the next label of `order` over all labels they share; intermediates
+ordered (open A ; open B), the last step into -1, -2, ...), with the dense oracle contraction for every
+step; for bosonic kinds it is also checked against one einsum over the whole network.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from oracle import layout as OL, dense as OD, contract as OC, sectors as OS  # noqa: E402
+from workloads import configs as W  # noqa: E402
+
+TOL = 1e-12
+
+
+def oracle_ncon(kind, specs, denses, labels, order, n_cod_out):
+    items = [(s["cod"], s["dom"], D, list(l)) for s, D, l in zip(specs, denses, labels)]
+    alive = [True] * len(items)
+    m = sum(1 for l in labels for x in l if x < 0)
+
+    def pair(a, b):
+        Ac, Ad, A, la = items[a]
+        Bc, Bd, B, lb = items[b]
+        oa = [x for x in la if x not in lb]
+        ob = [x for x in lb if x not in la]
+        last = sum(alive) == 2
+        lc, nc = ([-k for k in range(1, m + 1)], n_cod_out) if last else (oa + ob, len(oa))
+        D = OC.contract(kind, A, Ac + Ad, len(Ac), la, B, Bc + Bd, len(Bc), lb, lc, nc)
+        cod, dom = OC.output_spaces(Ac, Ad, Bc, Bd, la, lb, lc, nc)
+        alive[a] = alive[b] = False
+        items.append((cod, dom, D, lc))
+        alive.append(True)
+
+    for x in order:
+        hold = [i for i, it in enumerate(items) if alive[i] and x in it[3]]
+        if hold:
+            pair(hold[0], hold[1])
+    while sum(alive) > 1:
+        al = [i for i in range(len(items)) if alive[i]]
+        pair(al[0], al[1])
+    cod, dom, D, _ = items[-1]
+    return cod, dom, D
+
+
+def _network_cfg2(chi=64):
+    cfg = W.cfg2(chi=chi)
+    t = {k: v[0] for k, v in cfg["tensors"].items()}
+    # L(a', a, w) th(a, s1, s2, b) W1(w, s1', s1, w2) W2(w2, s2', s2, w3) R(w3, b', b): the DMRG H.theta
+    specs = [t["L"], t["theta"], t["W1"], t["W2"], t["R"]]
+    labels = [[-1, 1, 2], [1, 3, 4, 5], [2, -2, 3, 6], [6, -3, 4, 7], [7, -4, 5]]
+    return "U1", specs, labels, [1, 2, 3, 6, 4, 5, 7], 3
+
+
+def _network_cfg3(chi=96):
+    cfg = W.cfg3(chi=chi)
+    t = {k: v[0] for k, v in cfg["tensors"].items()}
+    specs = [t["L"], t["theta"], t["W1"], t["W2"], t["R"]]
+    labels = [[-1, 1, 2], [1, 3, 4, 5], [2, -2, 3, 6], [6, -3, 4, 7], [7, -4, 5]]
+    return "fU1xU1", specs, labels, [1, 2, 3, 6, 4, 5, 7], 3
+
+
+def _network_su2():
+    V = W.space("SU2", [((0,), 3), ((1,), 2), ((2,), 2)])
+    A = {"cod": [V, V], "dom": [V]}
+    B = {"cod": [V], "dom": [V, V]}
+    M = {"cod": [V], "dom": [V]}
+    # A[-1, 1, 2] B[2, -2, 3] M[3, 1]: a ring with two open legs; and a disconnected piece M2[-3, -4]
+    return "SU2", [A, B, M, M], [[-1, 1, 2], [2, -2, 3], [3, 1], [-3, -4]], [2, 3, 1], 2
+
+
+@pytest.mark.parametrize("maker", [_network_cfg2, _network_cfg3, _network_su2], ids=["cfg2", "cfg3", "su2"])
+def test_ncon_vs_oracle(maker):
+    from paper_2508_10076_b200 import tk
+    kind, specs, labels, order, n_cod_out = maker()
+    rng = np.random.default_rng(7)
+    lays = [OL.homspace_layout(kind, s["cod"], s["dom"]) for s in specs]
+    xs = [rng.standard_normal(l.nelems) for l in lays]
+    T = [tk.tensor_from_spec(s) for s in specs]
+    C = tk.tk_ncon_output(T, labels, order, n_cod_out)
+    cod, dom, D = oracle_ncon(kind, specs, [OD.to_dense(l, x) for l, x in zip(lays, xs)], labels, order, n_cod_out)
+    lc = OL.homspace_layout(kind, cod, dom)
+    assert C.nelems == lc.nelems
+    y0 = rng.standard_normal(lc.nelems)
+    c = torch.from_numpy(y0.copy()).cuda()
+    nws = tk.tk_ncon_workspace(T, labels, order, n_cod_out)
+    ws = torch.empty(nws // 8 + 32, dtype=torch.float64, device="cuda")
+    tk.tk_ncon(T, [torch.from_numpy(x).cuda() for x in xs], labels, order, n_cod_out, C, c, alpha=-0.5, beta=0.25,
+               ws=ws, ws_bytes=ws.numel() * 8)
+    torch.cuda.synchronize()
+    want = -0.5 * D + 0.25 * OD.to_dense(lc, y0)
+    assert OC.rel_frobenius(OD.to_dense(lc, c.cpu().numpy()), want) <= TOL
+    if not OS.is_fermionic(kind):  # bosonic: the whole network is one einsum (ncon semantics)
+        letters = {}
+        def L(x):
+            return letters.setdefault(x, "abcdefghijklmnopqrstuvwxyz"[len(letters)])
+        dens = [OD.to_dense(l, x) for l, x in zip(lays, xs)]
+        m = sum(1 for l in labels for x in l if x < 0)
+        spec = ",".join("".join(L(x) for x in l) for l in labels) + "->" + "".join(L(-k) for k in range(1, m + 1))
+        E = np.einsum(spec, *dens, optimize=True)
+        assert OC.rel_frobenius(-0.5 * E + 0.25 * OD.to_dense(lc, y0), want) <= 1e-12

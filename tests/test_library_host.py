@@ -380,3 +380,26 @@ def test_parse_deligne_spellings():
         la, da = sa.sectors()
         lb, db = sb.sectors()
         assert np.array_equal(la, lb) and np.array_equal(da, db)
+
+
+def test_ncon_output_and_errors():
+    """tk_ncon_output (include/tk.h): the HomSpace the pairwise replay gives; malformed networks rejected."""
+    V = W.space("U1", [((-1,), 2), ((0,), 3), ((1,), 2)])
+    A = tk.tensor_from_spec({"cod": [V, V], "dom": [V]})
+    B = tk.tensor_from_spec({"cod": [V], "dom": [V, V]})
+    M = tk.tensor_from_spec({"cod": [V], "dom": [V]})
+    C = tk.tk_ncon_output([A, B, M], [[-1, 1, 2], [2, -2, 3], [3, 1]], [2, 3, 1], 1)
+    # replay: A.B over label 2 -> (-1, 1 ; -2, 3), then with M over 3 and 1 -> (-1 ; -2)
+    T1 = tk.tk_contract_output(A, [-1, 1, 2], B, [2, -2, 3], [-1, 1, -2, 3], 2)
+    C2 = tk.tk_contract_output(T1, [-1, 1, -2, 3], M, [3, 1], [-1, -2], 1)
+    assert C.nelems == C2.nelems and C.info() == C2.info()
+    assert tk.tk_ncon_workspace([A, B, M], [[-1, 1, 2], [2, -2, 3], [3, 1]], [2, 3, 1], 1) > 0
+    bad = [([[-1, 1, 2], [2, -2, 3], [3, 4]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),    # 4 appears once
+           ([[-1, 1, 1], [2, -2, 3], [3, 2]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),    # trace in one tensor
+           ([[-1, 1, 2], [2, -3, 3], [3, 1]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),    # open labels -1, -3
+           ([[-1, 1, 2], [2, -2, 3], [3, 1]], [1, 2], "TK_ERR_MALFORMED_NETWORK"),       # order misses 3
+           ([[-1, 1, 2], [2, -2, 3], [3, 1]], [1, 2, 9], "TK_ERR_UNKNOWN_LABEL")]        # order names 9
+    for labels, order, status in bad:
+        with pytest.raises(tk.TKError) as e:
+            tk.tk_ncon_output([A, B, M], labels, order, 1)
+        assert e.value.status == status, (labels, order)
