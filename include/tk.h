@@ -172,8 +172,8 @@ tk_status tk_contract_tuples(const tk_tensor* A, const void* a, int32_t conjA, c
 
 /* ncon-style network contraction (the @tensor network convention):
  * n tensors T[i] with label lists labels[i] (one label per leg, codomain legs first): positive labels
- * are contracted and appear exactly twice, on two different tensors (a label twice on one tensor is a
- * trace: TK_ERR_MALFORMED_NETWORK); negative labels -1, -2, ..., -m are the open legs, which become the
+ * are contracted and appear exactly twice -- on two tensors, or twice on one tensor, which is a partial
+ * trace (Alg. 3, tk_trace; done first, bosonic and planar kinds, Float64); negative labels -1, -2, ..., -m are the open legs, which become the
  * output's legs in that order, the first n_cod_out of them its codomain. `order` lists every positive
  * label; the network is contracted pairwise in that order -- each step takes the two tensors holding the
  * next label and contracts all labels they share (tk_contract, reading C2; for fermionic kinds the order

@@ -23,10 +23,11 @@ struct Item {
 };
 
 struct Step {
-  int a, b;                 // items contracted
+  int a, b;                 // items contracted (b = -1: a partial trace of item a)
   std::vector<int32_t> labA, labB, labC;
   int32_t ncod;
   bool last;                // writes the network's output (alpha / beta, caller's buffer)
+  std::vector<int32_t> pt, qt, p, q;  // trace steps: tk_trace arguments
 };
 
 // Walks the network: validates the labels, decides the pairwise steps, creates the intermediate
@@ -56,10 +57,6 @@ void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* label
     if (e.first > 0 && e.second != 2) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: a positive label must appear twice");
     if (e.first < -nneg) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: open labels must be -1 .. -m");
   }
-  for (const Item& it : items)
-    for (size_t a = 0; a < it.lab.size(); ++a)
-      for (size_t b = a + 1; b < it.lab.size(); ++b)
-        if (it.lab[a] == it.lab[b]) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: traces within one tensor unsupported");
   if (n_cod_out < 0 || n_cod_out > nneg) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: bad output codomain count");
   std::vector<int32_t> seq(order, order + std::max(norder, 0));
   for (int32_t x : seq)
@@ -72,8 +69,52 @@ void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* label
 
   std::vector<bool> alive(items.size(), true);
   size_t off = 0, wsmax = 0;
+  // a label twice on one tensor is a partial trace (Alg. 3): done first, by tk_trace, into
+  // an intermediate that keeps the remaining legs in order (codomain legs stay codomain)
+  for (int i = 0; i < n; ++i) {
+    const Tensor& t = *(const Tensor*)items[i].t;
+    Step s{i, -1, items[i].lab, {}, {}, 0, false, {}, {}, {}, {}};
+    std::vector<bool> used(t.nlegs(), false);
+    for (int x = 0; x < t.nlegs(); ++x)
+      for (int y = x + 1; y < t.nlegs(); ++y)
+        if (items[i].lab[x] == items[i].lab[y]) {
+          // the ket leg is read as the codomain leg of the pair (include/tk.h, tk_trace)
+          const Space* sx = x < t.n_cod() ? t.cod[x] : t.dom[x - t.n_cod()];
+          const bool ket_x = !(sx->dual ^ (x >= t.n_cod()));
+          s.pt.push_back(ket_x ? x : y);
+          s.qt.push_back(ket_x ? y : x);
+          used[x] = used[y] = true;
+        }
+    if (s.pt.empty()) continue;
+    int nalive = 0;
+    for (bool al : alive) nalive += al;
+    for (int l = 0; l < t.nlegs(); ++l)
+      if (!used[l]) (l < t.n_cod() ? s.p : s.q).push_back(l);
+    for (int l : s.p) s.labC.push_back(items[i].lab[l]);
+    for (int l : s.q) s.labC.push_back(items[i].lab[l]);
+    s.ncod = (int32_t)s.p.size();
+    if (nalive == 1 && n == 1) TK_THROW(TK_ERR_UNSUPPORTED, "tk_ncon: a single tensor (use tk_trace)");
+    tk_tensor* C = nullptr;
+    tk_status st = tk_trace_output(items[i].t, s.pt.data(), s.qt.data(), (int32_t)s.pt.size(), s.p.data(),
+                                   (int32_t)s.p.size(), s.q.data(), (int32_t)s.q.size(), &C);
+    if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    size_t w = 0;
+    st = tk_trace_workspace(items[i].t, s.pt.data(), s.qt.data(), (int32_t)s.pt.size(), s.p.data(),
+                            (int32_t)s.p.size(), s.q.data(), (int32_t)s.q.size(), C, &w);
+    if (st != TK_OK) {
+      tk_tensor_release(C);
+      TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    }
+    wsmax = std::max(wsmax, w);
+    const Tensor& c = *(const Tensor*)C;
+    items.push_back(Item{C, true, s.labC, nullptr, off});
+    off = align256(off + (size_t)c.nelems * (c.dtype == TK_C64 ? 16 : 8));
+    alive[i] = false;
+    alive.push_back(true);
+    steps.push_back(s);
+  }
   auto contract_pair = [&](int a, int b) {
-    Step s{a, b, items[a].lab, items[b].lab, {}, 0, false};
+    Step s{a, b, items[a].lab, items[b].lab, {}, 0, false, {}, {}, {}, {}};
     std::vector<int32_t> oa, ob;
     for (int32_t x : s.labA)
       if (std::find(s.labB.begin(), s.labB.end(), x) == s.labB.end()) oa.push_back(x);
@@ -208,6 +249,15 @@ tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data,
   for (size_t k = 0; k < steps.size(); ++k) {
     const Step& s = steps[k];
     Item& ia = items[s.a];
+    if (s.b < 0) {  // partial trace of an input tensor
+      Item& ic = items[n + k];
+      const void* a = ia.data ? ia.data : (const void*)(w + ia.off);
+      tk_status st = tk_trace(ia.t, a, s.pt.data(), s.qt.data(), (int32_t)s.pt.size(), s.p.data(), (int32_t)s.p.size(),
+                              s.q.data(), (int32_t)s.q.size(), ic.t, w + ic.off, 1.0, 0.0, w + inter, ws_bytes - inter,
+                              stream);
+      if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+      continue;
+    }
     Item& ib = items[s.b];
     const void* a = ia.data ? ia.data : (const void*)(w + ia.off);
     const void* b = ib.data ? ib.data : (const void*)(w + ib.off);

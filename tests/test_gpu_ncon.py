@@ -19,7 +19,26 @@ TOL = 1e-12
 
 
 def oracle_ncon(kind, specs, denses, labels, order, n_cod_out):
-    items = [(s["cod"], s["dom"], D, list(l)) for s, D, l in zip(specs, denses, labels)]
+    items = []
+    for s, D, l in zip(specs, denses, labels):
+        l = list(l)
+        rep = [x for x in set(l) if l.count(x) == 2]
+        if rep:  # partial trace first (Alg. 3), remaining legs keep their side and order
+            N1 = len(s["cod"])
+            legs = s["cod"] + s["dom"]
+            pt, qt = [], []
+            for x in rep:
+                i, j = [k for k, y in enumerate(l) if y == x]
+                ket_i = not (legs[i]["dual"] ^ (i >= N1))
+                pt.append(i if ket_i else j)
+                qt.append(j if ket_i else i)
+            keep = [k for k in range(len(l)) if l[k] not in rep]
+            p = [k for k in keep if k < N1]
+            q = [k for k in keep if k >= N1]
+            D, c2, d2 = OC.partial_trace_dense(D, s["cod"], s["dom"], pt, qt, p, q)
+            s = {"cod": c2, "dom": d2}
+            l = [l[k] for k in p + q]
+        items.append((s["cod"], s["dom"], D, l))
     alive = [True] * len(items)
     m = sum(1 for l in labels for x in l if x < 0)
 
@@ -73,7 +92,16 @@ def _network_su2():
     return "SU2", [A, B, M, M], [[-1, 1, 2], [2, -2, 3], [3, 1], [-3, -4]], [2, 3, 1], 2
 
 
-@pytest.mark.parametrize("maker", [_network_cfg2, _network_cfg3, _network_su2], ids=["cfg2", "cfg3", "su2"])
+def _network_trace():
+    V = W.space("U1", [((-1,), 2), ((0,), 3), ((1,), 2)])
+    A = {"cod": [V, V], "dom": [V, V]}
+    B = {"cod": [V], "dom": [V, V]}
+    # A[-1, 1, 2, 1] traces its legs 1 and 3, then meets B[2, -2, -3]
+    return "U1", [A, B], [[-1, 1, 2, 1], [2, -2, -3]], [1, 2], 1
+
+
+@pytest.mark.parametrize("maker", [_network_cfg2, _network_cfg3, _network_su2, _network_trace],
+                         ids=["cfg2", "cfg3", "su2", "trace"])
 def test_ncon_vs_oracle(maker):
     from paper_2508_10076_b200 import tk
     kind, specs, labels, order, n_cod_out = maker()

@@ -395,11 +395,16 @@ def test_ncon_output_and_errors():
     assert C.nelems == C2.nelems and C.info() == C2.info()
     assert tk.tk_ncon_workspace([A, B, M], [[-1, 1, 2], [2, -2, 3], [3, 1]], [2, 3, 1], 1) > 0
     bad = [([[-1, 1, 2], [2, -2, 3], [3, 4]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),    # 4 appears once
-           ([[-1, 1, 1], [2, -2, 3], [3, 2]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),    # trace in one tensor
+           ([[-1, 1, 1], [2, -2, 3], [3, 2, 1]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),  # 1 three times
            ([[-1, 1, 2], [2, -3, 3], [3, 1]], [1, 2, 3], "TK_ERR_MALFORMED_NETWORK"),    # open labels -1, -3
            ([[-1, 1, 2], [2, -2, 3], [3, 1]], [1, 2], "TK_ERR_MALFORMED_NETWORK"),       # order misses 3
            ([[-1, 1, 2], [2, -2, 3], [3, 1]], [1, 2, 9], "TK_ERR_UNKNOWN_LABEL")]        # order names 9
     for labels, order, status in bad:
         with pytest.raises(tk.TKError) as e:
-            tk.tk_ncon_output([A, B, M], labels, order, 1)
+            tk.tk_ncon_output([A, B, M] if len(labels[2]) == 2 else [A, B, A], labels, order, 1)
         assert e.value.status == status, (labels, order)
+    # a label twice on one tensor is a partial trace (done first): A[-1, 1, 1] is the trace over legs 2, 3
+    Ct = tk.tk_ncon_output([A, M], [[-1, 1, 1], [-2, -3]], [1], 1)
+    T1 = tk.tk_trace_output(A, [1], [2], [0], [])
+    Cr = tk.tk_contract_output(T1, [-1], M, [-2, -3], [-1, -2, -3], 1)
+    assert Ct.nelems == Cr.nelems and Ct.info() == Cr.info()
