@@ -173,7 +173,7 @@ tk_status tk_contract_tuples(const tk_tensor* A, const void* a, int32_t conjA, c
 /* ncon-style network contraction (the @tensor network convention):
  * n tensors T[i] with label lists labels[i] (one label per leg, codomain legs first): positive labels
  * are contracted and appear exactly twice -- on two tensors, or twice on one tensor, which is a partial
- * trace (Alg. 3, tk_trace; done first, bosonic and planar kinds, Float64); negative labels -1, -2, ..., -m are the open legs, which become the
+ * trace (Alg. 3, tk_trace; done first, bosonic and planar kinds); negative labels -1, -2, ..., -m are the open legs, which become the
  * output's legs in that order, the first n_cod_out of them its codomain. `order` lists every positive
  * label; the network is contracted pairwise in that order -- each step takes the two tensors holding the
  * next label and contracts all labels they share (tk_contract, reading C2; for fermionic kinds the order
@@ -226,7 +226,7 @@ tk_status tk_svd_extract(const tk_tensor* A, const int32_t* p, int32_t np, const
  * "(a_1 ...; b_1^* ...)"), is contracted with leg qt[i], read as a domain leg; they must be a ket/bra pair
  * of one space (else TK_ERR_SPACE_MISMATCH). (p, q) arrange the remaining legs (indices of A's legs);
  * C's spaces follow the Alg. 2 selection rule (tk_trace_output). Planar kinds (Fib, Ising) need the pairs
- * nested in the cyclic leg order; fermionic kinds -> TK_ERR_UNSUPPORTED; Float64 only. Workspace:
+ * nested in the cyclic leg order; fermionic kinds -> TK_ERR_UNSUPPORTED; Float64 and ComplexF64. Workspace:
  * tk_trace_workspace bytes (A permuted so the pairs close at the tree ends), 256-byte aligned. */
 tk_status tk_trace_output(const tk_tensor* A, const int32_t* pt, const int32_t* qt, int32_t nt, const int32_t* p,
                           int32_t np, const int32_t* q, int32_t nq, tk_tensor** C);

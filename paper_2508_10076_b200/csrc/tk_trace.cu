@@ -40,20 +40,31 @@ struct TraceSrc {
   double coef;
 };
 
-__global__ void __launch_bounds__(256) trace_kernel(const double* __restrict__ At, double* __restrict__ C,
+// V = double (Float64) or double2 (ComplexF64, interleaved; the coefficients are real)
+__device__ __forceinline__ double tr_zero(double) { return 0.0; }
+__device__ __forceinline__ double2 tr_zero(double2) { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double tr_add(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 tr_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double tr_axpy(double c, double x, double y) { return fma(c, x, y); }
+__device__ __forceinline__ double2 tr_axpy(double c, double2 x, double2 y) {
+  return make_double2(fma(c, x.x, y.x), fma(c, x.y, y.y));
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) trace_kernel(const V* __restrict__ At, V* __restrict__ C,
                                                     const TraceDst* __restrict__ dsts,
                                                     const TraceSrc* __restrict__ srcs, double alpha, double beta) {
   const TraceDst d = dsts[blockIdx.x];
   const int64_t n = (int64_t)d.rows * d.cols;
   for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.y * blockDim.x) {
     const int64_t r = e % d.rows, cc = e / d.rows;
-    double acc = 0.0;
+    V acc = tr_zero(V{});
     for (int k = 0; k < d.src_count; ++k) {
       const TraceSrc s = srcs[d.src_begin + k];
       const int64_t base = s.off + r + (int64_t)s.ld * cc;
       int ntot = 1;
       for (int q = 0; q < s.nt; ++q) ntot *= s.T[q];
-      double part = 0.0;
+      V part = tr_zero(V{});
       for (int u = 0; u < ntot; ++u) {  // the diagonal of the traced pairs (mixed radix)
         int rem = u;
         int64_t o = 0;
@@ -62,13 +73,13 @@ __global__ void __launch_bounds__(256) trace_kernel(const double* __restrict__ A
           rem /= s.T[q];
           o += (int64_t)t * s.dstride[q];
         }
-        part += At[base + o];
+        part = tr_add(part, At[base + o]);
       }
-      acc = fma(s.coef, part, acc);
+      acc = tr_axpy(s.coef, part, acc);
     }
-    double* p = C + d.off + r + (int64_t)d.ld * cc;
-    double v = alpha * acc;
-    if (beta != 0.0) v = fma(beta, *p, v);
+    V* p = C + d.off + r + (int64_t)d.ld * cc;
+    V v = tr_axpy(alpha, acc, tr_zero(V{}));
+    if (beta != 0.0) v = tr_axpy(beta, *p, v);
     *p = v;
   }
 }
@@ -124,7 +135,6 @@ const Space* leg_as_dom(const Tensor& A, int i, Space** tmp) {  // (a_1^* ...; b
 TracePlan* get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std::vector<int>& qt,
                           const std::vector<int>& p, const std::vector<int>& q, const Tensor* C) {
   if (kind_fermionic(A.kind)) TK_THROW(TK_ERR_UNSUPPORTED, "tk_trace: fermionic kinds (supertrace) not supported");
-  if (A.dtype != TK_F64) TK_THROW(TK_ERR_UNSUPPORTED, "tk_trace: Float64 only in this build");
   if (pt.size() != qt.size() || pt.size() > (size_t)kTraceMaxPairs)
     TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_trace: 1..4 traced pairs, |pt| == |qt|");
   std::vector<int> pp(p), qq(q);
@@ -149,11 +159,13 @@ TracePlan* get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std
   auto it = g_trace_cache.find(key);
   if (it != g_trace_cache.end()) return it->second.get();
   auto P = std::make_unique<TracePlan>();
-  P->At = permuted_tensor(A, pp, qq, TK_F64);
+  // A~ in the workspace in A's own element type (ComplexF64: interleaved, offsets in complex elements)
+  const int eb = A.dtype == TK_C64 ? 16 : 8;
+  P->At = permuted_tensor(A, pp, qq, A.dtype);
   P->la = pad_layout(*P->At);
-  build_perm_plan(A, pp, qq, *P->At, P->pa, 8, nullptr, &P->la);
+  build_perm_plan(A, pp, qq, *P->At, P->pa, eb, nullptr, &P->la);
   P->pa.identity = false;
-  P->ws_bytes = align256((size_t)P->la.total * 8);
+  P->ws_bytes = align256((size_t)P->la.total * eb);
   if (C) {
     check_target(A, p, q, *C);
     const Tensor& At = *P->At;
@@ -288,11 +300,16 @@ tk_status tk_trace(const tk_tensor* A_, const void* a, const int32_t* pt, const 
     P->uploaded = true;
   }
   reset_launches();
-  run_permute(P->pa, a, ws, 1.0, 0.0, kPermReal, 1.0, st);
+  const bool cx = A.dtype == TK_C64;
+  run_permute(P->pa, a, ws, 1.0, 0.0, cx ? kPermCToC : kPermReal, 1.0, st);
   if (!P->dsts.empty()) {
-    trace_kernel<<<dim3((unsigned)P->dsts.size(), 4), 256, 0, st>>>((const double*)ws, (double*)c,
-                                                                   (const TraceDst*)P->d_dsts.p,
-                                                                   (const TraceSrc*)P->d_srcs.p, alpha, beta);
+    const dim3 grid((unsigned)P->dsts.size(), 4);
+    if (cx)
+      trace_kernel<double2><<<grid, 256, 0, st>>>((const double2*)ws, (double2*)c, (const TraceDst*)P->d_dsts.p,
+                                                 (const TraceSrc*)P->d_srcs.p, alpha, beta);
+    else
+      trace_kernel<double><<<grid, 256, 0, st>>>((const double*)ws, (double*)c, (const TraceDst*)P->d_dsts.p,
+                                                (const TraceSrc*)P->d_srcs.p, alpha, beta);
     check_cuda(cudaGetLastError(), "trace launch");
     add_launches(1);
   }
