@@ -1307,7 +1307,10 @@ __global__ void __launch_bounds__(MbarCfg::THREADS, 1)
 #ifndef TK_SMALL_STAGES
 #define TK_SMALL_STAGES 3
 #endif
-#define TK_SMALL 64, 64, 32, 16, 16, TK_SMALL_STAGES
+#ifndef TK_SMALL_WN
+#define TK_SMALL_WN 16  // warp tile 32 x WN (16: 8 warps per 64 x 64 tile)
+#endif
+#define TK_SMALL 64, 64, 32, TK_SMALL_WN, 16, TK_SMALL_STAGES
 #ifndef TK_SMALL_MINB
 #define TK_SMALL_MINB 2
 #endif
