@@ -1448,26 +1448,35 @@ __global__ void __launch_bounds__(kSkinnyThreads)
 template <int KM, int NM>
 __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
     gather_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                         const GatherTile* __restrict__ tiles, const GatherSeg* __restrict__ segs,
+                         const int64_t* __restrict__ slots, const GatherSeg* __restrict__ segs,
                          const int32_t* __restrict__ btab, double alpha, double beta) {
   constexpr int RPT = gather_rows(KM) / kGatherRows;  // rows per thread
   __shared__ double Bs[kSkinnyMax * kSkinnyMax];
   extern __shared__ __align__(16) double gather_dyn[];
   double (*As)[gather_rows(KM)] = reinterpret_cast<double (*)[gather_rows(KM)]>(gather_dyn);  // [KM][rows]
-  __shared__ __align__(16) GatherSeg ss[gather_seg_cap(KM)];
+  __shared__ __align__(16) GatherSeg sbig[gather_seg_cap(KM)];
+  __shared__ __align__(16) int64_t slot[kGatherSlotWords];
   pdl_trigger();
-  const GatherTile t = tiles[blockIdx.x];
-  const GemmGroup& g = t.g;
   const int tid = threadIdx.x;
-  {
-    const int4* src4 = reinterpret_cast<const int4*>(segs + t.seg0);
-    int4* dst4 = reinterpret_cast<int4*>(ss);
-    for (int i = tid; i < t.nseg * (int)(sizeof(GatherSeg) / 16); i += kGatherRows) dst4[i] = __ldg(src4 + i);
+  {  // the tile's slot: descriptor, first segments, first B~ table entries -- one coalesced copy
+    const int4* src4 = reinterpret_cast<const int4*>(slots + (int64_t)blockIdx.x * kGatherSlotWords);
+    for (int i = tid; i < kGatherSlotWords / 2; i += kGatherRows) reinterpret_cast<int4*>(slot)[i] = __ldg(src4 + i);
   }
-  const int K = g.K, N = g.N;
-  const int be = tid < K * N ? __ldg(btab + t.bt + tid) : -1;  // plan data: before the wait
   for (int i = tid; i < kSkinnyMax * kSkinnyMax; i += kGatherRows) Bs[i] = 0.0;
   __syncthreads();
+  const GatherTile& t = *reinterpret_cast<const GatherTile*>(slot);
+  const GemmGroup& g = t.g;
+  const GatherSeg* ss = reinterpret_cast<const GatherSeg*>(slot + 10);
+  if (t.nseg > kGatherSlotSegs) {  // rare: more segments than the slot holds
+    const int4* src4 = reinterpret_cast<const int4*>(segs + t.seg0);
+    int4* dst4 = reinterpret_cast<int4*>(sbig);
+    for (int i = tid; i < t.nseg * (int)(sizeof(GatherSeg) / 16); i += kGatherRows) dst4[i] = __ldg(src4 + i);
+    __syncthreads();
+    ss = sbig;
+  }
+  const int K = g.K, N = g.N;
+  const int32_t* sbt = reinterpret_cast<const int32_t*>(slot + 10 + 16 * kGatherSlotSegs);
+  const int be = tid < K * N ? (K * N <= kGatherSlotB ? sbt[tid] : __ldg(btab + t.bt + tid)) : -1;
   pdl_wait();
   // A~ rows first (cp.async, nothing held in registers), then the B~ block, then one wait for both
   uint32_t neg[RPT];
@@ -1533,7 +1542,7 @@ __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
   }
 }
 
-cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const GatherTile* tiles, int ntiles,
+cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const int64_t* slots, int ntiles,
                                const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
                                double beta, cudaStream_t st) {
   if (!ntiles) return cudaSuccess;
@@ -1546,7 +1555,7 @@ cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, cons
       cudaFuncSetAttribute(gather_skinny_kernel<KM, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
       set = true;                                                                                                 \
     }                                                                                                             \
-    launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, smem, st, A, B, C, tiles, segs, btab, alpha, beta); \
+    launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, smem, st, A, B, C, slots, segs, btab, alpha, beta); \
   }                                                                                                               \
   break;
   switch (kc * 3 + nc) {

@@ -179,7 +179,13 @@ struct GatherTile {
                        // + (coefficient < 0), or -1 for a structural zero): B needs no permute pass either
   GemmGroup g;
 };
-cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const GatherTile* tiles, int ntiles,
+// Per-tile slot (kGatherSlotWords 8-byte words): the GatherTile, its first kGatherSlotSegs segments and
+// the first kGatherSlotB entries of its B~ table, so a tile's descriptors arrive in one coalesced copy;
+// tiles with more segments / entries read the rest from `segs` / `btab`.
+constexpr int kGatherSlotSegs = 8, kGatherSlotB = 64;
+constexpr int kGatherSlotWords = 10 + 16 * kGatherSlotSegs + kGatherSlotB / 2;
+static_assert(sizeof(GatherTile) == 80 && kGatherSlotWords % 2 == 0, "gather slot layout");
+cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const int64_t* slots, int ntiles,
                                const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
                                double beta, cudaStream_t st);
 

@@ -658,8 +658,9 @@ struct ContractPlan {
   std::vector<GatherSeg> gsegs;
   std::vector<GatherTile> gtiles;
   std::vector<int32_t> btab;
+  std::vector<int64_t> gslots;
   int g_kmax = 0, g_nmax = 0;
-  DevBuf d_gsegs, d_gtiles, d_btab;
+  DevBuf d_gsegs, d_btab, d_gslots;
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
   bool uploaded = false;
@@ -678,8 +679,8 @@ struct ContractPlan {
     d_heads.upload(split_heads);
     d_jobs_ab.upload(jobs_ab);
     d_gsegs.upload(gsegs);
-    d_gtiles.upload(gtiles);
     d_btab.upload(btab);
+    d_gslots.upload(gslots);
     uploaded = true;
   }
 };
@@ -998,6 +999,17 @@ static void build_gather(const Tensor& A, ContractPlan& P) {
     }
     if (ti != tiles.size()) return;
   }
+  // per-tile slots (GatherTile | first kGatherSlotSegs segments | first kGatherSlotB table entries)
+  std::vector<int64_t> slots((size_t)tiles.size() * kGatherSlotWords, 0);
+  for (size_t ti = 0; ti < tiles.size(); ++ti) {
+    const GatherTile& t = tiles[ti];
+    int64_t* w = slots.data() + ti * kGatherSlotWords;
+    std::memcpy(w, &t, sizeof(GatherTile));
+    std::memcpy(w + 10, segs.data() + t.seg0, sizeof(GatherSeg) * std::min(t.nseg, kGatherSlotSegs));
+    int32_t* bw = reinterpret_cast<int32_t*>(w + 10 + 16 * kGatherSlotSegs);
+    for (int e = 0; e < std::min(t.g.K * t.g.N, kGatherSlotB); ++e) bw[e] = btab[t.bt + e];
+  }
+  P.gslots = std::move(slots);
   P.gather = true;
   P.btab = std::move(btab);
   P.gsegs = std::move(segs);
@@ -1471,7 +1483,7 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
     g_launches += (P->ntiles_big > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0) + !P->split_heads.empty();
   }
   if (P->gather) {
-    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const GatherTile*)P->d_gtiles.p,
+    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const int64_t*)P->d_gslots.p,
                                   (int)P->gtiles.size(), (const GatherSeg*)P->d_gsegs.p, (const int32_t*)P->d_btab.p,
                                   P->g_kmax, P->g_nmax, ga, gb, st),
                "gather gemm launch");
