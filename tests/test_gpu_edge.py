@@ -188,3 +188,17 @@ def test_gather_gemm_alpha_beta_and_output_permute(cfgfun, kind):
     lc3 = [lc2[2], lc2[0], lc2[4], lc2[1], lc2[3]]
     got, want, _ = _run(kind, T1, la2, specs[nb2], lb2, lc3, 2, alpha=2.0, beta=-1.0, seed=12)
     _check(got, want)
+
+
+# ------------------------------------------------------------------ recoupling groups of > 4 sources
+def test_recoupling_staged_path():
+    """SU(2) rank-4 permutes with spins up to 2 have recoupling groups of up to 5 source trees; groups
+    of more than 4 sources take the staged-shared-memory recoupling kernel (the rest run in the general
+    permute launch). Checked against the dense oracle."""
+    from tests.test_gpu_parity import _perm_case
+    secs = [((0,), 2), ((1,), 1), ((2,), 2), ((3,), 1), ((4,), 2)]
+    for p, q, beta in (([2, 0], [3, 1], 0.0), ([3, 1, 0], [2], 0.5), ([1, 3], [0, 2], 0.0)):
+        assert _perm_case("SU2", secs, [0, 0], [0, 0], p, q, alpha=-1.5, beta=beta) <= TOL, (p, q)
+    # fZ2 x SU(2) x SU(2): fermionic signs and two recoupled factors
+    secs2 = [((0, 0), 1), ((1, 1), 1), ((0, 2), 1), ((2, 0), 1), ((1, 3), 1), ((2, 2), 1)]
+    assert _perm_case("fSU2xSU2", secs2, [0, 0], [0, 0], [2, 0], [3, 1]) <= TOL
