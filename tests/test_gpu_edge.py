@@ -202,3 +202,14 @@ def test_recoupling_staged_path():
     # fZ2 x SU(2) x SU(2): fermionic signs and two recoupled factors
     secs2 = [((0, 0), 1), ((1, 1), 1), ((0, 2), 1), ((2, 0), 1), ((1, 3), 1), ((2, 2), 1)]
     assert _perm_case("fSU2xSU2", secs2, [0, 0], [0, 0], [2, 0], [3, 1]) <= TOL
+
+
+def test_large_permute_all_job_classes():
+    """A 24 M-element permute (>= 2^24: one launch per job class) whose sectors range from degeneracy 1 to
+    28, so rows, smem-tiled and packed jobs all occur (TK_PLAN_DEBUG), each pattern against the dense
+    oracle (1.9 GB dense arrays on the host)."""
+    from tests.test_gpu_parity import _perm_case
+    secs = [((-6,), 1), ((-5,), 1), ((-4,), 2), ((-3,), 8), ((-2,), 14), ((-1,), 22), ((0,), 28), ((1,), 22),
+            ((2,), 14), ((3,), 8), ((4,), 2), ((5,), 1), ((6,), 1)]
+    for p, q in (([0, 2], [1, 3]), ([2, 0], [1, 3]), ([3, 1], [0, 2])):
+        assert _perm_case("U1", secs, [0, 0], [0, 0], p, q, beta=0.5) <= TOL, (p, q)
