@@ -213,3 +213,15 @@ def test_large_permute_all_job_classes():
             ((2,), 14), ((3,), 8), ((4,), 2), ((5,), 1), ((6,), 1)]
     for p, q in (([0, 2], [1, 3]), ([2, 0], [1, 3]), ([3, 1], [0, 2])):
         assert _perm_case("U1", secs, [0, 0], [0, 0], p, q, beta=0.5) <= TOL, (p, q)
+
+
+def test_gather_gemm_wide_k():
+    """The gathered GEMM's K = 9..16 instance (K and N of 12 / 10): A (V, w ; V) contracted over w with
+    B (w' ; w), so every block is skinny and the operand permute is folded into the GEMM."""
+    V = W.space("U1", [((q,), d) for q, d in zip(range(-3, 4), [6, 11, 17, 20, 17, 11, 6])])
+    w = W.space("U1", [((0,), 12), ((1,), 10)])
+    A = {"cod": [V, w], "dom": [V]}
+    B = {"cod": [w], "dom": [w]}
+    for alpha, beta in ((1.0, 0.0), (-2.0, 0.5)):
+        got, want, _ = _run("U1", A, [1, 2, 3], B, [4, 2], [1, 3, 4], 2, alpha=alpha, beta=beta, seed=3)
+        _check(got, want)
