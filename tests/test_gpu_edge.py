@@ -225,3 +225,21 @@ def test_gather_gemm_wide_k():
     for alpha, beta in ((1.0, 0.0), (-2.0, 0.5)):
         got, want, _ = _run("U1", A, [1, 2, 3], B, [4, 2], [1, 3, 4], 2, alpha=alpha, beta=beta, seed=3)
         _check(got, want)
+
+
+def test_splitk_alpha_beta():
+    """The T3.R step of cfg2 runs split-K (partial tiles + ordered reduction): alpha / beta are applied by
+    the reduction kernel; also with an output permute after it."""
+    cfg = W.cfg2(chi=512)
+    specs = {k: v[0] for k, v in cfg["tensors"].items()}
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"][:3]:
+        cod, dom = OC.output_spaces(specs[na]["cod"], specs[na]["dom"], specs[nb]["cod"], specs[nb]["dom"],
+                                    la, lb, lc, ncod)
+        specs[nc] = {"cod": cod, "dom": dom}
+    (na, la, nb, lb, nc, lc, ncod) = cfg["steps"][3]
+    for alpha, beta in ((1.0, 0.0), (0.5, -1.25)):
+        got, want, _ = _run("U1", specs[na], la, specs[nb], lb, lc, ncod, alpha=alpha, beta=beta, seed=9)
+        _check(got, want)
+    lc2 = [lc[3], lc[0], lc[2], lc[1]]
+    got, want, _ = _run("U1", specs[na], la, specs[nb], lb, lc2, 2, alpha=-1.0, beta=0.5, seed=10)
+    _check(got, want)
