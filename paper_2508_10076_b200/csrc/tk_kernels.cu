@@ -1437,11 +1437,11 @@ __global__ void __launch_bounds__(kSkinnyThreads)
   }
 }
 
-// ---- gathered skinny GEMM (GatherSeg in tk_kernels.hpp): one thread per row of A~^c. The tile's
-// subblock descriptors are staged in shared memory before griddepcontrol.wait (plan data); each thread
-// then issues its row's K element loads from A with cp.async into As[k][thread] (all in flight at
-// once, no registers held), waits for its own copies only, and computes its C~ row against the
-// K x N block of B~ in shared memory.
+// ---- gathered skinny GEMM (GatherSeg in tk_kernels.hpp): one thread per row (two for K <= 8) of
+// A~^c. The tile's slot -- descriptor, subblock segments, B~ table -- is copied into shared memory
+// before griddepcontrol.wait (plan data); each thread then issues its rows' K element loads from A with
+// cp.async into As[k][row] (all in flight at once, no registers held) and the K x N block of B~ is
+// gathered from B through the table; after one wait every thread computes its C~ rows.
 #ifndef TK_GATHER_MINB
 #define TK_GATHER_MINB 3
 #endif
