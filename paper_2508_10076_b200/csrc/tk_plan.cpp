@@ -1156,7 +1156,8 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
     int slot = 0;
     for (const GemmTile& t : small) {
       const int K = t.k1;
-      const int S = std::min(std::min(want, K / 64), 16);  // kSplitMax in the reduction kernel
+      static const int min_chunk = getenv("TK_SPLIT_CHUNK") ? atoi(getenv("TK_SPLIT_CHUNK")) : 64;
+      const int S = std::min(std::min(want, K / min_chunk), 16);  // kSplitMax in the reduction kernel
       if (S < 2) {
         out.push_back(t);
         continue;
