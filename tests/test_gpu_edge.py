@@ -243,3 +243,17 @@ def test_splitk_alpha_beta():
     lc2 = [lc[3], lc[0], lc[2], lc[1]]
     got, want, _ = _run("U1", specs[na], la, specs[nb], lb, lc2, 2, alpha=-1.0, beta=0.5, seed=10)
     _check(got, want)
+
+
+# ------------------------------------------------------------------ determinism
+@pytest.mark.parametrize("cfgfun", [lambda: W.cfg2(chi=512), lambda: W.cfg3(chi=512), lambda: W.cfg7(n_mult=100)],
+                         ids=["cfg2", "cfg3", "cfg7"])
+def test_bitwise_deterministic(cfgfun):
+    """No atomics anywhere on the path (split-K sums its partial tiles in a fixed order): two runs of a
+    chain give bit-identical results."""
+    from tests import harness as H
+    cfg = cfgfun()
+    r1 = H.gpu_chain(cfg)
+    r2 = H.gpu_chain(cfg)
+    for k in r1:
+        assert np.array_equal(r1[k][1], r2[k][1]), k
