@@ -74,6 +74,9 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 #ifndef TK_ROWS_MINB
 #define TK_ROWS_MINB 6  // Float64 rows-only permute: 6 CTAs/SM (<= 40 registers): cfg4 5.41 vs 5.24 TB/s at 5
 #endif
+#ifndef TK_ROWS_MINB_C
+#define TK_ROWS_MINB_C TK_PERM_MINB  // ComplexF64 rows-only instances
+#endif
 #ifndef TK_ROWS_U
 #define TK_ROWS_U 8  // loads in flight per thread in the rows path (Float64)
 #endif
@@ -699,7 +702,7 @@ union PermSharedAll {
 // ROWS_ONLY: a launch whose jobs are all rows jobs (the large cfg4 permutes) uses a leaner instance
 // (48 registers instead of 64; measured 5.0 vs 4.6 TB/s on cfg4).
 template <int CM, bool ROWS_ONLY>
-__global__ void __launch_bounds__(kPermThreads, (ROWS_ONLY && CM == kPermReal) ? TK_ROWS_MINB : TK_PERM_MINB)
+__global__ void __launch_bounds__(kPermThreads, ROWS_ONLY ? (CM == kPermReal ? TK_ROWS_MINB : TK_ROWS_MINB_C) : TK_PERM_MINB)
     permute_kernel(PermOp op0, PermOp op1, const PermJob* __restrict__ jobs) {
   using IO = CIO<CM>;
   __shared__ __align__(16) typename std::conditional<ROWS_ONLY, PermShared, PermSharedAll>::type sh_;
