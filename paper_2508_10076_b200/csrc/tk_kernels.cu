@@ -1411,7 +1411,10 @@ __device__ __forceinline__ void skinny_rows(const double* __restrict__ Ag, doubl
   }
 }
 
-__global__ void __launch_bounds__(kSkinnyThreads)
+#ifndef TK_SKINNY_MINB
+#define TK_SKINNY_MINB 1
+#endif
+__global__ void __launch_bounds__(kSkinnyThreads, TK_SKINNY_MINB)
     gemm_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                        const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
                        double beta) {
