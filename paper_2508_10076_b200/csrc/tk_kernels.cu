@@ -1411,10 +1411,11 @@ __device__ __forceinline__ void skinny_rows(const double* __restrict__ Ag, doubl
   }
 }
 
-#ifndef TK_SKINNY_MINB
-#define TK_SKINNY_MINB 1
-#endif
+#ifdef TK_SKINNY_MINB  // A/B knob; the default leaves the register choice to ptxas (82 registers)
 __global__ void __launch_bounds__(kSkinnyThreads, TK_SKINNY_MINB)
+#else
+__global__ void __launch_bounds__(kSkinnyThreads)
+#endif
     gemm_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                        const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
                        double beta) {
