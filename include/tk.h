@@ -36,13 +36,23 @@
  * Ownership: tk_space / tk_tensor are immutable, reference-counted host objects; a tensor
  * retains its spaces. All tensor DATA lives in caller-owned device memory (e.g. PyTorch
  * tensors passed as raw pointers); the caller also provides the workspace. The library's
- * only device allocations are the small per-plan descriptor tables, owned by the plan cache
- * (freed by tk_cache_clear). Float64 data is double[]; ComplexF64 is interleaved (re, im).
- * Data pointers must be 8-byte aligned; workspace pointers 256-byte aligned.
+ * only device allocations are the small per-plan descriptor tables, owned by the plan cache.
+ * Plans are memoised per (structure, labels, device) in a mutex-guarded, bounded LRU cache
+ * (P:1547-1549); a plan's tables are uploaded once, on the device that is current when the
+ * plan is first used, in a capture-safe way (relaxed capture mode, a private stream), so the
+ * first tk_contract of a new pattern may run inside CUDA-graph capture. A graph captured from
+ * tk_* calls references those tables: do not call tk_cache_clear (which frees them) while such
+ * a graph is still replayed, nor while another thread is capturing. Layout and workspace
+ * queries (tk_*_output, tk_*_workspace) need no device. Float64 data is double[]; ComplexF64
+ * is interleaved (re, im). Data pointers must be 8-byte aligned; workspace pointers 256-byte
+ * aligned. The C ABI cannot check buffer sizes: data buffers must hold tk_tensor_nelems
+ * elements and the workspace the bytes tk_*_workspace returned.
  *
- * Errors: every call returns a tk_status; on error nothing is launched and no output is
- * touched; tk_last_error() returns a thread-local message. Kernels run asynchronously on
- * the given stream; launch failures map to TK_ERR_CUDA.
+ * Errors: every call returns a tk_status; tk_last_error() returns a thread-local message.
+ * Validation errors (every status but TK_ERR_CUDA) are raised before anything is launched, so
+ * outputs are untouched. Kernels run asynchronously on the given stream; a failing launch maps
+ * to TK_ERR_CUDA (the launch's own status, not an unrelated earlier error) and may leave the
+ * earlier launches of the same call enqueued, i.e. the output is then unspecified.
  */
 #ifndef TK_H_
 #define TK_H_
@@ -270,7 +280,10 @@ tk_status tk_permute_transfer_planar(const tk_tensor* A, const int32_t* p, int32
                                      int32_t nq, const tk_tensor* C, int32_t kappa_mode, double* out);
 
 const char* tk_last_error(void);
+/* Frees every memoised plan (contraction, permute, trace, SVD) and its device tables. */
 void tk_cache_clear(void);
+/* Number of memoised plans currently held (all caches; each cache is a bounded LRU). */
+int64_t tk_cache_size(void);
 const char* tk_version(void);
 
 #ifdef __cplusplus

@@ -3,6 +3,7 @@
 #include <array>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -21,6 +22,23 @@ struct Error : std::runtime_error {
 };
 void set_last_error(const std::string& m);
 #define TK_THROW(code, msg) throw ::tk::Error((code), (msg))
+
+// Tuning knobs used for A/B experiments (job sizes, kernel-class thresholds). A product build compiles
+// them to their defaults; only a build with -DTK_DEBUG_KNOBS (tools/build_variant.sh) reads the
+// environment, so no environment variable can silently change kernel selection in the shipped library.
+#ifdef TK_DEBUG_KNOBS
+inline long long knob(const char* name, long long dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+#else
+inline constexpr long long knob(const char*, long long dflt) { return dflt; }
+#endif
+// Diagnostic output only (plan statistics on stderr; never changes what runs): TK_PLAN_DEBUG=1.
+inline bool plan_debug() {
+  static const bool on = std::getenv("TK_PLAN_DEBUG") != nullptr;
+  return on;
+}
 
 // ------------------------------------------------------------------ sectors
 // Sector kinds (P:1011-1022 Z2; P:2347-2362 SVect; U1 S:138; Deligne products P:2380-2412;

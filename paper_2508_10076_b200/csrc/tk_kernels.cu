@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "tk_internal.hpp"
 #include "tk_kernels.hpp"
 
 namespace tk {
@@ -388,26 +389,12 @@ __device__ __forceinline__ void load_job_header(const PermGroup& g, const PermMe
   __syncthreads();
 }
 
-// cudaLaunchKernelEx with the programmatic-stream-serialization attribute (PDL); TK_NO_PDL=1 disables it
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute (PDL); returns the launch's
+// own status (never cudaGetLastError, which would also report and clear unrelated earlier errors)
 template <typename... KArgs, typename... Args>
-static void launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
-  static const bool pdl = getenv("TK_NO_PDL") == nullptr;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3((unsigned)block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
-template <typename... KArgs, typename... Args>
-static void launch_k2(void (*kern)(KArgs...), dim3 grid, int block, size_t smem, cudaStream_t st, Args... args) {
-  static const bool pdl = getenv("TK_NO_PDL") == nullptr;
+static cudaError_t launch_k2(void (*kern)(KArgs...), dim3 grid, int block, size_t smem, cudaStream_t st,
+                             Args... args) {
+  static const bool pdl = knob("TK_NO_PDL", 0) == 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3((unsigned)block);
@@ -418,7 +405,11 @@ static void launch_k2(void (*kern)(KArgs...), dim3 grid, int block, size_t smem,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  return launch_k2(kern, dim3((unsigned)grid), block, smem, st, args...);
 }
 
 // packed jobs of small single-member rows groups (see kPackGroups): per CTA, the groups' row tables
@@ -740,117 +731,6 @@ __global__ void __launch_bounds__(kPermThreads, ROWS_ONLY ? (CM == kPermReal ? T
     permute_rows<CM>(src, dst, g, job, sh, op.alpha, op.beta, op.ims);
 }
 
-// Box jobs (mode 2, large permutes whose leg 0 stays unit-stride on both sides but whose next legs
-// differ: the cfg4 operand and output permutes). A box n0 x m1 x m2 is contiguous along (leg 0, leg 2)
-// in the source -- m1 runs of n0*m2 elements -- and along (leg 0, leg 1) in the destination -- m2 runs
-// of n0*m1 -- so staging it in shared memory turns ~144-byte rows into runs of several KB on both
-// sides. A job is `count` consecutive boxes of one group; box u+1 streams in with cp.async (no
-// registers held) while box u is written out from the other buffer, so loads stay in flight through
-// the store phase. S[i1 * P1 + i2 * n0 + i0], plane pitch P1 = n0*m2 | 1.
-constexpr int kBoxBuf = kBoxElems + 64;  // doubles per buffer (a box plus its odd-pitch padding)
-template <int CM>
-__global__ void __launch_bounds__(kPermThreads, 3) permute_box_kernel(PermOp op, const PermJob* __restrict__ jobs) {
-  using IO = CIO<CM>;
-  using V = typename IO::V;
-  extern __shared__ __align__(16) unsigned char box_dyn[];
-  constexpr int kBuf = kBoxBuf * 8 / (int)sizeof(V);
-  V* S0 = reinterpret_cast<V*>(box_dyn);
-  pdl_trigger();
-  const PermJob job = jobs[blockIdx.x];
-  const PermGroup& g = op.groups[job.group];
-  const PermMember ms = op.members[g.src_mem], md = op.members[g.dst_mem];
-  const auto* src = (const typename IO::S*)op.src;
-  auto* dst = (typename IO::D*)op.dst;
-  const double c = op.alpha * op.coefs[g.coef_off];
-  const int tid = threadIdx.x;
-  const int n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
-  const int c1 = g.ct, c2 = g.R, T0 = g.T0, Tt = g.Tt;
-  const int64_t s1 = g.sa[1] + ms.ld * g.sb[1], d2 = g.da[2] + md.ld * g.db[2];
-  struct Box {
-    int64_t sbase, dbase;
-    int m1, m2;
-  };
-  auto box = [&](int64_t bb) {  // box index of a group < 2^31 (host-checked): 32-bit decode
-    uint32_t b = (uint32_t)bb;
-    const int b1 = (int)(b % (uint32_t)T0);
-    b /= (uint32_t)T0;
-    const int b2 = (int)(b % (uint32_t)Tt);
-    uint32_t rest = b / (uint32_t)Tt;
-    Box x{ms.off, md.off, 0, 0};
-    for (int l = 3; l < g.ndim; ++l) {
-      const uint32_t e = (uint32_t)g.ext[l], q = rest / e, i = rest - q * e;
-      rest = q;
-      x.sbase += (int64_t)i * (g.sa[l] + ms.ld * g.sb[l]);
-      x.dbase += (int64_t)i * (g.da[l] + md.ld * g.db[l]);
-    }
-    const int i1b = b1 * c1, i2b = b2 * c2;
-    x.m1 = min(c1, n1 - i1b);
-    x.m2 = min(c2, n2 - i2b);
-    x.sbase += (int64_t)i1b * s1 + (int64_t)i2b * n0;  // leg 2: source stride n0
-    x.dbase += (int64_t)i1b * n0 + (int64_t)i2b * d2;  // leg 1: destination stride n0
-    return x;
-  };
-  auto fetch = [&](const Box& x, V* S) {  // source runs: i1 major, contiguous over r = i2 * n0 + i0
-    const uint32_t Ls = (uint32_t)n0 * x.m2, tot = Ls * x.m1, P1 = Ls | 1;
-    FastDiv fs;
-    fs.init(Ls);
-    uint32_t i1 = fs.div((uint32_t)tid), r = tid - i1 * Ls;
-    const uint32_t qs = kPermThreads / Ls, rs_ = kPermThreads - qs * Ls;
-    for (uint32_t e = tid; e < tot; e += kPermThreads) {
-      stage_elem<CM>(S + i1 * P1 + r, src + x.sbase + (int64_t)i1 * s1 + r, ms.d1);
-      r += rs_;
-      i1 += qs;
-      if (r >= Ls) {
-        r -= Ls;
-        ++i1;
-      }
-    }
-  };
-  pdl_wait();  // tensor data only after the preceding grid has completed (PDL)
-  Box cur = box(job.first);
-  fetch(cur, S0);
-  cp_async_commit();
-  for (int u = 0; u < job.count; ++u) {
-    Box nxt{};
-    if (u + 1 < job.count) {
-      nxt = box(job.first + u + 1);
-      fetch(nxt, S0 + ((u + 1) & 1) * kBuf);
-    }
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();  // box u landed for all threads
-    const V* S = S0 + (u & 1) * kBuf;
-    // destination runs: i2 major, contiguous over rr = i1 * n0 + i0; per-thread (i2, i1, i0) walked
-    // incrementally (stride kPermThreads), no division per element
-    const uint32_t Ls = (uint32_t)n0 * cur.m2, Ld = (uint32_t)n0 * cur.m1, tot = Ld * cur.m2, P1 = Ls | 1;
-    FastDiv fd, f0;
-    fd.init(Ld);
-    f0.init((uint32_t)n0);
-    uint32_t i2 = fd.div((uint32_t)tid), rr = tid - i2 * Ld;
-    uint32_t i1 = f0.div(rr), i0 = rr - i1 * (uint32_t)n0;
-    const uint32_t q2 = kPermThreads / Ld, r2 = kPermThreads - q2 * Ld;
-    const uint32_t q0 = r2 / (uint32_t)n0, r0 = r2 - q0 * (uint32_t)n0;
-    for (uint32_t e = tid; e < tot; e += kPermThreads) {
-      IO::store(dst, cur.dbase + (int64_t)i2 * d2 + i1 * (uint32_t)n0 + i0, md.d1, md.d2,
-                Num<V>::scale(c, S[i1 * P1 + i2 * (uint32_t)n0 + i0]), op.beta, op.ims);
-      // advance rr by r2 (carrying into i2), i.e. (i1, i0) by (q0, r0) within the run
-      i2 += q2;
-      i0 += r0;
-      i1 += q0;
-      if (i0 >= (uint32_t)n0) {
-        i0 -= n0;
-        ++i1;
-      }
-      if (i1 >= (uint32_t)cur.m1) {
-        i1 -= cur.m1;
-        ++i2;
-      }
-    }
-    __syncthreads();  // buffer u & 1 is refilled by iteration u + 1's prefetch
-    cur = nxt;
-  }
-}
-
 // rows jobs of recoupling groups (SU(2): k_src x k_dst coefficient matrix in flight). The job's source
 // elements of all k_src members are staged in shared memory with cp.async -- one round trip for the
 // whole job instead of a chain of dependent loads per element (the sum over sources used to wait on
@@ -928,48 +808,43 @@ __global__ void __launch_bounds__(kPermThreads, 3)
 }
 
 template <int CM>
-static void launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int njobs, int njobs_multi, bool tiled,
-                              int variant, cudaStream_t st) {
+static cudaError_t set_permute_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(permute_kernel<CM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kTileElems * (int)sizeof(typename CIO<CM>::V));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(permute_recouple_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kRecoupleStage * 8);
+  return e;
+}
+
+template <int CM>
+static cudaError_t launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs, int njobs, int njobs_multi,
+                                     bool tiled, int variant, cudaStream_t st) {
   const int smem = tiled ? kTileElems * (int)sizeof(typename CIO<CM>::V) : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(permute_kernel<CM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kTileElems * (int)sizeof(typename CIO<CM>::V));
-    attr = true;
-  }
-  if (njobs && variant == kLaunchRowsOnly) launch_k(permute_kernel<CM, true>, njobs, kPermThreads, 0, st, op0, op1, jobs);
-  if (njobs && variant == kLaunchBox) {
-    constexpr int smem = 2 * kBoxBuf * 8;
-    static bool battr = false;
-    if (!battr) {
-      cudaFuncSetAttribute(permute_box_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      battr = true;
-    }
-    launch_k(permute_box_kernel<CM>, njobs, kPermThreads, smem, st, op0, jobs);
-  }
-  if (njobs && variant == kLaunchGeneral) launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
-  if (njobs_multi) {
-    constexpr int rsmem = kRecoupleStage * 8;
-    static bool rattr = false;
-    if (!rattr) {
-      cudaFuncSetAttribute(permute_recouple_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
-      rattr = true;
-    }
-    launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, rsmem, st, op0, op1, jobs + njobs);
-  }
+  cudaError_t e = cudaSuccess;
+  if (njobs && variant == kLaunchRowsOnly)
+    e = launch_k(permute_kernel<CM, true>, njobs, kPermThreads, 0, st, op0, op1, jobs);
+  if (e == cudaSuccess && njobs && variant == kLaunchGeneral)
+    e = launch_k(permute_kernel<CM, false>, njobs, kPermThreads, smem, st, op0, op1, jobs);
+  if (e == cudaSuccess && njobs_multi)
+    e = launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, kRecoupleStage * 8, st, op0, op1,
+                 jobs + njobs);
+  return e;
 }
 
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
                            bool tiled, int variant, int cm, cudaStream_t st) {
   switch (cm) {
-    case kPermReal: launch_permute_cm<kPermReal>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
-    case kPermCToC: launch_permute_cm<kPermCToC>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
-    case kPermCToPlanar: launch_permute_cm<kPermCToPlanar>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
-    case kPermCToRealRep: launch_permute_cm<kPermCToRealRep>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
-    case kPermPlanarToC: launch_permute_cm<kPermPlanarToC>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st); break;
+    case kPermReal: return launch_permute_cm<kPermReal>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st);
+    case kPermCToC: return launch_permute_cm<kPermCToC>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st);
+    case kPermCToPlanar:
+      return launch_permute_cm<kPermCToPlanar>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st);
+    case kPermCToRealRep:
+      return launch_permute_cm<kPermCToRealRep>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st);
+    case kPermPlanarToC:
+      return launch_permute_cm<kPermPlanarToC>(op0, op1, jobs, njobs, njobs_multi, tiled, variant, st);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- grouped FP64 GEMM (DMMA)
@@ -1553,22 +1428,20 @@ __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
   }
 }
 
+template <int KM, int NM>
+static cudaError_t set_gather_attr() {
+  return cudaFuncSetAttribute(gather_skinny_kernel<KM, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              KM * gather_rows(KM) * 8);
+}
+
 cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const int64_t* slots, int ntiles,
                                const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
                                double beta, cudaStream_t st) {
   if (!ntiles) return cudaSuccess;
   const int kc = kmax <= 4 ? 0 : (kmax <= 8 ? 1 : 2), nc = nmax <= 4 ? 0 : (nmax <= 8 ? 1 : 2);
-#define TK_GATHER(KM, NM)                                                                                       \
-  {                                                                                                               \
-    constexpr int smem = KM * gather_rows(KM) * 8;                                                                \
-    static bool set = false;                                                                                      \
-    if (!set) {                                                                                                   \
-      cudaFuncSetAttribute(gather_skinny_kernel<KM, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
-      set = true;                                                                                                 \
-    }                                                                                                             \
-    launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, smem, st, A, B, C, slots, segs, btab, alpha, beta); \
-  }                                                                                                               \
-  break;
+#define TK_GATHER(KM, NM)                                                                               \
+  return launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, KM * gather_rows(KM) * 8, st, A, B, C, \
+                  slots, segs, btab, alpha, beta);
   switch (kc * 3 + nc) {
     case 0: TK_GATHER(4, 4)
     case 1: TK_GATHER(4, 8)
@@ -1581,33 +1454,55 @@ cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, cons
     default: TK_GATHER(16, 16)
   }
 #undef TK_GATHER
-  return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, int ntiles_skinny, const GemmTile* split_heads,
                         int nsplit_heads, double* parts, double alpha, double beta, cudaStream_t st) {
   // big tiles: mbarrier pipeline, 16 warps of 32x32 on 128x128, BK 16, 6 stages, prefetch distance 2
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_mbar_kernel<TK_MBAR_PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMbarSmem);
-    cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
-    attr = true;
-  }
   const int base_vec = ((((uintptr_t)A) | ((uintptr_t)B)) & 15) == 0;
+  cudaError_t e = cudaSuccess;
   if (ntiles_big)
-    launch_k(gemm_mbar_kernel<TK_MBAR_PD>, ntiles_big, MbarCfg::THREADS, kMbarSmem, st, A, B, C, groups, tiles, alpha, beta,
-             base_vec);
-  if (ntiles_small)
-    launch_k(gemm_small_kernel, ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C, groups,
-             tiles + ntiles_big, alpha, beta, base_vec, parts);
-  if (nsplit_heads)
-    launch_k2(gemm_splitk_reduce_kernel, dim3(nsplit_heads, 4), 256, 0, st, C, groups, split_heads,
-              (const double*)parts, alpha, beta);
-  if (ntiles_skinny)
-    launch_k(gemm_skinny_kernel, ntiles_skinny, kSkinnyThreads, 0, st, A, B, C, groups,
-             tiles + ntiles_big + ntiles_small, alpha, beta);
-  return cudaGetLastError();
+    e = launch_k(gemm_mbar_kernel<TK_MBAR_PD>, ntiles_big, MbarCfg::THREADS, kMbarSmem, st, A, B, C, groups, tiles,
+                 alpha, beta, base_vec);
+  if (e == cudaSuccess && ntiles_small)
+    e = launch_k(gemm_small_kernel, ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C, groups,
+                 tiles + ntiles_big, alpha, beta, base_vec, parts);
+  if (e == cudaSuccess && nsplit_heads)
+    e = launch_k2(gemm_splitk_reduce_kernel, dim3(nsplit_heads, 4), 256, 0, st, C, groups, split_heads,
+                  (const double*)parts, alpha, beta);
+  if (e == cudaSuccess && ntiles_skinny)
+    e = launch_k(gemm_skinny_kernel, ntiles_skinny, kSkinnyThreads, 0, st, A, B, C, groups,
+                 tiles + ntiles_big + ntiles_small, alpha, beta);
+  return e;
+}
+
+// Kernel attributes (opt-in dynamic shared memory) are per device: set once per device, before the
+// first launch on it (callers run this ahead of any launch of a tk_* call).
+static PerDeviceOnce g_attrs;
+cudaError_t ensure_kernel_attrs() {
+  return g_attrs.run([] {
+    cudaError_t e = set_permute_attrs<kPermReal>();
+    if (e == cudaSuccess) e = set_permute_attrs<kPermCToC>();
+    if (e == cudaSuccess) e = set_permute_attrs<kPermCToPlanar>();
+    if (e == cudaSuccess) e = set_permute_attrs<kPermCToRealRep>();
+    if (e == cudaSuccess) e = set_permute_attrs<kPermPlanarToC>();
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_mbar_kernel<TK_MBAR_PD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kMbarSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg::SMEM);
+    if (e == cudaSuccess) e = set_gather_attr<4, 4>();
+    if (e == cudaSuccess) e = set_gather_attr<4, 8>();
+    if (e == cudaSuccess) e = set_gather_attr<4, 16>();
+    if (e == cudaSuccess) e = set_gather_attr<8, 4>();
+    if (e == cudaSuccess) e = set_gather_attr<8, 8>();
+    if (e == cudaSuccess) e = set_gather_attr<8, 16>();
+    if (e == cudaSuccess) e = set_gather_attr<16, 4>();
+    if (e == cudaSuccess) e = set_gather_attr<16, 8>();
+    if (e == cudaSuccess) e = set_gather_attr<16, 16>();
+    return e;
+  });
 }
 
 }  // namespace tk

@@ -1,6 +1,7 @@
 // Device-side descriptor tables shared by the host planner and the sm_100a kernels.
 #pragma once
 #include <cstdint>
+#include <mutex>
 
 #include <cuda_runtime.h>
 
@@ -74,7 +75,7 @@ constexpr int kTileElems = 4608;  // smem capacity of the two tile buffers (elem
 constexpr int kPackGroups = 32;
 constexpr int kPackRows = 1024;
 constexpr int kPackElems = 8192;
-enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3, kJobBox = 4, kJobSeg = 5 };
+enum PermJobType : int8_t { kJobRows = 0, kJobTiled = 1, kJobPacked = 2, kJobMulti = 3, kJobSeg = 5 };
 // Latency-regime jobs (kJobSeg, permutes below 2^24 elements): the planner precomputes everything a
 // CTA needs into one contiguous blob -- SegHeader, `ng` SegGroup chunks (a row range of one
 // single-member group each), then the source / destination offsets of every row start as int32
@@ -97,7 +98,6 @@ static_assert(sizeof(SegHeader) == 16 && sizeof(SegGroup) == 80, "seg blob layou
 constexpr int kSegWords = 2 + 10 * kPackGroups + kPackRows;  // rs + rd: 2 x kPackRows int32
 constexpr int kRecoupleStage = 4096;  // doubles of staged recoupling sources per CTA (32 KB)
 constexpr int kRecoupleDirect = 4;    // recoupling groups with <= 4 sources run beside the other jobs
-constexpr int kBoxElems = 4096;  // doubles per box (ComplexF64: half as many elements)
 struct PermJob {
   int32_t group;
   int16_t count;  // rows / tiles / packed groups of this job
@@ -136,14 +136,31 @@ struct GemmTile {
   GemmGroup g;         // copy of groups[group]: a CTA's descriptors arrive in one round trip
 };
 
-// launchers (tk_kernels.cu)
+// One-time per-device initialisation (kernel attributes are per device; std::call_once per ordinal).
+struct PerDeviceOnce {
+  static constexpr int kMaxDevices = 64;
+  std::once_flag flag[kMaxDevices];
+  cudaError_t err[kMaxDevices] = {};
+  template <class F>
+  cudaError_t run(F f) {
+    int d = 0;
+    cudaError_t e = cudaGetDevice(&d);
+    if (e != cudaSuccess) return e;
+    if (d < 0 || d >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::call_once(flag[d], [&] { err[d] = f(); });
+    return err[d];
+  }
+};
+// every kernel attribute of tk_kernels.cu on the current device (idempotent, thread-safe)
+cudaError_t ensure_kernel_attrs();
+
+// launchers (tk_kernels.cu); each returns the status of its own launches
 // ims = -1 conjugates the source (tk_contract conjA / conjB; modes 2 and 3 only). Modes 2 and 3
 // write workspace only and require beta == 0.
 // job table layout: [rows / tiled / packed jobs (njobs, one launch) | recoupling jobs (njobs_multi)];
 // `tiled`: some job is smem-tiled (dynamic shared memory needed). Modes 2 and 3 require beta == 0.
-// variant: kLaunchRowsOnly -- every job of the first launch is a rows job (leaner kernel instance);
-// kLaunchBox -- every job is a box job (mode 2, double-buffered shared-memory box kernel)
-enum PermLaunch : int { kLaunchGeneral = 0, kLaunchRowsOnly = 1, kLaunchBox = 3 };
+// variant: kLaunchRowsOnly -- every job of the first launch is a rows job (leaner kernel instance)
+enum PermLaunch : int { kLaunchGeneral = 0, kLaunchRowsOnly = 1 };
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
                            bool tiled, int variant, int cm, cudaStream_t st);
 // tile table layout: [big (128x128 DMMA) | small (64x64 DMMA) | skinny (streaming, GemmTile.pad = rows)]

@@ -150,49 +150,8 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
   g.c0 = g.ct = g.R = g.T0 = g.Tt = 1;
   g.lorder = 0 + 3 * 1 + 9 * 2;
   g.nrest = 1;
-  static const bool tile_all = getenv("TK_PERM_TILE_ALL") != nullptr;
-  // box mode is an opt-in experiment (TK_BOX=1): measured 2.7 TB/s on cfg4 against 5.0 TB/s for the
-  // rows path (profiles/r01_ncu_summary.md), so the rows path stays the default
-  static const bool no_box = getenv("TK_BOX") == nullptr;
+  static const bool tile_all = knob("TK_PERM_TILE_ALL", 0) != 0;
   bool lead_unit = (g.sa[0] == 1 && g.sb[0] == 0);
-  // mode 2 (box): leg 0 unit-stride on both sides but short (n0 < 128), and the source's next-fastest
-  // leg is not the destination's: swap those two legs through a shared-memory box
-  if (!no_box && lead_unit && g.ndim >= 3 && g.ksrc == 1 && g.kdst == 1 && g.ext[0] < 128) {
-    int sleg = 1;
-    for (int l = 2; l < g.ndim; ++l)
-      if (std::make_pair(g.sb[l], g.sa[l]) < std::make_pair(g.sb[sleg], g.sa[sleg])) sleg = l;
-    // the box kernel walks contiguous runs: source leg sleg right after leg 0 (stride n0, codomain),
-    // destination leg 1 right after leg 0 (stride n0, codomain)
-    const bool runs = g.sb[sleg] == 0 && g.sa[sleg] == g.ext[0] && g.db[1] == 0 && g.da[1] == g.ext[0];
-    if (sleg != 1 && runs) {
-      std::vector<int> order{0, 1, sleg};
-      for (int l = 2; l < g.ndim; ++l)
-        if (l != sleg) order.push_back(l);
-      PermGroup h = g;
-      for (int k = 0; k < g.ndim; ++k) {
-        h.ext[k] = g.ext[order[k]];
-        h.sa[k] = g.sa[order[k]];
-        h.sb[k] = g.sb[order[k]];
-        h.da[k] = g.da[order[k]];
-        h.db[k] = g.db[order[k]];
-      }
-      g = h;
-      g.mode = 2;
-      const int64_t n0 = g.ext[0], n1 = g.ext[1], n2 = g.ext[2];
-      // a box fills one shared-memory buffer of kBoxElems doubles (+ odd plane padding)
-      const int64_t budget = std::max<int64_t>(1, (kBoxElems * 8 / elem_bytes - 64) / n0);
-      int64_t c2 = std::min<int64_t>(n2, std::max<int64_t>(1, (int64_t)std::sqrt((double)budget)));
-      int64_t c1 = std::min<int64_t>(n1, std::max<int64_t>(1, budget / c2));
-      c2 = std::min<int64_t>(n2, std::max<int64_t>(1, budget / c1));
-      g.c0 = (int32_t)n0;
-      g.ct = (int32_t)c1;
-      g.R = (int32_t)c2;
-      g.T0 = (int32_t)((n1 + c1 - 1) / c1);
-      g.Tt = (int32_t)((n2 + c2 - 1) / c2);
-      g.nrest = g.nelem / (n0 * n1 * n2);
-      return;
-    }
-  }
   if (g.ndim >= 2 && g.ksrc == 1 && g.kdst == 1 && (!lead_unit || tile_all)) {
     g.mode = 1;
     g.tleg = 1;
@@ -266,7 +225,7 @@ struct SegBuilder {
     // the row leg: destination leg 0 for rows groups (unit stride on both sides); for transposing
     // groups the source-fastest leg, so loads stay coalesced and the stores scatter (TK_SEG_DSTLEG=1:
     // always destination leg 0)
-    static const bool dst_leg = getenv("TK_SEG_DSTLEG") != nullptr;
+    static const bool dst_leg = knob("TK_SEG_DSTLEG", 0) != 0;
     int L = 0;
     if (g.mode == 1 && !dst_leg)
       for (int l = 1; l < g.ndim; ++l)
@@ -326,24 +285,24 @@ struct SegBuilder {
 static void make_jobs(PermPlan& P) {
   // small single-member groups go last and are packed several per CTA (permute_packed_kernel)
   std::stable_partition(P.groups.begin(), P.groups.end(), [](const PermGroup& g) { return !packable(g); });
-  std::vector<PermJob> rows, multi, dmulti, tiles, packed, boxes;
+  std::vector<PermJob> rows, multi, dmulti, tiles, packed;
   // elements per CTA job: 8192 for large permutes, smaller for small ones so that a latency-bound
   // permute still spreads over about two waves of the 148 SMs x 4 resident CTAs
   int64_t total = 0;
   for (const PermGroup& g : P.groups) total += g.nelem;
-  static const int64_t job_div = getenv("TK_JOB_DIV") ? atoll(getenv("TK_JOB_DIV")) : 2 * 148 * 4;
-  static const int64_t job_max = getenv("TK_JOB_MAX") ? atoll(getenv("TK_JOB_MAX")) : kPackElems;
+  static const int64_t job_div = knob("TK_JOB_DIV", 2 * 148 * 4);
+  static const int64_t job_max = knob("TK_JOB_MAX", kPackElems);
   const int64_t job_elems = std::max<int64_t>(512, std::min<int64_t>(job_max, total / job_div));
   int64_t pack_elems = 0, pack_rows = 0;
   // latency regime: single-member rows / packable groups become kJobSeg blobs (TK_NO_SEG=1 disables)
-  static const bool no_seg = getenv("TK_NO_SEG") != nullptr;
+  static const bool no_seg = knob("TK_NO_SEG", 0) != 0;
   const bool seg = !no_seg && total < (int64_t(1) << 24);
   std::vector<PermJob> segs;
   // seg job size: about total / 296 elements (measured against 1184 / 592 / 148 jobs per permute: fewer,
   // larger jobs amortise each CTA's blob copy and tail -- cfg7 124 -> 112 us, cfg3 219 -> 213 us;
   // tools/gpu_ab17.sh), within [256, TK_SEG_MAX = 8192] elements (the row table holds 1024 rows)
-  static const int64_t seg_div = getenv("TK_SEG_DIV") ? atoll(getenv("TK_SEG_DIV")) : 2 * 148;
-  static const int64_t seg_max = getenv("TK_SEG_MAX") ? atoll(getenv("TK_SEG_MAX")) : kPackElems;
+  static const int64_t seg_div = knob("TK_SEG_DIV", 2 * 148);
+  static const int64_t seg_max = knob("TK_SEG_MAX", kPackElems);
   SegBuilder sb(P, segs, std::max<int64_t>(256, std::min<int64_t>(seg_max, total / seg_div)));
   for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
     const PermGroup& g = P.groups[gi];
@@ -365,15 +324,6 @@ static void make_jobs(PermPlan& P) {
       }
       continue;
     }
-    if (g.mode == 2) {
-      // several boxes per job: the box kernel streams box u+1 in while box u is written out
-      const int64_t nbox = (int64_t)g.T0 * g.Tt * g.nrest;
-      if (nbox >= INT32_MAX) TK_THROW(TK_ERR_UNSUPPORTED, "a group with >= 2^31 boxes");
-      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(4096, 4 * job_elems / ((int64_t)g.c0 * g.ct * g.R)));
-      for (int64_t r = 0; r < nbox; r += per)
-        boxes.push_back(PermJob{gi, (int16_t)std::min(per, nbox - r), kJobBox, 0, r});
-      continue;
-    }
     if (g.mode == 0) {
       int64_t nrows = g.nelem / g.ext[0];
       const bool single = g.ksrc == 1 && g.kdst == 1;
@@ -381,7 +331,7 @@ static void make_jobs(PermPlan& P) {
       const int64_t budget = single ? job_elems : std::min<int64_t>(job_elems, kRecoupleStage * 8 / P.elem_bytes / g.ksrc);
       int64_t per = std::max<int64_t>(1, std::min<int64_t>(kMaxRows, budget / std::max(1, g.ext[0])));
       // recoupling groups of few sources run inside the general launch (no second, serialised launch)
-      static const bool direct_ok = getenv("TK_NO_DIRECT_MULTI") == nullptr;
+      static const bool direct_ok = knob("TK_NO_DIRECT_MULTI", 0) == 0;
       auto& dst = single ? rows : (direct_ok && g.ksrc <= kRecoupleDirect ? dmulti : multi);
       for (int64_t r = 0; r < nrows; r += per)
         dst.push_back(PermJob{gi, (int16_t)std::min(per, nrows - r), (int8_t)(single ? kJobRows : kJobMulti), 0, r});
@@ -396,16 +346,14 @@ static void make_jobs(PermPlan& P) {
   // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
   sb.finish();
   rows.insert(rows.begin(), segs.begin(), segs.end());    // seg jobs lead the non-rows-only launch
-  P.njobs = (int)(tiles.size() + rows.size() + packed.size() + boxes.size() + dmulti.size());
+  P.njobs = (int)(tiles.size() + rows.size() + packed.size() + dmulti.size());
   P.njobs_rows = (int)(rows.size() - segs.size());
-  P.njobs_box = (int)boxes.size();
   P.njobs_multi = (int)multi.size();
-  P.tiled = !tiles.empty();  // tiled and box jobs need the dynamic shared-memory tile
+  P.tiled = !tiles.empty();  // tiled jobs need the dynamic shared-memory tile
   P.rows_only = tiles.empty() && packed.empty() && segs.empty() && dmulti.empty();
-  // large permutes (>= 2^24 elements) launch one kernel per job class: rows-only, box, the rest
+  // large permutes (>= 2^24 elements) launch one kernel per job class: rows-only, the rest
   P.split = total >= (int64_t(1) << 24);
-  if (!P.split && !boxes.empty()) TK_THROW(TK_ERR_CUDA, "internal: box jobs in a small permute");
-  static const bool dbg = getenv("TK_PLAN_DEBUG") != nullptr;
+  const bool dbg = plan_debug();
   if (dbg) {
     int64_t er = 0, et = 0, ep = 0, em = 0, gr = 0, gt = 0, gp = 0;
     for (const PermGroup& g : P.groups) {
@@ -436,7 +384,6 @@ static void make_jobs(PermPlan& P) {
             (long long)ep, multi.size(), (long long)em);
   }
   P.jobs = rows;
-  P.jobs.insert(P.jobs.end(), boxes.begin(), boxes.end());
   P.jobs.insert(P.jobs.end(), tiles.begin(), tiles.end());
   P.jobs.insert(P.jobs.end(), packed.begin(), packed.end());
   P.jobs.insert(P.jobs.end(), dmulti.begin(), dmulti.end());
@@ -664,16 +611,20 @@ struct ContractPlan {
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
   bool uploaded = false;
+  std::once_flag up_once;
   ~ContractPlan() {
     if (At) tk_tensor_release((tk_tensor*)At);
     if (Bt) tk_tensor_release((tk_tensor*)Bt);
     if (Ct) tk_tensor_release((tk_tensor*)Ct);
   }
+  void ensure_uploaded() {
+    std::call_once(up_once, [&] { upload(); });
+  }
   void upload() {
-    if (uploaded) return;
-    if (!pa.identity) pa.upload();
-    if (!pb.identity) pb.upload();
-    if (!pc.identity) pc.upload();
+    check_cuda(ensure_kernel_attrs(), "kernel attributes");
+    if (!pa.identity) pa.ensure_uploaded();
+    if (!pb.identity) pb.ensure_uploaded();
+    if (!pc.identity) pc.ensure_uploaded();
     d_ggroups.upload(ggroups);
     d_tiles.upload(tiles);
     d_heads.upload(split_heads);
@@ -829,7 +780,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // groups, coefficient +-1), Float64, and A~ is a genuine permute of A: then the A -> A~ pass (read A,
 // write A~, read A~ again in the GEMM) becomes the GEMM's own gather from A. TK_NO_GATHER=1 disables.
 static void build_gather(const Tensor& A, ContractPlan& P) {
-  static const bool off = getenv("TK_NO_GATHER") != nullptr;
+  static const bool off = knob("TK_NO_GATHER", 0) != 0;
   if (off || P.cplx || P.pa.identity || P.ntiles_skinny == 0 || A.nelems >= INT32_MAX) return;
   for (const GemmGroup& g : P.ggroups)
     if (g.K > 0 && (g.K > kSkinnyMax || g.N > kSkinnyMax)) return;
@@ -894,7 +845,7 @@ static void build_gather(const Tensor& A, ContractPlan& P) {
   for (const GemmGroup& g : P.ggroups)
     if (g.K > 0) rows_total += g.M;
   const int cap = gather_seg_cap(kcls);
-  static const int force_rows = getenv("TK_GATHER_ROWS") ? atoi(getenv("TK_GATHER_ROWS")) : 0;
+  static const int force_rows = (int)knob("TK_GATHER_ROWS", 0);
   int tile_rows = rows_total >= (int64_t)gather_rows(kcls) * 2 * 148 * 4 ? gather_rows(kcls) : kGatherRows;
   if (force_rows > 0) tile_rows = std::min(force_rows, gather_rows(kcls));
   for (int ci = 0; ci < (int)P.Ct->blocks.size(); ++ci) {
@@ -1020,7 +971,7 @@ static void build_gather(const Tensor& A, ContractPlan& P) {
   P.tiles.resize(P.ntiles_big + P.ntiles_small);
   P.ntiles_skinny = 0;
   P.merged_ab = false;
-  if (getenv("TK_PLAN_DEBUG"))
+  if (plan_debug())
     fprintf(stderr, "[tk gather] %zu tiles, %zu subblocks, K <= %d, N <= %d\n", P.gtiles.size(), P.gsegs.size(), kmax,
             nmax);
 }
@@ -1052,7 +1003,7 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   P.pa.identity = ia_id;
   P.pb.identity = ib_id;
   P.pc.identity = ic_id;
-  static const bool no_merge = getenv("TK_NO_MERGE") != nullptr;
+  static const bool no_merge = knob("TK_NO_MERGE", 0) != 0;
   if (!no_merge && !P.cplx && !ia_id && !ib_id && !P.pa.split && !P.pb.split) {
     P.merged_ab = true;
     auto take = [&](const PermPlan& pp, int8_t op, bool multi) {
@@ -1122,20 +1073,20 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
     int gi = (int)P.ggroups.size();
     P.ggroups.push_back(g);
     if (g.K > 0 && g.K <= kSkinnyMax && g.N <= kSkinnyMax) {  // streaming path (HBM-bound block)
-      static const int srows = getenv("TK_SKINNY_ROWS") ? atoi(getenv("TK_SKINNY_ROWS")) : kSkinnyRows;
+      static const int srows = (int)knob("TK_SKINNY_ROWS", kSkinnyRows);
       for (int m = 0; m < g.M; m += srows)
         skinny.push_back(GemmTile{gi, m, 0, std::min(srows, g.M - m), 0, g.K, -1, 0});
       continue;
     }
     // short-K blocks (K <= 128: the L.theta steps of the DMRG chains) take 64 x 64 tiles: 4x the CTAs,
     // 3 CTAs per SM, so tile epilogues overlap other tiles' main loops (measured cfg2 step 1: 30 -> 15 us)
-    static const int small_k = getenv("TK_GEMM_SMALL_K") ? atoi(getenv("TK_GEMM_SMALL_K")) : 128;
+    static const int small_k = (int)knob("TK_GEMM_SMALL_K", 128);
     bool isbig = g.M >= 96 && g.N >= 96 && g.K > small_k;
     int bm = isbig ? 128 : 64, bn = isbig ? 128 : 64;
     // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that one wave of
     // ~148 co-resident tiles covers a ~G x 12 rectangle and shares the A and B k-slices in L2
     // (row-major order re-read all of B from DRAM once per tile-row).
-    static const int band = getenv("TK_GEMM_BAND") ? atoi(getenv("TK_GEMM_BAND")) : 12;
+    static const int band = (int)knob("TK_GEMM_BAND", 12);
     const int ntm = (g.M + bm - 1) / bm, ntn = (g.N + bn - 1) / bn, G = band;
     for (int mb = 0; mb < ntm; mb += G)
       for (int nt = 0; nt < ntn; ++nt)
@@ -1146,17 +1097,17 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   // S slices of 64-multiples, each writing a partial tile; one reduction CTA per tile sums them in a
   // fixed order (deterministic) and applies alpha / beta.
   const int ntot = (int)(big.size() + small.size());
-  static const bool no_split = getenv("TK_NO_SPLITK") != nullptr;
+  static const bool no_split = knob("TK_NO_SPLITK", 0) != 0;
   // tiles/SM below which long-K tiles are split (re-measured after the seg / gather changes: target 2
   // gives cfg3 T3.R 47.5 us vs 52.7 at 4, cfg2 / cfg7 unchanged; tools/gpu_ab14.sh)
-  static const int split_target = getenv("TK_SPLIT_TARGET") ? atoi(getenv("TK_SPLIT_TARGET")) : 2;
+  static const int split_target = (int)knob("TK_SPLIT_TARGET", 2);
   if (!no_split && ntot > 0 && ntot < split_target * 148) {
     const int want = (split_target * 148 + ntot - 1) / ntot;
     std::vector<GemmTile> out;
     int slot = 0;
     for (const GemmTile& t : small) {
       const int K = t.k1;
-      static const int min_chunk = getenv("TK_SPLIT_CHUNK") ? atoi(getenv("TK_SPLIT_CHUNK")) : 64;
+      static const int min_chunk = (int)knob("TK_SPLIT_CHUNK", 64);
       const int S = std::min(std::min(want, K / min_chunk), 16);  // kSplitMax in the reduction kernel
       if (S < 2) {
         out.push_back(t);
@@ -1182,7 +1133,7 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   P.ntiles_big = (int)big.size();
   P.ntiles_small = (int)small.size();
   P.ntiles_skinny = (int)skinny.size();
-  if (getenv("TK_PLAN_DEBUG")) {
+  if (plan_debug()) {
     int mM = 0, mN = 0, mK = 0, nz = 0;
     double fpad = 0;
     for (const GemmGroup& g : P.ggroups) {
@@ -1209,10 +1160,106 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   build_gather(A, P);
 }
 
+// ------------------------------------------------------------------ device memory of plans
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -1;
+  }
+  return d;
+}
+
+namespace {
+struct UploadStreams {  // one library-private non-blocking stream per device, for table uploads
+  std::mutex mu;
+  std::map<int, cudaStream_t> st;
+};
+UploadStreams& upload_streams() {
+  static UploadStreams* u = new UploadStreams();  // intentionally leaked: usable during static destruction
+  return *u;
+}
+struct Graveyard {  // device memory of evicted / cleared plans, freed when no capture can be disturbed
+  std::mutex mu;
+  std::vector<std::pair<void*, int>> v;
+};
+Graveyard& graveyard() {
+  static Graveyard* g = new Graveyard();
+  return *g;
+}
+// relaxed capture mode for the calling thread while in scope (a cold plan may be built while the
+// caller's stream is capturing; the upload must neither join nor invalidate that capture)
+struct RelaxedCapture {
+  cudaStreamCaptureMode old = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&old); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&old); }
+};
+}  // namespace
+
+void upload_bytes(void** p, const void* host, size_t n) {
+  RelaxedCapture rc;
+  const int dev = current_device();
+  cudaStream_t s = nullptr;
+  {
+    UploadStreams& u = upload_streams();
+    std::lock_guard<std::mutex> g(u.mu);
+    auto it = u.st.find(dev);
+    if (it == u.st.end()) {
+      check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "upload stream");
+      u.st[dev] = s;
+    } else {
+      s = it->second;
+    }
+  }
+  if (dev < 0) TK_THROW(TK_ERR_CUDA, "no CUDA device: plan tables cannot be uploaded");
+  check_cuda(cudaMalloc(p, n), "cudaMalloc of plan table");
+  cudaError_t e = cudaMemcpyAsync(*p, host, n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(*p);
+    *p = nullptr;
+    check_cuda(e, "upload of plan table");
+  }
+}
+
+void free_later(void* p, int device) {
+  Graveyard& g = graveyard();
+  std::lock_guard<std::mutex> l(g.mu);
+  g.v.emplace_back(p, device);
+}
+
+static void free_now(std::vector<std::pair<void*, int>>& v) {
+  if (v.empty()) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& x : v) {
+    if (x.second >= 0) cudaSetDevice(x.second);
+    cudaFree(x.first);
+  }
+  cudaSetDevice(cur);
+  v.clear();
+}
+
+void free_deferred(cudaStream_t caller) {
+  Graveyard& g = graveyard();
+  std::vector<std::pair<void*, int>> v;
+  {
+    std::lock_guard<std::mutex> l(g.mu);
+    if (g.v.empty()) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(caller, &cs) != cudaSuccess) {
+      (void)cudaGetLastError();  // the query's own error; frees wait for a later call
+      return;
+    }
+    if (cs != cudaStreamCaptureStatusNone) return;
+    v.swap(g.v);
+  }
+  free_now(v);
+}
+
 // ------------------------------------------------------------------ plan cache
-static std::mutex g_cache_mu;
-static std::map<std::string, std::unique_ptr<ContractPlan>> g_contract_cache;
-static std::map<std::string, std::unique_ptr<PermPlan>> g_perm_cache;
+static PlanCache<ContractPlan> g_contract_cache;
+static PlanCache<PermPlan> g_perm_cache;
 
 static std::string labels_key(const int32_t* v, int n) {
   std::ostringstream os;
@@ -1220,25 +1267,27 @@ static std::string labels_key(const int32_t* v, int n) {
   return os.str();
 }
 
-static ContractPlan* get_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B, const int32_t* labB,
-                                       const Tensor& C, const int32_t* labC) {
-  std::string key = A.sig + "#" + labels_key(labA, A.nlegs()) + "#" + B.sig + "#" + labels_key(labB, B.nlegs()) +
-                    "#" + C.sig + "#" + labels_key(labC, C.nlegs());
-  std::lock_guard<std::mutex> g(g_cache_mu);
-  auto it = g_contract_cache.find(key);
-  if (it != g_contract_cache.end()) return it->second.get();
-  if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
-  Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
-  choose_contracted_order(A, B, t);
-  auto P = std::make_unique<ContractPlan>();
+static std::shared_ptr<ContractPlan> new_contract_plan(const Tensor& A, const Tensor& B, const Tensor& C,
+                                                       const Tuples& t) {
+  auto P = std::make_shared<ContractPlan>();
   build_contract_plan(A, B, C, t, *P);
-  ContractPlan* raw = P.get();
-  g_contract_cache[key] = std::move(P);
-  return raw;
+  return P;
 }
 
-static ContractPlan* get_contract_plan_tuples(const Tensor& A, const Tensor& B, const Tensor& C, const int32_t* tup,
-                                              const int32_t* ntup) {
+static std::shared_ptr<ContractPlan> get_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B,
+                                                       const int32_t* labB, const Tensor& C, const int32_t* labC) {
+  std::string key = A.sig + "#" + labels_key(labA, A.nlegs()) + "#" + B.sig + "#" + labels_key(labB, B.nlegs()) +
+                    "#" + C.sig + "#" + labels_key(labC, C.nlegs());
+  return g_contract_cache.get(key, [&] {
+    if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
+    Tuples t = tuples_from_labels(A, labA, B, labB, labC, C.nlegs(), C.n_cod());
+    choose_contracted_order(A, B, t);
+    return new_contract_plan(A, B, C, t);
+  });
+}
+
+static std::shared_ptr<ContractPlan> get_contract_plan_tuples(const Tensor& A, const Tensor& B, const Tensor& C,
+                                                              const int32_t* tup, const int32_t* ntup) {
   if (A.kind != B.kind || A.kind != C.kind) TK_THROW(TK_ERR_SECTOR_MISMATCH, "sector kinds differ");
   Tuples t = tuples_from_arrays(A, B, tup, ntup);
   std::ostringstream os;
@@ -1247,46 +1296,43 @@ static ContractPlan* get_contract_plan_tuples(const Tensor& A, const Tensor& B, 
     os << "#";
     for (int x : *v) os << x << ",";
   }
-  std::string key = os.str();
-  std::lock_guard<std::mutex> g(g_cache_mu);
-  auto it = g_contract_cache.find(key);
-  if (it != g_contract_cache.end()) return it->second.get();
-  auto P = std::make_unique<ContractPlan>();
-  build_contract_plan(A, B, C, t, *P);
-  ContractPlan* raw = P.get();
-  g_contract_cache[key] = std::move(P);
-  return raw;
+  return g_contract_cache.get(os.str(), [&] { return new_contract_plan(A, B, C, t); });
 }
 
-static PermPlan* get_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q, const Tensor& C) {
+static std::shared_ptr<PermPlan> get_perm_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q,
+                                               const Tensor& C) {
   std::ostringstream os;
   os << A.sig << "#";
   for (int x : p) os << x << ",";
   os << "#";
   for (int x : q) os << x << ",";
   os << "#" << C.sig;
-  std::string key = os.str();
-  std::lock_guard<std::mutex> g(g_cache_mu);
-  auto it = g_perm_cache.find(key);
-  if (it != g_perm_cache.end()) return it->second.get();
-  validate_perm(A, p, q);
-  check_target(A, p, q, C);
-  auto P = std::make_unique<PermPlan>();
-  build_perm_plan(A, p, q, C, *P, A.dtype == TK_C64 ? 16 : 8);
-  PermPlan* raw = P.get();
-  g_perm_cache[key] = std::move(P);
-  return raw;
+  return g_perm_cache.get(os.str(), [&] {
+    validate_perm(A, p, q);
+    check_target(A, p, q, C);
+    auto P = std::make_shared<PermPlan>();
+    build_perm_plan(A, p, q, C, *P, A.dtype == TK_C64 ? 16 : 8);
+    return P;
+  });
 }
 
 void cache_clear() {
-  {
-    std::lock_guard<std::mutex> g(g_cache_mu);
-    g_contract_cache.clear();
-    g_perm_cache.clear();
-  }
+  g_contract_cache.clear();
+  g_perm_cache.clear();
   svd_cache_clear();
   trace_cache_clear();
+  Graveyard& g = graveyard();
+  std::vector<std::pair<void*, int>> v;
+  {
+    std::lock_guard<std::mutex> l(g.mu);
+    v.swap(g.v);
+  }
+  free_now(v);
 }
+
+size_t cache_size() { return g_contract_cache.size() + g_perm_cache.size(); }
+size_t svd_cache_size();
+size_t trace_cache_size();
 
 // ------------------------------------------------------------------ profiling state
 struct Prof {
@@ -1314,27 +1360,23 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 static PermOp perm_op(PermPlan& P, const void* src, void* dst, double alpha, double beta, double ims) {
-  P.upload();
+  if (!P.uploaded) TK_THROW(TK_ERR_CUDA, "internal: plan tables not uploaded");
   return PermOp{src, dst, (const PermGroup*)P.d_groups.p, (const PermMember*)P.d_members.p, (const double*)P.d_coefs.p,
                 (const int64_t*)P.d_blob.p, alpha, beta, ims};
 }
 
 void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double beta, int cm, double ims,
-                        cudaStream_t st) {
+                 cudaStream_t st) {
   PermOp op = perm_op(P, src, dst, alpha, beta, ims);
   if (P.jobs.empty()) return;
   const PermJob* jobs = (const PermJob*)P.d_jobs.p;
   if (P.split) {
-    const int nrest = P.njobs - P.njobs_rows - P.njobs_box;
+    const int nrest = P.njobs - P.njobs_rows;
     if (P.njobs_rows)
       check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, kLaunchRowsOnly, cm, st), "permute launch");
-    if (P.njobs_box)
-      check_cuda(launch_permute(op, op, jobs + P.njobs_rows, P.njobs_box, 0, false, kLaunchBox, cm, st),
-                 "permute launch");
-    check_cuda(launch_permute(op, op, jobs + P.njobs_rows + P.njobs_box, nrest, P.njobs_multi, P.tiled,
-                              kLaunchGeneral, cm, st),
+    check_cuda(launch_permute(op, op, jobs + P.njobs_rows, nrest, P.njobs_multi, P.tiled, kLaunchGeneral, cm, st),
                "permute launch");
-    g_launches += (P.njobs_rows > 0) + (P.njobs_box > 0) + (nrest > 0) + (P.njobs_multi > 0);
+    g_launches += (P.njobs_rows > 0) + (nrest > 0) + (P.njobs_multi > 0);
   } else {
     const int variant = P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
     check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, variant, cm, st), "permute launch");
@@ -1381,7 +1423,9 @@ tk_status tk_permute(const tk_tensor* A_, const void* a, const int32_t* p, int32
   const Tensor& C = *(const Tensor*)C_;
   if (A.dtype != C.dtype) TK_THROW(TK_ERR_INVALID_ARGUMENT, "dtype mismatch");
   std::vector<int> pv(p, p + np), qv(q, q + nq);
-  PermPlan* P = get_perm_plan(A, pv, qv, C);
+  std::shared_ptr<PermPlan> P = get_perm_plan(A, pv, qv, C);
+  P->ensure_uploaded();
+  free_deferred((cudaStream_t)stream);
   g_launches = 0;
   run_permute(*P, a, c, alpha, beta, A.dtype == TK_C64 ? kPermCToC : kPermReal, 1.0, (cudaStream_t)stream);
   TK_API_END
@@ -1451,8 +1495,9 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
                          double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
   if (ws_bytes < P->ws_bytes || (P->ws_bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
   if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
-  P->upload();
+  P->ensure_uploaded();
   cudaStream_t st = (cudaStream_t)stream;
+  free_deferred(st);
   char* w = (char*)ws;
   const double* At = P->pa.identity ? (const double*)a : (const double*)(w + P->off_a);
   const double* Bt = P->pb.identity ? (const double*)b : (const double*)(w + P->off_b);
@@ -1508,7 +1553,7 @@ tk_status tk_contract_workspace(const tk_tensor* A, const int32_t* labA, const t
                                 const tk_tensor* C, const int32_t* labC, size_t* bytes) {
   TK_API_BEGIN
   if (!A || !B || !C || !labA || !labB || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  ContractPlan* P = get_contract_plan(*(const Tensor*)A, labA, *(const Tensor*)B, labB, *(const Tensor*)C, labC);
+  auto P = get_contract_plan(*(const Tensor*)A, labA, *(const Tensor*)B, labB, *(const Tensor*)C, labC);
   *bytes = P->ws_bytes;
   TK_API_END
 }
@@ -1523,8 +1568,8 @@ tk_status tk_contract(const tk_tensor* A_, const void* a, const int32_t* labA, i
   const Tensor& C = *(const Tensor*)C_;
   if ((conjA || conjB) && A.dtype == TK_F64) TK_THROW(TK_ERR_INVALID_ARGUMENT, "conj flags need ComplexF64");
   if ((!a && A.nelems) || (!b && B.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
-  ContractPlan* P = get_contract_plan(A, labA, B, labB, C, labC);
-  run_contract(P, a, b, c, conjA, conjB, alpha, beta, ws, ws_bytes, stream);
+  auto P = get_contract_plan(A, labA, B, labB, C, labC);
+  run_contract(P.get(), a, b, c, conjA, conjB, alpha, beta, ws, ws_bytes, stream);
   TK_API_END
 }
 
@@ -1553,7 +1598,7 @@ tk_status tk_contract_tuples_workspace(const tk_tensor* A, const tk_tensor* B, c
                                        const int32_t* ntup, size_t* bytes) {
   TK_API_BEGIN
   if (!A || !B || !C || !bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  ContractPlan* P = get_contract_plan_tuples(*(const Tensor*)A, *(const Tensor*)B, *(const Tensor*)C, tup, ntup);
+  auto P = get_contract_plan_tuples(*(const Tensor*)A, *(const Tensor*)B, *(const Tensor*)C, tup, ntup);
   *bytes = P->ws_bytes;
   TK_API_END
 }
@@ -1568,8 +1613,8 @@ tk_status tk_contract_tuples(const tk_tensor* A_, const void* a, int32_t conjA, 
   const Tensor& C = *(const Tensor*)C_;
   if ((conjA || conjB) && A.dtype == TK_F64) TK_THROW(TK_ERR_INVALID_ARGUMENT, "conj flags need ComplexF64");
   if ((!a && A.nelems) || (!b && B.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
-  ContractPlan* P = get_contract_plan_tuples(A, B, C, tup, ntup);
-  run_contract(P, a, b, c, conjA, conjB, alpha, beta, ws, ws_bytes, stream);
+  auto P = get_contract_plan_tuples(A, B, C, tup, ntup);
+  run_contract(P.get(), a, b, c, conjA, conjB, alpha, beta, ws, ws_bytes, stream);
   TK_API_END
 }
 
@@ -1594,5 +1639,7 @@ tk_status tk_phase_times(float* ms4, double* bytes4, double* flops) {
 int32_t tk_last_launch_count(void) { return g_launches; }
 
 void tk_cache_clear(void) { tk::cache_clear(); }
+
+int64_t tk_cache_size(void) { return (int64_t)(tk::cache_size() + tk::svd_cache_size() + tk::trace_cache_size()); }
 
 }  // extern "C"

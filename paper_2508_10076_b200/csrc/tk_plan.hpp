@@ -2,6 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <list>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "tk_internal.hpp"
@@ -9,21 +14,86 @@
 
 namespace tk {
 
+// ------------------------------------------------------------------ device context
+int current_device();  // cudaGetDevice, or -1 without a usable device (host-only layout / workspace queries)
+void check_cuda(cudaError_t e, const char* what);
+
 // ------------------------------------------------------------------ device buffers
+// Library-owned device memory: the descriptor tables of a plan, uploaded ONCE per plan (std::call_once
+// in Plan::ensure_uploaded; the plan cache does it inside its lock right after building the plan, so the
+// plan pointer never escapes without its tables; only host-only queries made without a device defer it
+// to the first device-side call). The upload is capture-safe: it runs in relaxed capture mode on a
+// library-private non-blocking stream and is waited for before returning, so a cold plan built while
+// the caller's stream is being captured into a CUDA graph neither joins the capture nor breaks it.
+// Frees are deferred (free_deferred()) to a point where no capture is in progress on the calling
+// stream, because cudaFree synchronises the device.
+void upload_bytes(void** p, const void* host, size_t n);
+void free_later(void* p, int device);
+void free_deferred(cudaStream_t caller);  // no-op while `caller` is capturing
 struct DevBuf {
   void* p = nullptr;
   size_t n = 0;
+  int dev = -1;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) free_later(p, dev);
   }
   template <typename T>
   void upload(const std::vector<T>& v) {
+    if (p) TK_THROW(TK_ERR_CUDA, "internal: plan table uploaded twice");
     n = v.size() * sizeof(T);
     if (n == 0) return;
-    if (cudaMalloc(&p, n) != cudaSuccess) TK_THROW(TK_ERR_CUDA, "cudaMalloc of plan table failed");
-    if (cudaMemcpy(p, v.data(), n, cudaMemcpyHostToDevice) != cudaSuccess)
-      TK_THROW(TK_ERR_CUDA, "upload of plan table failed");
+    dev = current_device();
+    upload_bytes(&p, v.data(), n);
   }
+};
+
+// ------------------------------------------------------------------ plan cache
+// Memoised plans ("crucial for performance"). The key always carries the device
+// ordinal, because a plan's tables live on the device it was built on. Plans are handed out as
+// shared_ptr taken under the lock, so tk_cache_clear / eviction never frees a plan another thread is
+// still launching from. Bounded LRU (kPlanCacheCap entries per cache): a DMRG sweep creates new bond
+// spaces after every truncation. A plan's tables must outlive any CUDA graph captured from it: do not
+// clear the cache (or let it evict) while such a graph is still replayed.
+constexpr size_t kPlanCacheCap = 512;
+template <class Plan>
+class PlanCache {
+ public:
+  template <class Build>
+  std::shared_ptr<Plan> get(const std::string& key0, Build build) {
+    const std::string key = key0 + "@dev" + std::to_string(current_device());
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = map_.find(key);
+    if (it != map_.end()) {
+      lru_.splice(lru_.begin(), lru_, it->second);
+      return it->second->second;
+    }
+    std::shared_ptr<Plan> P = build();  // throws: nothing cached
+    if (current_device() >= 0) P->ensure_uploaded();
+    lru_.emplace_front(key, P);
+    map_[key] = lru_.begin();
+    while (lru_.size() > kPlanCacheCap) {
+      map_.erase(lru_.back().first);
+      lru_.pop_back();
+    }
+    return P;
+  }
+  void clear() {
+    std::lock_guard<std::mutex> g(mu_);
+    map_.clear();
+    lru_.clear();
+  }
+  size_t size() {
+    std::lock_guard<std::mutex> g(mu_);
+    return lru_.size();
+  }
+
+ private:
+  std::mutex mu_;
+  std::list<std::pair<std::string, std::shared_ptr<Plan>>> lru_;
+  std::unordered_map<std::string, typename std::list<std::pair<std::string, std::shared_ptr<Plan>>>::iterator> map_;
 };
 
 // ------------------------------------------------------------------ permute plan
@@ -34,7 +104,7 @@ struct PermPlan {
   std::vector<double> coefs;
   std::vector<PermJob> jobs;
   std::vector<int64_t> blob;  // kJobSeg job blobs (SegHeader | SegGroup[ng] | rs | rd per job)
-  int njobs = 0, njobs_multi = 0, njobs_rows = 0, njobs_box = 0;  // jobs = [rows | box | seg/tiled/packed | recoupling]
+  int njobs = 0, njobs_multi = 0, njobs_rows = 0;  // jobs = [rows | seg/tiled/packed | recoupling]
   bool tiled = false, rows_only = false;
   bool split = false;  // large permute: rows jobs in their own (leaner) launch
   DevBuf d_groups, d_members, d_coefs, d_jobs, d_blob;
@@ -42,14 +112,17 @@ struct PermPlan {
   double bytes = 0;  // algorithmic bytes (each stored element read once and written once)
   int64_t n_src = 0, n_dst = 0;
   bool uploaded = false;
-  void upload() {
-    if (uploaded) return;
-    d_groups.upload(groups);
-    d_members.upload(members);
-    d_coefs.upload(coefs);
-    d_jobs.upload(jobs);
-    d_blob.upload(blob);
-    uploaded = true;
+  std::once_flag up_once;
+  void ensure_uploaded() {
+    std::call_once(up_once, [&] {
+      check_cuda(ensure_kernel_attrs(), "kernel attributes");
+      d_groups.upload(groups);
+      d_members.upload(members);
+      d_coefs.upload(coefs);
+      d_jobs.upload(jobs);
+      d_blob.upload(blob);
+      uploaded = true;
+    });
   }
 };
 

@@ -487,6 +487,22 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- host side
+static PerDeviceOnce g_svd_attrs;
+static cudaError_t ensure_svd_attrs() {
+  return g_svd_attrs.run([] {
+    cudaError_t e = cudaFuncSetAttribute(svd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(svd_cluster_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(svd_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(svd_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(svd_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes);
+    return e;
+  });
+}
+
 struct SvdPlan {
   Tensor* At = nullptr;
   PermPlan pa;
@@ -500,34 +516,42 @@ struct SvdPlan {
   size_t ws_bytes = 0, idx_off = 0;  // byte offset of the int32 index region
   int64_t n_sigma = 0;
   int smem_bytes = 0;
-  bool uploaded = false;
+  std::mutex outs_mu;
+  std::once_flag up_once;
+  void ensure_uploaded() {
+    std::call_once(up_once, [&] {
+      check_cuda(ensure_svd_attrs(), "svd kernel attributes");
+      pa.ensure_uploaded();
+      d_blocks.upload(blocks);
+      for (int c = 0; c < 5; ++c) d_lists[c].upload(lists[c]);
+    });
+  }
   std::map<std::string, std::unique_ptr<DevBuf>> outs;  // extraction tables per kept-count pattern
   ~SvdPlan() {
     if (At) tk_tensor_release((tk_tensor*)At);
   }
 };
 
-static std::mutex g_svd_mu;
-static std::map<std::string, std::unique_ptr<SvdPlan>> g_svd_cache;
+static PlanCache<SvdPlan> g_svd_cache;
 
-void svd_cache_clear() {
-  std::lock_guard<std::mutex> g(g_svd_mu);
-  g_svd_cache.clear();
-}
+void svd_cache_clear() { g_svd_cache.clear(); }
+size_t svd_cache_size() { return g_svd_cache.size(); }
 
-static SvdPlan* get_svd_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
+static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q);
+
+static std::shared_ptr<SvdPlan> get_svd_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
   if (A.dtype != TK_F64) TK_THROW(TK_ERR_UNSUPPORTED, "tk_svd: Float64 only in this build");
   std::ostringstream os;
   os << A.sig << "#";
   for (int x : p) os << x << ",";
   os << "#";
   for (int x : q) os << x << ",";
-  const std::string key = os.str();
-  std::lock_guard<std::mutex> g(g_svd_mu);
-  auto it = g_svd_cache.find(key);
-  if (it != g_svd_cache.end()) return it->second.get();
+  return g_svd_cache.get(os.str(), [&] { return build_svd_plan(A, p, q); });
+}
+
+static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
   validate_perm(A, p, q);
-  auto P = std::make_unique<SvdPlan>();
+  auto P = std::make_shared<SvdPlan>();
   P->At = permuted_tensor(A, p, q, TK_F64);
   P->la = pad_layout(*P->At);
   build_perm_plan(A, p, q, *P->At, P->pa, 8, nullptr, &P->la);
@@ -566,11 +590,11 @@ static SvdPlan* get_svd_plan(const Tensor& A, const std::vector<int>& p, const s
     b.smem = need2 <= kSvdSmemBytes ? 2 : (need1 <= kSvdSmemBytes ? 1 : 0);
     // cluster kernel: rows split over CS CTAs so that a round's critical path is <= ~48 rows per CTA
     int cls = 0;
-    static const bool no_cluster = getenv("TK_SVD_NO_CLUSTER") != nullptr;
+    static const bool no_cluster = knob("TK_SVD_NO_CLUSTER", 0) != 0;
     // blocks that fit one SM's shared memory stay on the single-CTA kernel (one barrier per round, measured
     // faster there); larger ones go to the cluster kernel with ~24 rows per CTA (cfg3: 32.8 -> 15.0 ms)
     if (!no_cluster && b.K <= kClusterMaxK && b.smem == 0) {
-      static const int rows_target = getenv("TK_SVD_ROWS") ? atoi(getenv("TK_SVD_ROWS")) : 24;
+      static const int rows_target = (int)knob("TK_SVD_ROWS", 24);
       const int want = b.R <= rows_target ? 1 : (b.R <= 2 * rows_target ? 2 : (b.R <= 4 * rows_target ? 4 : 8));
       for (int ci = 0, cs = 1; ci < 4; ++ci, cs *= 2) {
         const int64_t Rl = (b.R + cs - 1) / cs, Kl = (b.K + cs - 1) / cs;
@@ -592,9 +616,7 @@ static SvdPlan* get_svd_plan(const Tensor& A, const std::vector<int>& p, const s
   P->n_sigma = nsig;
   P->idx_off = align256((size_t)off * 8);
   P->ws_bytes = align256(P->idx_off + (size_t)nidx * 4);
-  SvdPlan* raw = P.get();
-  g_svd_cache[key] = std::move(P);
-  return raw;
+  return P;
 }
 
 static std::vector<int> ivec(const int32_t* v, int n) { return std::vector<int>(v, v + n); }
@@ -697,38 +719,21 @@ tk_status tk_svd(const tk_tensor* A_, const void* a, const int32_t* p, int32_t n
   if (!A_ || np < 0 || nq < 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
   const Tensor& A = *(const Tensor*)A_;
   if (!a && A.nelems) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
-  SvdPlan* P = get_svd_plan(A, ivec(p, np), ivec(q, nq));
+  auto P = get_svd_plan(A, ivec(p, np), ivec(q, nq));
   if (ws_bytes < P->ws_bytes || !ws) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
   if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  P->ensure_uploaded();
   cudaStream_t st = (cudaStream_t)stream;
-  if (!P->uploaded) {
-    P->d_blocks.upload(P->blocks);
-    for (int c = 0; c < 5; ++c) P->d_lists[c].upload(P->lists[c]);
-    P->uploaded = true;
-  }
+  free_deferred(st);
   reset_launches();
   run_permute(P->pa, a, ws, 1.0, 0.0, kPermReal, 1.0, st);
-  static const bool dbg = getenv("TK_SVD_DEBUG") != nullptr;
-  static bool attr = false;
-  if (!attr) {
-    check_cuda(cudaFuncSetAttribute(svd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
-               "svd smem attribute");
-    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
-               "svd smem attribute");
-    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
-               "svd smem attribute");
-    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
-               "svd smem attribute");
-    check_cuda(cudaFuncSetAttribute(svd_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdSmemBytes),
-               "svd smem attribute");
-    attr = true;
-  }
+  static const bool dbg = knob("TK_SVD_DEBUG", 0) != 0;
   double* wsd = (double*)ws;
   int32_t* idx = (int32_t*)((char*)ws + P->idx_off);
   if (!P->lists[0].empty()) {
     svd_jacobi_kernel<<<(unsigned)P->lists[0].size(), kSvdThreads, P->smem_bytes, st>>>(
         wsd, idx, (const SvdBlock*)P->d_blocks.p, (const int32_t*)P->d_lists[0].p, dbg ? 1 : 0);
-    check_cuda(cudaGetLastError(), "svd launch");
+    check_cuda(cudaPeekAtLastError(), "svd launch");
     add_launches(1);
   }
   for (int c = 1; c < 5; ++c) {
@@ -766,7 +771,7 @@ tk_status tk_svd_spectrum(const tk_tensor* A, const int32_t* p, int32_t np, cons
                           const void* ws, tk_stream stream, int32_t* n_blocks, int64_t* counts, double* sigma) {
   TK_API_BEGIN
   if (!A || !ws) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  SvdPlan* P = get_svd_plan(*(const Tensor*)A, ivec(p, np), ivec(q, nq));
+  auto P = get_svd_plan(*(const Tensor*)A, ivec(p, np), ivec(q, nq));
   if (n_blocks) *n_blocks = (int32_t)P->blocks.size();
   if (counts)
     for (size_t c = 0; c < P->blocks.size(); ++c) counts[c] = P->blocks[c].K;
@@ -785,7 +790,7 @@ tk_status tk_svd_truncate(const tk_tensor* A_, const int32_t* p, int32_t np, con
   TK_API_BEGIN
   if (!A_ || !ws || !W || !U || !S || !Vh) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
   const Tensor& A = *(const Tensor*)A_;
-  SvdPlan* P = get_svd_plan(A, ivec(p, np), ivec(q, nq));
+  auto P = get_svd_plan(A, ivec(p, np), ivec(q, nq));
   std::vector<double> sig(P->n_sigma);
   if (P->n_sigma) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -822,7 +827,7 @@ tk_status tk_svd_extract(const tk_tensor* A_, const int32_t* p, int32_t np, cons
   const Tensor& U = *(const Tensor*)U_;
   const Tensor& S = *(const Tensor*)S_;
   const Tensor& Vh = *(const Tensor*)Vh_;
-  SvdPlan* P = get_svd_plan(A, ivec(p, np), ivec(q, nq));
+  auto P = get_svd_plan(A, ivec(p, np), ivec(q, nq));
   const Tensor& At = *P->At;
   if (U.n_dom() != 1 || S.n_cod() != 1 || S.n_dom() != 1 || Vh.n_cod() != 1 || U.n_cod() != At.n_cod() ||
       Vh.n_dom() != At.n_dom())
@@ -856,7 +861,7 @@ tk_status tk_svd_extract(const tk_tensor* A_, const int32_t* p, int32_t np, cons
   const void* d_outs = nullptr;
   {
     std::string key((const char*)outs.data(), outs.size() * sizeof(SvdOut));
-    std::lock_guard<std::mutex> g(g_svd_mu);
+    std::lock_guard<std::mutex> g(P->outs_mu);
     auto& slot = P->outs[key];
     if (!slot) {
       slot = std::make_unique<DevBuf>();
@@ -865,11 +870,12 @@ tk_status tk_svd_extract(const tk_tensor* A_, const int32_t* p, int32_t np, cons
     d_outs = slot->p;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  P->ensure_uploaded();
   reset_launches();
   svd_extract_kernel<<<dim3((unsigned)outs.size(), 3), 256, 0, st>>>(
       (const double*)ws, (const int32_t*)((const char*)ws + P->idx_off), (const SvdBlock*)P->d_blocks.p,
       (const SvdOut*)d_outs, (double*)u, (double*)s, (double*)vh);
-  check_cuda(cudaGetLastError(), "svd extract launch");
+  check_cuda(cudaPeekAtLastError(), "svd extract launch");
   add_launches(1);
   TK_API_END
 }

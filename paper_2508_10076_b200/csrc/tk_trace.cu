@@ -95,14 +95,20 @@ struct TracePlan {
   std::vector<std::pair<int, std::pair<int, double>>> transfer;  // (A~ sub, (C sub, coef)) for tests
   DevBuf d_dsts, d_srcs;
   size_t ws_bytes = 0;
-  bool uploaded = false;
+  std::once_flag up_once;
+  void ensure_uploaded() {
+    std::call_once(up_once, [&] {
+      pa.ensure_uploaded();
+      d_dsts.upload(dsts);
+      d_srcs.upload(srcs);
+    });
+  }
   ~TracePlan() {
     if (At) tk_tensor_release((tk_tensor*)At);
   }
 };
 
-std::mutex g_trace_mu;
-std::map<std::string, std::unique_ptr<TracePlan>> g_trace_cache;
+PlanCache<TracePlan> g_trace_cache;
 
 // drop the last leg of a canonical left-to-right tree
 Tree peel(Kind k, const Tree& t) {
@@ -132,7 +138,11 @@ const Space* leg_as_dom(const Tensor& A, int i, Space** tmp) {  // (a_1^* ...; b
   return *tmp;
 }
 
-TracePlan* get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std::vector<int>& qt,
+std::shared_ptr<TracePlan> build_trace_plan(const Tensor& A, const std::vector<int>& pp, const std::vector<int>& qq,
+                                            size_t npairs, const std::vector<int>& p, const std::vector<int>& q,
+                                            const Tensor* C);
+
+std::shared_ptr<TracePlan> get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std::vector<int>& qt,
                           const std::vector<int>& p, const std::vector<int>& q, const Tensor* C) {
   if (kind_fermionic(A.kind)) TK_THROW(TK_ERR_UNSUPPORTED, "tk_trace: fermionic kinds (supertrace) not supported");
   if (pt.size() != qt.size() || pt.size() > (size_t)kTraceMaxPairs)
@@ -154,11 +164,13 @@ TracePlan* get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std
   os << "#";
   for (int x : qq) os << x << "," ;
   os << "#" << pt.size() << "#" << (C ? C->sig : std::string("-"));
-  const std::string key = os.str();
-  std::lock_guard<std::mutex> g(g_trace_mu);
-  auto it = g_trace_cache.find(key);
-  if (it != g_trace_cache.end()) return it->second.get();
-  auto P = std::make_unique<TracePlan>();
+  return g_trace_cache.get(os.str(), [&] { return build_trace_plan(A, pp, qq, pt.size(), p, q, C); });
+}
+
+std::shared_ptr<TracePlan> build_trace_plan(const Tensor& A, const std::vector<int>& pp, const std::vector<int>& qq,
+                                            size_t npairs, const std::vector<int>& p, const std::vector<int>& q,
+                                            const Tensor* C) {
+  auto P = std::make_shared<TracePlan>();
   // A~ in the workspace in A's own element type (ComplexF64: interleaved, offsets in complex elements)
   const int eb = A.dtype == TK_C64 ? 16 : 8;
   P->At = permuted_tensor(A, pp, qq, A.dtype);
@@ -169,7 +181,7 @@ TracePlan* get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std
   if (C) {
     check_target(A, p, q, *C);
     const Tensor& At = *P->At;
-    const int nt = (int)pt.size();
+    const int nt = (int)npairs;
     std::vector<std::vector<std::pair<int, double>>> per_dst(C->subs.size());
     for (int i = 0; i < (int)At.subs.size(); ++i) {
       Tree s = At.s_tree(i), f = At.f_tree(i);
@@ -230,19 +242,15 @@ TracePlan* get_trace_plan(const Tensor& A, const std::vector<int>& pt, const std
       P->dsts.push_back(d);
     }
   }
-  TracePlan* raw = P.get();
-  g_trace_cache[key] = std::move(P);
-  return raw;
+  return P;
 }
 
 std::vector<int> ivec(const int32_t* v, int n) { return std::vector<int>(v, v + n); }
 
 }  // namespace
 
-void trace_cache_clear() {
-  std::lock_guard<std::mutex> g(g_trace_mu);
-  g_trace_cache.clear();
-}
+void trace_cache_clear() { g_trace_cache.clear(); }
+size_t trace_cache_size() { return g_trace_cache.size(); }
 
 }  // namespace tk
 
@@ -290,15 +298,12 @@ tk_status tk_trace(const tk_tensor* A_, const void* a, const int32_t* pt, const 
   const Tensor& A = *(const Tensor*)A_;
   const Tensor& C = *(const Tensor*)C_;
   if ((!a && A.nelems) || (!c && C.nelems)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null data pointer");
-  TracePlan* P = get_trace_plan(A, ivec(pt, nt), ivec(qt, nt), ivec(p, np), ivec(q, nq), &C);
+  auto P = get_trace_plan(A, ivec(pt, nt), ivec(qt, nt), ivec(p, np), ivec(q, nq), &C);
   if (ws_bytes < P->ws_bytes || (P->ws_bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
   if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  P->ensure_uploaded();
   cudaStream_t st = (cudaStream_t)stream;
-  if (!P->uploaded) {
-    P->d_dsts.upload(P->dsts);
-    P->d_srcs.upload(P->srcs);
-    P->uploaded = true;
-  }
+  free_deferred(st);
   reset_launches();
   const bool cx = A.dtype == TK_C64;
   run_permute(P->pa, a, ws, 1.0, 0.0, cx ? kPermCToC : kPermReal, 1.0, st);
@@ -310,7 +315,7 @@ tk_status tk_trace(const tk_tensor* A_, const void* a, const int32_t* pt, const 
     else
       trace_kernel<double><<<grid, 256, 0, st>>>((const double*)ws, (double*)c, (const TraceDst*)P->d_dsts.p,
                                                 (const TraceSrc*)P->d_srcs.p, alpha, beta);
-    check_cuda(cudaGetLastError(), "trace launch");
+    check_cuda(cudaPeekAtLastError(), "trace launch");
     add_launches(1);
   }
   TK_API_END
@@ -323,7 +328,7 @@ tk_status tk_trace_transfer(const tk_tensor* A_, const int32_t* pt, const int32_
   if (!A_ || !C_ || !out || nt < 1) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
   const Tensor& A = *(const Tensor*)A_;
   const Tensor& C = *(const Tensor*)C_;
-  TracePlan* P = get_trace_plan(A, ivec(pt, nt), ivec(qt, nt), ivec(p, np), ivec(q, nq), &C);
+  auto P = get_trace_plan(A, ivec(pt, nt), ivec(qt, nt), ivec(p, np), ivec(q, nq), &C);
   // compose: A subblocks -> A~ subblocks (permute transfer) -> C subblocks (trace map)
   const Tensor& At = *P->At;
   std::vector<double> Tpa(A.subs.size() * At.subs.size());

@@ -113,6 +113,7 @@ _trace = _sig("tk_trace", [_p, _p, _i32p, _i32p, ctypes.c_int32, _i32p, ctypes.c
 _trace_transfer = _sig("tk_trace_transfer", [_p, _i32p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32, _i32p,
                                              ctypes.c_int32, _p, _dp])
 _cache_clear = _sig("tk_cache_clear", [], None)
+_cache_size = _sig("tk_cache_size", [], ctypes.c_int64)
 _version = _sig("tk_version", [], ctypes.c_char_p)
 
 EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sectors", "tk_space_dual",
@@ -123,7 +124,7 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_permute_transfer", "tk_permute_transfer_planar", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
             "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract", "tk_trace_output", "tk_trace_workspace",
             "tk_trace", "tk_trace_transfer", "tk_contract_tuples_output", "tk_contract_tuples_workspace",
-            "tk_contract_tuples", "tk_ncon_output", "tk_ncon_workspace", "tk_ncon"]
+            "tk_contract_tuples", "tk_ncon_output", "tk_ncon_workspace", "tk_ncon", "tk_cache_size"]
 
 
 def _i32(seq):
@@ -138,6 +139,45 @@ def _ptr(x):
     if isinstance(x, int):
         return x
     return x.data_ptr()
+
+
+_TORCH_DT = {TK_F64: "torch.float64", TK_C64: "torch.complex128"}
+
+
+def _data(t, x, what):
+    """Pointer to the data of tensor map `t` held in torch tensor `x`, after checking what the C ABI
+    cannot: a CUDA tensor, contiguous, of t's element type, with at least t.nelems elements.
+    Raw integer pointers are passed through unchecked (C-style callers own that contract)."""
+    if x is None or isinstance(x, int):
+        return x
+    inf = t.info()
+    if not x.is_cuda:
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if not x.is_contiguous():
+        raise ValueError(f"{what}: expected a contiguous tensor")
+    if str(x.dtype) != _TORCH_DT[inf["dtype"]]:
+        raise TypeError(f"{what}: dtype {x.dtype} does not match the tensor map ({_TORCH_DT[inf['dtype']]})")
+    if x.numel() < t.nelems:
+        raise ValueError(f"{what}: {x.numel()} elements < the tensor map's {t.nelems}")
+    return x.data_ptr()
+
+
+def _ws(ws, ws_bytes):
+    """Workspace pointer; a torch workspace must be CUDA, contiguous and hold ws_bytes."""
+    if ws is None or isinstance(ws, int):
+        return ws
+    if not ws.is_cuda or not ws.is_contiguous():
+        raise ValueError("workspace: expected a contiguous CUDA tensor")
+    if ws.numel() * ws.element_size() < ws_bytes:
+        raise ValueError(f"workspace: {ws.numel() * ws.element_size()} bytes < ws_bytes = {ws_bytes}")
+    return ws.data_ptr()
+
+
+def _labels(t, lab, what):
+    n = t.nlegs
+    if len(lab) != n:
+        raise ValueError(f"{what}: {len(lab)} labels for a tensor map with {n} legs")
+    return _i32(lab)
 
 
 def _stream(stream):
@@ -188,15 +228,24 @@ class Tensor:
 
     @property
     def nelems(self):
-        n = ctypes.c_int64()
-        _check(_tensor_nelems(self.h, ctypes.byref(n)))
-        return n.value
+        if getattr(self, "_nelems", None) is None:  # tensor maps are immutable: query once
+            n = ctypes.c_int64()
+            _check(_tensor_nelems(self.h, ctypes.byref(n)))
+            self._nelems = n.value
+        return self._nelems
+
+    @property
+    def nlegs(self):
+        inf = self.info()
+        return inf["n_cod"] + inf["n_dom"]
 
     def info(self):
-        v = [ctypes.c_int32() for _ in range(7)]
-        _check(_tensor_info(self.h, *[ctypes.byref(x) for x in v]))
-        keys = ("n_cod", "n_dom", "dtype", "width", "n_blocks", "n_subblocks", "key_len")
-        return dict(zip(keys, (x.value for x in v)))
+        if getattr(self, "_info", None) is None:
+            v = [ctypes.c_int32() for _ in range(7)]
+            _check(_tensor_info(self.h, *[ctypes.byref(x) for x in v]))
+            keys = ("n_cod", "n_dom", "dtype", "width", "n_blocks", "n_subblocks", "key_len")
+            self._info = dict(zip(keys, (x.value for x in v)))
+        return dict(self._info)
 
     def blocks(self):
         inf = self.info()
@@ -247,8 +296,8 @@ def tk_tensor_create(dtype, cod, dom):
 
 
 def tk_contract_output(A, labA, B, labB, labC, n_cod_C):
-    a, ap = _i32(labA)
-    b, bp = _i32(labB)
+    a, ap = _labels(A, labA, "labA")
+    b, bp = _labels(B, labB, "labB")
     c, cp = _i32(labC)
     h = _p()
     _check(_contract_output(A.h, ap, B.h, bp, cp, n_cod_C, ctypes.byref(h)))
@@ -266,8 +315,8 @@ def tk_permute_workspace(A, p, q, C):
 def tk_permute(A, a, p, q, C, c, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, stream=None):
     pa, pp = _i32(p)
     qa, qp = _i32(q)
-    _check(_permute(A.h, _ptr(a), pp, len(p), qp, len(q), C.h, _ptr(c), float(alpha), float(beta), _ptr(ws),
-                    ws_bytes, _stream(stream)))
+    _check(_permute(A.h, _data(A, a, "a"), pp, len(p), qp, len(q), C.h, _data(C, c, "c"), float(alpha), float(beta),
+                    _ws(ws, ws_bytes), ws_bytes, _stream(stream)))
 
 
 def tk_permute_transfer(A, p, q, C):
@@ -289,9 +338,9 @@ def tk_permute_transfer_planar(A, p, q, C, kappa_mode=-1):
 
 
 def tk_contract_workspace(A, labA, B, labB, C, labC):
-    a, ap = _i32(labA)
-    b, bp = _i32(labB)
-    c, cp = _i32(labC)
+    a, ap = _labels(A, labA, "labA")
+    b, bp = _labels(B, labB, "labB")
+    c, cp = _labels(C, labC, "labC")
     n = ctypes.c_size_t()
     _check(_contract_workspace(A.h, ap, B.h, bp, C.h, cp, ctypes.byref(n)))
     return n.value
@@ -299,11 +348,11 @@ def tk_contract_workspace(A, labA, B, labB, C, labC):
 
 def tk_contract(A, a, labA, B, b, labB, C, c, labC, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, conjA=False,
                 conjB=False, stream=None):
-    la, ap = _i32(labA)
-    lb, bp = _i32(labB)
-    lc, cp = _i32(labC)
-    _check(_contract(A.h, _ptr(a), ap, int(conjA), B.h, _ptr(b), bp, int(conjB), C.h, _ptr(c), cp, float(alpha),
-                     float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+    la, ap = _labels(A, labA, "labA")
+    lb, bp = _labels(B, labB, "labB")
+    lc, cp = _labels(C, labC, "labC")
+    _check(_contract(A.h, _data(A, a, "a"), ap, int(conjA), B.h, _data(B, b, "b"), bp, int(conjB), C.h,
+                     _data(C, c, "c"), cp, float(alpha), float(beta), _ws(ws, ws_bytes), ws_bytes, _stream(stream)))
 
 
 def _tuples(pA, qA, pB, qB, pAB, qAB):
@@ -333,8 +382,9 @@ def tk_contract_tuples(A, a, pA, qA, B, b, pB, qB, C, c, pAB, qAB, alpha=1.0, be
     """Alg. 4 with explicit tuples (include/tk.h): C = alpha permute(permute(A,(pA,qA)) o permute(B,(pB,qB)),
     (pAB,qAB)) + beta C."""
     keep, tp, np_ = _tuples(pA, qA, pB, qB, pAB, qAB)
-    _check(_contract_tuples(A.h, _ptr(a), int(conjA), B.h, _ptr(b), int(conjB), C.h, _ptr(c), tp, np_, float(alpha),
-                            float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+    _check(_contract_tuples(A.h, _data(A, a, "a"), int(conjA), B.h, _data(B, b, "b"), int(conjB), C.h,
+                            _data(C, c, "c"), tp, np_, float(alpha), float(beta), _ws(ws, ws_bytes), ws_bytes,
+                            _stream(stream)))
 
 
 def _ncon_args(tensors, labels, order):
@@ -362,10 +412,12 @@ def tk_ncon_workspace(tensors, labels, order, n_cod_out):
 
 
 def tk_ncon(tensors, datas, labels, order, n_cod_out, C, c, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, stream=None):
+    for i, (t, l) in enumerate(zip(tensors, labels)):
+        _labels(t, l, f"labels[{i}]")
     n, th, lp, keep, op, no = _ncon_args(tensors, labels, order)
-    dp = (_p * n)(*[_ptr(x) for x in datas])
-    _check(_ncon(n, ctypes.cast(th, _p), ctypes.cast(dp, _p), ctypes.cast(lp, _p), op, no, n_cod_out, C.h, _ptr(c),
-                 float(alpha), float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+    dp = (_p * n)(*[_data(t, x, f"datas[{i}]") for i, (t, x) in enumerate(zip(tensors, datas))])
+    _check(_ncon(n, ctypes.cast(th, _p), ctypes.cast(dp, _p), ctypes.cast(lp, _p), op, no, n_cod_out, C.h,
+                 _data(C, c, "c"), float(alpha), float(beta), _ws(ws, ws_bytes), ws_bytes, _stream(stream)))
 
 
 def tk_profile_enable(on=True):
@@ -409,7 +461,7 @@ def tk_svd_workspace(A, p, q):
 def tk_svd(A, a, p, q, ws, ws_bytes, stream=None):
     pa, pp = _i32(p)
     qa, qp = _i32(q)
-    _check(_svd(A.h, _ptr(a), pp, len(p), qp, len(q), _ptr(ws), ws_bytes, _stream(stream)))
+    _check(_svd(A.h, _data(A, a, "a"), pp, len(p), qp, len(q), _ws(ws, ws_bytes), ws_bytes, _stream(stream)))
 
 
 def tk_svd_spectrum(A, p, q, ws, stream=None):
@@ -445,8 +497,8 @@ def tk_svd_truncate(A, p, q, ws, max_dim=0, rel_tol=0.0, stream=None):
 def tk_svd_extract(A, p, q, ws, U, u, S, s, Vh, vh, stream=None):
     pa, pp = _i32(p)
     qa, qp = _i32(q)
-    _check(_svd_extract(A.h, pp, len(p), qp, len(q), _ptr(ws), U.h, _ptr(u), S.h, _ptr(s), Vh.h, _ptr(vh),
-                        _stream(stream)))
+    _check(_svd_extract(A.h, pp, len(p), qp, len(q), _ptr(ws), U.h, _data(U, u, "u"), S.h, _data(S, s, "s"), Vh.h,
+                        _data(Vh, vh, "vh"), _stream(stream)))
 
 
 def _trace_args(pt, qt, p, q):
@@ -470,7 +522,8 @@ def tk_trace_workspace(A, pt, qt, p, q, C):
 
 def tk_trace(A, a, pt, qt, p, q, C, c, alpha=1.0, beta=0.0, ws=None, ws_bytes=0, stream=None):
     keep, args = _trace_args(pt, qt, p, q)
-    _check(_trace(A.h, _ptr(a), *args, C.h, _ptr(c), float(alpha), float(beta), _ptr(ws), ws_bytes, _stream(stream)))
+    _check(_trace(A.h, _data(A, a, "a"), *args, C.h, _data(C, c, "c"), float(alpha), float(beta), _ws(ws, ws_bytes),
+                  ws_bytes, _stream(stream)))
 
 
 def tk_trace_transfer(A, pt, qt, p, q, C):
@@ -482,6 +535,10 @@ def tk_trace_transfer(A, pt, qt, p, q, C):
 
 def tk_cache_clear():
     _cache_clear()
+
+
+def tk_cache_size():
+    return int(_cache_size())
 
 
 def tk_version():

@@ -408,3 +408,46 @@ def test_ncon_output_and_errors():
     T1 = tk.tk_trace_output(A, [1], [2], [0], [])
     Cr = tk.tk_contract_output(T1, [-1], M, [-2, -3], [-1, -2, -3], 1)
     assert Ct.nelems == Cr.nelems and Ct.info() == Cr.info()
+
+
+# ------------------------------------------------------------------ plan cache (host side)
+def _tiny_pair(tag):
+    V = W.space("U1", [((-1,), 1), ((0,), 3), ((1,), 2), ((tag,), 1)])
+    A = tk.tensor_from_spec({"cod": [V, V], "dom": [V]})
+    B = tk.tensor_from_spec({"cod": [V], "dom": [V, V]})
+    return A, B
+
+
+def test_plan_cache_keys_and_bound():
+    """Plans are memoised per (structure, labels, device): a repeated query reuses the plan, other labels
+    or other spaces make new ones, the LRU keeps at most 512 per cache, tk_cache_clear empties it."""
+    tk.tk_cache_clear()
+    assert tk.tk_cache_size() == 0
+    A, B = _tiny_pair(3)
+    la, lb, lc = [1, 2, 3], [3, 4, 5], [1, 4, 2, 5]
+    C = tk.tk_contract_output(A, la, B, lb, lc, 2)
+    w1 = tk.tk_contract_workspace(A, la, B, lb, C, lc)
+    assert tk.tk_cache_size() == 1
+    assert tk.tk_contract_workspace(A, la, B, lb, C, lc) == w1
+    assert tk.tk_cache_size() == 1                        # same key: cached
+    lc2 = [4, 1, 2, 5]
+    C2 = tk.tk_contract_output(A, la, B, lb, lc2, 2)
+    tk.tk_contract_workspace(A, la, B, lb, C2, lc2)
+    assert tk.tk_cache_size() == 2                        # other output labels: a new plan
+    A3, B3 = _tiny_pair(4)
+    C3 = tk.tk_contract_output(A3, la, B3, lb, lc, 2)
+    tk.tk_contract_workspace(A3, la, B3, lb, C3, lc)
+    assert tk.tk_cache_size() == 3                        # other spaces: a new plan
+    for d in range(5, 5 + 520):                           # bounded LRU
+        Ad, Bd = _tiny_pair(d)
+        Cd = tk.tk_contract_output(Ad, la, Bd, lb, lc, 2)
+        tk.tk_contract_workspace(Ad, la, Bd, lb, Cd, lc)
+    assert tk.tk_cache_size() == 512
+    tk.tk_cache_clear()
+    assert tk.tk_cache_size() == 0
+
+
+def test_binding_rejects_bad_labels():
+    A, B = _tiny_pair(3)
+    with pytest.raises(ValueError):
+        tk.tk_contract_output(A, [1, 2], B, [3, 4, 5], [1, 4, 2, 5], 2)
