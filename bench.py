@@ -28,8 +28,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FP64_PEAK_TFLOPS = 37.0      # measured DMMA microbenchmark, profiles/r01_fp64_peak.txt
-DGEMM_TFLOPS = 35.45         # measured cuBLAS DGEMM 8192^3, profiles/r01_dgemm_peak.json
+CHAIN_CFGS = (2, 3, 5, 6, 7, 8)
+GEMM_KERNEL = "gemm_mbar_kernel (grouped DMMA GEMM over the coupled sectors)"   # the DMRG-shaped chains (Alg. 11 / 12 contractions), timed beside cfg4
 
 
 def load_peaks():
@@ -196,6 +196,107 @@ def whole_job_gflops(flops_per_step, steps, world, total_ms):
     return world * flops_per_step * steps / (total_ms * 1e-3) / 1e9
 
 
+# --------------------------------------------------------------------------- in-run peaks
+def measure_fp64_peak(stream, dev):
+    """FP64 roofline denominator measured in THIS process (MEASURED_PEAKS.json has no FP64 entry):
+    the library's DMMA probe (tk_dmma_probe: 148 x 4 CTAs of 8 warps, back-to-back independent
+    mma.sync m8n8k4 f64) and cuBLAS DGEMM 8192^3 through torch.matmul, best of 5 each (CUDA events)."""
+    import torch
+    from paper_2508_10076_b200 import tk
+    blocks, iters = 148 * 4, 65536
+
+    def probe(reps=1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fl = sum(tk.tk_dmma_probe(blocks, iters, stream=stream) for _ in range(reps))
+        e1.record(stream)
+        e1.synchronize()
+        return fl / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    probe()
+    dmma = max(probe() for _ in range(5))          # burst: ~35 ms launches
+    dmma_sus = probe(reps=40)                      # sustained: ~1.4 s back to back
+    n = 8192
+    x = torch.randn(n, n, dtype=torch.float64, device=dev)
+    y = torch.randn(n, n, dtype=torch.float64, device=dev)
+    with torch.cuda.stream(stream):
+        torch.matmul(x, y)
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            torch.matmul(x, y)
+            e1.record(stream)
+            e1.synchronize()
+            best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del x, y
+    return {"dmma_probe_tflops": round(dmma, 3), "dmma_probe_sustained_tflops": round(dmma_sus, 3),
+            "cublas_dgemm_8192_tflops": round(best, 3)}
+
+
+def time_chains(dev, stream, peak_flops, hbm_bytes_s, reps=30):
+    """Every DMRG-shaped chain (cfg2/3/5/6/7/8 at their full sizes) replayed as ONE CUDA graph; L2 is
+    flushed (a 256 MB write) before every timed replay; median of `reps` CUDA-event timings. Roofline per
+    SURVEY §8(d): sum over steps of tk_contract_roofline (GEMM blocks max(flops/P, bytes/BW) + permute
+    bytes/BW) at the in-run DMMA peak and MEASURED_PEAKS' HBM bandwidth."""
+    import torch
+    from paper_2508_10076_b200 import tk, layout_io
+    from workloads import configs as W
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    out = {}
+    for k in CHAIN_CFGS:
+        cfg = W.CONFIGS[k]()
+        T = {}
+        for name, (spec, idx) in cfg["tensors"].items():
+            t = tk.tensor_from_spec(spec)
+            T[name] = (t, torch.from_numpy(layout_io.fill(t, cfg["cfg"], idx)).to(dev))
+        steps, roof = [], {"flops": 0.0, "gemm_bytes": 0.0, "permute_bytes": 0.0, "seconds": 0.0}
+        for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+            A, B = T[na][0], T[nb][0]
+            C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+            T[nc] = (C, torch.zeros(C.nelems, dtype=torch.float64, device=dev))
+            nws = tk.tk_contract_workspace(A, la, B, lb, C, lc)
+            ws = torch.empty(max(nws // 8 + 64, 1), dtype=torch.float64, device=dev)
+            r = tk.tk_contract_roofline(A, la, B, lb, C, lc, peak_flops, hbm_bytes_s)
+            for key in roof:
+                roof[key] += r[key]
+            steps.append((na, la, nb, lb, nc, lc, ws))
+
+        def chain():
+            n = 0
+            for (na, la, nb, lb, nc, lc, ws) in steps:
+                tk.tk_contract(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], T[nc][1], lc, ws=ws,
+                               ws_bytes=ws.numel() * 8, stream=stream)
+                n += tk.tk_last_launch_count()
+            return n
+        with torch.cuda.stream(stream):
+            launches = chain()
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                chain()
+            for _ in range(3):
+                g.replay()
+            ts = []
+            for _ in range(reps):
+                flush.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+        us = float(np.median(ts))
+        out[f"cfg{k}"] = {"kind": cfg["kind"], "us_per_chain": round(us, 2), "steps": len(steps),
+                          "launches": launches, "block_flops": roof["flops"],
+                          "GFLOP_s": round(roof["flops"] / (us * 1e-6) / 1e9, 2),
+                          "roofline_us": round(roof["seconds"] * 1e6, 2),
+                          "roofline_frac": round(roof["seconds"] * 1e6 / us, 3),
+                          "permute_bytes": roof["permute_bytes"], "gemm_min_bytes": roof["gemm_bytes"]}
+        del g, T, steps
+        torch.cuda.empty_cache()
+    return out
+
+
 # --------------------------------------------------------------------------- GPU
 def run_gpu(args):
     import torch
@@ -236,6 +337,8 @@ def run_gpu(args):
     def step():
         tk.tk_contract(A, a, la, B, b, lb, C, c, lc, ws=ws, ws_bytes=ws.numel() * 8, stream=stream)
 
+    fp64 = measure_fp64_peak(stream, dev)           # roofline denominator, measured in this run
+    peak_tf = fp64["dmma_probe_sustained_tflops"]
     tk.tk_profile_enable(True)
     for _ in range(args.warmup):
         step()
@@ -321,6 +424,7 @@ def run_gpu(args):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     ph = phase / args.steps
     gemm_tf = flops / (ph[2] * 1e-3) / 1e12
+    gemm_alg_bytes = tk.tk_contract_roofline(A, la, B, lb, C, lc, 1e12, 1e12)["gemm_bytes"]
     perm = {}
     for i, nm in ((0, "permute_A"), (1, "permute_B"), (3, "permute_C")):
         if pbytes[i] > 0:
@@ -329,13 +433,20 @@ def run_gpu(args):
                         "frac_of_8TBs": round(gbs / 8000.0, 3), "bytes": int(pbytes[i])}
     perm_bytes = float(pbytes[0] + pbytes[1] + pbytes[3])
     perm_ms = float(ph[0] + ph[1] + ph[3])
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    # DRAM bytes per GEMM launch from the ncu --set full capture of this build (profiles/, named per round);
+    # ncu cannot run inside the timed process, so the capture's file and build are named beside the number
+    traffic, traffic_src = None, None
+    tfile = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get("gemm_dram_bytes_per_launch")
+            tj = json.load(open(tfile))
+            traffic = tj.get("gemm_dram_bytes_per_launch")
+            traffic_src = f"profiles/r02_ncu_traffic.json ({tj.get('build', '?')})"
         except Exception:
             traffic = None
+    chains = None
+    if not args.no_chains and not cplx:
+        chains = time_chains(dev, stream, peak_tf * 1e12, hbm * 1e9)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not cplx:
@@ -356,15 +467,22 @@ def run_gpu(args):
                                f"(reading C20)", "d_leg": args.d_leg, "parallelism": "replicas only",
                    "useful_flops_per_step": flops,
                    "l2": f"inputs ({A.nelems * esz / 1e9:.1f} GB/operand) >> 126 MB L2, no flush needed"},
-        "roofline": {"bound": "tensor", "kernel": "gemm_mbar_kernel<2> + gemm_small_kernel (grouped DMMA GEMM, one launch per tile class)",
-                     "achieved": round(gemm_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": round(gemm_tf / FP64_PEAK_TFLOPS, 4),
-                     "peak_source": "measured FP64 DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt;"
-                                    " MEASURED_PEAKS.json has no FP64 entry); cuBLAS DGEMM 8192^3 = 35.45",
-                     "traffic": traffic},
-        "permute": {"GB_s": round(perm_bytes / (perm_ms * 1e-3) / 1e9, 1) if perm_ms > 0 else None,
-                    "frac_of_measured_hbm": round(perm_bytes / (perm_ms * 1e-3) / 1e9 / hbm, 3) if perm_ms > 0 else None,
-                    "hbm_peak_gbs": hbm, "phases": perm},
+        "roofline": {"bound": "tensor", "kernel": GEMM_KERNEL,
+                     "achieved": round(gemm_tf, 3), "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": round(gemm_tf / peak_tf, 4),
+                     "peak_source": "this run: sustained tk_dmma_probe (FP64 DMMA, no memory traffic; "
+                                    "MEASURED_PEAKS.json has no FP64 entry)", "fp64_peaks_this_run": fp64,
+                     "frac_of_cublas_dgemm": round(gemm_tf / fp64["cublas_dgemm_8192_tflops"], 4),
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": gemm_alg_bytes},
+        "roofline_permute": {"bound": "hbm", "kernel": "permute_kernel (operand permutes A~, B~ and output C)",
+                             "achieved": round(perm_bytes / (perm_ms * 1e-3) / 1e9, 1) if perm_ms > 0 else None,
+                             "peak": hbm, "unit": "GB/s",
+                             "frac": round(perm_bytes / (perm_ms * 1e-3) / 1e9 / hbm, 4) if perm_ms > 0 else None,
+                             "frac_of_8TBs": round(perm_bytes / (perm_ms * 1e-3) / 1e9 / 8000.0, 4) if perm_ms > 0 else None,
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (torch copy, driver-written)",
+                             "algorithmic_bytes": perm_bytes, "phases": perm},
+        "chains": chains,
         "phase_ms": {"permute_A": round(float(ph[0]), 3), "permute_B": round(float(ph[1]), 3),
                      "gemm": round(float(ph[2]), 3), "permute_C": round(float(ph[3]), 3)},
         "planner_ms": {"cold": round(t_plan_cold * 1e3, 2), "cached": round(t_plan_cached * 1e3, 4)},
@@ -394,6 +512,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=24.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-chains", action="store_true", help="skip the cfg2/3/5/6/7/8 chain timings")
     args = ap.parse_args()
     if args.d_leg is None:
         args.d_leg = 320 if args.dtype == "c64" else 384

@@ -258,6 +258,20 @@ tk_status tk_profile_enable(int32_t on);
 tk_status tk_phase_times(float* ms4, double* bytes4, double* flops);
 /* Number of kernel launches issued by the most recent tk_contract / tk_permute call. */
 int32_t tk_last_launch_count(void);
+/* Roofline terms of one tk_contract through its plan; host only, no launch. out4 =
+ * [useful flops sum_c 2 M_c K_c N_c (8 M_c K_c N_c for ComplexF64, reading C21), the GEMM phase's
+ * minimum HBM bytes sum_c s (M_c K_c + K_c N_c + M_c N_c), the permute phase's algorithmic bytes
+ * (every permuted operand / output element read once and written once, s = 8 or 16 B), the roofline
+ * time in seconds sum_c max(flops_c / peak_flops, bytes_c / peak_bytes_per_s) + permute_bytes /
+ * peak_bytes_per_s]. Blocks with K_c = 0 count their zero fill (s M_c N_c bytes). */
+tk_status tk_contract_roofline(const tk_tensor* A, const int32_t* labA, const tk_tensor* B, const int32_t* labB,
+                               const tk_tensor* C, const int32_t* labC, double peak_flops, double peak_bytes_per_s,
+                               double* out4);
+/* FP64 tensor-pipe probe, so a caller can measure the GEMM phase's roofline denominator in its own
+ * process: launches `blocks` CTAs of 256 threads on `stream`; every warp issues iters x 8 independent
+ * DMMA m8n8k4 (mma.sync .f64, no memory traffic). *flops = the launch's flop count; the caller times
+ * it (CUDA events on `stream`). */
+tk_status tk_dmma_probe(int32_t blocks, int64_t iters, tk_stream stream, double* flops);
 
 /* ------------------------------------------------------- topological data (host) */
 /* F^{abc}_d[e,f] (e = a(x)b inner, f = b(x)c inner) and R^{ab}_c of the planner's tables,

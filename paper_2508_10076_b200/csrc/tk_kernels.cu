@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "tk_device.cuh"
 #include "tk_internal.hpp"
 #include "tk_kernels.hpp"
 
@@ -66,8 +67,6 @@ __device__ __forceinline__ void cp_async_wait() {
 // launch early (launch_dependents) and reads/writes tensor data only after griddepcontrol.wait, which
 // returns once the preceding grid has completed and its writes are visible. Descriptor tables (plan
 // constants) are read before the wait, so job/group decoding overlaps the previous kernel's tail.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 #ifndef TK_PERM_MINB
 #define TK_PERM_MINB 4       // resident permute CTAs per SM (register budget: 64 / thread at 256 x 4)
@@ -858,11 +857,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
 
-__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
 
 // Shared-memory pitches: As[k][m] with pitch BM+4 and Bs[n][k] with pitch BK+4 (both = 4 mod 16
 // doubles) make the m8n8k4 fragment loads conflict-free in each 16-lane phase of a 64-bit LDS.
@@ -1020,23 +1014,8 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
 // share of a stage's cp.async copies and signals them with cp.async.mbarrier.arrive.noinc on the
 // stage's "full" barrier; each warp waits only for the data it needs and releases the stage on an
 // "empty" barrier, so warps may drift up to STAGES-PD-1 stages apart without idling the DMMA pipe.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(bar)));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "TK_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
-      "@!p bra TK_WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
 }
 
 template <int BM, int BN, int WM, int WN, int BK, int STAGES, int PD>
@@ -1475,6 +1454,26 @@ cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmG
     e = launch_k(gemm_skinny_kernel, ntiles_skinny, kSkinnyThreads, 0, st, A, B, C, groups,
                  tiles + ntiles_big + ntiles_small, alpha, beta);
   return e;
+}
+
+// ---- FP64 tensor-pipe probe (tk_dmma_probe): back-to-back independent DMMAs, no memory traffic
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* __restrict__ sink, long long iters) {
+  const double a = threadIdx.x * 1e-3, b = 1.0 + blockIdx.x * 1e-6;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (long long it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma884(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 1234.5) sink[0] = s;  // never true; keeps the chain live
+}
+
+cudaError_t launch_dmma_probe(int blocks, long long iters, cudaStream_t st) {
+  return launch_k(dmma_probe_kernel, blocks, 256, 0, st, (double*)nullptr, iters);
 }
 
 // Kernel attributes (opt-in dynamic shared memory) are per device: set once per device, before the

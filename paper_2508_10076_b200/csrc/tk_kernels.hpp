@@ -133,6 +133,8 @@ struct GemmTile {
   int32_t k0, k1;      // k range of this tile (split-K: a slice of [0, K))
   int32_t slot;        // split-K: partial-tile slot (-1: write C directly); reduction heads: first slot
   int32_t nsplit;      // reduction heads: number of partial slots
+  int32_t tmap;        // big tiles of the TMA GEMM: index of the group's tensor-map pair
+  int32_t pad2_;
   GemmGroup g;         // copy of groups[group]: a CTA's descriptors arrive in one round trip
 };
 
@@ -211,5 +213,8 @@ cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, cons
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, int ntiles_skinny, const GemmTile* split_heads,
                         int nsplit_heads, double* parts, double alpha, double beta, cudaStream_t st);
+
+// FP64 tensor-pipe probe: blocks x 8 warps, each iters x 8 DMMA m8n8k4 (2 * 8 * 8 * 4 flops each)
+cudaError_t launch_dmma_probe(int blocks, long long iters, cudaStream_t st);
 
 }  // namespace tk

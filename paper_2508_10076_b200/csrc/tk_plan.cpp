@@ -15,6 +15,7 @@
 #include "tk_internal.hpp"
 #include "tk_kernels.hpp"
 #include "tk_plan.hpp"
+#include "tk_gemm_tma.hpp"
 
 namespace tk {
 
@@ -579,6 +580,8 @@ void permute_transfer_matrix(const Tensor& A, const std::vector<int>& p, const s
       }
 }
 
+int sm_count();
+
 // ------------------------------------------------------------------ contraction plan
 struct ContractPlan {
   Tensor* At = nullptr;  // A~ (canonical layout, reading C2 tuples)
@@ -610,6 +613,14 @@ struct ContractPlan {
   DevBuf d_gsegs, d_btab, d_gslots;
   size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
   double flops = 0;
+  // persistent TMA GEMM for the big tiles (tk_gemm_tma.cu): groups with a tensor-map pair, and the
+  // maps encoded for the last (A~, B~) workspace pointers seen (re-encoded when they change)
+  bool tma = false;
+  std::vector<int> tma_groups;
+  std::mutex tma_mu;
+  std::unique_ptr<GemmTmaParams> tma_params;
+  const void* tma_a = nullptr;
+  const void* tma_b = nullptr;
   bool uploaded = false;
   std::once_flag up_once;
   ~ContractPlan() {
@@ -1152,6 +1163,22 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
             "tiles, split slots %d | tile flops %.3g\n", P.ggroups.size(), nz, P.flops, mM, mN, mK, big.size(),
             small.size(), skinny.size(), P.nslots, fpad);
   }
+  // big tiles run on the persistent TMA kernel when both operands live in the padded workspace layout
+  // (TMA needs 16-byte aligned bases and strides; a caller's buffer used in place may not satisfy that)
+  static const bool no_tma = knob("TK_NO_TMA", 0) != 0;
+  if (!no_tma && !big.empty() && pla && plb) {
+    std::map<int, int> mi;
+    for (GemmTile& t : big) {
+      auto it = mi.find(t.group);
+      if (it == mi.end()) it = mi.emplace(t.group, (int)mi.size()).first;
+      t.tmap = it->second;
+    }
+    if ((int)mi.size() <= kTmaMaxGroups) {
+      P.tma = true;
+      P.tma_groups.resize(mi.size());
+      for (auto& kv : mi) P.tma_groups[kv.second] = kv.first;
+    }
+  }
   P.tiles = big;
   P.tiles.insert(P.tiles.end(), small.begin(), small.end());
   P.tiles.insert(P.tiles.end(), skinny.begin(), skinny.end());
@@ -1161,6 +1188,22 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
 }
 
 // ------------------------------------------------------------------ device memory of plans
+int sm_count() {  // multiprocessors of the current device (cached per device)
+  static std::mutex mu;
+  static std::map<int, int> n;
+  const int d = current_device();
+  std::lock_guard<std::mutex> g(mu);
+  auto it = n.find(d);
+  if (it != n.end()) return it->second;
+  int c = 148;
+  if (d < 0 || cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
+    (void)cudaGetLastError();
+    c = 148;
+  }
+  n[d] = c;
+  return c;
+}
+
 int current_device() {
   int d = 0;
   if (cudaGetDevice(&d) != cudaSuccess) {
@@ -1522,11 +1565,42 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
   prof_record(2, st);
   double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
   if (!P->tiles.empty()) {
-    check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, (const GemmTile*)P->d_tiles.p,
-                           P->ntiles_big, P->ntiles_small, P->ntiles_skinny, (const GemmTile*)P->d_heads.p,
-                           (int)P->split_heads.size(), (double*)(w + P->off_parts), ga, gb, st),
+    int nbig = P->ntiles_big;
+    const GemmTile* d_tiles = (const GemmTile*)P->d_tiles.p;
+    if (P->tma && nbig > 0) {
+      GemmTmaParams* prm = nullptr;
+      {
+        std::lock_guard<std::mutex> g(P->tma_mu);
+        if (!P->tma_params || P->tma_a != At || P->tma_b != Bt) {
+          if (!P->tma_params) P->tma_params = std::make_unique<GemmTmaParams>();
+          P->tma_a = P->tma_b = nullptr;
+          if (gemm_tma_encode(*P->tma_params, P->ggroups, P->tma_groups, At, Bt)) {
+            P->tma_a = At;
+            P->tma_b = Bt;
+          }
+        }
+        if (P->tma_a == At && P->tma_b == Bt) {
+          prm = new GemmTmaParams(*P->tma_params);  // per-call copy: output and scalars differ
+        }
+      }
+      if (prm) {
+        std::unique_ptr<GemmTmaParams> q(prm);
+        q->C = Ct;
+        q->tiles = d_tiles;
+        q->ntiles = nbig;
+        q->alpha = ga;
+        q->beta = gb;
+        check_cuda(launch_gemm_tma(*q, std::min(nbig, sm_count()), st), "tma gemm launch");
+        ++g_launches;
+        d_tiles += nbig;
+        nbig = 0;
+      }
+    }
+    check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, d_tiles, nbig, P->ntiles_small,
+                           P->ntiles_skinny, (const GemmTile*)P->d_heads.p, (int)P->split_heads.size(),
+                           (double*)(w + P->off_parts), ga, gb, st),
                "gemm launch");
-    g_launches += (P->ntiles_big > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0) + !P->split_heads.empty();
+    g_launches += (nbig > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0) + !P->split_heads.empty();
   }
   if (P->gather) {
     check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const int64_t*)P->d_gslots.p,
@@ -1637,6 +1711,40 @@ tk_status tk_phase_times(float* ms4, double* bytes4, double* flops) {
 }
 
 int32_t tk_last_launch_count(void) { return g_launches; }
+
+tk_status tk_contract_roofline(const tk_tensor* A, const int32_t* labA, const tk_tensor* B, const int32_t* labB,
+                               const tk_tensor* C, const int32_t* labC, double peak_flops, double peak_bytes_per_s,
+                               double* out4) {
+  TK_API_BEGIN
+  if (!A || !B || !C || !labA || !labB || !out4) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
+  if (!(peak_flops > 0) || !(peak_bytes_per_s > 0)) TK_THROW(TK_ERR_INVALID_ARGUMENT, "peaks must be positive");
+  auto P = get_contract_plan(*(const Tensor*)A, labA, *(const Tensor*)B, labB, *(const Tensor*)C, labC);
+  const double cm = P->cplx ? 2.0 : 1.0, s = P->cplx ? 16.0 : 8.0;
+  double flops = 0, gbytes = 0, t = 0;
+  for (const GemmGroup& g : P->ggroups) {  // the real-representation GEMM: M x cm K x cm N
+    const double M = g.M, K = g.K / cm, N = g.N / cm;
+    const double f = (P->cplx ? 8.0 : 2.0) * M * K * N;
+    const double by = s * (M * K + K * N + M * N);
+    flops += f;
+    gbytes += by;
+    t += std::max(f / peak_flops, by / peak_bytes_per_s);
+  }
+  const double pbytes = (P->pa.identity ? 0.0 : P->pa.bytes) + (P->pb.identity ? 0.0 : P->pb.bytes) +
+                        (P->pc.identity ? 0.0 : P->pc.bytes);
+  out4[0] = flops;
+  out4[1] = gbytes;
+  out4[2] = pbytes;
+  out4[3] = t + pbytes / peak_bytes_per_s;
+  TK_API_END
+}
+
+tk_status tk_dmma_probe(int32_t blocks, int64_t iters, tk_stream stream, double* flops) {
+  TK_API_BEGIN
+  if (blocks < 1 || iters < 1) TK_THROW(TK_ERR_INVALID_ARGUMENT, "blocks and iters must be >= 1");
+  check_cuda(launch_dmma_probe(blocks, (long long)iters, (cudaStream_t)stream), "dmma probe launch");
+  if (flops) *flops = (double)blocks * 8.0 * (double)iters * 8.0 * (2.0 * 8 * 8 * 4);
+  TK_API_END
+}
 
 void tk_cache_clear(void) { tk::cache_clear(); }
 

@@ -92,6 +92,9 @@ _ncon = _sig("tk_ncon", [ctypes.c_int32, _p, _p, _p, _i32p, ctypes.c_int32, ctyp
 _profile_enable = _sig("tk_profile_enable", [ctypes.c_int32])
 _phase_times = _sig("tk_phase_times", [ctypes.POINTER(ctypes.c_float), _dp, _dp])
 _last_launch_count = _sig("tk_last_launch_count", [], ctypes.c_int32)
+_contract_roofline = _sig("tk_contract_roofline", [_p, _i32p, _p, _i32p, _p, _i32p, ctypes.c_double, ctypes.c_double,
+                                                   _dp])
+_dmma_probe = _sig("tk_dmma_probe", [ctypes.c_int32, ctypes.c_int64, _p, _dp])
 _fsymbol = _sig("tk_fsymbol", [ctypes.c_char_p] + [_i32p] * 6 + [_dp])
 _rsymbol = _sig("tk_rsymbol", [ctypes.c_char_p] + [_i32p] * 3 + [_dp])
 _svd_workspace = _sig("tk_svd_workspace", [_p, _i32p, ctypes.c_int32, _i32p, ctypes.c_int32,
@@ -124,7 +127,8 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_permute_transfer", "tk_permute_transfer_planar", "tk_last_error", "tk_cache_clear", "tk_version", "tk_svd_workspace", "tk_svd",
             "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract", "tk_trace_output", "tk_trace_workspace",
             "tk_trace", "tk_trace_transfer", "tk_contract_tuples_output", "tk_contract_tuples_workspace",
-            "tk_contract_tuples", "tk_ncon_output", "tk_ncon_workspace", "tk_ncon", "tk_cache_size"]
+            "tk_contract_tuples", "tk_ncon_output", "tk_ncon_workspace", "tk_ncon", "tk_cache_size",
+            "tk_contract_roofline", "tk_dmma_probe"]
 
 
 def _i32(seq):
@@ -434,6 +438,23 @@ def tk_phase_times():
 
 def tk_last_launch_count():
     return int(_last_launch_count())
+
+
+def tk_contract_roofline(A, labA, B, labB, C, labC, peak_flops, peak_bytes_per_s):
+    """{flops, gemm_bytes, permute_bytes, seconds} of one tk_contract (include/tk.h)."""
+    a, ap = _labels(A, labA, "labA")
+    b, bp = _labels(B, labB, "labB")
+    c, cp = _labels(C, labC, "labC")
+    out = (ctypes.c_double * 4)()
+    _check(_contract_roofline(A.h, ap, B.h, bp, C.h, cp, float(peak_flops), float(peak_bytes_per_s), out))
+    return {"flops": out[0], "gemm_bytes": out[1], "permute_bytes": out[2], "seconds": out[3]}
+
+
+def tk_dmma_probe(blocks, iters, stream=None):
+    """Launch the FP64 tensor-pipe probe; returns its flop count (time it with CUDA events)."""
+    f = ctypes.c_double()
+    _check(_dmma_probe(int(blocks), int(iters), _stream(stream), ctypes.byref(f)))
+    return f.value
 
 
 def tk_fsymbol(kind, a, b, c, d, e, f):

@@ -50,7 +50,7 @@ def test_binding_checks_buffers():
     from paper_2508_10076_b200 import tk
     V = W.space("U1", [((-1,), 2), ((0,), 3), ((1,), 2)])
     A = tk.tensor_from_spec({"cod": [V, V], "dom": [V]})
-    C = tk.tensor_from_spec({"cod": [V], "dom": [V, V]})
+    C = tk.tensor_from_spec({"cod": [V], "dom": [W.dual(V), V]})
     a = torch.zeros(A.nelems, dtype=torch.float64, device="cuda")
     c = torch.zeros(C.nelems, dtype=torch.float64, device="cuda")
     with pytest.raises(TypeError):

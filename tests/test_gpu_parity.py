@@ -88,23 +88,6 @@ def test_alpha_beta_accumulate():
     assert rel_err_dense(lt, flat, want) <= TOL
 
 
-def test_cfg4_full_size_sampled():
-    """BASELINE cfg4 at its full (bench) size: sampled output subblocks via the tier-2 oracle."""
-    cfg = W.cfg4()
-    got = H.gpu_chain(cfg)
-    C, flat = got["C"]
-    lt = OL.homspace_layout("U1", *_spaces(cfg))
-    rng = np.random.default_rng(0)
-    idx = rng.choice(len(lt.subblocks), size=24, replace=False)
-    keys = [tuple(lt.subblocks[i].key[0]) + tuple(lt.subblocks[i].key[3]) for i in idx]
-    # oracle inputs restricted to what the sampled outputs need is done inside contract_blocks
-    ref = H.oracle_chain_blocks(cfg, out_keys_last=keys)
-    _, blocks = ref["C"]
-    err = rel_err_blocks(lt, flat, blocks, keys=set(keys))
-    assert err <= TOL, f"rel Frobenius {err:.3e}"
-    assert not np.isnan(flat).any()
-
-
 # ------------------------------------------------------------------ ComplexF64 (cfg4 names it)
 @pytest.mark.parametrize("cfgfun", [W.cfg1, W.cfg2, lambda: W.cfg3(chi=64), lambda: W.cfg4(d_leg=24),
                                     lambda: W.cfg5(mults=(3, 5, 4, 2, 2, 1, 1)),
@@ -151,22 +134,6 @@ def test_complex_alpha_beta():
     lt, D = ref["C"]
     want = 0.5 * D - 1.25 * OD.to_dense(lt, init["x"])
     assert rel_err_dense(lt, got["C"][1], want) <= TOL
-
-
-def test_cfg4_complex_bench_size_sampled():
-    """cfg4 ComplexF64 at its bench size (D_leg 320, reading C20): sampled output subblocks, tier 2."""
-    cfg = W.cfg4(d_leg=320)
-    got = H.gpu_chain(cfg, complex_=True)
-    C, flat = got["C"]
-    lt = OL.homspace_layout("U1", *_spaces(cfg))
-    rng = np.random.default_rng(1)
-    idx = rng.choice(len(lt.subblocks), size=16, replace=False)
-    keys = [tuple(lt.subblocks[i].key[0]) + tuple(lt.subblocks[i].key[3]) for i in idx]
-    ref = H.oracle_chain_blocks(cfg, out_keys_last=keys, complex_=True)
-    _, blocks = ref["C"]
-    err = rel_err_blocks(lt, flat, blocks, keys=set(keys))
-    assert err <= TOL, f"rel Frobenius {err:.3e}"
-    assert not np.isnan(flat).any()
 
 
 def _spaces(cfg):

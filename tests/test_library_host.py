@@ -451,3 +451,24 @@ def test_binding_rejects_bad_labels():
     A, B = _tiny_pair(3)
     with pytest.raises(ValueError):
         tk.tk_contract_output(A, [1, 2], B, [3, 4, 5], [1, 4, 2, 5], 2)
+
+
+@pytest.mark.parametrize("cfgfun", [lambda: W.cfg3(), lambda: W.cfg4(), lambda: W.cfg4(d_leg=320),
+                                    lambda: W.cfg7(), lambda: W.cfg8(), lambda: W.cfg2()],
+                         ids=["cfg3_chi2048", "cfg4_d384", "cfg4_d320", "cfg7_m700", "cfg8_m270", "cfg2"])
+def test_layout_equals_oracle_bench_sizes(cfgfun):
+    """Reading C25 at the sizes bench.py / tools/bench_configs.py time: every input tensor AND every
+    intermediate / output of the chain (tk_contract_output vs the oracle's output spaces) has the
+    oracle's block and subblock layout, integer for integer."""
+    cfg = cfgfun()
+    T = {n: (spec, tk.tensor_from_spec(spec)) for n, (spec, _) in cfg["tensors"].items()}
+    for spec, _ in T.values():
+        assert_same_layout(spec)
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+        (sa, A), (sb, B) = T[na], T[nb]
+        Ct = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+        cod, dom = OC.output_spaces(sa["cod"], sa["dom"], sb["cod"], sb["dom"], la, lb, lc, ncod)
+        spec = {"cod": cod, "dom": dom}
+        assert Ct.nelems == oracle_layout(spec).nelems
+        assert_same_layout(spec)
+        T[nc] = (spec, Ct)

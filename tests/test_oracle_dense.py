@@ -481,3 +481,65 @@ def test_alg4_tuples_fermionic_reorder_invariance():
     assert C.rel_frobenius(bos, cross) > 1e-3
     r3 = C.contract_alg4_tuples(A, Asp, 3, B, Bsp, 1, [1, 0], [3, 2], [0, 1], [2], [1, 2], [0])
     assert np.allclose(r3, cross, rtol=0, atol=1e-14)
+
+
+# ----------------------------------------------------------- SURVEY App. B integers (timed sizes)
+def _step_stats(cfg):
+    """Per step of a config, from the oracle's layouts only: (elements, subblocks) of the operands and of
+    C~, and the useful GEMM flops sum_c 2 M_c K_c N_c of A~ B~ under the reading-C2 tuples."""
+    kind = cfg["kind"]
+    spaces = {n: (t["cod"], t["dom"]) for n, (t, _) in cfg["tensors"].items()}
+    out = []
+    for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
+        (Ac, Ad), (Bc, Bd) = spaces[na], spaces[nb]
+        pA, qA, pB, qB, pAB, qAB = C.tuples_from_labels(la, lb, lc, ncod)
+        at = L.homspace_layout(kind, *C.permuted_spaces(Ac, Ad, pA, qA))
+        bt = L.homspace_layout(kind, *C.permuted_spaces(Bc, Bd, pB, qB))
+        bcols = {b[0]: (b[1], b[2]) for b in bt.blocks}
+        flops = sum(2 * r * k * bcols[c][1] for (c, r, k, _) in at.blocks if c in bcols)
+        cod, dom = C.output_spaces(Ac, Ad, Bc, Bd, la, lb, lc, ncod)
+        ct = L.homspace_layout(kind, cod, dom)
+        spaces[nc] = (cod, dom)
+        out.append({"A": (at.nelems, len(at.subblocks)), "B": (bt.nelems, len(bt.subblocks)),
+                    "C": (ct.nelems, len(ct.subblocks)), "flops": flops})
+    return out
+
+
+def test_appendix_b_cfg2_cfg3_chains():
+    """SURVEY App. B tables (independent survey scripts): cfg2 and cfg3 per-step operand sizes and flops."""
+    s2 = _step_stats(W.cfg2())
+    assert [x["flops"] for x in s2] == [53773296, 3322556, 3322556, 53773296]
+    assert sum(x["flops"] for x in s2) == 114191704
+    assert [x["A"] for x in s2] == [(122884, 49), (484894, 194), (484894, 194), (484894, 194)]
+    assert [x["B"] for x in s2] == [(98032, 66), (34, 10), (34, 10), (122884, 49)]
+    assert [x["C"] for x in s2] == [(484894, 194)] * 3 + [(98032, 66)]
+    s3 = _step_stats(W.cfg3())
+    assert [x["flops"] for x in s3] == [433399764, 60924864, 60924864, 433419928]
+    assert sum(x["flops"] for x in s3) == 988669420
+    assert [x["A"] for x in s3] == [(521456, 701), (6732096, 9756), (6732096, 9756), (6732096, 9756)]
+    assert [x["B"] for x in s3] == [(708260, 2008), (176, 44), (176, 44), (521456, 701)]
+    assert [x["C"] for x in s3] == [(6732096, 9756)] * 3 + [(708260, 2008)]
+    th = W.cfg3()["tensors"]["theta"][0]
+    lt = L.homspace_layout("fU1xU1", th["cod"], th["dom"])
+    assert (lt.nelems, len(lt.subblocks), len(lt.blocks)) == (708260, 2008, 157)
+
+
+@pytest.mark.parametrize("d_leg,elems,subs,blocks,flops", [
+    (64, 854974, 4579, 37, 409405460),
+    (128, 13569540, 5340, 39, 25757272064),
+    (320, 534794900, 6181, 41, 6401382315008),
+    (384, 1110720212, 6181, 41, 19215054235248),
+])
+def test_appendix_b_cfg4(d_leg, elems, subs, blocks, flops):
+    """stored elements, subblocks, GEMM blocks and useful flops per D_leg
+    (ComplexF64 at D_leg 320: 4x the real count, reading C21)."""
+    cfg = W.cfg4(d_leg=d_leg)
+    A = cfg["tensors"]["A"][0]
+    lt = L.homspace_layout("U1", A["cod"], A["dom"])
+    assert (lt.nelems, len(lt.subblocks)) == (elems, subs)
+    st = _step_stats(cfg)[0]
+    assert st["flops"] == flops and st["C"][0] == elems
+    (_, la, _, lb, _, lc, ncod) = cfg["steps"][0]
+    pA, qA, _, _, _, _ = C.tuples_from_labels(la, lb, lc, ncod)
+    at = L.homspace_layout("U1", *C.permuted_spaces(A["cod"], A["dom"], pA, qA))
+    assert len(at.blocks) == blocks
