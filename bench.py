@@ -28,8 +28,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CHAIN_CFGS = (2, 3, 5, 6, 7, 8)
-GEMM_KERNEL = "gemm_mbar_kernel (grouped DMMA GEMM over the coupled sectors)"   # the DMRG-shaped chains (Alg. 11 / 12 contractions), timed beside cfg4
+CHAIN_CFGS = (2, 3, 5, 6, 7, 8)   # the DMRG-shaped chains (Alg. 11 / 12 contractions), timed beside cfg4
+GEMM_KERNEL = ("gemm_tma_kernel (persistent, TMA-fed grouped DMMA GEMM over the coupled sectors; big tiles) "
+               "+ gemm_small_kernel (edge classes)")
 
 
 def load_peaks():
@@ -233,7 +234,7 @@ def measure_fp64_peak(stream, dev):
             "cublas_dgemm_8192_tflops": round(best, 3)}
 
 
-def time_chains(dev, stream, peak_flops, hbm_bytes_s, reps=30):
+def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
     """Every DMRG-shaped chain (cfg2/3/5/6/7/8 at their full sizes) replayed as ONE CUDA graph; L2 is
     flushed (a 256 MB write) before every timed replay; median of `reps` CUDA-event timings. Roofline per
     SURVEY §8(d): sum over steps of tk_contract_roofline (GEMM blocks max(flops/P, bytes/BW) + permute
@@ -242,6 +243,8 @@ def time_chains(dev, stream, peak_flops, hbm_bytes_s, reps=30):
     from paper_2508_10076_b200 import tk, layout_io
     from workloads import configs as W
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(dev)          # graphs are captured (and replayed) on a side stream
+    stream.wait_stream(stream0)
     out = {}
     for k in CHAIN_CFGS:
         cfg = W.CONFIGS[k]()
