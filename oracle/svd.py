@@ -94,8 +94,10 @@ def truncation(kind, spectra, max_dim=0, rel_tol=0.0):
 
 
 def truncated_reconstruction(layout, svds, keep):
-    """Reduced flat of sum_c u_c[:, :k] diag(s[:k]) vh_c[:k] in the layout of A~."""
-    flat = np.zeros(layout.nelems)
+    """Reduced flat of sum_c u_c[:, :k] diag(s[:k]) vh_c[:k] in the layout of A~ (complex blocks give a
+    complex flat)."""
+    cplx = any(np.iscomplexobj(u) for _, u, _, _ in svds)
+    flat = np.zeros(layout.nelems, dtype=np.complex128 if cplx else np.float64)
     for b, (c, u, s, vh) in enumerate(svds):
         k = keep[b]
         _, rows, cols, off = layout.blocks[b]
