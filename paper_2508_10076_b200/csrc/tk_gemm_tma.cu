@@ -44,12 +44,22 @@ size_t gemm_tma_smem_bytes() { return (size_t)STAGES * STAGE_BYTES + 2 * STAGES 
 // The TMA producer is lane 0 of warp 0 (a separate producer warp would be a 17th warp: 5 warps on one
 // SM sub-partition caps registers at 96 and spills the accumulators). It keeps its own cursor over the
 // CTA's (tile, k-slice) sequence, PD slices ahead of the consumers, continuing into the next tile.
+// Tiles are handed out dynamically (one atomicAdd per tile on a counter the host zeroes before the
+// launch), in the planner's order (long K first, L2-banded raster order): the tiles in flight on the
+// 148 SMs stay a contiguous window of that order, which keeps the A / B panels of a band in L2. The
+// producer posts each fetched tile index into a small shared-memory ring (read by the consumers once
+// the tile's first slice has landed); past the last tile it posts -1 and completes one extra "full"
+// phase without data, which ends the consumers' loop.
+constexpr int kRing = 8;  // > STAGES: a ring entry is overwritten only after every warp has read it
 struct TmaCursor {
-  int t, kt, nk, m0, n0, mi;
+  int t, kt, nk, m0, n0, mi, j;  // t < 0: no tiles left (end posted)
 };
 
-__device__ __forceinline__ void tma_cursor_tile(const GemmTmaParams& p, TmaCursor& c) {
-  if (c.t < p.ntiles) {
+__device__ __forceinline__ void tma_next_tile(const GemmTmaParams& p, TmaCursor& c, int* ring) {
+  c.t = atomicAdd(p.counter, 1);
+  if (c.t >= p.ntiles) c.t = -1;
+  ring[c.j++ % kRing] = c.t;
+  if (c.t >= 0) {
     const GemmTile& T = p.tiles[c.t];
     c.kt = 0;
     c.nk = (T.g.K + BK - 1) / BK;
@@ -61,24 +71,28 @@ __device__ __forceinline__ void tma_cursor_tile(const GemmTmaParams& p, TmaCurso
   }
 }
 
-// issue the loads of load iteration `it` (if any are left) and advance the cursor
+// issue the loads of load iteration `it` and advance the cursor; after the last tile, one data-less
+// phase of the next slot carries the end marker; afterwards nothing
 __device__ __forceinline__ void tma_produce(const GemmTmaParams& p, TmaCursor& c, uint32_t& it, double* As,
-                                            double* Bs, uint64_t* full, uint64_t* empty) {
-  if (c.t >= p.ntiles) return;
+                                            double* Bs, uint64_t* full, uint64_t* empty, int* ring) {
+  if (c.t == -2) return;
   const int s = (int)(it % STAGES);
   if (it >= (uint32_t)STAGES) mbar_wait(&empty[s], ((it / STAGES) & 1u) ^ 1u);
+  ++it;
+  if (c.t < 0) {  // end marker (already in the ring): release the waiting consumers
+    mbar_arrive(&full[s]);
+    c.t = -2;
+    return;
+  }
   mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
   tma_load_2d(As + s * A_STAGE, &p.amap[c.mi], c.m0, c.kt * BK, &full[s]);
   tma_load_2d(Bs + s * B_STAGE, &p.bmap[c.mi], c.kt * BK, c.n0, &full[s]);
-  ++it;
-  if (++c.kt == c.nk) {
-    c.t += gridDim.x;
-    tma_cursor_tile(p, c);
-  }
+  if (++c.kt == c.nk) tma_next_tile(p, c, ring);
 }
 
 __global__ void __launch_bounds__(THREADS, 1) gemm_tma_kernel(const __grid_constant__ GemmTmaParams p) {
   extern __shared__ __align__(1024) double tma_smem[];
+  __shared__ int ring[kRing];
   double* As = tma_smem;
   double* Bs = tma_smem + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_STAGE);
@@ -94,19 +108,24 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tma_kernel(const __grid_const
   }
   __syncthreads();
   pdl_trigger();
-  pdl_wait();  // A~ / B~ are written by the preceding permute kernels
-  TmaCursor cur{(int)blockIdx.x, 0, 0, 0, 0, 0};
+  pdl_wait();  // A~ / B~ are written by the preceding permute kernels (and the counter is zeroed)
+  TmaCursor cur{0, 0, 0, 0, 0, 0, 0};
   uint32_t load_it = 0;
   if (producer) {
-    tma_cursor_tile(p, cur);
-    for (int d = 0; d < PD; ++d) tma_produce(p, cur, load_it, As, Bs, full, empty);
+    tma_next_tile(p, cur, ring);
+    for (int d = 0; d < PD; ++d) tma_produce(p, cur, load_it, As, Bs, full, empty, ring);
   }
 
   // ---------------- consumers
   const int wm = warp & 3, wn = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
   uint32_t it = 0;
-  for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+  for (int j = 0;; ++j) {
+    // the next tile's first slice (or the end marker): its landing publishes the ring entry
+    if (producer) tma_produce(p, cur, load_it, As, Bs, full, empty, ring);
+    mbar_wait(&full[it % STAGES], (it / STAGES) & 1u);
+    const int t = ring[j % kRing];
+    if (t < 0) break;
     const int m0 = p.tiles[t].m0, n0 = p.tiles[t].n0;
     const GemmGroup g = p.tiles[t].g;
     const int nk = (g.K + BK - 1) / BK;
@@ -117,11 +136,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tma_kernel(const __grid_const
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int jj = 0; jj < 4; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
     for (int kt = 0; kt < nk; ++kt, ++it) {
-      if (producer) tma_produce(p, cur, load_it, As, Bs, full, empty);  // slice it + PD
       const int s = (int)(it % STAGES);
-      mbar_wait(&full[s], (it / STAGES) & 1u);
+      if (kt > 0) {
+        if (producer) tma_produce(p, cur, load_it, As, Bs, full, empty, ring);  // slice it + PD
+        mbar_wait(&full[s], (it / STAGES) & 1u);
+      }
       const double* as = As + s * A_STAGE + wm * 32 + gq;
       const double* bs = Bs + s * B_STAGE + (wn * 32 + gq) * BPITCH + tq;
       if (mf == 4 && nf == 4) {  // interior warps: the full 4 x 4 fragment grid, no guards

@@ -21,6 +21,7 @@ struct alignas(64) GemmTmaParams {
   CUtensorMap bmap[kTmaMaxGroups];
   double* C;
   const GemmTile* tiles;
+  int* counter;  // dynamic tile scheduler: zeroed (cudaMemsetAsync) before every launch
   int ntiles, pad_;
   double alpha, beta;
 };

@@ -611,7 +611,7 @@ struct ContractPlan {
   std::vector<int64_t> gslots;
   int g_kmax = 0, g_nmax = 0;
   DevBuf d_gsegs, d_btab, d_gslots;
-  size_t off_a = 0, off_b = 0, off_c = 0, ws_bytes = 0;
+  size_t off_a = 0, off_b = 0, off_c = 0, off_counter = 0, ws_bytes = 0;
   double flops = 0;
   // persistent TMA GEMM for the big tiles (tk_gemm_tma.cu): groups with a tensor-map pair, and the
   // maps encoded for the last (A~, B~) workspace pointers seen (re-encoded when they change)
@@ -1177,6 +1177,8 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
       P.tma = true;
       P.tma_groups.resize(mi.size());
       for (auto& kv : mi) P.tma_groups[kv.second] = kv.first;
+      P.off_counter = P.ws_bytes;  // the dynamic tile scheduler's counter (zeroed before each launch)
+      P.ws_bytes = align256(P.ws_bytes + 4);
     }
   }
   P.tiles = big;
@@ -1587,6 +1589,8 @@ static void run_contract(ContractPlan* P, const void* a, const void* b, void* c,
         std::unique_ptr<GemmTmaParams> q(prm);
         q->C = Ct;
         q->tiles = d_tiles;
+        q->counter = (int*)(w + P->off_counter);
+        check_cuda(cudaMemsetAsync(q->counter, 0, sizeof(int), st), "tile counter reset");
         q->ntiles = nbig;
         q->alpha = ga;
         q->beta = gb;

@@ -21,14 +21,16 @@ TOL = 1e-12
 
 def _run(kind, cod, dom, x, p, q, max_dim=0, rel_tol=0.0):
     from paper_2508_10076_b200 import tk
-    A = tk.tensor_from_spec({"cod": cod, "dom": dom})
+    cplx = np.iscomplexobj(x)
+    A = tk.tensor_from_spec({"cod": cod, "dom": dom}, tk.TK_C64 if cplx else tk.TK_F64)
     a = torch.from_numpy(x).cuda()
     nb = tk.tk_svd_workspace(A, p, q)
     ws = torch.empty(nb // 8 + 64, dtype=torch.float64, device="cuda")
     tk.tk_svd(A, a, p, q, ws, ws.numel() * 8)
     spec = tk.tk_svd_spectrum(A, p, q, ws)
     Wsp, U, S, Vh, err, nrm = tk.tk_svd_truncate(A, p, q, ws, max_dim, rel_tol)
-    bufs = [torch.full((T.nelems,), float("nan"), dtype=torch.float64, device="cuda") for T in (U, S, Vh)]
+    bufs = [torch.full((T.nelems,), float("nan"), dtype=torch.complex128 if cplx else torch.float64, device="cuda")
+            for T in (U, S, Vh)]
     tk.tk_svd_extract(A, p, q, ws, U, bufs[0], S, bufs[1], Vh, bufs[2])
     torch.cuda.synchronize()
     wsec, wdeg = Wsp.sectors()
@@ -65,10 +67,10 @@ def _check(kind, cod, dom, x, p, q, max_dim=0, rel_tol=0.0):
     # isometries, block by block: U^T U = 1, Vh Vh^T = 1
     for (c, rows, cols, off) in lu.blocks:
         m = u[off:off + rows * cols].reshape(rows, cols, order="F")
-        assert np.abs(m.T @ m - np.eye(cols)).max() <= 1e-12
+        assert np.abs(m.conj().T @ m - np.eye(cols)).max() <= 1e-12
     for (c, rows, cols, off) in lv.blocks:
         m = vh[off:off + rows * cols].reshape(rows, cols, order="F")
-        assert np.abs(m @ m.T - np.eye(rows)).max() <= 1e-12
+        assert np.abs(m @ m.conj().T - np.eye(rows)).max() <= 1e-12
 
 
 CASES = [
@@ -92,6 +94,45 @@ def test_svd_small(case, max_dim, rel_tol):
     _check(kind, cod, dom, x, p, q, max_dim, rel_tol)
 
 
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}_{i}" for i, c in enumerate(CASES)])
+@pytest.mark.parametrize("max_dim,rel_tol", [(0, 0.0), (12, 0.0)])
+def test_svd_small_complex(case, max_dim, rel_tol):
+    """ComplexF64 (unitary Jacobi: column q rephased by conj(gamma / |gamma|), then a real rotation)."""
+    kind, secs, cod_d, dom_d, p, q = case
+    V = W.space(kind, secs)
+    cod = [W.dual(V) if d else V for d in cod_d]
+    dom = [W.dual(V) if d else V for d in dom_d]
+    lt = OL.homspace_layout(kind, cod, dom)
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal(lt.nelems) + 1j * rng.standard_normal(lt.nelems)
+    _check(kind, cod, dom, x, p, q, max_dim, rel_tol)
+
+
+def test_svd_rank_deficient_and_graded():
+    """Blocks of low rank (exact zero singular values) and with singular values spread over 12 decades:
+    the spectrum stays accurate to eps ||A|| and U, Vh stay isometric."""
+    V = W.space("U1", [((-1,), 20), ((0,), 33), ((1,), 17)])
+    cod, dom = [V, V], [V]
+    lt = OL.homspace_layout("U1", cod, dom)
+    rng = np.random.default_rng(11)
+    x = np.zeros(lt.nelems)
+    for (c, rows, cols, off) in lt.blocks:
+        r = max(1, min(rows, cols) // 3)
+        m = rng.standard_normal((rows, r)) @ np.diag(10.0 ** -rng.uniform(0, 12, r)) @ rng.standard_normal((r, cols))
+        x[off:off + rows * cols] = m.reshape(-1, order="F")
+    _check("U1", cod, dom, x, [0, 1], [2], 0, 0.0)
+
+
+def test_svd_block_larger_than_2048():
+    """A single 2200 x 2100 block (min(rows, cols) > 2048: the round-1 limit) runs on an 8-CTA cluster
+    with its rows in the workspace."""
+    V = W.space("U1", [((0,), 2200)])
+    Wd = W.space("U1", [((0,), 2100)])
+    lt = OL.homspace_layout("U1", [V], [Wd])
+    x = np.random.default_rng(12).standard_normal(lt.nelems)
+    _check("U1", [V], [Wd], x, [0], [1], 1000, 0.0)
+
+
 def _two_site(cfg):
     from tests import harness as H
     spec, idx = cfg["tensors"]["theta"]
@@ -107,6 +148,15 @@ def test_svd_two_site(cfgfun, max_dim):
     cfg = cfgfun()
     cod, dom, x = _two_site(cfg)
     _check(cfg["kind"], cod, dom, x, [0, 1], [2, 3], max_dim)
+
+
+@pytest.mark.parametrize("cfgfun,max_dim", [(lambda: W.cfg2(), 512), (lambda: W.cfg3(chi=256), 256)],
+                         ids=["cfg2", "cfg3"])
+def test_svd_two_site_complex(cfgfun, max_dim):
+    cfg = cfgfun()
+    cod, dom, x = _two_site(cfg)
+    xi = np.random.default_rng(13).standard_normal(x.shape)
+    _check(cfg["kind"], cod, dom, x + 1j * xi, [0, 1], [2, 3], max_dim)
 
 
 def test_svd_su2_mps():

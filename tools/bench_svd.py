@@ -20,10 +20,13 @@ from workloads import configs as W  # noqa: E402
 
 
 def cases():
-    c2, c3, c6 = W.cfg2(), W.cfg3(), W.cfg6()
-    return [("cfg2 theta (alpha,s1 | s2,beta), max_dim 512", c2, "theta", [0, 1], [2, 3], 512),
-            ("cfg3 theta (alpha,s1 | s2,beta), max_dim 2048", c3, "theta", [0, 1], [2, 3], 2048),
-            ("cfg6 A (alpha,s | beta), max_dim 1172", c6, "A", [0, 1], [2], 1172)]
+    c2, c3, c6, c7, c8 = W.cfg2(), W.cfg3(), W.cfg6(), W.cfg7(), W.cfg8()
+    return [("cfg2 theta (alpha,s1 | s2,beta), max_dim 512", c2, "theta", [0, 1], [2, 3], 512, False),
+            ("cfg3 theta (alpha,s1 | s2,beta), max_dim 2048", c3, "theta", [0, 1], [2, 3], 2048, False),
+            ("cfg3 theta ComplexF64, max_dim 2048", c3, "theta", [0, 1], [2, 3], 2048, True),
+            ("cfg6 A (alpha,s | beta), max_dim 1172", c6, "A", [0, 1], [2], 1172, False),
+            ("cfg7 theta (alpha,s1 | s2,beta), max_dim 2058", c7, "theta", [0, 1], [2, 3], 2058, False),
+            ("cfg8 theta (alpha,s1 | s2,beta), max_dim 2008", c8, "theta", [0, 1], [2, 3], 2008, False)]
 
 
 def main():
@@ -31,10 +34,11 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--oracle", action="store_true")
     args = ap.parse_args()
-    for name, cfg, tname, p, q, md in cases():
+    for name, cfg, tname, p, q, md, cplx in cases():
         spec, idx = cfg["tensors"][tname]
-        A = tk.tensor_from_spec(spec)
-        a = torch.from_numpy(layout_io.fill(A, cfg["cfg"], idx)).cuda()
+        A = tk.tensor_from_spec(spec, tk.TK_C64 if cplx else tk.TK_F64)
+        a = torch.from_numpy(layout_io.fill(A, cfg["cfg"], idx, cplx)).cuda()
+        tdt = torch.complex128 if cplx else torch.float64
         nb = tk.tk_svd_workspace(A, p, q)
         ws = torch.empty(nb // 8 + 64, dtype=torch.float64, device="cuda")
         spec_ = None
@@ -48,7 +52,7 @@ def main():
             h0 = time.perf_counter()
             Wsp, U, S, Vh, err, nrm = tk.tk_svd_truncate(A, p, q, ws, md, 0.0)
             h1 = time.perf_counter()
-            bufs = [torch.empty(T.nelems, dtype=torch.float64, device="cuda") for T in (U, S, Vh)]
+            bufs = [torch.empty(T.nelems, dtype=tdt, device="cuda") for T in (U, S, Vh)]
             x0 = torch.cuda.Event(enable_timing=True)
             x0.record()
             tk.tk_svd_extract(A, p, q, ws, U, bufs[0], S, bufs[1], Vh, bufs[2])
@@ -67,7 +71,7 @@ def main():
             from oracle import svd as OS, layout as OL
             from tests import harness as H
             lt = OL.homspace_layout(cfg["kind"], spec["cod"], spec["dom"])
-            x = H.oracle_flat(lt, cfg["cfg"], idx)
+            x = H.oracle_flat(lt, cfg["cfg"], idx, cplx)
             t0 = time.perf_counter()
             lp, xp, _ = OS.permuted(cfg["kind"], spec["cod"], spec["dom"], x, p, q)
             svds = OS.block_svd(lp, xp)
