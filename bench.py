@@ -511,12 +511,15 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "c64"],
                     help="f64: the BASELINE metric (D_leg 384); c64: cfg4's ComplexF64 variant (D_leg 320)")
     ap.add_argument("--d-leg", type=int, default=None)
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="end-to-end steps (host buffers, copies inside the timed region); default: --steps")
     ap.add_argument("--cpu-budget-s", type=float, default=24.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-chains", action="store_true", help="skip the cfg2/3/5/6/7/8 chain timings")
     args = ap.parse_args()
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
     if args.d_leg is None:
         args.d_leg = 320 if args.dtype == "c64" else 384
     if args.impl == "reference":
