@@ -806,10 +806,206 @@ __global__ void __launch_bounds__(kPermThreads, 3)
   }
 }
 
+// ---- bulk-box permute (BoxRef in tk_kernels.hpp)
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+struct BulkBox {
+  int64_t sbase, dbase;  // element offsets of (0, i1b, i2b, rest) in source / destination
+  int64_t s1, d2;        // source stride of leg 1, destination stride of leg 2 (elements)
+  int32_t n0, m1, m2, g;
+  double c;
+  int64_t dd1, dd2;      // destination member's complex-mode offsets
+};
+
+// box lb of ref ri (boxes of a group < 2^31, host-checked)
+template <int CM>
+__device__ __forceinline__ BulkBox bulk_box(const PermOp& op, const BoxRef* __restrict__ refs, int ri, uint32_t lb) {
+  const PermGroup& g = op.groups[refs[ri].group];
+  const PermMember ms = op.members[g.src_mem], md = op.members[g.dst_mem];
+  uint32_t b = lb;
+  const int T1 = g.T0, T2 = g.Tt, c1 = g.ct, c2 = g.R;
+  const int b1 = (int)(b % (uint32_t)T1);
+  b /= (uint32_t)T1;
+  const int b2 = (int)(b % (uint32_t)T2);
+  uint32_t rest = b / (uint32_t)T2;
+  BulkBox x;
+  x.sbase = ms.off;
+  x.dbase = md.off;
+  for (int l = 3; l < g.ndim; ++l) {
+    const uint32_t e = (uint32_t)g.ext[l], q = rest / e, i = rest - q * e;
+    rest = q;
+    x.sbase += (int64_t)i * (g.sa[l] + ms.ld * g.sb[l]);
+    x.dbase += (int64_t)i * (g.da[l] + md.ld * g.db[l]);
+  }
+  x.n0 = g.ext[0];
+  const int i1b = b1 * c1, i2b = b2 * c2;
+  x.m1 = min(c1, g.ext[1] - i1b);
+  x.m2 = min(c2, g.ext[2] - i2b);
+  x.s1 = g.sa[1] + ms.ld * g.sb[1];
+  x.d2 = g.da[2] + md.ld * g.db[2];
+  x.sbase += (int64_t)i1b * x.s1 + (int64_t)i2b * x.n0;  // leg 2: source stride n0
+  x.dbase += (int64_t)i1b * x.n0 + (int64_t)i2b * x.d2;  // leg 1: destination stride n0
+  x.c = op.alpha * op.coefs[g.coef_off];
+  x.g = ri;
+  x.dd1 = md.d1;
+  x.dd2 = md.d2;
+  return x;
+}
+
+// a CTA's boxes form one contiguous range of the box order (neighbouring boxes of a group are
+// neighbours in memory); the cursor advances without searching
+struct BoxCursor {
+  int ri;        // current ref
+  uint32_t lb;   // box within the ref's group
+  uint32_t nb;   // boxes of that group
+};
+__device__ __forceinline__ uint32_t ref_boxes(const BoxRef* __restrict__ refs, int nrefs, int ri, int64_t nboxes) {
+  const int64_t end = ri + 1 < nrefs ? __ldg(&refs[ri + 1].first) : nboxes;
+  return (uint32_t)(end - __ldg(&refs[ri].first));
+}
+
+template <int CM>
+__global__ void __launch_bounds__(kBulkThreads, kBulkCTAs)
+    permute_bulk_kernel(PermOp op, const BoxRef* __restrict__ refs, int nrefs, long long nboxes) {
+  using IO = CIO<CM>;
+  using V = typename IO::V;
+  using S = typename IO::S;
+  constexpr int ES = (int)sizeof(S);  // source element bytes (8: a run needs a 16-byte envelope)
+  extern __shared__ __align__(128) double bulk_dyn[];
+  __shared__ __align__(8) uint64_t bar[kBulkNB];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kBulkNB; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  const S* src = (const S*)op.src;
+  auto* dst = (typename IO::D*)op.dst;
+  // slot pitch of a source run in a buffer (elements of S): run + envelope, rounded to 16 bytes
+  auto pitch = [](const BulkBox& x) {
+    const int run = x.n0 * x.m2;
+    return ES == 8 ? ((run + 3) & ~1) : run;
+  };
+  // warp 0 fetches box x into buffer buf: one bulk copy per source run (16-byte aligned envelope)
+  auto fetch = [&](const BulkBox& x, int buf) {
+    if (tid >= 32) return;
+    S* B = reinterpret_cast<S*>(bulk_dyn) + (size_t)buf * (kBulkBuf * 8 / ES);
+    const int P = pitch(x);
+    const uint32_t run_bytes = (uint32_t)(x.n0 * x.m2) * ES;
+    uint32_t bytes = 0;
+    for (int i1 = lane; i1 < x.m1; i1 += 32) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src + x.sbase + (int64_t)i1 * x.s1);
+      bytes += (uint32_t)(((a + run_bytes + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    if (lane == 0) {
+      fence_proxy_async();  // the buffer was last read through the generic proxy
+      mbar_arrive_expect_tx(&bar[buf], bytes);
+    }
+    __syncwarp();
+    for (int i1 = lane; i1 < x.m1; i1 += 32) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src + x.sbase + (int64_t)i1 * x.s1);
+      const uintptr_t a0 = a & ~uintptr_t(15);
+      bulk_g2s(B + (size_t)i1 * P, reinterpret_cast<const void*>(a0),
+               (uint32_t)(((a + run_bytes + 15) & ~uintptr_t(15)) - a0), &bar[buf]);
+    }
+  };
+  // this CTA's contiguous range [b0, b1) of the box order; the first box's ref by binary search (once)
+  const int64_t b0 = nboxes * blockIdx.x / gridDim.x, b1 = nboxes * (blockIdx.x + 1) / gridDim.x;
+  if (b0 >= b1) return;
+  BoxCursor cs;
+  {
+    int lo = 0, hi = nrefs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&refs[mid].first) <= b0) lo = mid; else hi = mid - 1;
+    }
+    cs.ri = lo;
+    cs.lb = (uint32_t)(b0 - __ldg(&refs[lo].first));
+    cs.nb = ref_boxes(refs, nrefs, lo, nboxes);
+  }
+  auto advance = [&]() {
+    if (++cs.lb == cs.nb) {
+      ++cs.ri;
+      cs.lb = 0;
+      if (cs.ri < nrefs) cs.nb = ref_boxes(refs, nrefs, cs.ri, nboxes);
+    }
+  };
+  // kBulkNB buffers: boxes u + 1 .. u + kBulkNB - 1 stream in while box u is written out
+  BulkBox cur = bulk_box<CM>(op, refs, cs.ri, cs.lb), nx1{};
+  fetch(cur, 0);
+  if (kBulkNB >= 3 && b0 + 1 < b1) {
+    advance();
+    nx1 = bulk_box<CM>(op, refs, cs.ri, cs.lb);
+    fetch(nx1, 1);
+  }
+  int64_t bx = b0;
+  for (int u = 0; bx < b1; ++bx, ++u) {
+    const int buf = u % kBulkNB;
+    BulkBox nx2{};
+    if (kBulkNB >= 3 && bx + 2 < b1) {
+      advance();
+      nx2 = bulk_box<CM>(op, refs, cs.ri, cs.lb);
+      fetch(nx2, (u + 2) % kBulkNB);  // that buffer held box u - 1, released by the barrier ending u - 1
+    }
+    if (kBulkNB == 2 && bx + 1 < b1) {  // double buffering: box u + 1 into the other buffer
+      advance();
+      nx1 = bulk_box<CM>(op, refs, cs.ri, cs.lb);
+      fetch(nx1, (u + 1) % kBulkNB);
+    }
+    mbar_wait(&bar[buf], (uint32_t)((u / kBulkNB) & 1));
+    // destination runs: i2 major, contiguous over e = i1 * n0 + i0; (i2, i1, i0) advanced by a fixed
+    // stride without divisions per element
+    const S* B = reinterpret_cast<const S*>(bulk_dyn) + (size_t)buf * (kBulkBuf * 8 / ES);
+    const int P = pitch(cur), n0 = cur.n0, m1 = cur.m1;
+    const uint32_t L = (uint32_t)n0 * m1, tot = L * cur.m2;
+    const int sph = ES == 8 ? (int)((reinterpret_cast<uintptr_t>(src + cur.sbase) >> 3) & 1) : 0;
+    const int s1ph = (int)(cur.s1 & 1);
+    uint32_t t = tid;
+    uint32_t i2 = t / L, e = t - i2 * L;
+    uint32_t i1 = e / (uint32_t)n0, i0 = e - i1 * (uint32_t)n0;
+    const uint32_t q2 = kBulkThreads / L, r2 = kBulkThreads - q2 * L;
+    const uint32_t q0 = r2 / (uint32_t)n0, r0 = r2 - q0 * (uint32_t)n0;
+    for (; t < tot; t += kBulkThreads) {
+      const int ph = ES == 8 ? ((sph + (int)i1 * s1ph) & 1) : 0;
+      const V x = B[(int64_t)i1 * P + ph + i2 * n0 + i0];  // S == V for every bulk mode (not planar)
+      IO::store(dst, cur.dbase + (int64_t)i2 * cur.d2 + i1 * n0 + i0, cur.dd1, cur.dd2, Num<V>::scale(cur.c, x),
+                op.beta, op.ims);
+      i2 += q2;
+      i0 += r0;
+      i1 += q0;
+      if (i0 >= (uint32_t)n0) {
+        i0 -= n0;
+        ++i1;
+      }
+      if (i1 >= (uint32_t)m1) {
+        i1 -= m1;
+        ++i2;
+      }
+    }
+    __syncthreads();  // buffer `buf` is refilled by the fetch of box u + kBulkNB
+    cur = nx1;
+    if (kBulkNB >= 3) nx1 = nx2;
+  }
+}
+
 template <int CM>
 static cudaError_t set_permute_attrs() {
   cudaError_t e = cudaFuncSetAttribute(permute_kernel<CM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kTileElems * (int)sizeof(typename CIO<CM>::V));
+  if constexpr (CM != kPermPlanarToC)
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(permute_bulk_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkNB * kBulkBuf * 8);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(permute_recouple_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kRecoupleStage * 8);
@@ -829,6 +1025,21 @@ static cudaError_t launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs
     e = launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, kRecoupleStage * 8, st, op0, op1,
                  jobs + njobs);
   return e;
+}
+
+cudaError_t launch_permute_bulk(const PermOp& op, const BoxRef* refs, int nrefs, int64_t nboxes, int grid, int cm,
+                                cudaStream_t st) {
+  const size_t smem = kBulkNB * kBulkBuf * 8;
+  const long long nb = (long long)nboxes;
+  switch (cm) {
+    case kPermReal: return launch_k(permute_bulk_kernel<kPermReal>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
+    case kPermCToC: return launch_k(permute_bulk_kernel<kPermCToC>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
+    case kPermCToPlanar:
+      return launch_k(permute_bulk_kernel<kPermCToPlanar>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
+    case kPermCToRealRep:
+      return launch_k(permute_bulk_kernel<kPermCToRealRep>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,
@@ -1165,62 +1376,6 @@ __global__ void __launch_bounds__(MbarCfg::THREADS, 1)
   gemm_tile_mbar<TK_MBAR, PD>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem);
 }
 
-#ifndef TK_SMALL_STAGES
-#define TK_SMALL_STAGES 3
-#endif
-#ifndef TK_SMALL_WN
-#define TK_SMALL_WN 16  // warp tile 32 x WN (16: 8 warps per 64 x 64 tile)
-#endif
-#define TK_SMALL 64, 64, 32, TK_SMALL_WN, 16, TK_SMALL_STAGES
-#ifndef TK_SMALL_MINB
-#define TK_SMALL_MINB 2
-#endif
-using SmallCfg = GemmCfg<TK_SMALL>;
-
-__global__ void __launch_bounds__(SmallCfg::THREADS, TK_SMALL_MINB)
-    gemm_small_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                      double beta, int base_vec, double* __restrict__ parts) {
-  extern __shared__ __align__(16) double smem[];
-  pdl_trigger();
-  const GemmTile t = tiles[blockIdx.x];
-  const GemmGroup& g = t.g;
-  pdl_wait();
-  double* part = t.slot >= 0 ? parts + (int64_t)t.slot * (64 * 64) : nullptr;
-  gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem, t.k0, t.k1, part);
-}
-
-// split-K reduction of 64 x 64 tiles: C = alpha * sum_s partial_s + beta * C, summed in slot order
-// (deterministic). gridDim.y = 4 quarters of a tile, one element per thread; all partial loads of an
-// element are issued before the (ordered) sum, so the kernel costs about one L2 round trip.
-constexpr int kSplitMax = 16;
-__global__ void __launch_bounds__(256)
-    gemm_splitk_reduce_kernel(double* __restrict__ C, const GemmGroup* __restrict__ groups,
-                              const GemmTile* __restrict__ heads, const double* __restrict__ parts, double alpha,
-                              double beta) {
-  pdl_trigger();
-  const GemmTile t = heads[blockIdx.x];
-  const GemmGroup& g = t.g;
-  pdl_wait();
-  double* Cg = C + g.c_off;
-  for (int e = blockIdx.y * 1024 + threadIdx.x; e < (blockIdx.y + 1) * 1024; e += 256) {
-    const int ml = e % 64, nl = e / 64;
-    const int m = t.m0 + ml, n = t.n0 + nl;
-    if (m >= g.M || n >= g.N) continue;
-    double x[kSplitMax];
-#pragma unroll
-    for (int sidx = 0; sidx < kSplitMax; ++sidx)
-      x[sidx] = sidx < t.nsplit ? parts[(int64_t)(t.slot + sidx) * (64 * 64) + e] : 0.0;
-    double acc = 0.0;
-#pragma unroll
-    for (int sidx = 0; sidx < kSplitMax; ++sidx) acc += x[sidx];
-    double* p = Cg + (int64_t)m + (int64_t)n * g.ldc;
-    double v = alpha * acc;
-    if (beta != 0.0) v = fma(beta, *p, v);
-    *p = v;
-  }
-}
-
 // ---- skinny blocks (N, K <= kSkinnyMax; the MPO steps T.W of the DMRG chains, M up to 2e5): a
 // streaming kernel, HBM-bound (AI = 2KN / 8(K+N) < 1 flop/B), so plain FMAs: the K x N operand sits in
 // shared memory, each thread owns rows of A~ / C~, loads A~[m, 0..K) (coalesced across the warp for
@@ -1265,20 +1420,12 @@ __device__ __forceinline__ void skinny_rows(const double* __restrict__ Ag, doubl
   }
 }
 
-#ifdef TK_SKINNY_MINB  // A/B knob; the default leaves the register choice to ptxas (82 registers)
-__global__ void __launch_bounds__(kSkinnyThreads, TK_SKINNY_MINB)
-#else
-__global__ void __launch_bounds__(kSkinnyThreads)
-#endif
-    gemm_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
-                       double beta) {
-  __shared__ double Bs[kSkinnyMax * kSkinnyMax];
-  pdl_trigger();
-  const GemmTile t = tiles[blockIdx.x];
+// one skinny tile (t.pad rows of one group), Bs = kSkinnyMax^2 doubles of shared memory
+__device__ __forceinline__ void skinny_tile(const double* __restrict__ A, const double* __restrict__ B,
+                                            double* __restrict__ C, const GemmTile& t, double alpha, double beta,
+                                            double* Bs) {
   const GemmGroup& g = t.g;
   const int K = g.K, N = g.N;
-  pdl_wait();
   for (int i = threadIdx.x; i < kSkinnyMax * kSkinnyMax; i += kSkinnyThreads) {
     const int k = i / kSkinnyMax, n = i % kSkinnyMax;
     Bs[i] = (k < K && n < N) ? alpha * B[g.b_off + k + (int64_t)n * g.ldb] : 0.0;
@@ -1300,6 +1447,81 @@ __global__ void __launch_bounds__(kSkinnyThreads)
     case 7: skinny_rows<16, 8>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
     default: skinny_rows<16, 16>(Ag, Cg, Bs, g, t.m0, mend, beta); break;
   }
+}
+
+#ifndef TK_SMALL_STAGES
+#define TK_SMALL_STAGES 3
+#endif
+#ifndef TK_SMALL_WN
+#define TK_SMALL_WN 16  // warp tile 32 x WN (16: 8 warps per 64 x 64 tile)
+#endif
+#define TK_SMALL 64, 64, 32, TK_SMALL_WN, 16, TK_SMALL_STAGES
+#ifndef TK_SMALL_MINB
+#define TK_SMALL_MINB 2
+#endif
+using SmallCfg = GemmCfg<TK_SMALL>;
+
+__global__ void __launch_bounds__(SmallCfg::THREADS, TK_SMALL_MINB)
+    gemm_small_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                      const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
+                      double beta, int base_vec, double* __restrict__ parts) {
+  extern __shared__ __align__(16) double smem[];
+  pdl_trigger();
+  const GemmTile t = tiles[blockIdx.x];
+  const GemmGroup& g = t.g;
+  pdl_wait();
+  if (t.tmap < 0) {  // a skinny tile riding in the small-tile launch (one launch fewer per contraction)
+    skinny_tile(A, B, C, t, alpha, beta, smem);
+    return;
+  }
+  double* part = t.slot >= 0 ? parts + (int64_t)t.slot * (64 * 64) : nullptr;
+  gemm_tile<TK_SMALL>(A, B, C, g, t.m0, t.n0, alpha, beta, base_vec && g.vec, smem, t.k0, t.k1, part);
+}
+
+// split-K reduction of 64 x 64 tiles: C = alpha * sum_s partial_s + beta * C, summed in slot order
+// (deterministic). gridDim.y = 4 quarters of a tile, one element per thread; all partial loads of an
+// element are issued before the (ordered) sum, so the kernel costs about one L2 round trip.
+constexpr int kSplitMax = 16;
+__global__ void __launch_bounds__(256)
+    gemm_splitk_reduce_kernel(double* __restrict__ C, const GemmGroup* __restrict__ groups,
+                              const GemmTile* __restrict__ heads, const double* __restrict__ parts, double alpha,
+                              double beta) {
+  pdl_trigger();
+  const GemmTile t = heads[blockIdx.x];
+  const GemmGroup& g = t.g;
+  pdl_wait();
+  double* Cg = C + g.c_off;
+  for (int e = blockIdx.y * 1024 + threadIdx.x; e < (blockIdx.y + 1) * 1024; e += 256) {
+    const int ml = e % 64, nl = e / 64;
+    const int m = t.m0 + ml, n = t.n0 + nl;
+    if (m >= g.M || n >= g.N) continue;
+    double x[kSplitMax];
+#pragma unroll
+    for (int sidx = 0; sidx < kSplitMax; ++sidx)
+      x[sidx] = sidx < t.nsplit ? parts[(int64_t)(t.slot + sidx) * (64 * 64) + e] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int sidx = 0; sidx < kSplitMax; ++sidx) acc += x[sidx];
+    double* p = Cg + (int64_t)m + (int64_t)n * g.ldc;
+    double v = alpha * acc;
+    if (beta != 0.0) v = fma(beta, *p, v);
+    *p = v;
+  }
+}
+
+#ifdef TK_SKINNY_MINB  // A/B knob; the default leaves the register choice to ptxas (82 registers)
+__global__ void __launch_bounds__(kSkinnyThreads, TK_SKINNY_MINB)
+#else
+__global__ void __launch_bounds__(kSkinnyThreads)
+#endif
+    gemm_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                       const GemmGroup* __restrict__ groups, const GemmTile* __restrict__ tiles, double alpha,
+                       double beta) {
+  __shared__ double Bs[kSkinnyMax * kSkinnyMax];
+  pdl_trigger();
+  const GemmTile t = tiles[blockIdx.x];
+  pdl_wait();
+  skinny_tile(A, B, C, t, alpha, beta, Bs);
 }
 
 // ---- gathered skinny GEMM (GatherSeg in tk_kernels.hpp): one thread per row (two for K <= 8) of
@@ -1444,13 +1666,15 @@ cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmG
   if (ntiles_big)
     e = launch_k(gemm_mbar_kernel<TK_MBAR_PD>, ntiles_big, MbarCfg::THREADS, kMbarSmem, st, A, B, C, groups, tiles,
                  alpha, beta, base_vec);
+  // skinny tiles (GemmTile::tmap == -1) ride in the small-tile launch when there is one: the tile
+  // tables are contiguous ([big | small | skinny]) and both use 256-thread CTAs
   if (e == cudaSuccess && ntiles_small)
-    e = launch_k(gemm_small_kernel, ntiles_small, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C, groups,
-                 tiles + ntiles_big, alpha, beta, base_vec, parts);
+    e = launch_k(gemm_small_kernel, ntiles_small + ntiles_skinny, SmallCfg::THREADS, SmallCfg::SMEM, st, A, B, C,
+                 groups, tiles + ntiles_big, alpha, beta, base_vec, parts);
   if (e == cudaSuccess && nsplit_heads)
     e = launch_k2(gemm_splitk_reduce_kernel, dim3(nsplit_heads, 4), 256, 0, st, C, groups, split_heads,
                   (const double*)parts, alpha, beta);
-  if (e == cudaSuccess && ntiles_skinny)
+  if (e == cudaSuccess && ntiles_skinny && !ntiles_small)
     e = launch_k(gemm_skinny_kernel, ntiles_skinny, kSkinnyThreads, 0, st, A, B, C, groups,
                  tiles + ntiles_big + ntiles_small, alpha, beta);
   return e;

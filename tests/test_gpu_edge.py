@@ -257,3 +257,37 @@ def test_bitwise_deterministic(cfgfun):
     r2 = H.gpu_chain(cfg)
     for k in r1:
         assert np.array_equal(r1[k][1], r2[k][1]), k
+
+
+# ------------------------------------------------------------------ bulk-box permute (large permutes)
+@pytest.mark.parametrize("cplx,alpha,beta", [(False, 1.0, 0.0), (False, -0.5, 0.25), (True, 0.75, -1.0)])
+def test_bulk_box_permute_large(cplx, alpha, beta):
+    """A permute above 2^24 elements whose leg 0 stays unit-stride while the next legs swap (the cfg4
+    pattern) runs on permute_bulk_kernel (cp.async.bulk source runs into shared memory, coalesced
+    destination runs); alpha / beta and ComplexF64 (tk_permute: interleaved -> interleaved)."""
+    from paper_2508_10076_b200 import tk
+    from oracle import layout as OL, dense as OD, contract as OC
+    V = W.space("U1", [((-1,), 26), ((0,), 39), ((1,), 26)])
+    cod, dom = [V, V], [V, V]
+    p, q = [0, 2], [1, 3]          # A (x1, x2; x3, x4) -> (x1, x3; x2, x4)
+    lt = OL.homspace_layout("U1", cod, dom)
+    assert lt.nelems >= 1 << 24
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal(lt.nelems) + (1j * rng.standard_normal(lt.nelems) if cplx else 0.0)
+    c2, d2 = OC.permuted_spaces(cod, dom, p, q)
+    ls = OL.homspace_layout("U1", c2, d2)
+    y0 = rng.standard_normal(ls.nelems) + (1j * rng.standard_normal(ls.nelems) if cplx else 0.0)
+    dt = tk.TK_C64 if cplx else tk.TK_F64
+    A = tk.tensor_from_spec({"cod": cod, "dom": dom}, dt)
+    C = tk.tensor_from_spec({"cod": c2, "dom": d2}, dt)
+    a = torch.from_numpy(x).cuda()
+    c = torch.from_numpy(y0.copy()).cuda() if beta != 0 else torch.full((ls.nelems,), float("nan"),
+                                                                           dtype=a.dtype, device="cuda")
+    tk.tk_permute(A, a, p, q, C, c, alpha=alpha, beta=beta)
+    torch.cuda.synchronize()
+    assert tk.tk_last_launch_count() >= 1
+    # the permute is a bijection of subblocks: compare subblock by subblock (no dense embedding needed)
+    ref = OD.from_dense(ls, OC.permute_dense(OD.to_dense(lt, x), [OD.parity_vector(s) for s in cod + dom], 2, p, q))
+    want = alpha * ref + (beta * y0 if beta != 0 else 0.0)
+    got = c.cpu().numpy()
+    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
