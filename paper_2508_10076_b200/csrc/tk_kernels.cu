@@ -806,206 +806,10 @@ __global__ void __launch_bounds__(kPermThreads, 3)
   }
 }
 
-// ---- bulk-box permute (BoxRef in tk_kernels.hpp)
-__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-struct BulkBox {
-  int64_t sbase, dbase;  // element offsets of (0, i1b, i2b, rest) in source / destination
-  int64_t s1, d2;        // source stride of leg 1, destination stride of leg 2 (elements)
-  int32_t n0, m1, m2, g;
-  double c;
-  int64_t dd1, dd2;      // destination member's complex-mode offsets
-};
-
-// box lb of ref ri (boxes of a group < 2^31, host-checked)
-template <int CM>
-__device__ __forceinline__ BulkBox bulk_box(const PermOp& op, const BoxRef* __restrict__ refs, int ri, uint32_t lb) {
-  const PermGroup& g = op.groups[refs[ri].group];
-  const PermMember ms = op.members[g.src_mem], md = op.members[g.dst_mem];
-  uint32_t b = lb;
-  const int T1 = g.T0, T2 = g.Tt, c1 = g.ct, c2 = g.R;
-  const int b1 = (int)(b % (uint32_t)T1);
-  b /= (uint32_t)T1;
-  const int b2 = (int)(b % (uint32_t)T2);
-  uint32_t rest = b / (uint32_t)T2;
-  BulkBox x;
-  x.sbase = ms.off;
-  x.dbase = md.off;
-  for (int l = 3; l < g.ndim; ++l) {
-    const uint32_t e = (uint32_t)g.ext[l], q = rest / e, i = rest - q * e;
-    rest = q;
-    x.sbase += (int64_t)i * (g.sa[l] + ms.ld * g.sb[l]);
-    x.dbase += (int64_t)i * (g.da[l] + md.ld * g.db[l]);
-  }
-  x.n0 = g.ext[0];
-  const int i1b = b1 * c1, i2b = b2 * c2;
-  x.m1 = min(c1, g.ext[1] - i1b);
-  x.m2 = min(c2, g.ext[2] - i2b);
-  x.s1 = g.sa[1] + ms.ld * g.sb[1];
-  x.d2 = g.da[2] + md.ld * g.db[2];
-  x.sbase += (int64_t)i1b * x.s1 + (int64_t)i2b * x.n0;  // leg 2: source stride n0
-  x.dbase += (int64_t)i1b * x.n0 + (int64_t)i2b * x.d2;  // leg 1: destination stride n0
-  x.c = op.alpha * op.coefs[g.coef_off];
-  x.g = ri;
-  x.dd1 = md.d1;
-  x.dd2 = md.d2;
-  return x;
-}
-
-// a CTA's boxes form one contiguous range of the box order (neighbouring boxes of a group are
-// neighbours in memory); the cursor advances without searching
-struct BoxCursor {
-  int ri;        // current ref
-  uint32_t lb;   // box within the ref's group
-  uint32_t nb;   // boxes of that group
-};
-__device__ __forceinline__ uint32_t ref_boxes(const BoxRef* __restrict__ refs, int nrefs, int ri, int64_t nboxes) {
-  const int64_t end = ri + 1 < nrefs ? __ldg(&refs[ri + 1].first) : nboxes;
-  return (uint32_t)(end - __ldg(&refs[ri].first));
-}
-
-template <int CM>
-__global__ void __launch_bounds__(kBulkThreads, kBulkCTAs)
-    permute_bulk_kernel(PermOp op, const BoxRef* __restrict__ refs, int nrefs, long long nboxes) {
-  using IO = CIO<CM>;
-  using V = typename IO::V;
-  using S = typename IO::S;
-  constexpr int ES = (int)sizeof(S);  // source element bytes (8: a run needs a 16-byte envelope)
-  extern __shared__ __align__(128) double bulk_dyn[];
-  __shared__ __align__(8) uint64_t bar[kBulkNB];
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) {
-    for (int i = 0; i < kBulkNB; ++i) mbar_init(&bar[i], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  pdl_trigger();
-  pdl_wait();
-  const S* src = (const S*)op.src;
-  auto* dst = (typename IO::D*)op.dst;
-  // slot pitch of a source run in a buffer (elements of S): run + envelope, rounded to 16 bytes
-  auto pitch = [](const BulkBox& x) {
-    const int run = x.n0 * x.m2;
-    return ES == 8 ? ((run + 3) & ~1) : run;
-  };
-  // warp 0 fetches box x into buffer buf: one bulk copy per source run (16-byte aligned envelope)
-  auto fetch = [&](const BulkBox& x, int buf) {
-    if (tid >= 32) return;
-    S* B = reinterpret_cast<S*>(bulk_dyn) + (size_t)buf * (kBulkBuf * 8 / ES);
-    const int P = pitch(x);
-    const uint32_t run_bytes = (uint32_t)(x.n0 * x.m2) * ES;
-    uint32_t bytes = 0;
-    for (int i1 = lane; i1 < x.m1; i1 += 32) {
-      const uintptr_t a = reinterpret_cast<uintptr_t>(src + x.sbase + (int64_t)i1 * x.s1);
-      bytes += (uint32_t)(((a + run_bytes + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15)));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-    if (lane == 0) {
-      fence_proxy_async();  // the buffer was last read through the generic proxy
-      mbar_arrive_expect_tx(&bar[buf], bytes);
-    }
-    __syncwarp();
-    for (int i1 = lane; i1 < x.m1; i1 += 32) {
-      const uintptr_t a = reinterpret_cast<uintptr_t>(src + x.sbase + (int64_t)i1 * x.s1);
-      const uintptr_t a0 = a & ~uintptr_t(15);
-      bulk_g2s(B + (size_t)i1 * P, reinterpret_cast<const void*>(a0),
-               (uint32_t)(((a + run_bytes + 15) & ~uintptr_t(15)) - a0), &bar[buf]);
-    }
-  };
-  // this CTA's contiguous range [b0, b1) of the box order; the first box's ref by binary search (once)
-  const int64_t b0 = nboxes * blockIdx.x / gridDim.x, b1 = nboxes * (blockIdx.x + 1) / gridDim.x;
-  if (b0 >= b1) return;
-  BoxCursor cs;
-  {
-    int lo = 0, hi = nrefs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(&refs[mid].first) <= b0) lo = mid; else hi = mid - 1;
-    }
-    cs.ri = lo;
-    cs.lb = (uint32_t)(b0 - __ldg(&refs[lo].first));
-    cs.nb = ref_boxes(refs, nrefs, lo, nboxes);
-  }
-  auto advance = [&]() {
-    if (++cs.lb == cs.nb) {
-      ++cs.ri;
-      cs.lb = 0;
-      if (cs.ri < nrefs) cs.nb = ref_boxes(refs, nrefs, cs.ri, nboxes);
-    }
-  };
-  // kBulkNB buffers: boxes u + 1 .. u + kBulkNB - 1 stream in while box u is written out
-  BulkBox cur = bulk_box<CM>(op, refs, cs.ri, cs.lb), nx1{};
-  fetch(cur, 0);
-  if (kBulkNB >= 3 && b0 + 1 < b1) {
-    advance();
-    nx1 = bulk_box<CM>(op, refs, cs.ri, cs.lb);
-    fetch(nx1, 1);
-  }
-  int64_t bx = b0;
-  for (int u = 0; bx < b1; ++bx, ++u) {
-    const int buf = u % kBulkNB;
-    BulkBox nx2{};
-    if (kBulkNB >= 3 && bx + 2 < b1) {
-      advance();
-      nx2 = bulk_box<CM>(op, refs, cs.ri, cs.lb);
-      fetch(nx2, (u + 2) % kBulkNB);  // that buffer held box u - 1, released by the barrier ending u - 1
-    }
-    if (kBulkNB == 2 && bx + 1 < b1) {  // double buffering: box u + 1 into the other buffer
-      advance();
-      nx1 = bulk_box<CM>(op, refs, cs.ri, cs.lb);
-      fetch(nx1, (u + 1) % kBulkNB);
-    }
-    mbar_wait(&bar[buf], (uint32_t)((u / kBulkNB) & 1));
-    // destination runs: i2 major, contiguous over e = i1 * n0 + i0; (i2, i1, i0) advanced by a fixed
-    // stride without divisions per element
-    const S* B = reinterpret_cast<const S*>(bulk_dyn) + (size_t)buf * (kBulkBuf * 8 / ES);
-    const int P = pitch(cur), n0 = cur.n0, m1 = cur.m1;
-    const uint32_t L = (uint32_t)n0 * m1, tot = L * cur.m2;
-    const int sph = ES == 8 ? (int)((reinterpret_cast<uintptr_t>(src + cur.sbase) >> 3) & 1) : 0;
-    const int s1ph = (int)(cur.s1 & 1);
-    uint32_t t = tid;
-    uint32_t i2 = t / L, e = t - i2 * L;
-    uint32_t i1 = e / (uint32_t)n0, i0 = e - i1 * (uint32_t)n0;
-    const uint32_t q2 = kBulkThreads / L, r2 = kBulkThreads - q2 * L;
-    const uint32_t q0 = r2 / (uint32_t)n0, r0 = r2 - q0 * (uint32_t)n0;
-    for (; t < tot; t += kBulkThreads) {
-      const int ph = ES == 8 ? ((sph + (int)i1 * s1ph) & 1) : 0;
-      const V x = B[(int64_t)i1 * P + ph + i2 * n0 + i0];  // S == V for every bulk mode (not planar)
-      IO::store(dst, cur.dbase + (int64_t)i2 * cur.d2 + i1 * n0 + i0, cur.dd1, cur.dd2, Num<V>::scale(cur.c, x),
-                op.beta, op.ims);
-      i2 += q2;
-      i0 += r0;
-      i1 += q0;
-      if (i0 >= (uint32_t)n0) {
-        i0 -= n0;
-        ++i1;
-      }
-      if (i1 >= (uint32_t)m1) {
-        i1 -= m1;
-        ++i2;
-      }
-    }
-    __syncthreads();  // buffer `buf` is refilled by the fetch of box u + kBulkNB
-    cur = nx1;
-    if (kBulkNB >= 3) nx1 = nx2;
-  }
-}
-
 template <int CM>
 static cudaError_t set_permute_attrs() {
   cudaError_t e = cudaFuncSetAttribute(permute_kernel<CM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kTileElems * (int)sizeof(typename CIO<CM>::V));
-  if constexpr (CM != kPermPlanarToC)
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(permute_bulk_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkNB * kBulkBuf * 8);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(permute_recouple_kernel<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kRecoupleStage * 8);
@@ -1025,21 +829,6 @@ static cudaError_t launch_permute_cm(PermOp op0, PermOp op1, const PermJob* jobs
     e = launch_k(permute_recouple_kernel<CM>, njobs_multi, kPermThreads, kRecoupleStage * 8, st, op0, op1,
                  jobs + njobs);
   return e;
-}
-
-cudaError_t launch_permute_bulk(const PermOp& op, const BoxRef* refs, int nrefs, int64_t nboxes, int grid, int cm,
-                                cudaStream_t st) {
-  const size_t smem = kBulkNB * kBulkBuf * 8;
-  const long long nb = (long long)nboxes;
-  switch (cm) {
-    case kPermReal: return launch_k(permute_bulk_kernel<kPermReal>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
-    case kPermCToC: return launch_k(permute_bulk_kernel<kPermCToC>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
-    case kPermCToPlanar:
-      return launch_k(permute_bulk_kernel<kPermCToPlanar>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
-    case kPermCToRealRep:
-      return launch_k(permute_bulk_kernel<kPermCToRealRep>, grid, kBulkThreads, smem, st, op, refs, nrefs, nb);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 cudaError_t launch_permute(const PermOp& op0, const PermOp& op1, const PermJob* jobs, int njobs, int njobs_multi,

@@ -35,9 +35,7 @@ struct PermGroup {
   int32_t T0, Tt;       // mode 1: number of chunks of leg 0 / leg tleg
   int32_t lorder;       // mode 1: load-phase walk order, 3 base-3 digits (fastest first) over
                         //         {0: leg 0 chunk, 1: leg tleg chunk, 2: rest block}
-  int32_t bulk;         // mode 0 groups of large permutes: 1 = bulk-box eligible (permute_bulk_kernel):
-                        //   legs ordered (0, 1 = dst-next, 2 = src-next, rest); box n0 x ct x R,
-                        //   T0 / Tt chunks of legs 1 / 2, nrest = product of legs 3..
+  int32_t pad0_;
   int64_t nrest;        // mode 1: product of the other legs' extents
   int32_t ext[kMaxLegs];
   int64_t sa[kMaxLegs], sb[kMaxLegs];
@@ -107,29 +105,6 @@ struct PermJob {
   int8_t op;      // which permute of a launch (0: A~ or the only one, 1: B~)
   int64_t first;
 };
-
-// Bulk-box permute (large abelian permutes whose leg 0 stays unit-stride on both sides while the next
-// legs differ: the cfg4 operand / output permutes). A box is n0 x c1 x c2 elements: in the source c1
-// contiguous runs of n0*c2 elements (leg 2 follows leg 0), in the destination c2 runs of n0*c1 (leg 1
-// follows leg 0). The CTA's copy engine fetches the source runs with cp.async.bulk (16-byte aligned
-// envelopes, completion counted on an mbarrier; no per-element load instructions) into one of two
-// shared-memory buffers while the threads write the previous box's destination runs with coalesced
-// stores. Persistent CTAs take boxes bx = blockIdx.x, + gridDim.x, ...; BoxRef gives each eligible
-// group's first box (prefix over groups).
-struct BoxRef {
-  int64_t first;  // first box index of the group
-  int32_t group;  // index into the plan's groups
-  int32_t pad;
-};
-#ifndef TK_BULK_BUF
-#define TK_BULK_BUF 4608
-#define TK_BULK_NB 2
-#define TK_BULK_CTAS 3
-#endif
-constexpr int kBulkBuf = TK_BULK_BUF;  // doubles per box buffer
-constexpr int kBulkNB = TK_BULK_NB;    // buffers per CTA (kBulkNB - 1 boxes in flight while one is written)
-constexpr int kBulkCTAs = TK_BULK_CTAS;  // resident CTAs per SM
-constexpr int kBulkThreads = 256;
 
 // One permute of a launch: data pointers, the plan's device tables, scalars.
 struct PermOp {
@@ -238,11 +213,6 @@ cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, cons
 cudaError_t launch_gemm(const double* A, const double* B, double* C, const GemmGroup* groups, const GemmTile* tiles,
                         int ntiles_big, int ntiles_small, int ntiles_skinny, const GemmTile* split_heads,
                         int nsplit_heads, double* parts, double alpha, double beta, cudaStream_t st);
-
-// bulk-box permute of `nrefs` eligible groups holding `nboxes` boxes (cm: kPermReal, kPermCToC,
-// kPermCToPlanar or kPermCToRealRep; src / dst 16-byte aligned)
-cudaError_t launch_permute_bulk(const PermOp& op, const BoxRef* refs, int nrefs, int64_t nboxes, int grid, int cm,
-                                cudaStream_t st);
 
 // FP64 tensor-pipe probe: blocks x 8 warps, each iters x 8 DMMA m8n8k4 (2 * 8 * 8 * 4 flops each)
 cudaError_t launch_dmma_probe(int blocks, long long iters, cudaStream_t st);

@@ -153,58 +153,6 @@ static void finish_group_geometry(PermGroup& g, const std::vector<int64_t>& src_
   g.nrest = 1;
   static const bool tile_all = knob("TK_PERM_TILE_ALL", 0) != 0;
   bool lead_unit = (g.sa[0] == 1 && g.sb[0] == 0);
-  g.bulk = 0;
-  // bulk-box eligibility (permute_bulk_kernel; used by large permutes only, make_jobs): leg 0 unit-stride
-  // on both sides, the source's next leg S (stride n0, codomain) differs from the destination's next leg
-  // D (stride n0, codomain). Legs are reordered (0, D, S, rest) -- the rows path is indifferent to the
-  // order of legs 1.. -- and a box n0 x c1 x c2 is sized to one shared-memory buffer.
-  static const bool no_bulk = knob("TK_NO_BULK", 0) != 0;
-  if (!no_bulk && lead_unit && g.ndim >= 3 && g.ksrc == 1 && g.kdst == 1) {
-    int sleg = 1;
-    for (int l = 2; l < g.ndim; ++l)
-      if (std::make_pair(g.sb[l], g.sa[l]) < std::make_pair(g.sb[sleg], g.sa[sleg])) sleg = l;
-    const bool runs = g.sb[sleg] == 0 && g.sa[sleg] == g.ext[0] && g.db[1] == 0 && g.da[1] == g.ext[0];
-    if (sleg != 1 && runs) {
-      std::vector<int> order{0, 1, sleg};
-      for (int l = 2; l < g.ndim; ++l)
-        if (l != sleg) order.push_back(l);
-      PermGroup h = g;
-      for (int k = 0; k < g.ndim; ++k) {
-        h.ext[k] = g.ext[order[k]];
-        h.sa[k] = g.sa[order[k]];
-        h.sb[k] = g.sb[order[k]];
-        h.da[k] = g.da[order[k]];
-        h.db[k] = g.db[order[k]];
-      }
-      const int64_t n0 = h.ext[0], n1 = h.ext[1], n2 = h.ext[2];
-      // buffer capacity in source elements; a real run needs a 16-byte envelope (+ up to 2 doubles)
-      const int64_t cap = (int64_t)kBulkBuf * 8 / elem_bytes;
-      auto pitch = [&](int64_t c2) { return elem_bytes == 8 ? ((n0 * c2 + 3) & ~int64_t(1)) : n0 * c2; };
-      int64_t best1 = 0, best2 = 0;
-      for (int64_t c2 = n2; c2 >= 1; --c2) {
-        const int64_t P = pitch(c2);
-        if (P > cap) continue;
-        const int64_t c1 = std::min(n1, cap / P);
-        // balanced source / destination run lengths, then the larger box
-        const int64_t sc = std::min(c1, c2), sb = std::min(best1, best2);
-        if (sc > sb || (sc == sb && c1 * c2 > best1 * best2)) {
-          best1 = c1;
-          best2 = c2;
-        }
-      }
-      const int64_t T1 = best1 ? (n1 + best1 - 1) / best1 : 0, T2 = best2 ? (n2 + best2 - 1) / best2 : 0;
-      if (best1 > 0 && T1 * T2 * (h.nelem / (n0 * n1 * n2)) < (int64_t(1) << 31)) {
-        g = h;
-        g.bulk = 1;
-        g.ct = (int32_t)best1;
-        g.R = (int32_t)best2;
-        g.T0 = (int32_t)T1;
-        g.Tt = (int32_t)T2;
-        g.nrest = g.nelem / (n0 * n1 * n2);
-        return;  // mode 0 (rows) for the rows fallback
-      }
-    }
-  }
   if (g.ndim >= 2 && g.ksrc == 1 && g.kdst == 1 && (!lead_unit || tile_all)) {
     g.mode = 1;
     g.tleg = 1;
@@ -338,7 +286,7 @@ struct SegBuilder {
 static void make_jobs(PermPlan& P) {
   // small single-member groups go last and are packed several per CTA (permute_packed_kernel)
   std::stable_partition(P.groups.begin(), P.groups.end(), [](const PermGroup& g) { return !packable(g); });
-  std::vector<PermJob> rows, rows_bulk, multi, dmulti, tiles, packed;
+  std::vector<PermJob> rows, multi, dmulti, tiles, packed;
   // elements per CTA job: 8192 for large permutes, smaller for small ones so that a latency-bound
   // permute still spreads over about two waves of the 148 SMs x 4 resident CTAs
   int64_t total = 0;
@@ -385,12 +333,7 @@ static void make_jobs(PermPlan& P) {
       int64_t per = std::max<int64_t>(1, std::min<int64_t>(kMaxRows, budget / std::max(1, g.ext[0])));
       // recoupling groups of few sources run inside the general launch (no second, serialised launch)
       static const bool direct_ok = knob("TK_NO_DIRECT_MULTI", 0) == 0;
-      const bool bulk = single && g.bulk && total >= (int64_t(1) << 24) && P.allow_bulk;
-      auto& dst = bulk ? rows_bulk : single ? rows : (direct_ok && g.ksrc <= kRecoupleDirect ? dmulti : multi);
-      if (bulk) {
-        P.refs.push_back(BoxRef{P.nboxes, gi, 0});
-        P.nboxes += (int64_t)g.T0 * g.Tt * g.nrest;
-      }
+      auto& dst = single ? rows : (direct_ok && g.ksrc <= kRecoupleDirect ? dmulti : multi);
       for (int64_t r = 0; r < nrows; r += per)
         dst.push_back(PermJob{gi, (int16_t)std::min(per, nrows - r), (int8_t)(single ? kJobRows : kJobMulti), 0, r});
     } else {
@@ -403,9 +346,6 @@ static void make_jobs(PermPlan& P) {
   // small permutes: one launch for rows, tiled and packed jobs (+ one for recoupling jobs); large ones
   // (>= 2^24 elements) run the rows jobs in a rows-only kernel instance and the rest in a second launch
   sb.finish();
-  // rows jobs of bulk-box groups lead the rows jobs (the rows launch skips them when the bulk kernel runs)
-  P.njobs_rows_bulk = (int)rows_bulk.size();
-  rows.insert(rows.begin(), rows_bulk.begin(), rows_bulk.end());
   rows.insert(rows.begin(), segs.begin(), segs.end());    // seg jobs lead the non-rows-only launch
   P.njobs = (int)(tiles.size() + rows.size() + packed.size() + dmulti.size());
   P.njobs_rows = (int)(rows.size() - segs.size());
@@ -439,8 +379,6 @@ static void make_jobs(PermPlan& P) {
     if (!segs.empty())
       fprintf(stderr, "[tk plan] seg: %zu jobs, max %d chunks / %d rows / %d elements per job\n", segs.size(), sg_ng,
               sg_rows, sg_el);
-    if (!P.refs.empty())
-      fprintf(stderr, "[tk plan] bulk boxes: %zu groups, %lld boxes\n", P.refs.size(), (long long)P.nboxes);
     fprintf(stderr, "[tk plan] %lld elems, job_elems %lld: rows %zu jobs (%lld groups, %lld el) | tiled %zu (%lld, %lld el) | "
             "packed %zu (%lld, %lld el) | multi %zu (%lld el)\n", (long long)total, (long long)job_elems, rows.size(),
             (long long)gr, (long long)er, tiles.size(), (long long)gt, (long long)et, packed.size(), (long long)gp,
@@ -1072,7 +1010,6 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   const int eb = P.cplx ? 16 : 8;
   build_perm_plan(A, t.pA, t.qA, *P.At, P.pa, eb, nullptr, pla);
   build_perm_plan(B, t.pB, t.qB, *P.Bt, P.pb, eb, nullptr, plb);
-  P.pc.allow_bulk = !P.cplx;  // the complex output permute reads planar C~ (not interleaved elements)
   build_perm_plan(*P.Ct, t.pAB, t.qAB, C, P.pc, eb, plc, nullptr);
   P.pa.identity = ia_id;
   P.pb.identity = ib_id;
@@ -1480,22 +1417,11 @@ void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double b
   const PermJob* jobs = (const PermJob*)P.d_jobs.p;
   if (P.split) {
     const int nrest = P.njobs - P.njobs_rows;
-    int skip = 0;  // rows jobs covered by the bulk-box kernel
-    const bool bulk_cm = cm == kPermReal || cm == kPermCToC || cm == kPermCToPlanar || cm == kPermCToRealRep;
-    const bool aligned = ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0;  // 16-byte envelopes / elements
-    if (!P.refs.empty() && bulk_cm && aligned) {
-      const int grid = (int)std::min<int64_t>(P.nboxes, kBulkCTAs * (int64_t)sm_count());
-      check_cuda(launch_permute_bulk(op, (const BoxRef*)P.d_refs.p, (int)P.refs.size(), P.nboxes, grid, cm, st),
-                 "bulk permute launch");
-      ++g_launches;
-      skip = P.njobs_rows_bulk;
-    }
-    if (P.njobs_rows > skip)
-      check_cuda(launch_permute(op, op, jobs + skip, P.njobs_rows - skip, 0, false, kLaunchRowsOnly, cm, st),
-                 "permute launch");
+    if (P.njobs_rows)
+      check_cuda(launch_permute(op, op, jobs, P.njobs_rows, 0, false, kLaunchRowsOnly, cm, st), "permute launch");
     check_cuda(launch_permute(op, op, jobs + P.njobs_rows, nrest, P.njobs_multi, P.tiled, kLaunchGeneral, cm, st),
                "permute launch");
-    g_launches += (P.njobs_rows > skip) + (nrest > 0) + (P.njobs_multi > 0);
+    g_launches += (P.njobs_rows > 0) + (nrest > 0) + (P.njobs_multi > 0);
   } else {
     const int variant = P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
     check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, variant, cm, st), "permute launch");

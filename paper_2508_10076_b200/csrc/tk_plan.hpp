@@ -105,12 +105,6 @@ struct PermPlan {
   std::vector<PermJob> jobs;
   std::vector<int64_t> blob;  // kJobSeg job blobs (SegHeader | SegGroup[ng] | rs | rd per job)
   int njobs = 0, njobs_multi = 0, njobs_rows = 0;  // jobs = [rows | seg/tiled/packed | recoupling]
-  // bulk-box groups (large permutes): their rows jobs lead the rows jobs (njobs_rows_bulk of them)
-  bool allow_bulk = true;
-  std::vector<BoxRef> refs;
-  int64_t nboxes = 0;
-  int njobs_rows_bulk = 0;
-  DevBuf d_refs;
   bool tiled = false, rows_only = false;
   bool split = false;  // large permute: rows jobs in their own (leaner) launch
   DevBuf d_groups, d_members, d_coefs, d_jobs, d_blob;
@@ -127,7 +121,6 @@ struct PermPlan {
       d_coefs.upload(coefs);
       d_jobs.upload(jobs);
       d_blob.upload(blob);
-      d_refs.upload(refs);
       uploaded = true;
     });
   }

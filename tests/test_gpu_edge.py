@@ -259,12 +259,12 @@ def test_bitwise_deterministic(cfgfun):
         assert np.array_equal(r1[k][1], r2[k][1]), k
 
 
-# ------------------------------------------------------------------ bulk-box permute (large permutes)
+# ------------------------------------------------------------------ large permutes (split launches)
 @pytest.mark.parametrize("cplx,alpha,beta", [(False, 1.0, 0.0), (False, -0.5, 0.25), (True, 0.75, -1.0)])
-def test_bulk_box_permute_large(cplx, alpha, beta):
-    """A permute above 2^24 elements whose leg 0 stays unit-stride while the next legs swap (the cfg4
-    pattern) runs on permute_bulk_kernel (cp.async.bulk source runs into shared memory, coalesced
-    destination runs); alpha / beta and ComplexF64 (tk_permute: interleaved -> interleaved)."""
+def test_large_permute_cfg4_pattern(cplx, alpha, beta):
+    """A permute above 2^24 elements (rows-only launch + tail launch) whose leg 0 stays unit-stride while
+    the next legs swap (the cfg4 pattern); alpha / beta and ComplexF64 (tk_permute: interleaved ->
+    interleaved)."""
     from paper_2508_10076_b200 import tk
     from oracle import layout as OL, dense as OD, contract as OC
     V = W.space("U1", [((-1,), 26), ((0,), 39), ((1,), 26)])

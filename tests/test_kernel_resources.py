@@ -3,7 +3,7 @@
 Occupancy is part of these kernels' design: the cfg4 rows-only permute must fit
 40 registers (6 CTAs of 256 threads per SM: 5.41 TB/s; 48 registers / 5 CTAs: 5.24; 56 / 4: 4.62), at the
 price of one spilled word; the big-tile GEMMs (TMA and cp.async) 128 (one 512-thread CTA per SM) without
-spills; the bulk-box permute 80 (3 CTAs of 256 threads per SM); the
+spills; the
 latency-path kernels at most a word or two (the general permute kernel carries every small-permute job
 type under the 64-register cap of 4 CTAs per SM).
 """
@@ -23,7 +23,6 @@ BUDGET = {  # demangled-name prefix -> (max registers, max stack bytes)
     "void tk::gemm_mbar_kernel<2>": (128, 0),
     "tk::gemm_small_kernel": (128, 0),
     "tk::gemm_tma_kernel": (128, 0),
-    "void tk::permute_bulk_kernel<0>": (80, 0),
     "tk::gemm_skinny_kernel": (85, 0),
     "void tk::permute_kernel<0, false>": (64, 16),
     "void tk::gather_skinny_kernel<8, 8>": (85, 0),
