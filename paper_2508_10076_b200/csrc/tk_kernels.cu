@@ -1244,7 +1244,10 @@ __device__ __forceinline__ void skinny_tile(const double* __restrict__ A, const 
 #ifndef TK_SMALL_WN
 #define TK_SMALL_WN 16  // warp tile 32 x WN (16: 8 warps per 64 x 64 tile)
 #endif
-#define TK_SMALL 64, 64, 32, TK_SMALL_WN, 16, TK_SMALL_STAGES
+#ifndef TK_SMALL_BK
+#define TK_SMALL_BK 16
+#endif
+#define TK_SMALL 64, 64, 32, TK_SMALL_WN, TK_SMALL_BK, TK_SMALL_STAGES
 #ifndef TK_SMALL_MINB
 #define TK_SMALL_MINB 2
 #endif

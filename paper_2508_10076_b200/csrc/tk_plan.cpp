@@ -297,7 +297,10 @@ static void make_jobs(PermPlan& P) {
   int64_t pack_elems = 0, pack_rows = 0;
   // latency regime: single-member rows / packable groups become kJobSeg blobs (TK_NO_SEG=1 disables)
   static const bool no_seg = knob("TK_NO_SEG", 0) != 0;
-  const bool seg = !no_seg && total < (int64_t(1) << 24);
+  // large-permute threshold: below it the latency regime (seg jobs, one launch), at or above it the
+  // bandwidth regime (rows-only launch + a launch for the rest)
+  static const int split_log2 = (int)knob("TK_SPLIT_LOG2", 24);
+  const bool seg = !no_seg && total < (int64_t(1) << split_log2);
   std::vector<PermJob> segs;
   // seg job size: about total / 296 elements (measured against 1184 / 592 / 148 jobs per permute: fewer,
   // larger jobs amortise each CTA's blob copy and tail -- cfg7 124 -> 112 us, cfg3 219 -> 213 us;
@@ -353,7 +356,7 @@ static void make_jobs(PermPlan& P) {
   P.tiled = !tiles.empty();  // tiled jobs need the dynamic shared-memory tile
   P.rows_only = tiles.empty() && packed.empty() && segs.empty() && dmulti.empty();
   // large permutes (>= 2^24 elements) launch one kernel per job class: rows-only, the rest
-  P.split = total >= (int64_t(1) << 24);
+  P.split = total >= (int64_t(1) << split_log2);
   const bool dbg = plan_debug();
   if (dbg) {
     int64_t er = 0, et = 0, ep = 0, em = 0, gr = 0, gt = 0, gp = 0;
