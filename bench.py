@@ -253,22 +253,45 @@ def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
             t = tk.tensor_from_spec(spec)
             T[name] = (t, torch.from_numpy(layout_io.fill(t, cfg["cfg"], idx)).to(dev))
         steps, roof = [], {"flops": 0.0, "gemm_bytes": 0.0, "permute_bytes": 0.0, "seconds": 0.0}
+        desc = {}
         for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
             A, B = T[na][0], T[nb][0]
-            C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+            desc[nc] = C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
             T[nc] = (C, torch.zeros(C.nelems, dtype=torch.float64, device=dev))
-            nws = tk.tk_contract_workspace(A, la, B, lb, C, lc)
-            ws = torch.empty(max(nws // 8 + 64, 1), dtype=torch.float64, device=dev)
             r = tk.tk_contract_roofline(A, la, B, lb, C, lc, peak_flops, hbm_bytes_s)
             for key in roof:
                 roof[key] += r[key]
-            steps.append((na, la, nb, lb, nc, lc, ws))
+        # calls: a consecutive pair that tk_contract2 runs as one kernel (the MPO steps T1.W1.W2 of the
+        # abelian chains) goes through it; every other step is one tk_contract
+        cs, i, nfused = cfg["steps"], 0, 0
+        while i < len(cs):
+            na, la, nb, lb, nc, lc, ncod = cs[i]
+            if i + 1 < len(cs) and cs[i + 1][0] == nc:
+                _, la2, nb2, lb2, nc2, lc2, _ = cs[i + 1]
+                nws, fu = tk.tk_contract2_workspace(T[na][0], la, T[nb][0], lb, desc[nc], lc, T[nb2][0], lb2,
+                                                    desc[nc2], lc2, want_fused=True)
+                if fu:
+                    ws = torch.empty(max(nws // 8 + 64, 1), dtype=torch.float64, device=dev)
+                    steps.append((na, la, nb, lb, nc, lc, ws, (nb2, lb2, nc2, lc2)))
+                    nfused += 1
+                    i += 2
+                    continue
+            nws = tk.tk_contract_workspace(T[na][0], la, T[nb][0], lb, T[nc][0], lc)
+            ws = torch.empty(max(nws // 8 + 64, 1), dtype=torch.float64, device=dev)
+            steps.append((na, la, nb, lb, nc, lc, ws, None))
+            i += 1
 
         def chain():
             n = 0
-            for (na, la, nb, lb, nc, lc, ws) in steps:
-                tk.tk_contract(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], T[nc][1], lc, ws=ws,
-                               ws_bytes=ws.numel() * 8, stream=stream)
+            for (na, la, nb, lb, nc, lc, ws, pair) in steps:
+                if pair is None:
+                    tk.tk_contract(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], T[nc][1], lc, ws=ws,
+                                   ws_bytes=ws.numel() * 8, stream=stream)
+                else:
+                    nb2, lb2, nc2, lc2 = pair
+                    tk.tk_contract2(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], lc, T[nb2][0],
+                                    T[nb2][1], lb2, T[nc2][0], T[nc2][1], lc2, ws=ws, ws_bytes=ws.numel() * 8,
+                                    stream=stream)
                 n += tk.tk_last_launch_count()
             return n
         with torch.cuda.stream(stream):
@@ -289,7 +312,8 @@ def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e3)
         us = float(np.median(ts))
-        out[f"cfg{k}"] = {"kind": cfg["kind"], "us_per_chain": round(us, 2), "steps": len(steps),
+        out[f"cfg{k}"] = {"kind": cfg["kind"], "us_per_chain": round(us, 2), "steps": len(cfg["steps"]),
+                          "fused_pairs": nfused,
                           "launches": launches, "block_flops": roof["flops"],
                           "GFLOP_s": round(roof["flops"] / (us * 1e-6) / 1e9, 2),
                           "roofline_us": round(roof["seconds"] * 1e6, 2),

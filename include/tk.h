@@ -160,6 +160,28 @@ tk_status tk_contract(const tk_tensor* A, const void* a, const int32_t* labA, in
                       const tk_tensor* C, void* c, const int32_t* labC, double alpha, double beta,
                       void* ws, size_t ws_bytes, tk_stream stream);
 
+/* Two consecutive contractions, C[labC] = alpha * ((A[labA] B1[labB1] -> T[labT]) [labT] B2[labB2])
+ * + beta * C: exactly tk_contract(A, B1 -> T, alpha 1, beta 0) followed by tk_contract(T, B2 -> C,
+ * alpha, beta), each reading C2 for its own tuples (the pairwise order of a contraction sequence,
+ * P:1414-1420; the MPO steps of the DMRG two-site update, Alg. 12). T is a descriptor only
+ * (its HomSpace must be tk_contract_output(A, labA, B1, labB1, labT)); its data is never materialised
+ * when both steps are gathered skinny contractions whose output needs no permute -- then one kernel
+ * applies both steps per fiber of T with the same per-element arithmetic. Otherwise the two
+ * contractions run as they are with T in the workspace. Float64 only (ComplexF64: call tk_contract
+ * twice); no conj flags. Data pointers are device memory in the canonical layouts; C is read only
+ * if beta != 0; the workspace (size from tk_contract2_workspace, 256-byte aligned) is caller-owned.
+ * tk_contract2_workspace also reports (*fused, if non-NULL) whether the pair runs as one kernel.
+ * Errors as tk_contract (raised before any launch). */
+tk_status tk_contract2_workspace(const tk_tensor* A, const int32_t* labA, const tk_tensor* B1,
+                                 const int32_t* labB1, const tk_tensor* T, const int32_t* labT,
+                                 const tk_tensor* B2, const int32_t* labB2, const tk_tensor* C,
+                                 const int32_t* labC, size_t* bytes, int32_t* fused);
+tk_status tk_contract2(const tk_tensor* A, const void* a, const int32_t* labA, const tk_tensor* B1,
+                       const void* b1, const int32_t* labB1, const tk_tensor* T, const int32_t* labT,
+                       const tk_tensor* B2, const void* b2, const int32_t* labB2, const tk_tensor* C,
+                       void* c, const int32_t* labC, double alpha, double beta, void* ws,
+                       size_t ws_bytes, tk_stream stream);
+
 /* Low-level Alg. 4 entry (Alg. 8; reading C1: B~ = permute(B, (pB, qB))):
  *   A~ = permute(A, (pA, qA)),  B~ = permute(B, (pB, qB)),  C~ = A~ o B~,
  *   C  = alpha * permute(C~, (pAB, qAB)) + beta * C.

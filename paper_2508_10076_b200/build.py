@@ -14,7 +14,8 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtk_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["tk_sectors.cpp", "tk_layout.cpp", "tk_trees.cpp", "tk_plan.cpp", "tk_capi.cpp", "tk_kernels.cu",
-           "tk_svd.cu", "tk_trace.cu", "tk_ncon.cpp", "tk_gemm_tma.cu"]
+           "tk_svd.cu", "tk_trace.cu", "tk_ncon.cpp", "tk_gemm_tma.cu",
+           "tk_fused.cu"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-gencode", "arch=compute_100a,code=sm_100a", "-Xptxas", "-v"]
 

@@ -1374,15 +1374,35 @@ __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
     }
     const int r0 = ss[lo].r0;
     while (lo > 0 && ss[lo - 1].r0 == r0) --lo;
+    // the row's mixed-radix digits over the row legs are the same for every column subblock of the row
+    // tree unless a subblock merged its legs differently: decode once, re-decode only when (nrl, ext)
+    // changes (the decode -- integer divisions -- dominated the kernel's instruction count)
+    int cnrl = -1;
+    int cext[4] = {0, 0, 0, 0};
+    uint32_t dig[4] = {0, 0, 0, 0};
     for (int s = lo; s < t.nseg && ss[s].r0 == r0; ++s) {
       const GatherSeg& q = ss[s];
-      uint32_t r = (uint32_t)(m - q.r0);
-      int rs = 0;
-      for (int l = 0; l < q.nrl; ++l) {
-        const uint32_t e = (uint32_t)q.ext[l], qq = r / e;
-        rs += (int)(r - qq * e) * q.str[l];
-        r = qq;
+      const int nrl = q.nrl;
+      bool same = nrl == cnrl;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) same = same && (l >= nrl || q.ext[l] == cext[l]);
+      if (!same) {
+        uint32_t r = (uint32_t)(m - q.r0);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          if (l < nrl) {
+            const uint32_t e = (uint32_t)q.ext[l], qq = r / e;
+            dig[l] = r - qq * e;
+            cext[l] = (int)e;
+            r = qq;
+          }
+        }
+        cnrl = nrl;
       }
+      int rs = 0;
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        if (l < nrl) rs += (int)dig[l] * q.str[l];
       const double* a = A + q.src + rs;
       for (int kk = 0; kk < q.nk; ++kk) cp_async8(&As[q.k0 + kk][lr], a + q.colsrc[kk], true);
       if (q.neg) neg[j] |= ((1u << q.nk) - 1u) << q.k0;

@@ -585,71 +585,6 @@ void permute_transfer_matrix(const Tensor& A, const std::vector<int>& p, const s
 
 int sm_count();
 
-// ------------------------------------------------------------------ contraction plan
-struct ContractPlan {
-  Tensor* At = nullptr;  // A~ (canonical layout, reading C2 tuples)
-  Tensor* Bt = nullptr;
-  Tensor* Ct = nullptr;
-  PermPlan pa, pb, pc;
-  PadLayout la, lb, lc;  // workspace layouts of A~, B~, C~
-  std::vector<GemmGroup> ggroups;
-  std::vector<GemmTile> tiles;
-  int ntiles_big = 0, ntiles_small = 0, ntiles_skinny = 0;
-  std::vector<GemmTile> split_heads;  // split-K reduction targets
-  int nslots = 0;
-  size_t off_parts = 0;
-  DevBuf d_heads;
-  bool cplx = false;  // ComplexF64: workspace in the real representation (PermCM), one real GEMM
-  // small Float64 contractions: both operand permutes in ONE launch (jobs of A~ = op 0, B~ = op 1)
-  bool merged_ab = false;
-  std::vector<PermJob> jobs_ab;
-  int njobs_ab = 0, njobs_ab_multi = 0;
-  bool ab_tiled = false;
-  DevBuf d_ggroups, d_tiles, d_jobs_ab;
-  // gathered skinny GEMM (build_gather): the A~ permute folded into the GEMM's loads
-  bool gather = false;
-  std::vector<GatherSeg> gsegs;
-  std::vector<GatherTile> gtiles;
-  std::vector<int32_t> btab;
-  std::vector<int64_t> gslots;
-  int g_kmax = 0, g_nmax = 0;
-  DevBuf d_gsegs, d_btab, d_gslots;
-  size_t off_a = 0, off_b = 0, off_c = 0, off_counter = 0, ws_bytes = 0;
-  double flops = 0;
-  // persistent TMA GEMM for the big tiles (tk_gemm_tma.cu): groups with a tensor-map pair, and the
-  // maps encoded for the last (A~, B~) workspace pointers seen (re-encoded when they change)
-  bool tma = false;
-  std::vector<int> tma_groups;
-  std::mutex tma_mu;
-  std::unique_ptr<GemmTmaParams> tma_params;
-  const void* tma_a = nullptr;
-  const void* tma_b = nullptr;
-  bool uploaded = false;
-  std::once_flag up_once;
-  ~ContractPlan() {
-    if (At) tk_tensor_release((tk_tensor*)At);
-    if (Bt) tk_tensor_release((tk_tensor*)Bt);
-    if (Ct) tk_tensor_release((tk_tensor*)Ct);
-  }
-  void ensure_uploaded() {
-    std::call_once(up_once, [&] { upload(); });
-  }
-  void upload() {
-    check_cuda(ensure_kernel_attrs(), "kernel attributes");
-    if (!pa.identity) pa.ensure_uploaded();
-    if (!pb.identity) pb.ensure_uploaded();
-    if (!pc.identity) pc.ensure_uploaded();
-    d_ggroups.upload(ggroups);
-    d_tiles.upload(tiles);
-    d_heads.upload(split_heads);
-    d_jobs_ab.upload(jobs_ab);
-    d_gsegs.upload(gsegs);
-    d_btab.upload(btab);
-    d_gslots.upload(gslots);
-    uploaded = true;
-  }
-};
-
 struct Tuples {
   std::vector<int> pA, qA, pB, qB, pAB, qAB;
 };
@@ -1322,8 +1257,8 @@ static std::shared_ptr<ContractPlan> new_contract_plan(const Tensor& A, const Te
   return P;
 }
 
-static std::shared_ptr<ContractPlan> get_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B,
-                                                       const int32_t* labB, const Tensor& C, const int32_t* labC) {
+std::shared_ptr<ContractPlan> get_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B,
+                                                const int32_t* labB, const Tensor& C, const int32_t* labC) {
   std::string key = A.sig + "#" + labels_key(labA, A.nlegs()) + "#" + B.sig + "#" + labels_key(labB, B.nlegs()) +
                     "#" + C.sig + "#" + labels_key(labC, C.nlegs());
   return g_contract_cache.get(key, [&] {
@@ -1365,6 +1300,7 @@ static std::shared_ptr<PermPlan> get_perm_plan(const Tensor& A, const std::vecto
 }
 
 void cache_clear() {
+  fused_cache_clear();
   g_contract_cache.clear();
   g_perm_cache.clear();
   svd_cache_clear();
@@ -1381,6 +1317,7 @@ void cache_clear() {
 size_t cache_size() { return g_contract_cache.size() + g_perm_cache.size(); }
 size_t svd_cache_size();
 size_t trace_cache_size();
+size_t fused_cache_size();
 
 // ------------------------------------------------------------------ profiling state
 struct Prof {
@@ -1429,6 +1366,99 @@ void run_permute(PermPlan& P, const void* src, void* dst, double alpha, double b
     const int variant = P.rows_only ? kLaunchRowsOnly : kLaunchGeneral;
     check_cuda(launch_permute(op, op, jobs, P.njobs, P.njobs_multi, P.tiled, variant, cm, st), "permute launch");
     g_launches += (P.njobs > 0) + (P.njobs_multi > 0);
+  }
+}
+
+// one contraction through a plan: operand permutes, grouped GEMM, output permute (Alg. 4)
+void run_contract(ContractPlan* P, const void* a, const void* b, void* c, int32_t conjA, int32_t conjB,
+                         double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
+  if (ws_bytes < P->ws_bytes || (P->ws_bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+  if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  P->ensure_uploaded();
+  cudaStream_t st = (cudaStream_t)stream;
+  free_deferred(st);
+  char* w = (char*)ws;
+  const double* At = P->pa.identity ? (const double*)a : (const double*)(w + P->off_a);
+  const double* Bt = P->pb.identity ? (const double*)b : (const double*)(w + P->off_b);
+  double* Ct = P->pc.identity ? (double*)c : (double*)(w + P->off_c);
+  g_launches = 0;
+  prof_record(0, st);
+  const bool cx = P->cplx;
+  if (P->gather) {  // A~ and B~ are gathered inside the GEMM: no permute pass
+    prof_record(1, st);
+  } else if (P->merged_ab) {
+    PermOp oa = perm_op(P->pa, a, (double*)At, 1.0, 0.0, 1.0), ob = perm_op(P->pb, b, (double*)Bt, 1.0, 0.0, 1.0);
+    check_cuda(launch_permute(oa, ob, (const PermJob*)P->d_jobs_ab.p, P->njobs_ab, P->njobs_ab_multi, P->ab_tiled,
+                              kLaunchGeneral, kPermReal, st),
+               "permute launch");
+    g_launches += (P->njobs_ab > 0) + (P->njobs_ab_multi > 0);
+  } else if (!P->pa.identity) {
+    run_permute(P->pa, a, (double*)At, 1.0, 0.0, cx ? kPermCToPlanar : kPermReal, conjA ? -1.0 : 1.0, st);
+  }
+  if (!P->gather) prof_record(1, st);
+  if (!P->gather && !P->merged_ab && !P->pb.identity)
+    run_permute(P->pb, b, (double*)Bt, 1.0, 0.0, cx ? kPermCToRealRep : kPermReal, conjB ? -1.0 : 1.0, st);
+  prof_record(2, st);
+  double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
+  if (!P->tiles.empty()) {
+    int nbig = P->ntiles_big;
+    const GemmTile* d_tiles = (const GemmTile*)P->d_tiles.p;
+    if (P->tma && nbig > 0) {
+      GemmTmaParams* prm = nullptr;
+      {
+        std::lock_guard<std::mutex> g(P->tma_mu);
+        if (!P->tma_params || P->tma_a != At || P->tma_b != Bt) {
+          if (!P->tma_params) P->tma_params = std::make_unique<GemmTmaParams>();
+          P->tma_a = P->tma_b = nullptr;
+          if (gemm_tma_encode(*P->tma_params, P->ggroups, P->tma_groups, At, Bt)) {
+            P->tma_a = At;
+            P->tma_b = Bt;
+          }
+        }
+        if (P->tma_a == At && P->tma_b == Bt) {
+          prm = new GemmTmaParams(*P->tma_params);  // per-call copy: output and scalars differ
+        }
+      }
+      if (prm) {
+        std::unique_ptr<GemmTmaParams> q(prm);
+        q->C = Ct;
+        q->tiles = d_tiles;
+        q->counter = (int*)(w + P->off_counter);
+        check_cuda(cudaMemsetAsync(q->counter, 0, sizeof(int), st), "tile counter reset");
+        q->ntiles = nbig;
+        q->alpha = ga;
+        q->beta = gb;
+        check_cuda(launch_gemm_tma(*q, std::min(nbig, sm_count()), st), "tma gemm launch");
+        ++g_launches;
+        d_tiles += nbig;
+        nbig = 0;
+      }
+    }
+    check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, d_tiles, nbig, P->ntiles_small,
+                           P->ntiles_skinny, (const GemmTile*)P->d_heads.p, (int)P->split_heads.size(),
+                           (double*)(w + P->off_parts), ga, gb, st),
+               "gemm launch");
+    g_launches += (nbig > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0 && P->ntiles_small == 0) +
+                  !P->split_heads.empty();
+  }
+  if (P->gather) {
+    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const int64_t*)P->d_gslots.p,
+                                  (int)P->gtiles.size(), (const GatherSeg*)P->d_gsegs.p, (const int32_t*)P->d_btab.p,
+                                  P->g_kmax, P->g_nmax, ga, gb, st),
+               "gather gemm launch");
+    g_launches += !P->gtiles.empty();
+  }
+  prof_record(3, st);
+  if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
+  prof_record(4, st);
+  if (g_prof.on) {
+    g_prof.have = true;
+    // merged operand permutes: phase 0 covers both A~ and B~, phase 1 is empty
+    g_prof.bytes[0] = (P->pa.identity ? 0 : P->pa.bytes) + (P->merged_ab ? P->pb.bytes : 0);
+    g_prof.bytes[1] = (P->pb.identity || P->merged_ab) ? 0 : P->pb.bytes;
+    g_prof.bytes[2] = 0;
+    g_prof.bytes[3] = P->pc.identity ? 0 : P->pc.bytes;
+    g_prof.flops = P->flops;
   }
 }
 
@@ -1536,99 +1566,6 @@ tk_status tk_contract_output(const tk_tensor* A_, const int32_t* labA, const tk_
   tk_tensor_release((tk_tensor*)Ct);
   *out = (tk_tensor*)C;
   TK_API_END
-}
-
-// one contraction through a plan: operand permutes, grouped GEMM, output permute (Alg. 4)
-static void run_contract(ContractPlan* P, const void* a, const void* b, void* c, int32_t conjA, int32_t conjB,
-                         double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream) {
-  if (ws_bytes < P->ws_bytes || (P->ws_bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
-  if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
-  P->ensure_uploaded();
-  cudaStream_t st = (cudaStream_t)stream;
-  free_deferred(st);
-  char* w = (char*)ws;
-  const double* At = P->pa.identity ? (const double*)a : (const double*)(w + P->off_a);
-  const double* Bt = P->pb.identity ? (const double*)b : (const double*)(w + P->off_b);
-  double* Ct = P->pc.identity ? (double*)c : (double*)(w + P->off_c);
-  g_launches = 0;
-  prof_record(0, st);
-  const bool cx = P->cplx;
-  if (P->gather) {  // A~ and B~ are gathered inside the GEMM: no permute pass
-    prof_record(1, st);
-  } else if (P->merged_ab) {
-    PermOp oa = perm_op(P->pa, a, (double*)At, 1.0, 0.0, 1.0), ob = perm_op(P->pb, b, (double*)Bt, 1.0, 0.0, 1.0);
-    check_cuda(launch_permute(oa, ob, (const PermJob*)P->d_jobs_ab.p, P->njobs_ab, P->njobs_ab_multi, P->ab_tiled,
-                              kLaunchGeneral, kPermReal, st),
-               "permute launch");
-    g_launches += (P->njobs_ab > 0) + (P->njobs_ab_multi > 0);
-  } else if (!P->pa.identity) {
-    run_permute(P->pa, a, (double*)At, 1.0, 0.0, cx ? kPermCToPlanar : kPermReal, conjA ? -1.0 : 1.0, st);
-  }
-  if (!P->gather) prof_record(1, st);
-  if (!P->gather && !P->merged_ab && !P->pb.identity)
-    run_permute(P->pb, b, (double*)Bt, 1.0, 0.0, cx ? kPermCToRealRep : kPermReal, conjB ? -1.0 : 1.0, st);
-  prof_record(2, st);
-  double ga = P->pc.identity ? alpha : 1.0, gb = P->pc.identity ? beta : 0.0;
-  if (!P->tiles.empty()) {
-    int nbig = P->ntiles_big;
-    const GemmTile* d_tiles = (const GemmTile*)P->d_tiles.p;
-    if (P->tma && nbig > 0) {
-      GemmTmaParams* prm = nullptr;
-      {
-        std::lock_guard<std::mutex> g(P->tma_mu);
-        if (!P->tma_params || P->tma_a != At || P->tma_b != Bt) {
-          if (!P->tma_params) P->tma_params = std::make_unique<GemmTmaParams>();
-          P->tma_a = P->tma_b = nullptr;
-          if (gemm_tma_encode(*P->tma_params, P->ggroups, P->tma_groups, At, Bt)) {
-            P->tma_a = At;
-            P->tma_b = Bt;
-          }
-        }
-        if (P->tma_a == At && P->tma_b == Bt) {
-          prm = new GemmTmaParams(*P->tma_params);  // per-call copy: output and scalars differ
-        }
-      }
-      if (prm) {
-        std::unique_ptr<GemmTmaParams> q(prm);
-        q->C = Ct;
-        q->tiles = d_tiles;
-        q->counter = (int*)(w + P->off_counter);
-        check_cuda(cudaMemsetAsync(q->counter, 0, sizeof(int), st), "tile counter reset");
-        q->ntiles = nbig;
-        q->alpha = ga;
-        q->beta = gb;
-        check_cuda(launch_gemm_tma(*q, std::min(nbig, sm_count()), st), "tma gemm launch");
-        ++g_launches;
-        d_tiles += nbig;
-        nbig = 0;
-      }
-    }
-    check_cuda(launch_gemm(At, Bt, Ct, (const GemmGroup*)P->d_ggroups.p, d_tiles, nbig, P->ntiles_small,
-                           P->ntiles_skinny, (const GemmTile*)P->d_heads.p, (int)P->split_heads.size(),
-                           (double*)(w + P->off_parts), ga, gb, st),
-               "gemm launch");
-    g_launches += (nbig > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0 && P->ntiles_small == 0) +
-                  !P->split_heads.empty();
-  }
-  if (P->gather) {
-    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const int64_t*)P->d_gslots.p,
-                                  (int)P->gtiles.size(), (const GatherSeg*)P->d_gsegs.p, (const int32_t*)P->d_btab.p,
-                                  P->g_kmax, P->g_nmax, ga, gb, st),
-               "gather gemm launch");
-    g_launches += !P->gtiles.empty();
-  }
-  prof_record(3, st);
-  if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
-  prof_record(4, st);
-  if (g_prof.on) {
-    g_prof.have = true;
-    // merged operand permutes: phase 0 covers both A~ and B~, phase 1 is empty
-    g_prof.bytes[0] = (P->pa.identity ? 0 : P->pa.bytes) + (P->merged_ab ? P->pb.bytes : 0);
-    g_prof.bytes[1] = (P->pb.identity || P->merged_ab) ? 0 : P->pb.bytes;
-    g_prof.bytes[2] = 0;
-    g_prof.bytes[3] = P->pc.identity ? 0 : P->pc.bytes;
-    g_prof.flops = P->flops;
-  }
 }
 
 tk_status tk_contract_workspace(const tk_tensor* A, const int32_t* labA, const tk_tensor* B, const int32_t* labB,
@@ -1756,6 +1693,7 @@ tk_status tk_dmma_probe(int32_t blocks, int64_t iters, tk_stream stream, double*
 
 void tk_cache_clear(void) { tk::cache_clear(); }
 
-int64_t tk_cache_size(void) { return (int64_t)(tk::cache_size() + tk::svd_cache_size() + tk::trace_cache_size()); }
+int64_t tk_cache_size(void) { return (int64_t)(tk::cache_size() + tk::svd_cache_size() + tk::trace_cache_size() +
+                                          tk::fused_cache_size()); }
 
 }  // extern "C"

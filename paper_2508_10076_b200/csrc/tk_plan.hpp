@@ -9,6 +9,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "tk_gemm_tma.hpp"
 #include "tk_internal.hpp"
 #include "tk_kernels.hpp"
 
@@ -158,5 +159,79 @@ size_t align256(size_t x);
 void add_launches(int n);
 void reset_launches();
 void svd_cache_clear();
+void fused_cache_clear();
+
+// ------------------------------------------------------------------ contraction plan (tk_plan.cpp)
+struct ContractPlan {
+  Tensor* At = nullptr;  // A~ (canonical layout, reading C2 tuples)
+  Tensor* Bt = nullptr;
+  Tensor* Ct = nullptr;
+  PermPlan pa, pb, pc;
+  PadLayout la, lb, lc;  // workspace layouts of A~, B~, C~
+  std::vector<GemmGroup> ggroups;
+  std::vector<GemmTile> tiles;
+  int ntiles_big = 0, ntiles_small = 0, ntiles_skinny = 0;
+  std::vector<GemmTile> split_heads;  // split-K reduction targets
+  int nslots = 0;
+  size_t off_parts = 0;
+  DevBuf d_heads;
+  bool cplx = false;  // ComplexF64: workspace in the real representation (PermCM), one real GEMM
+  // small Float64 contractions: both operand permutes in ONE launch (jobs of A~ = op 0, B~ = op 1)
+  bool merged_ab = false;
+  std::vector<PermJob> jobs_ab;
+  int njobs_ab = 0, njobs_ab_multi = 0;
+  bool ab_tiled = false;
+  DevBuf d_ggroups, d_tiles, d_jobs_ab;
+  // gathered skinny GEMM (build_gather): the A~ permute folded into the GEMM's loads
+  bool gather = false;
+  std::vector<GatherSeg> gsegs;
+  std::vector<GatherTile> gtiles;
+  std::vector<int32_t> btab;
+  std::vector<int64_t> gslots;
+  int g_kmax = 0, g_nmax = 0;
+  DevBuf d_gsegs, d_btab, d_gslots;
+  size_t off_a = 0, off_b = 0, off_c = 0, off_counter = 0, ws_bytes = 0;
+  double flops = 0;
+  // persistent TMA GEMM for the big tiles (tk_gemm_tma.cu): groups with a tensor-map pair, and the
+  // maps encoded for the last (A~, B~) workspace pointers seen (re-encoded when they change)
+  bool tma = false;
+  std::vector<int> tma_groups;
+  std::mutex tma_mu;
+  std::unique_ptr<GemmTmaParams> tma_params;
+  const void* tma_a = nullptr;
+  const void* tma_b = nullptr;
+  bool uploaded = false;
+  std::once_flag up_once;
+  ~ContractPlan() {
+    if (At) tk_tensor_release((tk_tensor*)At);
+    if (Bt) tk_tensor_release((tk_tensor*)Bt);
+    if (Ct) tk_tensor_release((tk_tensor*)Ct);
+  }
+  void ensure_uploaded() {
+    std::call_once(up_once, [&] { upload(); });
+  }
+  void upload() {
+    check_cuda(ensure_kernel_attrs(), "kernel attributes");
+    if (!pa.identity) pa.ensure_uploaded();
+    if (!pb.identity) pb.ensure_uploaded();
+    if (!pc.identity) pc.ensure_uploaded();
+    d_ggroups.upload(ggroups);
+    d_tiles.upload(tiles);
+    d_heads.upload(split_heads);
+    d_jobs_ab.upload(jobs_ab);
+    d_gsegs.upload(gsegs);
+    d_btab.upload(btab);
+    d_gslots.upload(gslots);
+    uploaded = true;
+  }
+};
+
+// memoised plan of tk_contract (labels, reading C2) and its execution (operand permutes, grouped GEMM,
+// output permute); `stream` is the caller's tk_stream
+std::shared_ptr<ContractPlan> get_contract_plan(const Tensor& A, const int32_t* labA, const Tensor& B,
+                                                const int32_t* labB, const Tensor& C, const int32_t* labC);
+void run_contract(ContractPlan* P, const void* a, const void* b, void* c, int32_t conjA, int32_t conjB,
+                  double alpha, double beta, void* ws, size_t ws_bytes, tk_stream stream);
+int sm_count();
 
 }  // namespace tk

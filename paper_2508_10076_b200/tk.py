@@ -78,6 +78,10 @@ _contract_workspace = _sig("tk_contract_workspace", [_p, _i32p, _p, _i32p, _p, _
                                                      ctypes.POINTER(ctypes.c_size_t)])
 _contract = _sig("tk_contract", [_p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p, ctypes.c_int32, _p, _p, _i32p,
                                  ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
+_contract2_workspace = _sig("tk_contract2_workspace", [_p, _i32p, _p, _i32p, _p, _i32p, _p, _i32p, _p, _i32p,
+                                                       ctypes.POINTER(ctypes.c_size_t), _i32p])
+_contract2 = _sig("tk_contract2", [_p, _p, _i32p, _p, _p, _i32p, _p, _i32p, _p, _p, _i32p, _p, _p, _i32p,
+                                   ctypes.c_double, ctypes.c_double, _p, ctypes.c_size_t, _p])
 _contract_tuples_output = _sig("tk_contract_tuples_output", [_p, _p, _i32p, _i32p, ctypes.POINTER(_p)])
 _contract_tuples_workspace = _sig("tk_contract_tuples_workspace", [_p, _p, _p, _i32p, _i32p,
                                                                    ctypes.POINTER(ctypes.c_size_t)])
@@ -128,7 +132,7 @@ EXPORTED = ["tk_space_create", "tk_space_parse", "tk_space_info", "tk_space_sect
             "tk_svd_spectrum", "tk_svd_truncate", "tk_svd_extract", "tk_trace_output", "tk_trace_workspace",
             "tk_trace", "tk_trace_transfer", "tk_contract_tuples_output", "tk_contract_tuples_workspace",
             "tk_contract_tuples", "tk_ncon_output", "tk_ncon_workspace", "tk_ncon", "tk_cache_size",
-            "tk_contract_roofline", "tk_dmma_probe"]
+            "tk_contract_roofline", "tk_dmma_probe", "tk_contract2_workspace", "tk_contract2"]
 
 
 def _i32(seq):
@@ -357,6 +361,28 @@ def tk_contract(A, a, labA, B, b, labB, C, c, labC, alpha=1.0, beta=0.0, ws=None
     lc, cp = _labels(C, labC, "labC")
     _check(_contract(A.h, _data(A, a, "a"), ap, int(conjA), B.h, _data(B, b, "b"), bp, int(conjB), C.h,
                      _data(C, c, "c"), cp, float(alpha), float(beta), _ws(ws, ws_bytes), ws_bytes, _stream(stream)))
+
+
+def tk_contract2_workspace(A, labA, B1, labB1, T, labT, B2, labB2, C, labC, want_fused=False):
+    """Workspace bytes of tk_contract2 (and, with want_fused, whether the pair runs as one kernel)."""
+    ls = [_labels(x, l, w) for x, l, w in ((A, labA, "labA"), (B1, labB1, "labB1"), (T, labT, "labT"),
+                                           (B2, labB2, "labB2"), (C, labC, "labC"))]
+    n = ctypes.c_size_t()
+    f = ctypes.c_int32(0)
+    _check(_contract2_workspace(A.h, ls[0][1], B1.h, ls[1][1], T.h, ls[2][1], B2.h, ls[3][1], C.h, ls[4][1],
+                                ctypes.byref(n), ctypes.cast(ctypes.byref(f), _i32p)))
+    return (n.value, bool(f.value)) if want_fused else n.value
+
+
+def tk_contract2(A, a, labA, B1, b1, labB1, T, labT, B2, b2, labB2, C, c, labC, alpha=1.0, beta=0.0, ws=None,
+                 ws_bytes=0, stream=None):
+    """C = alpha ((A B1 -> T) B2) + beta C: two tk_contract calls, fused into one kernel when both are
+    gathered skinny steps (include/tk.h). T is a descriptor only."""
+    ls = [_labels(x, l, w) for x, l, w in ((A, labA, "labA"), (B1, labB1, "labB1"), (T, labT, "labT"),
+                                           (B2, labB2, "labB2"), (C, labC, "labC"))]
+    _check(_contract2(A.h, _data(A, a, "a"), ls[0][1], B1.h, _data(B1, b1, "b1"), ls[1][1], T.h, ls[2][1], B2.h,
+                      _data(B2, b2, "b2"), ls[3][1], C.h, _data(C, c, "c"), ls[4][1], float(alpha), float(beta),
+                      _ws(ws, ws_bytes), ws_bytes, _stream(stream)))
 
 
 def _tuples(pA, qA, pB, qB, pAB, qAB):

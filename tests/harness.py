@@ -104,3 +104,60 @@ def gpu_chain(cfg, alpha=1.0, beta=0.0, c_init=None, keep=True, complex_=False, 
         T[nc] = (C, c)
         out[nc] = (C, c.cpu().numpy() if keep else None)
     return out
+
+
+def gpu_chain_fused(cfg, alpha=1.0, beta=0.0, c_init=None):
+    """Like gpu_chain, but every consecutive pair (step i's output is step i+1's A operand) that
+    tk_contract2 runs as ONE kernel goes through tk_contract2 (its intermediate is then absent from the
+    result). Returns ({name: (tk.Tensor, host flat)}, [fused step indices]). alpha / beta / c_init apply
+    to the last call that writes each output, as in gpu_chain."""
+    import torch
+    from paper_2508_10076_b200 import tk, layout_io
+    dev = torch.device("cuda")
+    T = {}
+    for name, (spec, idx) in cfg["tensors"].items():
+        t = tk.tensor_from_spec(spec)
+        T[name] = (t, torch.from_numpy(layout_io.fill(t, cfg["cfg"], idx)).to(dev))
+    steps = cfg["steps"]
+    desc = {}
+    for (na, la, nb, lb, nc, lc, ncod) in steps:
+        A = desc.get(na, T[na][0] if na in T else None)
+        desc[nc] = tk.tk_contract_output(A, la, desc.get(nb, T[nb][0] if nb in T else None), lb, lc, ncod)
+    out, fused = {}, []
+
+    def new_out(C):
+        if c_init is not None:
+            return torch.from_numpy(c_init(C)).to(dev)
+        return torch.full((C.nelems,), float("nan"), dtype=torch.float64, device=dev)
+
+    i = 0
+    while i < len(steps):
+        na, la, nb, lb, nc, lc, ncod = steps[i]
+        if i + 1 < len(steps) and steps[i + 1][0] == nc:
+            _, la2, nb2, lb2, nc2, lc2, _ = steps[i + 1]
+            Tm, C = desc[nc], desc[nc2]
+            n, fu = tk.tk_contract2_workspace(T[na][0], la, T[nb][0], lb, Tm, lc, T[nb2][0], lb2, C, lc2,
+                                              want_fused=True)
+            if fu:
+                c = new_out(C)
+                ws = torch.empty(max(n // 8 + 32, 1), dtype=torch.float64, device=dev)
+                tk.tk_contract2(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, Tm, lc, T[nb2][0], T[nb2][1], lb2,
+                                C, c, lc2, alpha=alpha, beta=beta, ws=ws, ws_bytes=ws.numel() * 8)
+                torch.cuda.synchronize()
+                T[nc2] = (C, c)
+                out[nc2] = (C, c.cpu().numpy())
+                fused.append(i)
+                i += 2
+                continue
+        A, a = T[na]
+        B, b = T[nb]
+        C = desc[nc]
+        c = new_out(C)
+        n = tk.tk_contract_workspace(A, la, B, lb, C, lc)
+        ws = torch.empty(max(n // 8 + 32, 1), dtype=torch.float64, device=dev)
+        tk.tk_contract(A, a, la, B, b, lb, C, c, lc, alpha=alpha, beta=beta, ws=ws, ws_bytes=ws.numel() * 8)
+        torch.cuda.synchronize()
+        T[nc] = (C, c)
+        out[nc] = (C, c.cpu().numpy())
+        i += 1
+    return out, fused

@@ -472,3 +472,45 @@ def test_layout_equals_oracle_bench_sizes(cfgfun):
         assert Ct.nelems == oracle_layout(spec).nelems
         assert_same_layout(spec)
         T[nc] = (spec, Ct)
+
+
+def _pair_descs(cfg, i):
+    steps = cfg["steps"]
+    T = {n: tk.tensor_from_spec(spec) for n, (spec, _) in cfg["tensors"].items()}
+    for (na, la, nb, lb, nc, lc, ncod) in steps[:i + 2]:
+        T[nc] = tk.tk_contract_output(T[na], la, T[nb], lb, lc, ncod)
+    (na, la, nb, lb, nc, lc, _), (_, la2, nb2, lb2, nc2, lc2, _) = steps[i], steps[i + 1]
+    return (T[na], la, T[nb], lb, T[nc], lc, T[nb2], lb2, T[nc2], lc2)
+
+
+@pytest.mark.parametrize("cfgfun,fused", [(W.cfg2, [False, True, False]), (lambda: W.cfg3(chi=96), [False, True, False]),
+                                          (W.cfg5, []), (W.cfg6, [False, False]),
+                                          (lambda: W.cfg7(n_mult=24), [False, False, False])],
+                         ids=["cfg2", "cfg3_chi96", "cfg5", "cfg6", "cfg7_m24"])
+def test_contract2_fusion_decision(cfgfun, fused):
+    """Host-only plan query: which consecutive pairs tk_contract2 runs as one kernel (the abelian MPO pair
+    T1.W1 -> T2, T2.W2 -> T3), and the workspace of the others (T plus the larger step workspace)."""
+    cfg = cfgfun()
+    steps = cfg["steps"]
+    got = []
+    for i in range(len(steps) - 1):
+        d = _pair_descs(cfg, i)
+        n, fu = tk.tk_contract2_workspace(*d, want_fused=True)
+        got.append(fu)
+        if fu:
+            assert n == 0
+        else:
+            A, la, B1, lb1, Tm, lt, B2, lb2, C, lc = d
+            n1 = tk.tk_contract_workspace(A, la, B1, lb1, Tm, lt)
+            n2 = tk.tk_contract_workspace(Tm, lt, B2, lb2, C, lc)
+            assert n >= Tm.nelems * 8 + max(n1, n2)
+    assert got == fused
+
+
+def test_contract2_errors():
+    cfg = W.cfg2()
+    A, la, B1, lb1, Tm, lt, B2, lb2, C, lc = _pair_descs(cfg, 1)
+    with pytest.raises(tk.TKError):  # T is not A.B1's output HomSpace
+        tk.tk_contract2_workspace(A, la, B1, lb1, C, lc, B2, lb2, C, lc)
+    with pytest.raises(ValueError):
+        tk.tk_contract2_workspace(A, la[:-1], B1, lb1, Tm, lt, B2, lb2, C, lc)
