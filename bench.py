@@ -236,9 +236,13 @@ def measure_fp64_peak(stream, dev):
 
 def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
     """Every DMRG-shaped chain (cfg2/3/5/6/7/8 at their full sizes) replayed as ONE CUDA graph; L2 is
-    flushed (a 256 MB write) before every timed replay; median of `reps` CUDA-event timings. Roofline per
-    SURVEY §8(d): sum over steps of tk_contract_roofline (GEMM blocks max(flops/P, bytes/BW) + permute
-    bytes/BW) at the in-run DMMA peak and MEASURED_PEAKS' HBM bandwidth."""
+    flushed (a 256 MB write) before every timed replay; median of `reps` CUDA-event timings. Two ways:
+    the network through tk_ncon (`us_per_chain`: the library orders the intermediates -- a gathered MPO
+    step stores straight into the next GEMM's operand order -- and runs the abelian MPO pair through
+    tk_contract2) and the config's explicit pairwise steps (`us_per_chain_pairwise`: one tk_contract per
+    step, intermediates in the config's orders). Roofline per SURVEY §8(d) over the config's pairwise steps: sum of
+    tk_contract_roofline (GEMM blocks max(flops/P, bytes/BW) + permute bytes/BW) at the in-run DMMA peak
+    and MEASURED_PEAKS' HBM bandwidth."""
     import torch
     from paper_2508_10076_b200 import tk, layout_io
     from workloads import configs as W
@@ -253,73 +257,71 @@ def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
             t = tk.tensor_from_spec(spec)
             T[name] = (t, torch.from_numpy(layout_io.fill(t, cfg["cfg"], idx)).to(dev))
         steps, roof = [], {"flops": 0.0, "gemm_bytes": 0.0, "permute_bytes": 0.0, "seconds": 0.0}
-        desc = {}
         for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
             A, B = T[na][0], T[nb][0]
-            desc[nc] = C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
+            C = tk.tk_contract_output(A, la, B, lb, lc, ncod)
             T[nc] = (C, torch.zeros(C.nelems, dtype=torch.float64, device=dev))
             r = tk.tk_contract_roofline(A, la, B, lb, C, lc, peak_flops, hbm_bytes_s)
             for key in roof:
                 roof[key] += r[key]
-        # calls: a consecutive pair that tk_contract2 runs as one kernel (the MPO steps T1.W1.W2 of the
-        # abelian chains) goes through it; every other step is one tk_contract
-        cs, i, nfused = cfg["steps"], 0, 0
-        while i < len(cs):
-            na, la, nb, lb, nc, lc, ncod = cs[i]
-            if i + 1 < len(cs) and cs[i + 1][0] == nc:
-                _, la2, nb2, lb2, nc2, lc2, _ = cs[i + 1]
-                nws, fu = tk.tk_contract2_workspace(T[na][0], la, T[nb][0], lb, desc[nc], lc, T[nb2][0], lb2,
-                                                    desc[nc2], lc2, want_fused=True)
-                if fu:
-                    ws = torch.empty(max(nws // 8 + 64, 1), dtype=torch.float64, device=dev)
-                    steps.append((na, la, nb, lb, nc, lc, ws, (nb2, lb2, nc2, lc2)))
-                    nfused += 1
-                    i += 2
-                    continue
+        # the config's explicit pairwise chain: one tk_contract per step, intermediates in the config's
+        # leg orders (the baseline the network path below is compared with)
+        for (na, la, nb, lb, nc, lc, ncod) in cfg["steps"]:
             nws = tk.tk_contract_workspace(T[na][0], la, T[nb][0], lb, T[nc][0], lc)
             ws = torch.empty(max(nws // 8 + 64, 1), dtype=torch.float64, device=dev)
-            steps.append((na, la, nb, lb, nc, lc, ws, None))
-            i += 1
+            steps.append((na, la, nb, lb, nc, lc, ws))
 
         def chain():
             n = 0
-            for (na, la, nb, lb, nc, lc, ws, pair) in steps:
-                if pair is None:
-                    tk.tk_contract(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], T[nc][1], lc, ws=ws,
-                                   ws_bytes=ws.numel() * 8, stream=stream)
-                else:
-                    nb2, lb2, nc2, lc2 = pair
-                    tk.tk_contract2(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], lc, T[nb2][0],
-                                    T[nb2][1], lb2, T[nc2][0], T[nc2][1], lc2, ws=ws, ws_bytes=ws.numel() * 8,
-                                    stream=stream)
+            for (na, la, nb, lb, nc, lc, ws) in steps:
+                tk.tk_contract(T[na][0], T[na][1], la, T[nb][0], T[nb][1], lb, T[nc][0], T[nc][1], lc, ws=ws,
+                               ws_bytes=ws.numel() * 8, stream=stream)
                 n += tk.tk_last_launch_count()
             return n
-        with torch.cuda.stream(stream):
-            launches = chain()
-            torch.cuda.synchronize(dev)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                chain()
-            for _ in range(3):
-                g.replay()
-            ts = []
-            for _ in range(reps):
-                flush.fill_(1.0)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                g.replay()
-                e1.record(stream)
-                e1.synchronize()
-                ts.append(e0.elapsed_time(e1) * 1e3)
-        us = float(np.median(ts))
-        out[f"cfg{k}"] = {"kind": cfg["kind"], "us_per_chain": round(us, 2), "steps": len(cfg["steps"]),
-                          "fused_pairs": nfused,
-                          "launches": launches, "block_flops": roof["flops"],
+        # the same network through tk_ncon (the library plans the intermediates' leg orders and runs the
+        # fusable pairs through tk_contract2; same pairwise order, same arithmetic)
+        names, nlabels, norder, ncod_out, out_name = W.chain_as_ncon(cfg)
+        nT = [T[nm][0] for nm in names]
+        nws_n = tk.tk_ncon_workspace(nT, nlabels, norder, ncod_out)
+        nws = torch.empty(max(nws_n // 8 + 64, 1), dtype=torch.float64, device=dev)
+        Cn = T[out_name][0]
+
+        def network():
+            tk.tk_ncon(nT, [T[nm][1] for nm in names], nlabels, norder, ncod_out, Cn, T[out_name][1], ws=nws,
+                       ws_bytes=nws.numel() * 8, stream=stream)
+            return tk.tk_last_launch_count()
+
+        def timed(fn):
+            with torch.cuda.stream(stream):
+                n = fn()
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    fn()
+                for _ in range(3):
+                    g.replay()
+                ts = []
+                for _ in range(reps):
+                    flush.fill_(1.0)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    g.replay()
+                    e1.record(stream)
+                    e1.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e3)
+            del g
+            return float(np.median(ts)), n
+        us_pw, launches_pw = timed(chain)
+        us, launches = timed(network)
+        out[f"cfg{k}"] = {"kind": cfg["kind"], "us_per_chain": round(us, 2), "launches": launches,
+                          "api": "tk_ncon", "steps": len(cfg["steps"]),
+                          "us_per_chain_pairwise": round(us_pw, 2), "launches_pairwise": launches_pw,
+                          "block_flops": roof["flops"],
                           "GFLOP_s": round(roof["flops"] / (us * 1e-6) / 1e9, 2),
                           "roofline_us": round(roof["seconds"] * 1e6, 2),
                           "roofline_frac": round(roof["seconds"] * 1e6 / us, 3),
                           "permute_bytes": roof["permute_bytes"], "gemm_min_bytes": roof["gemm_bytes"]}
-        del g, T, steps
+        del T, steps, nws
         torch.cuda.empty_cache()
     return out
 

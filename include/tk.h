@@ -207,12 +207,15 @@ tk_status tk_contract_tuples(const tk_tensor* A, const void* a, int32_t conjA, c
  * are contracted and appear exactly twice -- on two tensors, or twice on one tensor, which is a partial
  * trace (Alg. 3, tk_trace; done first, bosonic and planar kinds); negative labels -1, -2, ..., -m are the open legs, which become the
  * output's legs in that order, the first n_cod_out of them its codomain. `order` lists every positive
- * label; the network is contracted pairwise in that order -- each step takes the two tensors holding the
- * next label and contracts all labels they share (tk_contract, reading C2; for fermionic kinds the order
- * is part of the definition, reading C13). Disconnected pieces are joined by outer products at the end.
- * Intermediates keep the (open A ; open B) order and live in the workspace (tk_ncon_workspace bytes,
- * 256-byte aligned, caller-owned) together with the pairwise scratch. alpha / beta apply to the output
- * only. Errors: MALFORMED_NETWORK, UNKNOWN_LABEL (order), SPACE_MISMATCH (legs or C's HomSpace),
+ * label; the network is contracted pairwise in that order, a left fold -- each step takes the two
+ * tensors holding the next label and contracts all labels they share (tk_contract, reading C2), the
+ * running intermediate as the left operand A (two inputs: in list order; for fermionic kinds the
+ * operand order is part of the definition, reading C13). Disconnected pieces are joined by outer
+ * products at the end. Intermediates live in the workspace (tk_ncon_workspace bytes, 256-byte aligned,
+ * caller-owned) together with the pairwise scratch; their leg order is the library's choice (it
+ * changes no value): the producer's C~ order, or the consumer's operand order when the consumer would
+ * otherwise permute it in a pass of its own. Consecutive steps that tk_contract2 fuses (the abelian MPO
+ * pair) run as one kernel. alpha / beta apply to the output only. Errors: MALFORMED_NETWORK, UNKNOWN_LABEL (order), SPACE_MISMATCH (legs or C's HomSpace),
  * WORKSPACE_TOO_SMALL; a single tensor is TK_ERR_UNSUPPORTED (use tk_permute). */
 tk_status tk_ncon_output(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
                          int32_t norder, int32_t n_cod_out, tk_tensor** C);

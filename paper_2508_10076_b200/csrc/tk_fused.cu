@@ -37,18 +37,14 @@ namespace tk {
 namespace {
 constexpr int kFusedThreads = 128;  // 4 warps, each its own chunk of <= 32 fibers
 constexpr int kFusedWarps = kFusedThreads / 32;
-#ifndef TK_FUSED_FPT
-#define TK_FUSED_FPT 1
-#endif
-constexpr int kFusedFpt = TK_FUSED_FPT;  // fibers per thread (NM 4 / 8; NM 16 uses 1)
 constexpr int kFusedMaxIn = 64;     // inputs per class (the sign mask is 64 bits)
 constexpr int kFusedMaxMid = 64;    // T elements per fiber
 constexpr int kFusedMaxCoef = 1024; // coefficient entries per class (shared-memory doubles per warp)
 
-// A class program, in 8-byte words: header | ins[n_in] | t1[n_t1] | t2[n_t2] | midref[] | coef[]
+// A class program, in 8-byte words: header | ins[n_in] | t1[n_t1] | t2[n_t2] | outs[n_out] | midref[] | coef[]
 struct FusedHeader {
   int32_t F, nrl, n_in, n_t1, n_t2, n_mid, n_ref, n_coef1, n_coef;
-  int32_t pad;
+  int32_t n_out;
   int32_t ext[4];        // mixed radix of the fiber index f over step 1's row legs (first fastest)
   uint64_t neg_in;       // bit j: input j enters negated (its subblock's coefficient -1, C13)
 };
@@ -58,9 +54,8 @@ struct FusedIn {         // a step-1 input: T1 offset = base + sum_l digit_l(f) 
 struct FusedT1 {         // a step-1 row tree: T values mid0 + n (n < N) = sum_k in(in0 + k) coef[c0 + k NM + n]
   int32_t in0, K, N, mid0, c0, pad[3];
 };
-struct FusedT2 {         // a step-2 row tree: C[cbase + n ldc + f] = sum_k mid(midref[r0 + k]) coef[c0 + k N + n]
-  int64_t cbase;
-  int32_t ldc, K, N, r0, c0, pad;
+struct FusedT2 {         // a step-2 row tree: output n = sum_k mid(midref[r0 + k]) coef[c0 + k NM + n] -> outs[o0 + n]
+  int32_t K, N, r0, c0, o0, pad;
 };
 // midref: 2 * T-value index + (subblock coefficient < 0); coef: B~ table entry (2 * offset into W + sign,
 // -1 = structural zero) of each distinct GEMM group of the class, step 1's first (n_coef1 of them)
@@ -69,7 +64,7 @@ struct FusedChunk {      // fibers [f0, f0 + nf) of the class whose program star
   int32_t f0, nf;
 };
 static_assert(sizeof(FusedHeader) == 64 && sizeof(FusedIn) == 16 && sizeof(FusedT1) == 32 &&
-                  sizeof(FusedT2) == 32,
+                  sizeof(FusedT2) == 24,
               "fused layout");
 }  // namespace
 
@@ -80,17 +75,21 @@ __device__ __forceinline__ void fused_cp8(double* smem, const double* gmem) {
 
 // One warp per chunk of <= 32 fibers of one class (many classes are smaller than a CTA); 4 independent
 // warps per CTA. Per warp: the class's coefficients are resolved once into shared memory (W value, sign,
-// alpha for step 2: exactly the B~ value the gathered GEMM forms), each K x N table stored as K rows of
-// NM (zero-padded, 16-byte aligned: read as double2 broadcasts). Per thread (one fiber): for each step-1
-// row tree, its K inputs are loaded into registers and its N T values go to shared memory ([slot][thread],
-// conflict-free); then each step-2 row tree reads its K T values and writes its N outputs. Every product
-// is the gathered GEMM's own: acc_n = fma(+-a_k, b~_kn, acc_n) over k ascending, zeros included, so the
-// fused result is bitwise that of the two tk_contract calls. NM (4 / 8 / 16) bounds K and N of both steps.
-template <int NM, int FPT>
+// alpha for step 2 without an output permute: exactly the B~ value the gathered GEMM forms), each K x N
+// table stored as K rows of NM (zero-padded, 16-byte aligned: read as double2 broadcasts). Per thread (one
+// fiber): for each step-1 row tree, its K inputs are loaded into registers and its N T values go to shared
+// memory ([slot][thread], conflict-free); then each step-2 row tree reads its K T values and writes its N
+// outputs (through the output permute's map when step 2 has one). Every product is the gathered GEMM's
+// own: acc_n = fma(+-a_k, b~_kn, acc_n) over k ascending, zeros included, so the fused result is bitwise
+// that of the two tk_contract calls. NM (4 / 8 / 16) bounds K and N of both steps.
+// (Measured alternatives, cfg3: all inputs fetched up front by cp.async and T values recomputed where
+// consumed, 101 us; two fibers per thread, 86 us; next tree's inputs prefetched, 89 us; this, 77-90 us
+// against 2 x 42 us for the two gathered steps -- see DESIGN.md §6.4.)
+template <int NM>
 __global__ void __launch_bounds__(kFusedThreads)
     fused_pair_kernel(const double* __restrict__ T1, const double* __restrict__ W1, const double* __restrict__ W2,
                       double* __restrict__ C, const int64_t* __restrict__ progs, const FusedChunk* __restrict__ chunks,
-                      int nchunks, int max_mid, int max_coef, double alpha, double beta) {
+                      int nchunks, int max_mid, int max_coef, double calpha, double oalpha, double beta) {
   extern __shared__ __align__(16) double fsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
@@ -109,27 +108,26 @@ __global__ void __launch_bounds__(kFusedThreads)
   const int4* ins = reinterpret_cast<const int4*>(prog + 8);
   const int4* t1 = reinterpret_cast<const int4*>(prog + 8 + 2 * h.n_in);
   const FusedT2* t2 = reinterpret_cast<const FusedT2*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1);
-  const int32_t* midref = reinterpret_cast<const int32_t*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1 + 4 * h.n_t2);
+  const GatherOut* outs = reinterpret_cast<const GatherOut*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2);
+  const int32_t* midref =
+      reinterpret_cast<const int32_t*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2 + 4 * h.n_out);
   const int32_t* coefs = midref + ((h.n_ref + 1) & ~1);
   double* vmid = fsm;
-  double* cf = vmid + max_mid * FPT * kFusedThreads + warp * max_coef;
-  // the thread's fibers: f0 + lane + 32 i, i < FPT (a lane beyond the chunk computes nothing)
-  int fib[FPT], d0[FPT], d1[FPT], d2[FPT];
-#pragma unroll
-  for (int i = 0; i < FPT; ++i) {
-    fib[i] = ch.f0 + lane + 32 * i;
-    int r = min(fib[i], ch.f0 + ch.nf - 1);  // clamp: dead fibers load (valid) data and store nothing
-    d0[i] = d1[i] = d2[i] = 0;
-    if (h.nrl > 0) { d0[i] = r % h.ext[0]; r /= h.ext[0]; }
-    if (h.nrl > 1) { d1[i] = r % h.ext[1]; r /= h.ext[1]; }
-    if (h.nrl > 2) d2[i] = r % h.ext[2];
+  double* cf = vmid + max_mid * kFusedThreads + warp * max_coef;
+  const int f = ch.f0 + lane;
+  int d0 = 0, d1 = 0, d2 = 0;  // f's digits over step 1's row legs (first fastest)
+  {
+    int r = f;
+    if (h.nrl > 0) { d0 = r % h.ext[0]; r /= h.ext[0]; }
+    if (h.nrl > 1) { d1 = r % h.ext[1]; r /= h.ext[1]; }
+    if (h.nrl > 2) d2 = r % h.ext[2];
   }
   // the class's B~ values, one lane per entry
   for (int e = lane; e < h.n_coef; e += 32) {
     const int be = __ldg(coefs + e);
     double v = 0.0;
     if (be >= 0) {
-      v = e < h.n_coef1 ? __ldg(W1 + (be >> 1)) : alpha * __ldg(W2 + (be >> 1));
+      v = e < h.n_coef1 ? __ldg(W1 + (be >> 1)) : calpha * __ldg(W2 + (be >> 1));
       if (be & 1) v = -v;
     }
     cf[e] = v;
@@ -142,84 +140,69 @@ __global__ void __launch_bounds__(kFusedThreads)
   for (int t = 0; t < h.n_t1; ++t) {
     const int4 q = __ldg(t1 + 2 * t);  // in0, K, N, mid0
     const int c0 = __ldg(reinterpret_cast<const int*>(t1 + 2 * t + 1));
-    double a[FPT][NM];
+    double a[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
+      a[k] = 0.0;
       if (k < q.y) {
         const int4 x = __ldg(ins + q.x + k);
-#pragma unroll
-        for (int i = 0; i < FPT; ++i) a[i][k] = __ldg(T1 + (x.x + d0[i] * x.y + d1[i] * x.z + d2[i] * x.w));
+        a[k] = __ldg(T1 + (x.x + d0 * x.y + d1 * x.z + d2 * x.w));
       }
     }
-    double acc[FPT][NM];
+    double acc[NM];
 #pragma unroll
-    for (int i = 0; i < FPT; ++i)
-#pragma unroll
-      for (int n = 0; n < NM; ++n) acc[i][n] = 0.0;
+    for (int n = 0; n < NM; ++n) acc[n] = 0.0;
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
       if (k < q.y) {
-        const bool ng = (h.neg_in >> (q.x + k)) & 1;
+        const double ak = ((h.neg_in >> (q.x + k)) & 1) ? -a[k] : a[k];
         const double2* w = cf2 + (c0 + k * NM) / 2;
 #pragma unroll
         for (int j = 0; j < NM / 2; ++j) {
           const double2 b = w[j];
-#pragma unroll
-          for (int i = 0; i < FPT; ++i) {
-            const double ak = ng ? -a[i][k] : a[i][k];
-            acc[i][2 * j] = fma(ak, b.x, acc[i][2 * j]);
-            acc[i][2 * j + 1] = fma(ak, b.y, acc[i][2 * j + 1]);
-          }
+          acc[2 * j] = fma(ak, b.x, acc[2 * j]);
+          acc[2 * j + 1] = fma(ak, b.y, acc[2 * j + 1]);
         }
       }
     }
 #pragma unroll
     for (int n = 0; n < NM; ++n)
-      if (n < q.z)
-#pragma unroll
-        for (int i = 0; i < FPT; ++i) vmid[((q.w + n) * FPT + i) * kFusedThreads + tid] = acc[i][n];
+      if (n < q.z) vmid[(q.w + n) * kFusedThreads + tid] = acc[n];
   }
-  // step 2's GEMM per row tree: the fiber's outputs, C = alpha * (...) + beta * C (alpha in the coefficients)
+  // step 2's GEMM per row tree: the fiber's outputs, C = alpha * (...) + beta * C
   for (int t = 0; t < h.n_t2; ++t) {
     const FusedT2 q = t2[t];
-    double acc[FPT][NM];
+    double acc[NM];
 #pragma unroll
-    for (int i = 0; i < FPT; ++i)
-#pragma unroll
-      for (int n = 0; n < NM; ++n) acc[i][n] = 0.0;
+    for (int n = 0; n < NM; ++n) acc[n] = 0.0;
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
       if (k < q.K) {
         const int r = __ldg(midref + q.r0 + k);
-        double ak[FPT];
-#pragma unroll
-        for (int i = 0; i < FPT; ++i) {
-          ak[i] = vmid[((r >> 1) * FPT + i) * kFusedThreads + tid];
-          if (r & 1) ak[i] = -ak[i];
-        }
+        double ak = vmid[(r >> 1) * kFusedThreads + tid];
+        if (r & 1) ak = -ak;
         const double2* w = cf2 + (q.c0 + k * NM) / 2;
 #pragma unroll
         for (int j = 0; j < NM / 2; ++j) {
           const double2 b = w[j];
-#pragma unroll
-          for (int i = 0; i < FPT; ++i) {
-            acc[i][2 * j] = fma(ak[i], b.x, acc[i][2 * j]);
-            acc[i][2 * j + 1] = fma(ak[i], b.y, acc[i][2 * j + 1]);
-          }
+          acc[2 * j] = fma(ak, b.x, acc[2 * j]);
+          acc[2 * j + 1] = fma(ak, b.y, acc[2 * j + 1]);
         }
       }
     }
+    uint32_t e0 = (uint32_t)outs[q.o0].ext0, e1 = (uint32_t)outs[q.o0].ext1, r = (uint32_t)f;
+    const uint32_t o0 = r % e0;
+    r /= e0;
+    const uint32_t o1 = r % e1, o2 = r / e1;  // f's digits in the output map's radix
 #pragma unroll
-    for (int i = 0; i < FPT; ++i) {
-      if (fib[i] >= ch.f0 + ch.nf) continue;
-      double* p = C + q.cbase + fib[i];
-#pragma unroll
-      for (int n = 0; n < NM; ++n)
-        if (n < q.N) {
-          double* pn = p + (int64_t)n * q.ldc;
-          *pn = beta != 0.0 ? fma(beta, *pn, acc[i][n]) : acc[i][n];
-        }
-    }
+    for (int n = 0; n < NM; ++n)
+      if (n < q.N) {
+        const GatherOut o = outs[q.o0 + n];
+        double* pn = C + o.base + ((int64_t)o0 * o.str[0] + (int64_t)o1 * o.str[1] + (int64_t)o2 * o.str[2]);
+        double y = oalpha * acc[n];
+        if (o.neg) y = -y;
+        *pn = beta != 0.0 ? fma(beta, *pn, y) : y;
+      }
   }
 }
 
@@ -313,7 +296,9 @@ static bool build_fused(FusedPlan& F) {
   const ContractPlan& P1 = *F.p1;
   const ContractPlan& P2 = *F.p2;
   // both steps entirely gathered (no other GEMM tiles: K = 0 blocks of C would need their beta pass)
-  if (!P1.gather || !P2.gather || !P1.pc.identity || !P2.pc.identity || P1.cplx || P2.cplx) return false;
+  // step 1's output is T itself (C~1 canonical); step 2 may carry an output permute (abelian: each C~2
+  // subblock lands in one C subblock with a sign), folded into the fused kernel's stores
+  if (!P1.gather || !P2.gather || !P1.pc.identity || P1.cplx || P2.cplx) return false;
   if (!P1.tiles.empty() || !P2.tiles.empty()) return false;
   GatherIndex X1, X2;
   if (!index_gather(P1, X1) || !index_gather(P2, X2)) return false;
@@ -373,6 +358,12 @@ static bool build_fused(FusedPlan& F) {
       }
     }
   }
+  // output permute of step 2 (C~2 -> C), abelian: folded into the stores (OutMap, tk_plan.cpp)
+  std::unique_ptr<OutMap> om;
+  if (!P2.pc.identity) {
+    om = std::make_unique<OutMap>(P2.pc, P2.lc);
+    if (!om->ok()) return false;
+  }
   // classes, each one program
   std::map<int, std::vector<int>> cls;  // root -> members (step-1 trees < n1 <= step-2 trees)
   for (int i = 0; i < n1 + n2; ++i) cls[find_union(parent, i)].push_back(i);
@@ -428,14 +419,26 @@ static bool build_fused(FusedPlan& F) {
       mid0_of[t] = q.mid0;
       v1.push_back(q);
     }
+    std::vector<GatherOut> outs;
     for (int t : t2s) {
       const RowTree& rt = X2.trees[t];
       if (rt.nrows != Fr) return false;
       const GemmGroup& G = X2.groups[rt.grp];
       FusedT2 q{};
-      q.cbase = G.c_off + rt.r0;
-      if (G.ldc > INT32_MAX) return false;
-      q.ldc = (int32_t)G.ldc;
+      q.o0 = (int32_t)outs.size();
+      for (int n = 0; n < G.N; ++n) {
+        GatherOut o{};
+        if (P2.pc.identity) {  // C~2 is C: the tree's rows are contiguous
+          o.base = G.c_off + rt.r0 + (int64_t)n * G.ldc;
+          o.str[0] = 1;
+          o.ext0 = Fr;
+          o.ext1 = 1;
+        } else if (!om->map(G.c_off + rt.r0 + (int64_t)n * G.ldc, Fr, o) ||
+                   (n > 0 && (o.ext0 != outs[q.o0].ext0 || o.ext1 != outs[q.o0].ext1))) {
+          return false;
+        }
+        outs.push_back(o);
+      }
       q.K = G.K;
       q.N = G.N;
       q.r0 = (int32_t)midref.size();
@@ -457,6 +460,7 @@ static bool build_fused(FusedPlan& F) {
     h.n_t1 = (int32_t)v1.size();
     h.n_t2 = (int32_t)v2.size();
     h.n_ref = (int32_t)midref.size();
+    h.n_out = (int32_t)outs.size();
     h.n_coef1 = (int32_t)coef1.size();
     h.n_coef = (int32_t)(coef1.size() + coef2.size());
     if (h.n_coef > kFusedMaxCoef) return false;
@@ -474,6 +478,7 @@ static bool build_fused(FusedPlan& F) {
     put(ins.data(), ins.size() * sizeof(FusedIn));
     put(v1.data(), v1.size() * sizeof(FusedT1));
     put(v2.data(), v2.size() * sizeof(FusedT2));
+    put(outs.data(), outs.size() * sizeof(GatherOut));
     if (midref.size() & 1) midref.push_back(0);
     put(midref.data(), midref.size() * 4);
     coef1.insert(coef1.end(), coef2.begin(), coef2.end());
@@ -484,11 +489,10 @@ static bool build_fused(FusedPlan& F) {
     if (plan_debug() && getenv("TK_FUSED_ALL"))
       fprintf(stderr, "[tk fused] class: F %d, trees %zu + %zu, n_in %d, n_mid %d, n_coef %d\n", Fr, t1s.size(),
               t2s.size(), h.n_in, h.n_mid, h.n_coef);
-    const int cw = 32 * (F.nm == 16 ? 1 : kFusedFpt);  // fibers per warp
-    for (int f0 = 0; f0 < Fr; f0 += cw) F.chunks.push_back(FusedChunk{prog, f0, std::min(cw, Fr - f0)});
+    for (int f0 = 0; f0 < Fr; f0 += 32) F.chunks.push_back(FusedChunk{prog, f0, std::min(32, Fr - f0)});
   }
   F.max_coef = (F.max_coef + 1) & ~1;
-  F.smem = (F.max_mid * kFusedThreads * (F.nm == 16 ? 1 : kFusedFpt) + F.max_coef * kFusedWarps) * 8;
+  F.smem = (F.max_mid * kFusedThreads + F.max_coef * kFusedWarps) * 8;
   if (plan_debug())
     fprintf(stderr, "[tk fused] %zu classes, max n_in %d, max n_mid %d, max n_coef %d\n", cls.size(), F.max_in,
             F.max_mid, F.max_coef);
@@ -592,7 +596,7 @@ tk_status tk_contract2(const tk_tensor* A_, const void* a, const int32_t* labA, 
   F->ensure_uploaded();
   check_cuda(g_fused_attr.run([&] {
                cudaError_t e = cudaSuccess;
-               for (auto k : {fused_pair_kernel<4, kFusedFpt>, fused_pair_kernel<8, kFusedFpt>, fused_pair_kernel<16, 1>})
+               for (auto k : {fused_pair_kernel<4>, fused_pair_kernel<8>, fused_pair_kernel<16>})
                  if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                return e;
              }),
@@ -611,10 +615,11 @@ tk_status tk_contract2(const tk_tensor* A_, const void* a, const int32_t* labA, 
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   if (!F->chunks.empty()) {
-    auto kern = F->nm == 4 ? fused_pair_kernel<4, kFusedFpt> : F->nm == 8 ? fused_pair_kernel<8, kFusedFpt> : fused_pair_kernel<16, 1>;
+    auto kern = F->nm == 4 ? fused_pair_kernel<4> : F->nm == 8 ? fused_pair_kernel<8> : fused_pair_kernel<16>;
     check_cuda(cudaLaunchKernelEx(&cfg, kern, (const double*)a, (const double*)b1, (const double*)b2,
                                   (double*)c, (const int64_t*)F->d_progs.p, (const FusedChunk*)F->d_chunks.p,
-                                  (int)F->chunks.size(), F->max_mid, F->max_coef, alpha, beta),
+                                  (int)F->chunks.size(), F->max_mid, F->max_coef,
+                                  F->p2->pc.identity ? alpha : 1.0, F->p2->pc.identity ? 1.0 : alpha, beta),
                "fused launch");
     add_launches(1);
   }

@@ -1328,7 +1328,8 @@ template <int KM, int NM>
 __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
     gather_skinny_kernel(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                          const int64_t* __restrict__ slots, const GatherSeg* __restrict__ segs,
-                         const int32_t* __restrict__ btab, double alpha, double beta) {
+                         const int32_t* __restrict__ btab, const GatherOut* __restrict__ gouts, double alpha,
+                         double oalpha, double beta) {
   constexpr int RPT = gather_rows(KM) / kGatherRows;  // rows per thread
   __shared__ double Bs[kSkinnyMax * kSkinnyMax];
   extern __shared__ __align__(16) double gather_dyn[];
@@ -1359,9 +1360,11 @@ __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
   pdl_wait();
   // A~ rows first (cp.async, nothing held in registers), then the B~ block, then one wait for both
   uint32_t neg[RPT];
+  int rlo[RPT];          // the row's first segment (its row tree): the output map's index
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     neg[j] = 0;
+    rlo[j] = 0;
     const int lr = tid + j * kGatherRows;
     if (lr >= t.nrows) continue;
     const int m = t.m0 + lr;
@@ -1374,6 +1377,7 @@ __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
     }
     const int r0 = ss[lo].r0;
     while (lo > 0 && ss[lo - 1].r0 == r0) --lo;
+    rlo[j] = lo;
     // the row's mixed-radix digits over the row legs are the same for every column subblock of the row
     // tree unless a subblock merged its legs differently: decode once, re-decode only when (nrl, ext)
     // changes (the decode -- integer divisions -- dominated the kernel's instruction count)
@@ -1431,13 +1435,30 @@ __global__ void __launch_bounds__(kGatherRows, TK_GATHER_MINB)
         for (int n = 0; n < NM; ++n) acc[n] = fma(a, Bs[k * kSkinnyMax + n], acc[n]);
       }
     }
-    double* Cg = C + g.c_off + t.m0 + lr;
+    if (t.gout0 < 0) {
+      double* Cg = C + g.c_off + t.m0 + lr;
 #pragma unroll
-    for (int n = 0; n < NM; ++n)
-      if (n < N) {
-        double* cp = Cg + (int64_t)n * g.ldc;
-        *cp = beta != 0.0 ? fma(beta, *cp, acc[n]) : acc[n];
-      }
+      for (int n = 0; n < NM; ++n)
+        if (n < N) {
+          double* cp = Cg + (int64_t)n * g.ldc;
+          *cp = beta != 0.0 ? fma(beta, *cp, acc[n]) : acc[n];
+        }
+    } else {  // the output permute folded in: C~ element (row, n) -> C[base + digits . str], sign
+      const GatherOut* go = gouts + t.gout0 + rlo[j] * N;
+      uint32_t r = (uint32_t)(t.m0 + lr - ss[rlo[j]].r0), e0 = (uint32_t)go[0].ext0, e1 = (uint32_t)go[0].ext1;
+      const uint32_t d0 = r % e0;
+      r /= e0;
+      const uint32_t d1 = r % e1, d2 = r / e1;
+#pragma unroll
+      for (int n = 0; n < NM; ++n)
+        if (n < N) {
+          const GatherOut o = go[n];
+          double* cp = C + o.base + ((int64_t)d0 * o.str[0] + (int64_t)d1 * o.str[1] + (int64_t)d2 * o.str[2]);
+          double y = oalpha * acc[n];
+          if (o.neg) y = -y;
+          *cp = beta != 0.0 ? fma(beta, *cp, y) : y;
+        }
+    }
   }
 }
 
@@ -1448,13 +1469,13 @@ static cudaError_t set_gather_attr() {
 }
 
 cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const int64_t* slots, int ntiles,
-                               const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
-                               double beta, cudaStream_t st) {
+                               const GatherSeg* segs, const int32_t* btab, const GatherOut* gouts, int kmax, int nmax,
+                               double alpha, double oalpha, double beta, cudaStream_t st) {
   if (!ntiles) return cudaSuccess;
   const int kc = kmax <= 4 ? 0 : (kmax <= 8 ? 1 : 2), nc = nmax <= 4 ? 0 : (nmax <= 8 ? 1 : 2);
 #define TK_GATHER(KM, NM)                                                                               \
   return launch_k(gather_skinny_kernel<KM, NM>, ntiles, kGatherRows, KM * gather_rows(KM) * 8, st, A, B, C, \
-                  slots, segs, btab, alpha, beta);
+                  slots, segs, btab, gouts, alpha, oalpha, beta);
   switch (kc * 3 + nc) {
     case 0: TK_GATHER(4, 4)
     case 1: TK_GATHER(4, 8)

@@ -194,8 +194,10 @@ static_assert(sizeof(GatherSeg) == 128, "GatherSeg layout");
 struct GatherTile {
   int32_t m0, nrows;   // rows [m0, m0 + nrows) of the group's block
   int32_t seg0, nseg;  // its subblocks (row trees of those rows, every column tree), sorted by (r0, k0)
-  int32_t bt, pad;     // the group's K x N gather table for B~ (btab[bt + k * N + n]: 2 * offset into B
+  int32_t bt;          // the group's K x N gather table for B~ (btab[bt + k * N + n]: 2 * offset into B
                        // + (coefficient < 0), or -1 for a structural zero): B needs no permute pass either
+  int32_t gout0;       // -1: C~ is the output; else the output permute is folded in: the row tree starting
+                       // at the tile's segment s writes column n through gouts[gout0 + s * N + n]
   GemmGroup g;
 };
 // Per-tile slot (kGatherSlotWords 8-byte words): the GatherTile, its first kGatherSlotSegs segments and
@@ -204,9 +206,19 @@ struct GatherTile {
 constexpr int kGatherSlotSegs = 8, kGatherSlotB = 64;
 constexpr int kGatherSlotWords = 10 + 16 * kGatherSlotSegs + kGatherSlotB / 2;
 static_assert(sizeof(GatherTile) == 80 && kGatherSlotWords % 2 == 0, "gather slot layout");
+// Output permute folded into a GEMM's stores (abelian: each C~ subblock lands in one C subblock with a
+// sign): row r of a C~ row tree, column n, goes to C[base + d0 str[0] + d1 str[1] + d2 str[2]] (negated if
+// neg) with (d0, d1, d2) the mixed-radix digits of r over (ext0, ext1, rest) -- the permute's row legs of
+// extent > 1 in C~ order, first fastest. All columns of a row tree share the radix (host-checked).
+struct GatherOut {
+  int64_t base;
+  int32_t str[3], neg;
+  int32_t ext0, ext1;
+};
+static_assert(sizeof(GatherOut) == 32, "GatherOut layout");
 cudaError_t launch_gather_gemm(const double* A, const double* B, double* C, const int64_t* slots, int ntiles,
-                               const GatherSeg* segs, const int32_t* btab, int kmax, int nmax, double alpha,
-                               double beta, cudaStream_t st);
+                               const GatherSeg* segs, const int32_t* btab, const GatherOut* gouts, int kmax, int nmax,
+                               double alpha, double oalpha, double beta, cudaStream_t st);
 
 // split-K (small tiles of under-filled launches): partial 64x64 tiles in `parts`, then one reduction
 // CTA per head tile (deterministic order)

@@ -1,18 +1,25 @@
 // ncon-style network contraction (@tensor networks) on top of the pairwise
 // entry points: the network is contracted pair by pair in the caller's order, every step one
 // tk_contract (Alg. 4) whose intermediate lands in the caller's workspace. See include/tk.h.
+//
+// Intermediates are the library's own, so their leg order is chosen here (the arithmetic does not
+// depend on it: A~, B~ and C~ of every step are the same matrices whatever order an intermediate is
+// stored in). Default: the producer's C~ order (open legs of A, then of B: no output permute). When the
+// consumer would have to permute the intermediate in a separate pass (its A~ / B~ is not gathered) and
+// the producer is a gathered GEMM that can store straight into that order (GatherOut: the abelian output
+// permute folded into its stores), the intermediate is stored in the consumer's operand order instead:
+// the consumer's permute pass disappears. Consecutive steps whose pair tk_contract2 fuses run as one
+// call.
 #include <algorithm>
 #include <map>
 #include <string>
 #include <vector>
 
-#include "tk_internal.hpp"
+#include "tk_plan.hpp"
 
 using namespace tk;
 
 namespace {
-
-size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Item {
   const tk_tensor* t;       // the tensor (borrowed input or owned intermediate)
@@ -20,6 +27,7 @@ struct Item {
   std::vector<int32_t> lab;
   const void* data;         // input pointer, or nullptr for an intermediate (at ws + off)
   size_t off;
+  bool pair_result = false; // output of a pairwise step (a partial trace of an input stands for the input)
 };
 
 struct Step {
@@ -142,7 +150,7 @@ void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* label
     }
     wsmax = std::max(wsmax, w);
     const Tensor& c = *(const Tensor*)C;
-    Item it{C, true, s.labC, nullptr, off};
+    Item it{C, true, s.labC, nullptr, off, true};
     if (!s.last) off = align256(off + (size_t)c.nelems * (c.dtype == TK_C64 ? 16 : 8));
     alive[a] = alive[b] = false;
     items.push_back(it);
@@ -156,6 +164,8 @@ void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* label
         (a < 0 ? a : b) = i;
     if (a < 0) continue;  // contracted already (shared with an earlier label of the same pair)
     if (b < 0) TK_THROW(TK_ERR_MALFORMED_NETWORK, "tk_ncon: internal label bookkeeping");
+    // a left fold: the running intermediate is the left operand A (two inputs: list order)
+    if (items[b].pair_result && !items[a].pair_result) std::swap(a, b);
     contract_pair(a, b);
   }
   // disconnected pieces: outer products, left to right
@@ -167,7 +177,77 @@ void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* label
     contract_pair(al[0], al[1]);
   }
   if (steps.empty()) TK_THROW(TK_ERR_UNSUPPORTED, "tk_ncon: a single tensor (use tk_permute)");
+  // intermediate leg orders (see the file comment): X = output of step k, consumed by step j > k. Last
+  // step first: a decision reads the consumer's final output order, and only changes step k's.
+  static const bool no_relabel = knob("TK_NCON_NO_RELABEL", 0) != 0;
+  for (size_t k = steps.size(); k-- > 0 && !no_relabel;) {
+    if (steps[k].last || steps[k].b < 0) continue;
+    const int x = n + (int)k;
+    size_t j = k + 1;
+    while (j < steps.size() && steps[j].a != x && steps[j].b != x) ++j;
+    if (j == steps.size() || steps[j].b < 0) continue;
+    Step& c = steps[j];
+    const bool isA = c.a == x;
+    const Item& o = items[isA ? c.b : c.a];
+    const Tensor& tx = *(const Tensor*)items[x].t;
+    const Tensor& to = *(const Tensor*)o.t;
+    {  // the consumer as planned now: nothing to do when its operand is gathered or already in place
+      auto P = get_contract_plan(isA ? tx : to, c.labA.data(), isA ? to : tx, c.labB.data(),
+                                 *(const Tensor*)items[n + (int)j].t, c.labC.data());
+      if (P->gather || (isA ? P->pa.identity : P->pb.identity)) continue;
+    }
+    // the operand order of reading C2: A~ = (open legs in C's order | contracted legs in B's order),
+    // B~ = (contracted legs in A's order | open legs in C's order)
+    const std::vector<int32_t>& lx = items[x].lab;
+    const std::vector<int32_t>& lo = o.lab;
+    std::vector<int32_t> open, con;
+    for (int32_t l : c.labC)
+      if (std::find(lx.begin(), lx.end(), l) != lx.end()) open.push_back(l);
+    for (int32_t l : lo)
+      if (std::find(lx.begin(), lx.end(), l) != lx.end()) con.push_back(l);
+    std::vector<int32_t> nl = isA ? open : con;
+    nl.insert(nl.end(), (isA ? con : open).begin(), (isA ? con : open).end());
+    if (nl.size() != lx.size()) continue;
+    const int32_t ncod = (int32_t)(isA ? open.size() : con.size());
+    Step& p = steps[k];
+    tk_tensor* X = nullptr;
+    tk_status st = tk_contract_output(items[p.a].t, p.labA.data(), items[p.b].t, p.labB.data(), nl.data(), ncod, &X);
+    if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    {  // only where the producer absorbs the moved permute (a gathered GEMM storing through the map):
+       // anywhere else it would just move a pass (non-abelian recoupling permutes cost the same or more)
+      auto Pp = get_contract_plan(*(const Tensor*)items[p.a].t, p.labA.data(), *(const Tensor*)items[p.b].t,
+                                  p.labB.data(), *(const Tensor*)X, nl.data());
+      if (!(Pp->gather && (Pp->gout || Pp->pc.identity))) {
+        tk_tensor_release(X);
+        continue;
+      }
+    }
+    size_t w = 0;
+    st = tk_contract_workspace(items[p.a].t, p.labA.data(), items[p.b].t, p.labB.data(), X, nl.data(), &w);
+    if (st != TK_OK) {
+      tk_tensor_release(X);
+      TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    }
+    tk_tensor_release(const_cast<tk_tensor*>(items[x].t));
+    items[x].t = X;  // same element count: the workspace offset stays
+    items[x].lab = nl;
+    p.labC = nl;
+    p.ncod = ncod;
+    (isA ? c.labA : c.labB) = nl;
+    wsmax = std::max(wsmax, w);
+    size_t w2 = 0;
+    st = tk_contract_workspace(items[c.a].t, c.labA.data(), items[c.b].t, c.labB.data(), items[n + (int)j].t,
+                               c.labC.data(), &w2);
+    if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    wsmax = std::max(wsmax, w2);
+  }
   *bytes = off + wsmax;
+  if (plan_debug())
+    for (const Step& st : steps) {
+      fprintf(stderr, "[tk ncon] step %d x %d ->", st.a, st.b);
+      for (int32_t l : st.labC) fprintf(stderr, " %d", l);
+      fprintf(stderr, " (ncod %d)\n", st.ncod);
+    }
   if (out) {
     *out = const_cast<tk_tensor*>(items.back().t);
     items.back().owned = false;  // ownership moves to the caller
@@ -246,6 +326,7 @@ tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data,
       inter = std::max(inter, align256(it.off + (size_t)t.nelems * (t.dtype == TK_C64 ? 16 : 8)));
     }
   char* w = (char*)ws;
+  int launches = 0;
   for (size_t k = 0; k < steps.size(); ++k) {
     const Step& s = steps[k];
     Item& ia = items[s.a];
@@ -256,18 +337,46 @@ tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data,
                               s.q.data(), (int32_t)s.q.size(), ic.t, w + ic.off, 1.0, 0.0, w + inter, ws_bytes - inter,
                               stream);
       if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+      launches += tk_last_launch_count();
       continue;
     }
     Item& ib = items[s.b];
     const void* a = ia.data ? ia.data : (const void*)(w + ia.off);
     const void* b = ib.data ? ib.data : (const void*)(w + ib.off);
     Item& ic = items[n + k];
+    static const bool use_pair = knob("TK_NCON_FUSE", 1) != 0;
+    if (use_pair && !s.last && k + 1 < steps.size() && steps[k + 1].a == n + (int)k && steps[k + 1].b >= 0) {
+      // the pair (this step, the next) through tk_contract2: one kernel when it fuses
+      const Step& s2 = steps[k + 1];
+      Item& i2 = items[s2.b];
+      Item& io = items[n + k + 1];
+      const tk_tensor* C2 = s2.last ? C : io.t;
+      size_t w2 = 0;
+      int32_t fused = 0;
+      tk_status st = tk_contract2_workspace(ia.t, s.labA.data(), ib.t, s.labB.data(), ic.t, s.labC.data(), i2.t,
+                                            s2.labB.data(), C2, s2.labC.data(), &w2, &fused);
+      if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+      if (fused && w2 <= ws_bytes - inter) {
+        const void* b2 = i2.data ? i2.data : (const void*)(w + i2.off);
+        void* c2 = s2.last ? c : (void*)(w + io.off);
+        st = tk_contract2(ia.t, a, s.labA.data(), ib.t, b, s.labB.data(), ic.t, s.labC.data(), i2.t, b2,
+                          s2.labB.data(), C2, c2, s2.labC.data(), s2.last ? alpha : 1.0, s2.last ? beta : 0.0,
+                          w + inter, ws_bytes - inter, stream);
+        if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+        launches += tk_last_launch_count();
+        ++k;
+        continue;
+      }
+    }
     void* cc = s.last ? c : (void*)(w + ic.off);
     const tk_tensor* Ct = s.last ? C : ic.t;
     tk_status st = tk_contract(ia.t, a, s.labA.data(), 0, ib.t, b, s.labB.data(), 0, Ct, cc, s.labC.data(),
                                s.last ? alpha : 1.0, s.last ? beta : 0.0, w + inter, ws_bytes - inter, stream);
     if (st != TK_OK) TK_THROW(st, std::string("tk_ncon: ") + tk_last_error());
+    launches += tk_last_launch_count();
   }
+  reset_launches();  // tk_last_launch_count: the whole network
+  add_launches(launches);
   TK_API_END
 }
 

@@ -832,6 +832,7 @@ static void build_gather(const Tensor& A, ContractPlan& P) {
         ++last;
       }
       GatherTile t{};
+      t.gout0 = -1;
       t.g = gg;
       t.m0 = m0;
       t.nrows = end - m0;
@@ -923,6 +924,121 @@ static void build_gather(const Tensor& A, ContractPlan& P) {
   if (plan_debug())
     fprintf(stderr, "[tk gather] %zu tiles, %zu subblocks, K <= %d, N <= %d\n", P.gtiles.size(), P.gsegs.size(), kmax,
             nmax);
+}
+
+OutMap::OutMap(const PermPlan& pc, const PadLayout& lc) : pc_(pc), lc_(lc) {
+  for (int gi = 0; gi < (int)pc.groups.size(); ++gi) {
+    const PermGroup& g = pc.groups[gi];
+    const double cf = g.ksrc == 1 && g.kdst == 1 ? pc.coefs[g.coef_off] : 0.0;
+    if (cf != 1.0 && cf != -1.0) {  // recoupling (non-abelian) or a non-sign coefficient
+      ok_ = false;
+      return;
+    }
+    const PermMember ms = pc.members[g.src_mem];
+    const int b = (int)(std::upper_bound(lc.off.begin(), lc.off.end(), ms.off) - lc.off.begin()) - 1;
+    if (b < 0) {
+      ok_ = false;
+      return;
+    }
+    const int64_t rel = ms.off - lc.off[b];
+    int64_t nr = 1, nc = 1;
+    for (int l = 0; l < g.ndim; ++l) (g.sb[l] == 0 ? nr : nc) *= g.ext[l];
+    boxes_[lc.off[b]].push_back(Box{(int32_t)(rel % lc.ld[b]), (int32_t)nr, (int32_t)(rel / lc.ld[b]), (int32_t)nc, gi});
+  }
+}
+
+bool OutMap::map(int64_t src, int F, GatherOut& o) const {
+  if (!ok_) return false;
+  const int b = (int)(std::upper_bound(lc_.off.begin(), lc_.off.end(), src) - lc_.off.begin()) - 1;
+  if (b < 0) return false;
+  auto it = boxes_.find(lc_.off[b]);
+  if (it == boxes_.end()) return false;
+  const int64_t rel = src - lc_.off[b];
+  const int32_t r = (int32_t)(rel % lc_.ld[b]), c = (int32_t)(rel / lc_.ld[b]);
+  const Box* x = nullptr;
+  for (const Box& q : it->second)
+    if (q.r0 == r && c >= q.c0 && c < q.c0 + q.nc) x = &q;
+  if (!x || x->nr != F) return false;
+  const PermGroup& g = pc_.groups[x->g];
+  const PermMember md = pc_.members[g.dst_mem];
+  // row legs (sb = 0, extent > 1) by ascending source row stride: the radix of the row index
+  std::vector<int> rl, cl;
+  for (int l = 0; l < g.ndim; ++l)
+    if (g.ext[l] > 1) (g.sb[l] == 0 ? rl : cl).push_back(l);
+  std::sort(rl.begin(), rl.end(), [&](int u, int v) { return g.sa[u] < g.sa[v]; });
+  std::sort(cl.begin(), cl.end(), [&](int u, int v) { return g.sb[u] < g.sb[v]; });
+  if (rl.size() > 3) return false;
+  int64_t run = 1;
+  for (int l : rl) {
+    if (g.sa[l] != run) return false;
+    run *= g.ext[l];
+  }
+  o = GatherOut{};
+  o.ext0 = rl.size() > 0 ? g.ext[rl[0]] : 1;
+  o.ext1 = rl.size() > 1 ? g.ext[rl[1]] : 1;
+  for (size_t j = 0; j < rl.size(); ++j) {
+    const int64_t st = g.da[rl[j]] + md.ld * g.db[rl[j]];
+    if (st > INT32_MAX) return false;
+    o.str[j] = (int32_t)st;
+  }
+  int64_t crun = 1;  // the column's digits over the column legs (ascending source column stride)
+  for (int l : cl) {
+    if (g.sb[l] != crun) return false;
+    crun *= g.ext[l];
+  }
+  int64_t cc = c - x->c0;
+  o.base = md.off;
+  for (int l : cl) {
+    o.base += (cc % g.ext[l]) * (g.da[l] + md.ld * g.db[l]);
+    cc /= g.ext[l];
+  }
+  o.neg = pc_.coefs[g.coef_off] < 0;
+  return true;
+}
+
+// The output permute of a gathered plan folded into the gathered GEMM's stores (GatherTile::gout0): a
+// per-(row tree, column) map from the C~ row's digits to C. All-or-nothing per plan.
+static void fold_gather_output(ContractPlan& P) {
+  static const bool off = knob("TK_NO_GATHER_OUT", 0) != 0;
+  if (off || !P.gather || P.pc.identity || P.cplx) return;
+  if (!P.tiles.empty()) {
+    if (plan_debug()) fprintf(stderr, "[tk gather] output permute not folded: other GEMM tiles\n");
+    return;
+  }
+  OutMap om(P.pc, P.lc);
+  if (!om.ok()) {
+    if (plan_debug()) fprintf(stderr, "[tk gather] output permute not folded: not a signed map\n");
+    return;
+  }
+  std::vector<GatherOut> gouts;
+  std::vector<int32_t> g0(P.gtiles.size());
+  for (size_t ti = 0; ti < P.gtiles.size(); ++ti) {
+    const GatherTile& t = P.gtiles[ti];
+    g0[ti] = (int32_t)gouts.size();
+    gouts.resize(gouts.size() + (size_t)t.nseg * t.g.N);
+    for (int s = 0; s < t.nseg; ++s) {
+      const GatherSeg& q = P.gsegs[t.seg0 + s];
+      if (s > 0 && P.gsegs[t.seg0 + s - 1].r0 == q.r0) continue;  // not the first segment of its row tree
+      for (int n = 0; n < t.g.N; ++n) {
+        GatherOut& o = gouts[g0[ti] + (size_t)s * t.g.N + n];
+        if (!om.map(t.g.c_off + q.r0 + (int64_t)n * t.g.ldc, q.nrows, o) ||
+            (n > 0 && (o.ext0 != gouts[g0[ti] + (size_t)s * t.g.N].ext0 ||
+                       o.ext1 != gouts[g0[ti] + (size_t)s * t.g.N].ext1))) {
+          if (plan_debug())
+            fprintf(stderr, "[tk gather] output permute not folded: tile %zu seg %d col %d (r0 %d, %d rows, nrl %d)\n",
+                    ti, s, n, q.r0, q.nrows, q.nrl);
+          return;
+        }
+      }
+    }
+  }
+  for (size_t ti = 0; ti < P.gtiles.size(); ++ti) {
+    P.gtiles[ti].gout0 = g0[ti];
+    std::memcpy(P.gslots.data() + ti * kGatherSlotWords, &P.gtiles[ti], sizeof(GatherTile));
+  }
+  P.gouts = std::move(gouts);
+  P.gout = true;
+  if (plan_debug()) fprintf(stderr, "[tk gather] output permute folded in (%zu maps)\n", P.gouts.size());
 }
 
 static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& C, const Tuples& t, ContractPlan& P) {
@@ -1125,6 +1241,7 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
   for (GemmTile& t : P.tiles) t.g = P.ggroups[t.group];
   for (GemmTile& t : P.split_heads) t.g = P.ggroups[t.group];
   build_gather(A, P);
+  fold_gather_output(P);
 }
 
 // ------------------------------------------------------------------ device memory of plans
@@ -1441,15 +1558,17 @@ void run_contract(ContractPlan* P, const void* a, const void* b, void* c, int32_
     g_launches += (nbig > 0) + (P->ntiles_small > 0) + (P->ntiles_skinny > 0 && P->ntiles_small == 0) +
                   !P->split_heads.empty();
   }
-  if (P->gather) {
-    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, Ct, (const int64_t*)P->d_gslots.p,
-                                  (int)P->gtiles.size(), (const GatherSeg*)P->d_gsegs.p, (const int32_t*)P->d_btab.p,
-                                  P->g_kmax, P->g_nmax, ga, gb, st),
+  if (P->gather) {  // with the output permute folded in, the stores go to C itself (alpha, sign, beta there)
+    check_cuda(launch_gather_gemm((const double*)a, (const double*)b, P->gout ? (double*)c : Ct,
+                                  (const int64_t*)P->d_gslots.p, (int)P->gtiles.size(), (const GatherSeg*)P->d_gsegs.p,
+                                  (const int32_t*)P->d_btab.p, (const GatherOut*)P->d_gouts.p, P->g_kmax, P->g_nmax,
+                                  ga, alpha, P->gout ? beta : gb, st),
                "gather gemm launch");
     g_launches += !P->gtiles.empty();
   }
   prof_record(3, st);
-  if (!P->pc.identity) run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
+  if (!P->pc.identity && !P->gout)
+    run_permute(P->pc, Ct, c, alpha, beta, cx ? kPermPlanarToC : kPermReal, 1.0, st);
   prof_record(4, st);
   if (g_prof.on) {
     g_prof.have = true;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <list>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -161,6 +162,26 @@ void reset_launches();
 void svd_cache_clear();
 void fused_cache_clear();
 
+// Abelian output permute as an element map (tk_plan.cpp): a C~ row tree of F rows starting at padded
+// offset src (column n folded into src) lands in one C subblock with sign +-1; map() fills the GatherOut
+// (its own radix: the permute's row legs of extent > 1, at most 3), or returns false.
+class OutMap {
+ public:
+  OutMap(const PermPlan& pc, const PadLayout& lc);
+  bool ok() const { return ok_; }
+  bool map(int64_t src, int F, GatherOut& o) const;
+
+ private:
+  struct Box {
+    int32_t r0, nr, c0, nc;
+    int g;
+  };
+  const PermPlan& pc_;
+  const PadLayout& lc_;
+  std::map<int64_t, std::vector<Box>> boxes_;
+  bool ok_ = true;
+};
+
 // ------------------------------------------------------------------ contraction plan (tk_plan.cpp)
 struct ContractPlan {
   Tensor* At = nullptr;  // A~ (canonical layout, reading C2 tuples)
@@ -190,6 +211,9 @@ struct ContractPlan {
   std::vector<int64_t> gslots;
   int g_kmax = 0, g_nmax = 0;
   DevBuf d_gsegs, d_btab, d_gslots;
+  bool gout = false;  // the output permute folded into the gathered GEMM's stores (GatherOut)
+  std::vector<GatherOut> gouts;
+  DevBuf d_gouts;
   size_t off_a = 0, off_b = 0, off_c = 0, off_counter = 0, ws_bytes = 0;
   double flops = 0;
   // persistent TMA GEMM for the big tiles (tk_gemm_tma.cu): groups with a tensor-map pair, and the
@@ -222,6 +246,7 @@ struct ContractPlan {
     d_gsegs.upload(gsegs);
     d_btab.upload(btab);
     d_gslots.upload(gslots);
+    d_gouts.upload(gouts);
     uploaded = true;
   }
 };

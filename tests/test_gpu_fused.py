@@ -147,3 +147,111 @@ def test_fused_bitwise_equals_pair(cfgfun, alpha, beta):
     assert tk.tk_last_launch_count() == 1
     torch.cuda.synchronize()
     assert torch.equal(got, ref), f"max |diff| {float((got - ref).abs().max()):.3e}"
+
+
+def _ncon_chain(cfg, alpha=1.0, beta=0.0, c0=None):
+    from paper_2508_10076_b200 import tk, layout_io
+    dev = torch.device("cuda")
+    T = {}
+    for name, (spec, idx) in cfg["tensors"].items():
+        t = tk.tensor_from_spec(spec)
+        T[name] = (t, torch.from_numpy(layout_io.fill(t, cfg["cfg"], idx)).to(dev))
+    names, labels, order, ncod, _ = W.chain_as_ncon(cfg)
+    tens = [T[n][0] for n in names]
+    C = tk.tk_ncon_output(tens, labels, order, ncod)
+    c = torch.full((C.nelems,), float("nan"), dtype=torch.float64, device=dev) if c0 is None else c0.clone()
+    n = tk.tk_ncon_workspace(tens, labels, order, ncod)
+    ws = torch.empty(n // 8 + 32, dtype=torch.float64, device=dev)
+    tk.tk_ncon(tens, [T[x][1] for x in names], labels, order, ncod, C, c, alpha=alpha, beta=beta, ws=ws,
+               ws_bytes=ws.numel() * 8)
+    torch.cuda.synchronize()
+    return C, c
+
+
+@pytest.mark.parametrize("cfgfun", [W.cfg2, lambda: W.cfg3(chi=96), W.cfg6, lambda: W.cfg7(n_mult=24),
+                                    lambda: W.cfg8(n_mult=12)],
+                         ids=["cfg2", "cfg3_chi96", "cfg6", "cfg7_m24", "cfg8_m12"])
+def test_chain_through_ncon_dense_oracle(cfgfun):
+    """The chain as one tk_ncon network (library-chosen intermediate orders, fused MPO pair where it
+    applies) against the dense oracle of the chain's output."""
+    cfg = cfgfun()
+    C, c = _ncon_chain(cfg)
+    out_name = cfg["steps"][-1][4]
+    lt, D = H.oracle_chain_dense(cfg)[out_name]
+    flat = c.cpu().numpy()
+    assert C.nelems == lt.nelems
+    assert not np.isnan(flat).any()
+    assert _dense_err(lt, flat, D) <= TOL
+
+
+@pytest.mark.parametrize("cfgfun", [W.cfg2, W.cfg3, W.cfg7, W.cfg8], ids=["cfg2", "cfg3", "cfg7", "cfg8"])
+def test_chain_through_ncon_equals_pairwise(cfgfun):
+    """The timed sizes: the ncon network (left fold = the chain's operand order) equals the config's
+    explicit tk_contract chain -- the same A~, B~ per step; only the storage order of intermediates (so the
+    GEMM's operand strides and tiling) may differ, hence a rounding-level tolerance, not bitwise."""
+    cfg = cfgfun()
+    got = H.gpu_chain(cfg)  # explicit steps, intermediates in the config's orders
+    out_name = cfg["steps"][-1][4]
+    C, ref = got[out_name]
+    _, c = _ncon_chain(cfg)
+    c = c.cpu().numpy()
+    assert not np.isnan(c).any()
+    err = np.linalg.norm(c - ref) / np.linalg.norm(ref)
+    assert err <= 1e-13, f"rel {err:.3e}"
+
+
+@pytest.mark.parametrize("cfgfun", [W.cfg2, lambda: W.cfg3(chi=96), lambda: W.cfg3(chi=24)],
+                         ids=["cfg2", "cfg3_chi96", "cfg3_chi24"])
+@pytest.mark.parametrize("fuse", [False, True], ids=["gather", "fused"])
+def test_output_permute_folded(cfgfun, fuse):
+    """The MPO step T2.W2 written straight into R's operand order (T3 = (al', s1', s2' | c, be)): the
+    gathered GEMM (and the fused pair) fold the output permute into their stores, fermionic signs
+    included; alpha / beta through the folded map. Against the dense oracle."""
+    from paper_2508_10076_b200 import tk, layout_io
+    cfg = cfgfun()
+    st = list(cfg["steps"])
+    na, la, nb, lb, nc, lc, ncod = st[2]
+    al_, be, s1p, s2p, c_ = lc
+    st[2] = (na, la, nb, lb, nc, [al_, s1p, s2p, c_, be], 3)
+    cfg = dict(cfg, steps=st[:3])
+    ref = H.oracle_chain_dense(cfg)
+    lt, D = ref[nc]
+    dev = torch.device("cuda")
+    T = {}
+    for name, (spec, idx) in cfg["tensors"].items():
+        t = tk.tensor_from_spec(spec)
+        T[name] = (t, torch.from_numpy(layout_io.fill(t, cfg["cfg"], idx)).to(dev))
+    desc = {}
+    for (a, la_, b, lb_, c, lc_, nc_) in st[:3]:
+        desc[c] = tk.tk_contract_output(desc.get(a, T[a][0] if a in T else None), la_, T[b][0], lb_, lc_, nc_)
+    rng = np.random.default_rng(5)
+    c0 = rng.standard_normal(desc[nc].nelems)
+    alpha, beta = -0.75, 0.5
+    if fuse:
+        a1, l1, b1, lb1, t1, lt1, _ = st[0]
+        T[t1] = (desc[t1], torch.zeros(desc[t1].nelems, dtype=torch.float64, device=dev))
+        n = tk.tk_contract_workspace(T[a1][0], l1, T[b1][0], lb1, desc[t1], lt1)
+        ws = torch.empty(n // 8 + 32, dtype=torch.float64, device=dev)
+        tk.tk_contract(T[a1][0], T[a1][1], l1, T[b1][0], T[b1][1], lb1, desc[t1], T[t1][1], lt1, ws=ws,
+                       ws_bytes=ws.numel() * 8)
+        (pa, pla, pb, plb, pt, plt, _), (_, qla, qb, qlb, qc, qlc, _) = st[1], st[2]
+        n, fu = tk.tk_contract2_workspace(desc[pa], pla, T[pb][0], plb, desc[pt], plt, T[qb][0], qlb, desc[qc], qlc,
+                                          want_fused=True)
+        assert fu
+        c = torch.from_numpy(c0).to(dev)
+        tk.tk_contract2(desc[pa], T[pa][1], pla, T[pb][0], T[pb][1], plb, desc[pt], plt, T[qb][0], T[qb][1], qlb,
+                        desc[qc], c, qlc, alpha=alpha, beta=beta)
+    else:
+        for i, (a, la_, b, lb_, cc, lc_, nc_) in enumerate(st[:3]):
+            last = i == 2
+            out = torch.from_numpy(c0).to(dev) if last else torch.zeros(desc[cc].nelems, dtype=torch.float64,
+                                                                         device=dev)
+            n = tk.tk_contract_workspace(T[a][0], la_, T[b][0], lb_, desc[cc], lc_)
+            ws = torch.empty(n // 8 + 32, dtype=torch.float64, device=dev)
+            tk.tk_contract(T[a][0], T[a][1], la_, T[b][0], T[b][1], lb_, desc[cc], out, lc_,
+                           alpha=alpha if last else 1.0, beta=beta if last else 0.0, ws=ws, ws_bytes=ws.numel() * 8)
+            T[cc] = (desc[cc], out)
+        c = T[nc][1]
+    torch.cuda.synchronize()
+    want = alpha * D + beta * OD.to_dense(lt, c0)
+    assert OC.rel_frobenius(OD.to_dense(lt, c.cpu().numpy()), want) <= TOL

@@ -1,9 +1,11 @@
 """tk_ncon (network contraction) against the oracle -- needs a B200.
 
 The oracle side replays the network pair by pair exactly as include/tk.h specifies (each step
-contracts the two tensors holding the next label of `order` over all labels they share; intermediates
-ordered (open A ; open B), the last step into -1, -2, ...), with the dense oracle contraction for every
-step; for bosonic kinds it is also checked against one einsum over the whole network.
+contracts the two tensors holding the next label of `order` over all labels they share -- a left fold:
+the running intermediate is the left operand A, two inputs in list order; the last step into -1, -2,
+...), with the dense oracle contraction for every step; for bosonic kinds it is also checked against one
+einsum over the whole network. (The library may store intermediates in any leg order: that changes no
+value, so the replay keeps them (open A ; open B).)
 """
 import numpy as np
 import pytest
@@ -55,10 +57,14 @@ def oracle_ncon(kind, specs, denses, labels, order, n_cod_out):
         items.append((cod, dom, D, lc))
         alive.append(True)
 
+    n_in = len(items)
     for x in order:
         hold = [i for i, it in enumerate(items) if alive[i] and x in it[3]]
         if hold:
-            pair(hold[0], hold[1])
+            a, b = hold[0], hold[1]
+            if b >= n_in and a < n_in:  # left fold: the intermediate is A
+                a, b = b, a
+            pair(a, b)
     while sum(alive) > 1:
         al = [i for i in range(len(items)) if alive[i]]
         pair(al[0], al[1])

@@ -26,7 +26,7 @@ BUDGET = {  # demangled-name prefix -> (max registers, max stack bytes)
     "tk::gemm_skinny_kernel": (85, 0),
     "void tk::permute_kernel<0, false>": (64, 16),
     "void tk::gather_skinny_kernel<8, 8>": (85, 0),
-    "void tk::fused_pair_kernel<8, 1>": (80, 0),   # 6 CTAs of 128 per SM (cfg3's MPO pair)
+    "void tk::fused_pair_kernel<8>": (80, 0),
     "void tk::permute_recouple_kernel<0>": (85, 0),
 }
 

@@ -200,3 +200,24 @@ def cfg8(n_mult=270):
 
 
 CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6, 7: cfg7, 8: cfg8}
+
+
+def chain_as_ncon(cfg):
+    """The chain of a config as ONE ncon network (tk_ncon): (tensor names, labels per tensor, order,
+    n_cod_out, output name). Labels contracted along the chain stay positive; the final output's legs
+    become -1..-m in its label order; `order` lists each step's contracted labels, step by step, so the
+    network is contracted in the chain's own pairwise order. Pure relabelling, no arithmetic."""
+    steps = cfg["steps"]
+    inputs = list(cfg["tensors"])
+    lab = {}
+    for (na, la, nb, lb, nc, lc, ncod) in steps:
+        for name, l in ((na, la), (nb, lb)):
+            if name in cfg["tensors"]:
+                lab[name] = list(l)
+    na, la, nb, lb, out_name, lout, n_cod_out = steps[-1]
+    open_map = {x: -(i + 1) for i, x in enumerate(lout)}
+    labels = [[open_map.get(x, x) for x in lab[name]] for name in inputs]
+    order = []
+    for (na, la, nb, lb, nc, lc, ncod) in steps:
+        order += [x for x in la if x in lb and x not in order]
+    return inputs, labels, order, n_cod_out, out_name
