@@ -326,6 +326,64 @@ def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
     return out
 
 
+def time_svd(dev, stream, reps=7, oracle=True):
+    """The two-site truncated SVD that closes Alg. 12: theta (alpha, s1 ; s2, beta) of cfg2 and
+    cfg3 at full size, split as (alpha, s1) | (s2, beta). `us_svd` is tk_svd (permute into the workspace +
+    the blockwise Jacobi SVD), `us_extract` tk_svd_extract (U, S, Vh of the kept values), CUDA events on
+    the launching stream, median of `reps`; the global truncation (tk_svd_truncate, host) is timed by the
+    wall clock. The oracle (numpy LAPACK per block + its own permute, oracle/svd.py) runs on the host
+    cores beside it (rank 0 only, ~1 s)."""
+    import torch
+    from paper_2508_10076_b200 import tk, layout_io
+    from workloads import configs as W
+    out = {}
+    for name, cfg, md in (("cfg2", W.cfg2(), 512), ("cfg3", W.cfg3(), 2048)):
+        spec, idx = cfg["tensors"]["theta"]
+        A = tk.tensor_from_spec(spec)
+        a = torch.from_numpy(layout_io.fill(A, cfg["cfg"], idx)).to(dev)
+        p, q = [0, 1], [2, 3]
+        nb = tk.tk_svd_workspace(A, p, q)
+        ws = torch.empty(nb // 8 + 64, dtype=torch.float64, device=dev)
+        ts, tt, tx = [], [], []
+        for r in range(reps + 2):
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            tk.tk_svd(A, a, p, q, ws, ws.numel() * 8, stream=stream)
+            e1.record(stream)
+            h0 = time.perf_counter()
+            Wsp, U, S, Vh, err, nrm = tk.tk_svd_truncate(A, p, q, ws, md, 0.0, stream=stream)
+            h1 = time.perf_counter()
+            bufs = [torch.empty(T.nelems, dtype=torch.float64, device=dev) for T in (U, S, Vh)]
+            e2.record(stream)
+            tk.tk_svd_extract(A, p, q, ws, U, bufs[0], S, bufs[1], Vh, bufs[2], stream=stream)
+            e3.record(stream)
+            torch.cuda.synchronize(dev)
+            if r >= 2:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+                tt.append((h1 - h0) * 1e6)
+                tx.append(e2.elapsed_time(e3) * 1e3)
+        spec_ = tk.tk_svd_spectrum(A, p, q, ws, stream=stream)
+        d = {"blocks": len(spec_), "largest_block_k": max(len(x) for x in spec_), "elements": A.nelems, "max_dim": md,
+             "us_svd": round(float(np.median(ts)), 1), "us_truncate_host": round(float(np.median(tt)), 1),
+             "us_extract": round(float(np.median(tx)), 1), "trunc_err": err, "norm": nrm}
+        if oracle:
+            from oracle import svd as OS, layout as OL
+            from tests import harness as H
+            lt = OL.homspace_layout(cfg["kind"], spec["cod"], spec["dom"])
+            x = H.oracle_flat(lt, cfg["cfg"], idx)
+            t0 = time.perf_counter()
+            lp, xp, _ = OS.permuted(cfg["kind"], spec["cod"], spec["dom"], x, p, q)
+            svds = OS.block_svd(lp, xp)
+            OS.truncation(cfg["kind"], [(c, s_) for c, u, s_, vh in svds], md, 0.0)
+            d["oracle_s"] = round(time.perf_counter() - t0, 3)
+            d["oracle_cores"] = len(os.sched_getaffinity(0))
+            d["oracle_kind"] = "numpy LAPACK gesdd per block (oracle/svd.py), host cores"
+        out[name] = d
+        del ws, a
+    return out
+
+
 # --------------------------------------------------------------------------- GPU
 def run_gpu(args):
     import torch
@@ -476,6 +534,9 @@ def run_gpu(args):
     chains = None
     if not args.no_chains and not cplx:
         chains = time_chains(dev, stream, peak_tf * 1e12, hbm * 1e9)
+    svd = None
+    if not args.no_svd and not cplx:
+        svd = time_svd(dev, stream, oracle=(rank == 0 and world == 1 and not args.no_cpu_baseline))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not cplx:
@@ -512,6 +573,7 @@ def run_gpu(args):
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (torch copy, driver-written)",
                              "algorithmic_bytes": perm_bytes, "phases": perm},
         "chains": chains,
+        "svd": svd,
         "phase_ms": {"permute_A": round(float(ph[0]), 3), "permute_B": round(float(ph[1]), 3),
                      "gemm": round(float(ph[2]), 3), "permute_C": round(float(ph[3]), 3)},
         "planner_ms": {"cold": round(t_plan_cold * 1e3, 2), "cached": round(t_plan_cached * 1e3, 4)},
@@ -543,6 +605,7 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-chains", action="store_true", help="skip the cfg2/3/5/6/7/8 chain timings")
+    ap.add_argument("--no-svd", action="store_true", help="skip the two-site SVD timings (cfg2/cfg3 theta)")
     args = ap.parse_args()
     if args.e2e_steps is None:
         args.e2e_steps = args.steps

@@ -57,6 +57,8 @@ struct SvdBlock {
   int32_t cs;       // CTAs per cluster
   int32_t smem;     // 1: the CTA's rows of G and V live in shared memory; 0: in the workspace
   int32_t Rl, Kl;   // rows of G / of V per CTA
+  int32_t tile;     // 1: svd_jacobi_tile_kernel (RG rows of G per lane and column), 0: svd_jacobi_kernel
+  int32_t rg;
 };
 
 struct SvdOut {     // extraction target of one block (canonical layouts of U, S, Vh)
@@ -184,6 +186,22 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "@!p bra TK_CW_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// mbarrier wait (CTA scope) that turns a lost arrival into a kernel error instead of a hung GPU: after
+// ~2^34 cycles (~9 s) of waiting it traps. A Jacobi round waits a few microseconds at most.
+__device__ __forceinline__ void mbar_wait_guarded(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (1LL << 34)) __trap();
+  }
 }
 
 // pair pr of round r of the circle method over n players (player K, if K is odd, sits out); the two
@@ -461,6 +479,631 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
   if (CS > 1) cluster_sync_all();  // no CTA may exit while others still read its shared memory
 }
 
+// st.async of one double (the real gamma partial)
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(raddr), "d"(a),
+               "r"(rbar)
+               : "memory");
+}
+
+// Jacobi for the blocks of a DMRG bond (K <= 256 columns; round 2b). The kernel above is bound by
+// shared-memory traffic: per round it reads G twice and reads + writes G and V once more, and its
+// column-major slices put the four pairs of a warp on conflicting banks. Here one group of 8 lanes owns
+// one pair for the whole round: it loads the pair's rows of G ONCE into registers (RG rows per lane
+// per column), reduces (alpha, beta, gamma) over its lanes with three shuffle levels, sends the
+// partial to the other CTAs of the cluster (st.async, 24 B real / 32 B complex per pair and peer),
+// waits on its own mbarrier, adds the CS partials in rank order (bitwise identical in every CTA: same
+// rotations, same convergence decision), rotates the registers and stores them, then streams the
+// pair's rows of V (load, rotate, store). Per round the slices are read and written once: the floor is
+// 2 (rows of G + rows of V) K 8 B / 128 B per cycle per SM, so the planner picks CS per block to
+// balance that against the exchange (DSMEM ~20 B per cycle per SM) and the cluster-wide latency.
+// Shared memory holds the slices in 8-row tiles ([row / 8][column][row % 8]): a group's 8 lanes read
+// 64 contiguous bytes of a column, and the two groups of a half-warp (consecutive pairs) sit on
+// different 64-byte halves of the banks.
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ int named_bar_or(int id, int nthreads, int pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}\n"
+      : "=r"(r)
+      : "r"(pred), "r"(id), "r"(nthreads)
+      : "memory");
+  return r;
+}
+// tan of the Jacobi angle, t = sign(z) / (|z| + sqrt(1 + z^2)) with z = (beta - alpha) / (2 |gamma|), to
+// single precision: the rotation stays orthogonal to working precision because c = rsqrt(1 + t^2) and
+// s = c t are formed in double from this t; an angle off by ~1e-7 only leaves a residual ~1e-7 gamma
+// that the next sweep removes. alpha, beta, |gamma| are scaled by a power of two (exponent of |gamma|)
+// so that the float arithmetic neither overflows nor underflows; |z| > 2^59 takes t = 1 / (2 z) in double.
+__device__ __forceinline__ double jacobi_tan(double al, double be, double ag) {
+  const double d = be - al;
+  if (fabs(d) > 1.152921504606847e18 * ag) return ag / d;          // |z| > 2^59: t = 1 / (2 z)
+  const long long eb = (__double_as_longlong(ag) >> 52) & 0x7ff;  // biased exponent of |gamma|
+  const double sc = __longlong_as_double((2046LL - eb) << 52);      // 2^(1023 - e): ag * sc in [1, 2)
+  const double num = d * (0.5 * sc), den = ag * sc;
+  const float z = __double2float_rn(num) / __double2float_rn(den);
+  const float tf = copysignf(1.0f, z) / (fabsf(z) + sqrtf(fmaf(z, z, 1.0f)));
+  return (double)tf;
+}
+// (c, s) of the Jacobi rotation from the single-precision tangent, made orthogonal to working precision in
+// double: with d = c^2 + s^2 - 1 (|d| ~ 1e-7), scaling both by 1 - d/2 + 3d^2/8 leaves c^2 + s^2 = 1 + O(d^3).
+// The angle is accurate to ~1e-7, which only leaves a residual the next sweep removes (the first sweeps).
+__device__ __forceinline__ void jacobi_cs_fast(double al, double be, double ag, double& c, double& s) {
+  const double t = jacobi_tan(al, be, ag);
+  const float tf = (float)t;
+  const float cf = rsqrtf(fmaf(tf, tf, 1.0f));
+  const double cd = (double)cf, sd = cd * t;
+  const double d = fma(cd, cd, fma(sd, sd, -1.0));
+  const double sc = fma(d, fma(0.375, d, -0.5), 1.0);
+  c = cd * sc;
+  s = sd * sc;
+}
+constexpr int kTileL = 8;                            // lanes per pair
+constexpr int kTileThreads = 768;                    // 85 registers per thread: no spills up to RG 8
+constexpr int kTileMaxPairs = kTileThreads / kTileL;  // 96: K <= 192
+constexpr int kTileExactSweep = 5;                   // sweeps before this one use the single-precision tangent
+
+// DSMEM bulk copy (cp.async.bulk shared::cta -> shared::cluster), completion counted in bytes on the
+// receiving CTA's mbarrier
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Shared memory of the tile kernel: G in RG 8-row tiles and V in TV tiles, each tile [K + 1][8] (column
+// K is all zeros: the partner of the player sitting out when K is odd and of groups without a pair);
+// the partial sums [2][CS][npairs][4]; two mbarriers.
+__host__ __device__ inline int64_t tile_smem_bytes(int K, int rg, int tv, int cs, int es) {
+  const int64_t npairs = (K + 1) / 2;
+  return (int64_t)(rg + tv) * 8 * (K + 1) * es + 2 * cs * npairs * 32 + 16;
+}
+
+// Jacobi for the blocks of a DMRG bond (K <= 192 columns; round 2). One group of 8 lanes owns one column
+// pair for the whole round: it loads the pair's rows of G once into registers (RG rows per lane and
+// column), reduces (alpha, beta, gamma) over its lanes with three shuffle levels, and -- in a cluster --
+// the CTA's partials go to the other CTAs as ONE bulk copy per peer (cp.async.bulk into the peer's slot
+// [rank], completion on its mbarrier; st.async per pair costs ~1.6 cycles per message). Every CTA adds the
+// CS partials in rank order (bitwise identical everywhere: same rotations, same convergence decision),
+// rotates the registers, stores them, and streams the pair's rows of V. Only the warps that own pairs run
+// the rounds (named barrier 1). Shared memory holds the slices in 8-row tiles ([row / 8][column][row % 8]):
+// a group's 8 lanes read 64 contiguous bytes of a column.
+template <int CS, typename T, int RG>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    svd_jacobi_tile_kernel(void* __restrict__ wsv, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
+                           const int32_t* __restrict__ list, int debug) {
+  using N = SvNum<T>;
+  constexpr int L = kTileL;
+  constexpr bool CPLX = sizeof(T) == 16;
+  extern __shared__ __align__(16) double svd_dyn[];
+  const SvdBlock b = blocks[list[blockIdx.x / CS]];
+  const uint32_t rank = CS > 1 ? cluster_rank() : 0;
+  const int tid = threadIdx.x, grp = tid / L, gl = tid % L;
+  const int R = b.R, K = b.K, Rl = b.Rl, Kl = b.Kl;
+  const int n = K + (K & 1), npairs = n / 2, KP = K + 1;
+  const int r0 = min(R, (int)rank * Rl), nr = min(R, r0 + Rl) - r0;
+  const int v0 = min(K, (int)rank * Kl), nv = min(K, v0 + Kl) - v0;
+  const int tv = (Kl + 7) >> 3;               // 8-row tiles of V (G has RG tiles)
+  const int TS = KP * 8;                      // tile stride (elements)
+  T* G = reinterpret_cast<T*>(svd_dyn);       // [RG][K + 1][8]
+  T* V = G + (size_t)RG * TS;                 // [tv][K + 1][8]
+  double* part = reinterpret_cast<double*>(V + (size_t)tv * TS);  // [2][CS][npairs][4]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(part + 2 * CS * npairs * 4);
+  const T* A = reinterpret_cast<const T*>(wsv) + b.a_off;
+  if (CS > 1 && tid == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    fence_barrier_init();
+  }
+  pdl_wait();
+  // G: the CTA's rows of A~ (or A~^H), zero past the last row and in column K; V: rows of the identity
+  for (int64_t e = tid; e < (int64_t)RG * 8 * KP; e += kTileThreads) {
+    const int i = (int)(e % (RG * 8)), j = (int)(e / (RG * 8)), gi = r0 + i;
+    T x = N::zero();
+    if (i < nr && j < K) x = b.trans ? N::conj(A[j + (int64_t)gi * b.lda]) : A[gi + (int64_t)j * b.lda];
+    G[(i >> 3) * TS + j * 8 + (i & 7)] = x;
+  }
+  for (int64_t e = tid; e < (int64_t)tv * 8 * KP; e += kTileThreads) {
+    const int i = (int)(e % (tv * 8)), j = (int)(e / (tv * 8));
+    V[(i >> 3) * TS + j * 8 + (i & 7)] = (i < nv && v0 + i == j) ? N::one() : N::zero();
+  }
+  if (CS > 1) cluster_sync_all(); else __syncthreads();  // remote mbarriers initialised before any copy
+  const double tol = 2.3e-16 * sqrt((double)R);
+  const double tol2 = tol * tol;
+  uint32_t xph = 0;
+  int par = 0, sweep = 0;
+  const int pr = grp;
+#ifdef TK_SVD_TIMERS  // per-phase cycle counters (diagnostic builds: they cost registers)
+  long long tA = 0, tX = 0, tB = 0, tX0 = 0, tX1 = 0, t_start = clock64();
+#endif
+  // only the warps that own pairs run the rounds (named barrier 1 over them); the others wait at the
+  // block barrier after the loop
+  const int nact = min(kTileThreads, ((npairs * L + 31) / 32) * 32);
+  if (tid < nact) {
+    for (; sweep < kSvdMaxSweeps; ++sweep) {
+      const bool exact = sweep >= kTileExactSweep;
+      int any = 0;
+      for (int r = 0; r < n - 1; ++r) {
+#ifdef TK_SVD_TIMERS
+        const long long tq0 = clock64();
+#endif
+        double* pp = part + par * CS * npairs * 4;
+        int p = K, q = K;  // K: the zero column
+        if (pr < npairs) {
+          round_pair_fast(r, pr, n, K, p, q);
+          p = p < K ? p : K;
+          q = q < K ? q : K;
+        }
+        T* gp = G + p * 8 + gl;
+        T* gq = G + q * 8 + gl;
+        T xp[RG], xq[RG];
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+#pragma unroll
+        for (int t = 0; t < RG; ++t) {
+          xp[t] = gp[t * TS];
+          xq[t] = gq[t * TS];
+        }
+#pragma unroll
+        for (int t = 0; t < RG; ++t) {
+          al += N::abs2(xp[t]);
+          be += N::abs2(xq[t]);
+          N::dot(xp[t], xq[t], gr, gi);
+        }
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          gr += __shfl_xor_sync(0xffffffffu, gr, o);
+          if (CPLX) gi += __shfl_xor_sync(0xffffffffu, gi, o);
+        }
+#ifdef TK_SVD_TIMERS
+        const long long tq1 = clock64();
+#endif
+        if (CS > 1) {
+          // the CTA's partials into its own slot [rank]; one bulk copy of the slot to every peer
+          double* mine = pp + (size_t)rank * npairs * 4;
+          if (pr < npairs && gl == 0) {
+            *reinterpret_cast<double2*>(mine + pr * 4) = make_double2(al, be);
+            *reinterpret_cast<double2*>(mine + pr * 4 + 2) = make_double2(gr, gi);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, nact);
+#ifdef TK_SVD_TIMERS
+          const long long tx0 = clock64();
+#endif
+          // thread 0 expects the bytes; lane 0 of warp w copies the slot to peers rank + c, c = 1 + w (mod the
+          // active warps): one copy per warp, so the copies issue in parallel (lanes of one warp serialise)
+          {
+            const uint32_t bytes = (uint32_t)npairs * 32;
+            if (tid == 0) mbar_arrive_expect_tx(&xbar[par], (uint32_t)(CS - 1) * bytes);
+            if ((tid & 31) == 0) {
+              const int w = tid >> 5, nw = nact >> 5;
+              const uint32_t la = smem_u32(mine), lb = smem_u32(&xbar[par]);
+              for (int c = 1 + w; c < CS; c += nw) {
+                const uint32_t rk = (rank + c) % CS;
+                bulk_s2cluster(mapa_u32(la, rk), la, bytes, mapa_u32(lb, rk));
+              }
+            }
+          }
+#ifdef TK_SVD_TIMERS
+          const long long tx1 = clock64();
+          tX0 += tx0 - tq1;
+          tX1 += tx1 - tx0;
+#endif
+          mbar_wait_guarded(&xbar[par], (xph >> par) & 1u);  // CTA scope: the copies landed here
+          xph ^= 1u << par;
+          double a2 = 0.0, b2 = 0.0, g2 = 0.0, h2 = 0.0;
+          if (pr < npairs) {
+#pragma unroll
+            for (int c = 0; c < CS; ++c) {
+              const double* src = pp + ((size_t)c * npairs + pr) * 4;
+              const double2 v01 = *reinterpret_cast<const double2*>(src);
+              const double2 v23 = *reinterpret_cast<const double2*>(src + 2);
+              a2 += v01.x;
+              b2 += v01.y;
+              g2 += v23.x;
+              h2 += v23.y;
+            }
+          }
+          al = a2;
+          be = b2;
+          gr = g2;
+          gi = h2;
+        }
+#ifdef TK_SVD_TIMERS
+        const long long tq2 = clock64();
+#endif
+        const double ga2 = fma(gr, gr, gi * gi);
+        if (ga2 > tol2 * al * be && ga2 > 0.0) {
+          double ur, ui, ag;
+          if (CPLX) {  // the phase of gamma must be unit to working precision: double rsqrt
+            const double rga = rsqrt(ga2);
+            ur = gr * rga;
+            ui = gi * rga;
+            ag = ga2 * rga;
+          } else {
+            ur = gr < 0.0 ? -1.0 : 1.0;
+            ui = 0.0;
+            ag = fabs(gr);
+          }
+          double c, sn;
+          if (exact) {
+            const double zeta = 0.5 * (be - al) / ag;
+            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
+            sn = c * t;
+          } else {
+            jacobi_cs_fast(al, be, ag, c, sn);
+          }
+#pragma unroll
+          for (int t2 = 0; t2 < RG; ++t2) {
+            const T x = xp[t2], y = N::rephase(xq[t2], ur, ui);
+            gp[t2 * TS] = N::lin(c, x, -sn, y);
+            gq[t2 * TS] = N::lin(sn, x, c, y);
+          }
+          T* vp = V + p * 8 + gl;
+          T* vq = V + q * 8 + gl;
+#pragma unroll 2
+          for (int t2 = 0; t2 < tv; ++t2) {
+            const T x = vp[t2 * TS], y = N::rephase(vq[t2 * TS], ur, ui);
+            vp[t2 * TS] = N::lin(c, x, -sn, y);
+            vq[t2 * TS] = N::lin(sn, x, c, y);
+          }
+          any = 1;
+        }
+        par ^= 1;
+        named_bar_sync(1, nact);
+#ifdef TK_SVD_TIMERS
+        tA += tq1 - tq0;
+        tX += tq2 - tq1;
+        tB += clock64() - tq2;
+#endif
+      }
+      if (!named_bar_or(1, nact, any)) break;
+    }
+  }
+  __syncthreads();
+  if (debug && tid == 0 && rank == 0) {
+#ifdef TK_SVD_TIMERS
+    const long long nrd = (long long)(sweep + 1) * max(n - 1, 1);
+    printf("[tk svd tile] block %d: %d x %d, cluster %d, RG %d, %d sweeps, %lld cycles/round (A %lld X %lld [bar %lld issue %lld] B+S %lld)\n",
+           list[blockIdx.x / CS], R, K, CS, RG, sweep + 1, (clock64() - t_start) / nrd, tA / nrd, tX / nrd, tX0 / nrd,
+           tX1 / nrd, tB / nrd);
+#else
+    printf("[tk svd tile] block %d: %d x %d, cluster %d, RG %d, %d sweeps\n", list[blockIdx.x / CS], R, K, CS, RG,
+           sweep + 1);
+#endif
+  }
+  // column norms of the CTA's rows (no copy is in flight: every CTA left the loop after the same round)
+  double* nrm = part;  // >= K doubles
+  for (int j = tid >> 5; j < K; j += (kTileThreads / 32)) {
+    double x = 0.0;
+    for (int i = tid & 31; i < RG * 8; i += 32) x += N::abs2(G[(i >> 3) * TS + j * 8 + (i & 7)]);
+    x = warp_sum(x);
+    if ((tid & 31) == 0) nrm[j] = x;
+  }
+  if (CS > 1) cluster_sync_all(); else __syncthreads();
+  if (rank == 0) {
+    double* sig = part + 2 * CS * npairs * 4 - ((K + 1) & ~1);  // the top of the partial-sum region
+    for (int j = tid; j < K; j += kTileThreads) {
+      double x = 0.0;
+#pragma unroll
+      for (int c = 0; c < CS; ++c) x += (CS > 1 ? map_rank(nrm, (uint32_t)c) : nrm)[j];
+      sig[j] = sqrt(x);
+    }
+    __syncthreads();
+    double* sv = reinterpret_cast<double*>(wsv) + b.s_off;
+    int32_t* pv = idx + b.p_off;
+    for (int j = tid; j < K; j += kTileThreads) {
+      const double sj = sig[j];
+      int rk = 0;
+      for (int i = 0; i < K; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+      sv[rk] = sj;
+      pv[rk] = j;
+    }
+  }
+  // the CTA's rows of G and V back to the workspace (column-major, ld ldg / ldv)
+  T* Gw = reinterpret_cast<T*>(wsv) + b.g_off;
+  T* Vw = reinterpret_cast<T*>(wsv) + b.v_off;
+  for (int64_t e = tid; e < (int64_t)nr * K; e += kTileThreads) {
+    const int i = (int)(e % nr), j = (int)(e / nr);
+    Gw[r0 + i + (int64_t)j * b.ldg] = G[(i >> 3) * TS + j * 8 + (i & 7)];
+  }
+  for (int64_t e = tid; e < (int64_t)nv * K; e += kTileThreads) {
+    const int i = (int)(e % nv), j = (int)(e / nv);
+    Vw[v0 + i + (int64_t)j * b.ldv] = V[(i >> 3) * TS + j * 8 + (i & 7)];
+  }
+  if (CS > 1) cluster_sync_all();  // rank 0's reads of the other CTAs' norms are done before they exit
+}
+
+// ---------------------------------------------------------------- panel kernel (round 2)
+// One-sided Jacobi with the columns split over the cluster instead of the rows: the tile kernel above
+// pays a cluster-wide exchange of partial sums in EVERY round (measured ~1000-2700 cycles at 8 CTAs: the
+// slowest CTA's phase plus the DSMEM latency), which no amount of per-round tuning removed. Here a column
+// [G rows | V rows] lives entirely in one CTA, so a rotation needs no other CTA. The K columns form
+// P = 2 CS half-panels of m columns; CTA c holds two of them, T_c and B_c, and the half-panels meet in the
+// round-robin (circle) order with T_0 fixed:
+//   stage 0 (per sweep): all pairs among the CTA's own 2m columns (a circle tournament, 2m - 1 rounds);
+//   outer round o = 1 .. P-2: after a move, all m^2 pairs (T_c[i], B_c[(i + s) mod m]), s = 0 .. m-1;
+//   move: T_c -> T_{c+1} (1 <= c < CS-1), T_{CS-1} -> B_{CS-1}, B_0 -> T_1, B_c -> B_{c-1}: two DSMEM bulk
+//   copies per CTA (cp.async.bulk shared::cta -> shared::cluster), P - 1 moves per sweep (the last one
+//   restores the initial placement).
+// Per sweep that is (P m - 1) rounds, the same count as the scalar circle order, but only P - 1 of them
+// touch the cluster. Warp i owns T_c[i] in registers during an outer round; B columns stream through
+// shared memory (one load + one store per warp and round). A lane holds rows lane + 32 t of a column
+// (RPL per lane): G rows first (padded to a multiple of 32), then V rows.
+constexpr int kPanelThreadsReal = 768, kPanelThreadsCplx = 384;
+template <typename T>
+struct PanelCfg {
+  static constexpr int threads = sizeof(T) == 8 ? kPanelThreadsReal : kPanelThreadsCplx;
+};
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+// bytes of shared memory: T_in, T_out, B_cur, B_in ([m][Lc] each), 2m norms, CS flags, one mbarrier
+__host__ __device__ inline int64_t panel_smem_bytes(int m, int Lc, int cs, int es) {
+  return 4LL * m * Lc * es + 16LL * m + 8LL * cs + 64;
+}
+
+template <typename T, int RPL>
+__global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
+    svd_jacobi_panel_kernel(void* __restrict__ wsv, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
+                            const int32_t* __restrict__ list, int debug) {
+  using N = SvNum<T>;
+  constexpr bool CPLX = sizeof(T) == 16;
+  extern __shared__ __align__(16) double svd_dyn[];
+  const SvdBlock b = blocks[list[cluster_id_x()]];
+  const int CS = b.cs;
+  const uint32_t rank = CS > 1 ? cluster_rank() : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  const int R = b.R, K = b.K;
+  const int m = b.Kl;                     // columns per half-panel
+  const int P = 2 * CS;
+  const int Rp = (R + 31) & ~31, Kv = (K + 31) & ~31, Lc = Rp + Kv;
+  const int RGT = Rp >> 5;                // per-lane G rows
+  const int RT = Lc >> 5;                 // per-lane rows (<= RPL)
+  T* Tin = reinterpret_cast<T*>(svd_dyn);
+  T* Tout = Tin + (size_t)m * Lc;
+  T* Bcur = Tout + (size_t)m * Lc;
+  T* Bin = Bcur + (size_t)m * Lc;
+  double* nrm = reinterpret_cast<double*>(Bin + (size_t)m * Lc);  // 2m
+  int* flag = reinterpret_cast<int*>(nrm + 2 * m);                  // CS (flag[0] used)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(flag + CS) + 7) & ~uintptr_t(7));
+  const T* A = reinterpret_cast<const T*>(wsv) + b.a_off;
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    fence_barrier_init();
+  }
+  pdl_wait();
+  // initial placement: CTA c holds columns 2cm .. 2cm + 2m - 1 (T: the first m, B: the next m)
+  for (int64_t e = tid; e < (int64_t)2 * m * Lc; e += nthr) {
+    const int k = (int)(e / Lc), i = (int)(e % Lc);
+    const int j = (int)rank * 2 * m + k;
+    T x = N::zero();
+    if (j < K) {
+      if (i < R) x = b.trans ? N::conj(A[j + (int64_t)i * b.lda]) : A[i + (int64_t)j * b.lda];
+      else if (i >= Rp && i - Rp == j) x = N::one();
+    }
+    (k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc)[i] = x;
+  }
+  if (CS > 1) cluster_sync_all(); else __syncthreads();
+  const double tol = 2.3e-16 * sqrt((double)R);
+  const double tol2 = tol * tol;
+  uint32_t mph = 0;
+  int sweep = 0;
+  const bool act = warp < m;
+  T t[RPL], u[RPL];
+  for (; sweep < kSvdMaxSweeps; ++sweep) {
+    const bool exact = sweep >= kTileExactSweep;
+    int any = 0;
+    // rotate the pair (x, y) in registers; returns whether a rotation was applied
+    auto rotate = [&](T (&x)[RPL], T (&y)[RPL]) -> int {
+      double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r)
+        if (r < RGT) {
+          al += N::abs2(x[r]);
+          be += N::abs2(y[r]);
+          N::dot(x[r], y[r], gr, gi);
+        }
+      if (CPLX) {
+        warp_sum4(al, be, gr, gi);
+      } else {
+        double dd = 0.0;
+        warp_sum4(al, be, gr, dd);
+      }
+      const double ga2 = fma(gr, gr, gi * gi);
+      if (!(ga2 > tol2 * al * be && ga2 > 0.0)) return 0;
+      double ur, ui, ag;
+      if (CPLX) {
+        const double rga = rsqrt(ga2);
+        ur = gr * rga;
+        ui = gi * rga;
+        ag = ga2 * rga;
+      } else {
+        ur = gr < 0.0 ? -1.0 : 1.0;
+        ui = 0.0;
+        ag = fabs(gr);
+      }
+      double c, sn;
+      if (exact) {
+        const double zeta = 0.5 * (be - al) / ag;
+        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        c = rsqrt(fma(tt, tt, 1.0));
+        sn = c * tt;
+      } else {
+        jacobi_cs_fast(al, be, ag, c, sn);
+      }
+#pragma unroll
+      for (int r = 0; r < RPL; ++r)
+        if (r < RT) {
+          const T a0 = x[r], b0 = N::rephase(y[r], ur, ui);
+          x[r] = N::lin(c, a0, -sn, b0);
+          y[r] = N::lin(sn, a0, c, b0);
+        }
+      return 1;
+    };
+    // ---- stage 0: circle tournament over the CTA's 2m columns (players k < m: T_in[k], else B_cur[k - m])
+    {
+      const int n2 = 2 * m;
+      for (int r = 0; r < n2 - 1; ++r) {
+        if (act) {
+          int p, q;
+          round_pair_fast(r, warp, n2, n2, p, q);
+          T* cp = p < m ? Tin + (size_t)p * Lc : Bcur + (size_t)(p - m) * Lc;
+          T* cq = q < m ? Tin + (size_t)q * Lc : Bcur + (size_t)(q - m) * Lc;
+#pragma unroll
+          for (int rr = 0; rr < RPL; ++rr)
+            if (rr < RT) {
+              t[rr] = cp[lane + 32 * rr];
+              u[rr] = cq[lane + 32 * rr];
+            }
+          if (rotate(t, u)) {
+            any = 1;
+#pragma unroll
+            for (int rr = 0; rr < RPL; ++rr)
+              if (rr < RT) {
+                cp[lane + 32 * rr] = t[rr];
+                cq[lane + 32 * rr] = u[rr];
+              }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // ---- outer rounds: move, then all m^2 pairs (T_c[i], B_c[(i + s) mod m])
+    if (CS > 1) {
+      if (act) {
+#pragma unroll
+        for (int rr = 0; rr < RPL; ++rr)
+          if (rr < RT) t[rr] = Tin[(size_t)warp * Lc + lane + 32 * rr];
+      }
+      for (int o = 1; o < P; ++o) {
+        // move: T (registers) -> T_out; copies T_out and B_cur to their next places
+        if (act) {
+#pragma unroll
+          for (int rr = 0; rr < RPL; ++rr)
+            if (rr < RT) Tout[(size_t)warp * Lc + lane + 32 * rr] = t[rr];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        cluster_sync_all();  // every CTA is done with its landing buffers (T_in, B_in)
+        const uint32_t bytes = (uint32_t)((size_t)m * Lc * sizeof(T));
+        if (tid == 0) mbar_arrive_expect_tx(mbar, 2 * bytes);
+        if (tid == 0 || tid == 32) {  // two warps (blockDim >= 64): the copies issue in parallel
+          const bool isT = tid == 0;
+          uint32_t dst_rank;
+          bool dst_T;
+          const int c = (int)rank;
+          if (isT) {
+            if (c == 0) dst_rank = 0, dst_T = true;
+            else if (c == CS - 1) dst_rank = (uint32_t)c, dst_T = false;
+            else dst_rank = (uint32_t)(c + 1), dst_T = true;
+          } else {
+            if (c == 0) dst_rank = 1, dst_T = true;
+            else dst_rank = (uint32_t)(c - 1), dst_T = false;
+          }
+          const uint32_t src = smem_u32(isT ? Tout : Bcur);
+          const uint32_t dst = mapa_u32(smem_u32(dst_T ? Tin : Bin), dst_rank);
+          bulk_s2cluster(dst, src, bytes, mapa_u32(smem_u32(mbar), dst_rank));
+          bulk_commit_wait_read();
+        }
+        mbar_wait_guarded(mbar, mph & 1u);
+        mph ^= 1u;
+        {
+          T* x = Bcur;
+          Bcur = Bin;
+          Bin = x;
+        }
+        if (act) {
+#pragma unroll
+          for (int rr = 0; rr < RPL; ++rr)
+            if (rr < RT) t[rr] = Tin[(size_t)warp * Lc + lane + 32 * rr];
+        }
+        if (o == P - 1) break;  // the last move restores the initial placement
+        for (int s2 = 0; s2 < m; ++s2) {
+          if (act) {
+            T* cq = Bcur + (size_t)((warp + s2) % m) * Lc;
+#pragma unroll
+            for (int rr = 0; rr < RPL; ++rr)
+              if (rr < RT) u[rr] = cq[lane + 32 * rr];
+            if (rotate(t, u)) {
+              any = 1;
+#pragma unroll
+              for (int rr = 0; rr < RPL; ++rr)
+                if (rr < RT) cq[lane + 32 * rr] = u[rr];
+            }
+          }
+          __syncthreads();
+        }
+      }
+      // T back to T_in (the move above left T_in = the registers' columns, unchanged since)
+    }
+    // ---- convergence: OR over the cluster
+    const int cta_any = __syncthreads_or(any);
+    if (CS > 1) {
+      if (tid == 0) flag[0] = cta_any;
+      cluster_sync_all();
+      int all = 0;
+      for (int c = 0; c < CS; ++c) all |= *reinterpret_cast<const int*>(map_rank(reinterpret_cast<const double*>(flag), (uint32_t)c));
+      cluster_sync_all();  // flags read before anyone rewrites them
+      if (!all) break;
+    } else if (!cta_any) {
+      break;
+    }
+  }
+  if (debug && tid == 0 && rank == 0)
+    printf("[tk svd panel] block %d: %d x %d, cluster %d, m %d, RPL %d, %d sweeps\n", list[cluster_id_x()], R, K, CS, m,
+           RPL, sweep + 1);
+  // column norms of the CTA's 2m columns (G rows), ranked against every column of the block
+  for (int k = warp; k < 2 * m; k += nthr >> 5) {
+    const T* col = k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc;
+    double x = 0.0;
+    for (int i = lane; i < Rp; i += 32) x += N::abs2(col[i]);
+    x = warp_sum(x);
+    if (lane == 0) nrm[k] = sqrt(x);
+  }
+  if (CS > 1) cluster_sync_all(); else __syncthreads();
+  {
+    double* sv = reinterpret_cast<double*>(wsv) + b.s_off;
+    int32_t* pv = idx + b.p_off;
+    for (int k = tid; k < 2 * m; k += nthr) {
+      const int j = (int)rank * 2 * m + k;
+      if (j >= K) continue;
+      const double sj = nrm[k];
+      int rk = 0;
+      for (int i = 0; i < K; ++i) {
+        const int c = i / (2 * m), kk = i % (2 * m);
+        const double si = CS > 1 ? map_rank(nrm, (uint32_t)c)[kk] : nrm[kk];
+        rk += (si > sj) || (si == sj && i < j);
+      }
+      sv[rk] = sj;
+      pv[rk] = j;
+    }
+  }
+  // columns back to the workspace: G rows to G (ld ldg), V rows to V (ld ldv)
+  T* Gw = reinterpret_cast<T*>(wsv) + b.g_off;
+  T* Vw = reinterpret_cast<T*>(wsv) + b.v_off;
+  for (int64_t e = tid; e < (int64_t)2 * m * Lc; e += nthr) {
+    const int k = (int)(e / Lc), i = (int)(e % Lc);
+    const int j = (int)rank * 2 * m + k;
+    if (j >= K) continue;
+    const T x = (k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc)[i];
+    if (i < R) Gw[i + (int64_t)j * b.ldg] = x;
+    else if (i >= Rp && i - Rp < K) Vw[i - Rp + (int64_t)j * b.ldv] = x;
+  }
+  if (CS > 1) cluster_sync_all();  // the other CTAs' norm reads are done before anyone exits
+}
+
 // Non-transposed block (A~ V = G = U S): U[:, r] = G[:, perm r] / s_r, Vh[r, :] = V[:, perm r]^H.
 // Transposed (A~^H W = G): U[:, r] = W[:, perm r], Vh[r, :] = (G[:, perm r] / s_r)^H. S = diag(s).
 // One CTA per (block, part), part 0 = U, 1 = Vh, 2 = S.
@@ -528,17 +1171,74 @@ static cudaError_t set_svd_attrs_t() {
   if (e == cudaSuccess) e = set_svd_attr<8, T, true>();
   return e;
 }
+template <int CS, typename T, int RG>
+static cudaError_t set_tile_attr() {
+  return cudaFuncSetAttribute(svd_jacobi_tile_kernel<CS, T, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024);
+}
+template <int CS, typename T>
+static cudaError_t set_tile_attrs_cs() {
+  cudaError_t e = set_tile_attr<CS, T, 1>();
+  if (e == cudaSuccess) e = set_tile_attr<CS, T, 2>();
+  if (e == cudaSuccess) e = set_tile_attr<CS, T, 3>();
+  if (e == cudaSuccess) e = set_tile_attr<CS, T, 4>();
+  if constexpr (sizeof(T) == 8) {
+    if (e == cudaSuccess) e = set_tile_attr<CS, T, 6>();
+    if (e == cudaSuccess) e = set_tile_attr<CS, T, 8>();
+  }
+  return e;
+}
+template <typename T>
+static cudaError_t set_tile_attrs_t() {
+  cudaError_t e = set_tile_attrs_cs<1, T>();
+  if (e == cudaSuccess) e = set_tile_attrs_cs<2, T>();
+  if (e == cudaSuccess) e = set_tile_attrs_cs<4, T>();
+  if (e == cudaSuccess) e = set_tile_attrs_cs<8, T>();
+  return e;
+}
+template <typename T, int RPL>
+static cudaError_t set_panel_attr() {
+  return cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024);
+}
+template <typename T>
+static cudaError_t set_panel_attrs_t() {
+  cudaError_t e = set_panel_attr<T, 2>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 4>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 6>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 8>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 12>();
+  return e;
+}
 static PerDeviceOnce g_svd_attrs;
 static cudaError_t ensure_svd_attrs() {
   return g_svd_attrs.run([] {
     cudaError_t e = set_svd_attrs_t<double>();
     if (e == cudaSuccess) e = set_svd_attrs_t<double2>();
+    if (e == cudaSuccess) e = set_tile_attrs_t<double>();
+    if (e == cudaSuccess) e = set_tile_attrs_t<double2>();
+    if (e == cudaSuccess) e = set_panel_attrs_t<double>();
+    if (e == cudaSuccess) e = set_panel_attrs_t<double2>();
     return e;
   });
 }
 
-// launch classes: (log2 CS) x (shared memory, workspace)
-constexpr int kSvdClasses = 8;
+// launch classes: svd_jacobi_kernel (log2 CS) x (shared memory, workspace): 0..7;
+// svd_jacobi_tile_kernel 8 + 6 log2 CS + index of RG in kTileRG: 8..31
+// svd_jacobi_panel_kernel 32 + 5 log2 CS + index of RPL in kPanelRPL: 32..51
+constexpr int kSvdClasses = 52;
+constexpr int kPanelRPL[5] = {2, 4, 6, 8, 12};
+static int panel_rpl_index(int rpl) {
+  for (int i = 0; i < 5; ++i)
+    if (kPanelRPL[i] == rpl) return i;
+  return 4;
+}
+constexpr int kTileRG[6] = {1, 2, 3, 4, 6, 8};
+static int tile_rg_index(int rg) {
+  for (int i = 0; i < 6; ++i)
+    if (kTileRG[i] == rg) return i;
+  return 5;
+}
 struct SvdPlan {
   Tensor* At = nullptr;
   bool cplx = false;
@@ -548,6 +1248,7 @@ struct SvdPlan {
   DevBuf d_blocks;
   std::vector<int32_t> lists[kSvdClasses];
   int class_smem[kSvdClasses] = {};
+  int class_threads[kSvdClasses] = {};
   DevBuf d_lists[kSvdClasses];
   size_t ws_bytes = 0, idx_off = 0;  // byte offset of the int32 index region
   int64_t n_sigma = 0, sig_base = 0;  // sigma region (doubles from the workspace base)
@@ -583,6 +1284,222 @@ static std::shared_ptr<SvdPlan> get_svd_plan(const Tensor& A, const std::vector<
   return g_svd_cache.get(os.str(), [&] { return build_svd_plan(A, p, q); });
 }
 
+// svd_jacobi_tile_kernel at cluster size cs: registers per lane (RG), shared memory, and an estimate of
+// the cycles of one sweep (K rounds): the slices read and written once per round at 128 B per cycle
+// (+10 % for bank conflicts), the partial-sum exchange at ~20 B per cycle of DSMEM plus ~300 cycles of
+// its latency, and ~400 cycles of dependent chain (shuffles, rotation, barrier).
+struct TileCand {
+  bool ok = false;
+  int rg = 0, smem = 0;
+  double t = 0.0;
+};
+static TileCand tile_cand(const SvdBlock& b, int cs, int es) {
+  TileCand c;
+  if (b.K < 1 || b.K > 2 * kTileMaxPairs) return c;
+  const int Rl = (b.R + cs - 1) / cs, Kl = (b.K + cs - 1) / cs;
+  const int tg = (Rl + 7) / 8, tv = (Kl + 7) / 8;
+  int rg = 0;
+  for (int x : kTileRG)
+    if (x >= tg && (es == 8 || x <= 4)) {
+      rg = x;
+      break;
+    }
+  if (!rg) return c;
+  const int npairs = (b.K + 1) / 2;
+  const int64_t bytes = tile_smem_bytes(b.K, rg, tv, cs, es);
+  if (bytes > 227 * 1024) return c;
+  // per round: the busiest scheduler issues ~(warps / 4) x (~60 + 12 instructions per row of G and V a
+  // lane holds) at ~1.5 cycles each; the exchange (bulk copies + mbarrier) ~600 cycles in a cluster
+  const double warps = std::ceil(npairs * kTileL / 32.0);
+  const double per_warp = 60.0 + 12.0 * (rg + tv) * (es == 8 ? 1.0 : 2.0);
+  const double issue = std::ceil(warps / 4.0) * per_warp * 1.5;
+  const double lat = 500.0 + 14.0 * (rg + tv);
+  c.ok = true;
+  c.rg = rg;
+  c.smem = (int)bytes;
+  c.t = (std::max(issue, lat) + (cs > 1 ? 600.0 : 0.0)) * (b.K + (b.K & 1) - 1);
+  return c;
+}
+
+// svd_jacobi_panel_kernel at cluster size cs: m columns per half-panel, RPL rows per lane, shared memory, and
+// an estimate of the cycles of one sweep: (2m - 1) stage-0 rounds and (P - 2) m outer-round rounds of
+// ~700 cycles of dependent chain plus the warps' issue and shared-memory traffic, and P - 1 moves of two
+// half-panels over DSMEM (~1500 cycles + bytes at ~50 B per cycle).
+struct PanelCand {
+  bool ok = false;
+  int m = 0, rpl = 0, smem = 0, threads = 0;
+  double t = 0.0;
+};
+static PanelCand panel_cand(const SvdBlock& b, int cs, int es) {
+  PanelCand c;
+  if (b.K < 1 || b.K > 192) return c;
+  const int Rp = (b.R + 31) & ~31, Kv = (b.K + 31) & ~31, Lc = Rp + Kv;
+  const int rt = Lc / 32;
+  int rpl = 0;
+  for (int x : kPanelRPL)
+    if (x >= rt) {
+      rpl = x;
+      break;
+    }
+  if (!rpl) return c;
+  const int m = (b.K + 2 * cs - 1) / (2 * cs);
+  const int maxw = (es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 32;
+  if (m > maxw) return c;
+  if (cs > 1 && m < 1) return c;
+  const int64_t bytes = panel_smem_bytes(m, Lc, cs, es);
+  if (bytes > 227 * 1024) return c;
+  const double traffic = (double)m * Lc * es * 2 / 128.0;
+  const double t_in = 700.0 + 25.0 * m + traffic;
+  const double P = 2.0 * cs;
+  double sweep = (2.0 * m - 1) * (t_in + 0.5 * traffic);
+  if (cs > 1) sweep += (P - 2) * m * t_in + (P - 1) * (1500.0 + 2.0 * m * Lc * es / 50.0);
+  c.ok = true;
+  c.m = m;
+  c.rpl = rpl;
+  c.smem = (int)bytes;
+  c.threads = 32 * std::max(m, 2);
+  c.t = sweep;
+  return c;
+}
+
+// Cluster sizes of the tile-kernel blocks: all blocks run concurrently, so the step takes about
+// max(longest block, total CTA-time / SMs). Start from the fastest CS of every block (bound Lb), then
+// give every block the smallest CS that still finishes within the target, and raise the target to the
+// area bound while that moves it.
+static void assign_tile_blocks(SvdPlan& P, const std::vector<int>& tiles, int es) {
+  if (tiles.empty()) return;
+  static const int n_sm = [] {
+    int d = 0, n = 0;
+    if (cudaGetDevice(&d) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) == cudaSuccess &&
+        n > 0)
+      return n;
+    cudaGetLastError();
+    return 148;
+  }();
+  static const int force_cs = (int)knob("TK_SVD_TILE_CS", 0);
+  const int css[4] = {1, 2, 4, 8};
+  double Lb = 0.0;
+  for (int i : tiles) {
+    double best = 1e300;
+    for (int cs : css) {
+      const TileCand c = tile_cand(P.blocks[i], cs, es);
+      if (c.ok) best = std::min(best, c.t);
+    }
+    Lb = std::max(Lb, best);
+  }
+  std::vector<int> pick(tiles.size(), 8);
+  double target = Lb;
+  for (int it = 0; it < 6; ++it) {
+    double area = 0.0;
+    for (size_t k = 0; k < tiles.size(); ++k) {
+      const SvdBlock& b = P.blocks[tiles[k]];
+      int chosen = 0;
+      double ct = 0.0;
+      for (int cs : css) {
+        const TileCand c = tile_cand(b, cs, es);
+        if (!c.ok) continue;
+        if (force_cs ? cs == force_cs : c.t <= target * 1.0001) {
+          chosen = cs;
+          ct = c.t;
+          break;
+        }
+      }
+      if (!chosen) {  // (force_cs not feasible) the fastest feasible
+        double best = 1e300;
+        for (int cs : css) {
+          const TileCand c = tile_cand(b, cs, es);
+          if (c.ok && c.t < best) best = c.t, chosen = cs;
+        }
+        ct = best;
+      }
+      pick[k] = chosen;
+      area += chosen * ct;
+    }
+    const double nt = std::max(Lb, area / n_sm);
+    if (nt <= target * 1.01) break;
+    target = nt;
+  }
+  // longest blocks first inside every class
+  std::vector<std::pair<double, int>> order;
+  for (size_t k = 0; k < tiles.size(); ++k) {
+    SvdBlock& b = P.blocks[tiles[k]];
+    const TileCand c = tile_cand(b, pick[k], es);
+    b.tile = 1;
+    b.cs = pick[k];
+    b.rg = c.rg;
+    b.smem = 1;
+    b.Rl = (b.R + b.cs - 1) / b.cs;
+    b.Kl = (b.K + b.cs - 1) / b.cs;
+    order.push_back({-c.t, tiles[k]});
+    int l2cs = 0;
+    while ((1 << l2cs) < b.cs) ++l2cs;
+    const int cls = 8 + 6 * l2cs + tile_rg_index(b.rg);
+    P.class_smem[cls] = std::max(P.class_smem[cls], c.smem);
+  }
+  std::sort(order.begin(), order.end());
+  for (auto& o : order) {
+    const SvdBlock& b = P.blocks[o.second];
+    int l2cs = 0;
+    while ((1 << l2cs) < b.cs) ++l2cs;
+    P.lists[8 + 6 * l2cs + tile_rg_index(b.rg)].push_back((int32_t)o.second);
+  }
+}
+
+// Panel-kernel blocks: every block takes its fastest cluster size, then the smallest one within the
+// longest block's time (fewer SMs for the same step time).
+static void assign_panel_blocks(SvdPlan& P, const std::vector<int>& panels, int es) {
+  if (panels.empty()) return;
+  static const int force_cs = (int)knob("TK_SVD_PANEL_CS", 0);
+  const int css[4] = {1, 2, 4, 8};
+  double Lb = 0.0;
+  for (int i : panels) {
+    double best = 1e300;
+    for (int cs : css) {
+      const PanelCand c = panel_cand(P.blocks[i], cs, es);
+      if (c.ok) best = std::min(best, c.t);
+    }
+    Lb = std::max(Lb, best);
+  }
+  std::vector<std::pair<double, int>> order;
+  for (int i : panels) {
+    SvdBlock& b = P.blocks[i];
+    PanelCand pick;
+    for (int cs : css) {
+      const PanelCand c = panel_cand(b, cs, es);
+      if (c.ok && (force_cs ? cs == force_cs : c.t <= Lb * 1.0001)) {
+        pick = c;
+        b.cs = cs;
+        break;
+      }
+    }
+    if (!pick.ok) {
+      double best = 1e300;
+      for (int cs : css) {
+        const PanelCand c = panel_cand(b, cs, es);
+        if (c.ok && c.t < best) best = c.t, pick = c, b.cs = cs;
+      }
+    }
+    b.tile = 2;
+    b.rg = pick.rpl;
+    b.Kl = pick.m;
+    b.Rl = pick.threads;
+    b.smem = 1;
+    int l2cs = 0;
+    while ((1 << l2cs) < b.cs) ++l2cs;
+    const int cls = 32 + 5 * l2cs + panel_rpl_index(pick.rpl);
+    P.class_smem[cls] = std::max(P.class_smem[cls], pick.smem);
+    P.class_threads[cls] = std::max(P.class_threads[cls], pick.threads);
+    order.push_back({-pick.t, i});
+  }
+  std::sort(order.begin(), order.end());
+  for (auto& o : order) {
+    const SvdBlock& b = P.blocks[o.second];
+    int l2cs = 0;
+    while ((1 << l2cs) < b.cs) ++l2cs;
+    P.lists[32 + 5 * l2cs + panel_rpl_index(b.rg)].push_back((int32_t)o.second);
+  }
+}
+
 static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vector<int>& p, const std::vector<int>& q) {
   validate_perm(A, p, q);
   auto P = std::make_shared<SvdPlan>();
@@ -596,6 +1513,9 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
   // workspace (elements of T): A~ | transposed G blocks | V blocks ; then (doubles) sigma | global-mode
   // partial sums ; then (int32) sorted column indices
   static const int rows_target = (int)knob("TK_SVD_ROWS", kSvdRowsTarget);
+  static const bool tile_enabled = knob("TK_SVD_NO_TILE", 0) == 0;
+  static const bool panel_enabled = knob("TK_SVD_NO_PANEL", 0) == 0;
+  std::vector<int> tiles, panels;
   int64_t off = P->la.total;
   int64_t nsig = 0, nidx = 0, npart = 0;
   for (size_t c = 0; c < P->At->blocks.size(); ++c) {
@@ -624,6 +1544,18 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     nsig += b.K;
     b.p_off = nidx;
     nidx += b.K;
+    b.tile = 0;
+    b.rg = 0;
+    if (panel_enabled && panel_cand(b, 8, es).ok) {  // decided below, over all blocks
+      panels.push_back((int)P->blocks.size());
+      P->blocks.push_back(b);
+      continue;
+    }
+    if (tile_enabled && tile_cand(b, 8, es).ok) {  // decided below, over all blocks
+      tiles.push_back((int)P->blocks.size());
+      P->blocks.push_back(b);
+      continue;
+    }
     // cluster size: the smallest CS with <= rows_target rows of G per CTA whose rows of G and V fit the
     // shared-memory budget; else CS = 8 with the rows in the (L2-resident) workspace
     const int64_t npairs = (b.K + 1) / 2;
@@ -661,6 +1593,8 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     P->lists[cls].push_back((int32_t)P->blocks.size());
     P->blocks.push_back(b);
   }
+  assign_tile_blocks(*P, tiles, es);
+  assign_panel_blocks(*P, panels, es);
   // doubles from the workspace base: sigma, then the global-mode partial sums
   P->sig_base = (off * dpe + 31) & ~int64_t(31);
   const int64_t x_base = (P->sig_base + nsig + 1) & ~int64_t(1);  // 16-byte aligned partial sums
@@ -674,8 +1608,15 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     fprintf(stderr, "[tk svd] %zu blocks:", P->blocks.size());
     for (int c = 0; c < kSvdClasses; ++c)
       if (!P->lists[c].empty())
-        fprintf(stderr, " cs%d/%s x%zu (smem %d B)", 1 << (c / 2), (c & 1) ? "ws" : "smem", P->lists[c].size(),
-                P->class_smem[c]);
+        if (c >= 32)
+          fprintf(stderr, " panel cs%d/rpl%d x%zu (smem %d B, %d threads)", 1 << ((c - 32) / 5), kPanelRPL[(c - 32) % 5],
+                  P->lists[c].size(), P->class_smem[c], P->class_threads[c]);
+        else if (c < 8)
+          fprintf(stderr, " cs%d/%s x%zu (smem %d B)", 1 << (c / 2), (c & 1) ? "ws" : "smem", P->lists[c].size(),
+                  P->class_smem[c]);
+        else
+          fprintf(stderr, " tile cs%d/rg%d x%zu (smem %d B)", 1 << ((c - 8) / 6), kTileRG[(c - 8) % 6], P->lists[c].size(),
+                  P->class_smem[c]);
     fprintf(stderr, "\n");
   }
   P->ws_bytes = align256(P->idx_off + (size_t)nidx * 4);
@@ -717,8 +1658,83 @@ static cudaStream_t svd_aux_stream(int i) {
   return s;
 }
 
+template <int CS, typename T, int RG>
+static cudaError_t launch_tile_class(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P.lists[cls].size() * CS));
+  cfg.blockDim = dim3(kTileThreads);
+  cfg.dynamicSmemBytes = (size_t)P.class_smem[cls];
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  static const int debug = std::getenv("TK_SVD_DEBUG") ? 1 : 0;  // diagnostic print only
+  return cudaLaunchKernelEx(&cfg, svd_jacobi_tile_kernel<CS, T, RG>, ws, idx, (const SvdBlock*)P.d_blocks.p,
+                            (const int32_t*)P.d_lists[cls].p, debug);
+}
+template <int CS, typename T>
+static cudaError_t launch_tile_cs(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
+  switch ((cls - 8) % 6) {
+    case 0: return launch_tile_class<CS, T, 1>(P, cls, ws, idx, st);
+    case 1: return launch_tile_class<CS, T, 2>(P, cls, ws, idx, st);
+    case 2: return launch_tile_class<CS, T, 3>(P, cls, ws, idx, st);
+    case 3: return launch_tile_class<CS, T, 4>(P, cls, ws, idx, st);
+    default:
+      if constexpr (sizeof(T) == 8) {
+        if ((cls - 8) % 6 == 4) return launch_tile_class<CS, T, 6>(P, cls, ws, idx, st);
+        return launch_tile_class<CS, T, 8>(P, cls, ws, idx, st);
+      }
+      return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int RPL>
+static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
+  const unsigned cs = 1u << ((cls - 32) / 5);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P.lists[cls].size() * cs));
+  cfg.blockDim = dim3((unsigned)P.class_threads[cls]);
+  cfg.dynamicSmemBytes = (size_t)P.class_smem[cls];
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  static const int debug = std::getenv("TK_SVD_DEBUG") ? 1 : 0;  // diagnostic print only
+  return cudaLaunchKernelEx(&cfg, svd_jacobi_panel_kernel<T, RPL>, ws, idx, (const SvdBlock*)P.d_blocks.p,
+                            (const int32_t*)P.d_lists[cls].p, debug);
+}
+
 template <typename T>
 static cudaError_t launch_svd_cls(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
+  if (cls >= 32) {
+    switch ((cls - 32) % 5) {
+      case 0: return launch_panel_class<T, 2>(P, cls, ws, idx, st);
+      case 1: return launch_panel_class<T, 4>(P, cls, ws, idx, st);
+      case 2: return launch_panel_class<T, 6>(P, cls, ws, idx, st);
+      case 3: return launch_panel_class<T, 8>(P, cls, ws, idx, st);
+      default: return launch_panel_class<T, 12>(P, cls, ws, idx, st);
+    }
+  }
+  if (cls >= 8) {
+    switch ((cls - 8) / 6) {
+      case 0: return launch_tile_cs<1, T>(P, cls, ws, idx, st);
+      case 1: return launch_tile_cs<2, T>(P, cls, ws, idx, st);
+      case 2: return launch_tile_cs<4, T>(P, cls, ws, idx, st);
+      default: return launch_tile_cs<8, T>(P, cls, ws, idx, st);
+    }
+  }
   const int cs = 1 << (cls / 2);
   const bool sm = (cls & 1) == 0;
   switch (cs * 2 + (sm ? 0 : 1)) {

@@ -167,3 +167,74 @@ def test_svd_su2_mps():
     x = H.oracle_flat(lt, cfg["cfg"], idx)
     _check("SU2", spec["cod"], spec["dom"], x, [0, 1], [2], 20)
     _check("SU2", spec["cod"], spec["dom"], x, [0], [1, 2], 0, 1e-3)
+
+
+def _check_blocks(kind, cod, dom, x, p, q):
+    """Untruncated SVD at the timed sizes, compared block by block (the dense embedding of an
+    8192 x 8192 two-site matrix is too large for the oracle's einsum): every block's spectrum against
+    numpy LAPACK (1e-12 sigma_max), U_c S_c Vh_c against the oracle's permuted block (1e-12 relative to
+    ||A||), and the isometry of U_c and Vh_c."""
+    lp, xp, _ = OS.permuted(kind, cod, dom, x, list(p), list(q))
+    svds = OS.block_svd(lp, xp)
+    spec, wdeg, err, nrm, (u, s, vh) = _run(kind, cod, dom, x, p, q, 0, 0.0)
+    smax = max(float(sv[0]) for _, _, sv, _ in svds if len(sv))
+    anorm = float(np.linalg.norm(xp))
+    assert len(spec) == len(svds)
+    for got, (c, _, ref, _) in zip(spec, svds):
+        assert np.abs(got - ref).max(initial=0.0) <= TOL * smax, c
+    Wspace = W.space(kind, [(c, k) for c, k in wdeg.items()])
+    lu = OL.homspace_layout(kind, lp.cod, [Wspace])
+    ls = OL.homspace_layout(kind, [Wspace], [Wspace])
+    lv = OL.homspace_layout(kind, [Wspace], lp.dom)
+    ub = {c: (r, k, o) for c, r, k, o in lu.blocks}
+    sb = {c: (k, o) for c, k, _, o in ls.blocks}
+    vb = {c: (k, n, o) for c, k, n, o in lv.blocks}
+    worst = 0.0
+    for (c, rows, cols, off) in lp.blocks:
+        m = xp[off:off + rows * cols].reshape(rows, cols, order="F")
+        r, k, uo = ub[c]
+        mu = u[uo:uo + r * k].reshape(r, k, order="F")
+        ms = s[sb[c][1]:sb[c][1] + k * k].reshape(k, k, order="F")
+        k2, n, vo = vb[c]
+        mv = vh[vo:vo + k2 * n].reshape(k2, n, order="F")
+        worst = max(worst, np.linalg.norm(mu @ ms @ mv - m))
+        assert np.abs(mu.conj().T @ mu - np.eye(k)).max() <= 1e-12, c
+        assert np.abs(mv @ mv.conj().T - np.eye(k2)).max() <= 1e-12, c
+    assert worst <= TOL * anorm, worst / anorm
+
+
+@pytest.mark.parametrize("cfgname", ["cfg2", "cfg3", "cfg7", "cfg8"])
+def test_svd_two_site_full_size(cfgname):
+    """The two-site tensors at the sizes tools/bench_svd.py times (blocks up to 181 x 181 for cfg3):
+    the tile kernel at every cluster size the planner picks."""
+    cfg = getattr(W, cfgname)()
+    cod, dom, x = _two_site(cfg)
+    _check_blocks(cfg["kind"], cod, dom, x, [0, 1], [2, 3])
+
+
+def test_svd_two_site_full_size_complex():
+    cfg = W.cfg3()
+    cod, dom, x = _two_site(cfg)
+    xi = np.random.default_rng(14).standard_normal(x.shape)
+    _check_blocks(cfg["kind"], cod, dom, x + 1j * xi, [0, 1], [2, 3])
+
+
+# (rows, cols) of a single block: tile kernel at RG 1..8 and cluster sizes 1..8, ragged row tiles, odd
+# K (a player sits out), wide blocks (G = A~^H); K > 192 or more than 64 rows per CTA (32 complex) at
+# CS 8 go to the shared-memory / workspace cluster kernel
+TILE_SHAPES = [(1, 1), (7, 3), (3, 7), (33, 33), (64, 17), (130, 129), (181, 181), (192, 192), (511, 180),
+               (513, 100), (200, 193), (300, 257)]
+
+
+@pytest.mark.parametrize("shape", TILE_SHAPES, ids=[f"{r}x{c}" for r, c in TILE_SHAPES])
+@pytest.mark.parametrize("cplx", [False, True], ids=["f64", "c64"])
+def test_svd_tile_shapes(shape, cplx):
+    rows, cols = shape
+    V = W.space("U1", [((0,), rows)])
+    Wd = W.space("U1", [((0,), cols)])
+    lt = OL.homspace_layout("U1", [V], [Wd])
+    rng = np.random.default_rng(rows * 1000 + cols)
+    x = rng.standard_normal(lt.nelems)
+    if cplx:
+        x = x + 1j * rng.standard_normal(lt.nelems)
+    _check_blocks("U1", [V], [Wd], x, [0], [1])
