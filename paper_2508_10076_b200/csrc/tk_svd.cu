@@ -37,6 +37,7 @@
 #include <memory>
 #include <mutex>
 #include <sstream>
+#include <tuple>
 
 #include "tk_device.cuh"
 #include "tk_plan.hpp"
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // touch the cluster. Warp i owns T_c[i] in registers during an outer round; B columns stream through
 // shared memory (one load + one store per warp and round). A lane holds rows lane + 32 t of a column
 // (RPL per lane): G rows first (padded to a multiple of 32), then V rows.
-constexpr int kPanelThreadsReal = 768, kPanelThreadsCplx = 384;
+constexpr int kPanelThreadsReal = 768, kPanelThreadsCplx = 768;
 template <typename T>
 struct PanelCfg {
   static constexpr int threads = sizeof(T) == 8 ? kPanelThreadsReal : kPanelThreadsCplx;
@@ -849,12 +850,37 @@ __device__ __forceinline__ uint32_t cluster_id_x() {
 __device__ __forceinline__ void bulk_commit_wait_read() {
   asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
-// bytes of shared memory: T_in, T_out, B_cur, B_in ([m][Lc] each), 2m norms, CS flags, one mbarrier
+// bytes of shared memory: T_in, T_out, B_cur, B_in ([m][Lc] each), rotations [2][m][4] + flags [2][m],
+// 2m norms, convergence flags, one mbarrier
 __host__ __device__ inline int64_t panel_smem_bytes(int m, int Lc, int cs, int es) {
-  return 4LL * m * Lc * es + 16LL * m + 8LL * cs + 64;
+  return 4LL * m * Lc * es + 64LL * m + 8LL * m + 16 + 16LL * m + 16 + 16;
 }
 
-template <typename T, int RPL>
+// Jacobi rotation of [[alpha, |gamma|], [|gamma|, beta]] without a division: with rho = beta - alpha,
+// h = sqrt(rho^2 + 4 |gamma|^2) and d = |rho| + h, the tangent is t = sign(rho) 2|gamma| / d, so
+// c = d / sqrt(d^2 + 4|gamma|^2) and s = sign(rho) 2|gamma| / sqrt(d^2 + 4|gamma|^2) -- one sqrt and one
+// rsqrt (~250 cycles of dependent latency on B200 against ~450 for the textbook zeta/t/c chain), c and s
+// both to working precision (c^2 + s^2 = 1 + O(eps)). rho and |gamma| are first scaled by a power of two
+// (|gamma| into [1, 2)) so the squares neither overflow nor underflow; |rho| > 2^500 |gamma| gives
+// c = 1, s = |gamma| / rho.
+__device__ __forceinline__ void jacobi_rot(double al, double be, double ag, double& c, double& s) {
+  const long long eb = (__double_as_longlong(ag) >> 52) & 0x7ff;
+  const double sc = __longlong_as_double((2046LL - eb) << 52);
+  const double rho = (be - al) * sc, g = ag * sc;
+  if (fabs(rho) > 3.273390607896142e150) {  // 2^500
+    c = 1.0;
+    s = g / rho;
+    return;
+  }
+  const double g2 = 4.0 * g * g;
+  const double h = sqrt(fma(rho, rho, g2));
+  const double d = fabs(rho) + h;
+  const double r = rsqrt(fma(d, d, g2));
+  c = d * r;
+  s = copysign(2.0 * g * r, rho);
+}
+
+template <typename T, int RH>
 __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
     svd_jacobi_panel_kernel(void* __restrict__ wsv, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
                             const int32_t* __restrict__ list, int debug) {
@@ -866,18 +892,24 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
   const uint32_t rank = CS > 1 ? cluster_rank() : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
   const int R = b.R, K = b.K;
-  const int m = b.Kl;                     // columns per half-panel
+  const int m = b.Kl;  // columns per half-panel
   const int P = 2 * CS;
   const int Rp = (R + 31) & ~31, Kv = (K + 31) & ~31, Lc = Rp + Kv;
-  const int RGT = Rp >> 5;                // per-lane G rows
-  const int RT = Lc >> 5;                 // per-lane rows (<= RPL)
+  // warps 0 .. m-1 (G-warps) rotate the G rows of pair slot `pi` and decide the rotations; warps m .. 2m-1
+  // (V-warps) apply each slot's rotation to its V rows one round later, off the critical path
+  const bool gw = warp < m, vw = warp >= m && warp < 2 * m;
+  const int pi = gw ? warp : warp - m;
+  const int rb = gw ? 0 : Rp;                   // first row of this warp's part of a column
+  const int nrow = gw ? (Rp >> 5) : (Kv >> 5);  // rows per lane (<= RH)
   T* Tin = reinterpret_cast<T*>(svd_dyn);
   T* Tout = Tin + (size_t)m * Lc;
   T* Bcur = Tout + (size_t)m * Lc;
   T* Bin = Bcur + (size_t)m * Lc;
-  double* nrm = reinterpret_cast<double*>(Bin + (size_t)m * Lc);  // 2m
-  int* flag = reinterpret_cast<int*>(nrm + 2 * m);                  // CS (flag[0] used)
-  uint64_t* mbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(flag + CS) + 7) & ~uintptr_t(7));
+  double* rot = reinterpret_cast<double*>(Bin + (size_t)m * Lc);  // [2][m][4]: c, s, (ur, ui) or (s ur, c ur)
+  int* rflag = reinterpret_cast<int*>(rot + 8 * m);                  // [2][m]: rotation applied
+  double* nrm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rflag + 2 * m) + 15) & ~uintptr_t(15));  // 2m
+  int* flag = reinterpret_cast<int*>(nrm + 2 * m);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(flag + 2) + 7) & ~uintptr_t(7));
   const T* A = reinterpret_cast<const T*>(wsv) + b.a_off;
   if (tid == 0) {
     mbar_init(mbar, 1);
@@ -900,99 +932,156 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
   const double tol2 = tol * tol;
   uint32_t mph = 0;
   int sweep = 0;
-  const bool act = warp < m;
-  T t[RPL], u[RPL];
+  T t[RH], u[RH];
+#ifdef TK_SVD_TIMERS
+  long long pt[6] = {0, 0, 0, 0, 0, 0}, pts = 0, ptn = 0, pmv = 0;  // load, dots, reduce, rotation, update, barrier
+#define TK_PT(i) do { const long long _c = clock64(); pt[i] += _c - pts; pts = _c; } while (0)
+#else
+#define TK_PT(i) do { } while (0)
+#endif
+  // G-warp: dots of (x, y) over the G rows, the rotation (slot `pi`, parity `sl`), applied to x, y
+  auto g_rotate = [&](int sl) -> int {
+    double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+#pragma unroll
+    for (int r = 0; r < RH; ++r)
+      if (r < nrow) {
+        al += N::abs2(t[r]);
+        be += N::abs2(u[r]);
+        N::dot(t[r], u[r], gr, gi);
+      }
+    TK_PT(1);
+    warp_sum4(al, be, gr, gi);
+    TK_PT(2);
+    const double ga2 = fma(gr, gr, gi * gi);
+    const int doit = ga2 > tol2 * al * be && ga2 > 0.0;
+    if (!doit) {
+      if (lane == 0) rflag[sl * m + pi] = 0;
+      return 0;
+    }
+    double c, sn, q0, q1;
+    if (CPLX) {
+      const double rga = rsqrt(ga2);
+      q0 = gr * rga;  // the unit phase of gamma
+      q1 = gi * rga;
+      jacobi_rot(al, be, ga2 * rga, c, sn);
+#pragma unroll
+      for (int r = 0; r < RH; ++r)
+        if (r < nrow) {
+          const T x = t[r], y = N::rephase(u[r], q0, q1);
+          t[r] = N::lin(c, x, -sn, y);
+          u[r] = N::lin(sn, x, c, y);
+        }
+    } else {
+      jacobi_rot(al, be, fabs(gr), c, sn);
+      TK_PT(3);
+      const double ur = gr < 0.0 ? -1.0 : 1.0;
+      q0 = sn * ur;  // x' = c x - (s ur) y, y' = s x + (c ur) y
+      q1 = c * ur;
+#pragma unroll
+      for (int r = 0; r < RH; ++r)
+        if (r < nrow) {
+          const T x = t[r], y = u[r];
+          t[r] = N::lin(c, x, -q0, y);
+          u[r] = N::lin(sn, x, q1, y);
+        }
+    }
+    if (lane == 0) {
+      double* rr = rot + (sl * m + pi) * 4;
+      rr[0] = c;
+      rr[1] = sn;
+      rr[2] = q0;
+      rr[3] = q1;
+      rflag[sl * m + pi] = 1;
+    }
+    return 1;
+  };
+  // V-warp: the rotation of slot `pi`, parity `sl`, applied to x, y (V rows); returns whether one was applied
+  auto v_rotate = [&](int sl) -> int {
+    if (!rflag[sl * m + pi]) return 0;
+    const double* rr = rot + (sl * m + pi) * 4;
+    const double c = rr[0], sn = rr[1], q0 = rr[2], q1 = rr[3];
+#pragma unroll
+    for (int r = 0; r < RH; ++r)
+      if (r < nrow) {
+        if (CPLX) {
+          const T x = t[r], y = N::rephase(u[r], q0, q1);
+          t[r] = N::lin(c, x, -sn, y);
+          u[r] = N::lin(sn, x, c, y);
+        } else {
+          const T x = t[r], y = u[r];
+          t[r] = N::lin(c, x, -q0, y);
+          u[r] = N::lin(sn, x, q1, y);
+        }
+      }
+    return 1;
+  };
+  auto col = [&](int k) -> T* { return k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc; };
   for (; sweep < kSvdMaxSweeps; ++sweep) {
-    const bool exact = sweep >= kTileExactSweep;
     int any = 0;
-    // rotate the pair (x, y) in registers; returns whether a rotation was applied
-    auto rotate = [&](T (&x)[RPL], T (&y)[RPL]) -> int {
-      double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
-#pragma unroll
-      for (int r = 0; r < RPL; ++r)
-        if (r < RGT) {
-          al += N::abs2(x[r]);
-          be += N::abs2(y[r]);
-          N::dot(x[r], y[r], gr, gi);
-        }
-      if (CPLX) {
-        warp_sum4(al, be, gr, gi);
-      } else {
-        double dd = 0.0;
-        warp_sum4(al, be, gr, dd);
-      }
-      const double ga2 = fma(gr, gr, gi * gi);
-      if (!(ga2 > tol2 * al * be && ga2 > 0.0)) return 0;
-      double ur, ui, ag;
-      if (CPLX) {
-        const double rga = rsqrt(ga2);
-        ur = gr * rga;
-        ui = gi * rga;
-        ag = ga2 * rga;
-      } else {
-        ur = gr < 0.0 ? -1.0 : 1.0;
-        ui = 0.0;
-        ag = fabs(gr);
-      }
-      double c, sn;
-      if (exact) {
-        const double zeta = 0.5 * (be - al) / ag;
-        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        c = rsqrt(fma(tt, tt, 1.0));
-        sn = c * tt;
-      } else {
-        jacobi_cs_fast(al, be, ag, c, sn);
-      }
-#pragma unroll
-      for (int r = 0; r < RPL; ++r)
-        if (r < RT) {
-          const T a0 = x[r], b0 = N::rephase(y[r], ur, ui);
-          x[r] = N::lin(c, a0, -sn, b0);
-          y[r] = N::lin(sn, a0, c, b0);
-        }
-      return 1;
-    };
-    // ---- stage 0: circle tournament over the CTA's 2m columns (players k < m: T_in[k], else B_cur[k - m])
+    // ---- stage 0: circle tournament over the CTA's 2m columns (players k < m: T_in[k], else B_cur[k - m]);
+    // the V-warps run one round behind (round 2m - 1 is theirs alone)
     {
       const int n2 = 2 * m;
-      for (int r = 0; r < n2 - 1; ++r) {
-        if (act) {
+      for (int r = 0; r < n2; ++r) {
+        if (gw && r < n2 - 1) {
           int p, q;
-          round_pair_fast(r, warp, n2, n2, p, q);
-          T* cp = p < m ? Tin + (size_t)p * Lc : Bcur + (size_t)(p - m) * Lc;
-          T* cq = q < m ? Tin + (size_t)q * Lc : Bcur + (size_t)(q - m) * Lc;
+          round_pair_fast(r, pi, n2, n2, p, q);
+          T* cp = col(p) + rb + lane;
+          T* cq = col(q) + rb + lane;
 #pragma unroll
-          for (int rr = 0; rr < RPL; ++rr)
-            if (rr < RT) {
-              t[rr] = cp[lane + 32 * rr];
-              u[rr] = cq[lane + 32 * rr];
+          for (int k = 0; k < RH; ++k)
+            if (k < nrow) {
+              t[k] = cp[32 * k];
+              u[k] = cq[32 * k];
             }
-          if (rotate(t, u)) {
+          if (g_rotate(r & 1)) {
             any = 1;
 #pragma unroll
-            for (int rr = 0; rr < RPL; ++rr)
-              if (rr < RT) {
-                cp[lane + 32 * rr] = t[rr];
-                cq[lane + 32 * rr] = u[rr];
+            for (int k = 0; k < RH; ++k)
+              if (k < nrow) {
+                cp[32 * k] = t[k];
+                cq[32 * k] = u[k];
+              }
+          }
+        } else if (vw && r >= 1) {
+          int p, q;
+          round_pair_fast(r - 1, pi, n2, n2, p, q);
+          T* cp = col(p) + rb + lane;
+          T* cq = col(q) + rb + lane;
+          if (rflag[((r - 1) & 1) * m + pi]) {
+#pragma unroll
+            for (int k = 0; k < RH; ++k)
+              if (k < nrow) {
+                t[k] = cp[32 * k];
+                u[k] = cq[32 * k];
+              }
+            v_rotate((r - 1) & 1);
+#pragma unroll
+            for (int k = 0; k < RH; ++k)
+              if (k < nrow) {
+                cp[32 * k] = t[k];
+                cq[32 * k] = u[k];
               }
           }
         }
         __syncthreads();
       }
     }
-    // ---- outer rounds: move, then all m^2 pairs (T_c[i], B_c[(i + s) mod m])
+    // ---- outer rounds: move, then all m^2 pairs (T_c[i], B_c[(i + s) mod m]); the V-warps one round behind
     if (CS > 1) {
-      if (act) {
+      if (gw || vw) {
 #pragma unroll
-        for (int rr = 0; rr < RPL; ++rr)
-          if (rr < RT) t[rr] = Tin[(size_t)warp * Lc + lane + 32 * rr];
+        for (int k = 0; k < RH; ++k)
+          if (k < nrow) t[k] = Tin[(size_t)pi * Lc + rb + lane + 32 * k];
       }
       for (int o = 1; o < P; ++o) {
-        // move: T (registers) -> T_out; copies T_out and B_cur to their next places
-        if (act) {
+#ifdef TK_SVD_TIMERS
+        long long tmv = clock64();
+#endif
+        if (gw || vw) {
 #pragma unroll
-          for (int rr = 0; rr < RPL; ++rr)
-            if (rr < RT) Tout[(size_t)warp * Lc + lane + 32 * rr] = t[rr];
+          for (int k = 0; k < RH; ++k)
+            if (k < nrow) Tout[(size_t)pi * Lc + rb + lane + 32 * k] = t[k];
         }
         fence_proxy_async_smem();
         __syncthreads();
@@ -1001,9 +1090,9 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
         if (tid == 0) mbar_arrive_expect_tx(mbar, 2 * bytes);
         if (tid == 0 || tid == 32) {  // two warps (blockDim >= 64): the copies issue in parallel
           const bool isT = tid == 0;
+          const int c = (int)rank;
           uint32_t dst_rank;
           bool dst_T;
-          const int c = (int)rank;
           if (isT) {
             if (c == 0) dst_rank = 0, dst_T = true;
             else if (c == CS - 1) dst_rank = (uint32_t)c, dst_T = false;
@@ -1024,29 +1113,51 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
           Bcur = Bin;
           Bin = x;
         }
-        if (act) {
+        if (gw || vw) {
 #pragma unroll
-          for (int rr = 0; rr < RPL; ++rr)
-            if (rr < RT) t[rr] = Tin[(size_t)warp * Lc + lane + 32 * rr];
+          for (int k = 0; k < RH; ++k)
+            if (k < nrow) t[k] = Tin[(size_t)pi * Lc + rb + lane + 32 * k];
         }
+#ifdef TK_SVD_TIMERS
+        pt[0] += clock64() - tmv;
+        ++pmv;
+#endif
         if (o == P - 1) break;  // the last move restores the initial placement
-        for (int s2 = 0; s2 < m; ++s2) {
-          if (act) {
-            T* cq = Bcur + (size_t)((warp + s2) % m) * Lc;
+        for (int s2 = 0; s2 <= m; ++s2) {
+          if (gw && s2 < m) {
+#ifdef TK_SVD_TIMERS
+            pts = clock64();
+            ++ptn;
+#endif
+            T* cq = Bcur + (size_t)((pi + s2) % m) * Lc + lane;
 #pragma unroll
-            for (int rr = 0; rr < RPL; ++rr)
-              if (rr < RT) u[rr] = cq[lane + 32 * rr];
-            if (rotate(t, u)) {
+            for (int k = 0; k < RH; ++k)
+              if (k < nrow) u[k] = cq[32 * k];
+            if (g_rotate(s2 & 1)) {
               any = 1;
 #pragma unroll
-              for (int rr = 0; rr < RPL; ++rr)
-                if (rr < RT) cq[lane + 32 * rr] = u[rr];
+              for (int k = 0; k < RH; ++k)
+                if (k < nrow) cq[32 * k] = u[k];
+            }
+            TK_PT(4);
+          } else if (vw && s2 >= 1) {
+            if (rflag[((s2 - 1) & 1) * m + pi]) {
+              T* cq = Bcur + (size_t)((pi + s2 - 1) % m) * Lc + Rp + lane;
+#pragma unroll
+              for (int k = 0; k < RH; ++k)
+                if (k < nrow) u[k] = cq[32 * k];
+              v_rotate((s2 - 1) & 1);
+#pragma unroll
+              for (int k = 0; k < RH; ++k)
+                if (k < nrow) cq[32 * k] = u[k];
             }
           }
           __syncthreads();
+#ifdef TK_SVD_TIMERS
+          if (gw && s2 < m) TK_PT(5);
+#endif
         }
       }
-      // T back to T_in (the move above left T_in = the registers' columns, unchanged since)
     }
     // ---- convergence: OR over the cluster
     const int cta_any = __syncthreads_or(any);
@@ -1054,21 +1165,29 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
       if (tid == 0) flag[0] = cta_any;
       cluster_sync_all();
       int all = 0;
-      for (int c = 0; c < CS; ++c) all |= *reinterpret_cast<const int*>(map_rank(reinterpret_cast<const double*>(flag), (uint32_t)c));
+      for (int c = 0; c < CS; ++c)
+        all |= *reinterpret_cast<const int*>(map_rank(reinterpret_cast<const double*>(flag), (uint32_t)c));
       cluster_sync_all();  // flags read before anyone rewrites them
       if (!all) break;
     } else if (!cta_any) {
       break;
     }
   }
-  if (debug && tid == 0 && rank == 0)
-    printf("[tk svd panel] block %d: %d x %d, cluster %d, m %d, RPL %d, %d sweeps\n", list[cluster_id_x()], R, K, CS, m,
-           RPL, sweep + 1);
+  if (debug && tid == 0 && rank == 0) {
+    printf("[tk svd panel] block %d: %d x %d, cluster %d, m %d, RH %d, %d sweeps\n", list[cluster_id_x()], R, K, CS, m,
+           RH, sweep + 1);
+#ifdef TK_SVD_TIMERS
+    if (ptn)
+      printf("[tk svd panel] outer-round cycles per round: load+dots %lld reduce %lld rotation %lld update %lld barrier %lld\n",
+             pt[1] / ptn, pt[2] / ptn, pt[3] / ptn, pt[4] / ptn, pt[5] / ptn);
+    if (pmv) printf("[tk svd panel] cycles per move: %lld (%lld moves)\n", pt[0] / pmv, pmv);
+#endif
+  }
   // column norms of the CTA's 2m columns (G rows), ranked against every column of the block
   for (int k = warp; k < 2 * m; k += nthr >> 5) {
-    const T* col = k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc;
+    const T* cc = col(k);
     double x = 0.0;
-    for (int i = lane; i < Rp; i += 32) x += N::abs2(col[i]);
+    for (int i = lane; i < Rp; i += 32) x += N::abs2(cc[i]);
     x = warp_sum(x);
     if (lane == 0) nrm[k] = sqrt(x);
   }
@@ -1097,7 +1216,7 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
     const int k = (int)(e / Lc), i = (int)(e % Lc);
     const int j = (int)rank * 2 * m + k;
     if (j >= K) continue;
-    const T x = (k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc)[i];
+    const T x = col(k)[i];
     if (i < R) Gw[i + (int64_t)j * b.ldg] = x;
     else if (i >= Rp && i - Rp < K) Vw[i - Rp + (int64_t)j * b.ldv] = x;
   }
@@ -1196,18 +1315,24 @@ static cudaError_t set_tile_attrs_t() {
   if (e == cudaSuccess) e = set_tile_attrs_cs<8, T>();
   return e;
 }
-template <typename T, int RPL>
+template <typename T, int RH>
 static cudaError_t set_panel_attr() {
-  return cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024);
+  // clusters of 16 CTAs (non-portable; B200 allows them) for the largest blocks
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
 }
 template <typename T>
 static cudaError_t set_panel_attrs_t() {
-  cudaError_t e = set_panel_attr<T, 2>();
+  cudaError_t e = set_panel_attr<T, 1>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 2>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 3>();
   if (e == cudaSuccess) e = set_panel_attr<T, 4>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 5>();
   if (e == cudaSuccess) e = set_panel_attr<T, 6>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 8>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 12>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 7>();
   return e;
 }
 static PerDeviceOnce g_svd_attrs;
@@ -1225,13 +1350,14 @@ static cudaError_t ensure_svd_attrs() {
 
 // launch classes: svd_jacobi_kernel (log2 CS) x (shared memory, workspace): 0..7;
 // svd_jacobi_tile_kernel 8 + 6 log2 CS + index of RG in kTileRG: 8..31
-// svd_jacobi_panel_kernel 32 + 5 log2 CS + index of RPL in kPanelRPL: 32..51
-constexpr int kSvdClasses = 52;
-constexpr int kPanelRPL[5] = {2, 4, 6, 8, 12};
-static int panel_rpl_index(int rpl) {
-  for (int i = 0; i < 5; ++i)
-    if (kPanelRPL[i] == rpl) return i;
-  return 4;
+// svd_jacobi_panel_kernel 32 + 7 log2 CS + index of RH in kPanelRH: 32..66 (CS up to 16)
+constexpr int kSvdClasses = 67;
+constexpr int kPanelNRH = 7;
+constexpr int kPanelRH[kPanelNRH] = {1, 2, 3, 4, 5, 6, 7};
+static int panel_rpl_index(int rh) {
+  for (int i = 0; i < kPanelNRH; ++i)
+    if (kPanelRH[i] == rh) return i;
+  return kPanelNRH - 1;
 }
 constexpr int kTileRG[6] = {1, 2, 3, 4, 6, 8};
 static int tile_rg_index(int rg) {
@@ -1249,6 +1375,7 @@ struct SvdPlan {
   std::vector<int32_t> lists[kSvdClasses];
   int class_smem[kSvdClasses] = {};
   int class_threads[kSvdClasses] = {};
+  double class_t[kSvdClasses] = {};  // the longest estimated block time of the class (stream priority)
   DevBuf d_lists[kSvdClasses];
   size_t ws_bytes = 0, idx_off = 0;  // byte offset of the int32 index region
   int64_t n_sigma = 0, sig_base = 0;  // sigma region (doubles from the workspace base)
@@ -1334,30 +1461,32 @@ static PanelCand panel_cand(const SvdBlock& b, int cs, int es) {
   PanelCand c;
   if (b.K < 1 || b.K > 192) return c;
   const int Rp = (b.R + 31) & ~31, Kv = (b.K + 31) & ~31, Lc = Rp + Kv;
-  const int rt = Lc / 32;
-  int rpl = 0;
-  for (int x : kPanelRPL)
-    if (x >= rt) {
-      rpl = x;
+  const int rh_need = std::max(Rp, Kv) / 32;
+  int rh = 0;
+  for (int x : kPanelRH)
+    if (x >= rh_need) {
+      rh = x;
       break;
     }
-  if (!rpl) return c;
+  if (!rh) return c;
   const int m = (b.K + 2 * cs - 1) / (2 * cs);
-  const int maxw = (es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 32;
+  const int maxw = (es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 64;  // G-warps + V-warps
   if (m > maxw) return c;
-  if (cs > 1 && m < 1) return c;
   const int64_t bytes = panel_smem_bytes(m, Lc, cs, es);
   if (bytes > 227 * 1024) return c;
-  const double traffic = (double)m * Lc * es * 2 / 128.0;
-  const double t_in = 700.0 + 25.0 * m + traffic;
+  // cycles per round: ~900 of dependent chain (loads, dots, 32-lane reduction, rotation, update, barrier)
+  // plus ~(20 + 12 rows) per pair for the issue of the G- and V-warps; per move ~1500 + the two half-panels
+  // at ~30 B per cycle of DSMEM (fitted to B200 measurements of 181 x 181 at 8 and 16 CTAs: 2100 / 1550
+  // cycles per round, 4200 / 2800 per move)
+  const double t_in = 900.0 + m * (20.0 + 12.0 * rh * (es == 8 ? 1.0 : 2.0));
   const double P = 2.0 * cs;
-  double sweep = (2.0 * m - 1) * (t_in + 0.5 * traffic);
-  if (cs > 1) sweep += (P - 2) * m * t_in + (P - 1) * (1500.0 + 2.0 * m * Lc * es / 50.0);
+  double sweep = (2.0 * m) * t_in * 1.1;
+  if (cs > 1) sweep += (P - 2) * (m + 1) * t_in + (P - 1) * (1500.0 + 2.0 * m * Lc * es / 30.0);
   c.ok = true;
   c.m = m;
-  c.rpl = rpl;
+  c.rpl = rh;
   c.smem = (int)bytes;
-  c.threads = 32 * std::max(m, 2);
+  c.threads = 64 * std::max(m, 1);
   c.t = sweep;
   return c;
 }
@@ -1435,6 +1564,7 @@ static void assign_tile_blocks(SvdPlan& P, const std::vector<int>& tiles, int es
     while ((1 << l2cs) < b.cs) ++l2cs;
     const int cls = 8 + 6 * l2cs + tile_rg_index(b.rg);
     P.class_smem[cls] = std::max(P.class_smem[cls], c.smem);
+    P.class_t[cls] = std::max(P.class_t[cls], c.t);
   }
   std::sort(order.begin(), order.end());
   for (auto& o : order) {
@@ -1445,12 +1575,22 @@ static void assign_tile_blocks(SvdPlan& P, const std::vector<int>& tiles, int es
   }
 }
 
-// Panel-kernel blocks: every block takes its fastest cluster size, then the smallest one within the
-// longest block's time (fewer SMs for the same step time).
+// Panel-kernel blocks: the blocks run concurrently, so the SVD takes about max(longest block, total
+// CTA-time / SMs). Start from every block's fastest cluster size (bound Lb), give every block the
+// smallest cluster size that finishes within the target, and raise the target to the area bound while
+// that moves it (the largest blocks keep 8-16 CTAs, the many small ones 1-2).
 static void assign_panel_blocks(SvdPlan& P, const std::vector<int>& panels, int es) {
   if (panels.empty()) return;
   static const int force_cs = (int)knob("TK_SVD_PANEL_CS", 0);
-  const int css[4] = {1, 2, 4, 8};
+  static const int n_sm = [] {
+    int d = 0, n = 0;
+    if (cudaGetDevice(&d) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) == cudaSuccess &&
+        n > 0)
+      return n;
+    cudaGetLastError();
+    return 148;
+  }();
+  const int css[5] = {1, 2, 4, 8, 16};
   double Lb = 0.0;
   for (int i : panels) {
     double best = 1e300;
@@ -1460,43 +1600,61 @@ static void assign_panel_blocks(SvdPlan& P, const std::vector<int>& panels, int 
     }
     Lb = std::max(Lb, best);
   }
-  std::vector<std::pair<double, int>> order;
-  for (int i : panels) {
-    SvdBlock& b = P.blocks[i];
-    PanelCand pick;
-    for (int cs : css) {
-      const PanelCand c = panel_cand(b, cs, es);
-      if (c.ok && (force_cs ? cs == force_cs : c.t <= Lb * 1.0001)) {
-        pick = c;
-        b.cs = cs;
-        break;
-      }
-    }
-    if (!pick.ok) {
-      double best = 1e300;
+  std::vector<PanelCand> pick(panels.size());
+  std::vector<int> pick_cs(panels.size(), 1);
+  double target = Lb;
+  for (int it = 0; it < 8; ++it) {
+    double area = 0.0;
+    for (size_t k = 0; k < panels.size(); ++k) {
+      const SvdBlock& b = P.blocks[panels[k]];
+      PanelCand ch;
+      int chcs = 0;
       for (int cs : css) {
         const PanelCand c = panel_cand(b, cs, es);
-        if (c.ok && c.t < best) best = c.t, pick = c, b.cs = cs;
+        if (c.ok && (force_cs ? cs == force_cs : c.t <= target * 1.0001)) {
+          ch = c;
+          chcs = cs;
+          break;
+        }
       }
+      if (!ch.ok) {  // the fastest feasible
+        double best = 1e300;
+        for (int cs : css) {
+          const PanelCand c = panel_cand(b, cs, es);
+          if (c.ok && c.t < best) best = c.t, ch = c, chcs = cs;
+        }
+      }
+      pick[k] = ch;
+      pick_cs[k] = chcs;
+      area += chcs * ch.t;
     }
+    const double nt = std::max(Lb, area / n_sm);
+    if (force_cs || nt <= target * 1.01) break;
+    target = nt;
+  }
+  std::vector<std::pair<double, int>> order;
+  for (size_t k = 0; k < panels.size(); ++k) {
+    SvdBlock& b = P.blocks[panels[k]];
+    b.cs = pick_cs[k];
     b.tile = 2;
-    b.rg = pick.rpl;
-    b.Kl = pick.m;
-    b.Rl = pick.threads;
+    b.rg = pick[k].rpl;
+    b.Kl = pick[k].m;
+    b.Rl = pick[k].threads;
     b.smem = 1;
     int l2cs = 0;
     while ((1 << l2cs) < b.cs) ++l2cs;
-    const int cls = 32 + 5 * l2cs + panel_rpl_index(pick.rpl);
-    P.class_smem[cls] = std::max(P.class_smem[cls], pick.smem);
-    P.class_threads[cls] = std::max(P.class_threads[cls], pick.threads);
-    order.push_back({-pick.t, i});
+    const int cls = 32 + kPanelNRH * l2cs + panel_rpl_index(pick[k].rpl);
+    P.class_smem[cls] = std::max(P.class_smem[cls], pick[k].smem);
+    P.class_threads[cls] = std::max(P.class_threads[cls], pick[k].threads);
+    P.class_t[cls] = std::max(P.class_t[cls], pick[k].t);
+    order.push_back({-pick[k].t, panels[k]});
   }
   std::sort(order.begin(), order.end());
   for (auto& o : order) {
     const SvdBlock& b = P.blocks[o.second];
     int l2cs = 0;
     while ((1 << l2cs) < b.cs) ++l2cs;
-    P.lists[32 + 5 * l2cs + panel_rpl_index(b.rg)].push_back((int32_t)o.second);
+    P.lists[32 + kPanelNRH * l2cs + panel_rpl_index(b.rg)].push_back((int32_t)o.second);
   }
 }
 
@@ -1546,12 +1704,12 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     nidx += b.K;
     b.tile = 0;
     b.rg = 0;
-    if (panel_enabled && panel_cand(b, 8, es).ok) {  // decided below, over all blocks
+    if (panel_enabled && (panel_cand(b, 8, es).ok || panel_cand(b, 16, es).ok)) {  // decided below
       panels.push_back((int)P->blocks.size());
       P->blocks.push_back(b);
       continue;
     }
-    if (tile_enabled && tile_cand(b, 8, es).ok) {  // decided below, over all blocks
+    if (tile_enabled && tile_cand(b, 8, es).ok) {  // decided below, over all blocks (after the panel kernel)
       tiles.push_back((int)P->blocks.size());
       P->blocks.push_back(b);
       continue;
@@ -1591,6 +1749,7 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
       P->class_smem[cls] =
           std::max<int>(P->class_smem[cls], (int)(((int64_t)b.Rl + b.Kl) * b.K * es + 2 * b.cs * npairs * 32 + 32));
     P->lists[cls].push_back((int32_t)P->blocks.size());
+    P->class_t[cls] = 1e18;  // the blocks too large for the tile / panel kernels are the longest
     P->blocks.push_back(b);
   }
   assign_tile_blocks(*P, tiles, es);
@@ -1609,7 +1768,8 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     for (int c = 0; c < kSvdClasses; ++c)
       if (!P->lists[c].empty())
         if (c >= 32)
-          fprintf(stderr, " panel cs%d/rpl%d x%zu (smem %d B, %d threads)", 1 << ((c - 32) / 5), kPanelRPL[(c - 32) % 5],
+          fprintf(stderr, " panel cs%d/rh%d x%zu (smem %d B, %d threads)", 1 << ((c - 32) / kPanelNRH),
+                  kPanelRH[(c - 32) % kPanelNRH],
                   P->lists[c].size(), P->class_smem[c], P->class_threads[c]);
         else if (c < 8)
           fprintf(stderr, " cs%d/%s x%zu (smem %d B)", 1 << (c / 2), (c & 1) ? "ws" : "smem", P->lists[c].size(),
@@ -1648,13 +1808,23 @@ static cudaError_t launch_svd_class(const SvdPlan& P, int cls, void* ws, int32_t
 
 // Launch classes run concurrently: class 0 on the caller's stream, the others on library-private
 // streams forked from / joined to it with events (capturable: a CUDA graph gets the same fork-join).
-static cudaStream_t svd_aux_stream(int i) {
+// Library-private streams, per device, slot and priority level (0 = the device's greatest priority).
+// The SVD's launch classes run concurrently; the classes holding the longest blocks get the higher
+// priorities, so their clusters are placed first and the many small blocks backfill the SMs left over
+// (with equal priorities the small CTAs occupied the SMs an 8-CTA cluster needed and the longest block
+// started late).
+static cudaStream_t svd_aux_stream(int i, int level) {
   static std::mutex mu;
-  static std::map<std::pair<int, int>, cudaStream_t> st;
+  static std::map<std::tuple<int, int, int>, cudaStream_t> st;
   const int d = current_device();
   std::lock_guard<std::mutex> g(mu);
-  auto& s = st[{d, i}];
-  if (!s) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "svd stream");
+  auto& s = st[{d, i, level}];
+  if (!s) {
+    int least = 0, greatest = 0;
+    check_cuda(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
+    const int prio = std::min(least, greatest + level);  // greatest is numerically smallest
+    check_cuda(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio), "svd stream");
+  }
   return s;
 }
 
@@ -1694,9 +1864,9 @@ static cudaError_t launch_tile_cs(const SvdPlan& P, int cls, void* ws, int32_t* 
   }
 }
 
-template <typename T, int RPL>
+template <typename T, int RH>
 static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
-  const unsigned cs = 1u << ((cls - 32) / 5);
+  const unsigned cs = 1u << ((cls - 32) / kPanelNRH);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(P.lists[cls].size() * cs));
   cfg.blockDim = dim3((unsigned)P.class_threads[cls]);
@@ -1712,19 +1882,21 @@ static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32
   cfg.attrs = at;
   cfg.numAttrs = 2;
   static const int debug = std::getenv("TK_SVD_DEBUG") ? 1 : 0;  // diagnostic print only
-  return cudaLaunchKernelEx(&cfg, svd_jacobi_panel_kernel<T, RPL>, ws, idx, (const SvdBlock*)P.d_blocks.p,
+  return cudaLaunchKernelEx(&cfg, svd_jacobi_panel_kernel<T, RH>, ws, idx, (const SvdBlock*)P.d_blocks.p,
                             (const int32_t*)P.d_lists[cls].p, debug);
 }
 
 template <typename T>
 static cudaError_t launch_svd_cls(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
   if (cls >= 32) {
-    switch ((cls - 32) % 5) {
-      case 0: return launch_panel_class<T, 2>(P, cls, ws, idx, st);
-      case 1: return launch_panel_class<T, 4>(P, cls, ws, idx, st);
-      case 2: return launch_panel_class<T, 6>(P, cls, ws, idx, st);
-      case 3: return launch_panel_class<T, 8>(P, cls, ws, idx, st);
-      default: return launch_panel_class<T, 12>(P, cls, ws, idx, st);
+    switch ((cls - 32) % kPanelNRH) {
+      case 0: return launch_panel_class<T, 1>(P, cls, ws, idx, st);
+      case 1: return launch_panel_class<T, 2>(P, cls, ws, idx, st);
+      case 2: return launch_panel_class<T, 3>(P, cls, ws, idx, st);
+      case 3: return launch_panel_class<T, 4>(P, cls, ws, idx, st);
+      case 4: return launch_panel_class<T, 5>(P, cls, ws, idx, st);
+      case 5: return launch_panel_class<T, 6>(P, cls, ws, idx, st);
+      default: return launch_panel_class<T, 7>(P, cls, ws, idx, st);
     }
   }
   if (cls >= 8) {
@@ -1752,26 +1924,22 @@ static cudaError_t launch_svd_cls(const SvdPlan& P, int cls, void* ws, int32_t* 
 template <typename T>
 static void launch_svd_all(const SvdPlan& P, void* ws, int32_t* idx, cudaStream_t st) {
   std::vector<int> cl;
-  for (int c = kSvdClasses - 1; c >= 0; --c)  // largest clusters first (the longest blocks)
+  for (int c = kSvdClasses - 1; c >= 0; --c)
     if (!P.lists[c].empty()) cl.push_back(c);
   if (cl.empty()) return;
-  if (cl.size() == 1) {
-    check_cuda(launch_svd_cls<T>(P, cl[0], ws, idx, st), "svd launch");
-    add_launches(1);
-    return;
-  }
+  // longest classes first: they take the higher-priority streams
+  std::stable_sort(cl.begin(), cl.end(), [&](int a, int b) { return P.class_t[a] > P.class_t[b]; });
   cudaEvent_t fork = nullptr;
-  std::vector<cudaEvent_t> joins(cl.size() - 1, nullptr);
+  std::vector<cudaEvent_t> joins(cl.size(), nullptr);
   check_cuda(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "svd event");
   for (auto& e : joins) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "svd event");
   cudaError_t err = cudaEventRecord(fork, st);
-  for (size_t i = 1; i < cl.size() && err == cudaSuccess; ++i) {
-    cudaStream_t a = svd_aux_stream((int)i - 1);
+  for (size_t i = 0; i < cl.size() && err == cudaSuccess; ++i) {
+    cudaStream_t a = svd_aux_stream((int)i, std::min<int>((int)i, 5));
     err = cudaStreamWaitEvent(a, fork, 0);
     if (err == cudaSuccess) err = launch_svd_cls<T>(P, cl[i], ws, idx, a);
-    if (err == cudaSuccess) err = cudaEventRecord(joins[i - 1], a);
+    if (err == cudaSuccess) err = cudaEventRecord(joins[i], a);
   }
-  if (err == cudaSuccess) err = launch_svd_cls<T>(P, cl[0], ws, idx, st);
   for (auto& e : joins)
     if (err == cudaSuccess) err = cudaStreamWaitEvent(st, e, 0);
   cudaEventDestroy(fork);
