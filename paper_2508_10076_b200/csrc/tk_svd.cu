@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
   uint32_t mph = 0;
   int sweep = 0;
   T t[RH], u[RH];
+  int big = 0;  // a rotation of this sweep had a cosine above sqrt(tol)
 #ifdef TK_SVD_TIMERS
   long long pt[6] = {0, 0, 0, 0, 0, 0}, pts = 0, ptn = 0, pmv = 0;  // load, dots, reduce, rotation, update, barrier
 #define TK_PT(i) do { const long long _c = clock64(); pt[i] += _c - pts; pts = _c; } while (0)
@@ -954,6 +955,7 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
     TK_PT(2);
     const double ga2 = fma(gr, gr, gi * gi);
     const int doit = ga2 > tol2 * al * be && ga2 > 0.0;
+    if (doit && ga2 > tol * al * be) big = 1;  // cosine above sqrt(tol)
     if (!doit) {
       if (lane == 0) rflag[sl * m + pi] = 0;
       return 0;
@@ -1018,6 +1020,7 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
   auto col = [&](int k) -> T* { return k < m ? Tin + (size_t)k * Lc : Bcur + (size_t)(k - m) * Lc; };
   for (; sweep < kSvdMaxSweeps; ++sweep) {
     int any = 0;
+    big = 0;
     // ---- stage 0: circle tournament over the CTA's 2m columns (players k < m: T_in[k], else B_cur[k - m]);
     // the V-warps run one round behind (round 2m - 1 is theirs alone)
     {
@@ -1160,18 +1163,20 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
       }
     }
     // ---- convergence: OR over the cluster
-    const int cta_any = __syncthreads_or(any);
+    // Stop after a sweep without rotations, or after a sweep whose rotations all had cosines below
+    // sqrt(tol): each such rotation leaves its pair exactly orthogonal and perturbs the others by
+    // O(cosine^2) < tol, so the verification sweep the first rule needs (1 of ~12) is skipped.
+    const int cta_flag = (__syncthreads_or(any) ? 1 : 0) | (__syncthreads_or(big) ? 2 : 0);
+    int all = cta_flag;
     if (CS > 1) {
-      if (tid == 0) flag[0] = cta_any;
+      if (tid == 0) flag[0] = cta_flag;
       cluster_sync_all();
-      int all = 0;
+      all = 0;
       for (int c = 0; c < CS; ++c)
         all |= *reinterpret_cast<const int*>(map_rank(reinterpret_cast<const double*>(flag), (uint32_t)c));
       cluster_sync_all();  // flags read before anyone rewrites them
-      if (!all) break;
-    } else if (!cta_any) {
-      break;
     }
+    if (all != 3) break;
   }
   if (debug && tid == 0 && rank == 0) {
     printf("[tk svd panel] block %d: %d x %d, cluster %d, m %d, RH %d, %d sweeps\n", list[cluster_id_x()], R, K, CS, m,
