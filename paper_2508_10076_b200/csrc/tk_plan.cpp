@@ -1148,11 +1148,13 @@ static void build_contract_plan(const Tensor& A, const Tensor& B, const Tensor& 
     static const int small_k = (int)knob("TK_GEMM_SMALL_K", 128);
     bool isbig = g.M >= 96 && g.N >= 96 && g.K > small_k;
     int bm = isbig ? 128 : 64, bn = isbig ? 128 : 64;
-    // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that one wave of
-    // ~148 co-resident tiles covers a ~G x 12 rectangle and shares the A and B k-slices in L2
-    // (row-major order re-read all of B from DRAM once per tile-row).
-    static const int band = (int)knob("TK_GEMM_BAND", 12);
-    const int ntm = (g.M + bm - 1) / bm, ntn = (g.N + bn - 1) / bn, G = band;
+    // L2-friendly rasterisation: bands of G tile-rows, walked column by column, so that the ~148
+    // co-resident tiles share the A and B k-slices in L2 (row-major order re-read all of B from DRAM
+    // once per tile-row). Big tiles: G = 4, the measured DRAM minimum of the cfg4 GEMM (ncu, D_leg 384:
+    // 615 / 342 / 264 / 231 / 238 / 318 / 463 / 502 GB per launch at G = 1 / 2 / 3 / 4 / 6 / 12 / 24 / 48,
+    // the same 535 ms for every G -- the kernel is DMMA-bound either way); small tiles keep G = 12.
+    static const int band = (int)knob("TK_GEMM_BAND", 0);
+    const int ntm = (g.M + bm - 1) / bm, ntn = (g.N + bn - 1) / bn, G = band > 0 ? band : (isbig ? 4 : 12);
     for (int mb = 0; mb < ntm; mb += G)
       for (int nt = 0; nt < ntn; ++nt)
         for (int mt = mb; mt < std::min(ntm, mb + G); ++mt)
