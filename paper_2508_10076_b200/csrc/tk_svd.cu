@@ -58,8 +58,10 @@ struct SvdBlock {
   int32_t cs;       // CTAs per cluster
   int32_t smem;     // 1: the CTA's rows of G and V live in shared memory; 0: in the workspace
   int32_t Rl, Kl;   // rows of G / of V per CTA
-  int32_t tile;     // 1: svd_jacobi_tile_kernel (RG rows of G per lane and column), 0: svd_jacobi_kernel
-  int32_t rg;
+  int32_t tile;     // 2: svd_jacobi_panel_kernel, 1: svd_jacobi_tile_kernel, 0: svd_jacobi_kernel
+  int32_t rg;       // registers per lane (tile: rows of G; panel: rows per half of a column)
+  int32_t lp;       // panel: lanes per pair slot (32 or 16)
+  int32_t pad_;
 };
 
 struct SvdOut {     // extraction target of one block (canonical layouts of U, S, Vh)
@@ -838,6 +840,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // shared memory (one load + one store per warp and round). A lane holds rows lane + 32 t of a column
 // (RPL per lane): G rows first (padded to a multiple of 32), then V rows.
 constexpr int kPanelThreadsReal = 768, kPanelThreadsCplx = 768;
+constexpr int kPanelThreads16 = 384;  // two pair slots per warp: <= 12 slots, 168 registers per thread
 template <typename T>
 struct PanelCfg {
   static constexpr int threads = sizeof(T) == 8 ? kPanelThreadsReal : kPanelThreadsCplx;
@@ -880,8 +883,25 @@ __device__ __forceinline__ void jacobi_rot(double al, double be, double ag, doub
   s = copysign(2.0 * g * r, rho);
 }
 
-template <typename T, int RH>
-__global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
+// (a, b, c, d) summed over each group of LP lanes (LP = 32: the reduce-scatter butterfly; LP = 16: a
+// plain butterfly inside each half-warp, the fourth value only for ComplexF64)
+template <int LP, bool CPLX>
+__device__ __forceinline__ void group_sum4(double& a, double& b, double& c, double& d) {
+  if constexpr (LP == 32) {
+    warp_sum4(a, b, c, d);
+  } else {
+#pragma unroll
+    for (int o = LP / 2; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (CPLX) d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+  }
+}
+
+template <typename T, int RH, int LP>
+__global__ void __launch_bounds__(LP == 16 ? kPanelThreads16 : PanelCfg<T>::threads, 1)
     svd_jacobi_panel_kernel(void* __restrict__ wsv, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
                             const int32_t* __restrict__ list, int debug) {
   using N = SvNum<T>;
@@ -895,12 +915,17 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
   const int m = b.Kl;  // columns per half-panel
   const int P = 2 * CS;
   const int Rp = (R + 31) & ~31, Kv = (K + 31) & ~31, Lc = Rp + Kv;
-  // warps 0 .. m-1 (G-warps) rotate the G rows of pair slot `pi` and decide the rotations; warps m .. 2m-1
-  // (V-warps) apply each slot's rotation to its V rows one round later, off the critical path
-  const bool gw = warp < m, vw = warp >= m && warp < 2 * m;
-  const int pi = gw ? warp : warp - m;
-  const int rb = gw ? 0 : Rp;                   // first row of this warp's part of a column
-  const int nrow = gw ? (Rp >> 5) : (Kv >> 5);  // rows per lane (<= RH)
+  // LP lanes per pair slot (32 or 16: two slots per warp). Warps 0 .. GW-1 (G-warps) rotate the G rows of
+  // slot `pi` and decide the rotations; warps GW .. 2GW-1 (V-warps) apply each slot's rotation to its V
+  // rows one round later, off the critical path
+  constexpr int PPW = 32 / LP;
+  const int sub = lane / LP, ll = lane % LP;
+  const int GW = (m + PPW - 1) / PPW;
+  const bool gw = warp < GW, vw = warp >= GW && warp < 2 * GW;
+  const int pi = (gw ? warp : warp - GW) * PPW + sub;
+  const bool pact = pi < m;                        // the last warp's second slot may be empty
+  const int rb = gw ? 0 : Rp;                      // first row of this warp's part of a column
+  const int nrow = gw ? (Rp / LP) : (Kv / LP);     // rows per lane (<= RH)
   T* Tin = reinterpret_cast<T*>(svd_dyn);
   T* Tout = Tin + (size_t)m * Lc;
   T* Bcur = Tout + (size_t)m * Lc;
@@ -951,13 +976,13 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
         N::dot(t[r], u[r], gr, gi);
       }
     TK_PT(1);
-    warp_sum4(al, be, gr, gi);
+    group_sum4<LP, CPLX>(al, be, gr, gi);
     TK_PT(2);
     const double ga2 = fma(gr, gr, gi * gi);
     const int doit = ga2 > tol2 * al * be && ga2 > 0.0;
     if (doit && ga2 > tol * al * be) big = 1;  // cosine above sqrt(tol)
     if (!doit) {
-      if (lane == 0) rflag[sl * m + pi] = 0;
+      if (ll == 0 && pact) rflag[sl * m + pi] = 0;
       return 0;
     }
     double c, sn, q0, q1;
@@ -987,7 +1012,7 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
           u[r] = N::lin(sn, x, q1, y);
         }
     }
-    if (lane == 0) {
+    if (ll == 0 && pact) {
       double* rr = rot + (sl * m + pi) * 4;
       rr[0] = c;
       rr[1] = sn;
@@ -1027,43 +1052,43 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
       const int n2 = 2 * m;
       for (int r = 0; r < n2; ++r) {
         if (gw && r < n2 - 1) {
-          int p, q;
-          round_pair_fast(r, pi, n2, n2, p, q);
-          T* cp = col(p) + rb + lane;
-          T* cq = col(q) + rb + lane;
+          int p = 0, q = 0;
+          if (pact) round_pair_fast(r, pi, n2, n2, p, q);
+          T* cp = col(p) + rb + ll;
+          T* cq = col(q) + rb + ll;
 #pragma unroll
           for (int k = 0; k < RH; ++k)
             if (k < nrow) {
-              t[k] = cp[32 * k];
-              u[k] = cq[32 * k];
+              t[k] = pact ? cp[LP * k] : N::zero();
+              u[k] = pact ? cq[LP * k] : N::zero();
             }
-          if (g_rotate(r & 1)) {
+          if (g_rotate(r & 1)) {  // (an empty slot never rotates: its data are zero)
             any = 1;
 #pragma unroll
             for (int k = 0; k < RH; ++k)
               if (k < nrow) {
-                cp[32 * k] = t[k];
-                cq[32 * k] = u[k];
+                cp[LP * k] = t[k];
+                cq[LP * k] = u[k];
               }
           }
-        } else if (vw && r >= 1) {
+        } else if (vw && r >= 1 && pact) {
           int p, q;
           round_pair_fast(r - 1, pi, n2, n2, p, q);
-          T* cp = col(p) + rb + lane;
-          T* cq = col(q) + rb + lane;
+          T* cp = col(p) + rb + ll;
+          T* cq = col(q) + rb + ll;
           if (rflag[((r - 1) & 1) * m + pi]) {
 #pragma unroll
             for (int k = 0; k < RH; ++k)
               if (k < nrow) {
-                t[k] = cp[32 * k];
-                u[k] = cq[32 * k];
+                t[k] = cp[LP * k];
+                u[k] = cq[LP * k];
               }
             v_rotate((r - 1) & 1);
 #pragma unroll
             for (int k = 0; k < RH; ++k)
               if (k < nrow) {
-                cp[32 * k] = t[k];
-                cq[32 * k] = u[k];
+                cp[LP * k] = t[k];
+                cq[LP * k] = u[k];
               }
           }
         }
@@ -1072,19 +1097,19 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
     }
     // ---- outer rounds: move, then all m^2 pairs (T_c[i], B_c[(i + s) mod m]); the V-warps one round behind
     if (CS > 1) {
-      if (gw || vw) {
+      if ((gw || vw) && pact) {
 #pragma unroll
         for (int k = 0; k < RH; ++k)
-          if (k < nrow) t[k] = Tin[(size_t)pi * Lc + rb + lane + 32 * k];
+          if (k < nrow) t[k] = Tin[(size_t)pi * Lc + rb + ll + LP * k];
       }
       for (int o = 1; o < P; ++o) {
 #ifdef TK_SVD_TIMERS
         long long tmv = clock64();
 #endif
-        if (gw || vw) {
+        if ((gw || vw) && pact) {
 #pragma unroll
           for (int k = 0; k < RH; ++k)
-            if (k < nrow) Tout[(size_t)pi * Lc + rb + lane + 32 * k] = t[k];
+            if (k < nrow) Tout[(size_t)pi * Lc + rb + ll + LP * k] = t[k];
         }
         fence_proxy_async_smem();
         __syncthreads();
@@ -1116,10 +1141,10 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
           Bcur = Bin;
           Bin = x;
         }
-        if (gw || vw) {
+        if ((gw || vw) && pact) {
 #pragma unroll
           for (int k = 0; k < RH; ++k)
-            if (k < nrow) t[k] = Tin[(size_t)pi * Lc + rb + lane + 32 * k];
+            if (k < nrow) t[k] = Tin[(size_t)pi * Lc + rb + ll + LP * k];
         }
 #ifdef TK_SVD_TIMERS
         pt[0] += clock64() - tmv;
@@ -1132,27 +1157,30 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
             pts = clock64();
             ++ptn;
 #endif
-            T* cq = Bcur + (size_t)((pi + s2) % m) * Lc + lane;
+            T* cq = Bcur + (size_t)((pi + s2) % m) * Lc + ll;
 #pragma unroll
             for (int k = 0; k < RH; ++k)
-              if (k < nrow) u[k] = cq[32 * k];
+              if (k < nrow) {
+                u[k] = pact ? cq[LP * k] : N::zero();
+                if (!pact) t[k] = N::zero();
+              }
             if (g_rotate(s2 & 1)) {
               any = 1;
 #pragma unroll
               for (int k = 0; k < RH; ++k)
-                if (k < nrow) cq[32 * k] = u[k];
+                if (k < nrow) cq[LP * k] = u[k];
             }
             TK_PT(4);
-          } else if (vw && s2 >= 1) {
+          } else if (vw && s2 >= 1 && pact) {
             if (rflag[((s2 - 1) & 1) * m + pi]) {
-              T* cq = Bcur + (size_t)((pi + s2 - 1) % m) * Lc + Rp + lane;
+              T* cq = Bcur + (size_t)((pi + s2 - 1) % m) * Lc + Rp + ll;
 #pragma unroll
               for (int k = 0; k < RH; ++k)
-                if (k < nrow) u[k] = cq[32 * k];
+                if (k < nrow) u[k] = cq[LP * k];
               v_rotate((s2 - 1) & 1);
 #pragma unroll
               for (int k = 0; k < RH; ++k)
-                if (k < nrow) cq[32 * k] = u[k];
+                if (k < nrow) cq[LP * k] = u[k];
             }
           }
           __syncthreads();
@@ -1179,8 +1207,8 @@ __global__ void __launch_bounds__(PanelCfg<T>::threads, 1)
     if (all != 3) break;
   }
   if (debug && tid == 0 && rank == 0) {
-    printf("[tk svd panel] block %d: %d x %d, cluster %d, m %d, RH %d, %d sweeps\n", list[cluster_id_x()], R, K, CS, m,
-           RH, sweep + 1);
+    printf("[tk svd panel] block %d: %d x %d, cluster %d, m %d, RH %d, LP %d, %d sweeps\n", list[cluster_id_x()], R, K,
+           CS, m, RH, LP, sweep + 1);
 #ifdef TK_SVD_TIMERS
     if (ptn)
       printf("[tk svd panel] outer-round cycles per round: load+dots %lld reduce %lld rotation %lld update %lld barrier %lld\n",
@@ -1320,24 +1348,33 @@ static cudaError_t set_tile_attrs_t() {
   if (e == cudaSuccess) e = set_tile_attrs_cs<8, T>();
   return e;
 }
-template <typename T, int RH>
+template <typename T, int RH, int LP>
 static cudaError_t set_panel_attr() {
-  cudaError_t e = cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RH, LP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024);
   // clusters of 16 CTAs (non-portable; B200 allows them) for the largest blocks
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(svd_jacobi_panel_kernel<T, RH, LP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 template <typename T>
 static cudaError_t set_panel_attrs_t() {
-  cudaError_t e = set_panel_attr<T, 1>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 2>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 3>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 4>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 5>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 6>();
-  if (e == cudaSuccess) e = set_panel_attr<T, 7>();
+  cudaError_t e = set_panel_attr<T, 1, 32>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 2, 32>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 3, 32>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 4, 32>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 5, 32>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 6, 32>();
+  if (e == cudaSuccess) e = set_panel_attr<T, 7, 32>();
+  if constexpr (sizeof(T) == 8) {
+    if (e == cudaSuccess) e = set_panel_attr<T, 2, 16>();
+    if (e == cudaSuccess) e = set_panel_attr<T, 4, 16>();
+    if (e == cudaSuccess) e = set_panel_attr<T, 6, 16>();
+    if (e == cudaSuccess) e = set_panel_attr<T, 8, 16>();
+    if (e == cudaSuccess) e = set_panel_attr<T, 10, 16>();
+    if (e == cudaSuccess) e = set_panel_attr<T, 12, 16>();
+    if (e == cudaSuccess) e = set_panel_attr<T, 14, 16>();
+  }
   return e;
 }
 static PerDeviceOnce g_svd_attrs;
@@ -1355,14 +1392,21 @@ static cudaError_t ensure_svd_attrs() {
 
 // launch classes: svd_jacobi_kernel (log2 CS) x (shared memory, workspace): 0..7;
 // svd_jacobi_tile_kernel 8 + 6 log2 CS + index of RG in kTileRG: 8..31
-// svd_jacobi_panel_kernel 32 + 7 log2 CS + index of RH in kPanelRH: 32..66 (CS up to 16)
-constexpr int kSvdClasses = 67;
+// svd_jacobi_panel_kernel, 32 lanes per pair: 32 + 7 log2 CS + index of RH in kPanelRH (32..66);
+// 16 lanes per pair (two pair slots per warp): 67 + 7 log2 CS + index of RH in kPanelRH16 (67..101)
+constexpr int kSvdClasses = 102;
 constexpr int kPanelNRH = 7;
 constexpr int kPanelRH[kPanelNRH] = {1, 2, 3, 4, 5, 6, 7};
-static int panel_rpl_index(int rh) {
+constexpr int kPanelRH16[kPanelNRH] = {2, 4, 6, 8, 10, 12, 14};
+static int panel_rpl_index(int rh, int lp = 32) {
   for (int i = 0; i < kPanelNRH; ++i)
-    if (kPanelRH[i] == rh) return i;
+    if ((lp == 32 ? kPanelRH[i] : kPanelRH16[i]) == rh) return i;
   return kPanelNRH - 1;
+}
+static int panel_class(int cs, int rh, int lp) {
+  int l2cs = 0;
+  while ((1 << l2cs) < cs) ++l2cs;
+  return (lp == 32 ? 32 : 67) + kPanelNRH * l2cs + panel_rpl_index(rh, lp);
 }
 constexpr int kTileRG[6] = {1, 2, 3, 4, 6, 8};
 static int tile_rg_index(int rg) {
@@ -1459,39 +1503,47 @@ static TileCand tile_cand(const SvdBlock& b, int cs, int es) {
 // half-panels over DSMEM (~1500 cycles + bytes at ~50 B per cycle).
 struct PanelCand {
   bool ok = false;
-  int m = 0, rpl = 0, smem = 0, threads = 0;
+  int m = 0, rpl = 0, lp = 32, smem = 0, threads = 0;
   double t = 0.0;
 };
 static PanelCand panel_cand(const SvdBlock& b, int cs, int es) {
   PanelCand c;
   if (b.K < 1 || b.K > 192) return c;
+  static const int lp_knob = (int)knob("TK_SVD_LP", 16);
+  const int lp = es == 8 ? lp_knob : 32;  // two pair slots per warp (Float64)
   const int Rp = (b.R + 31) & ~31, Kv = (b.K + 31) & ~31, Lc = Rp + Kv;
-  const int rh_need = std::max(Rp, Kv) / 32;
+  const int rh_need = std::max(Rp, Kv) / lp;
   int rh = 0;
-  for (int x : kPanelRH)
+  for (int i = 0; i < kPanelNRH; ++i) {
+    const int x = lp == 32 ? kPanelRH[i] : kPanelRH16[i];
     if (x >= rh_need) {
       rh = x;
       break;
     }
+  }
   if (!rh) return c;
   const int m = (b.K + 2 * cs - 1) / (2 * cs);
-  const int maxw = (es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 64;  // G-warps + V-warps
-  if (m > maxw) return c;
+  const int ppw = 32 / lp;
+  const int gw = (m + ppw - 1) / ppw;
+  const int maxw = (lp == 16 ? kPanelThreads16 : es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 64;
+  if (gw > maxw) return c;  // (G-warps + V-warps)
   const int64_t bytes = panel_smem_bytes(m, Lc, cs, es);
   if (bytes > 227 * 1024) return c;
-  // cycles per round: ~900 of dependent chain (loads, dots, 32-lane reduction, rotation, update, barrier)
-  // plus ~(20 + 12 rows) per pair for the issue of the G- and V-warps; per move ~1500 + the two half-panels
-  // at ~30 B per cycle of DSMEM (fitted to B200 measurements of 181 x 181 at 8 and 16 CTAs: 2100 / 1550
-  // cycles per round, 4200 / 2800 per move)
-  const double t_in = 900.0 + m * (20.0 + 12.0 * rh * (es == 8 ? 1.0 : 2.0));
+  // cycles per round: ~900 of dependent chain (loads, dots, reduction, rotation, update, barrier) plus
+  // ~(20 + 12 rows) per pair for the issue of the G- and V-warps; per move ~1500 + the two half-panels at
+  // ~30 B per cycle of DSMEM (fitted to B200 measurements of 181 x 181 at 8 and 16 CTAs, 32 lanes per
+  // pair: 2100 / 1550 cycles per round, 4200 / 2800 per move)
+  const int rows = std::max(Rp, Kv) / 32;
+  const double t_in = 900.0 + m * (20.0 * 32 / lp + 12.0 * rows * (es == 8 ? 1.0 : 2.0));
   const double P = 2.0 * cs;
   double sweep = (2.0 * m) * t_in * 1.1;
   if (cs > 1) sweep += (P - 2) * (m + 1) * t_in + (P - 1) * (1500.0 + 2.0 * m * Lc * es / 30.0);
   c.ok = true;
   c.m = m;
   c.rpl = rh;
+  c.lp = lp;
   c.smem = (int)bytes;
-  c.threads = 64 * std::max(m, 1);
+  c.threads = 64 * gw;
   c.t = sweep;
   return c;
 }
@@ -1643,12 +1695,11 @@ static void assign_panel_blocks(SvdPlan& P, const std::vector<int>& panels, int 
     b.cs = pick_cs[k];
     b.tile = 2;
     b.rg = pick[k].rpl;
+    b.lp = pick[k].lp;
     b.Kl = pick[k].m;
-    b.Rl = pick[k].threads;
+    b.Rl = pick[k].threads;  // (not read by the kernel: blockDim)
     b.smem = 1;
-    int l2cs = 0;
-    while ((1 << l2cs) < b.cs) ++l2cs;
-    const int cls = 32 + kPanelNRH * l2cs + panel_rpl_index(pick[k].rpl);
+    const int cls = panel_class(b.cs, b.rg, b.lp);
     P.class_smem[cls] = std::max(P.class_smem[cls], pick[k].smem);
     P.class_threads[cls] = std::max(P.class_threads[cls], pick[k].threads);
     P.class_t[cls] = std::max(P.class_t[cls], pick[k].t);
@@ -1657,9 +1708,7 @@ static void assign_panel_blocks(SvdPlan& P, const std::vector<int>& panels, int 
   std::sort(order.begin(), order.end());
   for (auto& o : order) {
     const SvdBlock& b = P.blocks[o.second];
-    int l2cs = 0;
-    while ((1 << l2cs) < b.cs) ++l2cs;
-    P.lists[32 + kPanelNRH * l2cs + panel_rpl_index(b.rg)].push_back((int32_t)o.second);
+    P.lists[panel_class(b.cs, b.rg, b.lp)].push_back((int32_t)o.second);
   }
 }
 
@@ -1772,7 +1821,10 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     fprintf(stderr, "[tk svd] %zu blocks:", P->blocks.size());
     for (int c = 0; c < kSvdClasses; ++c)
       if (!P->lists[c].empty())
-        if (c >= 32)
+        if (c >= 67)
+          fprintf(stderr, " panel16 cs%d/rh%d x%zu (smem %d B, %d threads)", 1 << ((c - 67) / kPanelNRH),
+                  kPanelRH16[(c - 67) % kPanelNRH], P->lists[c].size(), P->class_smem[c], P->class_threads[c]);
+        else if (c >= 32)
           fprintf(stderr, " panel cs%d/rh%d x%zu (smem %d B, %d threads)", 1 << ((c - 32) / kPanelNRH),
                   kPanelRH[(c - 32) % kPanelNRH],
                   P->lists[c].size(), P->class_smem[c], P->class_threads[c]);
@@ -1869,9 +1921,9 @@ static cudaError_t launch_tile_cs(const SvdPlan& P, int cls, void* ws, int32_t* 
   }
 }
 
-template <typename T, int RH>
+template <typename T, int RH, int LP>
 static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
-  const unsigned cs = 1u << ((cls - 32) / kPanelNRH);
+  const unsigned cs = 1u << ((cls - (LP == 32 ? 32 : 67)) / kPanelNRH);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(P.lists[cls].size() * cs));
   cfg.blockDim = dim3((unsigned)P.class_threads[cls]);
@@ -1887,21 +1939,35 @@ static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32
   cfg.attrs = at;
   cfg.numAttrs = 2;
   static const int debug = std::getenv("TK_SVD_DEBUG") ? 1 : 0;  // diagnostic print only
-  return cudaLaunchKernelEx(&cfg, svd_jacobi_panel_kernel<T, RH>, ws, idx, (const SvdBlock*)P.d_blocks.p,
+  return cudaLaunchKernelEx(&cfg, svd_jacobi_panel_kernel<T, RH, LP>, ws, idx, (const SvdBlock*)P.d_blocks.p,
                             (const int32_t*)P.d_lists[cls].p, debug);
 }
 
 template <typename T>
 static cudaError_t launch_svd_cls(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
+  if (cls >= 67) {
+    if constexpr (sizeof(T) == 8) {
+      switch ((cls - 67) % kPanelNRH) {
+        case 0: return launch_panel_class<T, 2, 16>(P, cls, ws, idx, st);
+        case 1: return launch_panel_class<T, 4, 16>(P, cls, ws, idx, st);
+        case 2: return launch_panel_class<T, 6, 16>(P, cls, ws, idx, st);
+        case 3: return launch_panel_class<T, 8, 16>(P, cls, ws, idx, st);
+        case 4: return launch_panel_class<T, 10, 16>(P, cls, ws, idx, st);
+        case 5: return launch_panel_class<T, 12, 16>(P, cls, ws, idx, st);
+        default: return launch_panel_class<T, 14, 16>(P, cls, ws, idx, st);
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
   if (cls >= 32) {
     switch ((cls - 32) % kPanelNRH) {
-      case 0: return launch_panel_class<T, 1>(P, cls, ws, idx, st);
-      case 1: return launch_panel_class<T, 2>(P, cls, ws, idx, st);
-      case 2: return launch_panel_class<T, 3>(P, cls, ws, idx, st);
-      case 3: return launch_panel_class<T, 4>(P, cls, ws, idx, st);
-      case 4: return launch_panel_class<T, 5>(P, cls, ws, idx, st);
-      case 5: return launch_panel_class<T, 6>(P, cls, ws, idx, st);
-      default: return launch_panel_class<T, 7>(P, cls, ws, idx, st);
+      case 0: return launch_panel_class<T, 1, 32>(P, cls, ws, idx, st);
+      case 1: return launch_panel_class<T, 2, 32>(P, cls, ws, idx, st);
+      case 2: return launch_panel_class<T, 3, 32>(P, cls, ws, idx, st);
+      case 3: return launch_panel_class<T, 4, 32>(P, cls, ws, idx, st);
+      case 4: return launch_panel_class<T, 5, 32>(P, cls, ws, idx, st);
+      case 5: return launch_panel_class<T, 6, 32>(P, cls, ws, idx, st);
+      default: return launch_panel_class<T, 7, 32>(P, cls, ws, idx, st);
     }
   }
   if (cls >= 8) {
