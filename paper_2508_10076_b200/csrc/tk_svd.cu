@@ -841,7 +841,6 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 // (RPL per lane): G rows first (padded to a multiple of 32), then V rows.
 constexpr int kPanelThreadsReal = 768, kPanelThreadsCplx = 768;
 constexpr int kPanelThreads16 = 384;  // two pair slots per warp: <= 12 slots, 168 registers per thread
-constexpr int kPanelThreads8 = 256;   // four pair slots per warp: <= 16 slots, 255 registers per thread
 template <typename T>
 struct PanelCfg {
   static constexpr int threads = sizeof(T) == 8 ? kPanelThreadsReal : kPanelThreadsCplx;
@@ -902,7 +901,7 @@ __device__ __forceinline__ void group_sum4(double& a, double& b, double& c, doub
 }
 
 template <typename T, int RH, int LP>
-__global__ void __launch_bounds__(LP == 8 ? kPanelThreads8 : LP == 16 ? kPanelThreads16 : PanelCfg<T>::threads, 1)
+__global__ void __launch_bounds__(LP == 16 ? kPanelThreads16 : PanelCfg<T>::threads, 1)
     svd_jacobi_panel_kernel(void* __restrict__ wsv, int32_t* __restrict__ idx, const SvdBlock* __restrict__ blocks,
                             const int32_t* __restrict__ list, int debug) {
   using N = SvNum<T>;
@@ -1375,13 +1374,6 @@ static cudaError_t set_panel_attrs_t() {
     if (e == cudaSuccess) e = set_panel_attr<T, 10, 16>();
     if (e == cudaSuccess) e = set_panel_attr<T, 12, 16>();
     if (e == cudaSuccess) e = set_panel_attr<T, 14, 16>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 4, 8>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 8, 8>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 12, 8>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 16, 8>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 20, 8>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 24, 8>();
-    if (e == cudaSuccess) e = set_panel_attr<T, 28, 8>();
   }
   return e;
 }
@@ -1401,23 +1393,20 @@ static cudaError_t ensure_svd_attrs() {
 // launch classes: svd_jacobi_kernel (log2 CS) x (shared memory, workspace): 0..7;
 // svd_jacobi_tile_kernel 8 + 6 log2 CS + index of RG in kTileRG: 8..31
 // svd_jacobi_panel_kernel, 32 lanes per pair: 32 + 7 log2 CS + index of RH in kPanelRH (32..66);
-// 16 lanes per pair (two pair slots per warp): 67 + 7 log2 CS + index of RH in kPanelRH16 (67..101);
-// 8 lanes per pair (four slots per warp): 102 + 7 log2 CS + index of RH in kPanelRH8 (102..136)
-constexpr int kSvdClasses = 137;
+// 16 lanes per pair (two pair slots per warp): 67 + 7 log2 CS + index of RH in kPanelRH16 (67..101)
+constexpr int kSvdClasses = 102;
 constexpr int kPanelNRH = 7;
 constexpr int kPanelRH[kPanelNRH] = {1, 2, 3, 4, 5, 6, 7};
 constexpr int kPanelRH16[kPanelNRH] = {2, 4, 6, 8, 10, 12, 14};
-constexpr int kPanelRH8[kPanelNRH] = {4, 8, 12, 16, 20, 24, 28};
-static int panel_rh(int lp, int i) { return lp == 32 ? kPanelRH[i] : lp == 16 ? kPanelRH16[i] : kPanelRH8[i]; }
 static int panel_rpl_index(int rh, int lp = 32) {
   for (int i = 0; i < kPanelNRH; ++i)
-    if (panel_rh(lp, i) == rh) return i;
+    if ((lp == 32 ? kPanelRH[i] : kPanelRH16[i]) == rh) return i;
   return kPanelNRH - 1;
 }
 static int panel_class(int cs, int rh, int lp) {
   int l2cs = 0;
   while ((1 << l2cs) < cs) ++l2cs;
-  return (lp == 32 ? 32 : lp == 16 ? 67 : 102) + kPanelNRH * l2cs + panel_rpl_index(rh, lp);
+  return (lp == 32 ? 32 : 67) + kPanelNRH * l2cs + panel_rpl_index(rh, lp);
 }
 constexpr int kTileRG[6] = {1, 2, 3, 4, 6, 8};
 static int tile_rg_index(int rg) {
@@ -1526,7 +1515,7 @@ static PanelCand panel_cand(const SvdBlock& b, int cs, int es) {
   const int rh_need = std::max(Rp, Kv) / lp;
   int rh = 0;
   for (int i = 0; i < kPanelNRH; ++i) {
-    const int x = panel_rh(lp, i);
+    const int x = lp == 32 ? kPanelRH[i] : kPanelRH16[i];
     if (x >= rh_need) {
       rh = x;
       break;
@@ -1536,7 +1525,7 @@ static PanelCand panel_cand(const SvdBlock& b, int cs, int es) {
   const int m = (b.K + 2 * cs - 1) / (2 * cs);
   const int ppw = 32 / lp;
   const int gw = (m + ppw - 1) / ppw;
-  const int maxw = (lp == 8 ? kPanelThreads8 : lp == 16 ? kPanelThreads16 : es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 64;
+  const int maxw = (lp == 16 ? kPanelThreads16 : es == 8 ? kPanelThreadsReal : kPanelThreadsCplx) / 64;
   if (gw > maxw) return c;  // (G-warps + V-warps)
   const int64_t bytes = panel_smem_bytes(m, Lc, cs, es);
   if (bytes > 227 * 1024) return c;
@@ -1832,10 +1821,7 @@ static std::shared_ptr<SvdPlan> build_svd_plan(const Tensor& A, const std::vecto
     fprintf(stderr, "[tk svd] %zu blocks:", P->blocks.size());
     for (int c = 0; c < kSvdClasses; ++c)
       if (!P->lists[c].empty())
-        if (c >= 102)
-          fprintf(stderr, " panel8 cs%d/rh%d x%zu (smem %d B, %d threads)", 1 << ((c - 102) / kPanelNRH),
-                  kPanelRH8[(c - 102) % kPanelNRH], P->lists[c].size(), P->class_smem[c], P->class_threads[c]);
-        else if (c >= 67)
+        if (c >= 67)
           fprintf(stderr, " panel16 cs%d/rh%d x%zu (smem %d B, %d threads)", 1 << ((c - 67) / kPanelNRH),
                   kPanelRH16[(c - 67) % kPanelNRH], P->lists[c].size(), P->class_smem[c], P->class_threads[c]);
         else if (c >= 32)
@@ -1937,7 +1923,7 @@ static cudaError_t launch_tile_cs(const SvdPlan& P, int cls, void* ws, int32_t* 
 
 template <typename T, int RH, int LP>
 static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
-  const unsigned cs = 1u << ((cls - (LP == 32 ? 32 : LP == 16 ? 67 : 102)) / kPanelNRH);
+  const unsigned cs = 1u << ((cls - (LP == 32 ? 32 : 67)) / kPanelNRH);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(P.lists[cls].size() * cs));
   cfg.blockDim = dim3((unsigned)P.class_threads[cls]);
@@ -1959,20 +1945,6 @@ static cudaError_t launch_panel_class(const SvdPlan& P, int cls, void* ws, int32
 
 template <typename T>
 static cudaError_t launch_svd_cls(const SvdPlan& P, int cls, void* ws, int32_t* idx, cudaStream_t st) {
-  if (cls >= 102) {
-    if constexpr (sizeof(T) == 8) {
-      switch ((cls - 102) % kPanelNRH) {
-        case 0: return launch_panel_class<T, 4, 8>(P, cls, ws, idx, st);
-        case 1: return launch_panel_class<T, 8, 8>(P, cls, ws, idx, st);
-        case 2: return launch_panel_class<T, 12, 8>(P, cls, ws, idx, st);
-        case 3: return launch_panel_class<T, 16, 8>(P, cls, ws, idx, st);
-        case 4: return launch_panel_class<T, 20, 8>(P, cls, ws, idx, st);
-        case 5: return launch_panel_class<T, 24, 8>(P, cls, ws, idx, st);
-        default: return launch_panel_class<T, 28, 8>(P, cls, ws, idx, st);
-      }
-    }
-    return cudaErrorInvalidValue;
-  }
   if (cls >= 67) {
     if constexpr (sizeof(T) == 8) {
       switch ((cls - 67) % kPanelNRH) {
