@@ -20,6 +20,9 @@ einsum in float64 (fermions: a dense Alg. 4 with Koszul signs). Modules:
   planar      planar (cyclic) transposes on tree pairs for anyons (Fib, Ising) with no dense
               embedding; pinned against the dense SU(2) oracle and by pentagon / unitarity / rotation
 
-Parity status per function is listed in DESIGN.md §Oracle; the fermionic sign
-convention beyond the pins of reading C13 is "parity unpinned".
+Parity status per function is listed in DESIGN.md §Oracle. The paper prints no fermionic
+example; beyond the pins of reading C13 the fermionic convention is pinned by SVect's tensor
+product of even maps (= Kronecker) and by the Jordan-Wigner hopping matrices
+(tests/test_oracle_fermion_physics.py); the anyon factors by quantum traces
+(tests/test_oracle_anyon_dims.py).
 """
