@@ -42,6 +42,7 @@ constexpr int kFusedMaxMid = 64;    // T elements per fiber
 constexpr int kFusedMaxCoef = 1024; // coefficient entries per class (shared-memory doubles per warp)
 
 // A class program, in 8-byte words: header | ins[n_in] | t1[n_t1] | t2[n_t2] | outs[n_out] | midref[] | coef[]
+// (everything between the header and coef[] is staged in shared memory by the kernel)
 struct FusedHeader {
   int32_t F, nrl, n_in, n_t1, n_t2, n_mid, n_ref, n_coef1, n_coef;
   int32_t n_out;
@@ -74,22 +75,27 @@ __device__ __forceinline__ void fused_cp8(double* smem, const double* gmem) {
 }
 
 // One warp per chunk of <= 32 fibers of one class (many classes are smaller than a CTA); 4 independent
-// warps per CTA. Per warp: the class's coefficients are resolved once into shared memory (W value, sign,
-// alpha for step 2 without an output permute: exactly the B~ value the gathered GEMM forms), each K x N
-// table stored as K rows of NM (zero-padded, 16-byte aligned: read as double2 broadcasts). Per thread (one
-// fiber): for each step-1 row tree, its K inputs are loaded into registers and its N T values go to shared
-// memory ([slot][thread], conflict-free); then each step-2 row tree reads its K T values and writes its N
-// outputs (through the output permute's map when step 2 has one). Every product is the gathered GEMM's
-// own: acc_n = fma(+-a_k, b~_kn, acc_n) over k ascending, zeros included, so the fused result is bitwise
-// that of the two tk_contract calls. NM (4 / 8 / 16) bounds K and N of both steps.
-// (Measured alternatives, cfg3: all inputs fetched up front by cp.async and T values recomputed where
-// consumed, 101 us; two fibers per thread, 86 us; next tree's inputs prefetched, 89 us; this, 77-90 us
-// against 2 x 42 us for the two gathered steps -- see DESIGN.md §6.4.)
+// warps per CTA. Per warp, BEFORE griddepcontrol.wait (plan data only): the class program (input table,
+// row trees, output maps, T-value references) is copied into the warp's shared memory in one batch of
+// independent loads, and the class's coefficients are resolved into shared memory (W value, sign, alpha
+// for step 2 without an output permute: exactly the B~ value the gathered GEMM forms), each K x N table
+// stored as K rows of NM (zero-padded, 16-byte aligned: read as double2 broadcasts). After the wait the
+// only global loads are the fiber's T1 inputs: per step-1 row tree its K inputs (loaded together), its N
+// T values to shared memory
+// ([slot][thread], conflict-free); then each step-2 row tree reads its K T values and writes its N outputs
+// (through the output permute's map when step 2 has one). Every product is the gathered GEMM's own:
+// acc_n = fma(+-a_k, b~_kn, acc_n) over k ascending from zero, zeros included, so the fused result is
+// bitwise that of the two tk_contract calls. NM (4 / 8 / 16) bounds K and N of both steps.
+// (Measured alternatives, cfg3: all inputs fetched by cp.async and T values recomputed where consumed,
+// 101 us; two fibers per thread, 86 us; next tree's inputs prefetched, 89 us; program read from global
+// memory, one dependent load chain per row tree, 77-90 us; program staged and all of a fiber's inputs
+// issued at once (registers), 12 us slower than per tree -- see DESIGN.md §6.4.)
 template <int NM>
 __global__ void __launch_bounds__(kFusedThreads)
     fused_pair_kernel(const double* __restrict__ T1, const double* __restrict__ W1, const double* __restrict__ W2,
                       double* __restrict__ C, const int64_t* __restrict__ progs, const FusedChunk* __restrict__ chunks,
-                      int nchunks, int max_mid, int max_coef, double calpha, double oalpha, double beta) {
+                      int nchunks, int max_mid, int max_coef, int max_stage, double calpha, double oalpha,
+                      double beta) {
   extern __shared__ __align__(16) double fsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
@@ -105,15 +111,22 @@ __global__ void __launch_bounds__(kFusedThreads)
 #pragma unroll
     for (int i = 0; i < 4; ++i) h4[i] = __ldg(p4 + i);
   }
-  const int4* ins = reinterpret_cast<const int4*>(prog + 8);
-  const int4* t1 = reinterpret_cast<const int4*>(prog + 8 + 2 * h.n_in);
-  const FusedT2* t2 = reinterpret_cast<const FusedT2*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1);
-  const GatherOut* outs = reinterpret_cast<const GatherOut*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2);
-  const int32_t* midref =
-      reinterpret_cast<const int32_t*>(prog + 8 + 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2 + 4 * h.n_out);
-  const int32_t* coefs = midref + ((h.n_ref + 1) & ~1);
   double* vmid = fsm;
-  double* cf = vmid + max_mid * kFusedThreads + warp * max_coef;
+  double* cf = vmid + max_mid * kFusedThreads + warp * (max_coef + max_stage);
+  int64_t* sp = reinterpret_cast<int64_t*>(cf + max_coef);  // the staged program (after the header)
+  const int nst = 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2 + 4 * h.n_out + ((h.n_ref + 1) >> 1);
+  {
+    const longlong2* g2 = reinterpret_cast<const longlong2*>(prog + 8);
+    longlong2* s2 = reinterpret_cast<longlong2*>(sp);
+    for (int e = lane; e < (nst >> 1); e += 32) s2[e] = __ldg(g2 + e);
+    if ((nst & 1) && lane == 0) sp[nst - 1] = __ldg(prog + 8 + nst - 1);
+  }
+  const int4* sin = reinterpret_cast<const int4*>(sp);  // FusedIn[n_in]
+  const int4* t1 = sin + h.n_in;                         // FusedT1[n_t1] (2 x int4 each)
+  const FusedT2* t2 = reinterpret_cast<const FusedT2*>(sp + 2 * h.n_in + 4 * h.n_t1);
+  const GatherOut* outs = reinterpret_cast<const GatherOut*>(sp + 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2);
+  const int32_t* midref = reinterpret_cast<const int32_t*>(sp + 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2 + 4 * h.n_out);
+  const int32_t* coefs = reinterpret_cast<const int32_t*>(prog + 8 + nst);
   const int f = ch.f0 + lane;
   int d0 = 0, d1 = 0, d2 = 0;  // f's digits over step 1's row legs (first fastest)
   {
@@ -138,14 +151,14 @@ __global__ void __launch_bounds__(kFusedThreads)
   const double2* cf2 = reinterpret_cast<const double2*>(cf);
   // step 1's GEMM per row tree: the tree's K inputs (gathered from T1) -> its N T values
   for (int t = 0; t < h.n_t1; ++t) {
-    const int4 q = __ldg(t1 + 2 * t);  // in0, K, N, mid0
-    const int c0 = __ldg(reinterpret_cast<const int*>(t1 + 2 * t + 1));
+    const int4 q = t1[2 * t];  // in0, K, N, mid0
+    const int c0 = t1[2 * t + 1].x;
     double a[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
       a[k] = 0.0;
       if (k < q.y) {
-        const int4 x = __ldg(ins + q.x + k);
+        const int4 x = sin[q.x + k];
         a[k] = __ldg(T1 + (x.x + d0 * x.y + d1 * x.z + d2 * x.w));
       }
     }
@@ -172,21 +185,21 @@ __global__ void __launch_bounds__(kFusedThreads)
   // step 2's GEMM per row tree: the fiber's outputs, C = alpha * (...) + beta * C
   for (int t = 0; t < h.n_t2; ++t) {
     const FusedT2 q = t2[t];
-    double acc[NM];
+    double acc2[NM];
 #pragma unroll
-    for (int n = 0; n < NM; ++n) acc[n] = 0.0;
+    for (int n = 0; n < NM; ++n) acc2[n] = 0.0;
 #pragma unroll
     for (int k = 0; k < NM; ++k) {
       if (k < q.K) {
-        const int r = __ldg(midref + q.r0 + k);
+        const int r = midref[q.r0 + k];
         double ak = vmid[(r >> 1) * kFusedThreads + tid];
         if (r & 1) ak = -ak;
         const double2* w = cf2 + (q.c0 + k * NM) / 2;
 #pragma unroll
         for (int j = 0; j < NM / 2; ++j) {
           const double2 b = w[j];
-          acc[2 * j] = fma(ak, b.x, acc[2 * j]);
-          acc[2 * j + 1] = fma(ak, b.y, acc[2 * j + 1]);
+          acc2[2 * j] = fma(ak, b.x, acc2[2 * j]);
+          acc2[2 * j + 1] = fma(ak, b.y, acc2[2 * j + 1]);
         }
       }
     }
@@ -199,7 +212,7 @@ __global__ void __launch_bounds__(kFusedThreads)
       if (n < q.N) {
         const GatherOut o = outs[q.o0 + n];
         double* pn = C + o.base + ((int64_t)o0 * o.str[0] + (int64_t)o1 * o.str[1] + (int64_t)o2 * o.str[2]);
-        double y = oalpha * acc[n];
+        double y = oalpha * acc2[n];
         if (o.neg) y = -y;
         *pn = beta != 0.0 ? fma(beta, *pn, y) : y;
       }
@@ -279,7 +292,7 @@ struct FusedPlan {
   std::shared_ptr<ContractPlan> p1, p2;
   std::vector<int64_t> progs;
   std::vector<FusedChunk> chunks;
-  int smem = 0, max_in = 0, max_mid = 0, max_coef = 0, nm = 0;
+  int smem = 0, max_in = 0, max_mid = 0, max_coef = 0, max_stage = 0, nm = 0;
   DevBuf d_progs, d_chunks;
   size_t ws_bytes = 0, off_t = 0, off_ws = 0;  // unfused: T | the larger of the two steps' workspaces
   std::once_flag up_once;
@@ -484,6 +497,7 @@ static bool build_fused(FusedPlan& F) {
     coef1.insert(coef1.end(), coef2.begin(), coef2.end());
     put(coef1.data(), coef1.size() * 4);
     F.max_in = std::max(F.max_in, h.n_in);
+    F.max_stage = std::max(F.max_stage, 2 * h.n_in + 4 * h.n_t1 + 3 * h.n_t2 + 4 * h.n_out + ((h.n_ref + 1) >> 1));
     F.max_mid = std::max(F.max_mid, h.n_mid);
     F.max_coef = std::max(F.max_coef, h.n_coef);
     if (plan_debug() && getenv("TK_FUSED_ALL"))
@@ -492,10 +506,12 @@ static bool build_fused(FusedPlan& F) {
     for (int f0 = 0; f0 < Fr; f0 += 32) F.chunks.push_back(FusedChunk{prog, f0, std::min(32, Fr - f0)});
   }
   F.max_coef = (F.max_coef + 1) & ~1;
-  F.smem = (F.max_mid * kFusedThreads + F.max_coef * kFusedWarps) * 8;
+  // vmid [max_mid][threads] | per warp: coefficients [max_coef] + the staged program [max_stage] words
+  F.max_stage = (F.max_stage + 1) & ~1;
+  F.smem = (F.max_mid * kFusedThreads + (F.max_coef + F.max_stage) * kFusedWarps) * 8;
   if (plan_debug())
-    fprintf(stderr, "[tk fused] %zu classes, max n_in %d, max n_mid %d, max n_coef %d\n", cls.size(), F.max_in,
-            F.max_mid, F.max_coef);
+    fprintf(stderr, "[tk fused] %zu classes, max n_in %d, max n_mid %d, max n_coef %d, max staged words %d\n",
+            cls.size(), F.max_in, F.max_mid, F.max_coef, F.max_stage);
   return F.smem <= 200 * 1024;
 }
 
@@ -532,6 +548,12 @@ static std::shared_ptr<FusedPlan> get_fused_plan(const Tensor& A, const int32_t*
 }
 
 static PerDeviceOnce g_fused_attr;
+
+using FusedKern = void (*)(const double*, const double*, const double*, double*, const int64_t*, const FusedChunk*,
+                           int, int, int, int, double, double, double);
+static FusedKern fused_kernel_for(int nm) {
+  return nm == 4 ? fused_pair_kernel<4> : nm == 8 ? fused_pair_kernel<8> : fused_pair_kernel<16>;
+}
 
 }  // namespace tk
 
@@ -596,8 +618,10 @@ tk_status tk_contract2(const tk_tensor* A_, const void* a, const int32_t* labA, 
   F->ensure_uploaded();
   check_cuda(g_fused_attr.run([&] {
                cudaError_t e = cudaSuccess;
-               for (auto k : {fused_pair_kernel<4>, fused_pair_kernel<8>, fused_pair_kernel<16>})
-                 if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+               for (int nm : {4, 8, 16})
+                 if (e == cudaSuccess)
+                   e = cudaFuncSetAttribute(fused_kernel_for(nm), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024);
                return e;
              }),
              "fused kernel attribute");
@@ -615,10 +639,10 @@ tk_status tk_contract2(const tk_tensor* A_, const void* a, const int32_t* labA, 
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   if (!F->chunks.empty()) {
-    auto kern = F->nm == 4 ? fused_pair_kernel<4> : F->nm == 8 ? fused_pair_kernel<8> : fused_pair_kernel<16>;
+    auto kern = fused_kernel_for(F->nm);
     check_cuda(cudaLaunchKernelEx(&cfg, kern, (const double*)a, (const double*)b1, (const double*)b2,
                                   (double*)c, (const int64_t*)F->d_progs.p, (const FusedChunk*)F->d_chunks.p,
-                                  (int)F->chunks.size(), F->max_mid, F->max_coef,
+                                  (int)F->chunks.size(), F->max_mid, F->max_coef, F->max_stage,
                                   F->p2->pc.identity ? alpha : 1.0, F->p2->pc.identity ? 1.0 : alpha, beta),
                "fused launch");
     add_launches(1);
