@@ -85,7 +85,8 @@ __device__ __forceinline__ void fused_cp8(double* smem, const double* gmem) {
 // ([slot][thread], conflict-free); then each step-2 row tree reads its K T values and writes its N outputs
 // (through the output permute's map when step 2 has one). Every product is the gathered GEMM's own:
 // acc_n = fma(+-a_k, b~_kn, acc_n) over k ascending from zero, zeros included, so the fused result is
-// bitwise that of the two tk_contract calls. NM (4 / 8 / 16) bounds K and N of both steps.
+// bitwise that of the two tk_contract calls. NM (4 / 6 / 8 / 16) bounds K and N of both steps (the
+// coefficient rows are NM wide: NM = 6 for the D_W = 10 MPOs of cfg3, whose K, N <= 6, computes no padding).
 // (Measured alternatives, cfg3: all inputs fetched by cp.async and T values recomputed where consumed,
 // 101 us; two fibers per thread, 86 us; next tree's inputs prefetched, 89 us; program read from global
 // memory, one dependent load chain per row tree, 77-90 us; program staged and all of a fiber's inputs
@@ -321,7 +322,7 @@ static bool build_fused(FusedPlan& F) {
     for (const GemmGroup& g : X2.groups) nmax = std::max(nmax, (int)g.N);
     for (const GemmGroup& g : X1.groups) nmax = std::max(nmax, (int)g.K);
     for (const GemmGroup& g : X2.groups) nmax = std::max(nmax, (int)g.K);
-    F.nm = nmax <= 4 ? 4 : nmax <= 8 ? 8 : 16;
+    F.nm = nmax <= 4 ? 4 : nmax <= 6 ? 6 : nmax <= 8 ? 8 : 16;
     if (nmax > 16) return false;  // (T1 < 2^31 elements: build_gather's own condition)
   }
   // T offsets of step 1's output blocks: group by c_off (T is C~1 in its canonical layout)
@@ -552,7 +553,8 @@ static PerDeviceOnce g_fused_attr;
 using FusedKern = void (*)(const double*, const double*, const double*, double*, const int64_t*, const FusedChunk*,
                            int, int, int, int, double, double, double);
 static FusedKern fused_kernel_for(int nm) {
-  return nm == 4 ? fused_pair_kernel<4> : nm == 8 ? fused_pair_kernel<8> : fused_pair_kernel<16>;
+  return nm == 4 ? fused_pair_kernel<4> : nm == 6 ? fused_pair_kernel<6> : nm == 8 ? fused_pair_kernel<8>
+                                                                   : fused_pair_kernel<16>;
 }
 
 }  // namespace tk
@@ -618,7 +620,7 @@ tk_status tk_contract2(const tk_tensor* A_, const void* a, const int32_t* labA, 
   F->ensure_uploaded();
   check_cuda(g_fused_attr.run([&] {
                cudaError_t e = cudaSuccess;
-               for (int nm : {4, 8, 16})
+               for (int nm : {4, 6, 8, 16})
                  if (e == cudaSuccess)
                    e = cudaFuncSetAttribute(fused_kernel_for(nm), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             200 * 1024);
