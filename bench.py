@@ -330,8 +330,8 @@ def time_svd(dev, stream, reps=7, oracle=True):
     """The two-site truncated SVD that closes Alg. 12: theta (alpha, s1 ; s2, beta) of cfg2 and
     cfg3 at full size, split as (alpha, s1) | (s2, beta). `us_svd` is tk_svd (permute into the workspace +
     the blockwise Jacobi SVD), `us_extract` tk_svd_extract (U, S, Vh of the kept values), CUDA events on
-    the launching stream, median of `reps`; the global truncation (tk_svd_truncate, host) is timed by the
-    wall clock. The oracle (numpy LAPACK per block + its own permute, oracle/svd.py) runs on the host
+    the launching stream, median of `reps`; the global truncation (tk_svd_truncate: spectrum D2H + rule + new
+    host objects) is timed by the wall clock after tk_svd has completed. The oracle (numpy LAPACK per block + its own permute, oracle/svd.py) runs on the host
     cores beside it (rank 0 only, ~1 s)."""
     import torch
     from paper_2508_10076_b200 import tk, layout_io
@@ -351,6 +351,7 @@ def time_svd(dev, stream, reps=7, oracle=True):
             e0.record(stream)
             tk.tk_svd(A, a, p, q, ws, ws.numel() * 8, stream=stream)
             e1.record(stream)
+            e1.synchronize()  # so the host clock below times the truncation alone, not the wait for tk_svd
             h0 = time.perf_counter()
             Wsp, U, S, Vh, err, nrm = tk.tk_svd_truncate(A, p, q, ws, md, 0.0, stream=stream)
             h1 = time.perf_counter()

@@ -229,7 +229,8 @@ tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data,
 /* A~ = permute(A, (p, q)) = U S Vh, block by block (eq. svd, "directly acting on the matrix
  * representation" P:799-809; Alg. 9). U: (A~ codomain) <- W, S: W <- W diagonal, Vh: W <- (A~
  * domain), with W the new bond space: one sector per coupled sector c of A~, degeneracy k_c = kept values.
- * Float64 only. Three steps, all on the caller's workspace (tk_svd_workspace bytes, 256-byte aligned):
+ * Float64 and ComplexF64 (A = U S Vh with unitary-block U, Vh and real S stored in A's dtype). Three steps, all
+ * on the caller's workspace (tk_svd_workspace bytes, 256-byte aligned):
  *   tk_svd          permute + one-sided Jacobi SVD of every block (async on `stream`);
  *   tk_svd_truncate synchronises `stream`, reads the spectrum, applies the global truncation rule
  *                   (values sorted descending over all blocks, ties by block then index; a value of block c
@@ -238,7 +239,7 @@ tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data,
  *                   neither: keep all min(rows, cols) values) and returns new host objects W, U, S, Vh, the
  *                   truncation error sqrt(sum_dropped d_c s^2) and ||A|| = sqrt(sum_c d_c sum s^2);
  *   tk_svd_extract  writes U, S, Vh (canonical layouts, caller-owned device buffers) from the workspace.
- * The workspace must not change between the three calls. Blocks with min(rows, cols) > 2048 ->
+ * The workspace must not change between the three calls. Blocks with min(rows, cols) > 8192 ->
  * TK_ERR_UNSUPPORTED. Zero singular values give zero U (or Vh) columns. */
 tk_status tk_svd_workspace(const tk_tensor* A, const int32_t* p, int32_t np, const int32_t* q, int32_t nq,
                            size_t* bytes);

@@ -39,6 +39,10 @@ constexpr int THREADS = 32 * NCONS;
 constexpr int PD = STAGES - 2;  // prefetch distance: the producer waits only for a slice released 2 steps ago
 }  // namespace
 
+#ifndef TK_WARP_LATIN
+#define TK_WARP_LATIN 1
+#endif
+
 size_t gemm_tma_smem_bytes() { return (size_t)STAGES * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t); }
 
 // The TMA producer is lane 0 of warp 0 (a separate producer warp would be a 17th warp: 5 warps on one
@@ -117,7 +121,16 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tma_kernel(const __grid_const
   }
 
   // ---------------- consumers
+  // Warp -> 32 x 32 sub-tile as a Latin square over the 4 SM sub-partitions (a warp runs on sub-partition
+  // warp & 3, each with its own DMMA pipe): every sub-partition holds one warp of each tile-row band wm
+  // and one of each column band wn, so the fragments an edge tile skips (mf / nf below) come off all four
+  // pipes evenly. With wm = warp & 3 an M-edge tile idled whole sub-partitions while the others ran the
+  // full k-loop, and the skipped padding (1.5 % of cfg4's tile flops) saved no time.
+#if TK_WARP_LATIN
+  const int wm = warp >> 2, wn = ((warp & 3) + wm) & 3;
+#else
   const int wm = warp & 3, wn = warp >> 2;
+#endif
   const int gq = lane >> 2, tq = lane & 3;
   uint32_t it = 0;
   for (int j = 0;; ++j) {

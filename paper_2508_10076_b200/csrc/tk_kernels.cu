@@ -871,6 +871,27 @@ struct GemmCfg {
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 
+#ifndef TK_WARP_LATIN
+#define TK_WARP_LATIN 1
+#endif
+// Warp -> sub-tile (wm, wn) of a WARPS_M x WARPS_N warp grid. A warp runs on SM sub-partition warp & 3, each
+// with its own DMMA pipe; the fragment guards skip 8-row / 8-column fragments outside the block, so the
+// skipped work should come off all four pipes evenly. 4 x 4 grids (128 x 128 tiles): a Latin square, every
+// sub-partition holds one warp of each row band and one of each column band. 2 x 4 grids (64 x 64 tiles):
+// both row bands on every sub-partition (warps w and w + 4 share one), so an edge tile with <= 32 rows
+// keeps four pipes busy; with wm = warp % WARPS_M it idled sub-partitions 1 and 3.
+template <int WARPS_M, int WARPS_N>
+__device__ __forceinline__ void warp_subtile(int warp, int& wm, int& wn) {
+  wm = warp % WARPS_M, wn = warp / WARPS_M;
+#if TK_WARP_LATIN
+  if constexpr (WARPS_M == 4 && WARPS_N == 4) {
+    wm = warp >> 2, wn = ((warp & 3) + wm) & 3;
+  } else if constexpr (WARPS_M == 2 && WARPS_N == 4) {
+    wm = (warp + (warp >> 2)) & 1, wn = ((warp & 3) >> 1) + 2 * (warp >> 2);
+  }
+#endif
+}
+
 // k range [kb, ke) (split-K: ke - kb < K); part != nullptr: write the raw partial tile (BM x BN,
 // column-major) for the split-K reduction instead of alpha * acc + beta * C.
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
@@ -882,7 +903,8 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
+  int wm, wn;
+  warp_subtile<Cfg::WARPS_M, Cfg::WARPS_N>(warp, wm, wn);
   const int gq = lane >> 2, tq = lane & 3;
   const double* Ag = A + g.a_off;
   const double* Bg = B + g.b_off;
@@ -1029,7 +1051,8 @@ __device__ __forceinline__ void gemm_tile_mbar(const double* __restrict__ A, con
   uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::B_STAGE);
   uint64_t* empty = full + STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % Cfg::WARPS_M, wn = warp / Cfg::WARPS_M;
+  int wm, wn;
+  warp_subtile<Cfg::WARPS_M, Cfg::WARPS_N>(warp, wm, wn);
   const int gq = lane >> 2, tq = lane & 3;
   const double* Ag = A + g.a_off;
   const double* Bg = B + g.b_off;
