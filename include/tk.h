@@ -320,7 +320,7 @@ tk_status tk_permute_transfer_planar(const tk_tensor* A, const int32_t* p, int32
                                      int32_t nq, const tk_tensor* C, int32_t kappa_mode, double* out);
 
 const char* tk_last_error(void);
-/* Frees every memoised plan (contraction, permute, trace, SVD) and its device tables. */
+/* Frees every memoised plan (contraction, fused pair, network, permute, trace, SVD) and its device tables. */
 void tk_cache_clear(void);
 /* Number of memoised plans currently held (all caches; each cache is a bounded LRU). */
 int64_t tk_cache_size(void);

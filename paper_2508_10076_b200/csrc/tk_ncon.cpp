@@ -254,15 +254,55 @@ void ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* label
   }
 }
 
-struct Release {  // intermediate HomSpaces are freed on every exit path
-  std::vector<Item>& items;
-  ~Release() {
+// A planned network: the pairwise steps, the intermediate HomSpaces (owned) with their workspace offsets,
+// the output HomSpace (owned) and the workspace size. Planning walks every intermediate's fusion-tree
+// layout (cfg3's Alg. 12 chain: ~1 s of host time for a 190 us chain), so plans are cached like the
+// pairwise plans: keyed by the inputs' structure signatures, the labels, the order and n_cod_out; the
+// inputs of a cached plan are slots (the caller's tensors of the current call stand in for them).
+struct NconPlan {
+  std::vector<Item> items;
+  std::vector<Step> steps;
+  size_t bytes = 0;
+  tk_tensor* out = nullptr;
+  void ensure_uploaded() {}  // no device tables of its own (the pairwise plans hold them)
+  ~NconPlan() {
     for (Item& it : items)
       if (it.owned) tk_tensor_release(const_cast<tk_tensor*>(it.t));
+    if (out) tk_tensor_release(out);
   }
 };
 
+PlanCache<NconPlan> g_ncon_cache;
+
+std::shared_ptr<NconPlan> get_ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* labels,
+                                        const int32_t* order, int32_t norder, int32_t n_cod_out) {
+  if (n < 1 || !T || !labels) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: no tensors");
+  if (norder > 0 && !order) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: null order");
+  std::string key = "N";
+  for (int i = 0; i < n; ++i) {
+    if (!T[i]) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: null tensor");
+    const Tensor& t = *(const Tensor*)T[i];
+    if (t.nlegs() > 0 && !labels[i]) TK_THROW(TK_ERR_INVALID_ARGUMENT, "tk_ncon: null label list");
+    key += "#" + t.sig + "#";
+    for (int l = 0; l < t.nlegs(); ++l) key += std::to_string(labels[i][l]) + ",";
+  }
+  key += "#o";
+  for (int i = 0; i < norder; ++i) key += std::to_string(order[i]) + ",";
+  key += "#" + std::to_string(n_cod_out);
+  return g_ncon_cache.get(key, [&] {
+    auto P = std::make_shared<NconPlan>();  // a throw below frees the intermediates made so far
+    ncon_plan(n, T, labels, order, norder, n_cod_out, P->items, P->steps, &P->bytes, &P->out);
+    for (int i = 0; i < n; ++i) P->items[i].t = nullptr;  // input slots: never dereferenced from the cache
+    return P;
+  });
+}
+
 }  // namespace
+
+namespace tk {
+void ncon_cache_clear() { g_ncon_cache.clear(); }
+size_t ncon_cache_size() { return g_ncon_cache.size(); }
+}  // namespace tk
 
 #define TK_API_BEGIN try {
 #define TK_API_END                  \
@@ -281,43 +321,36 @@ extern "C" {
 
 tk_status tk_ncon_output(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
                          int32_t norder, int32_t n_cod_out, tk_tensor** out) {
-  std::vector<Item> items;
-  Release guard{items};
   TK_API_BEGIN
   if (!out) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  std::vector<Step> steps;
-  size_t bytes = 0;
-  ncon_plan(n, T, labels, order, norder, n_cod_out, items, steps, &bytes, out);
+  auto P = get_ncon_plan(n, T, labels, order, norder, n_cod_out);
+  tk_tensor_retain(P->out);  // the caller's own reference
+  *out = P->out;
   TK_API_END
 }
 
 tk_status tk_ncon_workspace(int32_t n, const tk_tensor* const* T, const int32_t* const* labels, const int32_t* order,
                             int32_t norder, int32_t n_cod_out, size_t* bytes) {
-  std::vector<Item> items;
-  Release guard{items};
   TK_API_BEGIN
   if (!bytes) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  std::vector<Step> steps;
-  ncon_plan(n, T, labels, order, norder, n_cod_out, items, steps, bytes, nullptr);
+  *bytes = get_ncon_plan(n, T, labels, order, norder, n_cod_out)->bytes;
   TK_API_END
 }
 
 tk_status tk_ncon(int32_t n, const tk_tensor* const* T, const void* const* data, const int32_t* const* labels,
                   const int32_t* order, int32_t norder, int32_t n_cod_out, const tk_tensor* C, void* c, double alpha,
                   double beta, void* ws, size_t ws_bytes, tk_stream stream) {
-  std::vector<Item> items;
-  Release guard{items};
   TK_API_BEGIN
   if (!data || !C) TK_THROW(TK_ERR_INVALID_ARGUMENT, "null argument");
-  std::vector<Step> steps;
-  size_t bytes = 0;
-  tk_tensor* out = nullptr;
-  ncon_plan(n, T, labels, order, norder, n_cod_out, items, steps, &bytes, &out);
-  const bool same = ((const Tensor*)out)->sig == ((const Tensor*)C)->sig;
-  tk_tensor_release(out);
-  if (!same) TK_THROW(TK_ERR_SPACE_MISMATCH, "tk_ncon: C does not have the network's output HomSpace");
+  auto P = get_ncon_plan(n, T, labels, order, norder, n_cod_out);
+  if (((const Tensor*)P->out)->sig != ((const Tensor*)C)->sig)
+    TK_THROW(TK_ERR_SPACE_MISMATCH, "tk_ncon: C does not have the network's output HomSpace");
+  const size_t bytes = P->bytes;
   if (ws_bytes < bytes || (bytes && !ws)) TK_THROW(TK_ERR_WORKSPACE_TOO_SMALL, "tk_ncon: workspace too small");
   if (((uintptr_t)ws & 255) != 0) TK_THROW(TK_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  std::vector<Item> items(P->items);  // this call's view: the caller's tensors and data in the input slots
+  const std::vector<Step>& steps = P->steps;
+  for (int i = 0; i < n; ++i) items[i].t = T[i];
   for (int i = 0; i < n; ++i) items[i].data = data[i];
   size_t inter = 0;  // intermediates occupy [0, inter) of the workspace, the pairwise scratch the rest
   for (const Item& it : items)

@@ -1419,6 +1419,7 @@ static std::shared_ptr<PermPlan> get_perm_plan(const Tensor& A, const std::vecto
 }
 
 void cache_clear() {
+  ncon_cache_clear();  // first: network plans hold intermediate HomSpaces, not pairwise plans
   fused_cache_clear();
   g_contract_cache.clear();
   g_perm_cache.clear();
@@ -1437,6 +1438,7 @@ size_t cache_size() { return g_contract_cache.size() + g_perm_cache.size(); }
 size_t svd_cache_size();
 size_t trace_cache_size();
 size_t fused_cache_size();
+size_t ncon_cache_size();
 
 // ------------------------------------------------------------------ profiling state
 struct Prof {
@@ -1815,6 +1817,6 @@ tk_status tk_dmma_probe(int32_t blocks, int64_t iters, tk_stream stream, double*
 void tk_cache_clear(void) { tk::cache_clear(); }
 
 int64_t tk_cache_size(void) { return (int64_t)(tk::cache_size() + tk::svd_cache_size() + tk::trace_cache_size() +
-                                          tk::fused_cache_size()); }
+                                          tk::fused_cache_size() + tk::ncon_cache_size()); }
 
 }  // extern "C"

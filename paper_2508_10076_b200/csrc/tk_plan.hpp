@@ -161,6 +161,7 @@ void add_launches(int n);
 void reset_launches();
 void svd_cache_clear();
 void fused_cache_clear();
+void ncon_cache_clear();  // tk_ncon.cpp: planned networks
 
 // Abelian output permute as an element map (tk_plan.cpp): a C~ row tree of F rows starting at padded
 // offset src (column n folded into src) lands in one C subblock with sign +-1; map() fills the GatherOut

@@ -447,6 +447,35 @@ def test_plan_cache_keys_and_bound():
     assert tk.tk_cache_size() == 0
 
 
+def test_ncon_plan_is_cached():
+    """A network's plan (pairwise steps, intermediate HomSpaces, workspace) is memoised by the inputs'
+    structure, labels, order and n_cod_out: a repeated query with NEW tensor objects of the same structure
+    builds nothing, returns the same workspace size and an output of the same HomSpace; another order or
+    other labels make a new plan; tk_cache_clear drops it."""
+    from workloads import configs as W
+    cfg = W.cfg2()
+    names, labels, order, ncod, out_name = W.chain_as_ncon(cfg)
+    tk.tk_cache_clear()
+    T1 = [tk.tensor_from_spec(cfg["tensors"][nm][0]) for nm in names]
+    w1 = tk.tk_ncon_workspace(T1, labels, order, ncod)
+    n1 = tk.tk_cache_size()
+    assert n1 > 0
+    T2 = [tk.tensor_from_spec(cfg["tensors"][nm][0]) for nm in names]   # fresh objects, same structure
+    assert tk.tk_ncon_workspace(T2, labels, order, ncod) == w1
+    assert tk.tk_cache_size() == n1
+    O1 = tk.tk_ncon_output(T1, labels, order, ncod)
+    O2 = tk.tk_ncon_output(T2, labels, order, ncod)
+    assert tk.tk_cache_size() == n1
+    assert O1.info() == O2.info() and O1.nelems == O2.nelems
+    del T1, O1                                                          # the cached plan does not borrow them
+    assert tk.tk_ncon_workspace(T2, labels, order, ncod) == w1
+    tk.tk_ncon_output(T2, labels, order, ncod - 1)                      # another output split: a new plan
+    assert tk.tk_cache_size() > n1
+    tk.tk_cache_clear()
+    assert tk.tk_cache_size() == 0
+    assert tk.tk_ncon_workspace(T2, labels, order, ncod) == w1          # rebuilt after the clear
+
+
 def test_binding_rejects_bad_labels():
     A, B = _tiny_pair(3)
     with pytest.raises(ValueError):
