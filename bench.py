@@ -242,7 +242,8 @@ def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
     tk_contract2) and the config's explicit pairwise steps (`us_per_chain_pairwise`: one tk_contract per
     step, intermediates in the config's orders). Roofline per SURVEY §8(d) over the config's pairwise steps: sum of
     tk_contract_roofline (GEMM blocks max(flops/P, bytes/BW) + permute bytes/BW) at the in-run DMMA peak
-    and MEASURED_PEAKS' HBM bandwidth."""
+    and MEASURED_PEAKS' HBM bandwidth. `us_per_call_eager`: the tk_ncon call issued without a graph, back to back
+    (host wall clock per call, plans cached, no L2 flush): the API's host cost shows where it exceeds the graph time."""
     import torch
     from paper_2508_10076_b200 import tk, layout_io
     from workloads import configs as W
@@ -313,9 +314,20 @@ def time_chains(dev, stream0, peak_flops, hbm_bytes_s, reps=30):
             return float(np.median(ts)), n
         us_pw, launches_pw = timed(chain)
         us, launches = timed(network)
+        # the same tk_ncon call without a graph: host wall clock per call, back to back (plans cached: what
+        # a caller's loop pays per chain when it does not capture a graph), stream drained at the end
+        with torch.cuda.stream(stream):
+            network()
+            torch.cuda.synchronize(dev)
+            h0 = time.perf_counter()
+            for _ in range(reps):
+                network()
+            torch.cuda.synchronize(dev)
+            us_eager = (time.perf_counter() - h0) / reps * 1e6
         out[f"cfg{k}"] = {"kind": cfg["kind"], "us_per_chain": round(us, 2), "launches": launches,
                           "api": "tk_ncon", "steps": len(cfg["steps"]),
                           "us_per_chain_pairwise": round(us_pw, 2), "launches_pairwise": launches_pw,
+                          "us_per_call_eager": round(us_eager, 2),
                           "block_flops": roof["flops"],
                           "GFLOP_s": round(roof["flops"] / (us * 1e-6) / 1e9, 2),
                           "roofline_us": round(roof["seconds"] * 1e6, 2),

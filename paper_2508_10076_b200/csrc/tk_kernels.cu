@@ -917,60 +917,75 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
 #pragma unroll
     for (int j = 0; j < Cfg::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  auto load_stage = [&](int kt, int s) {
-    const int k0 = kb + kt * BK;
-    double* as = As + s * Cfg::A_STAGE;
-    double* bs = Bs + s * Cfg::B_STAGE;
+  // Per-thread load geometry, hoisted out of the k loop: a thread copies the same (row, k-offset) pattern
+  // of every stage, so its global pointers advance by a constant per k-step and only the k < K test
+  // changes. (The straightforward per-element index -> (m, k) -> address form was ~140 of the ~300
+  // instructions a warp issued per k-step, and these kernels are issue-bound: ncu, cfg3 T3.R.)
+  constexpr int T = Cfg::THREADS;
+  static_assert(T % BM == 0 && T % BK == 0 && T % (BM / 2) == 0 && T % (BK / 2) == 0, "load geometry");
+  static_assert((BM * BK) % T == 0 && (BN * BK) % T == 0 && (BM / 2 * BK) % T == 0 && (BK / 2 * BN) % T == 0,
+                "load geometry");
+  // element (am, akq + i * AKS) of A's stage; element (bkk, bnq + i * BNS) of B's stage
+  const int ev = vec ? 2 : 1;  // elements per copy (constant divisors below: shifts)
+  const int am = vec ? 2 * (tid % (BM / 2)) : tid % BM, akq = vec ? tid / (BM / 2) : tid / BM;
+  const int bkk = vec ? 2 * (tid % (BK / 2)) : tid % BK, bnq = vec ? tid / (BK / 2) : tid / BK;
+  const int AKS = vec ? T / (BM / 2) : T / BM, BNS = vec ? T / (BK / 2) : T / BK;
+  // bytes of a copy that lie inside the block along the contiguous dimension (A: rows; B: k, per stage)
+  const int abytes = m0 + am + ev <= M ? 8 * ev : (m0 + am < M ? 8 : 0);
+  const double* pa0 = Ag + (m0 + am) + (int64_t)(kb + akq) * g.lda;
+  const double* pb0 = Bg + (kb + bkk) + (int64_t)(n0 + bnq) * g.ldb;
+  const int64_t astep = (int64_t)AKS * g.lda, bstep = (int64_t)BNS * g.ldb;
+  const int sa0 = akq * Cfg::LDA_S + am, sb0 = bnq * Cfg::LDB_S + bkk;
+  // stages are loaded in k order, one call per k-step: the pointers and the k origin run along
+  const double* pa = pa0;
+  const double* pb = pb0;
+  const int64_t akstep = (int64_t)BK * g.lda;
+  int k0 = kb - BK;
+  auto load_stage = [&](int s) {
+    k0 += BK;
+    double* as = As + s * Cfg::A_STAGE + sa0;
+    double* bs = Bs + s * Cfg::B_STAGE + sb0;
+    const int kbytes = k0 + bkk + ev <= K ? 8 * ev : (k0 + bkk < K ? 8 : 0);
     if (vec) {
 #pragma unroll
-      for (int i = 0; i < (BM / 2 * BK) / Cfg::THREADS; ++i) {
-        int idx = tid + i * Cfg::THREADS;
-        int m = 2 * (idx % (BM / 2)), k = idx / (BM / 2);
-        int gm = m0 + m, gk = k0 + k;
-        int nb = (gm < M && gk < K) ? (gm + 1 < M ? 16 : 8) : 0;
-        const double* gp = nb ? Ag + (int64_t)gm + (int64_t)gk * g.lda : A;
-        cp_async16(as + k * Cfg::LDA_S + m, gp, nb);
+      for (int i = 0; i < (BM / 2 * BK) / T; ++i) {
+        const int nb = k0 + akq + i * AKS < K ? abytes : 0;
+        cp_async16(as + i * AKS * Cfg::LDA_S, nb ? pa + i * astep : A, nb);
       }
 #pragma unroll
-      for (int i = 0; i < (BK / 2 * BN) / Cfg::THREADS; ++i) {
-        int idx = tid + i * Cfg::THREADS;
-        int k = 2 * (idx % (BK / 2)), n = idx / (BK / 2);
-        int gk = k0 + k, gn = n0 + n;
-        int nb = (gn < N && gk < K) ? (gk + 1 < K ? 16 : 8) : 0;
-        const double* gp = nb ? Bg + (int64_t)gk + (int64_t)gn * g.ldb : B;
-        cp_async16(bs + n * Cfg::LDB_S + k, gp, nb);
+      for (int i = 0; i < (BK / 2 * BN) / T; ++i) {
+        const int nb = n0 + bnq + i * BNS < N ? kbytes : 0;
+        cp_async16(bs + i * BNS * Cfg::LDB_S, nb ? pb + i * bstep : B, nb);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < (BM * BK) / Cfg::THREADS; ++i) {
-        int idx = tid + i * Cfg::THREADS;
-        int m = idx % BM, k = idx / BM;
-        bool ok = (m0 + m < M) && (k0 + k < K);
-        const double* gp = ok ? Ag + (int64_t)(m0 + m) + (int64_t)(k0 + k) * g.lda : A;
-        cp_async8(as + k * Cfg::LDA_S + m, gp, ok);
+      for (int i = 0; i < (BM * BK) / T; ++i) {
+        const bool ok = abytes != 0 && k0 + akq + i * AKS < K;
+        cp_async8(as + i * AKS * Cfg::LDA_S, ok ? pa + i * astep : A, ok);
       }
 #pragma unroll
-      for (int i = 0; i < (BN * BK) / Cfg::THREADS; ++i) {
-        int idx = tid + i * Cfg::THREADS;
-        int k = idx % BK, n = idx / BK;
-        bool ok = (n0 + n < N) && (k0 + k < K);
-        const double* gp = ok ? Bg + (int64_t)(k0 + k) + (int64_t)(n0 + n) * g.ldb : B;
-        cp_async8(bs + n * Cfg::LDB_S + k, gp, ok);
+      for (int i = 0; i < (BN * BK) / T; ++i) {
+        const bool ok = kbytes != 0 && n0 + bnq + i * BNS < N;
+        cp_async8(bs + i * BNS * Cfg::LDB_S, ok ? pb + i * bstep : B, ok);
       }
     }
+    pa += akstep;
+    pb += BK;
   };
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(s, s);
+    if (s < nk) load_stage(s);
     cp_async_commit();
   }
+  // warp-uniform: the warp's WM x WN sub-tile lies inside the block (8-row / 8-column fragment units)
+  const bool interior = m0 + wm * WM + (Cfg::MF - 1) * 8 < M && n0 + wn * WN + (Cfg::NF - 1) * 8 < N;
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
       int nxt = kt + STAGES - 1;
-      if (nxt < nk) load_stage(nxt, nxt % STAGES);
+      if (nxt < nk) load_stage(nxt % STAGES);
       cp_async_commit();
     }
     const double* as = As + (kt % STAGES) * Cfg::A_STAGE + wm * WM + gq;
@@ -978,6 +993,21 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ A, const do
     // padding is never multiplied: k-steps past K, and 8-row / 8-column fragments outside the block
     // (warp-uniform guards; small sectors are mostly padding in 64 x 64 tiles)
     const int kend = min(BK, K - (kb + kt * BK));
+    if (interior && kend == BK) {  // all of this warp's fragments inside the block, a full k-step: no guards
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[Cfg::MF], bf[Cfg::NF];
+#pragma unroll
+        for (int i = 0; i < Cfg::MF; ++i) af[i] = as[(kk + tq) * Cfg::LDA_S + i * 8];
+#pragma unroll
+        for (int j = 0; j < Cfg::NF; ++j) bf[j] = bs[j * 8 * Cfg::LDB_S + kk];
+#pragma unroll
+        for (int i = 0; i < Cfg::MF; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::NF; ++j) dmma884(acc[i][j], af[i], bf[j]);
+      }
+      continue;
+    }
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       if (kk >= kend) break;

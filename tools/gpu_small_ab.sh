@@ -1,16 +1,20 @@
-# small-tile GEMM: CTA-barrier pipeline (default) vs the mbarrier-pipelined tile (smb4: 4 stages, PD 2;
-# smb5: 5 stages, PD 3) on the DMRG chains; parity of the variant and of the default build
-cd /root/repo
-timeout 900 python -m pytest tests/test_gpu_fused.py tests/test_gpu_ncon.py -q -x > gpurun_out/sab_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/sab_pytest.log
-TK_LIB_PATH=_variants/libtk_smb4.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py -q -x > gpurun_out/sab_pytest_smb4.log 2>&1; echo "pytest smb4 rc=$?"; tail -1 gpurun_out/sab_pytest_smb4.log
-for i in 1 2; do
-  timeout 300 python tools/bench_chains.py 2,3,7,8 > gpurun_out/sab_base_$i.jsonl 2>&1; echo "base rc=$?"
-  TK_LIB_PATH=_variants/libtk_smb4.so timeout 300 python tools/bench_chains.py 2,3,7,8 > gpurun_out/sab_smb4_$i.jsonl 2>&1; echo "smb4 rc=$?"
-  TK_LIB_PATH=_variants/libtk_smb5.so timeout 300 python tools/bench_chains.py 2,3,7,8 > gpurun_out/sab_smb5_$i.jsonl 2>&1; echo "smb5 rc=$?"
+# A/B of the 64 x 64 DMMA tile (gemm_tile): default build against _variants/libtk_head.so (the previous
+# commit, tools/build_variant.sh head ""): parity of the default build, then the chains (bench_chains.py:
+# tk_ncon and pairwise, CUDA graphs, L2 flushed) alternating, then per-phase times of the configs.
+set -x
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py tests/test_gpu_fuzz.py tests/test_gpu_fused.py tests/test_gpu_ncon.py -m gpu -q -x > gpurun_out/small_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/small_pytest.log
+for r in 1 2; do
+  python tools/bench_chains.py 2,3,5,6,7,8 > gpurun_out/small_new_$r.jsonl 2> gpurun_out/small_new_$r.err; echo "new rc=$?"
+  TK_LIB_PATH=_variants/libtk_head.so python tools/bench_chains.py 2,3,5,6,7,8 > gpurun_out/small_old_$r.jsonl 2> gpurun_out/small_old_$r.err; echo "old rc=$?"
 done
+python tools/bench_configs.py --reps 30 --phases > gpurun_out/small_new_phases.jsonl 2>/dev/null
+TK_LIB_PATH=_variants/libtk_head.so python tools/bench_configs.py --reps 30 --phases > gpurun_out/small_old_phases.jsonl 2>/dev/null
 python - <<'PY'
 import json
-for tag in ("base_1","smb4_1","smb5_1","base_2","smb4_2","smb5_2"):
-    rows=[json.loads(l) for l in open(f"gpurun_out/sab_{tag}.jsonl") if l.startswith("{")]
-    print(tag, [(r["cfg"], r["us_per_chain"], r.get("us_per_chain_pairwise")) for r in rows])
+for n in ("new_1", "old_1", "new_2", "old_2"):
+    rows = [json.loads(l) for l in open(f"gpurun_out/small_{n}.jsonl") if l.startswith("{")]
+    print(n, {r["cfg"]: (r["us_per_chain"], r["us_per_chain_pairwise"]) for r in rows})
+for n in ("new", "old"):
+    rows = [json.loads(l) for l in open(f"gpurun_out/small_{n}_phases.jsonl") if l.startswith("{")]
+    print(n, {r["cfg"]: (r["us_per_chain_graph"], [p[2] for p in r["phase_us_per_step"]]) for r in rows})
 PY
