@@ -137,3 +137,38 @@ def test_ncon_vs_oracle(maker):
         spec = ",".join("".join(L(x) for x in l) for l in labels) + "->" + "".join(L(-k) for k in range(1, m + 1))
         E = np.einsum(spec, *dens, optimize=True)
         assert OC.rel_frobenius(-0.5 * E + 0.25 * OD.to_dense(lc, y0), want) <= 1e-12
+
+
+@pytest.mark.parametrize("maker", [_network_cfg3, _network_su2], ids=["cfg3", "su2"])
+def test_ncon_cached_plan_serves_new_tensor_objects(maker):
+    """A planned network is memoised by structure: a second call with FRESH tensor objects (the first ones
+    released) and other data reuses the plan -- its input slots are filled from the current call, the
+    intermediates are the plan's own -- and still matches the oracle."""
+    import gc
+    from paper_2508_10076_b200 import tk
+    kind, specs, labels, order, n_cod_out = maker()
+    lays = [OL.homspace_layout(kind, s["cod"], s["dom"]) for s in specs]
+    tk.tk_cache_clear()
+    for seed in (11, 12):
+        rng = np.random.default_rng(seed)
+        xs = [rng.standard_normal(l.nelems) for l in lays]
+        T = [tk.tensor_from_spec(s) for s in specs]          # new host objects every round
+        C = tk.tk_ncon_output(T, labels, order, n_cod_out)
+        n_plans = tk.tk_cache_size()
+        nws = tk.tk_ncon_workspace(T, labels, order, n_cod_out)
+        assert tk.tk_cache_size() == n_plans                  # output and workspace: one plan
+        ws = torch.empty(nws // 8 + 32, dtype=torch.float64, device="cuda")
+        c = torch.full((C.nelems,), float("nan"), dtype=torch.float64, device="cuda")
+        tk.tk_ncon(T, [torch.from_numpy(x).cuda() for x in xs], labels, order, n_cod_out, C, c, ws=ws,
+                   ws_bytes=ws.numel() * 8)
+        torch.cuda.synchronize()
+        if seed == 11:
+            after_first = tk.tk_cache_size()
+        else:
+            assert tk.tk_cache_size() == after_first          # nothing new was planned
+        cod, dom, D = oracle_ncon(kind, specs, [OD.to_dense(l, x) for l, x in zip(lays, xs)], labels, order,
+                                  n_cod_out)
+        lc = OL.homspace_layout(kind, cod, dom)
+        assert OC.rel_frobenius(OD.to_dense(lc, c.cpu().numpy()), D) <= TOL
+        del T, C
+        gc.collect()
