@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -119,7 +120,7 @@ struct Tensor {
   std::vector<Subblock> subs;
   int64_t nelems = 0;
   std::string sig;                      // structural signature (plan-cache key part)
-  std::map<std::string, int> sub_index; // tree-pair key -> subblock index
+  std::unordered_map<std::string, int> sub_index; // tree-pair key -> subblock index
   ~Tensor();
   int n_cod() const { return (int)cod.size(); }
   int n_dom() const { return (int)dom.size(); }

@@ -144,20 +144,24 @@ void enumerate_trees(Kind k, const std::vector<Space*>& legs, std::map<Sector, s
   }
 }
 
-static void put_sector(std::ostringstream& os, const Sector& s) { os << s.v[0] << "," << s.v[1] << ";"; }
+// Binary key of a tree pair (uncoupled | inner | coupled | uncoupled | inner labels, 8 bytes per sector, a
+// marker between the lists): built per subblock of every tensor and per planner lookup, so no streams here.
+static inline void put_sector(std::string& k, const Sector& s) { k.append(reinterpret_cast<const char*>(s.v), 8); }
 
 std::string tree_pair_key(const Tree& s, const Tree& f) {
-  std::ostringstream os;
-  for (auto& x : s.unc) put_sector(os, x);
-  os << "|";
-  for (auto& x : s.inner) put_sector(os, x);
-  os << "|";
-  put_sector(os, s.coupled);
-  os << "|";
-  for (auto& x : f.unc) put_sector(os, x);
-  os << "|";
-  for (auto& x : f.inner) put_sector(os, x);
-  return os.str();
+  static const int32_t bar[2] = {INT32_MIN, INT32_MIN};
+  std::string k;
+  k.reserve(8 * (s.unc.size() + s.inner.size() + f.unc.size() + f.inner.size() + 5));
+  for (auto& x : s.unc) put_sector(k, x);
+  k.append(reinterpret_cast<const char*>(bar), 8);
+  for (auto& x : s.inner) put_sector(k, x);
+  k.append(reinterpret_cast<const char*>(bar), 8);
+  put_sector(k, s.coupled);
+  k.append(reinterpret_cast<const char*>(bar), 8);
+  for (auto& x : f.unc) put_sector(k, x);
+  k.append(reinterpret_cast<const char*>(bar), 8);
+  for (auto& x : f.inner) put_sector(k, x);
+  return k;
 }
 
 Tensor::~Tensor() {
@@ -210,8 +214,8 @@ Tensor* make_tensor(tk_dtype dtype, const std::vector<Space*>& cod, const std::v
     if (it == dt.end()) continue;
     Block b;
     b.coupled = kv.first;
-    b.cod_trees = kv.second;
-    b.dom_trees = it->second;
+    b.cod_trees = std::move(kv.second);  // each coupled sector makes one block: the lists move
+    b.dom_trees = std::move(it->second);
     for (auto& tr : b.cod_trees) {
       b.row_off.push_back(b.rows);
       b.rows += tr.size;
