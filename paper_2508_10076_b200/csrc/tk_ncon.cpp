@@ -272,7 +272,9 @@ struct NconPlan {
   }
 };
 
-PlanCache<NconPlan> g_ncon_cache;
+// a planned network owns its intermediates' block layouts (tens of MB of host memory for cfg3-sized
+// chains), so this cache is kept much smaller than the pairwise ones
+PlanCache<NconPlan> g_ncon_cache(64);
 
 std::shared_ptr<NconPlan> get_ncon_plan(int32_t n, const tk_tensor* const* T, const int32_t* const* labels,
                                         const int32_t* order, int32_t norder, int32_t n_cod_out) {

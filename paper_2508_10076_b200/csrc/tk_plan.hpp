@@ -63,6 +63,7 @@ constexpr size_t kPlanCacheCap = 512;
 template <class Plan>
 class PlanCache {
  public:
+  explicit PlanCache(size_t cap = kPlanCacheCap) : cap_(cap) {}
   template <class Build>
   std::shared_ptr<Plan> get(const std::string& key0, Build build) {
     const std::string key = key0 + "@dev" + std::to_string(current_device());
@@ -76,7 +77,7 @@ class PlanCache {
     if (current_device() >= 0) P->ensure_uploaded();
     lru_.emplace_front(key, P);
     map_[key] = lru_.begin();
-    while (lru_.size() > kPlanCacheCap) {
+    while (lru_.size() > cap_) {
       map_.erase(lru_.back().first);
       lru_.pop_back();
     }
@@ -93,6 +94,7 @@ class PlanCache {
   }
 
  private:
+  size_t cap_;
   std::mutex mu_;
   std::list<std::pair<std::string, std::shared_ptr<Plan>>> lru_;
   std::unordered_map<std::string, typename std::list<std::pair<std::string, std::shared_ptr<Plan>>>::iterator> map_;
